@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""Benchmark of the batched NMGF solve phase (arxiv 2603.01064) on B200.
+
+Workload (BASELINE.json configs[1], the metric's configuration): 1D, n = 4096,
+sigma = 0.02, alpha = 1e-3 (default; --alpha), 6 levels (4096 -> 128),
+1024 RHS per GPU, CNN 3x16 k5 smoothers (W_seed), nu1 = nu2 = 1, level filter on.
+
+One "step" = one pass of the whole hot path over the batch: fp64 outer residual and
+convergence test, one NMGF V-cycle (all levels), fp64 update.
+  value = RHS * V-cycles / s, whole job (all ranks), device-timed (CUDA events, max
+          over ranks).  Weak scaling: every rank solves its own 1024-RHS shard.
+  e2e   = the same metric through the C ABI host-buffer entry nmg_vcycles_host
+          (H2D of y and x, one cycle, D2H of x inside the timed region).
+  solve = RHS solved to 1e-6 relative residual per second with the converging
+          W_lin stand-in weights at alpha = 1e-2.
+Inputs are larger than L2 (fp64 A 128 MiB + fp32 level operators 128 MiB streamed
+per step), so no explicit L2 flush is needed between steps.
+
+--impl reference times the fp64 CPU oracle (oracle/) on a bounded sample of the
+same workload on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import nmg_inputs as ni  # noqa: E402
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+FP64_NOMINAL_RATIO = 45.0 / 2250.0     # B200 nominal FP64 / dense BF16 (blackwell guide)
+TF32_NOMINAL_RATIO = 1100.0 / 2250.0
+
+
+def peaks():
+    try:
+        with open(PEAKS_FILE) as f:
+            p = json.load(f)
+        p["source"] = "measured (MEASURED_PEAKS.json)"
+        return p
+    except Exception:
+        p = dict(FALLBACK)
+        p["source"] = "fallback (B200_PROFILING.md)"
+        return p
+
+
+# ------------------------------------------------------------------ clocks sampler
+class ClockSampler:
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ algorithmic counts
+def algorithmic_counts(cfg, B):
+    """Per-step algorithmic FLOPs / bytes per kernel class."""
+    n = [cfg.n >> l for l in range(cfg.levels)]
+    L = cfg.levels
+    g64 = 2.0 * B * n[0] * n[0]
+    g32 = 0.0
+    for l in range(L - 1):
+        # r_l = y - A x (n x n), b_post = r - (A P) e (n x n/2)
+        g32 += 2.0 * B * n[l] * n[l] * (1.0 + (0.5 if cfg.nu2 else 0.0))
+        g32 += 2.0 * B * n[l] * n[l] * (max(cfg.nu1 - 1, 0) + max(cfg.nu2 - 1, 0))
+    cnn_per_pt = 2 * (cfg.channels * cfg.ksize + cfg.channels * cfg.channels * cfg.ksize + cfg.channels * cfg.ksize)
+    sm = sum((cfg.nu1 + cfg.nu2) * B * n[l] * cnn_per_pt for l in range(L - 1))
+    return {"gemm64": g64, "gemm32": g32, "smooth": sm,
+            "gemm64_bytes": 8.0 * (n[0] * n[0] + 3 * B * n[0])}
+
+
+# ------------------------------------------------------------------ oracle timing
+def oracle_rate(cfg, factors, weights, y, nrhs, cycles):
+    from oracle import nmg_oracle as O
+    H = O.build_hierarchy(cfg.dim, factors, cfg.alpha, cfg.levels, nu1=cfg.nu1, nu2=cfg.nu2)
+    for l, w in enumerate(weights):
+        O.load_weights(H, l + 1, ni.unflatten_params(cfg, w))
+    ys = y[:nrhs]
+    x = np.zeros_like(ys)
+    t0 = time.perf_counter()
+    for _ in range(cycles):
+        x = O.nmgf_cycle(H, x, ys)
+        O.relative_residual(H, x, ys)
+    dt = time.perf_counter() - t0
+    return nrhs * cycles / dt, dt
+
+
+def host_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        th = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"]
+        return max(th) if th else 1
+    except Exception:
+        return os.cpu_count()
+
+
+# ------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--alpha", type=float, default=1e-3)
+    ap.add_argument("--nrhs", type=int, default=None)
+    ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = ni.CONFIGS[1].replace(alpha=args.alpha)
+    if args.nrhs:
+        cfg = cfg.replace(nrhs=args.nrhs)
+    B = cfg.nrhs
+    workload = f"cfg1_1d_n{cfg.n}_L{cfg.levels}_rhs{B}_per_gpu_alpha{cfg.alpha:g}_Wseed"
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        factors = ni.operator_factors(cfg)
+        W = ni.weights_seed(cfg)
+        y, _ = ni.make_rhs(cfg, factors, cfg.alpha, nrhs=16)
+        rates, secs = [], 0.0
+        for _ in range(args.warmup):
+            oracle_rate(cfg, factors, W, y, 4, 1)
+        for _ in range(args.steps):
+            r, dt = oracle_rate(cfg, factors, W, y, 16, 1)
+            rates.append(r)
+            secs += dt
+        v = args.steps * 16 / secs
+        line = {"impl": "reference", "metric": "RHS*V-cycles/s (1D cfg1, fp64 CPU oracle)", "value": v,
+                "unit": "RHS*cycles/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": workload, "sample": "16 RHS x 1 cycle per step"},
+                "cpu_baseline": {"value": v, "unit": "RHS*cycles/s", "cores": host_threads(), "kind": "oracle",
+                                 "sample": "16 RHS x 1 cycle per step of the cfg1 workload"},
+                "e2e": {"value": v, "unit": "RHS*cycles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2603_01064_b200 as nmg
+
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+
+    factors = ni.operator_factors(cfg)
+    W = ni.weights_seed(cfg)
+    h = nmg.Hierarchy(1, cfg.n, cfg.levels, cfg.alpha, factors, nu1=cfg.nu1, nu2=cfg.nu2, max_rhs=B, device=local)
+    for l, w in enumerate(W):
+        h.load_weights(l + 1, ni.cnn_arch(cfg), w)
+    y_np, _ = ni.make_rhs(cfg, factors, cfg.alpha, nrhs=B, start=rank * B)
+    y = torch.tensor(y_np, dtype=torch.float64, device=dev)
+    x = torch.zeros_like(y)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        h.vcycle(y, x, stream)
+    torch.cuda.synchronize(dev)
+
+    # ---- timed region
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = h.launch_count()
+    barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            h.vcycle(y, x, stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    barrier()
+    launches = h.launch_count() - l0
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * B * args.steps / (ms / 1e3)
+
+    # ---- per-kernel-class device times (CUDA events on the launching stream)
+    h.profile(True)
+    for _ in range(args.steps):
+        h.vcycle(y, x, stream)
+    torch.cuda.synchronize(dev)
+    h.profile(False)
+    prof = h.profile_query()
+    tot_prof = sum(v[0] for v in prof.values())
+    counts = algorithmic_counts(cfg, B)
+    pk = peaks()
+    dom = max(prof, key=lambda k: prof[k][0])
+    dom_ms, dom_n = prof[dom]
+    avg_ms = dom_ms / max(dom_n, 1)
+    per_step_launches = dom_n / args.steps
+    if dom == "gemm64":
+        peak = pk["bf16_tflops"] * FP64_NOMINAL_RATIO
+        achieved = counts["gemm64"] / (avg_ms * 1e-3) / 1e12
+        roof = {"kernel": "dgemm_resid (fp64 outer residual, DMMA)", "bound": "tensor", "unit": "TFLOP/s",
+                "peak_note": "measured bf16 x nominal fp64/bf16 ratio 45/2250"}
+    elif dom == "gemm32":
+        peak = 148 * 128 * 2 * 1.965e9 / 1e12
+        achieved = counts["gemm32"] / (dom_ms / args.steps * 1e-3) / 1e12
+        roof = {"kernel": "sgemm (fp32 inner operator, all levels)", "bound": "alu", "unit": "TFLOP/s",
+                "peak_note": "FP32 FFMA 148 SM x 128 lanes x 2 x 1.965 GHz"}
+    else:
+        peak = 148 * 128 * 2 * 1.965e9 / 1e12
+        achieved = counts["smooth"] / (dom_ms / args.steps * 1e-3) / 1e12
+        roof = {"kernel": f"{dom} (per step)", "bound": "alu", "unit": "TFLOP/s",
+                "peak_note": "FP32 FFMA 148 SM x 128 lanes x 2 x 1.965 GHz"}
+    roof.update({"achieved": achieved, "peak": peak, "frac": achieved / peak, "traffic": None,
+                 "peak_source": pk["source"],
+                 "share_of_step": dom_ms / tot_prof if tot_prof else None,
+                 "classes_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
+                 "launches_per_step": {k: v[1] / args.steps for k, v in prof.items()}})
+
+    # ---- end to end through the host-buffer C-ABI entry
+    e2e = None
+    if not args.no_e2e:
+        yh = torch.empty(y.shape, dtype=torch.float64).pin_memory()
+        xh = torch.zeros(y.shape, dtype=torch.float64).pin_memory()
+        yh.copy_(torch.from_numpy(y_np))
+        yhn, xhn = yh.numpy(), xh.numpy()
+        h.vcycles_host(yhn, xhn, 1, stream=stream)
+        barrier()
+        torch.cuda.synchronize(dev)
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            h.vcycles_host(yhn, xhn, 1, stream=stream)
+        f1.record(stream)
+        torch.cuda.synchronize(dev)
+        ems = f0.elapsed_time(f1)
+        if world > 1:
+            t = torch.tensor([ems], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": world * B * args.steps / (ems / 1e3), "unit": "RHS*cycles/s",
+               "h2d_bytes_per_step": 2 * 8 * B * cfg.n, "d2h_bytes_per_step": 8 * B * cfg.n}
+
+    # ---- RHS solved to 1e-6 / s with converging stand-in weights (alpha = 1e-2)
+    solve = None
+    if not args.no_solve:
+        scfg = cfg.replace(alpha=1e-2)
+        sf = ni.operator_factors(scfg)
+        hs = nmg.Hierarchy(1, scfg.n, scfg.levels, scfg.alpha, sf, nu1=scfg.nu1, nu2=scfg.nu2, max_rhs=B,
+                           device=local)
+        for l, w in enumerate(ni.weights_lin(scfg)):
+            hs.load_weights(l + 1, ni.cnn_arch(scfg), w)
+        ys_np, _ = ni.make_rhs(scfg, sf, scfg.alpha, nrhs=B, start=rank * B)
+        ys = torch.tensor(ys_np, dtype=torch.float64, device=dev)
+        xs = torch.zeros_like(ys)
+        hs.solve(ys, xs, tol=1e-6, max_cycles=100, stream=stream)   # warm
+        xs.zero_()
+        barrier()
+        torch.cuda.synchronize(dev)
+        rep = hs.solve(ys, xs, tol=1e-6, max_cycles=100, stream=stream)
+        sec = rep["wall_seconds"]
+        if world > 1:
+            t = torch.tensor([sec], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            sec = float(t.item())
+        solve = {"value": world * int(rep["converged"].sum()) / sec, "unit": "RHS solved/s (relres<=1e-6)",
+                 "alpha": 1e-2, "weights": "W_lin stand-in", "cycles_max": int(rep["cycles"].max()),
+                 "cycles_mean": float(rep["cycles"].mean()), "converged": int(rep["converged"].sum()),
+                 "seconds": sec}
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only; bounded sample)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        rate, dt = oracle_rate(cfg, factors, W, y_np, 96, 2)
+        cpu = {"value": rate, "unit": "RHS*cycles/s", "cores": host_threads(), "kind": "oracle",
+               "sample": f"96 RHS x 2 cycles of the same workload ({dt:.1f} s)"}
+
+    if rank == 0:
+        line = {"metric": "RHS*V-cycles/s (1D cfg1: fp64 residual + NMGF V-cycle + update per step)",
+                "value": value, "unit": "RHS*cycles/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64 outer / f32 inner",
+                "data": "synthetic (seeded RHS; W_seed Kaiming-uniform weights)",
+                "config": {"workload": workload, "global_batch": world * B, "n": cfg.n, "levels": cfg.levels,
+                           "alpha": cfg.alpha, "nu1": cfg.nu1, "nu2": cfg.nu2, "parallelism": f"rhs-shard x{world}",
+                           "l2": "inputs larger than L2 (no flush)"},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "solve": solve,
+                "gpu_launches": launches, "clocks": clk.summary()}
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,188 @@
+/*
+ * nmg.h -- C ABI of the B200-native batched neural-multigrid solve
+ *          (arxiv 2603.01064, "A level-wise training scheme for learning
+ *          neural multigrid smoothers with application to integral equations").
+ *
+ * What the library computes (PAPER.md = P):
+ *   Solve A x = y for many right-hand sides y,
+ *   A = G + alpha I with G a structured smooth-kernel operator (P:51, P:473,
+ *   P:569), by repeated NMGF cycles x^tau = NMGF(x^{tau-1}, y), x^0 = 0
+ *   (Alg 3 "NMGF1d" P:315-339; Alg 4 "NMGF2d" P:373-401) until the
+ *   relative residual ||y - A x||_2 / ||y||_2 <= tol (1e-6).
+ *   Each level l < L: b = y_l - A^(l) x*, h = N_theta_l(b/||b||)||b||,
+ *   x = x* + F'_l(h) (level filter P:305), y_{l+1} = I_l^{l+1}(y_l - A^(l) x)
+ *   (P:331), recurse from 0 on the Galerkin operator, prolongate,
+ *   then nu2 post-smoothing steps (reading R9).  Level L: exact solve.
+ *
+ * Conventions (all functions):
+ *   - Level numbers are 1-based as in the paper: level 1 is the finest grid,
+ *     level L = desc.levels the coarsest (exact solve).
+ *   - Vector layout is RHS-major, contiguous: 1D [nrhs][n_l]; 2D [nrhs][n_l][n_l]
+ *     with each RHS a column-major n_l x n_l matrix (element (i1,i2) at
+ *     i1 + n_l*i2, the Vec convention of P:363).
+ *   - Pointers documented "device" must be cudaMalloc'd memory on desc.device;
+ *     "host" pointers are ordinary host memory (pinned preferred for *_host).
+ *   - Ownership: the caller owns every buffer it passes; the library deep-copies
+ *     operator factors and weights at create/load time and owns all device
+ *     workspaces.  nmg_vcycle / nmg_solve never allocate.
+ *   - Streams: device-pointer calls enqueue on the caller's stream and return
+ *     without synchronising, except nmg_solve, which synchronises once per cycle
+ *     and returns when done.
+ *   - Errors: no function throws or aborts across the ABI.  Every call returns
+ *     an nmg_status; nmg_last_error() gives a thread-local message.  After
+ *     NMG_ERR_CUDA the handle is poisoned and must be destroyed.
+ *   - Threading: a handle is used by one host thread / stream at a time.
+ *   - There is no CPU fallback: without a visible sm_100 device,
+ *     nmg_create_hierarchy fails with NMG_ERR_CUDA.
+ */
+#ifndef NMG_H
+#define NMG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct nmg_hierarchy nmg_hierarchy;   /* opaque, library-owned device state */
+
+typedef enum {
+  NMG_OK = 0,
+  NMG_ERR_INVALID_ARG = 1,  /* null pointer, n not a power of two, n_L < 2, alpha <= 0,
+                               nrhs > max_rhs, level out of range                         */
+  NMG_ERR_SHAPE = 2,        /* weight count inconsistent with the architecture            */
+  NMG_ERR_NOT_SPD = 3,      /* Cholesky pivot <= 0 at the coarsest level (index in msg)   */
+  NMG_ERR_NO_WEIGHTS = 4,   /* a cycle was requested while a level 1..L-1 has no smoother */
+  NMG_ERR_NONFINITE = 5,    /* NaN/Inf residual; report->fail_cycle / fail_rhs are set    */
+  NMG_ERR_CUDA = 6,         /* CUDA runtime / launch failure, or no sm_100 device         */
+  NMG_ERR_OOM = 7,          /* device allocation failed                                   */
+  NMG_ERR_UNSUPPORTED = 8   /* architecture / mode not implemented                        */
+} nmg_status;
+
+/* Problem descriptor (SPEC ProblemSpec analogue). */
+typedef struct {
+  int32_t dim;          /* 1 or 2                                                          */
+  int32_t n;            /* finest points per axis, power of two, n >> (levels-1) >= 2      */
+  int32_t levels;       /* L >= 1; levels 1..L-1 carry a smoother, level L is exact        */
+  double  alpha;        /* A = G + alpha I, alpha > 0 (Tikhonov weight)         */
+  int32_t nu1, nu2;     /* pre/post smoothing steps per level (paper nu2 = 0, P:233;
+                           BASELINE nu1 = nu2 = 1)                                         */
+  int32_t level_filter; /* 1: Alg 3/4 with F'_l; 0: Alg 2          */
+  int32_t max_rhs;      /* workspace sizing: largest nrhs ever passed                      */
+  int32_t device;       /* CUDA ordinal                                                    */
+} nmg_problem_desc;
+
+/* CNN smoother architecture (reading R7): n_layers convolutions 1 -> C -> ... -> C -> 1,
+ * kernel ksize (per axis), stride 1, zero "same" padding, bias, ReLU between layers,
+ * none after the last.  Supported: 1D (3, 16, 5); 2D (4, 32, 3) and (4, 48, 3). */
+typedef struct {
+  int32_t n_layers, channels, ksize;
+} nmg_cnn_arch;
+
+/* Solve report (SPEC SolveReport analogue), caller-allocated HOST memory. */
+typedef struct {
+  int32_t *cycles;       /* [nrhs] cycles applied to each RHS                              */
+  uint8_t *converged;    /* [nrhs] 1 if relres <= tol was reached                          */
+  double  *history;      /* [nrhs][max_cycles+1] relres after each cycle (index 0 = x0),
+                            NaN after the RHS froze; may be NULL                            */
+  double   wall_seconds; /* written: elapsed device time of the cycle loop                 */
+  int32_t  total_cycles; /* written: cycles executed for the batch                         */
+  int32_t  fail_cycle;   /* written on NMG_ERR_NONFINITE, else -1                          */
+  int32_t  fail_rhs;     /* written on NMG_ERR_NONFINITE, else -1                          */
+} nmg_report;
+
+/* Build the level hierarchy (host fp64 Galerkin chain A^(l+1) = I_l^{l+1} A^(l) I_{l+1}^l,
+ * P:160; coarsest Cholesky; device uploads).
+ *   factors (host, read-only, copied):
+ *     dim 1: G, n*n doubles row-major, symmetric                 (A = G + alpha I)
+ *     dim 2: B then C, each n*n doubles row-major, symmetric:
+ *            G = B (x) C, i.e. G Vec(X) = Vec(C X B^T)
+ *   out: receives the handle.  Errors: INVALID_ARG, NOT_SPD, CUDA, OOM. */
+nmg_status nmg_create_hierarchy(const nmg_problem_desc *desc, const double *factors,
+                                nmg_hierarchy **out);
+
+/* Load the smoother theta_l of level `level` (1..L-1), fp32 parameters in PyTorch
+ * state_dict order (w0, b0, w1, b1, ...; conv weights [out][in][k] / [out][in][k2][k1]).
+ * params: host, n_params floats, copied.  Loading a level twice replaces it.
+ * Errors: INVALID_ARG, SHAPE, UNSUPPORTED, CUDA. */
+nmg_status nmg_load_smoother_weights(nmg_hierarchy *h, int32_t level, const nmg_cnn_arch *arch,
+                                     const float *params, size_t n_params);
+
+/* One cycle x <- NMGF(x, y) for nrhs right-hand sides (one tau step), computed in
+ * correction form x + NMGF(0, y - A x) (pin P11): fp64 outer residual, fp32-accurate
+ * inner cycle, fp64 update.  y, x: device fp64 [nrhs][N]; x in/out.  Asynchronous. */
+nmg_status nmg_vcycle(nmg_hierarchy *h, int32_t nrhs, const double *y, double *x, void *stream);
+
+/* Outer iteration from the x passed in (x0 = 0 for the paper's solve) until every
+ * RHS has relres <= tol or max_cycles; converged RHS are frozen.  y, x: device
+ * fp64 [nrhs][N]; rep: host (may be NULL).  Synchronises once per cycle.
+ * Errors: NONFINITE (rep->fail_*), NO_WEIGHTS, CUDA. */
+nmg_status nmg_solve(nmg_hierarchy *h, int32_t nrhs, const double *y, double *x, double tol,
+                     int32_t max_cycles, nmg_report *rep, void *stream);
+
+/* Same as nmg_vcycle repeated `cycles` times, but y and x are HOST buffers: the call
+ * copies y and x host->device, runs the cycles and copies x back (end-to-end path).
+ * relres (host, may be NULL) receives [nrhs] fp64 relative residuals of the input x
+ * measured before the last cycle.  Synchronous. */
+nmg_status nmg_vcycles_host(nmg_hierarchy *h, int32_t nrhs, const double *y_host, double *x_host,
+                            int32_t cycles, double *relres_host, void *stream);
+
+/* fp64 residual r = y - A x at level 1 and relres = ||r||/||y|| per RHS.
+ * y, x: device fp64 [nrhs][N]; r: device fp64 [nrhs][N] or NULL; relres: device fp64
+ * [nrhs] or NULL.  Asynchronous. */
+nmg_status nmg_residual(nmg_hierarchy *h, int32_t nrhs, const double *y, const double *x,
+                        double *r, double *relres, void *stream);
+
+/* Diagnostic single-operator entry for parity tests (fp32 device buffers unless noted).
+ * level is 1-based.  op:
+ *   NMG_OP_APPLY     out = A^(l) in                          in/out [nrhs][N_l]
+ *   NMG_OP_RESIDUAL  out = out - A^(l) in  (out holds y_l)    in/out [nrhs][N_l]
+ *   NMG_OP_RESTRICT  out = I_l^{l+1} in                       in [nrhs][N_l], out [nrhs][N_{l+1}]
+ *   NMG_OP_PROLONG   out = out + I_{l+1}^l in                 in [nrhs][N_{l+1}], out [nrhs][N_l]
+ *   NMG_OP_FILTER    out = F'_l(in)                           in/out [nrhs][N_l]
+ *   NMG_OP_CNN       out = N_theta_l(in)                      in/out [nrhs][N_l]
+ *   NMG_OP_SMOOTH    out = out + F'_l(||in|| N(in/||in||))    in = b, out = x  [nrhs][N_l]
+ *   NMG_OP_COARSE    out = (A^(L))^{-1} in  (level must be L)  in/out [nrhs][N_L]
+ *   NMG_OP_CYCLE0    out = NMGF(0, in) at level l (fp32)       in/out [nrhs][N_l]
+ * Asynchronous. */
+enum {
+  NMG_OP_APPLY = 0, NMG_OP_RESIDUAL = 1, NMG_OP_RESTRICT = 2, NMG_OP_PROLONG = 3,
+  NMG_OP_FILTER = 4, NMG_OP_CNN = 5, NMG_OP_SMOOTH = 6, NMG_OP_COARSE = 7, NMG_OP_CYCLE0 = 8
+};
+nmg_status nmg_debug_level_op(nmg_hierarchy *h, int32_t level, int32_t op, int32_t nrhs,
+                              const void *in, void *out, void *stream);
+
+/* Per-kernel-class device timing for roofline reports: while enabled, the library
+ * records a CUDA event pair on the launching stream around every kernel it enqueues
+ * and accumulates the elapsed time per class.  nmg_profile(h, 1) clears and starts,
+ * nmg_profile(h, 0) stops.  nmg_profile_query synchronises on the recorded events and
+ * returns the total device milliseconds and launch count of class `kclass`. */
+enum {
+  NMG_K_GEMM64 = 0,    /* fp64 outer residual GEMM (+ norm partials)           */
+  NMG_K_GEMM32 = 1,    /* fp32-accurate inner operator applies                  */
+  NMG_K_SMOOTH = 2,    /* fused norm + CNN + level filter + update              */
+  NMG_K_TRANSFER = 3,  /* restriction / prolongation                            */
+  NMG_K_COARSE = 4,    /* coarsest Cholesky solve                               */
+  NMG_K_MISC = 5,      /* relres, update, norms, conversions                    */
+  NMG_K_COUNT = 6
+};
+nmg_status nmg_profile(nmg_hierarchy *h, int32_t enable);
+nmg_status nmg_profile_query(nmg_hierarchy *h, int32_t kclass, double *total_ms, int64_t *launches);
+
+/* Number of the library's own kernel launches enqueued since the handle was created
+ * (bench evidence, "gpu_launches"). */
+int64_t nmg_launch_count(const nmg_hierarchy *h);
+
+void nmg_destroy_hierarchy(nmg_hierarchy *h);
+
+/* Thread-local message for the last non-OK status on this thread ("" if none). */
+const char *nmg_last_error(void);
+
+/* Library version string. */
+const char *nmg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NMG_H */

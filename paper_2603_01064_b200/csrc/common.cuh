@@ -1,0 +1,36 @@
+// Shared device/host helpers for the nmg library (sm_100a only).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "nmg kernels are written for sm_100a only"
+#endif
+
+#define NMG_HD __host__ __device__ __forceinline__
+#define NMG_D __device__ __forceinline__
+
+namespace nmg {
+
+constexpr int kWarp = 32;
+
+NMG_HD int ceil_div(int a, int b) { return (a + b - 1) / b; }
+NMG_HD int64_t ceil_div64(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Deterministic block-wide sum of one double per thread (fixed tree; blockDim.x a
+// multiple of 32, <= 1024).  All threads receive the total.
+NMG_D double block_sum_f64(double v, double* scratch /* >= 32 doubles */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  double t = (lane < nw) ? scratch[lane] : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  return t;
+}
+
+}  // namespace nmg

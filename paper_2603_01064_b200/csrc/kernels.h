@@ -1,0 +1,73 @@
+// Host-side launchers of the nmg device kernels (all enqueue on `s`).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace nmg {
+
+// ---- GEMMs -----------------------------------------------------------------
+// Operand conventions: X is [M][K] row-major (K contiguous, leading dim ldx).
+// W is either K-major ([N][K], ldw) or N-major ([K][N], ldw).
+// D[m][n] = (C ? C[m][n] : 0) - sign * sum_k X[m][k] W(n,k)     (sign = +1: residual form)
+// Batched over blockIdx.z with element strides sx/sw/sc/sd.
+struct Gemm32Args {
+  int M, N, K, batch;
+  const float* X; int64_t ldx, sx;
+  const float* W; int64_t ldw, sw; bool w_kmajor;
+  const float* C; int64_t ldc, sc;       // may be null (then D = acc)
+  float* D; int64_t ldd, sd;
+  bool negate;                            // D = C - acc (true) or C + acc (false)
+};
+void gemm_f32(const Gemm32Args& a, cudaStream_t s);
+
+// fp64 residual GEMM (DMMA): R = Y - X W^T-ish with the same conventions (W K-major,
+// batch 1).  Writes r32 (fp32, ldr32) and optionally r64; writes per-row sums of r^2
+// for each 64-wide column tile into part[m * n_tiles + tile] (fp64), deterministic.
+struct Gemm64Args {
+  int M, N, K;
+  const double* X; int64_t ldx;
+  const double* W; int64_t ldw;          // [N][K] row-major
+  const double* Y; int64_t ldy;          // may be null (then R = -acc... used for apply)
+  float* r32; int64_t ldr32;             // may be null
+  double* r64; int64_t ldr64;            // may be null
+  double* part;                           // may be null; [M][ceil(N/64)]
+  bool negate;                            // R = Y - acc (true) / Y + acc
+};
+int gemm_f64_ntiles(int N);
+void gemm_f64(const Gemm64Args& a, cudaStream_t s);
+
+// ---- 1D smoother: norm -> CNN (3 layers, C=16, k=5) -> F' -> update ----------
+struct Smooth1dArgs {
+  int n, nrhs;
+  const float* b; int64_t ldb;     // input rows
+  float* x; int64_t ldx;           // output rows
+  const float* params;             // 1473 floats, state_dict order
+  const float2* twiddle; int tw_n; // exp(-2 pi i k / tw_n), k < tw_n/2
+  bool normalize;                  // h = s N(b/s) (true) or h = N(b) (debug)
+  bool filter;                     // apply F'_l
+  bool accumulate;                 // x += (true) or x = (false)
+};
+void smooth1d(const Smooth1dArgs& a, cudaStream_t s);
+size_t smooth1d_smem(int n);
+
+// ---- 1D transfers (reading R4) ------------------------------------------------
+void restrict1d(int nrhs, int n_f, const float* f, int64_t ldf, float* c, int64_t ldc, cudaStream_t s);
+void prolong_add1d(int nrhs, int n_c, const float* c, int64_t ldc, float* f, int64_t ldf, cudaStream_t s);
+
+// ---- 1D filter only (debug op) ------------------------------------------------
+void filter1d(int n, int nrhs, const float* in, float* out, const float2* tw, int tw_n, cudaStream_t s);
+
+// ---- coarse solve: Cholesky factor applied by forward/back substitution ---------
+void coarse_chol_solve(int nc, int nrhs, const double* Lrow, const double* Lcol,
+                       const float* y, int64_t ldy, float* x, int64_t ldx, cudaStream_t s);
+
+// ---- outer (fp64) helpers --------------------------------------------------------
+void row_norms_f64(int nrhs, int N, const double* y, int64_t ldy, double* out, cudaStream_t s);
+void relres_finalize(int nrhs, int ntiles, const double* part, const double* ynorm, double* relres,
+                     double tol, uint8_t* active, cudaStream_t s);
+void update_x(int nrhs, int N, double* x, int64_t ldx, const float* d, int64_t ldd,
+              const uint8_t* active, cudaStream_t s);
+void f64_to_f32(int64_t count, const double* in, float* out, cudaStream_t s);
+void f32_to_f64(int64_t count, const float* in, double* out, cudaStream_t s);
+
+}  // namespace nmg

@@ -1,0 +1,702 @@
+// C-ABI implementation: hierarchy construction (host fp64), device workspaces,
+// and the NMGF cycle orchestration on one stream.
+//
+// Paper mapping (PAPER.md = P):
+//   Galerkin chain  A^(l+1) = I_l^{l+1} A^(l) I_{l+1}^l        Alg 1, Alg 3
+//   smoothing step  b = y - A x*, h = N(b/|b|)|b|, x = x*+F'(h)  Alg 3
+//   restriction     y_{l+1} = I_l^{l+1}(y_l - A x)
+//   correction      x += I_{l+1}^l NMGF(0, y_{l+1})
+//   coarse          x_L = (A^(L))^{-1} y_L
+//   outer loop      x^tau = NMGF(x^{tau-1}, y), relres <= tol
+// Implementation choices that differ from a literal transcription:
+//   * correction form x + NMGF(0, y - A x) with an fp64 outer residual (pin P11);
+//   * the post-smoothing residual is b = r_l - (A_l P_l) e  (A_l P_l precomputed),
+//     which equals y_l - A_l (x_l + P_l e) exactly and halves that GEMM.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/nmg.h"
+#include "kernels.h"
+
+using namespace nmg;
+
+namespace {
+
+thread_local std::string g_err;
+
+nmg_status fail(nmg_status st, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define NMG_CUDA(expr)                                                                     \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess) {                                                               \
+      return fail(_e == cudaErrorMemoryAllocation ? NMG_ERR_OOM : NMG_ERR_CUDA, "%s: %s (%s:%d)", \
+                  #expr, cudaGetErrorString(_e), __FILE__, __LINE__);                       \
+    }                                                                                      \
+  } while (0)
+
+#define NMG_TRY(expr)                 \
+  do {                                \
+    nmg_status _s = (expr);           \
+    if (_s != NMG_OK) return _s;      \
+  } while (0)
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  ~DevBuf() { if (p) cudaFree(p); }
+  nmg_status alloc(size_t count) {
+    if (p) { cudaFree(p); p = nullptr; }
+    n = count;
+    if (count == 0) return NMG_OK;
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    if (e != cudaSuccess) return fail(NMG_ERR_OOM, "cudaMalloc(%zu bytes): %s", count * sizeof(T), cudaGetErrorString(e));
+    return NMG_OK;
+  }
+  nmg_status upload(const T* h, size_t count) {
+    NMG_TRY(alloc(count));
+    NMG_CUDA(cudaMemcpy(p, h, count * sizeof(T), cudaMemcpyHostToDevice));
+    return NMG_OK;
+  }
+};
+
+// ---------------------------------------------------------------- host fp64 transfers
+// R (n_f/2 x n_f) applied to the rows of a column block: out = R * A  (A: n_f x cols)
+void host_restrict_rows(const std::vector<double>& A, int n_f, int cols, std::vector<double>& out) {
+  const int n_c = n_f / 2;
+  out.assign((size_t)n_c * cols, 0.0);
+  for (int j = 0; j < n_c; ++j) {
+    const int taps[4] = {std::max(2 * j - 1, 0), 2 * j, 2 * j + 1, std::min(2 * j + 2, n_f - 1)};
+    const double wts[4] = {1.0 / 8, 3.0 / 8, 3.0 / 8, 1.0 / 8};
+    double* o = &out[(size_t)j * cols];
+    for (int t = 0; t < 4; ++t) {
+      const double* a = &A[(size_t)taps[t] * cols];
+      for (int c = 0; c < cols; ++c) o[c] += wts[t] * a[c];
+    }
+  }
+}
+// out = A * P  (A: rows x n_f, P: n_f x n_f/2)
+void host_prolong_cols(const std::vector<double>& A, int rows, int n_f, std::vector<double>& out) {
+  const int n_c = n_f / 2;
+  out.assign((size_t)rows * n_c, 0.0);
+  for (int r = 0; r < rows; ++r) {
+    const double* a = &A[(size_t)r * n_f];
+    double* o = &out[(size_t)r * n_c];
+    for (int i = 0; i < n_f; ++i) {
+      const int j = i >> 1;
+      const int k = std::min(std::max((i & 1) ? j + 1 : j - 1, 0), n_c - 1);
+      o[j] += 0.75 * a[i];
+      o[k] += 0.25 * a[i];
+    }
+  }
+}
+// Galerkin: R A P for square A (n_f x n_f)
+void host_galerkin(const std::vector<double>& A, int n_f, std::vector<double>& out) {
+  std::vector<double> AP;
+  host_prolong_cols(A, n_f, n_f, AP);          // n_f x n_c
+  host_restrict_rows(AP, n_f, n_f / 2, out);   // n_c x n_c
+}
+
+bool host_cholesky(std::vector<double>& A, int n, int* bad_pivot) {   // in place, lower
+  for (int j = 0; j < n; ++j) {
+    double d = A[(size_t)j * n + j];
+    for (int k = 0; k < j; ++k) d -= A[(size_t)j * n + k] * A[(size_t)j * n + k];
+    if (!(d > 0.0)) { *bad_pivot = j; return false; }
+    const double ljj = std::sqrt(d);
+    A[(size_t)j * n + j] = ljj;
+    for (int i = j + 1; i < n; ++i) {
+      double s = A[(size_t)i * n + j];
+      for (int k = 0; k < j; ++k) s -= A[(size_t)i * n + k] * A[(size_t)j * n + k];
+      A[(size_t)i * n + j] = s / ljj;
+    }
+    for (int i = 0; i < j; ++i) A[(size_t)i * n + j] = 0.0;
+  }
+  return true;
+}
+
+std::vector<float> to_f32(const std::vector<double>& v) {
+  std::vector<float> o(v.size());
+  for (size_t i = 0; i < v.size(); ++i) o[i] = (float)v[i];
+  return o;
+}
+
+int ilog2(int v) { int l = 0; while ((1 << l) < v) ++l; return l; }
+
+}  // namespace
+
+// ======================================================================= handle
+struct nmg_hierarchy {
+  nmg_problem_desc d{};
+  int L = 0;
+  std::vector<int> n;      // points per axis, level 0 = finest
+  std::vector<int64_t> N;  // unknowns per level
+  // level-1 fp64 operator (1D: A; 2D: B, C)
+  DevBuf<double> A64, B64, C64;
+  // per smoothed level (l < L-1) fp32 operators
+  std::vector<std::unique_ptr<DevBuf<float>>> A32, AP32;
+  // coarse Cholesky factor (row-major L and L^T)
+  DevBuf<double> Lrow, Lcol;
+  int nc = 0;
+  // smoother weights per level
+  std::vector<std::unique_ptr<DevBuf<float>>> W;
+  std::vector<int> w_loaded;
+  nmg_cnn_arch arch{};
+  DevBuf<float2> tw;
+  int tw_n = 0;
+  // workspaces
+  std::vector<std::unique_ptr<DevBuf<float>>> wy, wx, wr, wb;
+  DevBuf<double> part, ynorm, relres;
+  DevBuf<uint8_t> active;
+  DevBuf<double> hy, hx;   // staging for nmg_vcycles_host (lazy)
+  int ntiles = 0;
+  int64_t launches = 0;
+  bool poisoned = false;
+  // profiling (nmg_profile): event pairs per kernel class
+  bool prof_on = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  struct Rec { int cls; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  ~nmg_hierarchy() { for (auto e : ev_pool) cudaEventDestroy(e); }
+};
+
+namespace {
+
+nmg_status check_launch(nmg_hierarchy* h) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    h->poisoned = true;
+    return fail(NMG_ERR_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+  }
+  return NMG_OK;
+}
+
+cudaEvent_t prof_event(nmg_hierarchy* h) {
+  if (h->ev_used == h->ev_pool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    h->ev_pool.push_back(e);
+  }
+  return h->ev_pool[h->ev_used++];
+}
+
+// Counts one library launch of class `cls`; when profiling, brackets it with events.
+struct Prof {
+  nmg_hierarchy* h; int cls; cudaStream_t s; cudaEvent_t a = nullptr;
+  Prof(nmg_hierarchy* h_, int cls_, cudaStream_t s_) : h(h_), cls(cls_), s(s_) {
+    h->launches++;
+    if (h->prof_on && (a = prof_event(h))) cudaEventRecord(a, s);
+  }
+  ~Prof() {
+    if (!a) return;
+    cudaEvent_t b = prof_event(h);
+    if (!b) return;
+    cudaEventRecord(b, s);
+    h->recs.push_back({cls, a, b});
+  }
+};
+
+// ---------------------------------------------------------------- 1D level operations
+nmg_status smooth_level(nmg_hierarchy* h, int l, int nrhs, const float* b, float* x, bool accumulate,
+                        cudaStream_t s) {
+  Smooth1dArgs a{};
+  a.n = h->n[l]; a.nrhs = nrhs;
+  a.b = b; a.ldb = a.n;
+  a.x = x; a.ldx = a.n;
+  a.params = h->W[l]->p;
+  a.twiddle = h->tw.p; a.tw_n = h->tw_n;
+  a.normalize = true;
+  a.filter = h->d.level_filter != 0;
+  a.accumulate = accumulate;
+  { Prof p(h, NMG_K_SMOOTH, s); smooth1d(a, s); }
+  return check_launch(h);
+}
+
+// D = C - X * W^T-ish  (W: [N][K] K-major), fp32
+nmg_status resid_gemm(nmg_hierarchy* h, int M, int N, int K, const float* X, const float* W, const float* C,
+                      float* D, cudaStream_t s) {
+  Gemm32Args g{};
+  g.M = M; g.N = N; g.K = K; g.batch = 1;
+  g.X = X; g.ldx = K; g.sx = 0;
+  g.W = W; g.ldw = K; g.sw = 0; g.w_kmajor = true;
+  g.C = C; g.ldc = N; g.sc = 0;
+  g.D = D; g.ldd = N; g.sd = 0;
+  g.negate = true;
+  { Prof p(h, NMG_K_GEMM32, s); gemm_f32(g, s); }
+  return check_launch(h);
+}
+
+// NMGF(0, y_l) at level l (0-based): input wy[l], output wx[l].
+nmg_status cycle_level_1d(nmg_hierarchy* h, int l, int nrhs, cudaStream_t s) {
+  const int n = h->n[l];
+  float* y = h->wy[l]->p;
+  float* x = h->wx[l]->p;
+  if (l == h->L - 1) {
+    { Prof p(h, NMG_K_COARSE, s); coarse_chol_solve(h->nc, nrhs, h->Lrow.p, h->Lcol.p, y, n, x, n, s); }
+    return check_launch(h);
+  }
+  float* r = h->wr[l]->p;
+  float* b = h->wb[l]->p;
+  const float* A = h->A32[l]->p;
+  const float* AP = h->AP32[l]->p;
+  const int nu1 = h->d.nu1, nu2 = h->d.nu2;
+  const float* rl = y;
+  if (nu1 >= 1) {
+    NMG_TRY(smooth_level(h, l, nrhs, y, x, false, s));           // x = x* + F'(h), x* = 0
+    for (int k = 1; k < nu1; ++k) {
+      NMG_TRY(resid_gemm(h, nrhs, n, n, x, A, y, b, s));          // b = y - A x
+      NMG_TRY(smooth_level(h, l, nrhs, b, x, true, s));
+    }
+    NMG_TRY(resid_gemm(h, nrhs, n, n, x, A, y, r, s));            // r_l = y - A x
+    rl = r;
+  } else {
+    NMG_CUDA(cudaMemsetAsync(x, 0, sizeof(float) * (size_t)nrhs * n, s));
+  }
+  { Prof p(h, NMG_K_TRANSFER, s); restrict1d(nrhs, n, rl, n, h->wy[l + 1]->p, n / 2, s); }   // y_{l+1} = R r_l
+  NMG_TRY(check_launch(h));
+  NMG_TRY(cycle_level_1d(h, l + 1, nrhs, s));
+  const float* e = h->wx[l + 1]->p;
+  if (nu2 >= 1) {
+    NMG_TRY(resid_gemm(h, nrhs, n, n / 2, e, AP, rl, b, s));       // b = r_l - (A P) e
+  }
+  { Prof p(h, NMG_K_TRANSFER, s); prolong_add1d(nrhs, n / 2, e, n / 2, x, n, s); }   // x += P e
+  NMG_TRY(check_launch(h));
+  if (nu2 >= 1) {
+    NMG_TRY(smooth_level(h, l, nrhs, b, x, true, s));
+    for (int k = 1; k < nu2; ++k) {
+      NMG_TRY(resid_gemm(h, nrhs, n, n, x, A, y, b, s));
+      NMG_TRY(smooth_level(h, l, nrhs, b, x, true, s));
+    }
+  }
+  return NMG_OK;
+}
+
+nmg_status inner_cycle(nmg_hierarchy* h, int nrhs, cudaStream_t s) {
+  if (h->d.dim == 1) return cycle_level_1d(h, 0, nrhs, s);
+  return fail(NMG_ERR_UNSUPPORTED, "2D cycle not implemented yet");
+}
+
+// fp64 residual at level 1: r32 = y - A x -> wy[0]; optional r64; norm partials -> part
+nmg_status outer_residual(nmg_hierarchy* h, int nrhs, const double* y, const double* x, double* r64,
+                          bool want_part, cudaStream_t s) {
+  if (h->d.dim != 1) return fail(NMG_ERR_UNSUPPORTED, "2D residual not implemented yet");
+  Gemm64Args g{};
+  const int n = h->n[0];
+  g.M = nrhs; g.N = n; g.K = n;
+  g.X = x; g.ldx = n;
+  g.W = h->A64.p; g.ldw = n;
+  g.Y = y; g.ldy = n;
+  g.r32 = h->wy[0]->p; g.ldr32 = n;
+  g.r64 = r64; g.ldr64 = n;
+  g.part = want_part ? h->part.p : nullptr;
+  g.negate = true;
+  { Prof p(h, NMG_K_GEMM64, s); gemm_f64(g, s); }
+  return check_launch(h);
+}
+
+nmg_status check_ready(nmg_hierarchy* h, int nrhs) {
+  if (!h) return fail(NMG_ERR_INVALID_ARG, "null handle");
+  if (h->poisoned) return fail(NMG_ERR_CUDA, "handle poisoned by an earlier CUDA error");
+  if (nrhs < 0 || nrhs > h->d.max_rhs) return fail(NMG_ERR_INVALID_ARG, "nrhs %d outside [0, max_rhs=%d]", nrhs, h->d.max_rhs);
+  for (int l = 0; l < h->L - 1; ++l)
+    if (!h->w_loaded[l]) return fail(NMG_ERR_NO_WEIGHTS, "level %d has no smoother weights", l + 1);
+  NMG_CUDA(cudaSetDevice(h->d.device));
+  return NMG_OK;
+}
+
+// one outer step: residual (+relres/active), inner cycle, masked update
+nmg_status outer_step(nmg_hierarchy* h, int nrhs, const double* y, double* x, double tol, bool use_active,
+                      cudaStream_t s) {
+  const int64_t N = h->N[0];
+  NMG_TRY(outer_residual(h, nrhs, y, x, nullptr, true, s));
+  { Prof p(h, NMG_K_MISC, s); relres_finalize(nrhs, h->ntiles, h->part.p, h->ynorm.p, h->relres.p, tol, h->active.p, s); }
+  NMG_TRY(check_launch(h));
+  NMG_TRY(inner_cycle(h, nrhs, s));
+  { Prof p(h, NMG_K_MISC, s); update_x(nrhs, (int)N, x, N, h->wx[0]->p, N, use_active ? h->active.p : nullptr, s); }
+  return check_launch(h);
+}
+
+}  // namespace
+
+// ======================================================================= C ABI
+extern "C" {
+
+const char* nmg_last_error(void) { return g_err.c_str(); }
+const char* nmg_version(void) { return "nmg-b200 0.1 (sm_100a)"; }
+int64_t nmg_launch_count(const nmg_hierarchy* h) { return h ? h->launches : 0; }
+
+nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* factors, nmg_hierarchy** out) {
+  g_err.clear();
+  if (!desc || !factors || !out) return fail(NMG_ERR_INVALID_ARG, "null argument");
+  *out = nullptr;
+  const nmg_problem_desc& d = *desc;
+  if (d.dim != 1 && d.dim != 2) return fail(NMG_ERR_INVALID_ARG, "dim must be 1 or 2 (got %d)", d.dim);
+  if (d.n < 2 || (d.n & (d.n - 1))) return fail(NMG_ERR_INVALID_ARG, "n must be a power of two >= 2 (got %d)", d.n);
+  if (d.levels < 1 || (d.n >> (d.levels - 1)) < 2)
+    return fail(NMG_ERR_INVALID_ARG, "levels %d too deep for n = %d", d.levels, d.n);
+  if (!(d.alpha > 0.0)) return fail(NMG_ERR_INVALID_ARG, "alpha must be > 0");
+  if (d.nu1 < 0 || d.nu2 < 0 || d.max_rhs < 1) return fail(NMG_ERR_INVALID_ARG, "bad nu1/nu2/max_rhs");
+  const int nc = d.n >> (d.levels - 1);
+  const int Nc = d.dim == 1 ? nc : nc * nc;
+  if (Nc > 256) return fail(NMG_ERR_UNSUPPORTED, "coarsest system %d > 256 unknowns", Nc);
+  if (d.dim == 1 && d.n > 8192) return fail(NMG_ERR_UNSUPPORTED, "1D n > 8192");
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= d.device || d.device < 0)
+    return fail(NMG_ERR_CUDA, "no CUDA device %d visible (no CPU fallback exists)", d.device);
+  cudaDeviceProp prop;
+  NMG_CUDA(cudaGetDeviceProperties(&prop, d.device));
+  if (prop.major != 10) return fail(NMG_ERR_CUDA, "device %d is sm_%d%d; this library is built for sm_100a", d.device, prop.major, prop.minor);
+  NMG_CUDA(cudaSetDevice(d.device));
+
+  auto h = std::make_unique<nmg_hierarchy>();
+  h->d = d;
+  h->L = d.levels;
+  for (int l = 0; l < h->L; ++l) {
+    h->n.push_back(d.n >> l);
+    h->N.push_back(d.dim == 1 ? (int64_t)(d.n >> l) : (int64_t)(d.n >> l) * (d.n >> l));
+  }
+  h->nc = Nc;
+  const int n = d.n;
+  const size_t nn = (size_t)n * n;
+
+  std::vector<double> Acoarse;
+  if (d.dim == 1) {
+    std::vector<double> A(factors, factors + nn);
+    for (int i = 0; i < n; ++i) A[(size_t)i * n + i] += d.alpha;
+    NMG_TRY(h->A64.upload(A.data(), nn));
+    for (int l = 0; l < h->L - 1; ++l) {
+      const int nl = h->n[l];
+      h->A32.emplace_back(new DevBuf<float>());
+      h->AP32.emplace_back(new DevBuf<float>());
+      NMG_TRY(h->A32.back()->upload(to_f32(A).data(), (size_t)nl * nl));
+      std::vector<double> AP, Ac;
+      host_prolong_cols(A, nl, nl, AP);                 // A_l P_l : nl x nl/2
+      NMG_TRY(h->AP32.back()->upload(to_f32(AP).data(), (size_t)nl * (nl / 2)));
+      host_restrict_rows(AP, nl, nl / 2, Ac);           // R A P
+      A.swap(Ac);
+    }
+    Acoarse = A;
+  } else {
+    std::vector<double> B(factors, factors + nn), C(factors + nn, factors + 2 * nn), Q(nn, 0.0);
+    for (int i = 0; i < n; ++i) Q[(size_t)i * n + i] = 1.0;
+    NMG_TRY(h->B64.upload(B.data(), nn));
+    NMG_TRY(h->C64.upload(C.data(), nn));
+    for (int l = 0; l < h->L - 1; ++l) {
+      const int nl = h->n[l];
+      std::vector<double> t;
+      host_galerkin(B, nl, t); B.swap(t);
+      host_galerkin(C, nl, t); C.swap(t);
+      host_galerkin(Q, nl, t); Q.swap(t);
+    }
+    Acoarse.assign((size_t)Nc * Nc, 0.0);
+    for (int i2 = 0; i2 < nc; ++i2)
+      for (int i1 = 0; i1 < nc; ++i1)
+        for (int j2 = 0; j2 < nc; ++j2)
+          for (int j1 = 0; j1 < nc; ++j1)
+            Acoarse[(size_t)(i1 + nc * i2) * Nc + (j1 + nc * j2)] =
+                B[(size_t)i2 * nc + j2] * C[(size_t)i1 * nc + j1] +
+                d.alpha * Q[(size_t)i2 * nc + j2] * Q[(size_t)i1 * nc + j1];
+  }
+  int bad = -1;
+  if (!host_cholesky(Acoarse, Nc, &bad))
+    return fail(NMG_ERR_NOT_SPD, "coarsest operator not SPD: Cholesky pivot %d <= 0", bad);
+  std::vector<double> Lt((size_t)Nc * Nc);
+  for (int i = 0; i < Nc; ++i)
+    for (int j = 0; j < Nc; ++j) Lt[(size_t)j * Nc + i] = Acoarse[(size_t)i * Nc + j];
+  NMG_TRY(h->Lrow.upload(Acoarse.data(), Acoarse.size()));
+  NMG_TRY(h->Lcol.upload(Lt.data(), Lt.size()));
+
+  // twiddles exp(-2 pi i k / tw_n), k < tw_n / 2
+  h->tw_n = n;
+  {
+    std::vector<float2> tw(std::max(1, n / 2));
+    for (int k = 0; k < n / 2; ++k) {
+      const double ang = -2.0 * M_PI * (double)k / (double)n;
+      tw[k] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+    }
+    NMG_TRY(h->tw.upload(tw.data(), tw.size()));
+  }
+  // weights slots
+  h->w_loaded.assign(std::max(0, h->L - 1), 0);
+  for (int l = 0; l < h->L - 1; ++l) h->W.emplace_back(new DevBuf<float>());
+  // workspaces
+  const size_t B = (size_t)d.max_rhs;
+  for (int l = 0; l < h->L; ++l) {
+    for (auto* v : {&h->wy, &h->wx, &h->wr, &h->wb}) {
+      v->emplace_back(new DevBuf<float>());
+      const bool need = (v == &h->wy || v == &h->wx) || l < h->L - 1;
+      if (need) NMG_TRY(v->back()->alloc(B * (size_t)h->N[l]));
+    }
+  }
+  h->ntiles = gemm_f64_ntiles((int)h->N[0]);
+  NMG_TRY(h->part.alloc(B * h->ntiles));
+  NMG_TRY(h->ynorm.alloc(B));
+  NMG_TRY(h->relres.alloc(B));
+  NMG_TRY(h->active.alloc(B));
+  NMG_CUDA(cudaDeviceSynchronize());
+  *out = h.release();
+  return NMG_OK;
+}
+
+nmg_status nmg_load_smoother_weights(nmg_hierarchy* h, int32_t level, const nmg_cnn_arch* arch,
+                                     const float* params, size_t n_params) {
+  g_err.clear();
+  if (!h || !arch || !params) return fail(NMG_ERR_INVALID_ARG, "null argument");
+  if (level < 1 || level > h->L - 1) return fail(NMG_ERR_INVALID_ARG, "level %d outside 1..%d", level, h->L - 1);
+  const bool ok1 = h->d.dim == 1 && arch->n_layers == 3 && arch->channels == 16 && arch->ksize == 5;
+  const bool ok2 = h->d.dim == 2 && arch->n_layers == 4 && (arch->channels == 32 || arch->channels == 48) &&
+                   arch->ksize == 3;
+  if (!ok1 && !ok2)
+    return fail(NMG_ERR_UNSUPPORTED, "CNN arch (%d layers, %d ch, k %d) not supported for dim %d",
+                arch->n_layers, arch->channels, arch->ksize, h->d.dim);
+  const int C = arch->channels, k = arch->ksize, kk = h->d.dim == 1 ? k : k * k;
+  size_t want = 0;
+  int cin = 1;
+  for (int i = 0; i < arch->n_layers; ++i) {
+    const int cout = (i == arch->n_layers - 1) ? 1 : C;
+    want += (size_t)cout * cin * kk + cout;
+    cin = cout;
+  }
+  if (n_params != want) return fail(NMG_ERR_SHAPE, "expected %zu parameters, got %zu", want, n_params);
+  NMG_CUDA(cudaSetDevice(h->d.device));
+  NMG_TRY(h->W[level - 1]->upload(params, n_params));
+  h->w_loaded[level - 1] = 1;
+  h->arch = *arch;
+  return NMG_OK;
+}
+
+nmg_status nmg_residual(nmg_hierarchy* h, int32_t nrhs, const double* y, const double* x, double* r,
+                        double* relres, void* stream) {
+  g_err.clear();
+  if (!h || !y || !x) return fail(NMG_ERR_INVALID_ARG, "null argument");
+  if (nrhs < 0 || nrhs > h->d.max_rhs) return fail(NMG_ERR_INVALID_ARG, "bad nrhs");
+  NMG_CUDA(cudaSetDevice(h->d.device));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (nrhs == 0) return NMG_OK;
+  NMG_TRY(outer_residual(h, nrhs, y, x, r, relres != nullptr, s));
+  if (relres) {
+    row_norms_f64(nrhs, (int)h->N[0], y, h->N[0], h->ynorm.p, s);
+    relres_finalize(nrhs, h->ntiles, h->part.p, h->ynorm.p, relres, -1.0, nullptr, s);
+    h->launches += 2;
+  }
+  return check_launch(h);
+}
+
+nmg_status nmg_vcycle(nmg_hierarchy* h, int32_t nrhs, const double* y, double* x, void* stream) {
+  g_err.clear();
+  NMG_TRY(check_ready(h, nrhs));
+  if (!y || !x) return fail(NMG_ERR_INVALID_ARG, "null y/x");
+  if (nrhs == 0) return NMG_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  { Prof p(h, NMG_K_MISC, s); row_norms_f64(nrhs, (int)h->N[0], y, h->N[0], h->ynorm.p, s); }
+  return outer_step(h, nrhs, y, x, -1.0, false, s);
+}
+
+nmg_status nmg_solve(nmg_hierarchy* h, int32_t nrhs, const double* y, double* x, double tol, int32_t max_cycles,
+                     nmg_report* rep, void* stream) {
+  g_err.clear();
+  NMG_TRY(check_ready(h, nrhs));
+  if (!y || !x || max_cycles < 0) return fail(NMG_ERR_INVALID_ARG, "bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (rep) { rep->fail_cycle = -1; rep->fail_rhs = -1; rep->total_cycles = 0; rep->wall_seconds = 0; }
+  if (nrhs == 0) return NMG_OK;
+  const int64_t N = h->N[0];
+  std::vector<double> rr(nrhs);
+  std::vector<uint8_t> act(nrhs, 1);
+  std::vector<int32_t> cyc(nrhs, 0);
+  if (rep && rep->history)
+    for (size_t i = 0; i < (size_t)nrhs * (max_cycles + 1); ++i) rep->history[i] = NAN;
+  cudaEvent_t e0, e1;
+  NMG_CUDA(cudaEventCreate(&e0));
+  NMG_CUDA(cudaEventCreate(&e1));
+  NMG_CUDA(cudaEventRecord(e0, s));
+  row_norms_f64(nrhs, (int)N, y, N, h->ynorm.p, s);
+  NMG_TRY(outer_residual(h, nrhs, y, x, nullptr, true, s));
+  relres_finalize(nrhs, h->ntiles, h->part.p, h->ynorm.p, h->relres.p, tol, h->active.p, s);
+  h->launches += 2;
+  NMG_TRY(check_launch(h));
+  nmg_status st = NMG_OK;
+  int tau = 0;
+  for (;; ++tau) {
+    NMG_CUDA(cudaMemcpyAsync(rr.data(), h->relres.p, sizeof(double) * nrhs, cudaMemcpyDeviceToHost, s));
+    NMG_CUDA(cudaStreamSynchronize(s));
+    int nact = 0;
+    for (int b = 0; b < nrhs; ++b) {
+      if (!act[b]) continue;
+      if (!std::isfinite(rr[b])) {
+        if (rep) { rep->fail_cycle = tau; rep->fail_rhs = b; }
+        st = fail(NMG_ERR_NONFINITE, "non-finite residual at cycle %d, rhs %d", tau, b);
+        break;
+      }
+      if (rep && rep->history) rep->history[(size_t)b * (max_cycles + 1) + tau] = rr[b];
+      if (rr[b] <= tol) act[b] = 0; else ++nact;
+    }
+    if (st != NMG_OK || nact == 0 || tau == max_cycles) break;
+    NMG_TRY(inner_cycle(h, nrhs, s));
+    update_x(nrhs, (int)N, x, N, h->wx[0]->p, N, h->active.p, s);
+    h->launches++;
+    NMG_TRY(check_launch(h));
+    for (int b = 0; b < nrhs; ++b) if (act[b]) cyc[b] = tau + 1;
+    NMG_TRY(outer_residual(h, nrhs, y, x, nullptr, true, s));
+    relres_finalize(nrhs, h->ntiles, h->part.p, h->ynorm.p, h->relres.p, tol, h->active.p, s);
+    h->launches++;
+    NMG_TRY(check_launch(h));
+  }
+  NMG_CUDA(cudaEventRecord(e1, s));
+  NMG_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (rep) {
+    rep->wall_seconds = ms * 1e-3;
+    rep->total_cycles = tau;
+    for (int b = 0; b < nrhs; ++b) {
+      if (rep->cycles) rep->cycles[b] = cyc[b];
+      if (rep->converged) rep->converged[b] = act[b] ? 0 : 1;
+    }
+  }
+  return st;
+}
+
+nmg_status nmg_vcycles_host(nmg_hierarchy* h, int32_t nrhs, const double* y_host, double* x_host, int32_t cycles,
+                            double* relres_host, void* stream) {
+  g_err.clear();
+  NMG_TRY(check_ready(h, nrhs));
+  if (!y_host || !x_host || cycles < 0) return fail(NMG_ERR_INVALID_ARG, "bad arguments");
+  if (nrhs == 0) return NMG_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t cnt = (size_t)h->d.max_rhs * h->N[0];
+  if (!h->hy.p) { NMG_TRY(h->hy.alloc(cnt)); NMG_TRY(h->hx.alloc(cnt)); }
+  const size_t bytes = sizeof(double) * (size_t)nrhs * h->N[0];
+  NMG_CUDA(cudaMemcpyAsync(h->hy.p, y_host, bytes, cudaMemcpyHostToDevice, s));
+  NMG_CUDA(cudaMemcpyAsync(h->hx.p, x_host, bytes, cudaMemcpyHostToDevice, s));
+  row_norms_f64(nrhs, (int)h->N[0], h->hy.p, h->N[0], h->ynorm.p, s);
+  h->launches++;
+  for (int c = 0; c < cycles; ++c) NMG_TRY(outer_step(h, nrhs, h->hy.p, h->hx.p, -1.0, false, s));
+  if (relres_host)
+    NMG_CUDA(cudaMemcpyAsync(relres_host, h->relres.p, sizeof(double) * nrhs, cudaMemcpyDeviceToHost, s));
+  NMG_CUDA(cudaMemcpyAsync(x_host, h->hx.p, bytes, cudaMemcpyDeviceToHost, s));
+  NMG_CUDA(cudaStreamSynchronize(s));
+  return NMG_OK;
+}
+
+nmg_status nmg_debug_level_op(nmg_hierarchy* h, int32_t level, int32_t op, int32_t nrhs, const void* in, void* out,
+                              void* stream) {
+  g_err.clear();
+  if (!h || !in || !out) return fail(NMG_ERR_INVALID_ARG, "null argument");
+  if (level < 1 || level > h->L) return fail(NMG_ERR_INVALID_ARG, "level %d outside 1..%d", level, h->L);
+  if (nrhs < 0 || nrhs > h->d.max_rhs) return fail(NMG_ERR_INVALID_ARG, "bad nrhs");
+  NMG_CUDA(cudaSetDevice(h->d.device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int l = level - 1;
+  const float* fin = (const float*)in;
+  float* fout = (float*)out;
+  if (h->d.dim != 1) return fail(NMG_ERR_UNSUPPORTED, "2D debug ops not implemented yet");
+  const int n = h->n[l];
+  const bool smoothed = l < h->L - 1;
+  switch (op) {
+    case NMG_OP_APPLY:
+    case NMG_OP_RESIDUAL: {
+      if (!smoothed) return fail(NMG_ERR_INVALID_ARG, "no fp32 operator stored at the coarsest level");
+      Gemm32Args g{};
+      g.M = nrhs; g.N = n; g.K = n; g.batch = 1;
+      g.X = fin; g.ldx = n; g.W = h->A32[l]->p; g.ldw = n; g.w_kmajor = true;
+      g.C = op == NMG_OP_RESIDUAL ? fout : nullptr; g.ldc = n;
+      g.D = fout; g.ldd = n;
+      g.negate = op == NMG_OP_RESIDUAL;
+      gemm_f32(g, s);
+      break;
+    }
+    case NMG_OP_RESTRICT:
+      if (!smoothed) return fail(NMG_ERR_INVALID_ARG, "no coarser level");
+      restrict1d(nrhs, n, fin, n, fout, n / 2, s);
+      break;
+    case NMG_OP_PROLONG:
+      if (!smoothed) return fail(NMG_ERR_INVALID_ARG, "no coarser level");
+      prolong_add1d(nrhs, n / 2, fin, n / 2, fout, n, s);
+      break;
+    case NMG_OP_FILTER:
+      filter1d(n, nrhs, fin, fout, h->tw.p, h->tw_n, s);
+      break;
+    case NMG_OP_CNN:
+    case NMG_OP_SMOOTH: {
+      if (!smoothed || !h->w_loaded[l]) return fail(NMG_ERR_NO_WEIGHTS, "no smoother at level %d", level);
+      Smooth1dArgs a{};
+      a.n = n; a.nrhs = nrhs; a.b = fin; a.ldb = n; a.x = fout; a.ldx = n;
+      a.params = h->W[l]->p; a.twiddle = h->tw.p; a.tw_n = h->tw_n;
+      a.normalize = op == NMG_OP_SMOOTH;
+      a.filter = op == NMG_OP_SMOOTH && h->d.level_filter != 0;
+      a.accumulate = op == NMG_OP_SMOOTH;
+      smooth1d(a, s);
+      break;
+    }
+    case NMG_OP_COARSE:
+      if (smoothed) return fail(NMG_ERR_INVALID_ARG, "COARSE needs level == L");
+      coarse_chol_solve(h->nc, nrhs, h->Lrow.p, h->Lcol.p, fin, n, fout, n, s);
+      break;
+    case NMG_OP_CYCLE0: {
+      for (int q = l; q < h->L - 1; ++q)
+        if (!h->w_loaded[q]) return fail(NMG_ERR_NO_WEIGHTS, "level %d has no smoother", q + 1);
+      NMG_CUDA(cudaMemcpyAsync(h->wy[l]->p, fin, sizeof(float) * (size_t)nrhs * n, cudaMemcpyDeviceToDevice, s));
+      NMG_TRY(cycle_level_1d(h, l, nrhs, s));
+      NMG_CUDA(cudaMemcpyAsync(fout, h->wx[l]->p, sizeof(float) * (size_t)nrhs * n, cudaMemcpyDeviceToDevice, s));
+      break;
+    }
+    default:
+      return fail(NMG_ERR_INVALID_ARG, "unknown op %d", op);
+  }
+  h->launches++;
+  return check_launch(h);
+}
+
+nmg_status nmg_profile(nmg_hierarchy* h, int32_t enable) {
+  if (!h) return fail(NMG_ERR_INVALID_ARG, "null handle");
+  if (enable) { h->recs.clear(); h->ev_used = 0; }
+  h->prof_on = enable != 0;
+  return NMG_OK;
+}
+
+nmg_status nmg_profile_query(nmg_hierarchy* h, int32_t kclass, double* total_ms, int64_t* launches) {
+  if (!h || !total_ms || !launches) return fail(NMG_ERR_INVALID_ARG, "null argument");
+  double tot = 0.0;
+  int64_t cnt = 0;
+  for (auto& r : h->recs) {
+    if (r.cls != kclass) continue;
+    NMG_CUDA(cudaEventSynchronize(r.b));
+    float ms = 0.f;
+    NMG_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+    tot += ms;
+    ++cnt;
+  }
+  *total_ms = tot;
+  *launches = cnt;
+  return NMG_OK;
+}
+
+void nmg_destroy_hierarchy(nmg_hierarchy* h) {
+  if (!h) return;
+  cudaSetDevice(h->d.device);
+  cudaDeviceSynchronize();
+  delete h;
+}
+
+}  // extern "C"

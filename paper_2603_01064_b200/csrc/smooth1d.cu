@@ -1,0 +1,199 @@
+// Fused 1D neural smoothing step, one CTA per right-hand side (Alg 3):
+//   s = ||b||_2 (fp64, deterministic tree)                       P:328 (reading R10)
+//   h = s * N_theta(b / s)   CNN 1->16->16->1, k = 5, ReLU       reading R7
+//   x = x* + F'_l(h)          F'_l = Re(IDFT(m'_l (.) DFT(.)))    P:305, P:329 (reading R5)
+// All three layers run on-chip per 252-point tile (6-point halo recompute); the
+// filtered update is done on the whole row held in shared memory.
+#include "common.cuh"
+#include "fft.cuh"
+#include "kernels.h"
+
+namespace nmg {
+namespace {
+
+constexpr int C = 16, KS = 5, HALO = KS / 2;      // per-layer halo 2, 3 layers -> 6
+constexpr int NT = 256;
+constexpr int T3 = 252;                           // outputs per tile
+constexpr int W2 = T3 + 2 * HALO;                 // 256 layer-2 positions = 16 groups x 16
+constexpr int W1 = W2 + 2 * HALO;                 // 260 layer-1 positions
+constexpr int S1 = W1 + 1;                        // odd smem strides
+constexpr int S2 = W2 + 1;
+constexpr int PP = 16;                            // layer-2 positions per thread
+constexpr int NPARAM = C * 1 * KS + C + C * C * KS + C + 1 * C * KS + 1;   // 1473
+constexpr int UPAD = 3 * HALO;                    // 6
+
+__global__ void __launch_bounds__(NT, 2) smooth1d_kernel(Smooth1dArgs a) {
+  extern __shared__ __align__(16) float sm[];
+  const int n = a.n, tid = threadIdx.x;
+  const int rhs = blockIdx.x;
+  float* w = sm;                                  // NPARAM (padded to 1480)
+  float* u = w + 1480;                            // n + 2*UPAD
+  float2* cb = reinterpret_cast<float2*>(u + ((n + 2 * UPAD + 3) & ~3));   // n complex
+  float* a1 = reinterpret_cast<float*>(cb + n);   // C x S1
+  float* a2 = a1 + C * S1;                        // C x S2
+  __shared__ double red[32];
+
+  const float* w0 = w;                 // [16][1][5]
+  const float* b0 = w0 + C * KS;       // [16]
+  const float* w1 = b0 + C;            // [16][16][5]
+  const float* b1 = w1 + C * C * KS;   // [16]
+  const float* w2 = b1 + C;            // [1][16][5]
+  const float* b2 = w2 + C * KS;       // [1]
+
+  for (int i = tid; i < NPARAM; i += NT) w[i] = __ldg(a.params + i);
+  const float* brow = a.b + (int64_t)rhs * a.ldb;
+  double ss = 0.0;
+  for (int j = tid; j < n; j += NT) {
+    const float v = brow[j];
+    u[UPAD + j] = v;
+    ss += (double)v * (double)v;
+  }
+  if (tid < UPAD) { u[tid] = 0.f; u[UPAD + n + tid] = 0.f; }
+  double s = 1.0;
+  if (a.normalize) {
+    s = sqrt(block_sum_f64(ss, red));
+    if (s == 0.0) {                               // ||b|| = 0 => h = 0 (reading R10)
+      if (!a.accumulate) {
+        float* xrow = a.x + (int64_t)rhs * a.ldx;
+        for (int j = tid; j < n; j += NT) xrow[j] = 0.f;
+      }
+      return;
+    }
+  }
+  __syncthreads();
+  if (a.normalize) {
+    for (int j = tid; j < n; j += NT) u[UPAD + j] = (float)((double)u[UPAD + j] / s);
+  }
+  const float sf = (float)s;
+  const int log2n = 31 - __clz(n);
+
+  // layer-2 thread role: output channel o, position group pg
+  const int o = tid & (C - 1), pg = tid >> 4;
+  float wr[C * KS];
+#pragma unroll
+  for (int i = 0; i < C * KS; ++i) wr[i] = 0.f;
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < C * KS; ++i) wr[i] = w1[o * C * KS + i];
+  const float bo = b1[o];
+
+  for (int t0 = 0; t0 < n; t0 += T3) {
+    // ---- layer 1: a1[c][jj], position p = t0 - 4 + jj, zero outside [0, n)
+    for (int idx = tid; idx < C * W1; idx += NT) {
+      const int c = idx / W1, jj = idx - c * W1;
+      const int p = t0 - 2 * HALO + jj;
+      float v = 0.f;
+      if (p >= 0 && p < n) {
+        float acc = b0[c];
+#pragma unroll
+        for (int t = 0; t < KS; ++t) acc = fmaf(w0[c * KS + t], u[UPAD + p + t - HALO], acc);
+        v = fmaxf(acc, 0.f);
+      }
+      a1[c * S1 + jj] = v;
+    }
+    __syncthreads();
+    // ---- layer 2: a2[o][jj2], position p = t0 - 2 + jj2
+    {
+      float acc[PP];
+#pragma unroll
+      for (int i = 0; i < PP; ++i) acc[i] = bo;
+      const int base = pg * PP;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        float win[PP + KS - 1];
+        const float* src = a1 + c * S1 + base;
+#pragma unroll
+        for (int i = 0; i < PP + KS - 1; ++i) win[i] = src[i];
+#pragma unroll
+        for (int t = 0; t < KS; ++t) {
+          const float wv = wr[c * KS + t];
+#pragma unroll
+          for (int i = 0; i < PP; ++i) acc[i] = fmaf(wv, win[i + t], acc[i]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < PP; ++i) {
+        const int p = t0 - HALO + base + i;
+        a2[o * S2 + base + i] = (p >= 0 && p < n) ? fmaxf(acc[i], 0.f) : 0.f;
+      }
+    }
+    __syncthreads();
+    // ---- layer 3: h[p], p = t0 + jj3
+    if (tid < T3) {
+      const int p = t0 + tid;
+      if (p < n) {
+        float acc = b2[0];
+#pragma unroll 4
+        for (int c = 0; c < C; ++c) {
+#pragma unroll
+          for (int t = 0; t < KS; ++t) acc = fmaf(w2[c * KS + t], a2[c * S2 + tid + t], acc);
+        }
+        const float hv = acc * sf;
+        if (a.filter) {
+          cb[bitrev(p, log2n)] = make_float2(hv, 0.f);
+        } else {
+          float* xrow = a.x + (int64_t)rhs * a.ldx;
+          xrow[p] = a.accumulate ? xrow[p] + hv : hv;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (!a.filter) return;
+
+  // ---- level filter F'_l on the whole row
+  fft_dit_forward(cb, n, a.twiddle, a.tw_n, tid, NT);
+  for (int k = tid; k < n; k += NT) {
+    const float m = level_mask_1d(k, n);
+    const float2 v = cb[k];
+    cb[k] = make_float2(v.x * m, v.y * m);
+  }
+  __syncthreads();
+  fft_dif_inverse(cb, n, a.twiddle, a.tw_n, tid, NT);
+  const float inv_n = 1.0f / (float)n;
+  float* xrow = a.x + (int64_t)rhs * a.ldx;
+  for (int j = tid; j < n; j += NT) {
+    const float v = cb[bitrev(j, log2n)].x * inv_n;
+    xrow[j] = a.accumulate ? xrow[j] + v : v;
+  }
+}
+
+// Filter only (debug op NMG_OP_FILTER): out = F'(in).
+__global__ void __launch_bounds__(NT) filter1d_kernel(int n, const float* in, float* out,
+                                                      const float2* tw, int tw_n) {
+  extern __shared__ __align__(16) float sm[];
+  float2* cb = reinterpret_cast<float2*>(sm);
+  const int rhs = blockIdx.x, tid = threadIdx.x;
+  const int log2n = 31 - __clz(n);
+  for (int j = tid; j < n; j += NT) cb[bitrev(j, log2n)] = make_float2(in[(int64_t)rhs * n + j], 0.f);
+  __syncthreads();
+  fft_dit_forward(cb, n, tw, tw_n, tid, NT);
+  for (int k = tid; k < n; k += NT) {
+    const float m = level_mask_1d(k, n);
+    cb[k] = make_float2(cb[k].x * m, cb[k].y * m);
+  }
+  __syncthreads();
+  fft_dif_inverse(cb, n, tw, tw_n, tid, NT);
+  for (int j = tid; j < n; j += NT) out[(int64_t)rhs * n + j] = cb[bitrev(j, log2n)].x / (float)n;
+}
+
+}  // namespace
+
+size_t smooth1d_smem(int n) {
+  size_t f = 1480 + ((n + 2 * UPAD + 3) & ~3) + 2 * (size_t)n + C * S1 + C * S2;
+  return f * sizeof(float);
+}
+
+void smooth1d(const Smooth1dArgs& a, cudaStream_t s) {
+  const size_t smem = smooth1d_smem(a.n);
+  cudaFuncSetAttribute(smooth1d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  smooth1d_kernel<<<a.nrhs, NT, smem, s>>>(a);
+}
+
+void filter1d(int n, int nrhs, const float* in, float* out, const float2* tw, int tw_n, cudaStream_t s) {
+  const size_t smem = 2 * (size_t)n * sizeof(float);
+  cudaFuncSetAttribute(filter1d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  filter1d_kernel<<<nrhs, NT, smem, s>>>(n, in, out, tw, tw_n);
+}
+
+}  // namespace nmg
