@@ -118,7 +118,8 @@ __global__ void relres_kernel(int nrhs, int ntiles, const double* __restrict__ p
   double s = 0.0;
   for (int t = 0; t < ntiles; ++t) s += part[(int64_t)b * ntiles + t];
   const double yn = ynorm[b];
-  const double rr = (yn > 0.0) ? sqrt(s) / yn : 0.0;   // y = 0: converged at x = 0
+  // y = 0: converged at x = 0; a non-finite ||y|| or residual propagates as NaN/Inf
+  const double rr = (yn > 0.0) ? sqrt(s) / yn : (yn == 0.0 && s == 0.0 ? 0.0 : sqrt(s) / yn);
   relres[b] = rr;
   if (active) active[b] = (rr > tol || rr != rr) ? 1 : 0;
 }

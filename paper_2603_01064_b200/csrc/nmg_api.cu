@@ -486,11 +486,12 @@ nmg_status nmg_load_smoother_weights(nmg_hierarchy* h, int32_t level, const nmg_
 nmg_status nmg_residual(nmg_hierarchy* h, int32_t nrhs, const double* y, const double* x, double* r,
                         double* relres, void* stream) {
   g_err.clear();
-  if (!h || !y || !x) return fail(NMG_ERR_INVALID_ARG, "null argument");
+  if (!h) return fail(NMG_ERR_INVALID_ARG, "null handle");
   if (nrhs < 0 || nrhs > h->d.max_rhs) return fail(NMG_ERR_INVALID_ARG, "bad nrhs");
+  if (nrhs == 0) return NMG_OK;
+  if (!y || !x) return fail(NMG_ERR_INVALID_ARG, "null argument");
   NMG_CUDA(cudaSetDevice(h->d.device));
   cudaStream_t s = (cudaStream_t)stream;
-  if (nrhs == 0) return NMG_OK;
   NMG_TRY(outer_residual(h, nrhs, y, x, r, relres != nullptr, s));
   if (relres) {
     row_norms_f64(nrhs, (int)h->N[0], y, h->N[0], h->ynorm.p, s);
@@ -503,8 +504,8 @@ nmg_status nmg_residual(nmg_hierarchy* h, int32_t nrhs, const double* y, const d
 nmg_status nmg_vcycle(nmg_hierarchy* h, int32_t nrhs, const double* y, double* x, void* stream) {
   g_err.clear();
   NMG_TRY(check_ready(h, nrhs));
-  if (!y || !x) return fail(NMG_ERR_INVALID_ARG, "null y/x");
   if (nrhs == 0) return NMG_OK;
+  if (!y || !x) return fail(NMG_ERR_INVALID_ARG, "null y/x");
   cudaStream_t s = (cudaStream_t)stream;
   { Prof p(h, NMG_K_MISC, s); row_norms_f64(nrhs, (int)h->N[0], y, h->N[0], h->ynorm.p, s); }
   return outer_step(h, nrhs, y, x, -1.0, false, s);
@@ -514,10 +515,10 @@ nmg_status nmg_solve(nmg_hierarchy* h, int32_t nrhs, const double* y, double* x,
                      nmg_report* rep, void* stream) {
   g_err.clear();
   NMG_TRY(check_ready(h, nrhs));
-  if (!y || !x || max_cycles < 0) return fail(NMG_ERR_INVALID_ARG, "bad arguments");
   cudaStream_t s = (cudaStream_t)stream;
   if (rep) { rep->fail_cycle = -1; rep->fail_rhs = -1; rep->total_cycles = 0; rep->wall_seconds = 0; }
   if (nrhs == 0) return NMG_OK;
+  if (!y || !x || max_cycles < 0) return fail(NMG_ERR_INVALID_ARG, "bad arguments");
   const int64_t N = h->N[0];
   std::vector<double> rr(nrhs);
   std::vector<uint8_t> act(nrhs, 1);
@@ -581,8 +582,8 @@ nmg_status nmg_vcycles_host(nmg_hierarchy* h, int32_t nrhs, const double* y_host
                             double* relres_host, void* stream) {
   g_err.clear();
   NMG_TRY(check_ready(h, nrhs));
-  if (!y_host || !x_host || cycles < 0) return fail(NMG_ERR_INVALID_ARG, "bad arguments");
   if (nrhs == 0) return NMG_OK;
+  if (!y_host || !x_host || cycles < 0) return fail(NMG_ERR_INVALID_ARG, "bad arguments");
   cudaStream_t s = (cudaStream_t)stream;
   const size_t cnt = (size_t)h->d.max_rhs * h->N[0];
   if (!h->hy.p) { NMG_TRY(h->hy.alloc(cnt)); NMG_TRY(h->hx.alloc(cnt)); }
@@ -602,9 +603,11 @@ nmg_status nmg_vcycles_host(nmg_hierarchy* h, int32_t nrhs, const double* y_host
 nmg_status nmg_debug_level_op(nmg_hierarchy* h, int32_t level, int32_t op, int32_t nrhs, const void* in, void* out,
                               void* stream) {
   g_err.clear();
-  if (!h || !in || !out) return fail(NMG_ERR_INVALID_ARG, "null argument");
+  if (!h) return fail(NMG_ERR_INVALID_ARG, "null handle");
   if (level < 1 || level > h->L) return fail(NMG_ERR_INVALID_ARG, "level %d outside 1..%d", level, h->L);
   if (nrhs < 0 || nrhs > h->d.max_rhs) return fail(NMG_ERR_INVALID_ARG, "bad nrhs");
+  if (nrhs == 0) return NMG_OK;
+  if (!in || !out) return fail(NMG_ERR_INVALID_ARG, "null argument");
   NMG_CUDA(cudaSetDevice(h->d.device));
   cudaStream_t s = (cudaStream_t)stream;
   const int l = level - 1;

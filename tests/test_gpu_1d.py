@@ -33,7 +33,7 @@ def T(a, dtype=torch.float32):
 def cfg0():
     f = ni.operator_factors(CFG0)
     W = weights_for(CFG0, "seed")
-    return f, W, oracle_hierarchy(CFG0, f, W), gpu_hierarchy(CFG0, f, W, max_rhs=64)
+    return f, W, oracle_hierarchy(CFG0, f, W), gpu_hierarchy(CFG0, f, W, max_rhs=256)
 
 
 @pytest.fixture(scope="module")
