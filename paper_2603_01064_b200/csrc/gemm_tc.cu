@@ -1,0 +1,252 @@
+// fp32-accurate operator apply on the 5th-gen tensor cores (tcgen05, kind::tf32):
+//   D = C - X W^T   with  X = Xh + Xl,  W = Wh + Wl  (tf32 hi/lo splits, "3xTF32")
+//   X W^T ~= Xh Wh^T + Xh Wl^T + Xl Wh^T, all three accumulated in one TMEM tile.
+// This is the inner-cycle residual r_l = y_l - A^(l) x_l (Alg 3, Alg 1
+// P:158) and the post-smoothing residual b = r_l - (A^(l) I_{l+1}^l) e.
+//
+// Kernel anatomy (one 128 x 256 output tile per CTA, 128 threads):
+//   warp 0 / lane 0 : TMA producer (cp.async.bulk.tensor, SWIZZLE_64B, 4-stage ring)
+//   warp 1 / lane 0 : MMA issuer (tcgen05.mma.cta_group::1.kind::tf32, M=128 N=256 K=8)
+//   warp 2          : TMEM allocator (256 fp32 columns)
+//   all 4 warps     : epilogue (tcgen05.ld 32x32b.x32 -> registers -> C - acc -> global)
+#include <cuda.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace nmg {
+namespace {
+
+constexpr int TBM = 128, TBN = 256, TBK = 16, TSTAGES = 4, TNT = 128;
+constexpr int A_BYTES = TBM * TBK * 4;                    // 8 KB
+constexpr int B_BYTES = TBN * TBK * 4;                    // 16 KB
+constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;    // 48 KB
+constexpr int TC_SMEM = TSTAGES * STAGE_BYTES + 1024 /*barriers*/ + 1024 /*align slack*/;
+
+NMG_D uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+NMG_D void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+NMG_D void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes));
+}
+NMG_D void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(a),
+      "r"(parity));
+}
+NMG_D void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+NMG_D void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(map) : "memory");
+}
+
+// UMMA shared-memory descriptor, K-major, SWIZZLE_64B: rows of 64 bytes, 8-row core
+// groups 512 bytes apart (SBO), LBO unused (1), version 1 (sm_100), layout type 4.
+NMG_D uint64_t umma_desc_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                  // LBO (ignored for swizzled K-major)
+  d |= (uint64_t)(512 >> 4) << 32;         // SBO
+  d |= (uint64_t)1 << 46;                  // version
+  d |= (uint64_t)4 << 61;                  // SWIZZLE_64B
+  return d;
+}
+
+// Instruction descriptor: D f32, A/B tf32, both K-major, N = 256, M = 128.
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TBN >> 3) << 17) |
+                            ((uint32_t)(TBM >> 4) << 24);
+
+NMG_D void umma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(kIdesc), "r"(accumulate));
+}
+NMG_D void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__global__ void __launch_bounds__(TNT, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tXh, const __grid_constant__ CUtensorMap tXl,
+                   const __grid_constant__ CUtensorMap tWh, const __grid_constant__ CUtensorMap tWl,
+                   TcGemmArgs a) {
+  extern __shared__ uint8_t smraw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + TSTAGES * STAGE_BYTES);
+  uint64_t* empty = full + TSTAGES;
+  uint64_t* done = empty + TSTAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m0 = blockIdx.y * TBM, n0 = blockIdx.x * TBN;
+  const int KT = ceil_div(a.K, TBK);
+
+  if (tid == 0) {
+    for (int s = 0; s < TSTAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    prefetch_tmap(&tXh); prefetch_tmap(&tXl); prefetch_tmap(&tWh); prefetch_tmap(&tWl);
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TBN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {   // ---------------- TMA producer
+      for (int kt = 0; kt < KT; ++kt) {
+        const int s = kt % TSTAGES;
+        const uint32_t ph = (uint32_t)(kt / TSTAGES) & 1u;
+        mbar_wait(&empty[s], ph ^ 1u);
+        uint8_t* st = sm + s * STAGE_BYTES;
+        mbar_expect_tx(&full[s], STAGE_BYTES);
+        const int k0 = kt * TBK;
+        tma_load_2d(st, &tXh, &full[s], k0, m0);
+        tma_load_2d(st + A_BYTES, &tXl, &full[s], k0, m0);
+        tma_load_2d(st + 2 * A_BYTES, &tWh, &full[s], k0, n0);
+        tma_load_2d(st + 2 * A_BYTES + B_BYTES, &tWl, &full[s], k0, n0);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {   // ---------------- MMA issuer
+      for (int kt = 0; kt < KT; ++kt) {
+        const int s = kt % TSTAGES;
+        const uint32_t ph = (uint32_t)(kt / TSTAGES) & 1u;
+        mbar_wait(&full[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t st = smem_u32(sm + s * STAGE_BYTES);
+#pragma unroll
+        for (int ks = 0; ks < TBK / 8; ++ks) {
+          const uint32_t ko = ks * 32;   // 8 tf32 = 32 bytes along the 64-byte swizzled row
+          const uint64_t dxh = umma_desc_sw64(st + ko);
+          const uint64_t dxl = umma_desc_sw64(st + A_BYTES + ko);
+          const uint64_t dwh = umma_desc_sw64(st + 2 * A_BYTES + ko);
+          const uint64_t dwl = umma_desc_sw64(st + 2 * A_BYTES + B_BYTES + ko);
+          umma_tf32(tmem, dxh, dwh, (kt | ks) ? 1u : 0u);
+          umma_tf32(tmem, dxh, dwl, 1u);
+          umma_tf32(tmem, dxl, dwh, 1u);
+        }
+        umma_commit(&empty[s]);      // slot reusable when these MMAs retire
+      }
+      umma_commit(done);             // accumulator complete
+    }
+    __syncwarp();
+  }
+
+  // ---------------- epilogue: all 4 warps, warp w owns TMEM lanes 32w..32w+31 (rows)
+  mbar_wait(done, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const int row = warp * 32 + lane;
+  const int m = m0 + row;
+  const bool mok = m < a.M;
+  const float* crow = a.C ? a.C + (int64_t)m * a.ldc : nullptr;
+  float* drow = a.D + (int64_t)m * a.ldd;
+#pragma unroll 1
+  for (int c = 0; c < TBN / 32; ++c) {
+    uint32_t v[32];
+    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c * 32);
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+    const int nb = n0 + c * 32;
+    if (mok) {
+      if (nb + 32 <= a.N) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          float4 o;
+          float acc[4] = {__uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
+                          __uint_as_float(v[j + 3])};
+          if (a.negate) { acc[0] = -acc[0]; acc[1] = -acc[1]; acc[2] = -acc[2]; acc[3] = -acc[3]; }
+          if (crow) {
+            const float4 cv = *reinterpret_cast<const float4*>(crow + nb + j);
+            o = make_float4(cv.x + acc[0], cv.y + acc[1], cv.z + acc[2], cv.w + acc[3]);
+          } else {
+            o = make_float4(acc[0], acc[1], acc[2], acc[3]);
+          }
+          *reinterpret_cast<float4*>(drow + nb + j) = o;
+        }
+      } else {
+        for (int j = 0; j < 32 && nb + j < a.N; ++j) {
+          float acc = __uint_as_float(v[j]);
+          if (a.negate) acc = -acc;
+          drow[nb + j] = crow ? crow[nb + j] + acc : acc;
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TBN));
+  }
+}
+
+// ---- tf32 hi/lo split: hi = cvt.rna.tf32(x), lo = cvt.rna.tf32(x - hi) -------------
+__global__ void split_tf32_kernel(int64_t count, const float* __restrict__ x, float* __restrict__ hi,
+                                  float* __restrict__ lo) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const float v = x[i];
+  uint32_t h;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(h) : "f"(v));
+  const float hf = __uint_as_float(h);
+  uint32_t l;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(l) : "f"(v - hf));
+  hi[i] = hf;
+  lo[i] = __uint_as_float(l);
+}
+
+}  // namespace
+
+int tc_gemm_smem_bytes() { return TC_SMEM; }
+int tc_gemm_block_n() { return TBN; }
+int tc_gemm_block_m() { return TBM; }
+
+void tc_gemm(const CUtensorMap* xh, const CUtensorMap* xl, const CUtensorMap* wh, const CUtensorMap* wl,
+             const TcGemmArgs& a, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+    attr = true;
+  }
+  dim3 grid(ceil_div(a.N, TBN), ceil_div(a.M, TBM));
+  tc_gemm_kernel<<<grid, TNT, TC_SMEM, s>>>(*xh, *xl, *wh, *wl, a);
+}
+
+void split_tf32(int64_t count, const float* x, float* hi, float* lo, cudaStream_t s) {
+  split_tf32_kernel<<<(int)ceil_div64(count, 256), 256, 0, s>>>(count, x, hi, lo);
+}
+
+}  // namespace nmg

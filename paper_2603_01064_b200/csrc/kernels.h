@@ -1,5 +1,6 @@
 // Host-side launchers of the nmg device kernels (all enqueue on `s`).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -35,6 +36,21 @@ struct Gemm64Args {
 };
 int gemm_f64_ntiles(int N);
 void gemm_f64(const Gemm64Args& a, cudaStream_t s);
+
+// tcgen05 3xTF32 GEMM: D = C -/+ X W^T with X = Xh + Xl ([M][K], tensor maps with box
+// {16, 128}) and W = Wh + Wl ([N][K], box {16, 256}), SWIZZLE_64B, fp32 row-major C/D.
+struct TcGemmArgs {
+  int M, N, K;
+  const float* C; int64_t ldc;           // may be null
+  float* D; int64_t ldd;
+  bool negate;
+};
+void tc_gemm(const CUtensorMap* xh, const CUtensorMap* xl, const CUtensorMap* wh, const CUtensorMap* wl,
+             const TcGemmArgs& a, cudaStream_t s);
+int tc_gemm_smem_bytes();
+int tc_gemm_block_n();
+int tc_gemm_block_m();
+void split_tf32(int64_t count, const float* x, float* hi, float* lo, cudaStream_t s);
 
 // ---- 1D smoother: norm -> CNN (3 layers, C=16, k=5) -> F' -> update ----------
 struct Smooth1dArgs {

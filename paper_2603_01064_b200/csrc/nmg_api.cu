@@ -12,9 +12,12 @@
 //   * correction form x + NMGF(0, y - A x) with an fp64 outer residual (pin P11);
 //   * the post-smoothing residual is b = r_l - (A_l P_l) e  (A_l P_l precomputed),
 //     which equals y_l - A_l (x_l + P_l e) exactly and halves that GEMM.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -137,7 +140,52 @@ std::vector<float> to_f32(const std::vector<double>& v) {
   return o;
 }
 
-int ilog2(int v) { int l = 0; while ((1 << l) < v) ++l; return l; }
+// Host emulation of cvt.rna.tf32.f32 (round to nearest, ties away from zero).
+float tf32_rna(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  if ((u & 0x7F800000u) != 0x7F800000u) { u += 0x1000u; u &= 0xFFFFE000u; }
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
+}
+void split_host(const std::vector<double>& v, std::vector<float>& hi, std::vector<float>& lo) {
+  hi.resize(v.size());
+  lo.resize(v.size());
+  for (size_t i = 0; i < v.size(); ++i) {
+    const float f = (float)v[i];
+    hi[i] = tf32_rna(f);
+    lo[i] = tf32_rna(f - hi[i]);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+nmg_status get_encoder() {
+  if (g_encode) return NMG_OK;
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
+    return fail(NMG_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return NMG_OK;
+}
+
+// 2D fp32 row-major [rows][cols] tensor map, box {16, box_rows}, SWIZZLE_64B.
+nmg_status make_map(CUtensorMap* m, const float* p, int64_t rows, int64_t cols, int box_rows) {
+  NMG_TRY(get_encoder());
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * sizeof(float)};
+  cuuint32_t box[2] = {16u, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1u, 1u};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)p, dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(NMG_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) rows=%lld cols=%lld", (int)r,
+                                     (long long)rows, (long long)cols);
+  return NMG_OK;
+}
 
 }  // namespace
 
@@ -149,8 +197,12 @@ struct nmg_hierarchy {
   std::vector<int64_t> N;  // unknowns per level
   // level-1 fp64 operator (1D: A; 2D: B, C)
   DevBuf<double> A64, B64, C64;
-  // per smoothed level (l < L-1) fp32 operators
-  std::vector<std::unique_ptr<DevBuf<float>>> A32, AP32;
+  // per smoothed level (l < L-1) fp32 operators (SIMT path) and tf32 hi/lo splits (tcgen05)
+  std::vector<std::unique_ptr<DevBuf<float>>> A32, AP32, A32h, A32l, AP32h, AP32l;
+  std::vector<CUtensorMap> mAh, mAl, mAPh, mAPl;        // W operand maps per level
+  std::vector<std::unique_ptr<DevBuf<float>>> sxh, sxl;  // X splits per level [max_rhs][n_l]
+  std::vector<CUtensorMap> mXh, mXl;
+  bool use_tc = true;
   // coarse Cholesky factor (row-major L and L^T)
   DevBuf<double> Lrow, Lcol;
   int nc = 0;
@@ -231,15 +283,39 @@ nmg_status smooth_level(nmg_hierarchy* h, int l, int nrhs, const float* b, float
 
 // D = C - X * W^T-ish  (W: [N][K] K-major), fp32
 nmg_status resid_gemm(nmg_hierarchy* h, int M, int N, int K, const float* X, const float* W, const float* C,
-                      float* D, cudaStream_t s) {
+                      float* D, cudaStream_t s, bool negate = true) {
   Gemm32Args g{};
   g.M = M; g.N = N; g.K = K; g.batch = 1;
   g.X = X; g.ldx = K; g.sx = 0;
   g.W = W; g.ldw = K; g.sw = 0; g.w_kmajor = true;
   g.C = C; g.ldc = N; g.sc = 0;
   g.D = D; g.ldd = N; g.sd = 0;
-  g.negate = true;
+  g.negate = negate;
   { Prof p(h, NMG_K_GEMM32, s); gemm_f32(g, s); }
+  return check_launch(h);
+}
+
+// D = C - A_l X   (which = 0: W = A_l, K = n_l;  which = 1: W = A_l P_l, K = n_l / 2)
+// X lives in wx[lx] (lx = l for A_l, l + 1 for A_l P_l).  tcgen05 3xTF32 when the
+// shape allows, else the SIMT kernel.
+nmg_status level_resid(nmg_hierarchy* h, int l, int which, int nrhs, const float* C, float* D, cudaStream_t s,
+                       bool negate = true) {
+  const int n = h->n[l];
+  const int K = which == 0 ? n : n / 2;
+  const int lx = which == 0 ? l : l + 1;
+  const float* X = h->wx[lx]->p;
+  const bool tc = h->use_tc && n % 16 == 0 && K % 16 == 0 && K >= 16;
+  if (!tc) return resid_gemm(h, nrhs, n, K, X, which == 0 ? h->A32[l]->p : h->AP32[l]->p, C, D, s, negate);
+  { Prof p(h, NMG_K_MISC, s); split_tf32((int64_t)nrhs * K, X, h->sxh[lx]->p, h->sxl[lx]->p, s); }
+  NMG_TRY(check_launch(h));
+  TcGemmArgs g{};
+  g.M = nrhs; g.N = n; g.K = K;
+  g.C = C; g.ldc = n; g.D = D; g.ldd = n; g.negate = negate;
+  {
+    Prof p(h, NMG_K_GEMM32, s);
+    if (which == 0) tc_gemm(&h->mXh[lx], &h->mXl[lx], &h->mAh[l], &h->mAl[l], g, s);
+    else tc_gemm(&h->mXh[lx], &h->mXl[lx], &h->mAPh[l], &h->mAPl[l], g, s);
+  }
   return check_launch(h);
 }
 
@@ -254,17 +330,15 @@ nmg_status cycle_level_1d(nmg_hierarchy* h, int l, int nrhs, cudaStream_t s) {
   }
   float* r = h->wr[l]->p;
   float* b = h->wb[l]->p;
-  const float* A = h->A32[l]->p;
-  const float* AP = h->AP32[l]->p;
   const int nu1 = h->d.nu1, nu2 = h->d.nu2;
   const float* rl = y;
   if (nu1 >= 1) {
     NMG_TRY(smooth_level(h, l, nrhs, y, x, false, s));           // x = x* + F'(h), x* = 0
     for (int k = 1; k < nu1; ++k) {
-      NMG_TRY(resid_gemm(h, nrhs, n, n, x, A, y, b, s));          // b = y - A x
+      NMG_TRY(level_resid(h, l, 0, nrhs, y, b, s));              // b = y - A x
       NMG_TRY(smooth_level(h, l, nrhs, b, x, true, s));
     }
-    NMG_TRY(resid_gemm(h, nrhs, n, n, x, A, y, r, s));            // r_l = y - A x
+    NMG_TRY(level_resid(h, l, 0, nrhs, y, r, s));                 // r_l = y - A x
     rl = r;
   } else {
     NMG_CUDA(cudaMemsetAsync(x, 0, sizeof(float) * (size_t)nrhs * n, s));
@@ -274,14 +348,14 @@ nmg_status cycle_level_1d(nmg_hierarchy* h, int l, int nrhs, cudaStream_t s) {
   NMG_TRY(cycle_level_1d(h, l + 1, nrhs, s));
   const float* e = h->wx[l + 1]->p;
   if (nu2 >= 1) {
-    NMG_TRY(resid_gemm(h, nrhs, n, n / 2, e, AP, rl, b, s));       // b = r_l - (A P) e
+    NMG_TRY(level_resid(h, l, 1, nrhs, rl, b, s));                // b = r_l - (A P) e
   }
   { Prof p(h, NMG_K_TRANSFER, s); prolong_add1d(nrhs, n / 2, e, n / 2, x, n, s); }   // x += P e
   NMG_TRY(check_launch(h));
   if (nu2 >= 1) {
     NMG_TRY(smooth_level(h, l, nrhs, b, x, true, s));
     for (int k = 1; k < nu2; ++k) {
-      NMG_TRY(resid_gemm(h, nrhs, n, n, x, A, y, b, s));
+      NMG_TRY(level_resid(h, l, 0, nrhs, y, b, s));
       NMG_TRY(smooth_level(h, l, nrhs, b, x, true, s));
     }
   }
@@ -390,6 +464,17 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
       std::vector<double> AP, Ac;
       host_prolong_cols(A, nl, nl, AP);                 // A_l P_l : nl x nl/2
       NMG_TRY(h->AP32.back()->upload(to_f32(AP).data(), (size_t)nl * (nl / 2)));
+      {
+        std::vector<float> hi, lo;
+        h->A32h.emplace_back(new DevBuf<float>()); h->A32l.emplace_back(new DevBuf<float>());
+        h->AP32h.emplace_back(new DevBuf<float>()); h->AP32l.emplace_back(new DevBuf<float>());
+        split_host(A, hi, lo);
+        NMG_TRY(h->A32h.back()->upload(hi.data(), hi.size()));
+        NMG_TRY(h->A32l.back()->upload(lo.data(), lo.size()));
+        split_host(AP, hi, lo);
+        NMG_TRY(h->AP32h.back()->upload(hi.data(), hi.size()));
+        NMG_TRY(h->AP32l.back()->upload(lo.data(), lo.size()));
+      }
       host_restrict_rows(AP, nl, nl / 2, Ac);           // R A P
       A.swap(Ac);
     }
@@ -444,6 +529,32 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
       v->emplace_back(new DevBuf<float>());
       const bool need = (v == &h->wy || v == &h->wx) || l < h->L - 1;
       if (need) NMG_TRY(v->back()->alloc(B * (size_t)h->N[l]));
+    }
+  }
+  {
+    const char* env = std::getenv("NMG_GEMM");
+    h->use_tc = !(env && std::string(env) == "simt");
+  }
+  if (d.dim == 1) {
+    h->mAh.resize(h->L); h->mAl.resize(h->L); h->mAPh.resize(h->L); h->mAPl.resize(h->L);
+    h->mXh.resize(h->L); h->mXl.resize(h->L);
+    for (int l = 0; l < h->L; ++l) {
+      const int nl = h->n[l];
+      h->sxh.emplace_back(new DevBuf<float>());
+      h->sxl.emplace_back(new DevBuf<float>());
+      if (nl % 16 != 0) continue;   // small levels use the SIMT kernel
+      NMG_TRY(h->sxh.back()->alloc(B * nl));
+      NMG_TRY(h->sxl.back()->alloc(B * nl));
+      NMG_TRY(make_map(&h->mXh[l], h->sxh.back()->p, (int64_t)B, nl, tc_gemm_block_m()));
+      NMG_TRY(make_map(&h->mXl[l], h->sxl.back()->p, (int64_t)B, nl, tc_gemm_block_m()));
+      if (l < h->L - 1) {
+        NMG_TRY(make_map(&h->mAh[l], h->A32h[l]->p, nl, nl, tc_gemm_block_n()));
+        NMG_TRY(make_map(&h->mAl[l], h->A32l[l]->p, nl, nl, tc_gemm_block_n()));
+        if ((nl / 2) % 16 == 0) {
+          NMG_TRY(make_map(&h->mAPh[l], h->AP32h[l]->p, nl, nl / 2, tc_gemm_block_n()));
+          NMG_TRY(make_map(&h->mAPl[l], h->AP32l[l]->p, nl, nl / 2, tc_gemm_block_n()));
+        }
+      }
     }
   }
   h->ntiles = gemm_f64_ntiles((int)h->N[0]);
@@ -620,6 +731,11 @@ nmg_status nmg_debug_level_op(nmg_hierarchy* h, int32_t level, int32_t op, int32
     case NMG_OP_APPLY:
     case NMG_OP_RESIDUAL: {
       if (!smoothed) return fail(NMG_ERR_INVALID_ARG, "no fp32 operator stored at the coarsest level");
+      if (h->use_tc && n % 16 == 0) {
+        NMG_CUDA(cudaMemcpyAsync(h->wx[l]->p, fin, sizeof(float) * (size_t)nrhs * n, cudaMemcpyDeviceToDevice, s));
+        NMG_TRY(level_resid(h, l, 0, nrhs, op == NMG_OP_RESIDUAL ? fout : nullptr, fout, s, op == NMG_OP_RESIDUAL));
+        return NMG_OK;
+      }
       Gemm32Args g{};
       g.M = nrhs; g.N = n; g.K = n; g.batch = 1;
       g.X = fin; g.ldx = n; g.W = h->A32[l]->p; g.ldw = n; g.w_kmajor = true;

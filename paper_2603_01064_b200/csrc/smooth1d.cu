@@ -16,11 +16,12 @@ constexpr int NT = 256;
 constexpr int T3 = 252;                           // outputs per tile
 constexpr int W2 = T3 + 2 * HALO;                 // 256 layer-2 positions = 16 groups x 16
 constexpr int W1 = W2 + 2 * HALO;                 // 260 layer-1 positions
-constexpr int S1 = W1 + 1;                        // odd smem strides
-constexpr int S2 = W2 + 1;
+constexpr int S1 = W1;                            // 260: 16B-aligned rows (LDS.128 windows)
+constexpr int S2 = W2 + 4;                        // 260: 2-way max on the STS.128 writes
 constexpr int PP = 16;                            // layer-2 positions per thread
 constexpr int NPARAM = C * 1 * KS + C + C * C * KS + C + 1 * C * KS + 1;   // 1473
 constexpr int UPAD = 3 * HALO;                    // 6
+constexpr int Q3 = T3 / 4;                        // 63 layer-3 position quads
 
 __global__ void __launch_bounds__(NT, 2) smooth1d_kernel(Smooth1dArgs a) {
   extern __shared__ __align__(16) float sm[];
@@ -65,31 +66,35 @@ __global__ void __launch_bounds__(NT, 2) smooth1d_kernel(Smooth1dArgs a) {
     for (int j = tid; j < n; j += NT) u[UPAD + j] = (float)((double)u[UPAD + j] / s);
   }
   const float sf = (float)s;
-  const int log2n = 31 - __clz(n);
 
-  // layer-2 thread role: output channel o, position group pg
+  // layer-2 thread role: output channel o, position group pg (16 positions)
   const int o = tid & (C - 1), pg = tid >> 4;
-  float wr[C * KS];
-#pragma unroll
-  for (int i = 0; i < C * KS; ++i) wr[i] = 0.f;
   __syncthreads();
+  float wr[C * KS];
 #pragma unroll
   for (int i = 0; i < C * KS; ++i) wr[i] = w1[o * C * KS + i];
   const float bo = b1[o];
+  // layer-1 role: channel c1 = tid & 15, positions (tid >> 4) + 16 k
+  float w0r[KS];
+#pragma unroll
+  for (int t = 0; t < KS; ++t) w0r[t] = w0[o * KS + t];
+  const float b0r = b0[o];
+  // layer-3 role: position quad q3 = tid >> 2 (< 63), channel group cg = tid & 3 (4 channels)
+  const int q3 = tid >> 2, cg = tid & 3;
 
   for (int t0 = 0; t0 < n; t0 += T3) {
     // ---- layer 1: a1[c][jj], position p = t0 - 4 + jj, zero outside [0, n)
-    for (int idx = tid; idx < C * W1; idx += NT) {
-      const int c = idx / W1, jj = idx - c * W1;
+#pragma unroll 1
+    for (int jj = pg; jj < W1; jj += NT / C) {
       const int p = t0 - 2 * HALO + jj;
       float v = 0.f;
       if (p >= 0 && p < n) {
-        float acc = b0[c];
+        float acc = b0r;
 #pragma unroll
-        for (int t = 0; t < KS; ++t) acc = fmaf(w0[c * KS + t], u[UPAD + p + t - HALO], acc);
+        for (int t = 0; t < KS; ++t) acc = fmaf(w0r[t], u[UPAD + p + t - HALO], acc);
         v = fmaxf(acc, 0.f);
       }
-      a1[c * S1 + jj] = v;
+      a1[o * S1 + jj] = v;
     }
     __syncthreads();
     // ---- layer 2: a2[o][jj2], position p = t0 - 2 + jj2
@@ -100,10 +105,13 @@ __global__ void __launch_bounds__(NT, 2) smooth1d_kernel(Smooth1dArgs a) {
       const int base = pg * PP;
 #pragma unroll
       for (int c = 0; c < C; ++c) {
-        float win[PP + KS - 1];
-        const float* src = a1 + c * S1 + base;
+        float win[PP + 4];
+        const float4* src = reinterpret_cast<const float4*>(a1 + c * S1 + base);
 #pragma unroll
-        for (int i = 0; i < PP + KS - 1; ++i) win[i] = src[i];
+        for (int i = 0; i < (PP + 4) / 4; ++i) {
+          const float4 v = src[i];
+          win[4 * i] = v.x; win[4 * i + 1] = v.y; win[4 * i + 2] = v.z; win[4 * i + 3] = v.w;
+        }
 #pragma unroll
         for (int t = 0; t < KS; ++t) {
           const float wv = wr[c * KS + t];
@@ -112,28 +120,53 @@ __global__ void __launch_bounds__(NT, 2) smooth1d_kernel(Smooth1dArgs a) {
         }
       }
 #pragma unroll
-      for (int i = 0; i < PP; ++i) {
-        const int p = t0 - HALO + base + i;
-        a2[o * S2 + base + i] = (p >= 0 && p < n) ? fmaxf(acc[i], 0.f) : 0.f;
+      for (int i = 0; i < PP; i += 4) {
+        float4 v;
+        float* vv = reinterpret_cast<float*>(&v);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int p = t0 - HALO + base + i + k;
+          vv[k] = (p >= 0 && p < n) ? fmaxf(acc[i + k], 0.f) : 0.f;
+        }
+        *reinterpret_cast<float4*>(a2 + o * S2 + base + i) = v;
       }
     }
     __syncthreads();
-    // ---- layer 3: h[p], p = t0 + jj3
-    if (tid < T3) {
-      const int p = t0 + tid;
-      if (p < n) {
-        float acc = b2[0];
-#pragma unroll 4
-        for (int c = 0; c < C; ++c) {
+    // ---- layer 3: h[p], p = t0 + 4 q3 + k; channels split in 4 groups, reduced by shuffles
+    // (all 256 threads take part in the shuffles; quad 63 reads the row padding and is dropped)
+    {
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-          for (int t = 0; t < KS; ++t) acc = fmaf(w2[c * KS + t], a2[c * S2 + tid + t], acc);
+      for (int cc = 0; cc < C / 4; ++cc) {
+        const int c = cg * (C / 4) + cc;
+        const float4* src = reinterpret_cast<const float4*>(a2 + c * S2 + 4 * q3);
+        const float4 v0 = src[0], v1 = src[1];
+        const float win[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+        for (int t = 0; t < KS; ++t) {
+          const float wv = w2[c * KS + t];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) acc[k] = fmaf(wv, win[k + t], acc[k]);
         }
-        const float hv = acc * sf;
-        if (a.filter) {
-          cb[bitrev(p, log2n)] = make_float2(hv, 0.f);
-        } else {
-          float* xrow = a.x + (int64_t)rhs * a.ldx;
-          xrow[p] = a.accumulate ? xrow[p] + hv : hv;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], 1);
+        acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], 2);
+      }
+      if (cg == 0 && q3 < Q3) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int p = t0 + 4 * q3 + k;
+          if (p < n) {
+            const float hv = (acc[k] + b2[0]) * sf;
+            if (a.filter) {
+              cb[p] = make_float2(hv, 0.f);
+            } else {
+              float* xrow = a.x + (int64_t)rhs * a.ldx;
+              xrow[p] = a.accumulate ? xrow[p] + hv : hv;
+            }
+          }
         }
       }
     }
@@ -141,19 +174,21 @@ __global__ void __launch_bounds__(NT, 2) smooth1d_kernel(Smooth1dArgs a) {
   }
   if (!a.filter) return;
 
-  // ---- level filter F'_l on the whole row
-  fft_dit_forward(cb, n, a.twiddle, a.tw_n, tid, NT);
+  // ---- level filter F'_l on the whole row: DIF forward (bit-reversed spectrum),
+  //      mask, DIT inverse (natural order) -- no permutation passes
+  const int log2n = 31 - __clz(n);
+  fft_dif_forward(cb, n, a.twiddle, a.tw_n, tid, NT);
   for (int k = tid; k < n; k += NT) {
-    const float m = level_mask_1d(k, n);
+    const float m = level_mask_1d(bitrev(k, log2n), n);
     const float2 v = cb[k];
     cb[k] = make_float2(v.x * m, v.y * m);
   }
   __syncthreads();
-  fft_dif_inverse(cb, n, a.twiddle, a.tw_n, tid, NT);
+  fft_dit_inverse(cb, n, a.twiddle, a.tw_n, tid, NT);
   const float inv_n = 1.0f / (float)n;
   float* xrow = a.x + (int64_t)rhs * a.ldx;
   for (int j = tid; j < n; j += NT) {
-    const float v = cb[bitrev(j, log2n)].x * inv_n;
+    const float v = cb[j].x * inv_n;
     xrow[j] = a.accumulate ? xrow[j] + v : v;
   }
 }

@@ -96,6 +96,24 @@ def test_apply_and_residual(cfg0, nrhs):
         assert rel_l2(r.cpu().numpy(), y - want) < 1e-5
 
 
+@pytest.mark.parametrize("lvl", [1, 2, 3, 4, 5])
+def test_apply_cfg1_levels_ragged(cfg1, lvl):
+    """tcgen05 3xTF32 operator apply at every smoothed level of config 1, ragged batch."""
+    _, _, H, h = cfg1
+    n = CFG1.n >> (lvl - 1)
+    nrhs = 131
+    rng = np.random.default_rng(10 + lvl)
+    x = rng.standard_normal((nrhs, n)).astype(np.float32)
+    y = rng.standard_normal((nrhs, n)).astype(np.float32)
+    want = O.apply_A(H, lvl - 1, x.astype(np.float64))
+    out = torch.zeros(nrhs, n, device=DEV)
+    h.debug_op(lvl, nmg.OP_APPLY, T(x), out)
+    assert rel_l2(out.cpu().numpy(), want) < 1e-5
+    r = T(y)
+    h.debug_op(lvl, nmg.OP_RESIDUAL, T(x), r)
+    assert rel_l2(r.cpu().numpy(), y - want) < 1e-5
+
+
 def test_filter(cfg0):
     _, _, H, h = cfg0
     rng = np.random.default_rng(2)
