@@ -21,7 +21,7 @@ Structure, in the paper's order:
 
 Everything is fp64 (numpy float64).  CNN weights arrive as fp32 values and are
 used as fp64 numbers.  Library primitives used as single steps: matrix
-products (numpy/BLAS), np.fft (DFT), np.tensordot (channel contraction).
+products (numpy/BLAS), np.fft (DFT), np.tensordot (channel contraction per tap).
 
 parity unpinned: CNN outputs with ReLU active under W_seed beyond the
 library-conv comparison (tests/test_oracle_pins.py::test_cnn_*), and the
@@ -282,7 +282,8 @@ def conv_same(x: np.ndarray, W: np.ndarray, b: np.ndarray) -> np.ndarray:
         xp[:, :, p:p + n] = x
         y = np.zeros((Bn, W.shape[0], n)) + b[None, :, None]
         for t in range(k):
-            y += np.einsum('oc,bci->boi', W[:, :, t], xp[:, :, t:t + n])
+            # contraction over input channels c of W[o, c, t] and x[b, c, i + t - k//2]
+            y += np.tensordot(W[:, :, t], xp[:, :, t:t + n], axes=([1], [1])).transpose(1, 0, 2)
         return y
     Bn, Ci, n2, n1 = x.shape
     xp = np.zeros((Bn, Ci, n2 + 2 * p, n1 + 2 * p))
@@ -290,7 +291,9 @@ def conv_same(x: np.ndarray, W: np.ndarray, b: np.ndarray) -> np.ndarray:
     y = np.zeros((Bn, W.shape[0], n2, n1)) + b[None, :, None, None]
     for t2 in range(k):
         for t1 in range(k):
-            y += np.einsum('oc,bcij->boij', W[:, :, t2, t1], xp[:, :, t2:t2 + n2, t1:t1 + n1])
+            # contraction over c of W[o, c, t2, t1] and x[b, c, i2 + t2 - k//2, i1 + t1 - k//2]
+            y += np.tensordot(W[:, :, t2, t1], xp[:, :, t2:t2 + n2, t1:t1 + n1],
+                              axes=([1], [1])).transpose(1, 0, 2, 3)
     return y
 
 

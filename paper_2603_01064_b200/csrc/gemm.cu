@@ -113,8 +113,15 @@ __global__ void __launch_bounds__(NT) sgemm_kernel(Gemm32Args a) {
       const int n = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
       if (n >= N) continue;
       float v = a.negate ? -acc[i][j] : acc[i][j];
-      if (C) v = C[(int64_t)m * a.ldc + n] + v;
-      D[(int64_t)m * a.ldd + n] = v;
+      if (a.tblock) {
+        const int64_t tb = a.tblock;
+        const int64_t off = (m / tb) * tb * tb + (int64_t)n * tb + (m % tb);
+        if (C) v = C[off] + v;
+        D[off] = v;
+      } else {
+        if (C) v = C[(int64_t)m * a.ldc + n] + v;
+        D[(int64_t)m * a.ldd + n] = v;
+      }
     }
   }
 }
@@ -245,9 +252,19 @@ __global__ void __launch_bounds__(DNT) dgemm_resid_kernel(Gemm64Args a) {
         const int n = n0 + wn * 32 + j * 8 + t * 2 + e;
         if (m < M && n < N) {
           double v = a.negate ? -acc[i][j][e] : acc[i][j][e];
-          if (a.Y) v = a.Y[(int64_t)m * a.ldy + n] + v;
-          if (a.r32) a.r32[(int64_t)m * a.ldr32 + n] = (float)v;
-          if (a.r64) a.r64[(int64_t)m * a.ldr64 + n] = v;
+          if (a.tblock) {
+            const int64_t tb = a.tblock;
+            const int64_t off = (m / tb) * tb * tb + (int64_t)n * tb + (m % tb);
+            if (a.Y) v = a.Y[off] + v;
+            if (a.ax) v = fma(-a.alpha, a.ax[off], v);
+            if (a.r32) a.r32[off] = (float)v;
+            if (a.r64) a.r64[off] = v;
+          } else {
+            if (a.Y) v = a.Y[(int64_t)m * a.ldy + n] + v;
+            if (a.ax) v = fma(-a.alpha, a.ax[(int64_t)m * a.ldy + n], v);
+            if (a.r32) a.r32[(int64_t)m * a.ldr32 + n] = (float)v;
+            if (a.r64) a.r64[(int64_t)m * a.ldr64 + n] = v;
+          }
           sq += v * v;
         }
       }

@@ -86,6 +86,63 @@ NMG_D void umma_commit(uint64_t* bar) {
                : "memory");
 }
 
+NMG_D void tc_store_chunk(const TcGemmArgs& a, const uint32_t (&v)[32], int m, int nb, const float* crow,
+                          float* drow) {
+    if (a.tblock) {
+      // transposed store within tb x tb blocks: lanes hold consecutive rows -> coalesced
+      const int64_t tb = a.tblock;
+      const int64_t base = ((int64_t)m / tb) * tb * tb + (m % tb);
+#pragma unroll 4
+      for (int j = 0; j < 32; ++j) {
+        const int n = nb + j;
+        if (n >= a.N) break;
+        float acc = __uint_as_float(v[j]);
+        if (a.negate) acc = -acc;
+        const int64_t off = base + (int64_t)n * tb;
+        if (a.Dh) {
+          uint32_t hh, ll;
+          asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(hh) : "f"(acc));
+          asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(ll) : "f"(acc - __uint_as_float(hh)));
+          a.Dh[off] = __uint_as_float(hh);
+          a.Dl[off] = __uint_as_float(ll);
+        } else {
+          a.D[off] = a.C ? a.C[off] + acc : acc;
+        }
+      }
+      return;
+    }
+    if (nb + 32 <= a.N && !a.Dh) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        float4 o;
+        float acc[4] = {__uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
+                        __uint_as_float(v[j + 3])};
+        if (a.negate) { acc[0] = -acc[0]; acc[1] = -acc[1]; acc[2] = -acc[2]; acc[3] = -acc[3]; }
+        if (crow) {
+          const float4 cv = *reinterpret_cast<const float4*>(crow + nb + j);
+          o = make_float4(cv.x + acc[0], cv.y + acc[1], cv.z + acc[2], cv.w + acc[3]);
+        } else {
+          o = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        }
+        *reinterpret_cast<float4*>(drow + nb + j) = o;
+      }
+    } else {
+      for (int j = 0; j < 32 && nb + j < a.N; ++j) {
+        float acc = __uint_as_float(v[j]);
+        if (a.negate) acc = -acc;
+        if (a.Dh) {
+          uint32_t hh, ll;
+          asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(hh) : "f"(acc));
+          asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(ll) : "f"(acc - __uint_as_float(hh)));
+          a.Dh[(int64_t)m * a.ldd + nb + j] = __uint_as_float(hh);
+          a.Dl[(int64_t)m * a.ldd + nb + j] = __uint_as_float(ll);
+        } else {
+          drow[nb + j] = crow ? crow[nb + j] + acc : acc;
+        }
+      }
+    }
+  }
+
 __global__ void __launch_bounds__(TNT, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tXh, const __grid_constant__ CUtensorMap tXl,
                    const __grid_constant__ CUtensorMap tWh, const __grid_constant__ CUtensorMap tWl,
@@ -166,7 +223,7 @@ __global__ void __launch_bounds__(TNT, 1)
   const int m = m0 + row;
   const bool mok = m < a.M;
   const float* crow = a.C ? a.C + (int64_t)m * a.ldc : nullptr;
-  float* drow = a.D + (int64_t)m * a.ldd;
+  float* drow = a.D ? a.D + (int64_t)m * a.ldd : nullptr;
 #pragma unroll 1
   for (int c = 0; c < TBN / 32; ++c) {
     uint32_t v[32];
@@ -181,30 +238,8 @@ __global__ void __launch_bounds__(TNT, 1)
         : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
     const int nb = n0 + c * 32;
-    if (mok) {
-      if (nb + 32 <= a.N) {
-#pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-          float4 o;
-          float acc[4] = {__uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
-                          __uint_as_float(v[j + 3])};
-          if (a.negate) { acc[0] = -acc[0]; acc[1] = -acc[1]; acc[2] = -acc[2]; acc[3] = -acc[3]; }
-          if (crow) {
-            const float4 cv = *reinterpret_cast<const float4*>(crow + nb + j);
-            o = make_float4(cv.x + acc[0], cv.y + acc[1], cv.z + acc[2], cv.w + acc[3]);
-          } else {
-            o = make_float4(acc[0], acc[1], acc[2], acc[3]);
-          }
-          *reinterpret_cast<float4*>(drow + nb + j) = o;
-        }
-      } else {
-        for (int j = 0; j < 32 && nb + j < a.N; ++j) {
-          float acc = __uint_as_float(v[j]);
-          if (a.negate) acc = -acc;
-          drow[nb + j] = crow ? crow[nb + j] + acc : acc;
-        }
-      }
-    }
+    if (mok) tc_store_chunk(a, v, m, nb, crow, drow);
+    __syncwarp();
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();

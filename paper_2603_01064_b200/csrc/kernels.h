@@ -18,6 +18,8 @@ struct Gemm32Args {
   const float* C; int64_t ldc, sc;       // may be null (then D = acc)
   float* D; int64_t ldd, sd;
   bool negate;                            // D = C - acc (true) or C + acc (false)
+  int tblock = 0;                         // >0: row m, col j stored at (m/tb)*tb*ldd + j*tb + m%tb
+                                          //     (C read at the same place); batch must be 1
 };
 void gemm_f32(const Gemm32Args& a, cudaStream_t s);
 
@@ -33,6 +35,10 @@ struct Gemm64Args {
   double* r64; int64_t ldr64;            // may be null
   double* part;                           // may be null; [M][ceil(N/64)]
   bool negate;                            // R = Y - acc (true) / Y + acc
+  int tblock = 0;                         // >0: transposed store within tb x tb blocks (see Gemm32Args);
+                                          //     Y, ax, r32, r64 all use that mapping with ld = tb
+  const double* ax = nullptr;             // optional: R -= alpha * ax (same location as R)
+  double alpha = 0.0;
 };
 int gemm_f64_ntiles(int N);
 void gemm_f64(const Gemm64Args& a, cudaStream_t s);
@@ -42,8 +48,10 @@ void gemm_f64(const Gemm64Args& a, cudaStream_t s);
 struct TcGemmArgs {
   int M, N, K;
   const float* C; int64_t ldc;           // may be null
-  float* D; int64_t ldd;
+  float* D; int64_t ldd;                 // fp32 output (ignored when Dh is set)
   bool negate;
+  int tblock = 0;                        // >0: transposed store within tblock x tblock blocks
+  float* Dh = nullptr; float* Dl = nullptr;   // optional tf32 hi/lo split output (no C)
 };
 void tc_gemm(const CUtensorMap* xh, const CUtensorMap* xl, const CUtensorMap* wh, const CUtensorMap* wl,
              const TcGemmArgs& a, cudaStream_t s);
@@ -80,10 +88,30 @@ void coarse_chol_solve(int nc, int nrhs, const double* Lrow, const double* Lcol,
 // ---- outer (fp64) helpers --------------------------------------------------------
 void row_norms_f64(int nrhs, int N, const double* y, int64_t ldy, double* out, cudaStream_t s);
 void relres_finalize(int nrhs, int ntiles, const double* part, const double* ynorm, double* relres,
-                     double tol, uint8_t* active, cudaStream_t s);
+                     double tol, uint8_t* active, cudaStream_t s, int rows_per_rhs = 1);
 void update_x(int nrhs, int N, double* x, int64_t ldx, const float* d, int64_t ldd,
               const uint8_t* active, cudaStream_t s);
 void f64_to_f32(int64_t count, const double* in, float* out, cudaStream_t s);
 void f32_to_f64(int64_t count, const float* in, double* out, cudaStream_t s);
+
+// ---- 2D level operations (level2d.cu) -------------------------------------------
+struct Cnn2dArgs {
+  int n, nrhs, C;
+  const float* b;          // input [nrhs][n][n]
+  const double* norms;     // per-RHS ||b|| (null: h = N(b), debug)
+  const float* params;     // device layout: w0, b0, w1 [c][t2][t1][o], b1, w2 [c][t2][t1][o], b2, w3, b3
+  float2* Z;               // if set: write (h, 0) for the filter passes
+  float* x;                // else: x = h / x += h
+  bool accumulate;
+};
+void cnn2d(const Cnn2dArgs& a, cudaStream_t s);
+int cnn2d_smem(int C);
+void restrict2d(int nrhs, int n_f, const float* f, float* c, cudaStream_t s);
+void prolong_add2d(int nrhs, int n_c, const float* c, float* f, cudaStream_t s);
+void qstencil(int nrhs, int n, int hb, float alpha, const float* Q, const float* X, const float* C, float* D,
+              cudaStream_t s);
+void norms_f32(int nrhs, int64_t N, const float* x, double* part, int chunks, double* out, cudaStream_t s);
+void filter2d(int nrhs, int n, float2* Z, const float2* tw, int tw_n, float* x, bool accumulate, cudaStream_t s);
+void real_to_complex(int64_t count, const float* x, float2* Z, cudaStream_t s);
 
 }  // namespace nmg

@@ -1,0 +1,419 @@
+// 2D level operations (Alg 4 "NMGF2d" P:373-401).  Layout: each RHS is an
+// n x n column-major matrix X (element (i1, i2) at i1 + n i2, Vec convention P:363),
+// i.e. a row-major [i2][i1] array; batches are RHS-major.
+//   * restrict2d / prolong_add2d : hat I = I (x) I, tensor products of reading R4
+//   * qstencil_resid             : D = C - alpha Q X Q^T (banded Galerkin mass term)
+//   * norms_f32                  : ||B_l||_2 Frobenius per RHS in fp64 (R10)
+//   * cnn2d_kernel               : fused 4-layer 3x3 CNN smoother N_theta (R7), FFMA
+//   * fft2d_*                    : level filter hat F'_l = Re(IDFT2(M' (.) DFT2(.)))
+#include "common.cuh"
+#include "fft.cuh"
+#include "kernels.h"
+
+namespace nmg {
+namespace {
+
+inline int nblk(int64_t n, int t) { return (int)ceil_div64(n, t); }
+
+NMG_D float r1d(float fm, float f0, float f1, float fp) {
+  return __fmul_rn(__fadd_rn(__fadd_rn(fm, fp), __fmul_rn(3.0f, __fadd_rn(f0, f1))), 0.125f);
+}
+
+// coarse (b, j2, j1) = R (rows) of R (cols): first along i1 for the 4 fine rows, then i2
+__global__ void restrict2d_kernel(int nrhs, int n_c, const float* __restrict__ f, float* __restrict__ c) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t per = (int64_t)n_c * n_c;
+  if (idx >= nrhs * per) return;
+  const int b = (int)(idx / per);
+  const int rem = (int)(idx - b * per);
+  const int j2 = rem / n_c, j1 = rem - j2 * n_c;
+  const int n_f = 2 * n_c;
+  const float* F = f + (int64_t)b * n_f * n_f;
+  const int c1[4] = {max(2 * j1 - 1, 0), 2 * j1, 2 * j1 + 1, min(2 * j1 + 2, n_f - 1)};
+  const int c2[4] = {max(2 * j2 - 1, 0), 2 * j2, 2 * j2 + 1, min(2 * j2 + 2, n_f - 1)};
+  float r[4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const float* row = F + (int64_t)c2[a] * n_f;
+    r[a] = r1d(row[c1[0]], row[c1[1]], row[c1[2]], row[c1[3]]);
+  }
+  c[idx] = r1d(r[0], r[1], r[2], r[3]);
+}
+
+NMG_D float p1d(float cj, float ck) { return __fadd_rn(__fmul_rn(0.75f, cj), __fmul_rn(0.25f, ck)); }
+
+__global__ void prolong_add2d_kernel(int nrhs, int n_c, const float* __restrict__ c, float* __restrict__ f) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int n_f = 2 * n_c;
+  const int64_t per = (int64_t)n_f * n_f;
+  if (idx >= nrhs * per) return;
+  const int b = (int)(idx / per);
+  const int rem = (int)(idx - b * per);
+  const int i2 = rem / n_f, i1 = rem - i2 * n_f;
+  const int j1 = i1 >> 1, k1 = min(max((i1 & 1) ? j1 + 1 : j1 - 1, 0), n_c - 1);
+  const int j2 = i2 >> 1, k2 = min(max((i2 & 1) ? j2 + 1 : j2 - 1, 0), n_c - 1);
+  const float* C = c + (int64_t)b * n_c * n_c;
+  const float vj = p1d(C[j2 * n_c + j1], C[j2 * n_c + k1]);
+  const float vk = p1d(C[k2 * n_c + j1], C[k2 * n_c + k1]);
+  f[idx] = __fadd_rn(f[idx], p1d(vj, vk));
+}
+
+// D[b][i2][i1] = C[..] - alpha * sum_{a2, a1} Q[i2][a2] Q[i1][a1] X[b][a2][a1], |a - i| <= hb
+__global__ void qstencil_kernel(int nrhs, int n, int hb, float alpha, const float* __restrict__ Q,
+                                const float* __restrict__ X, const float* __restrict__ C, float* __restrict__ D) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t per = (int64_t)n * n;
+  if (idx >= nrhs * per) return;
+  const int b = (int)(idx / per);
+  const int rem = (int)(idx - b * per);
+  const int i2 = rem / n, i1 = rem - i2 * n;
+  const float* Xb = X + (int64_t)b * per;
+  float acc = 0.f;
+  for (int a2 = max(i2 - hb, 0); a2 <= min(i2 + hb, n - 1); ++a2) {
+    const float q2 = Q[(int64_t)i2 * n + a2];
+    float t = 0.f;
+    for (int a1 = max(i1 - hb, 0); a1 <= min(i1 + hb, n - 1); ++a1) t = fmaf(Q[(int64_t)i1 * n + a1], Xb[(int64_t)a2 * n + a1], t);
+    acc = fmaf(q2, t, acc);
+  }
+  D[idx] = (C ? C[idx] : 0.f) - alpha * acc;
+}
+
+// per-RHS sum of squares, fp64, two stages (fixed order => deterministic)
+__global__ void __launch_bounds__(256) sumsq_partial_kernel(int64_t N, int chunks, const float* __restrict__ x,
+                                                            double* __restrict__ part) {
+  __shared__ double red[32];
+  const int b = blockIdx.y, ch = blockIdx.x;
+  const int64_t len = ceil_div64(N, chunks);
+  const int64_t lo = ch * len, hi = min(N, lo + len);
+  const float* r = x + (int64_t)b * N;
+  double s = 0.0;
+  for (int64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) s += (double)r[j] * (double)r[j];
+  s = block_sum_f64(s, red);
+  if (threadIdx.x == 0) part[(int64_t)b * chunks + ch] = s;
+}
+__global__ void sumsq_final_kernel(int nrhs, int chunks, const double* __restrict__ part, double* __restrict__ out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nrhs) return;
+  double s = 0.0;
+  for (int c = 0; c < chunks; ++c) s += part[(int64_t)b * chunks + c];
+  out[b] = sqrt(s);
+}
+
+// ------------------------------------------------------------------ fused 2D CNN (FFMA)
+// Output tile 16 x 16; 4 layers with 3x3 kernels => halo 4.  Activation planes are
+// channel-major [c][y][x] with row stride PS.  Region sizes: in 24, L1 22, L2 20, L3 18.
+constexpr int CT = 16;            // output tile
+constexpr int PS = 24;            // plane row stride (>= 22 + 2 slack for 4-wide groups)
+
+template <int C>
+struct Cnn2dSmem {
+  static constexpr int IN = 24 * PS + 8;          // input plane (+ slack)
+  static constexpr int A1 = C * 22 * PS + 8;      // layer-1 output; later layer-3 output
+  static constexpr int A2 = C * 20 * PS + 8;      // layer-2 output
+  static constexpr int W14 = C * 9 + C + C * 9 + 1 + 3;  // layer 1 and 4 params
+  static constexpr int FLOATS = IN + A1 + A2 + W14;
+};
+
+// one hidden layer C -> C on an output region of w x w (input region w+2), from `in` to `out`.
+// Items: (og: C/8 output-channel groups) x (rows w) x (x-groups of 4).  Pixels outside the
+// image are written as zeros (zero "same" padding of the next layer).
+template <int C>
+NMG_D void cnn_hidden_layer(const float* __restrict__ in, float* __restrict__ out, int w,
+                            const float* __restrict__ W, const float* __restrict__ Bv, int gy0, int gx0, int n,
+                            int tid) {
+  const int xg = (w + 3) / 4;
+  const int items = (C / 8) * w * xg;
+  for (int it = tid; it < items; it += 256) {
+    const int og = it / (w * xg);
+    const int rem = it - og * (w * xg);
+    const int y = rem / xg;
+    const int x = (rem - y * xg) * 4;
+    float acc[4][8];
+#pragma unroll
+    for (int o = 0; o < 8; ++o) {
+      const float bb = __ldg(Bv + og * 8 + o);
+#pragma unroll
+      for (int p = 0; p < 4; ++p) acc[p][o] = bb;
+    }
+#pragma unroll 2
+    for (int c = 0; c < C; ++c) {
+#pragma unroll
+      for (int t2 = 0; t2 < 3; ++t2) {
+        const float* src = in + (c * (w + 2) + y + t2) * PS + x;
+        const float4 v0 = *reinterpret_cast<const float4*>(src);
+        const float2 v1 = *reinterpret_cast<const float2*>(src + 4);
+        const float win[6] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y};
+#pragma unroll
+        for (int t1 = 0; t1 < 3; ++t1) {
+          // weights layout [c][t2][t1][o] (prepared on the host)
+          const float4* wp = reinterpret_cast<const float4*>(W + ((c * 3 + t2) * 3 + t1) * C + og * 8);
+          const float4 wa = __ldg(wp), wb = __ldg(wp + 1);
+          const float wv[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+#pragma unroll
+          for (int p = 0; p < 4; ++p)
+#pragma unroll
+            for (int o = 0; o < 8; ++o) acc[p][o] = fmaf(wv[o], win[p + t1], acc[p][o]);
+        }
+      }
+    }
+    const int gy = gy0 + y;
+#pragma unroll
+    for (int o = 0; o < 8; ++o) {
+      float* dst = out + ((og * 8 + o) * w + y) * PS + x;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const int gx = gx0 + x + p;
+        const bool inside = gy >= 0 && gy < n && gx >= 0 && gx < n && (x + p) < w;
+        dst[p] = inside ? fmaxf(acc[p][o], 0.f) : 0.f;
+      }
+    }
+  }
+}
+
+template <int C>
+__global__ void __launch_bounds__(256, 1) cnn2d_kernel(Cnn2dArgs a) {
+  extern __shared__ __align__(16) float sm[];
+  using L = Cnn2dSmem<C>;
+  float* in = sm;
+  float* act1 = in + L::IN;
+  float* act2 = act1 + L::A1;
+  float* w14 = act2 + L::A2;
+  const int tid = threadIdx.x;
+  const int n = a.n;
+  const int tiles_x = ceil_div(n, CT);
+  const int tile = blockIdx.x, b = blockIdx.y;
+  const int ty0 = (tile / tiles_x) * CT, tx0 = (tile % tiles_x) * CT;
+  const float* P = a.params;          // [w0 C*9][b0 C][w1' C*C*9][b1 C][w2' C*C*9][b2 C][w3 C*9][b3 1]
+  const float* w1t = P + C * 9 + C;   // hidden-layer weights, host-transposed to [c][t2][t1][o]
+  const float* b1 = w1t + C * C * 9;
+  const float* w2t = b1 + C;
+  const float* b2 = w2t + C * C * 9;
+  const float* w3 = b2 + C;
+  const float b3 = __ldg(w3 + C * 9);
+  for (int i = tid; i < C * 9 + C; i += 256) w14[i] = __ldg(P + i);                 // w0, b0
+  for (int i = tid; i < C * 9; i += 256) w14[C * 9 + C + i] = __ldg(w3 + i);       // w3
+  const double s = a.norms ? a.norms[b] : 1.0;
+  const float* X = a.b + (int64_t)b * n * n;
+  if (s == 0.0) {   // ||b|| = 0 => h = 0
+    if (a.Z || !a.accumulate) {
+      for (int i = tid; i < CT * CT; i += 256) {
+        const int y = ty0 + i / CT, x = tx0 + i % CT;
+        if (y < n && x < n) {
+          if (a.Z) a.Z[((int64_t)b * n + y) * n + x] = make_float2(0.f, 0.f);
+          else a.x[((int64_t)b * n + y) * n + x] = 0.f;
+        }
+      }
+    }
+    return;
+  }
+  // input region 24 x 24 at (ty0 - 4, tx0 - 4), scaled by 1/s, zero outside
+  for (int i = tid; i < 24 * 24; i += 256) {
+    const int y = i / 24, x = i % 24;
+    const int gy = ty0 - 4 + y, gx = tx0 - 4 + x;
+    float v = 0.f;
+    if (gy >= 0 && gy < n && gx >= 0 && gx < n) v = (float)((double)X[(int64_t)gy * n + gx] / s);
+    in[y * PS + x] = v;
+  }
+  __syncthreads();
+  // layer 1: 1 -> C on 22 x 22 at (ty0 - 3, tx0 - 3)
+  for (int i = tid; i < C * 22 * 22; i += 256) {
+    const int c = i / (22 * 22), rem = i - c * 22 * 22, y = rem / 22, x = rem % 22;
+    const int gy = ty0 - 3 + y, gx = tx0 - 3 + x;
+    float v = 0.f;
+    if (gy >= 0 && gy < n && gx >= 0 && gx < n) {
+      float acc = w14[C * 9 + c];
+#pragma unroll
+      for (int t2 = 0; t2 < 3; ++t2)
+#pragma unroll
+        for (int t1 = 0; t1 < 3; ++t1) acc = fmaf(w14[c * 9 + t2 * 3 + t1], in[(y + t2) * PS + x + t1], acc);
+      v = fmaxf(acc, 0.f);
+    }
+    act1[(c * 22 + y) * PS + x] = v;
+  }
+  __syncthreads();
+  cnn_hidden_layer<C>(act1, act2, 20, w1t, b1, ty0 - 2, tx0 - 2, n, tid);   // layer 2 on 20 x 20
+  __syncthreads();
+  cnn_hidden_layer<C>(act2, act1, 18, w2t, b2, ty0 - 1, tx0 - 1, n, tid);   // layer 3 on 18 x 18
+  __syncthreads();
+  // layer 4: C -> 1 on 16 x 16
+  {
+    const int y = tid / CT, x = tid % CT;
+    const int gy = ty0 + y, gx = tx0 + x;
+    float acc = b3;
+    const float* w3s = w14 + C * 9 + C;
+    for (int c = 0; c < C; ++c) {
+#pragma unroll
+      for (int t2 = 0; t2 < 3; ++t2)
+#pragma unroll
+        for (int t1 = 0; t1 < 3; ++t1) acc = fmaf(w3s[c * 9 + t2 * 3 + t1], act1[(c * 18 + y + t2) * PS + x + t1], acc);
+    }
+    if (gy < n && gx < n) {
+      const float hv = acc * (float)s;
+      const int64_t off = ((int64_t)b * n + gy) * n + gx;
+      if (a.Z) a.Z[off] = make_float2(hv, 0.f);
+      else a.x[off] = a.accumulate ? a.x[off] + hv : hv;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ 2D FFT filter passes
+// rows: R rows of length n per CTA (R*n <= 4096 complex in smem), in place in Z
+__global__ void __launch_bounds__(256) fft_rows_kernel(int n, int64_t nrows, float2* __restrict__ Z,
+                                                       const float2* __restrict__ tw, int tw_n, int inverse,
+                                                       float* __restrict__ x, int accumulate, float scale) {
+  extern __shared__ __align__(16) float2 cb[];
+  const int R = max(1, 4096 / n);
+  const int64_t r0 = (int64_t)blockIdx.x * R;
+  const int rows = (int)min((int64_t)R, nrows - r0);
+  const int tot = rows * n;
+  for (int i = threadIdx.x; i < tot; i += 256) cb[i] = Z[r0 * n + i];
+  __syncthreads();
+  // butterflies over all rows at once
+  const int halfn = n >> 1;
+  if (!inverse) {
+    for (int len = n; len >= 2; len >>= 1) {
+      const int half = len >> 1, step = tw_n / len;
+      for (int i = threadIdx.x; i < rows * halfn; i += 256) {
+        const int row = i / halfn, ii = i - row * halfn;
+        const int pos = ii & (half - 1);
+        const int j0 = row * n + ((ii - pos) << 1) + pos, j1 = j0 + half;
+        const float2 w = __ldg(tw + pos * step);
+        const float2 u = cb[j0], v = cb[j1];
+        cb[j0] = make_float2(u.x + v.x, u.y + v.y);
+        cb[j1] = cmul(make_float2(u.x - v.x, u.y - v.y), w);
+      }
+      __syncthreads();
+    }
+    for (int i = threadIdx.x; i < tot; i += 256) Z[r0 * n + i] = cb[i];
+  } else {
+    for (int len = 2; len <= n; len <<= 1) {
+      const int half = len >> 1, step = tw_n / len;
+      for (int i = threadIdx.x; i < rows * halfn; i += 256) {
+        const int row = i / halfn, ii = i - row * halfn;
+        const int pos = ii & (half - 1);
+        const int j0 = row * n + ((ii - pos) << 1) + pos, j1 = j0 + half;
+        const float2 w = __ldg(tw + pos * step);
+        const float2 u = cb[j0], v = cmulc(cb[j1], w);
+        cb[j0] = make_float2(u.x + v.x, u.y + v.y);
+        cb[j1] = make_float2(u.x - v.x, u.y - v.y);
+      }
+      __syncthreads();
+    }
+    for (int i = threadIdx.x; i < tot; i += 256) {
+      const float v = cb[i].x * scale;
+      const int64_t o = r0 * n + i;
+      x[o] = accumulate ? x[o] + v : v;
+    }
+  }
+}
+
+// columns: CTA = (group of G columns, RHS); DIF forward along i2, mask, DIT inverse
+__global__ void __launch_bounds__(256) fft_cols_kernel(int n, int G, float2* __restrict__ Z,
+                                                       const float2* __restrict__ tw, int tw_n) {
+  extern __shared__ __align__(16) float2 cb[];   // [n][G]
+  const int b = blockIdx.y, k0 = blockIdx.x * G;
+  float2* Zb = Z + (int64_t)b * n * n;
+  const int log2n = 31 - __clz(n);
+  for (int i = threadIdx.x; i < n * G; i += 256) {
+    const int r = i / G, c = i - r * G;
+    cb[i] = Zb[(int64_t)r * n + k0 + c];
+  }
+  __syncthreads();
+  const int halfn = n >> 1;
+  for (int len = n; len >= 2; len >>= 1) {
+    const int half = len >> 1, step = tw_n / len;
+    for (int i = threadIdx.x; i < halfn * G; i += 256) {
+      const int c = i % G, ii = i / G;
+      const int pos = ii & (half - 1);
+      const int j0 = ((ii - pos) << 1) + pos, j1 = j0 + half;
+      const float2 w = __ldg(tw + pos * step);
+      const float2 u = cb[j0 * G + c], v = cb[j1 * G + c];
+      cb[j0 * G + c] = make_float2(u.x + v.x, u.y + v.y);
+      cb[j1 * G + c] = cmul(make_float2(u.x - v.x, u.y - v.y), w);
+    }
+    __syncthreads();
+  }
+  // mask: position r holds k2 = bitrev(r); column c holds k1 = bitrev(k0 + c) (rows were DIF'd)
+  for (int i = threadIdx.x; i < n * G; i += 256) {
+    const int r = i / G, c = i - r * G;
+    const int a2 = bitrev(r, log2n), a1 = bitrev(k0 + c, log2n);
+    const float q2 = (float)(2 * min(a2, n - a2)) / (float)n;
+    const float q1 = (float)(2 * min(a1, n - a1)) / (float)n;
+    const float m = sqrtf(fmaxf(q1, q2));
+    cb[i] = make_float2(cb[i].x * m, cb[i].y * m);
+  }
+  __syncthreads();
+  for (int len = 2; len <= n; len <<= 1) {
+    const int half = len >> 1, step = tw_n / len;
+    for (int i = threadIdx.x; i < halfn * G; i += 256) {
+      const int c = i % G, ii = i / G;
+      const int pos = ii & (half - 1);
+      const int j0 = ((ii - pos) << 1) + pos, j1 = j0 + half;
+      const float2 w = __ldg(tw + pos * step);
+      const float2 u = cb[j0 * G + c], v = cmulc(cb[j1 * G + c], w);
+      cb[j0 * G + c] = make_float2(u.x + v.x, u.y + v.y);
+      cb[j1 * G + c] = make_float2(u.x - v.x, u.y - v.y);
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < n * G; i += 256) {
+    const int r = i / G, c = i - r * G;
+    Zb[(int64_t)r * n + k0 + c] = cb[i];
+  }
+}
+
+__global__ void real_to_complex_kernel(int64_t count, const float* __restrict__ x, float2* __restrict__ Z) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) Z[i] = make_float2(x[i], 0.f);
+}
+
+}  // namespace
+
+void restrict2d(int nrhs, int n_f, const float* f, float* c, cudaStream_t s) {
+  const int n_c = n_f / 2;
+  restrict2d_kernel<<<nblk((int64_t)nrhs * n_c * n_c, 256), 256, 0, s>>>(nrhs, n_c, f, c);
+}
+void prolong_add2d(int nrhs, int n_c, const float* c, float* f, cudaStream_t s) {
+  prolong_add2d_kernel<<<nblk((int64_t)nrhs * 4 * n_c * n_c, 256), 256, 0, s>>>(nrhs, n_c, c, f);
+}
+void qstencil(int nrhs, int n, int hb, float alpha, const float* Q, const float* X, const float* C, float* D,
+              cudaStream_t s) {
+  qstencil_kernel<<<nblk((int64_t)nrhs * n * n, 256), 256, 0, s>>>(nrhs, n, hb, alpha, Q, X, C, D);
+}
+void norms_f32(int nrhs, int64_t N, const float* x, double* part, int chunks, double* out, cudaStream_t s) {
+  sumsq_partial_kernel<<<dim3(chunks, nrhs), 256, 0, s>>>(N, chunks, x, part);
+  sumsq_final_kernel<<<nblk(nrhs, 128), 128, 0, s>>>(nrhs, chunks, part, out);
+}
+int cnn2d_smem(int C) {
+  return (C == 32 ? Cnn2dSmem<32>::FLOATS : Cnn2dSmem<48>::FLOATS) * (int)sizeof(float);
+}
+void cnn2d(const Cnn2dArgs& a, cudaStream_t s) {
+  const int tiles = ceil_div(a.n, CT) * ceil_div(a.n, CT);
+  dim3 grid(tiles, a.nrhs);
+  const int smem = cnn2d_smem(a.C);
+  if (a.C == 32) {
+    cudaFuncSetAttribute(cnn2d_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cnn2d_kernel<32><<<grid, 256, smem, s>>>(a);
+  } else {
+    cudaFuncSetAttribute(cnn2d_kernel<48>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cnn2d_kernel<48><<<grid, 256, smem, s>>>(a);
+  }
+}
+void filter2d(int nrhs, int n, float2* Z, const float2* tw, int tw_n, float* x, bool accumulate, cudaStream_t s) {
+  const int64_t nrows = (int64_t)nrhs * n;
+  const int R = std::max(1, 4096 / n);
+  const size_t smr = sizeof(float2) * (size_t)R * n;
+  cudaFuncSetAttribute(fft_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
+  fft_rows_kernel<<<nblk(nrows, R), 256, smr, s>>>(n, nrows, Z, tw, tw_n, 0, nullptr, 0, 1.f);
+  const int G = std::min(n, std::max(1, 16384 / n));
+  const size_t smc = sizeof(float2) * (size_t)n * G;
+  cudaFuncSetAttribute(fft_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
+  fft_cols_kernel<<<dim3(n / G, nrhs), 256, smc, s>>>(n, G, Z, tw, tw_n);
+  fft_rows_kernel<<<nblk(nrows, R), 256, smr, s>>>(n, nrows, Z, tw, tw_n, 1, x, accumulate ? 1 : 0,
+                                                   1.0f / ((float)n * (float)n));
+}
+void real_to_complex(int64_t count, const float* x, float2* Z, cudaStream_t s) {
+  real_to_complex_kernel<<<nblk(count, 256), 256, 0, s>>>(count, x, Z);
+}
+
+}  // namespace nmg

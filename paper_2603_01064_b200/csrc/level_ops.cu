@@ -112,11 +112,12 @@ __global__ void __launch_bounds__(256) row_norms_kernel(int N, const double* __r
 
 __global__ void relres_kernel(int nrhs, int ntiles, const double* __restrict__ part,
                               const double* __restrict__ ynorm, double* __restrict__ relres, double tol,
-                              uint8_t* __restrict__ active) {
+                              uint8_t* __restrict__ active, int rows_per_rhs) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= nrhs) return;
   double s = 0.0;
-  for (int t = 0; t < ntiles; ++t) s += part[(int64_t)b * ntiles + t];
+  const int64_t cnt = (int64_t)ntiles * rows_per_rhs;
+  for (int64_t t = 0; t < cnt; ++t) s += part[(int64_t)b * cnt + t];
   const double yn = ynorm[b];
   // y = 0: converged at x = 0; a non-finite ||y|| or residual propagates as NaN/Inf
   const double rr = (yn > 0.0) ? sqrt(s) / yn : (yn == 0.0 && s == 0.0 ? 0.0 : sqrt(s) / yn);
@@ -174,8 +175,8 @@ void row_norms_f64(int nrhs, int N, const double* y, int64_t ldy, double* out, c
 }
 
 void relres_finalize(int nrhs, int ntiles, const double* part, const double* ynorm, double* relres, double tol,
-                     uint8_t* active, cudaStream_t s) {
-  relres_kernel<<<nblk(nrhs, 128), 128, 0, s>>>(nrhs, ntiles, part, ynorm, relres, tol, active);
+                     uint8_t* active, cudaStream_t s, int rows_per_rhs) {
+  relres_kernel<<<nblk(nrhs, 128), 128, 0, s>>>(nrhs, ntiles, part, ynorm, relres, tol, active, rows_per_rhs);
 }
 
 void update_x(int nrhs, int N, double* x, int64_t ldx, const float* d, int64_t ldd, const uint8_t* active,

@@ -203,6 +203,15 @@ struct nmg_hierarchy {
   std::vector<std::unique_ptr<DevBuf<float>>> sxh, sxl;  // X splits per level [max_rhs][n_l]
   std::vector<CUtensorMap> mXh, mXl;
   bool use_tc = true;
+  // 2D: A_l = B_l (x) C_l + alpha Q_l (x) Q_l; fp32 factors (SIMT), tf32 hi/lo (tcgen05)
+  std::vector<std::unique_ptr<DevBuf<float>>> B32, C32, B32h, B32l, C32h, C32l, Q32;
+  std::vector<int> qhb;                                  // Q_l half-bandwidth
+  std::vector<CUtensorMap> mBh, mBl, mCh, mCl, mTh, mTl;
+  std::vector<std::unique_ptr<DevBuf<float>>> tth, ttl;  // step-1 output (transposed blocks), hi/lo
+  DevBuf<float2> Z;                                      // filter spectrum workspace
+  DevBuf<double> snorm, spart;                           // smoother norms
+  DevBuf<double> T64;                                    // fp64 outer step-1 output
+  int rows_per_rhs = 1;
   // coarse Cholesky factor (row-major L and L^T)
   DevBuf<double> Lrow, Lcol;
   int nc = 0;
@@ -362,15 +371,129 @@ nmg_status cycle_level_1d(nmg_hierarchy* h, int l, int nrhs, cudaStream_t s) {
   return NMG_OK;
 }
 
+// ---------------------------------------------------------------- 2D level operations
+// D = Cin -/+ A_l X,  A_l X = Mat(hat A Vec X) = C_l X B_l^T + alpha Q_l X Q_l^T.
+// On the row-major [i2][i1] arrays (arr = X^T) this is B arr C^T + alpha Q arr Q^T:
+//   step 1: Tt = blockT(arr C^T)   (M = nrhs*n rows, transposed store within n x n blocks)
+//   stencil: D = Cin -/+ alpha Q arr Q^T
+//   step 2: D = D -/+ blockT(Tt B^T)
+nmg_status apply2d(nmg_hierarchy* h, int l, int nrhs, const float* X, const float* Cin, float* D, cudaStream_t s,
+                   bool negate = true) {
+  const int n = h->n[l];
+  const int M = nrhs * n;
+  const bool tc = h->use_tc && n % 16 == 0;
+  if (tc) {
+    { Prof p(h, NMG_K_MISC, s); split_tf32((int64_t)M * n, X, h->sxh[l]->p, h->sxl[l]->p, s); }
+    TcGemmArgs g{};
+    g.M = M; g.N = n; g.K = n; g.tblock = n; g.Dh = h->tth[l]->p; g.Dl = h->ttl[l]->p; g.negate = false;
+    { Prof p(h, NMG_K_GEMM32, s); tc_gemm(&h->mXh[l], &h->mXl[l], &h->mCh[l], &h->mCl[l], g, s); }
+  } else {
+    Gemm32Args g{};
+    g.M = M; g.N = n; g.K = n; g.batch = 1;
+    g.X = X; g.ldx = n; g.W = h->C32[l]->p; g.ldw = n; g.w_kmajor = true;
+    g.C = nullptr; g.D = h->tth[l]->p; g.ldd = n; g.negate = false; g.tblock = n;
+    { Prof p(h, NMG_K_GEMM32, s); gemm_f32(g, s); }
+  }
+  NMG_TRY(check_launch(h));
+  { Prof p(h, NMG_K_MISC, s);
+    qstencil(nrhs, n, h->qhb[l], negate ? (float)h->d.alpha : -(float)h->d.alpha, h->Q32[l]->p, X, Cin, D, s); }
+  NMG_TRY(check_launch(h));
+  if (tc) {
+    TcGemmArgs g{};
+    g.M = M; g.N = n; g.K = n; g.tblock = n; g.C = D; g.D = D; g.negate = negate;
+    { Prof p(h, NMG_K_GEMM32, s); tc_gemm(&h->mTh[l], &h->mTl[l], &h->mBh[l], &h->mBl[l], g, s); }
+  } else {
+    Gemm32Args g{};
+    g.M = M; g.N = n; g.K = n; g.batch = 1;
+    g.X = h->tth[l]->p; g.ldx = n; g.W = h->B32[l]->p; g.ldw = n; g.w_kmajor = true;
+    g.C = D; g.D = D; g.ldd = n; g.negate = negate; g.tblock = n;
+    { Prof p(h, NMG_K_GEMM32, s); gemm_f32(g, s); }
+  }
+  return check_launch(h);
+}
+
+// x = x* + hat F'(||b|| N(b/||b||))   (Alg 4)
+nmg_status smooth2d(nmg_hierarchy* h, int l, int nrhs, const float* b, float* x, bool accumulate, cudaStream_t s,
+                    bool normalize = true, bool filter = true) {
+  const int n = h->n[l];
+  const int64_t N = (int64_t)n * n;
+  const int chunks = (int)std::min<int64_t>(64, std::max<int64_t>(1, N / 4096));
+  if (normalize) {
+    { Prof p(h, NMG_K_SMOOTH, s); norms_f32(nrhs, N, b, h->spart.p, chunks, h->snorm.p, s); }
+    NMG_TRY(check_launch(h));
+  }
+  const bool filt = filter && h->d.level_filter != 0;
+  Cnn2dArgs a{};
+  a.n = n; a.nrhs = nrhs; a.C = h->arch.channels;
+  a.b = b; a.norms = normalize ? h->snorm.p : nullptr; a.params = h->W[l]->p;
+  a.Z = filt ? h->Z.p : nullptr; a.x = x; a.accumulate = accumulate;
+  { Prof p(h, NMG_K_SMOOTH, s); cnn2d(a, s); }
+  NMG_TRY(check_launch(h));
+  if (filt) {
+    { Prof p(h, NMG_K_SMOOTH, s); filter2d(nrhs, n, h->Z.p, h->tw.p, h->tw_n, x, accumulate, s); }
+    NMG_TRY(check_launch(h));
+  }
+  return NMG_OK;
+}
+
+nmg_status cycle_level_2d(nmg_hierarchy* h, int l, int nrhs, cudaStream_t s) {
+  const int n = h->n[l];
+  float* y = h->wy[l]->p;
+  float* x = h->wx[l]->p;
+  if (l == h->L - 1) {
+    { Prof p(h, NMG_K_COARSE, s); coarse_chol_solve(h->nc, nrhs, h->Lrow.p, h->Lcol.p, y, h->nc, x, h->nc, s); }
+    return check_launch(h);
+  }
+  float* r = h->wr[l]->p;
+  float* b = h->wb[l]->p;
+  const size_t bytes = sizeof(float) * (size_t)nrhs * n * n;
+  if (h->d.nu1 >= 1) {
+    NMG_TRY(smooth2d(h, l, nrhs, y, x, false, s));
+    for (int k = 1; k < h->d.nu1; ++k) {
+      NMG_TRY(apply2d(h, l, nrhs, x, y, b, s));
+      NMG_TRY(smooth2d(h, l, nrhs, b, x, true, s));
+    }
+    NMG_TRY(apply2d(h, l, nrhs, x, y, r, s));
+  } else {
+    NMG_CUDA(cudaMemsetAsync(x, 0, bytes, s));
+    NMG_CUDA(cudaMemcpyAsync(r, y, bytes, cudaMemcpyDeviceToDevice, s));
+  }
+  { Prof p(h, NMG_K_TRANSFER, s); restrict2d(nrhs, n, r, h->wy[l + 1]->p, s); }
+  NMG_TRY(check_launch(h));
+  NMG_TRY(cycle_level_2d(h, l + 1, nrhs, s));
+  { Prof p(h, NMG_K_TRANSFER, s); prolong_add2d(nrhs, n / 2, h->wx[l + 1]->p, x, s); }
+  NMG_TRY(check_launch(h));
+  for (int k = 0; k < h->d.nu2; ++k) {
+    NMG_TRY(apply2d(h, l, nrhs, x, y, b, s));
+    NMG_TRY(smooth2d(h, l, nrhs, b, x, true, s));
+  }
+  return NMG_OK;
+}
+
 nmg_status inner_cycle(nmg_hierarchy* h, int nrhs, cudaStream_t s) {
   if (h->d.dim == 1) return cycle_level_1d(h, 0, nrhs, s);
-  return fail(NMG_ERR_UNSUPPORTED, "2D cycle not implemented yet");
+  return cycle_level_2d(h, 0, nrhs, s);
 }
 
 // fp64 residual at level 1: r32 = y - A x -> wy[0]; optional r64; norm partials -> part
 nmg_status outer_residual(nmg_hierarchy* h, int nrhs, const double* y, const double* x, double* r64,
                           bool want_part, cudaStream_t s) {
-  if (h->d.dim != 1) return fail(NMG_ERR_UNSUPPORTED, "2D residual not implemented yet");
+  if (h->d.dim == 2) {
+    const int n = h->n[0];
+    Gemm64Args g{};
+    g.M = nrhs * n; g.N = n; g.K = n;
+    g.X = x; g.ldx = n; g.W = h->C64.p; g.ldw = n;
+    g.Y = nullptr; g.r32 = nullptr; g.r64 = h->T64.p; g.part = nullptr; g.negate = false; g.tblock = n;
+    { Prof p(h, NMG_K_GEMM64, s); gemm_f64(g, s); }
+    NMG_TRY(check_launch(h));
+    Gemm64Args q{};
+    q.M = nrhs * n; q.N = n; q.K = n;
+    q.X = h->T64.p; q.ldx = n; q.W = h->B64.p; q.ldw = n;
+    q.Y = y; q.r32 = h->wy[0]->p; q.r64 = r64; q.part = want_part ? h->part.p : nullptr;
+    q.negate = true; q.tblock = n; q.ax = x; q.alpha = h->d.alpha;
+    { Prof p(h, NMG_K_GEMM64, s); gemm_f64(q, s); }
+    return check_launch(h);
+  }
   Gemm64Args g{};
   const int n = h->n[0];
   g.M = nrhs; g.N = n; g.K = n;
@@ -400,11 +523,53 @@ nmg_status outer_step(nmg_hierarchy* h, int nrhs, const double* y, double* x, do
                       cudaStream_t s) {
   const int64_t N = h->N[0];
   NMG_TRY(outer_residual(h, nrhs, y, x, nullptr, true, s));
-  { Prof p(h, NMG_K_MISC, s); relres_finalize(nrhs, h->ntiles, h->part.p, h->ynorm.p, h->relres.p, tol, h->active.p, s); }
+  { Prof p(h, NMG_K_MISC, s); relres_finalize(nrhs, h->ntiles, h->part.p, h->ynorm.p, h->relres.p, tol, h->active.p, s, h->rows_per_rhs); }
   NMG_TRY(check_launch(h));
   NMG_TRY(inner_cycle(h, nrhs, s));
   { Prof p(h, NMG_K_MISC, s); update_x(nrhs, (int)N, x, N, h->wx[0]->p, N, use_active ? h->active.p : nullptr, s); }
   return check_launch(h);
+}
+
+nmg_status debug_2d(nmg_hierarchy* h, int l, int op, int nrhs, const float* fin, float* fout, cudaStream_t s) {
+  const int n = h->n[l];
+  const bool smoothed = l < h->L - 1;
+  const size_t bytes = sizeof(float) * (size_t)nrhs * n * n;
+  switch (op) {
+    case NMG_OP_APPLY:
+    case NMG_OP_RESIDUAL:
+      if (!smoothed) return fail(NMG_ERR_INVALID_ARG, "no fp32 operator stored at the coarsest level");
+      return apply2d(h, l, nrhs, fin, op == NMG_OP_RESIDUAL ? fout : nullptr, fout, s, op == NMG_OP_RESIDUAL);
+    case NMG_OP_RESTRICT:
+      if (!smoothed) return fail(NMG_ERR_INVALID_ARG, "no coarser level");
+      { Prof p(h, NMG_K_TRANSFER, s); restrict2d(nrhs, n, fin, fout, s); }
+      return check_launch(h);
+    case NMG_OP_PROLONG:
+      if (!smoothed) return fail(NMG_ERR_INVALID_ARG, "no coarser level");
+      { Prof p(h, NMG_K_TRANSFER, s); prolong_add2d(nrhs, n / 2, fin, fout, s); }
+      return check_launch(h);
+    case NMG_OP_FILTER:
+      if (!smoothed) return fail(NMG_ERR_INVALID_ARG, "no filter at the coarsest level");
+      { Prof p(h, NMG_K_SMOOTH, s); real_to_complex((int64_t)nrhs * n * n, fin, h->Z.p, s); }
+      { Prof p(h, NMG_K_SMOOTH, s); filter2d(nrhs, n, h->Z.p, h->tw.p, h->tw_n, fout, false, s); }
+      return check_launch(h);
+    case NMG_OP_CNN:
+    case NMG_OP_SMOOTH:
+      if (!smoothed || !h->w_loaded[l]) return fail(NMG_ERR_NO_WEIGHTS, "no smoother at level %d", l + 1);
+      return smooth2d(h, l, nrhs, fin, fout, op == NMG_OP_SMOOTH, s, op == NMG_OP_SMOOTH, op == NMG_OP_SMOOTH);
+    case NMG_OP_COARSE:
+      if (smoothed) return fail(NMG_ERR_INVALID_ARG, "COARSE needs level == L");
+      { Prof p(h, NMG_K_COARSE, s); coarse_chol_solve(h->nc, nrhs, h->Lrow.p, h->Lcol.p, fin, h->nc, fout, h->nc, s); }
+      return check_launch(h);
+    case NMG_OP_CYCLE0:
+      for (int q = l; q < h->L - 1; ++q)
+        if (!h->w_loaded[q]) return fail(NMG_ERR_NO_WEIGHTS, "level %d has no smoother", q + 1);
+      NMG_CUDA(cudaMemcpyAsync(h->wy[l]->p, fin, bytes, cudaMemcpyDeviceToDevice, s));
+      NMG_TRY(cycle_level_2d(h, l, nrhs, s));
+      NMG_CUDA(cudaMemcpyAsync(fout, h->wx[l]->p, bytes, cudaMemcpyDeviceToDevice, s));
+      return NMG_OK;
+    default:
+      return fail(NMG_ERR_INVALID_ARG, "unknown op %d", op);
+  }
 }
 
 }  // namespace
@@ -486,6 +651,26 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
     NMG_TRY(h->C64.upload(C.data(), nn));
     for (int l = 0; l < h->L - 1; ++l) {
       const int nl = h->n[l];
+      const size_t nn2 = (size_t)nl * nl;
+      auto up = [&](std::vector<std::unique_ptr<DevBuf<float>>>& v, const float* src) -> nmg_status {
+        v.emplace_back(new DevBuf<float>());
+        return v.back()->upload(src, nn2);
+      };
+      NMG_TRY(up(h->B32, to_f32(B).data()));
+      NMG_TRY(up(h->C32, to_f32(C).data()));
+      NMG_TRY(up(h->Q32, to_f32(Q).data()));
+      std::vector<float> hi, lo;
+      split_host(B, hi, lo);
+      NMG_TRY(up(h->B32h, hi.data()));
+      NMG_TRY(up(h->B32l, lo.data()));
+      split_host(C, hi, lo);
+      NMG_TRY(up(h->C32h, hi.data()));
+      NMG_TRY(up(h->C32l, lo.data()));
+      int hb = 0;
+      for (int i = 0; i < nl; ++i)
+        for (int j = 0; j < nl; ++j)
+          if (Q[(size_t)i * nl + j] != 0.0) hb = std::max(hb, std::abs(i - j));
+      h->qhb.push_back(hb);
       std::vector<double> t;
       host_galerkin(B, nl, t); B.swap(t);
       host_galerkin(C, nl, t); C.swap(t);
@@ -557,8 +742,34 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
       }
     }
   }
-  h->ntiles = gemm_f64_ntiles((int)h->N[0]);
-  NMG_TRY(h->part.alloc(B * h->ntiles));
+  if (d.dim == 2) {
+    h->mBh.resize(h->L); h->mBl.resize(h->L); h->mCh.resize(h->L); h->mCl.resize(h->L);
+    h->mTh.resize(h->L); h->mTl.resize(h->L); h->mXh.resize(h->L); h->mXl.resize(h->L);
+    for (int l = 0; l < h->L; ++l) {
+      const int nl = h->n[l];
+      for (auto* v : {&h->sxh, &h->sxl, &h->tth, &h->ttl}) {
+        v->emplace_back(new DevBuf<float>());
+        if (l < h->L - 1) NMG_TRY(v->back()->alloc(B * (size_t)nl * nl));
+      }
+      if (l >= h->L - 1 || nl % 16 != 0) continue;
+      const int64_t rows = (int64_t)B * nl;
+      NMG_TRY(make_map(&h->mXh[l], h->sxh[l]->p, rows, nl, tc_gemm_block_m()));
+      NMG_TRY(make_map(&h->mXl[l], h->sxl[l]->p, rows, nl, tc_gemm_block_m()));
+      NMG_TRY(make_map(&h->mTh[l], h->tth[l]->p, rows, nl, tc_gemm_block_m()));
+      NMG_TRY(make_map(&h->mTl[l], h->ttl[l]->p, rows, nl, tc_gemm_block_m()));
+      NMG_TRY(make_map(&h->mBh[l], h->B32h[l]->p, nl, nl, tc_gemm_block_n()));
+      NMG_TRY(make_map(&h->mBl[l], h->B32l[l]->p, nl, nl, tc_gemm_block_n()));
+      NMG_TRY(make_map(&h->mCh[l], h->C32h[l]->p, nl, nl, tc_gemm_block_n()));
+      NMG_TRY(make_map(&h->mCl[l], h->C32l[l]->p, nl, nl, tc_gemm_block_n()));
+    }
+    NMG_TRY(h->Z.alloc(B * (size_t)h->N[0]));
+    NMG_TRY(h->snorm.alloc(B));
+    NMG_TRY(h->spart.alloc(B * 64));
+    NMG_TRY(h->T64.alloc(B * (size_t)h->N[0]));
+    h->rows_per_rhs = n;
+  }
+  h->ntiles = gemm_f64_ntiles(d.dim == 1 ? (int)h->N[0] : n);
+  NMG_TRY(h->part.alloc(B * h->ntiles * (size_t)h->rows_per_rhs));
   NMG_TRY(h->ynorm.alloc(B));
   NMG_TRY(h->relres.alloc(B));
   NMG_TRY(h->active.alloc(B));
@@ -588,7 +799,20 @@ nmg_status nmg_load_smoother_weights(nmg_hierarchy* h, int32_t level, const nmg_
   }
   if (n_params != want) return fail(NMG_ERR_SHAPE, "expected %zu parameters, got %zu", want, n_params);
   NMG_CUDA(cudaSetDevice(h->d.device));
-  NMG_TRY(h->W[level - 1]->upload(params, n_params));
+  if (h->d.dim == 2) {
+    // device layout: hidden-layer weights transposed to [c][t2][t1][o] (see cnn2d_kernel)
+    std::vector<float> dev(params, params + n_params);
+    size_t off = (size_t)C * 9 + C;                        // after w0, b0
+    for (int layer = 1; layer <= 2; ++layer) {
+      for (int o = 0; o < C; ++o)
+        for (int c = 0; c < C; ++c)
+          for (int t = 0; t < 9; ++t) dev[off + ((size_t)c * 9 + t) * C + o] = params[off + ((size_t)o * C + c) * 9 + t];
+      off += (size_t)C * C * 9 + C;
+    }
+    NMG_TRY(h->W[level - 1]->upload(dev.data(), n_params));
+  } else {
+    NMG_TRY(h->W[level - 1]->upload(params, n_params));
+  }
   h->w_loaded[level - 1] = 1;
   h->arch = *arch;
   return NMG_OK;
@@ -606,7 +830,7 @@ nmg_status nmg_residual(nmg_hierarchy* h, int32_t nrhs, const double* y, const d
   NMG_TRY(outer_residual(h, nrhs, y, x, r, relres != nullptr, s));
   if (relres) {
     row_norms_f64(nrhs, (int)h->N[0], y, h->N[0], h->ynorm.p, s);
-    relres_finalize(nrhs, h->ntiles, h->part.p, h->ynorm.p, relres, -1.0, nullptr, s);
+    relres_finalize(nrhs, h->ntiles, h->part.p, h->ynorm.p, relres, -1.0, nullptr, s, h->rows_per_rhs);
     h->launches += 2;
   }
   return check_launch(h);
@@ -642,7 +866,7 @@ nmg_status nmg_solve(nmg_hierarchy* h, int32_t nrhs, const double* y, double* x,
   NMG_CUDA(cudaEventRecord(e0, s));
   row_norms_f64(nrhs, (int)N, y, N, h->ynorm.p, s);
   NMG_TRY(outer_residual(h, nrhs, y, x, nullptr, true, s));
-  relres_finalize(nrhs, h->ntiles, h->part.p, h->ynorm.p, h->relres.p, tol, h->active.p, s);
+  relres_finalize(nrhs, h->ntiles, h->part.p, h->ynorm.p, h->relres.p, tol, h->active.p, s, h->rows_per_rhs);
   h->launches += 2;
   NMG_TRY(check_launch(h));
   nmg_status st = NMG_OK;
@@ -668,7 +892,7 @@ nmg_status nmg_solve(nmg_hierarchy* h, int32_t nrhs, const double* y, double* x,
     NMG_TRY(check_launch(h));
     for (int b = 0; b < nrhs; ++b) if (act[b]) cyc[b] = tau + 1;
     NMG_TRY(outer_residual(h, nrhs, y, x, nullptr, true, s));
-    relres_finalize(nrhs, h->ntiles, h->part.p, h->ynorm.p, h->relres.p, tol, h->active.p, s);
+    relres_finalize(nrhs, h->ntiles, h->part.p, h->ynorm.p, h->relres.p, tol, h->active.p, s, h->rows_per_rhs);
     h->launches++;
     NMG_TRY(check_launch(h));
   }
@@ -724,7 +948,7 @@ nmg_status nmg_debug_level_op(nmg_hierarchy* h, int32_t level, int32_t op, int32
   const int l = level - 1;
   const float* fin = (const float*)in;
   float* fout = (float*)out;
-  if (h->d.dim != 1) return fail(NMG_ERR_UNSUPPORTED, "2D debug ops not implemented yet");
+  if (h->d.dim == 2) return debug_2d(h, l, op, nrhs, fin, fout, s);
   const int n = h->n[l];
   const bool smoothed = l < h->L - 1;
   switch (op) {

@@ -1,0 +1,170 @@
+"""GPU parity of the 2D path (configs 2, 3, 4; Alg 4) against the fp64 oracle."""
+import numpy as np
+import pytest
+
+import nmg_inputs as ni
+from tests._setup import gpu_hierarchy, history_close, oracle_hierarchy, rel_l2, weights_for
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2603_01064_b200 as nmg  # noqa: E402
+from oracle import nmg_oracle as O  # noqa: E402
+
+DEV = torch.device("cuda:0")
+# small 2D cases the oracle finishes in seconds: several tiles, a ragged tile edge (n=48 is
+# not a power of two, so use n = 64 with 16x16 CNN tiles and n = 32), B != C (gauss_cos)
+SMALL = ni.CONFIGS[2].replace(n=64, levels=3, nrhs=5)
+SMALL_COS = ni.CONFIGS[4].replace(n=64, levels=3, nrhs=3, sigma=0.05)
+
+
+def T(a, dtype=torch.float32):
+    return torch.tensor(np.ascontiguousarray(a), dtype=dtype, device=DEV)
+
+
+def _both(cfg, kind="seed", max_rhs=None):
+    f = ni.operator_factors(cfg)
+    W = weights_for(cfg, kind)
+    return f, W, oracle_hierarchy(cfg, f, W), gpu_hierarchy(cfg, f, W, max_rhs=max_rhs or max(cfg.nrhs, 16))
+
+
+@pytest.fixture(scope="module")
+def small():
+    return _both(SMALL, max_rhs=64 * 64)
+
+
+@pytest.fixture(scope="module")
+def small_cos():
+    return _both(SMALL_COS)
+
+
+def test_transfers_bit_exact_2d(small):
+    _, _, H, h = small
+    rng = np.random.default_rng(0)
+    for lvl in (1, 2):
+        n = SMALL.n >> (lvl - 1)
+        f = rng.integers(-64, 64, size=(3, n, n)).astype(np.float32)
+        out = torch.zeros(3, n // 2, n // 2, device=DEV)
+        h.debug_op(lvl, nmg.OP_RESTRICT, T(f), out)
+        assert np.array_equal(out.cpu().numpy().astype(np.float64), O.restrict(H, lvl - 1, f.astype(np.float64)))
+        c = rng.integers(-64, 64, size=(3, n // 2, n // 2)).astype(np.float32)
+        base = rng.integers(-64, 64, size=(3, n, n)).astype(np.float32)
+        acc = T(base)
+        h.debug_op(lvl, nmg.OP_PROLONG, T(c), acc)
+        want = base + O.interpolate(H, lvl - 1, c.astype(np.float64))
+        assert np.array_equal(acc.cpu().numpy().astype(np.float64), want)
+
+
+@pytest.mark.parametrize("which", ["small", "small_cos"])
+def test_apply_2d(which, small, small_cos):
+    cfg, (f, W, H, h) = (SMALL, small) if which == "small" else (SMALL_COS, small_cos)
+    rng = np.random.default_rng(1)
+    for lvl in range(1, cfg.levels):
+        n = cfg.n >> (lvl - 1)
+        x = rng.standard_normal((3, n, n)).astype(np.float32)
+        want = O.apply_A(H, lvl - 1, x.astype(np.float64))
+        out = torch.zeros(3, n, n, device=DEV)
+        h.debug_op(lvl, nmg.OP_APPLY, T(x), out)
+        assert rel_l2(out.cpu().numpy(), want) < 1e-5
+        y = rng.standard_normal((3, n, n)).astype(np.float32)
+        r = T(y)
+        h.debug_op(lvl, nmg.OP_RESIDUAL, T(x), r)
+        assert rel_l2(r.cpu().numpy(), y - want) < 1e-5
+
+
+def test_filter_2d(small):
+    _, _, H, h = small
+    rng = np.random.default_rng(2)
+    for lvl in (1, 2):
+        n = SMALL.n >> (lvl - 1)
+        x = rng.standard_normal((4, n, n)).astype(np.float32)
+        out = torch.zeros(4, n, n, device=DEV)
+        h.debug_op(lvl, nmg.OP_FILTER, T(x), out)
+        assert rel_l2(out.cpu().numpy(), O.level_filter(H, lvl - 1, x.astype(np.float64))) < 2e-6
+
+
+def test_cnn_and_smooth_2d(small):
+    _, _, H, h = small
+    rng = np.random.default_rng(3)
+    n = SMALL.n
+    u = rng.standard_normal((3, n, n)).astype(np.float32)
+    out = torch.zeros(3, n, n, device=DEV)
+    h.debug_op(1, nmg.OP_CNN, T(u), out)
+    assert rel_l2(out.cpu().numpy(), O.cnn_forward(H.weights[0], u.astype(np.float64))) < 1e-5
+    b = (2.5 * rng.standard_normal((3, n, n))).astype(np.float32)
+    x0 = rng.standard_normal((3, n, n)).astype(np.float32)
+    xs = T(x0)
+    h.debug_op(1, nmg.OP_SMOOTH, T(b), xs)
+    s = np.sqrt((b.astype(np.float64) ** 2).sum(axis=(1, 2)))[:, None, None]
+    hv = O.cnn_forward(H.weights[0], b / s) * s
+    want = x0 + O.level_filter(H, 0, hv)
+    assert rel_l2(xs.cpu().numpy() - x0, want - x0) < 1e-5
+
+
+def test_coarse_2d(small):
+    _, _, H, h = small
+    nc = SMALL.n >> (SMALL.levels - 1)
+    y = np.random.default_rng(4).standard_normal((6, nc, nc)).astype(np.float32)
+    out = torch.zeros(6, nc, nc, device=DEV)
+    h.debug_op(SMALL.levels, nmg.OP_COARSE, T(y), out)
+    assert rel_l2(out.cpu().numpy(), O.coarse_solve(H, y.astype(np.float64))) < 1e-6
+
+
+@pytest.mark.parametrize("which", ["small", "small_cos"])
+def test_outer_residual_2d(which, small, small_cos):
+    cfg, (f, W, H, h) = (SMALL, small) if which == "small" else (SMALL_COS, small_cos)
+    rng = np.random.default_rng(5)
+    y = rng.standard_normal((3, cfg.n, cfg.n))
+    x = rng.standard_normal((3, cfg.n, cfg.n))
+    r = torch.zeros(3, cfg.n, cfg.n, dtype=torch.float64, device=DEV)
+    rr = torch.zeros(3, dtype=torch.float64, device=DEV)
+    h.residual(T(y, torch.float64), T(x, torch.float64), r, rr)
+    want = y - O.apply_A(H, 0, x)
+    assert rel_l2(r.cpu().numpy(), want) < 1e-12
+    nrm = np.sqrt((want ** 2).sum(axis=(1, 2))) / np.sqrt((y ** 2).sum(axis=(1, 2)))
+    assert np.allclose(rr.cpu().numpy(), nrm, rtol=1e-12)
+
+
+@pytest.mark.parametrize("which", ["small", "small_cos"])
+def test_cycle_history_2d_small(which, small, small_cos):
+    cfg, (f, W, H, h) = (SMALL, small) if which == "small" else (SMALL_COS, small_cos)
+    y, _ = ni.make_rhs(cfg, f, cfg.alpha)
+    yd = T(y, torch.float64)
+    xd = torch.zeros_like(yd)
+    rep = h.solve(yd, xd, tol=1e-300, max_cycles=4)
+    orc = O.solve(H, y, tol=1e-300, max_cycles=4, freeze=False)
+    ok, err = history_close(rep["history"], orc.history)
+    assert ok, err
+
+
+def test_homogeneity_and_batch_invariance_2d(small):
+    f, _, _, h = small
+    y, _ = ni.make_rhs(SMALL, f, SMALL.alpha)
+    outs = []
+    for s in (1.0, 4.0):
+        yd = T(s * y, torch.float64)
+        xd = torch.zeros_like(yd)
+        h.vcycle(yd, xd)
+        outs.append(xd.cpu().numpy() / s)
+    assert np.array_equal(outs[0], outs[1])
+    y1 = T(y[2:3], torch.float64)
+    x1 = torch.zeros_like(y1)
+    h.vcycle(y1, x1)
+    assert np.array_equal(x1.cpu().numpy()[0], outs[0][2])
+
+
+@pytest.mark.parametrize("cfg_id,nrhs,cycles", [(2, 2, 2), (3, 1, 1), (4, 1, 1)])
+def test_full_size_configs_subset(cfg_id, nrhs, cycles):
+    """BASELINE configs 2-4 at full grid size on a seeded RHS subset: residual histories."""
+    cfg = ni.CONFIGS[cfg_id].replace(nrhs=nrhs)
+    f, W, H, h = _both(cfg, max_rhs=nrhs)
+    y, _ = ni.make_rhs(cfg, f, cfg.alpha, nrhs=nrhs)
+    yd = T(y, torch.float64)
+    xd = torch.zeros_like(yd)
+    rep = h.solve(yd, xd, tol=1e-300, max_cycles=cycles)
+    orc = O.solve(H, y, tol=1e-300, max_cycles=cycles, freeze=False)
+    ok, err = history_close(rep["history"], orc.history)
+    assert ok, err
