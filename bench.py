@@ -203,6 +203,7 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_2603_01064_b200 as nmg
+    from paper_2603_01064_b200.parallel import max_over_ranks, weak_shard
 
     if world > 1:
         torch.cuda.set_device(local)
@@ -215,7 +216,8 @@ def main():
     h = nmg.Hierarchy(1, cfg.n, cfg.levels, cfg.alpha, factors, nu1=cfg.nu1, nu2=cfg.nu2, max_rhs=B, device=local)
     for l, w in enumerate(W):
         h.load_weights(l + 1, ni.cnn_arch(cfg), w)
-    y_np, _ = ni.make_rhs(cfg, factors, cfg.alpha, nrhs=B, start=rank * B)
+    start, _ = weak_shard(B, rank)
+    y_np, _ = ni.make_rhs(cfg, factors, cfg.alpha, nrhs=B, start=start)
     y = torch.tensor(y_np, dtype=torch.float64, device=dev)
     x = torch.zeros_like(y)
     stream = torch.cuda.current_stream(dev)
@@ -241,11 +243,7 @@ def main():
         torch.cuda.synchronize(dev)
     barrier()
     launches = h.launch_count() - l0
-    ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(e0.elapsed_time(e1))
     value = world * B * args.steps / (ms / 1e3)
 
     # ---- per-kernel-class device times (CUDA events on the launching stream)
@@ -299,11 +297,7 @@ def main():
             h.vcycles_host(yhn, xhn, 1, stream=stream)
         f1.record(stream)
         torch.cuda.synchronize(dev)
-        ems = f0.elapsed_time(f1)
-        if world > 1:
-            t = torch.tensor([ems], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
+        ems = max_over_ranks(f0.elapsed_time(f1))
         e2e = {"value": world * B * args.steps / (ems / 1e3), "unit": "RHS*cycles/s",
                "h2d_bytes_per_step": 2 * 8 * B * cfg.n, "d2h_bytes_per_step": 8 * B * cfg.n}
 
@@ -316,7 +310,7 @@ def main():
                            device=local)
         for l, w in enumerate(ni.weights_lin(scfg)):
             hs.load_weights(l + 1, ni.cnn_arch(scfg), w)
-        ys_np, _ = ni.make_rhs(scfg, sf, scfg.alpha, nrhs=B, start=rank * B)
+        ys_np, _ = ni.make_rhs(scfg, sf, scfg.alpha, nrhs=B, start=start)
         ys = torch.tensor(ys_np, dtype=torch.float64, device=dev)
         xs = torch.zeros_like(ys)
         hs.solve(ys, xs, tol=1e-6, max_cycles=100, stream=stream)   # warm
@@ -324,11 +318,7 @@ def main():
         barrier()
         torch.cuda.synchronize(dev)
         rep = hs.solve(ys, xs, tol=1e-6, max_cycles=100, stream=stream)
-        sec = rep["wall_seconds"]
-        if world > 1:
-            t = torch.tensor([sec], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            sec = float(t.item())
+        sec = max_over_ranks(rep["wall_seconds"])
         solve = {"value": world * int(rep["converged"].sum()) / sec, "unit": "RHS solved/s (relres<=1e-6)",
                  "alpha": 1e-2, "weights": "W_lin stand-in", "cycles_max": int(rep["cycles"].max()),
                  "cycles_mean": float(rep["cycles"].mean()), "converged": int(rep["converged"].sum()),
