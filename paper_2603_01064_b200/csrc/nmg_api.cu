@@ -187,6 +187,20 @@ nmg_status make_map(CUtensorMap* m, const float* p, int64_t rows, int64_t cols, 
   return NMG_OK;
 }
 
+// padded activation tensor [rows][Wp][32] fp32 (rows = nrhs * Wp), box {16, 32, 10}, SWIZZLE_64B
+nmg_status make_act_map(CUtensorMap* m, const float* p, int64_t rows, int Wp) {
+  NMG_TRY(get_encoder());
+  cuuint64_t dims[3] = {32u, (cuuint64_t)Wp, (cuuint64_t)rows};
+  cuuint64_t strides[2] = {32u * sizeof(float), (cuuint64_t)Wp * 32u * sizeof(float)};
+  cuuint32_t box[3] = {16u, 32u, 10u};
+  cuuint32_t es[3] = {1u, 1u, 1u};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)p, dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(NMG_ERR_CUDA, "cuTensorMapEncodeTiled (3D) failed (%d)", (int)r);
+  return NMG_OK;
+}
+
 }  // namespace
 
 // ======================================================================= handle
@@ -212,6 +226,14 @@ struct nmg_hierarchy {
   DevBuf<double> snorm, spart;                           // smoother norms
   DevBuf<double> T64;                                    // fp64 outer step-1 output
   int rows_per_rhs = 1;
+  // 2D CNN hidden layers on tcgen05 (C = 32): padded hi/lo activations, A-operand weights
+  bool conv_tc = false;
+  int num_sms = 148;
+  int conv_chunk = 0;
+  DevBuf<float> act1h, act1l, act2h, act2l;
+  std::vector<std::unique_ptr<DevBuf<float>>> WA;        // per level: [layer 0 hi, lo, layer 1 hi, lo]
+  std::vector<CUtensorMap> mWAh, mWAl;                   // [level * 2 + layer]
+  std::vector<CUtensorMap> mA1h, mA1l, mA2h, mA2l;       // per level activation maps
   // coarse Cholesky factor (row-major L and L^T)
   DevBuf<double> Lrow, Lcol;
   int nc = 0;
@@ -423,6 +445,39 @@ nmg_status smooth2d(nmg_hierarchy* h, int l, int nrhs, const float* b, float* x,
     NMG_TRY(check_launch(h));
   }
   const bool filt = filter && h->d.level_filter != 0;
+  if (h->conv_tc && h->arch.channels == 32 && n >= 8) {
+    const int C = 32;
+    const float* P = h->W[l]->p;
+    const float* w0 = P;
+    const float* b0 = P + C * 9;
+    const float* b1 = b0 + C + C * C * 9;
+    const float* b2 = b1 + C + C * C * 9;
+    const float* w3 = b2 + C;
+    const float* b3 = w3 + C * 9;
+    const double* nrm = normalize ? h->snorm.p : nullptr;
+    for (int r0 = 0; r0 < nrhs; r0 += h->conv_chunk) {
+      const int cnt = std::min(h->conv_chunk, nrhs - r0);
+      const int64_t off = (int64_t)r0 * N;
+      { Prof p(h, NMG_K_SMOOTH, s);
+        conv_in(n, cnt, b + off, nrm ? nrm + r0 : nullptr, w0, b0, h->act1h.p, h->act1l.p, h->act2h.p, h->act2l.p, s); }
+      ConvTcArgs ca{};
+      ca.n = n; ca.nrhs = cnt; ca.bias = b1; ca.out_hi = h->act2h.p; ca.out_lo = h->act2l.p;
+      { Prof p(h, NMG_K_SMOOTH, s);
+        conv3x3_tc(&h->mWAh[l * 2], &h->mWAl[l * 2], &h->mA1h[l], &h->mA1l[l], ca, h->num_sms, s); }
+      ca.bias = b2; ca.out_hi = h->act1h.p; ca.out_lo = h->act1l.p;
+      { Prof p(h, NMG_K_SMOOTH, s);
+        conv3x3_tc(&h->mWAh[l * 2 + 1], &h->mWAl[l * 2 + 1], &h->mA2h[l], &h->mA2l[l], ca, h->num_sms, s); }
+      { Prof p(h, NMG_K_SMOOTH, s);
+        conv_out(n, cnt, h->act1h.p, h->act1l.p, nrm ? nrm + r0 : nullptr, w3, b3, filt ? h->Z.p + off : nullptr,
+                 x + off, accumulate, s); }
+      NMG_TRY(check_launch(h));
+    }
+    if (filt) {
+      { Prof p(h, NMG_K_SMOOTH, s); filter2d(nrhs, n, h->Z.p, h->tw.p, h->tw_n, x, accumulate, s); }
+      NMG_TRY(check_launch(h));
+    }
+    return NMG_OK;
+  }
   Cnn2dArgs a{};
   a.n = n; a.nrhs = nrhs; a.C = h->arch.channels;
   a.b = b; a.norms = normalize ? h->snorm.p : nullptr; a.params = h->W[l]->p;
@@ -767,6 +822,34 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
     NMG_TRY(h->spart.alloc(B * 64));
     NMG_TRY(h->T64.alloc(B * (size_t)h->N[0]));
     h->rows_per_rhs = n;
+    {
+      const char* env = std::getenv("NMG_CONV");
+      h->conv_tc = h->use_tc && !(env && std::string(env) == "ffma");
+      int sms = 0;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d.device);
+      h->num_sms = sms > 0 ? sms : 148;
+    }
+    if (h->conv_tc) {
+      const int64_t Wp = n + 2;
+      const int64_t per = Wp * Wp * 32;                         // floats per RHS per array
+      const int64_t budget = (int64_t)6 << 30;                  // floats over the 4 arrays (24 GiB)
+      h->conv_chunk = (int)std::max<int64_t>(1, std::min<int64_t>(B, budget / (4 * per)));
+      for (auto* buf : {&h->act1h, &h->act1l, &h->act2h, &h->act2l}) {
+        NMG_TRY(buf->alloc((size_t)h->conv_chunk * per));
+        NMG_CUDA(cudaMemset(buf->p, 0, sizeof(float) * buf->n));
+      }
+      h->mA1h.resize(h->L); h->mA1l.resize(h->L); h->mA2h.resize(h->L); h->mA2l.resize(h->L);
+      for (int l = 0; l < h->L - 1; ++l) {
+        const int Wl = h->n[l] + 2;
+        const int64_t rows = (int64_t)h->conv_chunk * Wl;
+        NMG_TRY(make_act_map(&h->mA1h[l], h->act1h.p, rows, Wl));
+        NMG_TRY(make_act_map(&h->mA1l[l], h->act1l.p, rows, Wl));
+        NMG_TRY(make_act_map(&h->mA2h[l], h->act2h.p, rows, Wl));
+        NMG_TRY(make_act_map(&h->mA2l[l], h->act2l.p, rows, Wl));
+      }
+      h->mWAh.resize(2 * h->L); h->mWAl.resize(2 * h->L);
+      for (int l = 0; l < h->L - 1; ++l) h->WA.emplace_back(new DevBuf<float>());
+    }
   }
   h->ntiles = gemm_f64_ntiles(d.dim == 1 ? (int)h->N[0] : n);
   NMG_TRY(h->part.alloc(B * h->ntiles * (size_t)h->rows_per_rhs));
@@ -810,6 +893,39 @@ nmg_status nmg_load_smoother_weights(nmg_hierarchy* h, int32_t level, const nmg_
       off += (size_t)C * C * 9 + C;
     }
     NMG_TRY(h->W[level - 1]->upload(dev.data(), n_params));
+    if (h->conv_tc && C == 32) {
+      // A operand of the tcgen05 conv: rows (t1, o) = 32 t1 + o (96 of 128), K blocks (t2, 16-ch chunk)
+      const int NCH = 2, AM = 128, BLK = AM * 16;
+      std::vector<double> A((size_t)2 * 3 * NCH * BLK, 0.0);
+      size_t woff = (size_t)C * 9 + C;
+      for (int layer = 0; layer < 2; ++layer) {
+        double* Al = A.data() + (size_t)layer * 3 * NCH * BLK;
+        for (int t2 = 0; t2 < 3; ++t2)
+          for (int ch = 0; ch < NCH; ++ch)
+            for (int t1 = 0; t1 < 3; ++t1)
+              for (int o = 0; o < C; ++o)
+                for (int k = 0; k < 16; ++k) {
+                  const int c = ch * 16 + k;
+                  Al[((size_t)(t2 * NCH + ch) * AM + t1 * 32 + o) * 16 + k] =
+                      params[woff + (((size_t)o * C + c) * 3 + t2) * 3 + t1];
+                }
+        woff += (size_t)C * C * 9 + C;
+      }
+      std::vector<float> hi, lo;
+      split_host(A, hi, lo);
+      const size_t half = (size_t)3 * NCH * BLK;
+      std::vector<float> packed(4 * half);
+      for (int layer = 0; layer < 2; ++layer) {
+        std::copy(hi.begin() + layer * half, hi.begin() + (layer + 1) * half, packed.begin() + (2 * layer) * half);
+        std::copy(lo.begin() + layer * half, lo.begin() + (layer + 1) * half, packed.begin() + (2 * layer + 1) * half);
+      }
+      DevBuf<float>& wa = *h->WA[level - 1];
+      NMG_TRY(wa.upload(packed.data(), packed.size()));
+      for (int layer = 0; layer < 2; ++layer) {
+        NMG_TRY(make_map(&h->mWAh[(level - 1) * 2 + layer], wa.p + (2 * layer) * half, 3 * NCH * AM, 16, AM));
+        NMG_TRY(make_map(&h->mWAl[(level - 1) * 2 + layer], wa.p + (2 * layer + 1) * half, 3 * NCH * AM, 16, AM));
+      }
+    }
   } else {
     NMG_TRY(h->W[level - 1]->upload(params, n_params));
   }
