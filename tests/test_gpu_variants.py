@@ -1,0 +1,116 @@
+"""GPU parity of cycle variants: nu2 = 0 (the paper's backslash cycle), filter off
+(Alg 2), a single-level hierarchy (exact solve), nu1 = 2 / nu2 = 2, nu1 = 0,
+the paper's own operator form G = K, and the SIMT/FFMA fallbacks."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import nmg_inputs as ni
+from tests._setup import gpu_hierarchy, history_close, oracle_hierarchy, rel_l2, weights_for
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import nmg_oracle as O  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def _run(cfg, kind="seed", level_filter=True, paper_form=False, cycles=4, tol=1e-300):
+    f = ni.operator_factors(cfg, paper_form=paper_form)
+    W = weights_for(cfg, kind)
+    H = oracle_hierarchy(cfg, f, W, level_filter=level_filter)
+    h = gpu_hierarchy(cfg, f, W, max_rhs=cfg.nrhs, level_filter=level_filter)
+    y, _ = ni.make_rhs(cfg, f, cfg.alpha)
+    yd = torch.tensor(y, dtype=torch.float64, device=DEV)
+    xd = torch.zeros_like(yd)
+    rep = h.solve(yd, xd, tol=tol, max_cycles=cycles)
+    orc = O.solve(H, y, tol=tol, max_cycles=cycles, freeze=tol > 1e-100)
+    return rep, orc, xd.cpu().numpy()
+
+
+@pytest.mark.parametrize("nu1,nu2", [(1, 0), (2, 2), (0, 1)])
+def test_smoothing_counts_1d(nu1, nu2):
+    cfg = ni.CONFIGS[0].replace(nu1=nu1, nu2=nu2)
+    rep, orc, _ = _run(cfg)
+    ok, err = history_close(rep["history"], orc.history)
+    assert ok, err
+
+
+def test_filter_off_1d():
+    rep, orc, _ = _run(ni.CONFIGS[0], level_filter=False)
+    ok, err = history_close(rep["history"], orc.history)
+    assert ok, err
+
+
+def test_single_level_is_exact_solve():
+    """L = 1: each cycle is the coarse Cholesky solve.  The inner cycle's fp32 output limits one
+    cycle to ~kappa * u_fp32; the fp64 correction-form outer iteration then refines it."""
+    cfg = ni.CONFIGS[0].replace(n=64, levels=1, nrhs=3)
+    rep, orc, x = _run(cfg, cycles=3)
+    assert rep["history"][:, 1].max() < 1e-4
+    assert rep["history"][:, 3].max() < 1e-10
+    assert rel_l2(x, orc.x) < 1e-8
+
+
+def test_paper_form_operator_1d():
+    """A = alpha I + K instead of the BASELINE K^T K + alpha I."""
+    cfg = ni.CONFIGS[0].replace(alpha=1e-2)
+    rep, orc, _ = _run(cfg, paper_form=True)
+    ok, err = history_close(rep["history"], orc.history)
+    assert ok, err
+
+
+def test_wlin_nu2_zero_converges_like_oracle():
+    cfg = ni.CONFIGS[0].replace(nu2=0)
+    rep, orc, _ = _run(cfg, kind="lin", cycles=60, tol=1e-6)
+    assert rep["converged"].all() and orc.converged.all()
+    assert np.abs(rep["cycles"] - orc.cycles).max() <= 1
+    ok, err = history_close(rep["history"], orc.history)
+    assert ok, err
+
+
+@pytest.mark.parametrize("nu1,nu2,filt", [(1, 0, True), (2, 1, False)])
+def test_variants_2d(nu1, nu2, filt):
+    cfg = ni.CONFIGS[2].replace(n=32, levels=2, nrhs=2, nu1=nu1, nu2=nu2)
+    rep, orc, _ = _run(cfg, level_filter=filt, cycles=3)
+    ok, err = history_close(rep["history"], orc.history)
+    assert ok, err
+
+
+def test_paper_form_operator_2d():
+    """hat A = alpha I (x) I + K (x) K."""
+    cfg = ni.CONFIGS[2].replace(n=32, levels=2, nrhs=2, alpha=1e-2)
+    rep, orc, _ = _run(cfg, paper_form=True, cycles=3)
+    ok, err = history_close(rep["history"], orc.history)
+    assert ok, err
+
+
+@pytest.mark.parametrize("env", ["NMG_GEMM=simt", "NMG_CONV=ffma"])
+def test_fallback_kernels_match(env, tmp_path):
+    """The SIMT GEMM / FFMA CNN kernels (used for shapes the tensor-core kernels do not
+    take) agree with the oracle too; run in a subprocess so the env switch applies."""
+    code = (
+        "import sys; sys.path.insert(0, '.');"
+        "import numpy as np, torch, nmg_inputs as ni;"
+        "from tests._setup import *; from oracle import nmg_oracle as O;"
+        "cfg = ni.CONFIGS[2].replace(n=64, levels=3, nrhs=2);"
+        "f = ni.operator_factors(cfg); W = weights_for(cfg, 'seed');"
+        "H = oracle_hierarchy(cfg, f, W); h = gpu_hierarchy(cfg, f, W, max_rhs=2);"
+        "y, _ = ni.make_rhs(cfg, f, cfg.alpha);"
+        "yd = torch.tensor(y, dtype=torch.float64, device='cuda'); xd = torch.zeros_like(yd);"
+        "rep = h.solve(yd, xd, tol=1e-300, max_cycles=3);"
+        "orc = O.solve(H, y, tol=1e-300, max_cycles=3, freeze=False);"
+        "ok, err = history_close(rep['history'], orc.history); print('ERR', err); assert ok"
+    )
+    k, v = env.split("=")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, k: v},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
