@@ -95,4 +95,50 @@ NMG_D float level_mask_1d(int k, int n) {
   return sqrtf((float)(2 * m) / (float)n);
 }
 
+// In-place level filter F'(h) = Re(IDFT_n(m' (.) DFT_n(h))) of a REAL row h[0..n) held in
+// shared memory, via one n/2-point complex FFT of z[k] = h[2k] + i h[2k+1] (the standard
+// real-input packing), the mask applied on the unpacked half spectrum, and one n/2-point
+// inverse FFT.  The row is processed alone (no pairing with other right-hand sides).
+// Block-cooperative; starts and ends with __syncthreads().
+NMG_D void real_level_filter(float* hbuf, int n, const float2* __restrict__ tw, int tw_n, int tid, int nthr) {
+  float2* z = reinterpret_cast<float2*>(hbuf);
+  const int m = n >> 1;
+  __syncthreads();
+  if (m >= 2) fft_dif_forward(z, m, tw, tw_n, tid, nthr);       // Z in bit-reversed order
+  const int lm = (m >= 2) ? 31 - __clz(m) : 0;
+  const int wstep = tw_n / n;                                     // W_n^k = tw[k * wstep]
+  // pair (k, m - k): unpack H, apply the mask, repack for the inverse
+  for (int k = tid; k <= (m >> 1); k += nthr) {
+    const int kk = (m - k) & (m - 1);                             // m - k (mod m)
+    const int pk = lm ? bitrev(k, lm) : 0, pkk = lm ? bitrev(kk, lm) : 0;
+    const float2 Zk = z[pk], Zc = z[pkk];
+    const float mk = sqrtf((float)(2 * k) / (float)n);            // mu[k],   k <= m
+    const float mc = sqrtf((float)(2 * (m - k)) / (float)n);      // mu[m-k]
+    const float sp = 0.5f * (mk + mc), sm = 0.5f * (mk - mc);
+    // k side: E = (Zk + conj Zc)/2, O = -i (Zk - conj Zc)/2
+    float2 E = make_float2(0.5f * (Zk.x + Zc.x), 0.5f * (Zk.y - Zc.y));
+    float2 O = make_float2(0.5f * (Zk.y + Zc.y), -0.5f * (Zk.x - Zc.x));
+    float2 W = __ldg(tw + k * wstep);                              // e^{-2 pi i k / n}
+    float2 WO = cmul(W, O);
+    float2 Eg = make_float2(sp * E.x + sm * WO.x, sp * E.y + sm * WO.y);
+    float2 WcE = cmulc(E, W);                                      // W^{-k} E
+    float2 Og = make_float2(sm * WcE.x + sp * O.x, sm * WcE.y + sp * O.y);
+    const float2 Zk2 = make_float2(Eg.x - Og.y, Eg.y + Og.x);      // Eg + i Og
+    if (kk != k) {
+      // m - k side (same formulas with k -> m - k, mu swapped)
+      float2 E2 = make_float2(0.5f * (Zc.x + Zk.x), 0.5f * (Zc.y - Zk.y));
+      float2 O2 = make_float2(0.5f * (Zc.y + Zk.y), -0.5f * (Zc.x - Zk.x));
+      float2 W2 = __ldg(tw + kk * wstep);
+      float2 WO2 = cmul(W2, O2);
+      float2 Eg2 = make_float2(sp * E2.x - sm * WO2.x, sp * E2.y - sm * WO2.y);
+      float2 WcE2 = cmulc(E2, W2);
+      float2 Og2 = make_float2(-sm * WcE2.x + sp * O2.x, -sm * WcE2.y + sp * O2.y);
+      z[pkk] = make_float2(Eg2.x - Og2.y, Eg2.y + Og2.x);
+    }
+    z[pk] = Zk2;
+  }
+  __syncthreads();
+  if (m >= 2) fft_dit_inverse(z, m, tw, tw_n, tid, nthr);        // natural order, unnormalised
+}
+
 }  // namespace nmg

@@ -8,6 +8,8 @@
 #include "fft.cuh"
 #include "kernels.h"
 
+#include <algorithm>
+
 namespace nmg {
 namespace {
 
@@ -29,8 +31,8 @@ __global__ void __launch_bounds__(NT, 2) smooth1d_kernel(Smooth1dArgs a) {
   const int rhs = blockIdx.x;
   float* w = sm;                                  // NPARAM (padded to 1480)
   float* u = w + 1480;                            // n + 2*UPAD
-  float2* cb = reinterpret_cast<float2*>(u + ((n + 2 * UPAD + 3) & ~3));   // n complex
-  float* a1 = reinterpret_cast<float*>(cb + n);   // C x S1
+  float* hb = u + ((n + 2 * UPAD + 3) & ~3);     // h row (n floats; n/2 complex for the filter)
+  float* a1 = hb + ((n + 3) & ~3);                 // C x S1
   float* a2 = a1 + C * S1;                        // C x S2
   __shared__ double red[32];
 
@@ -83,18 +85,23 @@ __global__ void __launch_bounds__(NT, 2) smooth1d_kernel(Smooth1dArgs a) {
   const int q3 = tid >> 2, cg = tid & 3;
 
   for (int t0 = 0; t0 < n; t0 += T3) {
-    // ---- layer 1: a1[c][jj], position p = t0 - 4 + jj, zero outside [0, n)
+    // ---- layer 1: a1[c][jj], position p = t0 - 4 + jj, zero outside [0, n); 4 positions per
+    //      thread (u window of 8 via two LDS.128, one STS.128)
 #pragma unroll 1
-    for (int jj = pg; jj < W1; jj += NT / C) {
-      const int p = t0 - 2 * HALO + jj;
-      float v = 0.f;
-      if (p >= 0 && p < n) {
+    for (int qd = pg; qd < W1 / 4; qd += NT / C) {
+      const float4* up = reinterpret_cast<const float4*>(u + t0 + 4 * qd);   // u[UPAD + p - 2], p = t0-4+4qd
+      const float4 ua = up[0], ub = up[1];
+      const float uw[8] = {ua.x, ua.y, ua.z, ua.w, ub.x, ub.y, ub.z, ub.w};
+      float r[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int p = t0 - 2 * HALO + 4 * qd + k;
         float acc = b0r;
 #pragma unroll
-        for (int t = 0; t < KS; ++t) acc = fmaf(w0r[t], u[UPAD + p + t - HALO], acc);
-        v = fmaxf(acc, 0.f);
+        for (int t = 0; t < KS; ++t) acc = fmaf(w0r[t], uw[k + t], acc);
+        r[k] = (p >= 0 && p < n) ? fmaxf(acc, 0.f) : 0.f;
       }
-      a1[o * S1 + jj] = v;
+      *reinterpret_cast<float4*>(a1 + o * S1 + 4 * qd) = make_float4(r[0], r[1], r[2], r[3]);
     }
     __syncthreads();
     // ---- layer 2: a2[o][jj2], position p = t0 - 2 + jj2
@@ -161,7 +168,7 @@ __global__ void __launch_bounds__(NT, 2) smooth1d_kernel(Smooth1dArgs a) {
           if (p < n) {
             const float hv = (acc[k] + b2[0]) * sf;
             if (a.filter) {
-              cb[p] = make_float2(hv, 0.f);
+              hb[p] = hv;
             } else {
               float* xrow = a.x + (int64_t)rhs * a.ldx;
               xrow[p] = a.accumulate ? xrow[p] + hv : hv;
@@ -174,21 +181,12 @@ __global__ void __launch_bounds__(NT, 2) smooth1d_kernel(Smooth1dArgs a) {
   }
   if (!a.filter) return;
 
-  // ---- level filter F'_l on the whole row: DIF forward (bit-reversed spectrum),
-  //      mask, DIT inverse (natural order) -- no permutation passes
-  const int log2n = 31 - __clz(n);
-  fft_dif_forward(cb, n, a.twiddle, a.tw_n, tid, NT);
-  for (int k = tid; k < n; k += NT) {
-    const float m = level_mask_1d(bitrev(k, log2n), n);
-    const float2 v = cb[k];
-    cb[k] = make_float2(v.x * m, v.y * m);
-  }
-  __syncthreads();
-  fft_dit_inverse(cb, n, a.twiddle, a.tw_n, tid, NT);
-  const float inv_n = 1.0f / (float)n;
+  // ---- level filter F'_l on the whole row (real-input FFT packing, see fft.cuh)
+  real_level_filter(hb, n, a.twiddle, a.tw_n, tid, NT);
+  const float scale = 2.0f / (float)n;             // 1/(n/2) of the half-length inverse
   float* xrow = a.x + (int64_t)rhs * a.ldx;
   for (int j = tid; j < n; j += NT) {
-    const float v = cb[j].x * inv_n;
+    const float v = hb[j] * scale;
     xrow[j] = a.accumulate ? xrow[j] + v : v;
   }
 }
@@ -197,25 +195,17 @@ __global__ void __launch_bounds__(NT, 2) smooth1d_kernel(Smooth1dArgs a) {
 __global__ void __launch_bounds__(NT) filter1d_kernel(int n, const float* in, float* out,
                                                       const float2* tw, int tw_n) {
   extern __shared__ __align__(16) float sm[];
-  float2* cb = reinterpret_cast<float2*>(sm);
   const int rhs = blockIdx.x, tid = threadIdx.x;
-  const int log2n = 31 - __clz(n);
-  for (int j = tid; j < n; j += NT) cb[bitrev(j, log2n)] = make_float2(in[(int64_t)rhs * n + j], 0.f);
-  __syncthreads();
-  fft_dit_forward(cb, n, tw, tw_n, tid, NT);
-  for (int k = tid; k < n; k += NT) {
-    const float m = level_mask_1d(k, n);
-    cb[k] = make_float2(cb[k].x * m, cb[k].y * m);
-  }
-  __syncthreads();
-  fft_dif_inverse(cb, n, tw, tw_n, tid, NT);
-  for (int j = tid; j < n; j += NT) out[(int64_t)rhs * n + j] = cb[bitrev(j, log2n)].x / (float)n;
+  for (int j = tid; j < n; j += NT) sm[j] = in[(int64_t)rhs * n + j];
+  real_level_filter(sm, n, tw, tw_n, tid, NT);
+  const float scale = 2.0f / (float)n;
+  for (int j = tid; j < n; j += NT) out[(int64_t)rhs * n + j] = sm[j] * scale;
 }
 
 }  // namespace
 
 size_t smooth1d_smem(int n) {
-  size_t f = 1480 + ((n + 2 * UPAD + 3) & ~3) + 2 * (size_t)n + C * S1 + C * S2;
+  size_t f = 1480 + ((n + 2 * UPAD + 3) & ~3) + ((n + 3) & ~3) + C * S1 + C * S2;
   return f * sizeof(float);
 }
 
@@ -226,7 +216,7 @@ void smooth1d(const Smooth1dArgs& a, cudaStream_t s) {
 }
 
 void filter1d(int n, int nrhs, const float* in, float* out, const float2* tw, int tw_n, cudaStream_t s) {
-  const size_t smem = 2 * (size_t)n * sizeof(float);
+  const size_t smem = (size_t)std::max(n, 4) * sizeof(float);
   cudaFuncSetAttribute(filter1d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   filter1d_kernel<<<nrhs, NT, smem, s>>>(n, in, out, tw, tw_n);
 }
