@@ -25,11 +25,12 @@ constexpr int NPARAM = C * 1 * KS + C + C * C * KS + C + 1 * C * KS + 1;   // 14
 constexpr int UPAD = 3 * HALO;                    // 6
 constexpr int Q3 = T3 / 4;                        // 63 layer-3 position quads
 
-__global__ void __launch_bounds__(NT, 2) smooth1d_kernel(Smooth1dArgs a) {
+__global__ void __launch_bounds__(NT, 3) smooth1d_kernel(Smooth1dArgs a) {
   extern __shared__ __align__(16) float sm[];
   const int n = a.n, tid = threadIdx.x;
   const int rhs = blockIdx.x;
-  float* w = sm;                                  // NPARAM (padded to 1480)
+  float* w = sm;                                  // NPARAM (padded to 1480); layer-2 block transposed
+  float* w1t = w + C * KS + C;                    // layer-2 weights as [c][t][o] (1280)
   float* u = w + 1480;                            // n + 2*UPAD
   float* hb = u + ((n + 2 * UPAD + 3) & ~3);     // h row (n floats; n/2 complex for the filter)
   float* a1 = hb + ((n + 3) & ~3);                 // C x S1
@@ -43,7 +44,12 @@ __global__ void __launch_bounds__(NT, 2) smooth1d_kernel(Smooth1dArgs a) {
   const float* w2 = b1 + C;            // [1][16][5]
   const float* b2 = w2 + C * KS;       // [1]
 
-  for (int i = tid; i < NPARAM; i += NT) w[i] = __ldg(a.params + i);
+  for (int i = tid; i < NPARAM; i += NT)
+    if (i < C * KS + C || i >= C * KS + C + C * C * KS) w[i] = __ldg(a.params + i);
+  for (int i = tid; i < C * C * KS; i += NT) {          // [o][c][t] -> [c][t][o]
+    const int oo = i / (C * KS), rem = i - oo * C * KS;   // rem = c * KS + t
+    w1t[rem * C + oo] = __ldg(a.params + C * KS + C + i);
+  }
   const float* brow = a.b + (int64_t)rhs * a.ldb;
   double ss = 0.0;
   for (int j = tid; j < n; j += NT) {
@@ -69,18 +75,18 @@ __global__ void __launch_bounds__(NT, 2) smooth1d_kernel(Smooth1dArgs a) {
   }
   const float sf = (float)s;
 
-  // layer-2 thread role: output channel o, position group pg (16 positions)
+  // layer-1 role: channel o = tid & 15, position quads pg + 16 k
   const int o = tid & (C - 1), pg = tid >> 4;
   __syncthreads();
-  float wr[C * KS];
-#pragma unroll
-  for (int i = 0; i < C * KS; ++i) wr[i] = w1[o * C * KS + i];
-  const float bo = b1[o];
-  // layer-1 role: channel c1 = tid & 15, positions (tid >> 4) + 16 k
   float w0r[KS];
 #pragma unroll
   for (int t = 0; t < KS; ++t) w0r[t] = w0[o * KS + t];
   const float b0r = b0[o];
+  // layer-2 role: output channels 4 og .. 4 og + 3, positions 4 pq .. 4 pq + 3
+  const int og = tid & 3, pq = tid >> 2;
+  float b1r[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) b1r[k] = b1[4 * og + k];
   // layer-3 role: position quad q3 = tid >> 2 (< 63), channel group cg = tid & 3 (4 channels)
   const int q3 = tid >> 2, cg = tid & 3;
 
@@ -104,38 +110,39 @@ __global__ void __launch_bounds__(NT, 2) smooth1d_kernel(Smooth1dArgs a) {
       *reinterpret_cast<float4*>(a1 + o * S1 + 4 * qd) = make_float4(r[0], r[1], r[2], r[3]);
     }
     __syncthreads();
-    // ---- layer 2: a2[o][jj2], position p = t0 - 2 + jj2
+    // ---- layer 2: a2[o][jj2], position p = t0 - 2 + jj2; thread: 4 channels x 4 positions,
+    //      weights broadcast from shared memory ([c][t][o] layout, one LDS.128 per tap)
     {
-      float acc[PP];
+      float acc[4][4];
 #pragma unroll
-      for (int i = 0; i < PP; ++i) acc[i] = bo;
-      const int base = pg * PP;
+      for (int k = 0; k < 4; ++k)
 #pragma unroll
+        for (int i = 0; i < 4; ++i) acc[k][i] = b1r[k];
+      const int base = 4 * pq;
+#pragma unroll 4
       for (int c = 0; c < C; ++c) {
-        float win[PP + 4];
         const float4* src = reinterpret_cast<const float4*>(a1 + c * S1 + base);
-#pragma unroll
-        for (int i = 0; i < (PP + 4) / 4; ++i) {
-          const float4 v = src[i];
-          win[4 * i] = v.x; win[4 * i + 1] = v.y; win[4 * i + 2] = v.z; win[4 * i + 3] = v.w;
-        }
+        const float4 v0 = src[0], v1 = src[1];
+        const float win[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
         for (int t = 0; t < KS; ++t) {
-          const float wv = wr[c * KS + t];
+          const float4 wv = *reinterpret_cast<const float4*>(w1t + (c * KS + t) * C + 4 * og);
+          const float ww[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
-          for (int i = 0; i < PP; ++i) acc[i] = fmaf(wv, win[i + t], acc[i]);
+          for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[k][i] = fmaf(ww[k], win[i + t], acc[k][i]);
         }
       }
 #pragma unroll
-      for (int i = 0; i < PP; i += 4) {
-        float4 v;
-        float* vv = reinterpret_cast<float*>(&v);
+      for (int k = 0; k < 4; ++k) {
+        float r[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int p = t0 - HALO + base + i + k;
-          vv[k] = (p >= 0 && p < n) ? fmaxf(acc[i + k], 0.f) : 0.f;
+        for (int i = 0; i < 4; ++i) {
+          const int p = t0 - HALO + base + i;
+          r[i] = (p >= 0 && p < n) ? fmaxf(acc[k][i], 0.f) : 0.f;
         }
-        *reinterpret_cast<float4*>(a2 + o * S2 + base + i) = v;
+        *reinterpret_cast<float4*>(a2 + (4 * og + k) * S2 + base) = make_float4(r[0], r[1], r[2], r[3]);
       }
     }
     __syncthreads();
