@@ -17,11 +17,15 @@
 namespace nmg {
 namespace {
 
-constexpr int TBM = 128, TBN = 256, TBK = 16, TSTAGES = 4, TNT = 128;
+constexpr int TBM = 128, TBK = 16, TSTAGES = 4, TNT = 128;
 constexpr int A_BYTES = TBM * TBK * 4;                    // 8 KB
-constexpr int B_BYTES = TBN * TBK * 4;                    // 16 KB
-constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;    // 48 KB
-constexpr int TC_SMEM = TSTAGES * STAGE_BYTES + 1024 /*barriers*/ + 1024 /*align slack*/;
+template <int TBN> struct TcCfg {
+  static constexpr int B_BYTES = TBN * TBK * 4;                     // 16 KB at N = 256
+  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;     // 48 KB at N = 256
+  static constexpr int SMEM = TSTAGES * STAGE_BYTES + 1024 /*barriers*/ + 1024 /*align slack*/;
+  static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TBN >> 3) << 17) |
+                                    ((uint32_t)(TBM >> 4) << 24);   // D f32, A/B tf32 K-major, M=128
+};
 
 NMG_D uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
@@ -67,18 +71,14 @@ NMG_D uint64_t umma_desc_sw64(uint32_t saddr) {
   return d;
 }
 
-// Instruction descriptor: D f32, A/B tf32, both K-major, N = 256, M = 128.
-constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TBN >> 3) << 17) |
-                            ((uint32_t)(TBM >> 4) << 24);
-
-NMG_D void umma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
+NMG_D void umma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate, uint32_t idesc) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "setp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
       "}\n" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(kIdesc), "r"(accumulate));
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
 }
 NMG_D void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
@@ -143,12 +143,15 @@ NMG_D void tc_store_chunk(const TcGemmArgs& a, const uint32_t (&v)[32], int m, i
     }
   }
 
+template <int TBN>
 __global__ void __launch_bounds__(TNT, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tXh, const __grid_constant__ CUtensorMap tXl,
                    const __grid_constant__ CUtensorMap tWh, const __grid_constant__ CUtensorMap tWl,
                    TcGemmArgs a) {
   extern __shared__ uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  constexpr int B_BYTES = TcCfg<TBN>::B_BYTES, STAGE_BYTES = TcCfg<TBN>::STAGE_BYTES;
+  constexpr uint32_t kIdesc = TcCfg<TBN>::IDESC;
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + TSTAGES * STAGE_BYTES);
   uint64_t* empty = full + TSTAGES;
   uint64_t* done = empty + TSTAGES;
@@ -205,9 +208,9 @@ __global__ void __launch_bounds__(TNT, 1)
           const uint64_t dxl = umma_desc_sw64(st + A_BYTES + ko);
           const uint64_t dwh = umma_desc_sw64(st + 2 * A_BYTES + ko);
           const uint64_t dwl = umma_desc_sw64(st + 2 * A_BYTES + B_BYTES + ko);
-          umma_tf32(tmem, dxh, dwh, (kt | ks) ? 1u : 0u);
-          umma_tf32(tmem, dxh, dwl, 1u);
-          umma_tf32(tmem, dxl, dwh, 1u);
+          umma_tf32(tmem, dxh, dwh, (kt | ks) ? 1u : 0u, kIdesc);
+          umma_tf32(tmem, dxh, dwl, 1u, kIdesc);
+          umma_tf32(tmem, dxl, dwh, 1u, kIdesc);
         }
         umma_commit(&empty[s]);      // slot reusable when these MMAs retire
       }
@@ -265,19 +268,25 @@ __global__ void split_tf32_kernel(int64_t count, const float* __restrict__ x, fl
 
 }  // namespace
 
-int tc_gemm_smem_bytes() { return TC_SMEM; }
-int tc_gemm_block_n() { return TBN; }
 int tc_gemm_block_m() { return TBM; }
 
 void tc_gemm(const CUtensorMap* xh, const CUtensorMap* xl, const CUtensorMap* wh, const CUtensorMap* wl,
-             const TcGemmArgs& a, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
-    attr = true;
+             const TcGemmArgs& a, cudaStream_t s, int bn) {
+  static bool attr256 = false, attr64 = false;
+  dim3 grid(ceil_div(a.N, bn), ceil_div(a.M, TBM));
+  if (bn == 256) {
+    if (!attr256) {
+      cudaFuncSetAttribute(tc_gemm_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<256>::SMEM);
+      attr256 = true;
+    }
+    tc_gemm_kernel<256><<<grid, TNT, TcCfg<256>::SMEM, s>>>(*xh, *xl, *wh, *wl, a);
+  } else {
+    if (!attr64) {
+      cudaFuncSetAttribute(tc_gemm_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<64>::SMEM);
+      attr64 = true;
+    }
+    tc_gemm_kernel<64><<<grid, TNT, TcCfg<64>::SMEM, s>>>(*xh, *xl, *wh, *wl, a);
   }
-  dim3 grid(ceil_div(a.N, TBN), ceil_div(a.M, TBM));
-  tc_gemm_kernel<<<grid, TNT, TC_SMEM, s>>>(*xh, *xl, *wh, *wl, a);
 }
 
 void split_tf32(int64_t count, const float* x, float* hi, float* lo, cudaStream_t s) {

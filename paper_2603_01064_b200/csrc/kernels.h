@@ -53,11 +53,15 @@ struct TcGemmArgs {
   int tblock = 0;                        // >0: transposed store within tblock x tblock blocks
   float* Dh = nullptr; float* Dl = nullptr;   // optional tf32 hi/lo split output (no C)
 };
+// bn = 256 or 64 (tile width; W maps must use box rows = bn)
 void tc_gemm(const CUtensorMap* xh, const CUtensorMap* xl, const CUtensorMap* wh, const CUtensorMap* wl,
-             const TcGemmArgs& a, cudaStream_t s);
-int tc_gemm_smem_bytes();
-int tc_gemm_block_n();
+             const TcGemmArgs& a, cudaStream_t s, int bn);
 int tc_gemm_block_m();
+// tile width heuristic: 256 when that already fills the GPU, else 64
+inline int tc_pick_bn(int M, int N, int num_sms) {
+  const int t256 = ((M + 127) / 128) * ((N + 255) / 256);
+  return (N >= 256 && t256 >= (num_sms * 4) / 5) ? 256 : 64;
+}
 void split_tf32(int64_t count, const float* x, float* hi, float* lo, cudaStream_t s);
 
 // ---- 1D smoother: norm -> CNN (3 layers, C=16, k=5) -> F' -> update ----------
@@ -70,6 +74,8 @@ struct Smooth1dArgs {
   bool normalize;                  // h = s N(b/s) (true) or h = N(b) (debug)
   bool filter;                     // apply F'_l
   bool accumulate;                 // x += (true) or x = (false)
+  float* xh = nullptr;             // optional: tf32 hi/lo split of the updated x (for the GEMM)
+  float* xl = nullptr;
 };
 void smooth1d(const Smooth1dArgs& a, cudaStream_t s);
 size_t smooth1d_smem(int n);
@@ -83,7 +89,8 @@ void filter1d(int n, int nrhs, const float* in, float* out, const float2* tw, in
 
 // ---- coarse solve: Cholesky factor applied by forward/back substitution ---------
 void coarse_chol_solve(int nc, int nrhs, const double* Lrow, const double* Lcol,
-                       const float* y, int64_t ldy, float* x, int64_t ldx, cudaStream_t s);
+                       const float* y, int64_t ldy, float* x, int64_t ldx, cudaStream_t s,
+                       float* xh = nullptr, float* xl = nullptr);
 
 // ---- outer (fp64) helpers --------------------------------------------------------
 void row_norms_f64(int nrhs, int N, const double* y, int64_t ldy, double* out, cudaStream_t s);

@@ -4,6 +4,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <algorithm>
+
 namespace nmg {
 namespace {
 
@@ -99,6 +101,77 @@ __global__ void __launch_bounds__(256) coarse_kernel(int nc, int nrhs, const dou
   }
 }
 
+// Same solve with the factor staged in shared memory (row stride nc + 1 doubles, so the
+// column walk of the forward sweep is conflict-free) and 1 / L_ii precomputed; nc <= 128.
+template <int NQ>
+__global__ void __launch_bounds__(256) coarse_smem_kernel(int nc, int nrhs, const double* __restrict__ Lrow,
+                                                          const float* __restrict__ y, int64_t ldy,
+                                                          float* __restrict__ x, int64_t ldx,
+                                                          float* __restrict__ xh, float* __restrict__ xl) {
+  extern __shared__ double Ls[];             // [nc][nc + 1], then dinv[nc]
+  const int S = nc + 1;
+  double* dinv = Ls + (size_t)nc * S;
+  for (int i = threadIdx.x; i < nc * nc; i += blockDim.x) {
+    const int r = i / nc, c = i - r * nc;
+    Ls[r * S + c] = Lrow[i];
+  }
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) dinv[i] = 1.0 / Lrow[(size_t)i * nc + i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  for (int b = blockIdx.x * wpb + (threadIdx.x >> 5); b < nrhs; b += gridDim.x * wpb) {
+    double z[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int j = q * 32 + lane;
+      z[q] = (j < nc) ? (double)y[(int64_t)b * ldy + j] : 0.0;
+    }
+#pragma unroll
+    for (int q0 = 0; q0 < NQ; ++q0) {
+      for (int il = 0; il < 32; ++il) {
+        const int i = q0 * 32 + il;
+        if (i >= nc) break;
+        const double zi = __shfl_sync(0xffffffffu, z[q0], il) * dinv[i];
+        if (lane == il) z[q0] = zi;
+#pragma unroll
+        for (int q = q0; q < NQ; ++q) {
+          const int j = q * 32 + lane;
+          if (j > i && j < nc) z[q] = fma(-Ls[j * S + i], zi, z[q]);
+        }
+      }
+    }
+#pragma unroll
+    for (int q0 = NQ - 1; q0 >= 0; --q0) {
+      for (int il = 31; il >= 0; --il) {
+        const int i = q0 * 32 + il;
+        if (i >= nc) continue;
+        const double xi = __shfl_sync(0xffffffffu, z[q0], il) * dinv[i];
+        if (lane == il) z[q0] = xi;
+#pragma unroll
+        for (int q = 0; q <= q0; ++q) {
+          const int j = q * 32 + lane;
+          if (j < i) z[q] = fma(-Ls[i * S + j], xi, z[q]);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int j = q * 32 + lane;
+      if (j < nc) {
+        const float v = (float)z[q];
+        x[(int64_t)b * ldx + j] = v;
+        if (xh) {
+          uint32_t hh, ll;
+          asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(hh) : "f"(v));
+          asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(ll) : "f"(v - __uint_as_float(hh)));
+          xh[(int64_t)b * ldx + j] = __uint_as_float(hh);
+          xl[(int64_t)b * ldx + j] = __uint_as_float(ll);
+        }
+      }
+    }
+  }
+}
+
 // ---- fp64 outer helpers ----------------------------------------------------------
 __global__ void __launch_bounds__(256) row_norms_kernel(int N, const double* __restrict__ y, int64_t ldy,
                                                         double* __restrict__ out) {
@@ -157,9 +230,23 @@ void prolong_add1d(int nrhs, int n_c, const float* c, int64_t ldc, float* f, int
 }
 
 void coarse_chol_solve(int nc, int nrhs, const double* Lrow, const double* Lcol, const float* y, int64_t ldy,
-                       float* x, int64_t ldx, cudaStream_t s) {
+                       float* x, int64_t ldx, cudaStream_t s, float* xh, float* xl) {
   const int grid = ceil_div(nrhs, 8);
   const int nq = ceil_div(nc, 32);
+  if (nc <= 128) {
+    const size_t smem = sizeof(double) * ((size_t)nc * (nc + 1) + nc);
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int g = std::min(grid, sms);
+#define NMG_COARSE_S(Q)                                                                                 \
+  case Q:                                                                                               \
+    cudaFuncSetAttribute(coarse_smem_kernel<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    coarse_smem_kernel<Q><<<g, 256, smem, s>>>(nc, nrhs, Lrow, y, ldy, x, ldx, xh, xl);                  \
+    return;
+    switch (nq) { NMG_COARSE_S(1) NMG_COARSE_S(2) NMG_COARSE_S(3) NMG_COARSE_S(4) default: break; }
+#undef NMG_COARSE_S
+  }
 #define NMG_COARSE(Q) \
   case Q: coarse_kernel<Q><<<grid, 256, 0, s>>>(nc, nrhs, Lrow, Lcol, y, ldy, x, ldx); break;
   switch (nq) {

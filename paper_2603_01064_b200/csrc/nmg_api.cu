@@ -213,14 +213,17 @@ struct nmg_hierarchy {
   DevBuf<double> A64, B64, C64;
   // per smoothed level (l < L-1) fp32 operators (SIMT path) and tf32 hi/lo splits (tcgen05)
   std::vector<std::unique_ptr<DevBuf<float>>> A32, AP32, A32h, A32l, AP32h, AP32l;
-  std::vector<CUtensorMap> mAh, mAl, mAPh, mAPl;        // W operand maps per level
+  std::vector<CUtensorMap> mAh, mAl, mAPh, mAPl;        // W operand maps per level (box 256)
+  std::vector<CUtensorMap> mAh64, mAl64, mAPh64, mAPl64; // same with box 64
   std::vector<std::unique_ptr<DevBuf<float>>> sxh, sxl;  // X splits per level [max_rhs][n_l]
   std::vector<CUtensorMap> mXh, mXl;
+  std::vector<char> split_fresh;                         // sxh/sxl[l] hold the split of wx[l]
   bool use_tc = true;
   // 2D: A_l = B_l (x) C_l + alpha Q_l (x) Q_l; fp32 factors (SIMT), tf32 hi/lo (tcgen05)
   std::vector<std::unique_ptr<DevBuf<float>>> B32, C32, B32h, B32l, C32h, C32l, Q32;
   std::vector<int> qhb;                                  // Q_l half-bandwidth
   std::vector<CUtensorMap> mBh, mBl, mCh, mCl, mTh, mTl;
+  std::vector<CUtensorMap> mBh64, mBl64, mCh64, mCl64;
   std::vector<std::unique_ptr<DevBuf<float>>> tth, ttl;  // step-1 output (transposed blocks), hi/lo
   DevBuf<float2> Z;                                      // filter spectrum workspace
   DevBuf<double> snorm, spart;                           // smoother norms
@@ -308,7 +311,10 @@ nmg_status smooth_level(nmg_hierarchy* h, int l, int nrhs, const float* b, float
   a.normalize = true;
   a.filter = h->d.level_filter != 0;
   a.accumulate = accumulate;
+  const bool split = x == h->wx[l]->p && h->sxh.size() > (size_t)l && h->sxh[l]->p;
+  if (split) { a.xh = h->sxh[l]->p; a.xl = h->sxl[l]->p; }
   { Prof p(h, NMG_K_SMOOTH, s); smooth1d(a, s); }
+  if (h->split_fresh.size() > (size_t)l) h->split_fresh[l] = split ? 1 : 0;
   return check_launch(h);
 }
 
@@ -337,15 +343,23 @@ nmg_status level_resid(nmg_hierarchy* h, int l, int which, int nrhs, const float
   const float* X = h->wx[lx]->p;
   const bool tc = h->use_tc && n % 16 == 0 && K % 16 == 0 && K >= 16;
   if (!tc) return resid_gemm(h, nrhs, n, K, X, which == 0 ? h->A32[l]->p : h->AP32[l]->p, C, D, s, negate);
-  { Prof p(h, NMG_K_MISC, s); split_tf32((int64_t)nrhs * K, X, h->sxh[lx]->p, h->sxl[lx]->p, s); }
-  NMG_TRY(check_launch(h));
+  if (!h->split_fresh[lx]) {
+    { Prof p(h, NMG_K_MISC, s); split_tf32((int64_t)nrhs * K, X, h->sxh[lx]->p, h->sxl[lx]->p, s); }
+    NMG_TRY(check_launch(h));
+    h->split_fresh[lx] = 1;
+  }
   TcGemmArgs g{};
   g.M = nrhs; g.N = n; g.K = K;
   g.C = C; g.ldc = n; g.D = D; g.ldd = n; g.negate = negate;
   {
     Prof p(h, NMG_K_GEMM32, s);
-    if (which == 0) tc_gemm(&h->mXh[lx], &h->mXl[lx], &h->mAh[l], &h->mAl[l], g, s);
-    else tc_gemm(&h->mXh[lx], &h->mXl[lx], &h->mAPh[l], &h->mAPl[l], g, s);
+    const int bn = tc_pick_bn(nrhs, n, h->num_sms);
+    if (which == 0)
+      tc_gemm(&h->mXh[lx], &h->mXl[lx], bn == 256 ? &h->mAh[l] : &h->mAh64[l], bn == 256 ? &h->mAl[l] : &h->mAl64[l],
+              g, s, bn);
+    else
+      tc_gemm(&h->mXh[lx], &h->mXl[lx], bn == 256 ? &h->mAPh[l] : &h->mAPh64[l],
+              bn == 256 ? &h->mAPl[l] : &h->mAPl64[l], g, s, bn);
   }
   return check_launch(h);
 }
@@ -356,7 +370,10 @@ nmg_status cycle_level_1d(nmg_hierarchy* h, int l, int nrhs, cudaStream_t s) {
   float* y = h->wy[l]->p;
   float* x = h->wx[l]->p;
   if (l == h->L - 1) {
-    { Prof p(h, NMG_K_COARSE, s); coarse_chol_solve(h->nc, nrhs, h->Lrow.p, h->Lcol.p, y, n, x, n, s); }
+    float* xh = (h->sxh.size() > (size_t)l && h->sxh[l]->p && h->nc <= 128) ? h->sxh[l]->p : nullptr;
+    { Prof p(h, NMG_K_COARSE, s);
+      coarse_chol_solve(h->nc, nrhs, h->Lrow.p, h->Lcol.p, y, n, x, n, s, xh, xh ? h->sxl[l]->p : nullptr); }
+    h->split_fresh[l] = xh ? 1 : 0;
     return check_launch(h);
   }
   float* r = h->wr[l]->p;
@@ -373,6 +390,7 @@ nmg_status cycle_level_1d(nmg_hierarchy* h, int l, int nrhs, cudaStream_t s) {
     rl = r;
   } else {
     NMG_CUDA(cudaMemsetAsync(x, 0, sizeof(float) * (size_t)nrhs * n, s));
+    h->split_fresh[l] = 0;
   }
   { Prof p(h, NMG_K_TRANSFER, s); restrict1d(nrhs, n, rl, n, h->wy[l + 1]->p, n / 2, s); }   // y_{l+1} = R r_l
   NMG_TRY(check_launch(h));
@@ -382,6 +400,7 @@ nmg_status cycle_level_1d(nmg_hierarchy* h, int l, int nrhs, cudaStream_t s) {
     NMG_TRY(level_resid(h, l, 1, nrhs, rl, b, s));                // b = r_l - (A P) e
   }
   { Prof p(h, NMG_K_TRANSFER, s); prolong_add1d(nrhs, n / 2, e, n / 2, x, n, s); }   // x += P e
+  h->split_fresh[l] = 0;
   NMG_TRY(check_launch(h));
   if (nu2 >= 1) {
     NMG_TRY(smooth_level(h, l, nrhs, b, x, true, s));
@@ -408,7 +427,10 @@ nmg_status apply2d(nmg_hierarchy* h, int l, int nrhs, const float* X, const floa
     { Prof p(h, NMG_K_MISC, s); split_tf32((int64_t)M * n, X, h->sxh[l]->p, h->sxl[l]->p, s); }
     TcGemmArgs g{};
     g.M = M; g.N = n; g.K = n; g.tblock = n; g.Dh = h->tth[l]->p; g.Dl = h->ttl[l]->p; g.negate = false;
-    { Prof p(h, NMG_K_GEMM32, s); tc_gemm(&h->mXh[l], &h->mXl[l], &h->mCh[l], &h->mCl[l], g, s); }
+    const int bn = tc_pick_bn(M, n, h->num_sms);
+    { Prof p(h, NMG_K_GEMM32, s);
+      tc_gemm(&h->mXh[l], &h->mXl[l], bn == 256 ? &h->mCh[l] : &h->mCh64[l], bn == 256 ? &h->mCl[l] : &h->mCl64[l],
+              g, s, bn); }
   } else {
     Gemm32Args g{};
     g.M = M; g.N = n; g.K = n; g.batch = 1;
@@ -423,7 +445,10 @@ nmg_status apply2d(nmg_hierarchy* h, int l, int nrhs, const float* X, const floa
   if (tc) {
     TcGemmArgs g{};
     g.M = M; g.N = n; g.K = n; g.tblock = n; g.C = D; g.D = D; g.negate = negate;
-    { Prof p(h, NMG_K_GEMM32, s); tc_gemm(&h->mTh[l], &h->mTl[l], &h->mBh[l], &h->mBl[l], g, s); }
+    const int bn = tc_pick_bn(M, n, h->num_sms);
+    { Prof p(h, NMG_K_GEMM32, s);
+      tc_gemm(&h->mTh[l], &h->mTl[l], bn == 256 ? &h->mBh[l] : &h->mBh64[l], bn == 256 ? &h->mBl[l] : &h->mBl64[l],
+              g, s, bn); }
   } else {
     Gemm32Args g{};
     g.M = M; g.N = n; g.K = n; g.batch = 1;
@@ -668,6 +693,11 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
     h->N.push_back(d.dim == 1 ? (int64_t)(d.n >> l) : (int64_t)(d.n >> l) * (d.n >> l));
   }
   h->nc = Nc;
+  {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d.device);
+    h->num_sms = sms > 0 ? sms : 148;
+  }
   const int n = d.n;
   const size_t nn = (size_t)n * n;
 
@@ -777,6 +807,7 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
   }
   if (d.dim == 1) {
     h->mAh.resize(h->L); h->mAl.resize(h->L); h->mAPh.resize(h->L); h->mAPl.resize(h->L);
+    h->mAh64.resize(h->L); h->mAl64.resize(h->L); h->mAPh64.resize(h->L); h->mAPl64.resize(h->L);
     h->mXh.resize(h->L); h->mXl.resize(h->L);
     for (int l = 0; l < h->L; ++l) {
       const int nl = h->n[l];
@@ -788,11 +819,15 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
       NMG_TRY(make_map(&h->mXh[l], h->sxh.back()->p, (int64_t)B, nl, tc_gemm_block_m()));
       NMG_TRY(make_map(&h->mXl[l], h->sxl.back()->p, (int64_t)B, nl, tc_gemm_block_m()));
       if (l < h->L - 1) {
-        NMG_TRY(make_map(&h->mAh[l], h->A32h[l]->p, nl, nl, tc_gemm_block_n()));
-        NMG_TRY(make_map(&h->mAl[l], h->A32l[l]->p, nl, nl, tc_gemm_block_n()));
+        NMG_TRY(make_map(&h->mAh[l], h->A32h[l]->p, nl, nl, 256));
+        NMG_TRY(make_map(&h->mAl[l], h->A32l[l]->p, nl, nl, 256));
+        NMG_TRY(make_map(&h->mAh64[l], h->A32h[l]->p, nl, nl, 64));
+        NMG_TRY(make_map(&h->mAl64[l], h->A32l[l]->p, nl, nl, 64));
         if ((nl / 2) % 16 == 0) {
-          NMG_TRY(make_map(&h->mAPh[l], h->AP32h[l]->p, nl, nl / 2, tc_gemm_block_n()));
-          NMG_TRY(make_map(&h->mAPl[l], h->AP32l[l]->p, nl, nl / 2, tc_gemm_block_n()));
+          NMG_TRY(make_map(&h->mAPh[l], h->AP32h[l]->p, nl, nl / 2, 256));
+          NMG_TRY(make_map(&h->mAPl[l], h->AP32l[l]->p, nl, nl / 2, 256));
+          NMG_TRY(make_map(&h->mAPh64[l], h->AP32h[l]->p, nl, nl / 2, 64));
+          NMG_TRY(make_map(&h->mAPl64[l], h->AP32l[l]->p, nl, nl / 2, 64));
         }
       }
     }
@@ -800,6 +835,7 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
   if (d.dim == 2) {
     h->mBh.resize(h->L); h->mBl.resize(h->L); h->mCh.resize(h->L); h->mCl.resize(h->L);
     h->mTh.resize(h->L); h->mTl.resize(h->L); h->mXh.resize(h->L); h->mXl.resize(h->L);
+    h->mBh64.resize(h->L); h->mBl64.resize(h->L); h->mCh64.resize(h->L); h->mCl64.resize(h->L);
     for (int l = 0; l < h->L; ++l) {
       const int nl = h->n[l];
       for (auto* v : {&h->sxh, &h->sxl, &h->tth, &h->ttl}) {
@@ -812,10 +848,14 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
       NMG_TRY(make_map(&h->mXl[l], h->sxl[l]->p, rows, nl, tc_gemm_block_m()));
       NMG_TRY(make_map(&h->mTh[l], h->tth[l]->p, rows, nl, tc_gemm_block_m()));
       NMG_TRY(make_map(&h->mTl[l], h->ttl[l]->p, rows, nl, tc_gemm_block_m()));
-      NMG_TRY(make_map(&h->mBh[l], h->B32h[l]->p, nl, nl, tc_gemm_block_n()));
-      NMG_TRY(make_map(&h->mBl[l], h->B32l[l]->p, nl, nl, tc_gemm_block_n()));
-      NMG_TRY(make_map(&h->mCh[l], h->C32h[l]->p, nl, nl, tc_gemm_block_n()));
-      NMG_TRY(make_map(&h->mCl[l], h->C32l[l]->p, nl, nl, tc_gemm_block_n()));
+      NMG_TRY(make_map(&h->mBh[l], h->B32h[l]->p, nl, nl, 256));
+      NMG_TRY(make_map(&h->mBl[l], h->B32l[l]->p, nl, nl, 256));
+      NMG_TRY(make_map(&h->mCh[l], h->C32h[l]->p, nl, nl, 256));
+      NMG_TRY(make_map(&h->mCl[l], h->C32l[l]->p, nl, nl, 256));
+      NMG_TRY(make_map(&h->mBh64[l], h->B32h[l]->p, nl, nl, 64));
+      NMG_TRY(make_map(&h->mBl64[l], h->B32l[l]->p, nl, nl, 64));
+      NMG_TRY(make_map(&h->mCh64[l], h->C32h[l]->p, nl, nl, 64));
+      NMG_TRY(make_map(&h->mCl64[l], h->C32l[l]->p, nl, nl, 64));
     }
     NMG_TRY(h->Z.alloc(B * (size_t)h->N[0]));
     NMG_TRY(h->snorm.alloc(B));
@@ -851,6 +891,7 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
       for (int l = 0; l < h->L - 1; ++l) h->WA.emplace_back(new DevBuf<float>());
     }
   }
+  h->split_fresh.assign(h->L, 0);
   h->ntiles = gemm_f64_ntiles(d.dim == 1 ? (int)h->N[0] : n);
   NMG_TRY(h->part.alloc(B * h->ntiles * (size_t)h->rows_per_rhs));
   NMG_TRY(h->ynorm.alloc(B));
@@ -1073,6 +1114,7 @@ nmg_status nmg_debug_level_op(nmg_hierarchy* h, int32_t level, int32_t op, int32
       if (!smoothed) return fail(NMG_ERR_INVALID_ARG, "no fp32 operator stored at the coarsest level");
       if (h->use_tc && n % 16 == 0) {
         NMG_CUDA(cudaMemcpyAsync(h->wx[l]->p, fin, sizeof(float) * (size_t)nrhs * n, cudaMemcpyDeviceToDevice, s));
+        h->split_fresh[l] = 0;
         NMG_TRY(level_resid(h, l, 0, nrhs, op == NMG_OP_RESIDUAL ? fout : nullptr, fout, s, op == NMG_OP_RESIDUAL));
         return NMG_OK;
       }

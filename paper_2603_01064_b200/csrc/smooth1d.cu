@@ -62,9 +62,17 @@ __global__ void __launch_bounds__(NT, 3) smooth1d_kernel(Smooth1dArgs a) {
   if (a.normalize) {
     s = sqrt(block_sum_f64(ss, red));
     if (s == 0.0) {                               // ||b|| = 0 => h = 0 (reading R10)
-      if (!a.accumulate) {
-        float* xrow = a.x + (int64_t)rhs * a.ldx;
-        for (int j = tid; j < n; j += NT) xrow[j] = 0.f;
+      float* xrow = a.x + (int64_t)rhs * a.ldx;
+      for (int j = tid; j < n; j += NT) {
+        const float xv = a.accumulate ? xrow[j] : 0.f;
+        xrow[j] = xv;
+        if (a.xh) {
+          uint32_t hh, ll;
+          asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(hh) : "f"(xv));
+          asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(ll) : "f"(xv - __uint_as_float(hh)));
+          a.xh[(int64_t)rhs * a.ldx + j] = __uint_as_float(hh);
+          a.xl[(int64_t)rhs * a.ldx + j] = __uint_as_float(ll);
+        }
       }
       return;
     }
@@ -178,7 +186,15 @@ __global__ void __launch_bounds__(NT, 3) smooth1d_kernel(Smooth1dArgs a) {
               hb[p] = hv;
             } else {
               float* xrow = a.x + (int64_t)rhs * a.ldx;
-              xrow[p] = a.accumulate ? xrow[p] + hv : hv;
+              const float xv = a.accumulate ? xrow[p] + hv : hv;
+              xrow[p] = xv;
+              if (a.xh) {
+                uint32_t hh, ll;
+                asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(hh) : "f"(xv));
+                asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(ll) : "f"(xv - __uint_as_float(hh)));
+                a.xh[(int64_t)rhs * a.ldx + p] = __uint_as_float(hh);
+                a.xl[(int64_t)rhs * a.ldx + p] = __uint_as_float(ll);
+              }
             }
           }
         }
@@ -194,7 +210,15 @@ __global__ void __launch_bounds__(NT, 3) smooth1d_kernel(Smooth1dArgs a) {
   float* xrow = a.x + (int64_t)rhs * a.ldx;
   for (int j = tid; j < n; j += NT) {
     const float v = hb[j] * scale;
-    xrow[j] = a.accumulate ? xrow[j] + v : v;
+    const float xv = a.accumulate ? xrow[j] + v : v;
+    xrow[j] = xv;
+    if (a.xh) {
+      uint32_t hh, ll;
+      asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(hh) : "f"(xv));
+      asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(ll) : "f"(xv - __uint_as_float(hh)));
+      a.xh[(int64_t)rhs * a.ldx + j] = __uint_as_float(hh);
+      a.xl[(int64_t)rhs * a.ldx + j] = __uint_as_float(ll);
+    }
   }
 }
 
