@@ -69,7 +69,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -154,7 +154,7 @@ def host_threads():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--alpha", type=float, default=1e-3)
@@ -258,24 +258,31 @@ def main():
     pk = peaks()
     dom = max(prof, key=lambda k: prof[k][0])
     dom_ms, dom_n = prof[dom]
-    avg_ms = dom_ms / max(dom_n, 1)
-    per_step_launches = dom_n / args.steps
+    step_ms = dom_ms / args.steps                       # all launches of the class in one step
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            traffic = json.load(fh).get(dom)            # ncu dram read+write bytes per step
+    except Exception:
+        pass
     if dom == "gemm64":
         peak = pk["bf16_tflops"] * FP64_NOMINAL_RATIO
-        achieved = counts["gemm64"] / (avg_ms * 1e-3) / 1e12
-        roof = {"kernel": "dgemm_resid (fp64 outer residual, DMMA)", "bound": "tensor", "unit": "TFLOP/s",
-                "peak_note": "measured bf16 x nominal fp64/bf16 ratio 45/2250"}
+        achieved = counts["gemm64"] / (step_ms * 1e-3) / 1e12
+        roof = {"kernel": "dgemm_resid_kernel (fp64 outer residual, DMMA)", "bound": "tensor", "unit": "TFLOP/s",
+                "peak_note": "FP64 tensor: measured bf16 x nominal fp64/bf16 ratio 45/2250"}
     elif dom == "gemm32":
-        peak = 148 * 128 * 2 * 1.965e9 / 1e12
-        achieved = counts["gemm32"] / (dom_ms / args.steps * 1e-3) / 1e12
-        roof = {"kernel": "sgemm (fp32 inner operator, all levels)", "bound": "alu", "unit": "TFLOP/s",
-                "peak_note": "FP32 FFMA 148 SM x 128 lanes x 2 x 1.965 GHz"}
+        peak = pk["bf16_tflops"] * TF32_NOMINAL_RATIO / 3.0
+        achieved = counts["gemm32"] / (step_ms * 1e-3) / 1e12
+        roof = {"kernel": "tc_gemm_kernel (3xTF32 tcgen05, all levels)", "bound": "tensor", "unit": "TFLOP/s",
+                "peak_note": "TF32 tensor (measured bf16 x 1.1/2.25) / 3 passes"}
     else:
         peak = 148 * 128 * 2 * 1.965e9 / 1e12
-        achieved = counts["smooth"] / (dom_ms / args.steps * 1e-3) / 1e12
-        roof = {"kernel": f"{dom} (per step)", "bound": "alu", "unit": "TFLOP/s",
-                "peak_note": "FP32 FFMA 148 SM x 128 lanes x 2 x 1.965 GHz"}
-    roof.update({"achieved": achieved, "peak": peak, "frac": achieved / peak, "traffic": None,
+        achieved = counts["smooth"] / (step_ms * 1e-3) / 1e12
+        roof = {"kernel": "smooth1d_kernel (norm + 3-layer CNN + level filter), all launches of a step",
+                "bound": "alu", "unit": "TFLOP/s",
+                "peak_note": "FP32 FFMA: 148 SM x 128 lanes x 2 FLOP x 1.965 GHz (CNN FLOPs only, 2880/point)"}
+    roof.update({"achieved": achieved, "peak": peak, "frac": achieved / peak, "traffic": traffic,
+                 "traffic_note": "ncu dram__bytes_read+write per step, profiles/traffic.json" if traffic else None,
                  "peak_source": pk["source"],
                  "share_of_step": dom_ms / tot_prof if tot_prof else None,
                  "classes_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
@@ -327,9 +334,9 @@ def main():
     # ---- CPU oracle baseline (rank 0, N = 1 only; bounded sample)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        rate, dt = oracle_rate(cfg, factors, W, y_np, 96, 2)
+        rate, dt = oracle_rate(cfg, factors, W, y_np, 128, 8)
         cpu = {"value": rate, "unit": "RHS*cycles/s", "cores": host_threads(), "kind": "oracle",
-               "sample": f"96 RHS x 2 cycles of the same workload ({dt:.1f} s)"}
+               "sample": f"128 RHS x 8 cycles of the same workload ({dt:.1f} s)"}
 
     if rank == 0:
         line = {"metric": "RHS*V-cycles/s (1D cfg1: fp64 residual + NMGF V-cycle + update per step)",

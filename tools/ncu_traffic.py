@@ -1,0 +1,50 @@
+#!/usr/bin/env python
+"""Aggregate an ncu CSV (metrics dram__bytes_read.sum, dram__bytes_write.sum, gpu__time_duration.sum)
+of `bench.py --steps 1` into per-kernel-class DRAM bytes of ONE step (the last `per_step` launches of
+the library) and write profiles/traffic.json.  Usage: ncu_traffic.py CSV PER_STEP_LAUNCHES OUT"""
+import collections
+import csv
+import json
+import sys
+
+CLASS = [("dgemm", "gemm64"), ("tc_gemm", "gemm32"), ("sgemm", "gemm32"), ("smooth1d", "smooth"),
+         ("cnn2d", "smooth"), ("conv", "smooth"), ("fft", "smooth"), ("sumsq", "smooth"),
+         ("restrict", "transfer"), ("prolong", "transfer"), ("coarse", "coarse")]
+
+
+def cls(name):
+    for key, c in CLASS:
+        if key in name:
+            return c
+    return "misc"
+
+
+def main(path, per_step, out):
+    rows = list(csv.reader(open(path)))
+    h = [r for r in rows if "Kernel Name" in r][0]
+    hi = rows.index(h)
+    ki, mi, vi, ui, ii = (h.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit", "ID"))
+    launches = collections.OrderedDict()
+    for r in rows[hi + 1:]:
+        if len(r) <= vi or "nmg::" not in r[ki]:
+            continue
+        v = float(r[vi].replace(",", ""))
+        u = r[ui]
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "nsecond": 1e-9,
+                 "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3}.get(u, 1)
+        launches.setdefault(r[ii], {"name": r[ki]})[r[mi]] = v * scale
+    last = list(launches.values())[-per_step:]
+    agg = collections.defaultdict(lambda: {"bytes": 0.0, "s": 0.0, "n": 0})
+    for L in last:
+        c = agg[cls(L["name"])]
+        c["bytes"] += L.get("dram__bytes_read.sum", 0) + L.get("dram__bytes_write.sum", 0)
+        c["s"] += L.get("gpu__time_duration.sum", 0)
+        c["n"] += 1
+    res = {k: v["bytes"] for k, v in agg.items()}
+    json.dump(res, open(out, "w"), indent=1)
+    for k, v in agg.items():
+        print(f"{k:9s} launches {v['n']:3d}  dram {v['bytes'] / 1e6:10.1f} MB  time {v['s'] * 1e3:8.3f} ms (cold, serialised)")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], int(sys.argv[2]), sys.argv[3])
