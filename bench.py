@@ -220,7 +220,8 @@ def main():
     y_np, _ = ni.make_rhs(cfg, factors, cfg.alpha, nrhs=B, start=start)
     y = torch.tensor(y_np, dtype=torch.float64, device=dev)
     x = torch.zeros_like(y)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)          # non-default stream: the library replays a CUDA graph
+    torch.cuda.set_stream(stream)
 
     def barrier():
         if world > 1:

@@ -239,9 +239,14 @@ void coarse_chol_solve(int nc, int nrhs, const double* Lrow, const double* Lcol,
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int g = std::min(grid, sms);
+    static bool attr[5] = {false, false, false, false, false};
+    const int full = (int)(sizeof(double) * ((size_t)128 * 129 + 128));
 #define NMG_COARSE_S(Q)                                                                                 \
   case Q:                                                                                               \
-    cudaFuncSetAttribute(coarse_smem_kernel<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    if (!attr[Q]) {                                                                                     \
+      cudaFuncSetAttribute(coarse_smem_kernel<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, full);    \
+      attr[Q] = true;                                                                                   \
+    }                                                                                                   \
     coarse_smem_kernel<Q><<<g, 256, smem, s>>>(nc, nrhs, Lrow, y, ldy, x, ldx, xh, xl);                  \
     return;
     switch (nq) { NMG_COARSE_S(1) NMG_COARSE_S(2) NMG_COARSE_S(3) NMG_COARSE_S(4) default: break; }

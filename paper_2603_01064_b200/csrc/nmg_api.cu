@@ -260,7 +260,16 @@ struct nmg_hierarchy {
   size_t ev_used = 0;
   struct Rec { int cls; cudaEvent_t a, b; };
   std::vector<Rec> recs;
-  ~nmg_hierarchy() { for (auto e : ev_pool) cudaEventDestroy(e); }
+  // CUDA graph of one nmg_vcycle (keyed by nrhs, buffers and stream)
+  bool use_graph = true;
+  int g_nrhs = -1, g_seen = 0;
+  const void* g_y = nullptr; void* g_x = nullptr; cudaStream_t g_s = nullptr;
+  cudaGraphExec_t g_exec = nullptr;
+  int64_t g_launches = 0;
+  ~nmg_hierarchy() {
+    for (auto e : ev_pool) cudaEventDestroy(e);
+    if (g_exec) cudaGraphExecDestroy(g_exec);
+  }
 };
 
 namespace {
@@ -804,6 +813,8 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
   {
     const char* env = std::getenv("NMG_GEMM");
     h->use_tc = !(env && std::string(env) == "simt");
+    const char* genv = std::getenv("NMG_GRAPH");
+    h->use_graph = !(genv && std::string(genv) == "0");
   }
   if (d.dim == 1) {
     h->mAh.resize(h->L); h->mAl.resize(h->L); h->mAPh.resize(h->L); h->mAPl.resize(h->L);
@@ -999,8 +1010,54 @@ nmg_status nmg_vcycle(nmg_hierarchy* h, int32_t nrhs, const double* y, double* x
   if (nrhs == 0) return NMG_OK;
   if (!y || !x) return fail(NMG_ERR_INVALID_ARG, "null y/x");
   cudaStream_t s = (cudaStream_t)stream;
-  { Prof p(h, NMG_K_MISC, s); row_norms_f64(nrhs, (int)h->N[0], y, h->N[0], h->ynorm.p, s); }
-  return outer_step(h, nrhs, y, x, -1.0, false, s);
+  auto body = [&]() -> nmg_status {
+    { Prof p(h, NMG_K_MISC, s); row_norms_f64(nrhs, (int)h->N[0], y, h->N[0], h->ynorm.p, s); }
+    return outer_step(h, nrhs, y, x, -1.0, false, s);
+  };
+  // CUDA graph: the first call with a given (nrhs, y, x, stream) runs eagerly, the second
+  // captures the whole cycle, later calls replay it (launch-latency bound small configs).
+  const bool key = h->g_nrhs == nrhs && h->g_y == y && h->g_x == x && h->g_s == s;
+  if (!h->use_graph || s == nullptr || h->prof_on) return body();
+  if (key && h->g_exec) {
+    NMG_CUDA(cudaGraphLaunch(h->g_exec, s));
+    h->launches += h->g_launches;
+    return NMG_OK;
+  }
+  if (!key) {
+    if (h->g_exec) { cudaGraphExecDestroy(h->g_exec); h->g_exec = nullptr; }
+    h->g_nrhs = nrhs; h->g_y = y; h->g_x = x; h->g_s = s; h->g_seen = 0;
+  }
+  if (h->g_seen++ == 0) return body();
+  const int64_t l0 = h->launches;
+  if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    h->use_graph = false;
+    return body();
+  }
+  nmg_status st = body();
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(s, &g);
+  if (st != NMG_OK || e != cudaSuccess || !g) {
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    h->use_graph = false;
+    h->launches = l0;
+    h->poisoned = false;
+    return body();
+  }
+  h->g_launches = h->launches - l0;
+  h->launches = l0;
+  e = cudaGraphInstantiate(&h->g_exec, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    h->g_exec = nullptr;
+    h->use_graph = false;
+    return body();
+  }
+  NMG_CUDA(cudaGraphLaunch(h->g_exec, s));
+  h->launches += h->g_launches;
+  return NMG_OK;
 }
 
 nmg_status nmg_solve(nmg_hierarchy* h, int32_t nrhs, const double* y, double* x, double tol, int32_t max_cycles,

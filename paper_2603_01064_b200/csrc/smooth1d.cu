@@ -242,7 +242,11 @@ size_t smooth1d_smem(int n) {
 
 void smooth1d(const Smooth1dArgs& a, cudaStream_t s) {
   const size_t smem = smooth1d_smem(a.n);
-  cudaFuncSetAttribute(smooth1d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(smooth1d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smooth1d_smem(8192));
+    attr = smooth1d_smem(8192);
+  }
   smooth1d_kernel<<<a.nrhs, NT, smem, s>>>(a);
 }
 

@@ -32,6 +32,8 @@ def main():
     reps = -(-B // pool.shape[0])
     y = torch.tensor(np.concatenate([pool] * reps)[:B], dtype=torch.float64, device="cuda")
     x = torch.zeros_like(y)
+    st = torch.cuda.Stream()
+    torch.cuda.set_stream(st)
     h.vcycle(y, x)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
