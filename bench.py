@@ -113,6 +113,15 @@ def algorithmic_counts(cfg, B):
     """Per-step algorithmic FLOPs / bytes per kernel class."""
     n = [cfg.n >> l for l in range(cfg.levels)]
     L = cfg.levels
+    if cfg.dim == 2:
+        # Kronecker pair: 2 GEMMs of 2 n^3 FLOP per RHS per apply; applies per level:
+        # pre residual + post residual (+ extra smoothing steps)
+        g64 = 4.0 * B * n[0] ** 3
+        g32 = sum(4.0 * B * n[l] ** 3 * (1 + cfg.nu2 + max(cfg.nu1 - 1, 0)) for l in range(L - 1))
+        C = cfg.channels
+        per_px = 2 * (9 * C + 2 * 9 * C * C + 9 * C)
+        sm = sum((cfg.nu1 + cfg.nu2) * B * n[l] ** 2 * per_px for l in range(L - 1))
+        return {"gemm64": g64, "gemm32": g32, "smooth": sm}
     g64 = 2.0 * B * n[0] * n[0]
     g32 = 0.0
     for l in range(L - 1):
@@ -154,7 +163,8 @@ def host_threads():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4])
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--alpha", type=float, default=1e-3)
@@ -169,33 +179,51 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    cfg = ni.CONFIGS[1].replace(alpha=args.alpha)
+    cid = args.config
+    cfg = ni.CONFIGS[cid]
+    if cid == 1 or args.alpha != 1e-3:
+        cfg = cfg.replace(alpha=args.alpha if cid == 1 else cfg.alpha)
     if args.nrhs:
         cfg = cfg.replace(nrhs=args.nrhs)
+    if args.steps is None:
+        args.steps = {0: 500, 1: 200, 2: 30, 3: 3, 4: 10}[cid]
+    if cid == 3:
+        args.no_e2e = True            # 2 x 4 GiB pinned host buffers per rank: skipped
     B = cfg.nrhs
-    workload = f"cfg1_1d_n{cfg.n}_L{cfg.levels}_rhs{B}_per_gpu_alpha{cfg.alpha:g}_Wseed"
+    pool = cfg.dim == 2 and B > 8     # 2D: 8 seeded RHS tiled to the batch (throughput is value-independent)
+    workload = (f"{cfg.name}_{cfg.dim}d_n{cfg.n}_L{cfg.levels}_rhs{B}_per_gpu_alpha{cfg.alpha:g}_C{cfg.channels}"
+                f"_Wseed")
+
+    def make_y(nrhs, start):
+        if not pool:
+            return ni.make_rhs(cfg, factors, cfg.alpha, nrhs=nrhs, start=start)[0]
+        base = ni.make_rhs(cfg, factors, cfg.alpha, nrhs=8, start=start)[0]
+        return np.ascontiguousarray(np.concatenate([base] * (-(-nrhs // 8)))[:nrhs])
 
     if args.impl == "reference":
         if rank != 0:
             return
         factors = ni.operator_factors(cfg)
         W = ni.weights_seed(cfg)
-        y, _ = ni.make_rhs(cfg, factors, cfg.alpha, nrhs=16)
+        ns = 16 if cfg.dim == 1 else 1
+        y, _ = ni.make_rhs(cfg, factors, cfg.alpha, nrhs=ns)
         rates, secs = [], 0.0
-        for _ in range(args.warmup):
-            oracle_rate(cfg, factors, W, y, 4, 1)
-        for _ in range(args.steps):
-            r, dt = oracle_rate(cfg, factors, W, y, 16, 1)
+        for _ in range(min(args.warmup, 1)):
+            oracle_rate(cfg, factors, W, y, min(ns, 4), 1)
+        ref_steps = args.steps if cfg.dim == 1 else min(args.steps, 3)
+        for _ in range(ref_steps):
+            r, dt = oracle_rate(cfg, factors, W, y, ns, 1)
             rates.append(r)
             secs += dt
-        v = args.steps * 16 / secs
-        line = {"impl": "reference", "metric": "RHS*V-cycles/s (1D cfg1, fp64 CPU oracle)", "value": v,
+        args.steps = ref_steps
+        v = args.steps * ns / secs
+        line = {"impl": "reference", "metric": f"RHS*V-cycles/s ({cfg.name}, fp64 CPU oracle)", "value": v,
                 "unit": "RHS*cycles/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": workload, "sample": "16 RHS x 1 cycle per step"},
+                "config": {"workload": workload, "sample": f"{ns} RHS x 1 cycle per step"},
                 "cpu_baseline": {"value": v, "unit": "RHS*cycles/s", "cores": host_threads(), "kind": "oracle",
-                                 "sample": "16 RHS x 1 cycle per step of the cfg1 workload"},
+                                 "sample": f"{ns} RHS x 1 cycle per step of the {cfg.name} workload"},
                 "e2e": {"value": v, "unit": "RHS*cycles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
         return
@@ -213,11 +241,12 @@ def main():
 
     factors = ni.operator_factors(cfg)
     W = ni.weights_seed(cfg)
-    h = nmg.Hierarchy(1, cfg.n, cfg.levels, cfg.alpha, factors, nu1=cfg.nu1, nu2=cfg.nu2, max_rhs=B, device=local)
+    h = nmg.Hierarchy(cfg.dim, cfg.n, cfg.levels, cfg.alpha, factors, nu1=cfg.nu1, nu2=cfg.nu2, max_rhs=B,
+                      device=local)
     for l, w in enumerate(W):
         h.load_weights(l + 1, ni.cnn_arch(cfg), w)
     start, _ = weak_shard(B, rank)
-    y_np, _ = ni.make_rhs(cfg, factors, cfg.alpha, nrhs=B, start=start)
+    y_np = make_y(B, start)
     y = torch.tensor(y_np, dtype=torch.float64, device=dev)
     x = torch.zeros_like(y)
     stream = torch.cuda.Stream(dev)          # non-default stream: the library replays a CUDA graph
@@ -276,10 +305,17 @@ def main():
         achieved = counts["gemm32"] / (step_ms * 1e-3) / 1e12
         roof = {"kernel": "tc_gemm_kernel (3xTF32 tcgen05, all levels)", "bound": "tensor", "unit": "TFLOP/s",
                 "peak_note": "TF32 tensor (measured bf16 x 1.1/2.25) / 3 passes"}
+    elif cfg.dim == 2 and cfg.channels == 32:
+        peak = pk["bf16_tflops"] * TF32_NOMINAL_RATIO / 3.0
+        achieved = counts["smooth"] / (step_ms * 1e-3) / 1e12
+        roof = {"kernel": "2D smoother: conv3x3_tc hidden layers (3xTF32 tcgen05) + FFMA first/last layers + FFT filter",
+                "bound": "tensor", "unit": "TFLOP/s",
+                "peak_note": "TF32 tensor (measured bf16 x 1.1/2.25) / 3 passes; CNN FLOPs only"}
     else:
         peak = 148 * 128 * 2 * 1.965e9 / 1e12
         achieved = counts["smooth"] / (step_ms * 1e-3) / 1e12
-        roof = {"kernel": "smooth1d_kernel (norm + 3-layer CNN + level filter), all launches of a step",
+        roof = {"kernel": ("smooth1d_kernel (norm + 3-layer CNN + level filter), all launches of a step"
+                           if cfg.dim == 1 else "cnn2d_kernel (FFMA 4-layer CNN) + FFT filter"),
                 "bound": "alu", "unit": "TFLOP/s",
                 "peak_note": "FP32 FFMA: 148 SM x 128 lanes x 2 FLOP x 1.965 GHz (CNN FLOPs only, 2880/point)"}
     roof.update({"achieved": achieved, "peak": peak, "frac": achieved / peak, "traffic": traffic,
@@ -307,12 +343,12 @@ def main():
         torch.cuda.synchronize(dev)
         ems = max_over_ranks(f0.elapsed_time(f1))
         e2e = {"value": world * B * args.steps / (ems / 1e3), "unit": "RHS*cycles/s",
-               "h2d_bytes_per_step": 2 * 8 * B * cfg.n, "d2h_bytes_per_step": 8 * B * cfg.n}
+               "h2d_bytes_per_step": 2 * 8 * B * cfg.N, "d2h_bytes_per_step": 8 * B * cfg.N}
 
     # ---- RHS solved to 1e-6 / s with converging stand-in weights (alpha = 1e-2)
     solve = None
-    if not args.no_solve:
-        scfg = cfg.replace(alpha=1e-2)
+    if not args.no_solve and cfg.dim == 1:
+        scfg = cfg.replace(alpha=1e-2 if cid == 1 else cfg.alpha)
         sf = ni.operator_factors(scfg)
         hs = nmg.Hierarchy(1, scfg.n, scfg.levels, scfg.alpha, sf, nu1=scfg.nu1, nu2=scfg.nu2, max_rhs=B,
                            device=local)
@@ -328,26 +364,29 @@ def main():
         rep = hs.solve(ys, xs, tol=1e-6, max_cycles=100, stream=stream)
         sec = max_over_ranks(rep["wall_seconds"])
         solve = {"value": world * int(rep["converged"].sum()) / sec, "unit": "RHS solved/s (relres<=1e-6)",
-                 "alpha": 1e-2, "weights": "W_lin stand-in", "cycles_max": int(rep["cycles"].max()),
+                 "alpha": scfg.alpha, "weights": "W_lin stand-in", "cycles_max": int(rep["cycles"].max()),
                  "cycles_mean": float(rep["cycles"].mean()), "converged": int(rep["converged"].sum()),
                  "seconds": sec}
 
     # ---- CPU oracle baseline (rank 0, N = 1 only; bounded sample)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        rate, dt = oracle_rate(cfg, factors, W, y_np, 128, 8)
+        nr, nc = {0: (8, 200), 1: (128, 8), 2: (4, 2), 3: (1, 1), 4: (1, 1)}[cid]
+        rate, dt = oracle_rate(cfg, factors, W, y_np, nr, nc)
         cpu = {"value": rate, "unit": "RHS*cycles/s", "cores": host_threads(), "kind": "oracle",
-               "sample": f"128 RHS x 8 cycles of the same workload ({dt:.1f} s)"}
+               "sample": f"{nr} RHS x {nc} cycles of the same workload ({dt:.1f} s)"}
 
     if rank == 0:
-        line = {"metric": "RHS*V-cycles/s (1D cfg1: fp64 residual + NMGF V-cycle + update per step)",
+        line = {"metric": f"RHS*V-cycles/s ({cfg.name}: fp64 residual + NMGF V-cycle + update per step)",
                 "value": value, "unit": "RHS*cycles/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64 outer / f32 inner",
                 "data": "synthetic (seeded RHS; W_seed Kaiming-uniform weights)",
                 "config": {"workload": workload, "global_batch": world * B, "n": cfg.n, "levels": cfg.levels,
+                           "rhs": "8-RHS seeded pool tiled to the batch" if pool else "seeded, distinct",
                            "alpha": cfg.alpha, "nu1": cfg.nu1, "nu2": cfg.nu2, "parallelism": f"rhs-shard x{world}",
-                           "l2": "inputs larger than L2 (no flush)"},
+                           "l2": ("working set fits L2 (latency-bound config, no flush)" if cid == 0
+                                  else "inputs larger than L2 (no flush)")},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "solve": solve,
                 "gpu_launches": launches, "clocks": clk.summary()}
         print(json.dumps(line))
