@@ -10,11 +10,13 @@
 // in shared memory; the t1 shift is applied in the epilogue (out(x) = D0(x-1) + D1(x) +
 // D2(x+1)), so the 32-wide tile yields 30 valid output columns.
 //
-// Activations live in HBM as padded pixel-major tensors [b][n+2][n+2][C] (1-pixel zero
-// border), split into tf32 hi/lo arrays.  Roles (192 threads, persistent CTAs):
+// Activations live in HBM as padded pixel-major fp32 tensors [b][n+2][n+2][C] (1-pixel
+// zero border).  Roles (256 threads, persistent CTAs):
 //   warp 0 : TMA producer (weights once; per tile two 16-channel input chunks, SWIZZLE_64B)
+//   warps 6-7 : form the tf32 lo part lo = x - trunc_tf32(x) of each landed chunk in smem
+//              (the tensor core reads the fp32 chunk itself as the hi part)
 //   warp 1 : MMA issuer (tcgen05.mma kind::tf32, M=128 N=256 K=8), double-buffered TMEM
-//   warps 2-5 : epilogue (tcgen05.ld -> cross-tap sum through smem -> bias/ReLU -> hi/lo)
+//   warps 2-5 : epilogue (tcgen05.ld -> cross-tap sum through smem -> bias/ReLU -> fp32)
 #include <cuda.h>
 
 #include <algorithm>
@@ -37,7 +39,7 @@ constexpr int B_STAGE = 2 * B_HALF;         // hi + lo (40 KB)
 constexpr int NSTAGE = 2;
 constexpr int SX_BYTES = 3 * 32 * 33 * 4;   // epilogue exchange [t1][o][xx]
 constexpr int CONV_SMEM = 2 * A_BYTES + NSTAGE * B_STAGE + SX_BYTES + 256 + 1024;
-constexpr int NTHR = 192;
+constexpr int NTHR = 256;                   // + warps 6-7: tf32 lo converters
 
 NMG_D uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 NMG_D void mb_init(uint64_t* b, uint32_t c) {
@@ -109,8 +111,7 @@ NMG_D TileCoord tile_coord(int t, int tiles_y, int tiles_x) {
 
 __global__ void __launch_bounds__(NTHR, 1)
     conv3x3_tc_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
-                      const __grid_constant__ CUtensorMap mInh, const __grid_constant__ CUtensorMap mInl,
-                      ConvTcArgs a) {
+                      const __grid_constant__ CUtensorMap mInh, ConvTcArgs a) {
   extern __shared__ uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   uint8_t* Ah = sm;
@@ -123,7 +124,8 @@ __global__ void __launch_bounds__(NTHR, 1)
   uint64_t* b_empty = bars + 3;     // [NSTAGE]
   uint64_t* t_full = bars + 5;      // [2]
   uint64_t* t_empty = bars + 7;     // [2]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 9);
+  uint64_t* b_conv = bars + 9;      // [NSTAGE] lo part formed
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 11);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = a.n, Wp = n + 2;
@@ -132,7 +134,7 @@ __global__ void __launch_bounds__(NTHR, 1)
 
   if (tid == 0) {
     mb_init(a_full, 1);
-    for (int s = 0; s < NSTAGE; ++s) { mb_init(&b_full[s], 1); mb_init(&b_empty[s], 1); }
+    for (int s = 0; s < NSTAGE; ++s) { mb_init(&b_full[s], 1); mb_init(&b_empty[s], 1); mb_init(&b_conv[s], 2); }
     for (int s = 0; s < 2; ++s) { mb_init(&t_full[s], 1); mb_init(&t_empty[s], 4); }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -161,9 +163,8 @@ __global__ void __launch_bounds__(NTHR, 1)
           const uint32_t ph = (uint32_t)(it / NSTAGE) & 1u;
           mb_wait(&b_empty[s], ph ^ 1u);
           uint8_t* st = Bs + s * B_STAGE;
-          mb_expect(&b_full[s], B_STAGE);
+          mb_expect(&b_full[s], B_HALF);
           tma3d(st, &mInh, &b_full[s], ch * 16, tc.X0, row0);
-          tma3d(st + B_HALF, &mInl, &b_full[s], ch * 16, tc.X0, row0);
         }
       }
     }
@@ -180,7 +181,7 @@ __global__ void __launch_bounds__(NTHR, 1)
         const uint32_t d = tmem + (uint32_t)(ab * 256);
         for (int ch = 0; ch < NCH; ++ch, ++it) {
           const int s = it % NSTAGE;
-          mb_wait(&b_full[s], (uint32_t)(it / NSTAGE) & 1u);
+          mb_wait(&b_conv[s], (uint32_t)(it / NSTAGE) & 1u);
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
           const uint32_t bh = bs + s * B_STAGE, bl = bh + B_HALF;
 #pragma unroll
@@ -203,6 +204,30 @@ __global__ void __launch_bounds__(NTHR, 1)
       }
     }
     __syncwarp();
+  } else if (warp >= 6) {  // ---------------------------------------------- lo converters
+    const int ct = tid - 192;         // 0..63
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int ch = 0; ch < NCH; ++ch, ++it) {
+        const int s = it % NSTAGE;
+        mb_wait(&b_full[s], (uint32_t)(it / NSTAGE) & 1u);
+        const float4* hi = reinterpret_cast<const float4*>(Bs + s * B_STAGE);
+        float4* lo = reinterpret_cast<float4*>(Bs + s * B_STAGE + B_HALF);
+#pragma unroll 4
+        for (int i = ct; i < B_HALF / 16; i += 64) {
+          const float4 v = hi[i];
+          float4 r;
+          r.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+          r.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+          r.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+          r.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+          lo[i] = r;
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mb_arrive(&b_conv[s]);
+      }
+    }
   } else {               // ------------------------------------------------ epilogue (warps 2..5)
     const int q = warp & 3;            // TMEM lane quarter this warp may access: t1 = q (q = 3: padding)
     const int et = tid - 64;           // epilogue thread 0..127
@@ -246,11 +271,7 @@ __global__ void __launch_bounds__(NTHR, 1)
             const int X = tc.X0 + xx;                   // padded column = image x + 1
             if (xx < TW - 1 && X <= n) {
               const float acc = d0[xx - 1] + d1[xx] + d2[xx + 1] + bias;
-              float hi, lo;
-              tf32_split(fmaxf(acc, 0.f), hi, lo);
-              const int64_t off = (rowoff + X) * CC + o;
-              a.out_hi[off] = hi;
-              a.out_lo[off] = lo;
+              a.out[(rowoff + X) * CC + o] = fmaxf(acc, 0.f);
             }
           }
         }
@@ -273,8 +294,7 @@ __global__ void __launch_bounds__(NTHR, 1)
 __global__ void __launch_bounds__(256) conv_in_kernel(int n, int nrhs, const float* __restrict__ b,
                                                       const double* __restrict__ norms,
                                                       const float* __restrict__ w0, const float* __restrict__ b0,
-                                                      float* __restrict__ oh, float* __restrict__ ol,
-                                                      float* __restrict__ zh, float* __restrict__ zl) {
+                                                      float* __restrict__ o1, float* __restrict__ z2) {
   // thread = (padded pixel, 4-channel quad): a warp writes 4 whole pixels (512 contiguous bytes)
   __shared__ float ws[CC * 9 + CC];
   for (int i = threadIdx.x; i < CC * 10; i += blockDim.x) ws[i] = i < CC * 9 ? __ldg(w0 + i) : __ldg(b0 + i - CC * 9);
@@ -291,10 +311,8 @@ __global__ void __launch_bounds__(256) conv_in_kernel(int n, int nrhs, const flo
   const int64_t off = idx * CC + g * 4;
   if (Y == 0 || X == 0 || Y == n + 1 || X == n + 1) {
     const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-    *reinterpret_cast<float4*>(oh + off) = z;
-    *reinterpret_cast<float4*>(ol + off) = z;
-    *reinterpret_cast<float4*>(zh + off) = z;
-    *reinterpret_cast<float4*>(zl + off) = z;
+    *reinterpret_cast<float4*>(o1 + off) = z;
+    *reinterpret_cast<float4*>(z2 + off) = z;
     return;
   }
   const int y = Y - 1, x = X - 1;
@@ -309,24 +327,23 @@ __global__ void __launch_bounds__(256) conv_in_kernel(int n, int nrhs, const flo
       const int yy = y + t2 - 1, xx = x + t1 - 1;
       u[t2 * 3 + t1] = (yy >= 0 && yy < n && xx >= 0 && xx < n) ? (float)((double)__ldg(B + (int64_t)yy * n + xx) * inv) : 0.f;
     }
-  float hv[4], lv[4];
+  float hv[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int c = g * 4 + j;
     float acc = ws[CC * 9 + c];
 #pragma unroll
     for (int t = 0; t < 9; ++t) acc = fmaf(ws[c * 9 + t], u[t], acc);
-    tf32_split(fmaxf(acc, 0.f), hv[j], lv[j]);
+    hv[j] = fmaxf(acc, 0.f);
   }
-  *reinterpret_cast<float4*>(oh + off) = make_float4(hv[0], hv[1], hv[2], hv[3]);
-  *reinterpret_cast<float4*>(ol + off) = make_float4(lv[0], lv[1], lv[2], lv[3]);
+  *reinterpret_cast<float4*>(o1 + off) = make_float4(hv[0], hv[1], hv[2], hv[3]);
 }
 
 // ---------------------------------------------------------------- layer 4 (C -> 1), FFMA
 // h(y, x) = s * (b3 + sum_{c,t} w3[c][t] a3(y + t2 - 1, x + t1 - 1, c)); 32 x 16 output tile per
 // CTA (128 threads, 4 consecutive pixels each), input staged in two 16-channel halves.
 constexpr int OW = 32, OH = 16, OPAD = 17;
-__global__ void __launch_bounds__(128) conv_out_kernel(int n, const float* __restrict__ ih, const float* __restrict__ il,
+__global__ void __launch_bounds__(128) conv_out_kernel(int n, const float* __restrict__ ih,
                                                        const double* __restrict__ norms, const float* __restrict__ w3,
                                                        const float* __restrict__ b3, float2* __restrict__ Z,
                                                        float* __restrict__ x, int accumulate) {
@@ -349,9 +366,7 @@ __global__ void __launch_bounds__(128) conv_out_kernel(int n, const float* __res
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       if (Y < Wp && X < Wp) {
         const int64_t off = (((int64_t)rb * Wp + Y) * Wp + X) * CC + half * 16 + c4 * 4;
-        const float4 h4 = *reinterpret_cast<const float4*>(ih + off);
-        const float4 l4 = *reinterpret_cast<const float4*>(il + off);
-        v = make_float4(h4.x + l4.x, h4.y + l4.y, h4.z + l4.z, h4.w + l4.w);
+        v = *reinterpret_cast<const float4*>(ih + off);
       }
       float* d = tile + p * OPAD + c4 * 4;
       d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
@@ -415,8 +430,8 @@ void zero_border(int n, int nrhs, int C, float* buf, cudaStream_t s) {
 
 int conv_tc_smem() { return CONV_SMEM; }
 
-void conv3x3_tc(const CUtensorMap* ah, const CUtensorMap* al, const CUtensorMap* ih, const CUtensorMap* il,
-                const ConvTcArgs& a, int num_sms, cudaStream_t s) {
+void conv3x3_tc(const CUtensorMap* ah, const CUtensorMap* al, const CUtensorMap* in, const ConvTcArgs& a,
+                int num_sms, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(conv3x3_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, CONV_SMEM);
@@ -424,19 +439,19 @@ void conv3x3_tc(const CUtensorMap* ah, const CUtensorMap* al, const CUtensorMap*
   }
   const int tiles = a.nrhs * ceil_div(a.n, TW - 2) * ceil_div(a.n, TR);
   const int grid = std::min(tiles, num_sms);
-  conv3x3_tc_kernel<<<grid, NTHR, CONV_SMEM, s>>>(*ah, *al, *ih, *il, a);
+  conv3x3_tc_kernel<<<grid, NTHR, CONV_SMEM, s>>>(*ah, *al, *in, a);
 }
 
-void conv_in(int n, int nrhs, const float* b, const double* norms, const float* w0, const float* b0, float* oh,
-             float* ol, float* zh, float* zl, cudaStream_t s) {
+void conv_in(int n, int nrhs, const float* b, const double* norms, const float* w0, const float* b0, float* o1,
+             float* z2, cudaStream_t s) {
   const int64_t total = (int64_t)nrhs * (n + 2) * (n + 2) * (CC / 4);
-  conv_in_kernel<<<(int)ceil_div64(total, 256), 256, 0, s>>>(n, nrhs, b, norms, w0, b0, oh, ol, zh, zl);
+  conv_in_kernel<<<(int)ceil_div64(total, 256), 256, 0, s>>>(n, nrhs, b, norms, w0, b0, o1, z2);
 }
 
-void conv_out(int n, int nrhs, const float* ih, const float* il, const double* norms, const float* w3,
-              const float* b3, float2* Z, float* x, bool accumulate, cudaStream_t s) {
+void conv_out(int n, int nrhs, const float* in, const double* norms, const float* w3, const float* b3, float2* Z,
+              float* x, bool accumulate, cudaStream_t s) {
   dim3 grid(ceil_div(n, OW) * ceil_div(n, OH), nrhs);
-  conv_out_kernel<<<grid, 128, 0, s>>>(n, ih, il, norms, w3, b3, Z, x, accumulate ? 1 : 0);
+  conv_out_kernel<<<grid, 128, 0, s>>>(n, in, norms, w3, b3, Z, x, accumulate ? 1 : 0);
 }
 
 }  // namespace nmg

@@ -122,19 +122,19 @@ void filter2d(int nrhs, int n, float2* Z, const float2* tw, int tw_n, float* x, 
 void real_to_complex(int64_t count, const float* x, float2* Z, cudaStream_t s);
 
 // ---- 2D CNN on tensor cores (conv_tc.cu), C = 32 ------------------------------------
-// Activations: padded pixel-major [b][n+2][n+2][32] fp32 tf32 hi/lo pairs, zero border.
+// Activations: padded pixel-major fp32 [b][n+2][n+2][32], zero border.
 struct ConvTcArgs {
   int n, nrhs;
   const float* bias;        // [32]
-  float* out_hi; float* out_lo;
+  float* out;
 };
-void conv3x3_tc(const CUtensorMap* ah, const CUtensorMap* al, const CUtensorMap* ih, const CUtensorMap* il,
-                const ConvTcArgs& a, int num_sms, cudaStream_t s);
+void conv3x3_tc(const CUtensorMap* ah, const CUtensorMap* al, const CUtensorMap* in, const ConvTcArgs& a,
+                int num_sms, cudaStream_t s);
 int conv_tc_smem();
-void conv_in(int n, int nrhs, const float* b, const double* norms, const float* w0, const float* b0, float* oh,
-             float* ol, float* zh, float* zl, cudaStream_t s);   // also zeroes borders of (oh, ol, zh, zl)
-void conv_out(int n, int nrhs, const float* ih, const float* il, const double* norms, const float* w3,
-              const float* b3, float2* Z, float* x, bool accumulate, cudaStream_t s);
+void conv_in(int n, int nrhs, const float* b, const double* norms, const float* w0, const float* b0, float* o1,
+             float* z2, cudaStream_t s);   // also zeroes the borders of o1 and z2
+void conv_out(int n, int nrhs, const float* in, const double* norms, const float* w3, const float* b3, float2* Z,
+              float* x, bool accumulate, cudaStream_t s);
 void zero_border(int n, int nrhs, int C, float* buf, cudaStream_t s);
 
 }  // namespace nmg

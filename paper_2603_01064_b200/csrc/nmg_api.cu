@@ -233,10 +233,10 @@ struct nmg_hierarchy {
   bool conv_tc = false;
   int num_sms = 148;
   int conv_chunk = 0;
-  DevBuf<float> act1h, act1l, act2h, act2l;
+  DevBuf<float> act1, act2;
   std::vector<std::unique_ptr<DevBuf<float>>> WA;        // per level: [layer 0 hi, lo, layer 1 hi, lo]
   std::vector<CUtensorMap> mWAh, mWAl;                   // [level * 2 + layer]
-  std::vector<CUtensorMap> mA1h, mA1l, mA2h, mA2l;       // per level activation maps
+  std::vector<CUtensorMap> mA1, mA2;                     // per level activation maps
   // coarse Cholesky factor (row-major L and L^T)
   DevBuf<double> Lrow, Lcol;
   int nc = 0;
@@ -493,17 +493,15 @@ nmg_status smooth2d(nmg_hierarchy* h, int l, int nrhs, const float* b, float* x,
       const int cnt = std::min(h->conv_chunk, nrhs - r0);
       const int64_t off = (int64_t)r0 * N;
       { Prof p(h, NMG_K_SMOOTH, s);
-        conv_in(n, cnt, b + off, nrm ? nrm + r0 : nullptr, w0, b0, h->act1h.p, h->act1l.p, h->act2h.p, h->act2l.p, s); }
+        conv_in(n, cnt, b + off, nrm ? nrm + r0 : nullptr, w0, b0, h->act1.p, h->act2.p, s); }
       ConvTcArgs ca{};
-      ca.n = n; ca.nrhs = cnt; ca.bias = b1; ca.out_hi = h->act2h.p; ca.out_lo = h->act2l.p;
+      ca.n = n; ca.nrhs = cnt; ca.bias = b1; ca.out = h->act2.p;
+      { Prof p(h, NMG_K_SMOOTH, s); conv3x3_tc(&h->mWAh[l * 2], &h->mWAl[l * 2], &h->mA1[l], ca, h->num_sms, s); }
+      ca.bias = b2; ca.out = h->act1.p;
+      { Prof p(h, NMG_K_SMOOTH, s); conv3x3_tc(&h->mWAh[l * 2 + 1], &h->mWAl[l * 2 + 1], &h->mA2[l], ca, h->num_sms, s); }
       { Prof p(h, NMG_K_SMOOTH, s);
-        conv3x3_tc(&h->mWAh[l * 2], &h->mWAl[l * 2], &h->mA1h[l], &h->mA1l[l], ca, h->num_sms, s); }
-      ca.bias = b2; ca.out_hi = h->act1h.p; ca.out_lo = h->act1l.p;
-      { Prof p(h, NMG_K_SMOOTH, s);
-        conv3x3_tc(&h->mWAh[l * 2 + 1], &h->mWAl[l * 2 + 1], &h->mA2h[l], &h->mA2l[l], ca, h->num_sms, s); }
-      { Prof p(h, NMG_K_SMOOTH, s);
-        conv_out(n, cnt, h->act1h.p, h->act1l.p, nrm ? nrm + r0 : nullptr, w3, b3, filt ? h->Z.p + off : nullptr,
-                 x + off, accumulate, s); }
+        conv_out(n, cnt, h->act1.p, nrm ? nrm + r0 : nullptr, w3, b3, filt ? h->Z.p + off : nullptr, x + off,
+                 accumulate, s); }
       NMG_TRY(check_launch(h));
     }
     if (filt) {
@@ -883,20 +881,18 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
     if (h->conv_tc) {
       const int64_t Wp = n + 2;
       const int64_t per = Wp * Wp * 32;                         // floats per RHS per array
-      const int64_t budget = (int64_t)6 << 30;                  // floats over the 4 arrays (24 GiB)
-      h->conv_chunk = (int)std::max<int64_t>(1, std::min<int64_t>(B, budget / (4 * per)));
-      for (auto* buf : {&h->act1h, &h->act1l, &h->act2h, &h->act2l}) {
+      const int64_t budget = (int64_t)6 << 30;                  // floats over the 2 arrays (24 GiB)
+      h->conv_chunk = (int)std::max<int64_t>(1, std::min<int64_t>(B, budget / (2 * per)));
+      for (auto* buf : {&h->act1, &h->act2}) {
         NMG_TRY(buf->alloc((size_t)h->conv_chunk * per));
         NMG_CUDA(cudaMemset(buf->p, 0, sizeof(float) * buf->n));
       }
-      h->mA1h.resize(h->L); h->mA1l.resize(h->L); h->mA2h.resize(h->L); h->mA2l.resize(h->L);
+      h->mA1.resize(h->L); h->mA2.resize(h->L);
       for (int l = 0; l < h->L - 1; ++l) {
         const int Wl = h->n[l] + 2;
         const int64_t rows = (int64_t)h->conv_chunk * Wl;
-        NMG_TRY(make_act_map(&h->mA1h[l], h->act1h.p, rows, Wl));
-        NMG_TRY(make_act_map(&h->mA1l[l], h->act1l.p, rows, Wl));
-        NMG_TRY(make_act_map(&h->mA2h[l], h->act2h.p, rows, Wl));
-        NMG_TRY(make_act_map(&h->mA2l[l], h->act2l.p, rows, Wl));
+        NMG_TRY(make_act_map(&h->mA1[l], h->act1.p, rows, Wl));
+        NMG_TRY(make_act_map(&h->mA2[l], h->act2.p, rows, Wl));
       }
       h->mWAh.resize(2 * h->L); h->mWAl.resize(2 * h->L);
       for (int l = 0; l < h->L - 1; ++l) h->WA.emplace_back(new DevBuf<float>());
