@@ -291,52 +291,71 @@ __global__ void __launch_bounds__(NTHR, 1)
 // ---------------------------------------------------------------- layer 1 (1 -> C), FFMA
 // a1(y, x, c) = ReLU(b0[c] + sum_t w0[c][t] u(y + t2 - 1, x + t1 - 1)), u = b / ||b||, into the
 // padded hi/lo tensors; border pixels of a1 and a2 (this level's layout) are set to zero.
-__global__ void __launch_bounds__(256) conv_in_kernel(int n, int nrhs, const float* __restrict__ b,
+__global__ void __launch_bounds__(256) conv_in_kernel(int n, const float* __restrict__ b,
                                                       const double* __restrict__ norms,
                                                       const float* __restrict__ w0, const float* __restrict__ b0,
                                                       float* __restrict__ o1, float* __restrict__ z2) {
-  // thread = (padded pixel, 4-channel quad): a warp writes 4 whole pixels (512 contiguous bytes)
+  // CTA = 256 consecutive padded pixels of one RHS (blockIdx.y); thread = one pixel, all 32
+  // channels into shared memory, then fully coalesced float4 stores of the 32 KB block.
   __shared__ float ws[CC * 9 + CC];
+  __shared__ float4 tile[256 * (CC / 4) + 32];
   for (int i = threadIdx.x; i < CC * 10; i += blockDim.x) ws[i] = i < CC * 9 ? __ldg(w0 + i) : __ldg(b0 + i - CC * 9);
   __syncthreads();
   const int Wp = n + 2;
-  const int64_t per = (int64_t)Wp * Wp;
-  const int64_t gidx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int g = (int)(gidx & (CC / 4 - 1));
-  const int64_t idx = gidx / (CC / 4);
-  if (idx >= (int64_t)nrhs * per) return;
-  const int rb = (int)(idx / per);
-  const int rem = (int)(idx - rb * per);
-  const int Y = rem / Wp, X = rem - Y * Wp;
-  const int64_t off = idx * CC + g * 4;
-  if (Y == 0 || X == 0 || Y == n + 1 || X == n + 1) {
-    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-    *reinterpret_cast<float4*>(o1 + off) = z;
-    *reinterpret_cast<float4*>(z2 + off) = z;
-    return;
-  }
-  const int y = Y - 1, x = X - 1;
+  const int per = Wp * Wp;
+  const int rb = blockIdx.y;
+  const int p0 = blockIdx.x * 256;
+  const int p = p0 + threadIdx.x;
   const double s = norms ? norms[rb] : 1.0;
   const double inv = (s != 0.0) ? 1.0 / s : 0.0;
   const float* B = b + (int64_t)rb * n * n;
-  float u[9];
+  float4* trow = tile + threadIdx.x * (CC / 4) + (threadIdx.x >> 3);   // +1 float4 per 8 rows: fewer conflicts
+  if (p < per) {
+    const int Y = p / Wp, X = p - Y * Wp;
+    if (Y == 0 || X == 0 || Y == n + 1 || X == n + 1) {
 #pragma unroll
-  for (int t2 = 0; t2 < 3; ++t2)
+      for (int g = 0; g < CC / 4; ++g) trow[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      const int y = Y - 1, x = X - 1;
+      float u[9];
 #pragma unroll
-    for (int t1 = 0; t1 < 3; ++t1) {
-      const int yy = y + t2 - 1, xx = x + t1 - 1;
-      u[t2 * 3 + t1] = (yy >= 0 && yy < n && xx >= 0 && xx < n) ? (float)((double)__ldg(B + (int64_t)yy * n + xx) * inv) : 0.f;
+      for (int t2 = 0; t2 < 3; ++t2)
+#pragma unroll
+        for (int t1 = 0; t1 < 3; ++t1) {
+          const int yy = y + t2 - 1, xx = x + t1 - 1;
+          u[t2 * 3 + t1] = (yy >= 0 && yy < n && xx >= 0 && xx < n) ? (float)((double)__ldg(B + yy * n + xx) * inv) : 0.f;
+        }
+#pragma unroll
+      for (int g = 0; g < CC / 4; ++g) {
+        float hv[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int c = g * 4 + j;
+          float acc = ws[CC * 9 + c];
+#pragma unroll
+          for (int t = 0; t < 9; ++t) acc = fmaf(ws[c * 9 + t], u[t], acc);
+          hv[j] = fmaxf(acc, 0.f);
+        }
+        trow[g] = make_float4(hv[0], hv[1], hv[2], hv[3]);
+      }
     }
-  float hv[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int c = g * 4 + j;
-    float acc = ws[CC * 9 + c];
-#pragma unroll
-    for (int t = 0; t < 9; ++t) acc = fmaf(ws[c * 9 + t], u[t], acc);
-    hv[j] = fmaxf(acc, 0.f);
   }
-  *reinterpret_cast<float4*>(o1 + off) = make_float4(hv[0], hv[1], hv[2], hv[3]);
+  __syncthreads();
+  const int cnt = min(256, per - p0);
+  float4* out = reinterpret_cast<float4*>(o1 + ((int64_t)rb * per + p0) * CC);
+  for (int i = threadIdx.x; i < cnt * (CC / 4); i += 256) {
+    const int px = i / (CC / 4), g = i - px * (CC / 4);
+    out[i] = tile[px * (CC / 4) + (px >> 3) + g];
+  }
+  // zero border of the second activation tensor (this level's layout)
+  if (p < per) {
+    const int Y = p / Wp, X = p - Y * Wp;
+    if (Y == 0 || X == 0 || Y == n + 1 || X == n + 1) {
+      float4* q = reinterpret_cast<float4*>(z2 + ((int64_t)rb * per + p) * CC);
+#pragma unroll
+      for (int g = 0; g < CC / 4; ++g) q[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
 }
 
 // ---------------------------------------------------------------- layer 4 (C -> 1), FFMA
@@ -444,8 +463,8 @@ void conv3x3_tc(const CUtensorMap* ah, const CUtensorMap* al, const CUtensorMap*
 
 void conv_in(int n, int nrhs, const float* b, const double* norms, const float* w0, const float* b0, float* o1,
              float* z2, cudaStream_t s) {
-  const int64_t total = (int64_t)nrhs * (n + 2) * (n + 2) * (CC / 4);
-  conv_in_kernel<<<(int)ceil_div64(total, 256), 256, 0, s>>>(n, nrhs, b, norms, w0, b0, o1, z2);
+  dim3 grid(ceil_div((n + 2) * (n + 2), 256), nrhs);
+  conv_in_kernel<<<grid, 256, 0, s>>>(n, b, norms, w0, b0, o1, z2);
 }
 
 void conv_out(int n, int nrhs, const float* in, const double* norms, const float* w3, const float* b3, float2* Z,
