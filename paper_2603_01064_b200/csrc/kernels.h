@@ -79,6 +79,8 @@ struct Smooth1dArgs {
 };
 void smooth1d(const Smooth1dArgs& a, cudaStream_t s);
 size_t smooth1d_smem(int n);
+// same step with the 16 -> 16 layer on tcgen05 (3xTF32), smooth1d_tc.cu
+void smooth1d_tc(const Smooth1dArgs& a, cudaStream_t s);
 
 // ---- 1D transfers (reading R4) ------------------------------------------------
 void restrict1d(int nrhs, int n_f, const float* f, int64_t ldf, float* c, int64_t ldc, cudaStream_t s);

@@ -219,6 +219,7 @@ struct nmg_hierarchy {
   std::vector<CUtensorMap> mXh, mXl;
   std::vector<char> split_fresh;                         // sxh/sxl[l] hold the split of wx[l]
   bool use_tc = true;
+  bool smooth_tc = false;                                // 1D smoother layer 2 on tcgen05 (opt-in)
   // 2D: A_l = B_l (x) C_l + alpha Q_l (x) Q_l; fp32 factors (SIMT), tf32 hi/lo (tcgen05)
   std::vector<std::unique_ptr<DevBuf<float>>> B32, C32, B32h, B32l, C32h, C32l, Q32;
   std::vector<int> qhb;                                  // Q_l half-bandwidth
@@ -322,7 +323,7 @@ nmg_status smooth_level(nmg_hierarchy* h, int l, int nrhs, const float* b, float
   a.accumulate = accumulate;
   const bool split = x == h->wx[l]->p && h->sxh.size() > (size_t)l && h->sxh[l]->p;
   if (split) { a.xh = h->sxh[l]->p; a.xl = h->sxl[l]->p; }
-  { Prof p(h, NMG_K_SMOOTH, s); smooth1d(a, s); }
+  { Prof p(h, NMG_K_SMOOTH, s); if (h->smooth_tc) smooth1d_tc(a, s); else smooth1d(a, s); }
   if (h->split_fresh.size() > (size_t)l) h->split_fresh[l] = split ? 1 : 0;
   return check_launch(h);
 }
@@ -813,6 +814,10 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
     h->use_tc = !(env && std::string(env) == "simt");
     const char* genv = std::getenv("NMG_GRAPH");
     h->use_graph = !(genv && std::string(genv) == "0");
+    const char* senv = std::getenv("NMG_SMOOTH1D");
+    // measured slower than the FFMA kernel (16 channels: the A tile is re-read from smem for only
+    // N = 16 outputs per MMA, 32 cycles/MMA smem-bound, no overlap within the CTA): opt-in only
+    h->smooth_tc = h->use_tc && (senv && std::string(senv) == "tc");
   }
   if (d.dim == 1) {
     h->mAh.resize(h->L); h->mAl.resize(h->L); h->mAPh.resize(h->L); h->mAPl.resize(h->L);
@@ -1200,7 +1205,7 @@ nmg_status nmg_debug_level_op(nmg_hierarchy* h, int32_t level, int32_t op, int32
       a.normalize = op == NMG_OP_SMOOTH;
       a.filter = op == NMG_OP_SMOOTH && h->d.level_filter != 0;
       a.accumulate = op == NMG_OP_SMOOTH;
-      smooth1d(a, s);
+      if (h->smooth_tc) smooth1d_tc(a, s); else smooth1d(a, s);
       break;
     }
     case NMG_OP_COARSE:

@@ -1,0 +1,31 @@
+#!/usr/bin/env python
+"""Small end-to-end run for compute-sanitizer (memcheck / racecheck / synccheck): config 0,
+a 2D 64x64 three-level hierarchy (tensor-core conv + Kronecker GEMMs), every debug op."""
+import os, sys
+import numpy as np
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import nmg_inputs as ni
+
+def run(cfg, nrhs):
+    import torch
+    import paper_2603_01064_b200 as nmg
+    f = ni.operator_factors(cfg)
+    h = nmg.Hierarchy(cfg.dim, cfg.n, cfg.levels, cfg.alpha, f, nu1=cfg.nu1, nu2=cfg.nu2, max_rhs=nrhs)
+    for l, w in enumerate(ni.weights_seed(cfg)):
+        h.load_weights(l + 1, ni.cnn_arch(cfg), w)
+    y, _ = ni.make_rhs(cfg, f, cfg.alpha, nrhs=nrhs)
+    yd = torch.tensor(y, dtype=torch.float64, device="cuda")
+    xd = torch.zeros_like(yd)
+    rep = h.solve(yd, xd, tol=1e-300, max_cycles=2)
+    shp = (nrhs,) + (cfg.n,) * cfg.dim
+    b = torch.randn(shp, device="cuda")
+    for op in (nmg.OP_APPLY, nmg.OP_RESIDUAL, nmg.OP_FILTER, nmg.OP_CNN, nmg.OP_SMOOTH, nmg.OP_CYCLE0):
+        h.debug_op(1, op, b, torch.zeros_like(b))
+    torch.cuda.synchronize()
+    print(cfg.name, "history", rep["history"][:, -1])
+
+if __name__ == "__main__":
+    run(ni.CONFIGS[0], 8)
+    run(ni.CONFIGS[2].replace(n=64, levels=3), 3)
+    print("sanitize run done")
