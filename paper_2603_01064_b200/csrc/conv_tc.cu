@@ -37,9 +37,10 @@ constexpr int A_BYTES = 3 * NCH * A_BLK;    // 48 KB per hi / lo
 constexpr int B_HALF = RR * TW * 16 * 4;    // one chunk region, hi or lo (20 KB)
 constexpr int B_STAGE = 2 * B_HALF;         // hi + lo (40 KB)
 constexpr int NSTAGE = 2;
-constexpr int SX_BYTES = 3 * 32 * 33 * 4;   // epilogue exchange [t1][o][xx]
+constexpr int NGRP = 2;                     // epilogue warp groups (rows r = g, g + 3, ...)
+constexpr int SX_BYTES = NGRP * 3 * 32 * 33 * 4;   // epilogue exchange [group][t1][o][xx]
 constexpr int CONV_SMEM = 2 * A_BYTES + NSTAGE * B_STAGE + SX_BYTES + 256 + 1024;
-constexpr int NTHR = 256;                   // + warps 6-7: tf32 lo converters
+constexpr int NTHR = 384;                   // warps 6-7: tf32 lo converters; 2-5, 8-11, 12-15: epilogue
 
 NMG_D uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 NMG_D void mb_init(uint64_t* b, uint32_t c) {
@@ -112,8 +113,9 @@ NMG_D TileCoord tile_coord(int t, int tiles_y, int tiles_x) {
 __global__ void __launch_bounds__(NTHR, 1)
     conv3x3_tc_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
                       const __grid_constant__ CUtensorMap mInh, ConvTcArgs a) {
-  extern __shared__ uint8_t smraw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  // keep the pointer derived from the __shared__ array (shared-space loads/stores, not generic)
+  uint8_t* sm = smraw + ((1024u - (su32(smraw) & 1023u)) & 1023u);
   uint8_t* Ah = sm;
   uint8_t* Al = Ah + A_BYTES;
   uint8_t* Bs = Al + A_BYTES;                                  // NSTAGE x (hi | lo)
@@ -135,7 +137,7 @@ __global__ void __launch_bounds__(NTHR, 1)
   if (tid == 0) {
     mb_init(a_full, 1);
     for (int s = 0; s < NSTAGE; ++s) { mb_init(&b_full[s], 1); mb_init(&b_empty[s], 1); mb_init(&b_conv[s], 2); }
-    for (int s = 0; s < 2; ++s) { mb_init(&t_full[s], 1); mb_init(&t_empty[s], 4); }
+    for (int s = 0; s < 2; ++s) { mb_init(&t_full[s], 1); mb_init(&t_empty[s], 4 * NGRP); }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {
@@ -204,7 +206,7 @@ __global__ void __launch_bounds__(NTHR, 1)
       }
     }
     __syncwarp();
-  } else if (warp >= 6) {  // ---------------------------------------------- lo converters
+  } else if (warp == 6 || warp == 7) {  // --------------------------------- lo converters
     const int ct = tid - 192;         // 0..63
     int it = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -228,11 +230,13 @@ __global__ void __launch_bounds__(NTHR, 1)
         if (lane == 0) mb_arrive(&b_conv[s]);
       }
     }
-  } else {               // ------------------------------------------------ epilogue (warps 2..5)
+  } else {               // ------------------------------------------------ epilogue (warps 2-5, 8-11)
     const int q = warp & 3;            // TMEM lane quarter this warp may access: t1 = q (q = 3: padding)
-    const int et = tid - 64;           // epilogue thread 0..127
+    const int grp = warp < 8 ? 0 : (warp < 12 ? 1 : 2);   // group g handles tile rows g, g + NGRP, ...
+    static_assert(NTHR == 64 + 64 + NGRP * 128, "warp roles: producer, MMA, 2 converters, NGRP x 4 epilogue");
     const int o = lane;                // output channel handled in the combine phase
-    const int xw = et >> 5;            // combine phase: columns xx = 1 + xw + 4 k
+    const int xw = (warp - (grp == 0 ? 2 : (grp == 1 ? 8 : 12))) & 3;   // combine: columns 1 + xw + 4 k
+    float* sxg = sx + grp * 3 * 32 * 33;
     const float bias = __ldg(a.bias + o);
     int k = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
@@ -240,7 +244,7 @@ __global__ void __launch_bounds__(NTHR, 1)
       const TileCoord tc = tile_coord(t, tiles_y, tiles_x);
       mb_wait(&t_full[ab], (uint32_t)(k >> 1) & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      for (int r = 0; r < TR; ++r) {
+      for (int r = grp; r < TR; r += NGRP) {
         uint32_t v[32];
         const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * 256 + r * TW);
         asm volatile(
@@ -254,17 +258,17 @@ __global__ void __launch_bounds__(NTHR, 1)
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
         if (q < 3) {
-          float* dst = sx + (q * 32 + lane) * 33;      // [t1][o][xx]
+          float* dst = sxg + (q * 32 + lane) * 33;     // [t1][o][xx]
 #pragma unroll
           for (int j = 0; j < 32; ++j) dst[j] = __uint_as_float(v[j]);
         }
-        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        asm volatile("bar.sync %0, 128;\n" ::"r"(1 + grp) : "memory");
         const int y = tc.y0 + r;
         if (y < n) {
           const int64_t rowoff = ((int64_t)tc.b * Wp + (y + 1)) * Wp;
-          const float* d0 = sx + o * 33;
-          const float* d1 = sx + (32 + o) * 33;
-          const float* d2 = sx + (64 + o) * 33;
+          const float* d0 = sxg + o * 33;
+          const float* d1 = sxg + (32 + o) * 33;
+          const float* d2 = sxg + (64 + o) * 33;
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             const int xx = 1 + xw + 4 * kk;
@@ -275,7 +279,7 @@ __global__ void __launch_bounds__(NTHR, 1)
             }
           }
         }
-        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        asm volatile("bar.sync %0, 128;\n" ::"r"(1 + grp) : "memory");
       }
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
       if (lane == 0) mb_arrive(&t_empty[ab]);
