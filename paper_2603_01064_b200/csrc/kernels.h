@@ -43,6 +43,22 @@ struct Gemm64Args {
 int gemm_f64_ntiles(int N);
 void gemm_f64(const Gemm64Args& a, cudaStream_t s);
 
+// fp64-accurate residual via exact int8 digit products on tcgen05 (ozaki.cu)
+struct OzakiArgs {
+  int M, N, K;                           // N % 64 == 0, K % 64 == 0
+  const double* Y; int64_t ldy;
+  float* r32; int64_t ldr32;             // may be null
+  double* r64; int64_t ldr64;            // may be null
+  double* part;                          // may be null; [M][N/64]
+  const int* ex;                         // [M] row exponents of X
+  const int* ew;                         // [N] row exponents of W
+};
+int ozaki_digits();
+// digit planes [S][plane / K rows][K]: plane = (rows allocated per plane) * K
+void ozaki_split_rows(int M, int K, const double* X, int64_t ldx, int8_t* dig, int64_t plane, int* ex,
+                      cudaStream_t s);
+void ozaki_resid(const CUtensorMap* mx, const CUtensorMap* mw, const OzakiArgs& a, cudaStream_t s);
+
 // tcgen05 3xTF32 GEMM: D = C -/+ X W^T with X = Xh + Xl ([M][K], tensor maps with box
 // {16, 128}) and W = Wh + Wl ([N][K], box {16, 256}), SWIZZLE_64B, fp32 row-major C/D.
 struct TcGemmArgs {

@@ -187,6 +187,20 @@ nmg_status make_map(CUtensorMap* m, const float* p, int64_t rows, int64_t cols, 
   return NMG_OK;
 }
 
+// digit planes [S][rows][K] int8, box {64, box_rows, S}, SWIZZLE_64B
+nmg_status make_digit_map(CUtensorMap* m, const int8_t* p, int S, int64_t rows, int64_t K, int box_rows) {
+  NMG_TRY(get_encoder());
+  cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)S};
+  cuuint64_t strides[2] = {(cuuint64_t)K, (cuuint64_t)(rows * K)};
+  cuuint32_t box[3] = {64u, (cuuint32_t)box_rows, (cuuint32_t)S};
+  cuuint32_t es[3] = {1u, 1u, 1u};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)p, dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(NMG_ERR_CUDA, "cuTensorMapEncodeTiled (digits) failed (%d)", (int)r);
+  return NMG_OK;
+}
+
 // padded activation tensor [rows][Wp][32] fp32 (rows = nrhs * Wp), box {16, 32, 10}, SWIZZLE_64B
 nmg_status make_act_map(CUtensorMap* m, const float* p, int64_t rows, int Wp) {
   NMG_TRY(get_encoder());
@@ -220,6 +234,11 @@ struct nmg_hierarchy {
   std::vector<char> split_fresh;                         // sxh/sxl[l] hold the split of wx[l]
   bool use_tc = true;
   bool smooth_tc = false;                                // 1D smoother layer 2 on tcgen05 (opt-in)
+  // fp64 outer residual via int8 digit products (Ozaki-style), 1D
+  bool ozaki = false;
+  DevBuf<int8_t> wdig, xdig;
+  DevBuf<int> wexp, xexp;
+  CUtensorMap mWd{}, mXd{};
   // 2D: A_l = B_l (x) C_l + alpha Q_l (x) Q_l; fp32 factors (SIMT), tf32 hi/lo (tcgen05)
   std::vector<std::unique_ptr<DevBuf<float>>> B32, C32, B32h, B32l, C32h, C32l, Q32;
   std::vector<int> qhb;                                  // Q_l half-bandwidth
@@ -582,6 +601,21 @@ nmg_status outer_residual(nmg_hierarchy* h, int nrhs, const double* y, const dou
     { Prof p(h, NMG_K_GEMM64, s); gemm_f64(q, s); }
     return check_launch(h);
   }
+  if (h->ozaki) {
+    const int n = h->n[0];
+    { Prof p(h, NMG_K_GEMM64, s);
+      ozaki_split_rows(nrhs, n, x, n, h->xdig.p, (int64_t)h->d.max_rhs * n, h->xexp.p, s); }
+    NMG_TRY(check_launch(h));
+    OzakiArgs o{};
+    o.M = nrhs; o.N = n; o.K = n;
+    o.Y = y; o.ldy = n;
+    o.r32 = h->wy[0]->p; o.ldr32 = n;
+    o.r64 = r64; o.ldr64 = n;
+    o.part = want_part ? h->part.p : nullptr;
+    o.ex = h->xexp.p; o.ew = h->wexp.p;
+    { Prof p(h, NMG_K_GEMM64, s); ozaki_resid(&h->mXd, &h->mWd, o, s); }
+    return check_launch(h);
+  }
   Gemm64Args g{};
   const int n = h->n[0];
   g.M = nrhs; g.N = n; g.K = n;
@@ -901,6 +935,40 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
       }
       h->mWAh.resize(2 * h->L); h->mWAl.resize(2 * h->L);
       for (int l = 0; l < h->L - 1; ++l) h->WA.emplace_back(new DevBuf<float>());
+    }
+  }
+  if (d.dim == 1) {
+    const char* fenv = std::getenv("NMG_FP64");
+    h->ozaki = h->use_tc && n % 64 == 0 && n >= 64 && !(fenv && std::string(fenv) == "dmma");
+    if (h->ozaki) {
+      // W digits of A (rows n, K = n), host: exponent per row, S truncation digits
+      const int S = ozaki_digits();
+      std::vector<double> A(factors, factors + nn);
+      for (int i = 0; i < n; ++i) A[(size_t)i * n + i] += d.alpha;
+      std::vector<int8_t> dig((size_t)S * nn);
+      std::vector<int> ew(n);
+      for (int r = 0; r < n; ++r) {
+        double mx = 0.0;
+        for (int k = 0; k < n; ++k) mx = std::max(mx, std::fabs(A[(size_t)r * n + k]));
+        int e = 0;
+        if (mx > 0.0) std::frexp(mx, &e);
+        ew[r] = e;
+        for (int k = 0; k < n; ++k) {
+          double v = std::ldexp(A[(size_t)r * n + k], -e);
+          for (int i = 0; i < S; ++i) {
+            v *= 128.0;
+            const double dg = std::trunc(v);
+            v -= dg;
+            dig[((size_t)i * n + r) * n + k] = (int8_t)(int)dg;
+          }
+        }
+      }
+      NMG_TRY(h->wdig.upload(dig.data(), dig.size()));
+      NMG_TRY(h->wexp.upload(ew.data(), ew.size()));
+      NMG_TRY(h->xdig.alloc((size_t)S * B * n));
+      NMG_TRY(h->xexp.alloc(B));
+      NMG_TRY(make_digit_map(&h->mWd, h->wdig.p, S, n, n, 64));
+      NMG_TRY(make_digit_map(&h->mXd, h->xdig.p, S, (int64_t)B, n, 128));
     }
   }
   h->split_fresh.assign(h->L, 0);

@@ -1,0 +1,240 @@
+// fp64-accurate outer residual r = y - X W^T (PAPER.md P:312-313 outer iteration, stop rule
+// P:479) emulated with EXACT integer products on the tcgen05 INT8 tensor cores (Ozaki-style
+// digit splitting):
+//   x_mk = 2^{ex_m} sum_{i=1..S} X_i[m][k] 2^{-7 i},   W_nk = 2^{ew_n} sum_{j=1..S} W_j[n][k] 2^{-7 j}
+// with int8 digits |X_i|, |W_j| <= 127 (truncation of the scaled mantissa, so every digit and
+// the remainder 2^{-7 S} are exact), and
+//   (X W^T)_mn = 2^{ex_m + ew_n} sum_{d=2}^{S+1} 2^{-7 d} sum_{i+j=d} (X_i W_j^T)_mn
+// (pairs with i + j > S + 1 contribute below the digit truncation and are dropped).  Each
+// X_i W_j^T is an exact int32 GEMM (K 127^2 (S) < 2^31); the diagonals d are accumulated in
+// separate TMEM int32 accumulators and combined in fp64 in the epilogue, fused with y - (.),
+// the fp32 copy for the inner cycle and the per-row ||r||^2 partials.
+// S = 7 digits: 49 bits per operand relative to the row maximum.
+#include <cuda.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace nmg {
+namespace {
+
+constexpr int OS = 7;                       // digits per operand
+constexpr int NDIAG = OS;                   // diagonals d = 2 .. OS + 1
+constexpr int OBM = 128, OBN = 64, OBK = 64, ONSTAGE = 2, ONT = 128;
+constexpr int XS_BYTES = OS * OBM * OBK;    // 56 KB
+constexpr int WS_BYTES = OS * OBN * OBK;    // 28 KB
+constexpr int OSTAGE = XS_BYTES + WS_BYTES;
+constexpr int OZ_SMEM = ONSTAGE * OSTAGE + 256 + 1024;
+
+NMG_D uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+NMG_D void mb_init(uint64_t* b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(c));
+}
+NMG_D void mb_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes));
+}
+NMG_D void mb_wait(uint64_t* b, uint32_t ph) {
+  asm volatile(
+      "{\n.reg .pred P1;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE_%=;\nbra WAIT_%=;\nDONE_%=:\n}\n" ::"r"(su32(b)),
+      "r"(ph));
+}
+NMG_D void tma3d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(
+          su32(dst)),
+      "l"(m), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+NMG_D uint64_t desc_sw64(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;
+  return d;
+}
+// D s32, A/B int8 (signed), K-major, N = 64, M = 128
+constexpr uint32_t kIdescI8 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OBN >> 3) << 17) |
+                              ((uint32_t)(OBM >> 4) << 24);
+NMG_D void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(kIdescI8), "r"(acc));
+}
+
+__global__ void __launch_bounds__(ONT, 1)
+    ozaki_resid_kernel(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mW,
+                       OzakiArgs a) {
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  uint8_t* sm = smraw + ((1024u - (su32(smraw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + ONSTAGE * OSTAGE);
+  uint64_t* empty = full + ONSTAGE;
+  uint64_t* done = empty + ONSTAGE;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m0 = blockIdx.y * OBM, n0 = blockIdx.x * OBN;
+  const int KT = a.K / OBK;
+
+  if (tid == 0) {
+    for (int s = 0; s < ONSTAGE; ++s) { mb_init(&full[s], 1); mb_init(&empty[s], 1); }
+    mb_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(su32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {   // TMA producer: all S digit planes of X and W for one 64-wide K block
+      for (int kt = 0; kt < KT; ++kt) {
+        const int s = kt % ONSTAGE;
+        mb_wait(&empty[s], ((uint32_t)(kt / ONSTAGE) & 1u) ^ 1u);
+        uint8_t* st = sm + s * OSTAGE;
+        mb_expect(&full[s], OSTAGE);
+        tma3d(st, &mX, &full[s], kt * OBK, m0, 0);
+        tma3d(st + XS_BYTES, &mW, &full[s], kt * OBK, n0, 0);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {   // MMA issuer: 28 digit-pair products per 32-wide K step
+      for (int kt = 0; kt < KT; ++kt) {
+        const int s = kt % ONSTAGE;
+        mb_wait(&full[s], (uint32_t)(kt / ONSTAGE) & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t xs = su32(sm + s * OSTAGE), ws = xs + XS_BYTES;
+#pragma unroll
+        for (int ks = 0; ks < OBK / 32; ++ks) {
+#pragma unroll
+          for (int i = 1; i <= OS; ++i) {
+#pragma unroll
+            for (int j = 1; j <= OS + 1 - i; ++j) {
+              const int d = i + j - 2;                       // accumulator 0 .. OS - 1
+              const uint64_t da = desc_sw64(xs + (i - 1) * OBM * OBK + ks * 32);
+              const uint64_t db = desc_sw64(ws + (j - 1) * OBN * OBK + ks * 32);
+              // the first product into diagonal d is the pair (i = 1, j = d + 1) at kt = ks = 0
+              mma_i8(tmem + (uint32_t)(d * OBN), da, db, (kt == 0 && ks == 0 && i == 1) ? 0u : 1u);
+            }
+          }
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                         su32(&empty[s]))
+                     : "memory");
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(done))
+                   : "memory");
+    }
+    __syncwarp();
+  }
+  // ---------------- epilogue: warp w owns rows 32 w .. 32 w + 31 (TMEM lanes)
+  mb_wait(done, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const int m = m0 + warp * 32 + lane;
+  double acc[OBN];
+#pragma unroll
+  for (int c = 0; c < OBN; ++c) acc[c] = 0.0;
+#pragma unroll
+  for (int d = OS - 1; d >= 0; --d) {          // smallest terms first
+    const double sc = ldexp(1.0, -7 * (d + 2));
+#pragma unroll
+    for (int half = 0; half < OBN / 32; ++half) {
+      uint32_t v[32];
+      const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(d * OBN + half * 32);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+            "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+            "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc[half * 32 + j] = fma((double)(int)v[j], sc, acc[half * 32 + j]);
+    }
+  }
+  double sq = 0.0;
+  if (m < a.M) {
+    const int exm = a.ex[m];
+    const double* yr = a.Y + (int64_t)m * a.ldy + n0;
+    float* r32 = a.r32 ? a.r32 + (int64_t)m * a.ldr32 + n0 : nullptr;
+    double* r64 = a.r64 ? a.r64 + (int64_t)m * a.ldr64 + n0 : nullptr;
+#pragma unroll
+    for (int c = 0; c < OBN; ++c) {
+      const double v = yr[c] - ldexp(acc[c], exm + a.ew[n0 + c]);
+      if (r32) r32[c] = (float)v;
+      if (r64) r64[c] = v;
+      sq += v * v;
+    }
+    if (a.part) a.part[(int64_t)m * gridDim.x + blockIdx.x] = sq;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+}
+
+// digits of the rows of X (fp64 [M][K]): ex[m] with max_k |x_mk| < 2^{ex[m]}, then S truncation
+// digits of x * 2^{-ex}; one CTA per row.  Layout of `dig`: [S][M][K] int8.
+__global__ void __launch_bounds__(256) ozaki_split_rows_kernel(int M, int K, const double* __restrict__ X, int64_t ldx,
+                                                               int8_t* __restrict__ dig, int64_t plane,
+                                                               int* __restrict__ ex) {
+  __shared__ double red[32];
+  const int m = blockIdx.x;
+  const double* xr = X + (int64_t)m * ldx;
+  double mx = 0.0;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) mx = fmax(mx, fabs(xr[k]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t = fmax(t, __shfl_xor_sync(0xffffffffu, t, o));
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  mx = red[0];
+  int e = 0;
+  if (mx > 0.0) { frexp(mx, &e); }             // mx in [2^{e-1}, 2^e)
+  if (threadIdx.x == 0) ex[m] = e;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    double r = ldexp(xr[k], -e);               // |r| < 1
+#pragma unroll
+    for (int i = 0; i < OS; ++i) {
+      r *= 128.0;
+      const double dgt = trunc(r);             // |dgt| <= 127
+      r -= dgt;
+      dig[(int64_t)i * plane + (int64_t)m * K + k] = (int8_t)(int)dgt;
+    }
+  }
+}
+
+}  // namespace
+
+int ozaki_digits() { return OS; }
+
+void ozaki_split_rows(int M, int K, const double* X, int64_t ldx, int8_t* dig, int64_t plane, int* ex,
+                      cudaStream_t s) {
+  ozaki_split_rows_kernel<<<M, 256, 0, s>>>(M, K, X, ldx, dig, plane, ex);
+}
+
+void ozaki_resid(const CUtensorMap* mx, const CUtensorMap* mw, const OzakiArgs& a, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(ozaki_resid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM);
+    attr = true;
+  }
+  dim3 grid(a.N / OBN, ceil_div(a.M, OBM));
+  ozaki_resid_kernel<<<grid, ONT, OZ_SMEM, s>>>(*mx, *mw, a);
+}
+
+}  // namespace nmg

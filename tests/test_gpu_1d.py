@@ -175,6 +175,23 @@ def test_outer_residual_fp64(cfg0, cfg1):
         assert np.allclose(rr.cpu().numpy(), np.linalg.norm(want, axis=1) / np.linalg.norm(y, axis=1), rtol=1e-12)
 
 
+def test_outer_residual_wide_dynamic_range(cfg1):
+    """The fp64 residual is emulated with exact int8 digit products (7 digits per operand,
+    per-row exponents): entries spanning 11 decades in one row still give a residual within
+    1e-12 of the fp64 oracle, relative to ||y|| + ||A|| ||x||."""
+    f, W, H, h = cfg1
+    rng = np.random.default_rng(6)
+    nrhs = 3
+    x = rng.standard_normal((nrhs, CFG1.n)) * 10.0 ** rng.uniform(-8, 3, size=(nrhs, CFG1.n))
+    y = O.apply_A(H, 0, x) + 1e-6 * rng.standard_normal((nrhs, CFG1.n))   # near-converged
+    r = torch.zeros(nrhs, CFG1.n, dtype=torch.float64, device=DEV)
+    h.residual(T(y, torch.float64), T(x, torch.float64), r, None)
+    want = y - O.apply_A(H, 0, x)
+    scale = np.linalg.norm(y, axis=1) + np.abs(H.A[0]).sum(1).max() * np.abs(x).max(axis=1)
+    err = np.linalg.norm(r.cpu().numpy() - want, axis=1) / scale
+    assert err.max() < 1e-12, err
+
+
 def test_inner_cycle_from_zero(cfg0):
     """NMGF(0, y) in fp32 vs the oracle's fp64 cycle (whole inner V-cycle)."""
     f, W, H, h = cfg0

@@ -100,7 +100,7 @@ def test_fallback_kernels_match(env, tmp_path):
         "import sys; sys.path.insert(0, '.');"
         "import numpy as np, torch, nmg_inputs as ni;"
         "from tests._setup import *; from oracle import nmg_oracle as O;"
-        "cfg = (ni.CONFIGS[0] if 'SMOOTH1D' in %r else ni.CONFIGS[2].replace(n=64, levels=3, nrhs=2));"
+        "cfg = (ni.CONFIGS[0].replace(nrhs=2) if 'SMOOTH1D' in %r else ni.CONFIGS[2].replace(n=64, levels=3, nrhs=2));"
         "f = ni.operator_factors(cfg); W = weights_for(cfg, 'seed');"
         "H = oracle_hierarchy(cfg, f, W); h = gpu_hierarchy(cfg, f, W, max_rhs=2);"
         "y, _ = ni.make_rhs(cfg, f, cfg.alpha);"
