@@ -14,7 +14,7 @@ def main():
     h = nmg.Hierarchy(1, cfg.n, cfg.levels, cfg.alpha, f, max_rhs=1024)
     for l, w in enumerate(ni.weights_seed(cfg)):
         h.load_weights(l + 1, ni.cnn_arch(cfg), w)
-    for lvl in (1, 2):
+    for lvl in (1, 2, 3, 4, 5):
         n = cfg.n >> (lvl - 1)
         b = torch.randn(1024, n, device="cuda")
         x = torch.zeros_like(b)
