@@ -111,7 +111,8 @@ void coarse_chol_solve(int nc, int nrhs, const double* Lrow, const double* Lcol,
                        float* xh = nullptr, float* xl = nullptr);
 
 // ---- outer (fp64) helpers --------------------------------------------------------
-void row_norms_f64(int nrhs, int N, const double* y, int64_t ldy, double* out, cudaStream_t s);
+void row_norms_f64(int nrhs, int N, const double* y, int64_t ldy, double* out, double* work /*[nrhs][64]*/,
+                   cudaStream_t s);
 void relres_finalize(int nrhs, int ntiles, const double* part, const double* ynorm, double* relres,
                      double tol, uint8_t* active, cudaStream_t s, int rows_per_rhs = 1);
 void update_x(int nrhs, int N, double* x, int64_t ldx, const float* d, int64_t ldd,

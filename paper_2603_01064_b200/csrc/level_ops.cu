@@ -173,24 +173,41 @@ __global__ void __launch_bounds__(256) coarse_smem_kernel(int nc, int nrhs, cons
 }
 
 // ---- fp64 outer helpers ----------------------------------------------------------
-__global__ void __launch_bounds__(256) row_norms_kernel(int N, const double* __restrict__ y, int64_t ldy,
-                                                        double* __restrict__ out) {
+// per-RHS ||y||_2 in fp64: stage 1 chunk partials (grid chunks x nrhs), stage 2 fixed-order sum
+__global__ void __launch_bounds__(256) row_sumsq_partial_kernel(int64_t N, int chunks, const double* __restrict__ y,
+                                                                int64_t ldy, double* __restrict__ part) {
   __shared__ double red[32];
-  const double* r = y + (int64_t)blockIdx.x * ldy;
+  const int b = blockIdx.y, ch = blockIdx.x;
+  const int64_t len = ceil_div64(N, chunks);
+  const int64_t lo = ch * len, hi = min(N, lo + len);
+  const double* r = y + (int64_t)b * ldy;
   double s = 0.0;
-  for (int j = threadIdx.x; j < N; j += blockDim.x) s += r[j] * r[j];
+  for (int64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) s += r[j] * r[j];
   s = block_sum_f64(s, red);
-  if (threadIdx.x == 0) out[blockIdx.x] = sqrt(s);
+  if (threadIdx.x == 0) part[(int64_t)b * chunks + ch] = s;
+}
+__global__ void __launch_bounds__(256) row_norms_final_kernel(int chunks, const double* __restrict__ part,
+                                                              double* __restrict__ out) {
+  __shared__ double red[32];
+  const int b = blockIdx.x;
+  double s = 0.0;
+  for (int c = threadIdx.x; c < chunks; c += blockDim.x) s += part[(int64_t)b * chunks + c];
+  s = block_sum_f64(s, red);
+  if (threadIdx.x == 0) out[b] = sqrt(s);
 }
 
-__global__ void relres_kernel(int nrhs, int ntiles, const double* __restrict__ part,
-                              const double* __restrict__ ynorm, double* __restrict__ relres, double tol,
-                              uint8_t* __restrict__ active, int rows_per_rhs) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= nrhs) return;
-  double s = 0.0;
+// relres = sqrt(sum of the residual GEMM's ||r||^2 partials) / ||y||, one block per RHS
+// (fixed-order tree => deterministic)
+__global__ void __launch_bounds__(256) relres_kernel(int ntiles, const double* __restrict__ part,
+                                                     const double* __restrict__ ynorm, double* __restrict__ relres,
+                                                     double tol, uint8_t* __restrict__ active, int rows_per_rhs) {
+  __shared__ double red[32];
+  const int b = blockIdx.x;
   const int64_t cnt = (int64_t)ntiles * rows_per_rhs;
-  for (int64_t t = 0; t < cnt; ++t) s += part[(int64_t)b * cnt + t];
+  double s = 0.0;
+  for (int64_t t = threadIdx.x; t < cnt; t += blockDim.x) s += part[(int64_t)b * cnt + t];
+  s = block_sum_f64(s, red);
+  if (threadIdx.x != 0) return;
   const double yn = ynorm[b];
   // y = 0: converged at x = 0; a non-finite ||y|| or residual propagates as NaN/Inf
   const double rr = (yn > 0.0) ? sqrt(s) / yn : (yn == 0.0 && s == 0.0 ? 0.0 : sqrt(s) / yn);
@@ -262,13 +279,16 @@ void coarse_chol_solve(int nc, int nrhs, const double* Lrow, const double* Lcol,
 #undef NMG_COARSE
 }
 
-void row_norms_f64(int nrhs, int N, const double* y, int64_t ldy, double* out, cudaStream_t s) {
-  row_norms_kernel<<<nrhs, 256, 0, s>>>(N, y, ldy, out);
+void row_norms_f64(int nrhs, int N, const double* y, int64_t ldy, double* out, double* part, cudaStream_t s) {
+  // a few chunks per RHS so that small batches of long vectors still fill the GPU; part: [nrhs][64]
+  const int chunks = (int)std::min<int64_t>(64, std::max<int64_t>(1, N / 8192));
+  row_sumsq_partial_kernel<<<dim3(chunks, nrhs), 256, 0, s>>>(N, chunks, y, ldy, part);
+  row_norms_final_kernel<<<nrhs, 64, 0, s>>>(chunks, part, out);
 }
 
 void relres_finalize(int nrhs, int ntiles, const double* part, const double* ynorm, double* relres, double tol,
                      uint8_t* active, cudaStream_t s, int rows_per_rhs) {
-  relres_kernel<<<nblk(nrhs, 128), 128, 0, s>>>(nrhs, ntiles, part, ynorm, relres, tol, active, rows_per_rhs);
+  relres_kernel<<<nrhs, rows_per_rhs > 1 ? 256 : 32, 0, s>>>(ntiles, part, ynorm, relres, tol, active, rows_per_rhs);
 }
 
 void update_x(int nrhs, int N, double* x, int64_t ldx, const float* d, int64_t ldd, const uint8_t* active,

@@ -268,7 +268,7 @@ struct nmg_hierarchy {
   int tw_n = 0;
   // workspaces
   std::vector<std::unique_ptr<DevBuf<float>>> wy, wx, wr, wb;
-  DevBuf<double> part, ynorm, relres;
+  DevBuf<double> part, ynorm, relres, ywork;
   DevBuf<uint8_t> active;
   DevBuf<double> hy, hx;   // staging for nmg_vcycles_host (lazy)
   int ntiles = 0;
@@ -975,6 +975,7 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
   h->ntiles = gemm_f64_ntiles(d.dim == 1 ? (int)h->N[0] : n);
   NMG_TRY(h->part.alloc(B * h->ntiles * (size_t)h->rows_per_rhs));
   NMG_TRY(h->ynorm.alloc(B));
+  NMG_TRY(h->ywork.alloc(B * 64));
   NMG_TRY(h->relres.alloc(B));
   NMG_TRY(h->active.alloc(B));
   NMG_CUDA(cudaDeviceSynchronize());
@@ -1066,7 +1067,7 @@ nmg_status nmg_residual(nmg_hierarchy* h, int32_t nrhs, const double* y, const d
   cudaStream_t s = (cudaStream_t)stream;
   NMG_TRY(outer_residual(h, nrhs, y, x, r, relres != nullptr, s));
   if (relres) {
-    row_norms_f64(nrhs, (int)h->N[0], y, h->N[0], h->ynorm.p, s);
+    row_norms_f64(nrhs, (int)h->N[0], y, h->N[0], h->ynorm.p, h->ywork.p, s);
     relres_finalize(nrhs, h->ntiles, h->part.p, h->ynorm.p, relres, -1.0, nullptr, s, h->rows_per_rhs);
     h->launches += 2;
   }
@@ -1080,7 +1081,7 @@ nmg_status nmg_vcycle(nmg_hierarchy* h, int32_t nrhs, const double* y, double* x
   if (!y || !x) return fail(NMG_ERR_INVALID_ARG, "null y/x");
   cudaStream_t s = (cudaStream_t)stream;
   auto body = [&]() -> nmg_status {
-    { Prof p(h, NMG_K_MISC, s); row_norms_f64(nrhs, (int)h->N[0], y, h->N[0], h->ynorm.p, s); }
+    { Prof p(h, NMG_K_MISC, s); row_norms_f64(nrhs, (int)h->N[0], y, h->N[0], h->ynorm.p, h->ywork.p, s); }
     return outer_step(h, nrhs, y, x, -1.0, false, s);
   };
   // CUDA graph: the first call with a given (nrhs, y, x, stream) runs eagerly, the second
@@ -1147,7 +1148,7 @@ nmg_status nmg_solve(nmg_hierarchy* h, int32_t nrhs, const double* y, double* x,
   NMG_CUDA(cudaEventCreate(&e0));
   NMG_CUDA(cudaEventCreate(&e1));
   NMG_CUDA(cudaEventRecord(e0, s));
-  row_norms_f64(nrhs, (int)N, y, N, h->ynorm.p, s);
+  row_norms_f64(nrhs, (int)N, y, N, h->ynorm.p, h->ywork.p, s);
   NMG_TRY(outer_residual(h, nrhs, y, x, nullptr, true, s));
   relres_finalize(nrhs, h->ntiles, h->part.p, h->ynorm.p, h->relres.p, tol, h->active.p, s, h->rows_per_rhs);
   h->launches += 2;
@@ -1208,7 +1209,7 @@ nmg_status nmg_vcycles_host(nmg_hierarchy* h, int32_t nrhs, const double* y_host
   const size_t bytes = sizeof(double) * (size_t)nrhs * h->N[0];
   NMG_CUDA(cudaMemcpyAsync(h->hy.p, y_host, bytes, cudaMemcpyHostToDevice, s));
   NMG_CUDA(cudaMemcpyAsync(h->hx.p, x_host, bytes, cudaMemcpyHostToDevice, s));
-  row_norms_f64(nrhs, (int)h->N[0], h->hy.p, h->N[0], h->ynorm.p, s);
+  row_norms_f64(nrhs, (int)h->N[0], h->hy.p, h->N[0], h->ynorm.p, h->ywork.p, s);
   h->launches++;
   for (int c = 0; c < cycles; ++c) NMG_TRY(outer_step(h, nrhs, h->hy.p, h->hx.p, -1.0, false, s));
   if (relres_host)
