@@ -234,8 +234,14 @@ def main():
     from paper_2603_01064_b200.parallel import max_over_ranks, weak_shard
 
     if world > 1:
+        ndev = torch.cuda.device_count()
+        local = local % ndev            # (test mode only: more ranks than GPUs share devices)
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("NMG_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
 
