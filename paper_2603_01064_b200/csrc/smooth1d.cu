@@ -98,7 +98,9 @@ __global__ void __launch_bounds__(NT, 3) smooth1d_kernel(Smooth1dArgs a) {
   // layer-3 role: position quad q3 = tid >> 2 (< 63), channel group cg = tid & 3 (4 channels)
   const int q3 = tid >> 2, cg = tid & 3;
 
-  for (int t0 = 0; t0 < n; t0 += T3) {
+  // layer 3 of tile k and layer 1 of tile k + 1 share one barrier phase (disjoint buffers)
+  {
+    const int t0 = 0;
     // ---- layer 1: a1[c][jj], position p = t0 - 4 + jj, zero outside [0, n); 4 positions per
     //      thread (u window of 8 via two LDS.128, one STS.128)
 #pragma unroll 1
@@ -117,7 +119,9 @@ __global__ void __launch_bounds__(NT, 3) smooth1d_kernel(Smooth1dArgs a) {
       }
       *reinterpret_cast<float4*>(a1 + o * S1 + 4 * qd) = make_float4(r[0], r[1], r[2], r[3]);
     }
-    __syncthreads();
+  }
+  __syncthreads();
+  for (int t0 = 0; t0 < n; t0 += T3) {
     // ---- layer 2: a2[o][jj2], position p = t0 - 2 + jj2; thread: 4 channels x 4 positions,
     //      weights broadcast from shared memory ([c][t][o] layout, one LDS.128 per tap)
     {
@@ -198,6 +202,27 @@ __global__ void __launch_bounds__(NT, 3) smooth1d_kernel(Smooth1dArgs a) {
             }
           }
         }
+      }
+    }
+    if (t0 + T3 < n) {
+      const int t1 = t0 + T3;
+      // ---- layer 1: a1[c][jj], position p = t1 - 4 + jj, zero outside [0, n); 4 positions per
+      //      thread (u window of 8 via two LDS.128, one STS.128)
+  #pragma unroll 1
+      for (int qd = pg; qd < W1 / 4; qd += NT / C) {
+        const float4* up = reinterpret_cast<const float4*>(u + t1 + 4 * qd);   // u[UPAD + p - 2], p = t1-4+4qd
+        const float4 ua = up[0], ub = up[1];
+        const float uw[8] = {ua.x, ua.y, ua.z, ua.w, ub.x, ub.y, ub.z, ub.w};
+        float r[4];
+  #pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int p = t1 - 2 * HALO + 4 * qd + k;
+          float acc = b0r;
+  #pragma unroll
+          for (int t = 0; t < KS; ++t) acc = fmaf(w0r[t], uw[k + t], acc);
+          r[k] = (p >= 0 && p < n) ? fmaxf(acc, 0.f) : 0.f;
+        }
+        *reinterpret_cast<float4*>(a1 + o * S1 + 4 * qd) = make_float4(r[0], r[1], r[2], r[3]);
       }
     }
     __syncthreads();
