@@ -156,4 +156,30 @@ void conv_out(int n, int nrhs, const float* in, const double* norms, const float
               float* x, bool accumulate, cudaStream_t s);
 void zero_border(int n, int nrhs, int C, float* buf, cudaStream_t s);
 
+// ---- 2D CNN, FP16x3 tcgen05 column-strip kernels (conv_strip.cu), n % 128 == 0, C = 32/48 --
+// Layers 1+2 (strip_l12): b -> a2 (scaled f16 hi/lo, [b][y][x][C]); layers 3+4 (strip_l34,
+// a2 through the 5D tensor maps) -> Q (float4 [b][y][x]: per-t1 partial sums of layer 4);
+// strip_combine: h = s (b3 + Q0(x-1) + Q1(x) + Q2(x+1)) -> Z or x.
+struct StripArgs {
+  int n, nrhs, C, ysplit;
+  const float* b;             // l12: input [nrhs][n][n]
+  const double* norms;        // l12: per-RHS ||b|| (null: 1)
+  const float* w_in;          // l12: w0 [C][9] followed by b0 [C]
+  const float* w_out;         // l34: w3 [C][9]
+  const uint16_t* wh;         // hidden-layer weights x T, f16 hi/lo, canonical [3C/8][3C][8]
+  const uint16_t* wl;
+  const float* bias;          // hidden-layer bias [C]
+  float in_scale;             // l12: S1 (a1 is split as a1 S1)
+  float out_scale;            // l12: S2 (a2 is stored as a2 S2)
+  float d_scale;              // 1 / (S T) of this layer
+  uint16_t* out_h;            // l12: a2 hi/lo
+  uint16_t* out_l;
+  float* q;                   // l34: float4 [nrhs][n][n]
+};
+int strip_ysplit(int n, int nrhs, int num_sms);
+void strip_l12(const StripArgs& a, int num_sms, cudaStream_t s);
+void strip_l34(const CUtensorMap* mh, const CUtensorMap* ml, const StripArgs& a, int num_sms, cudaStream_t s);
+void strip_combine(int n, int nrhs, const float* q, const double* norms, const float* b3, float2* Z, float* x,
+                   bool accumulate, cudaStream_t s);
+
 }  // namespace nmg

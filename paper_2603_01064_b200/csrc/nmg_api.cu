@@ -15,6 +15,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
+#include <cuda_fp16.h>
 
 #include <chrono>
 #include <cstdlib>
@@ -159,6 +160,24 @@ void split_host(const std::vector<double>& v, std::vector<float>& hi, std::vecto
   }
 }
 
+uint16_t f16_rn(float x) {
+  const __half h = __float2half_rn(x);
+  uint16_t b;
+  std::memcpy(&b, &h, 2);
+  return b;
+}
+float f16_f(uint16_t b) {
+  __half h;
+  std::memcpy(&h, &b, 2);
+  return __half2float(h);
+}
+// largest power of two S with S * bound <= 2^14 (f16 hi parts keep 2 bits of headroom)
+float pow2_scale(double bound) {
+  if (!(bound > 0.0) || !std::isfinite(bound)) return 1.0f;
+  const int e = (int)std::floor(std::log2(16384.0 / bound));
+  return std::ldexp(1.0f, std::max(-60, std::min(60, e)));
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
 nmg_status get_encoder() {
@@ -215,6 +234,22 @@ nmg_status make_act_map(CUtensorMap* m, const float* p, int64_t rows, int Wp) {
   return NMG_OK;
 }
 
+// a2 activations f16 [rhs][y][x][C] viewed as 5D {8 ch, x, C/8 chunk, y, rhs}; box
+// {8, 130, C/8, 1, 1} lands as the canonical no-swizzle K-major row buffer [C/8][130][8];
+// x = -1 and x = n are out of bounds and zero-filled (the conv's zero padding).
+nmg_status make_a2_map(CUtensorMap* m, const uint16_t* p, int n, int C, int64_t nrhs) {
+  NMG_TRY(get_encoder());
+  cuuint64_t dims[5] = {8u, (cuuint64_t)n, (cuuint64_t)(C / 8), (cuuint64_t)n, (cuuint64_t)nrhs};
+  cuuint64_t strides[4] = {(cuuint64_t)C * 2u, 16u, (cuuint64_t)n * C * 2u, (cuuint64_t)n * n * C * 2u};
+  cuuint32_t box[5] = {8u, 130u, (cuuint32_t)(C / 8), 1u, 1u};
+  cuuint32_t es[5] = {1u, 1u, 1u, 1u, 1u};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, (void*)p, dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(NMG_ERR_CUDA, "cuTensorMapEncodeTiled (a2 5D) failed (%d)", (int)r);
+  return NMG_OK;
+}
+
 }  // namespace
 
 // ======================================================================= handle
@@ -257,6 +292,14 @@ struct nmg_hierarchy {
   std::vector<std::unique_ptr<DevBuf<float>>> WA;        // per level: [layer 0 hi, lo, layer 1 hi, lo]
   std::vector<CUtensorMap> mWAh, mWAl;                   // [level * 2 + layer]
   std::vector<CUtensorMap> mA1, mA2;                     // per level activation maps
+  // 2D CNN on tcgen05 FP16x3 column-strip kernels (levels with n % 128 == 0, C = 32 / 48)
+  bool conv_bf = false;
+  int bf_C = 0, bf_chunk = 0;
+  std::vector<float> strip_sc;                           // per level: S1, T1, S2, T2
+  DevBuf<uint16_t> a2h, a2l;                             // [chunk][n][n][C] f16 hi / lo (scaled by S2)
+  DevBuf<float> qbuf;                                    // [chunk][n][n][4]
+  std::vector<CUtensorMap> mA2h, mA2l;                   // per level
+  std::vector<std::unique_ptr<DevBuf<uint16_t>>> WB;     // per level: hidden 1 hi, lo, hidden 2 hi, lo
   // coarse Cholesky factor (row-major L and L^T)
   DevBuf<double> Lrow, Lcol;
   int nc = 0;
@@ -499,6 +542,41 @@ nmg_status smooth2d(nmg_hierarchy* h, int l, int nrhs, const float* b, float* x,
     NMG_TRY(check_launch(h));
   }
   const bool filt = filter && h->d.level_filter != 0;
+  if (h->conv_bf && n % 128 == 0 && h->bf_C == h->arch.channels) {
+    const int C = h->arch.channels;
+    const float* P = h->W[l]->p;
+    const float* b1 = P + C * 9 + C + C * C * 9;
+    const float* b2 = b1 + C + C * C * 9;
+    const float* w3 = b2 + C;
+    const float* b3 = w3 + C * 9;
+    const size_t plane = (size_t)9 * C * C;
+    const uint16_t* wb = h->WB[l]->p;
+    const float* sc = &h->strip_sc[(size_t)4 * l];
+    const double* nrm = normalize ? h->snorm.p : nullptr;
+    for (int r0 = 0; r0 < nrhs; r0 += h->bf_chunk) {
+      const int cnt = std::min(h->bf_chunk, nrhs - r0);
+      const int64_t off = (int64_t)r0 * N;
+      StripArgs a{};
+      a.n = n; a.nrhs = cnt; a.C = C; a.ysplit = strip_ysplit(n, cnt, h->num_sms);
+      a.b = b + off; a.norms = nrm ? nrm + r0 : nullptr;
+      a.w_in = P; a.w_out = w3;
+      a.wh = wb; a.wl = wb + plane; a.bias = b1;
+      a.in_scale = sc[0]; a.out_scale = sc[2]; a.d_scale = 1.0f / (sc[0] * sc[1]);
+      a.out_h = h->a2h.p; a.out_l = h->a2l.p; a.q = h->qbuf.p;
+      { Prof p(h, NMG_K_SMOOTH, s); strip_l12(a, h->num_sms, s); }
+      a.wh = wb + 2 * plane; a.wl = wb + 3 * plane; a.bias = b2;
+      a.d_scale = 1.0f / (sc[2] * sc[3]);
+      { Prof p(h, NMG_K_SMOOTH, s); strip_l34(&h->mA2h[l], &h->mA2l[l], a, h->num_sms, s); }
+      { Prof p(h, NMG_K_SMOOTH, s);
+        strip_combine(n, cnt, h->qbuf.p, a.norms, b3, filt ? h->Z.p + off : nullptr, x + off, accumulate, s); }
+      NMG_TRY(check_launch(h));
+    }
+    if (filt) {
+      { Prof p(h, NMG_K_SMOOTH, s); filter2d(nrhs, n, h->Z.p, h->tw.p, h->tw_n, x, accumulate, s); }
+      NMG_TRY(check_launch(h));
+    }
+    return NMG_OK;
+  }
   if (h->conv_tc && h->arch.channels == 32 && n >= 8) {
     const int C = 32;
     const float* P = h->W[l]->p;
@@ -913,12 +991,19 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
     {
       const char* env = std::getenv("NMG_CONV");
       h->conv_tc = h->use_tc && !(env && std::string(env) == "ffma");
+      // FP16x3 column-strip kernels for levels with n % 128 == 0 (NMG_CONV=tf32 keeps the
+      // older 3xTF32 pixel-N kernel at every level, C = 32 only)
+      h->conv_bf = h->conv_tc && !(env && std::string(env) == "tf32");
       int sms = 0;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d.device);
       h->num_sms = sms > 0 ? sms : 148;
     }
     if (h->conv_tc) {
-      const int64_t Wp = n + 2;
+      // the 3xTF32 kernel serves the levels the BF16 strip kernels do not (n < 128)
+      int nold = 0;
+      for (int l = 0; l < h->L - 1; ++l)
+        if (!(h->conv_bf && h->n[l] % 128 == 0)) nold = std::max(nold, h->n[l]);
+      const int64_t Wp = std::max(nold, 2) + 2;
       const int64_t per = Wp * Wp * 32;                         // floats per RHS per array
       const int64_t budget = (int64_t)6 << 30;                  // floats over the 2 arrays (24 GiB)
       h->conv_chunk = (int)std::max<int64_t>(1, std::min<int64_t>(B, budget / (2 * per)));
@@ -928,6 +1013,7 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
       }
       h->mA1.resize(h->L); h->mA2.resize(h->L);
       for (int l = 0; l < h->L - 1; ++l) {
+        if (h->n[l] > nold) continue;
         const int Wl = h->n[l] + 2;
         const int64_t rows = (int64_t)h->conv_chunk * Wl;
         NMG_TRY(make_act_map(&h->mA1[l], h->act1.p, rows, Wl));
@@ -935,6 +1021,8 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
       }
       h->mWAh.resize(2 * h->L); h->mWAl.resize(2 * h->L);
       for (int l = 0; l < h->L - 1; ++l) h->WA.emplace_back(new DevBuf<float>());
+      h->mA2h.resize(h->L); h->mA2l.resize(h->L);
+      for (int l = 0; l < h->L - 1; ++l) h->WB.emplace_back(new DevBuf<uint16_t>());
     }
   }
   if (d.dim == 1) {
@@ -1015,6 +1103,79 @@ nmg_status nmg_load_smoother_weights(nmg_hierarchy* h, int32_t level, const nmg_
       off += (size_t)C * C * 9 + C;
     }
     NMG_TRY(h->W[level - 1]->upload(dev.data(), n_params));
+    if (h->conv_bf) {
+      // Scales (powers of two) from rigorous bounds: |u| <= 1 (||u||_2 = 1), |a1| <= B1,
+      // |a2| <= B2; weights of each hidden layer scaled by T so max |w T| <= 2^14.
+      double B1 = 0.0;
+      for (int c = 0; c < C; ++c) {
+        double sacc = std::fabs((double)params[(size_t)C * 9 + c]);
+        for (int t = 0; t < 9; ++t) sacc += std::fabs((double)params[(size_t)c * 9 + t]);
+        B1 = std::max(B1, sacc);
+      }
+      const size_t L1 = (size_t)C * 9 + C, L2 = L1 + (size_t)C * C * 9 + C;
+      double B2 = 0.0, wm1 = 0.0, wm2 = 0.0;
+      for (int o = 0; o < C; ++o) {
+        double sacc = 0.0;
+        for (size_t i = 0; i < (size_t)C * 9; ++i) {
+          const double w = std::fabs((double)params[L1 + (size_t)o * C * 9 + i]);
+          sacc += w;
+          wm1 = std::max(wm1, w);
+        }
+        B2 = std::max(B2, sacc * B1 + std::fabs((double)params[L1 + (size_t)C * C * 9 + o]));
+      }
+      for (size_t i = 0; i < (size_t)C * C * 9; ++i) wm2 = std::max(wm2, std::fabs((double)params[L2 + i]));
+      const float S1 = pow2_scale(B1), S2 = pow2_scale(B2), T1 = pow2_scale(wm1), T2 = pow2_scale(wm2);
+      if (h->strip_sc.size() < (size_t)4 * h->L) h->strip_sc.assign((size_t)4 * h->L, 1.0f);
+      float* sc = &h->strip_sc[(size_t)4 * (level - 1)];
+      sc[0] = S1; sc[1] = T1; sc[2] = S2; sc[3] = T2;
+      // B operand of the strip kernels: W'[n' = t2 C + o][k' = t1 C + c] = w[o][c][t2][t1] T, f16
+      // hi/lo, canonical no-swizzle K-major layout: element (n', k') at ((k'/8) N + n') 8 + k' % 8
+      const int N = 3 * C;
+      const size_t plane = (size_t)N * N;
+      std::vector<uint16_t> wb(4 * plane);
+      size_t woff = L1;
+      for (int layer = 0; layer < 2; ++layer) {
+        uint16_t* hi = wb.data() + (2 * layer) * plane;
+        uint16_t* lo = wb.data() + (2 * layer + 1) * plane;
+        const float T = layer == 0 ? T1 : T2;
+        for (int t2 = 0; t2 < 3; ++t2)
+          for (int o = 0; o < C; ++o)
+            for (int t1 = 0; t1 < 3; ++t1)
+              for (int c = 0; c < C; ++c) {
+                const float w = params[woff + (((size_t)o * C + c) * 3 + t2) * 3 + t1] * T;
+                const int np = t2 * C + o, kp = t1 * C + c;
+                const size_t at = ((size_t)(kp / 8) * N + np) * 8 + kp % 8;
+                hi[at] = f16_rn(w);
+                lo[at] = f16_rn(w - f16_f(hi[at]));
+              }
+        woff += (size_t)C * C * 9 + C;
+      }
+      NMG_TRY(h->WB[level - 1]->upload(wb.data(), wb.size()));
+      if (h->bf_C != C) {
+        // activation workspaces for one RHS chunk at the finest strip level
+        int nmax = 0;
+        for (int l = 0; l < h->L - 1; ++l)
+          if (h->n[l] % 128 == 0) nmax = std::max(nmax, h->n[l]);
+        if (nmax > 0) {
+          const int64_t px = (int64_t)nmax * nmax;
+          const int64_t per = px * C * 4 + px * 16;                     // bytes per RHS
+          const int64_t budget = (int64_t)16 << 30;
+          const int64_t B = h->d.max_rhs;
+          const int64_t cmax = std::max<int64_t>(1, std::min<int64_t>(B, budget / per));
+          const int64_t nch = (B + cmax - 1) / cmax;
+          h->bf_chunk = (int)((B + nch - 1) / nch);
+          NMG_TRY(h->a2h.alloc((size_t)h->bf_chunk * px * C));
+          NMG_TRY(h->a2l.alloc((size_t)h->bf_chunk * px * C));
+          NMG_TRY(h->qbuf.alloc((size_t)h->bf_chunk * px * 4));
+          for (int l = 0; l < h->L - 1; ++l) {
+            if (h->n[l] % 128 != 0) continue;
+            NMG_TRY(make_a2_map(&h->mA2h[l], h->a2h.p, h->n[l], C, h->bf_chunk));
+            NMG_TRY(make_a2_map(&h->mA2l[l], h->a2l.p, h->n[l], C, h->bf_chunk));
+          }
+        }
+        h->bf_C = C;
+      }
+    }
     if (h->conv_tc && C == 32) {
       // A operand of the tcgen05 conv: rows (t1, o) = 32 t1 + o (96 of 128), K blocks (t2, 16-ch chunk)
       const int NCH = 2, AM = 128, BLK = AM * 16;

@@ -168,3 +168,25 @@ def test_full_size_configs_subset(cfg_id, nrhs, cycles):
     orc = O.solve(H, y, tol=1e-300, max_cycles=cycles, freeze=False)
     ok, err = history_close(rep["history"], orc.history)
     assert ok, err
+
+
+@pytest.mark.parametrize("C,n,nrhs", [(32, 256, 3), (48, 128, 2), (48, 256, 1)])
+def test_cnn_strip_kernels(C, n, nrhs):
+    """BF16x3 column-strip CNN kernels (n % 128 == 0): several 128-pixel strips, y-split units
+    (few RHS), the first/last rows and columns (zero padding), C = 32 and 48; the CNN alone
+    (OP_CNN, no normalisation) and one smoothing step (norm + CNN + F')."""
+    cfg = ni.CONFIGS[3 if C == 48 else 2].replace(n=n, levels=4 if n == 128 else 5, nrhs=nrhs)
+    f, W, H, h = _both(cfg, max_rhs=nrhs)
+    rng = np.random.default_rng(11)
+    u = (rng.standard_normal((nrhs, n, n)) / n).astype(np.float32)
+    out = torch.zeros(nrhs, n, n, device=DEV)
+    h.debug_op(1, nmg.OP_CNN, T(u), out)
+    assert rel_l2(out.cpu().numpy(), O.cnn_forward(H.weights[0], u.astype(np.float64))) < 1e-5
+    b = (3.0 * rng.standard_normal((nrhs, n, n))).astype(np.float32)
+    x0 = rng.standard_normal((nrhs, n, n)).astype(np.float32)
+    xs = T(x0)
+    h.debug_op(1, nmg.OP_SMOOTH, T(b), xs)
+    s = np.sqrt((b.astype(np.float64) ** 2).sum(axis=(1, 2)))[:, None, None]
+    hv = O.cnn_forward(H.weights[0], b / s) * s
+    want = x0 + O.level_filter(H, 0, hv)
+    assert rel_l2(xs.cpu().numpy() - x0, want - x0) < 1e-5
