@@ -31,8 +31,8 @@
 // dropped Al Bl term and the representation error are ~2^-22 relative per product (BF16x3
 // would be 2^-17, which the filtered smoothing increment amplifies past 1e-5).
 //
-// Warp roles (768 threads, one CTA per SM): warps 0-4 producer, warp 5 MMA issuer, warps
-// 8-23 epilogue (warp w reads TMEM lanes 32 (w % 4).., channel group (w - 8) / 4 of 4).
+// Warp roles (448 threads, one CTA per SM): warps 0-7 epilogue (warp w reads TMEM lanes
+// 32 (w % 4).., channel half w / 4), warps 8-12 producer, warp 13 MMA issuer.
 #include <cuda.h>
 #include <cuda_fp16.h>
 
@@ -47,15 +47,16 @@ namespace {
 constexpr int SEG = 128;        // pixels per strip (MMA M)
 constexpr int RP = SEG + 2;     // rows of the activation buffer (x halo)
 constexpr int NSTG = 3;         // activation ring depth
-constexpr int NTHR = 768;
-constexpr int EPI0 = 8;         // first epilogue warp
-constexpr int NGRP = 4;         // epilogue channel groups
+constexpr int NTHR = 448;
+constexpr int NGRP = 2;         // epilogue channel groups
+constexpr int PROD0 = 8;        // first producer warp
+constexpr int MMAW = 13;        // MMA warp
 
 template <int C>
 struct Cfg {
   static constexpr int N = 3 * C;                       // (t2, o)
   static constexpr int K = 3 * C;                       // (t1, c)
-  static constexpr int CG = C / NGRP;                   // channels per epilogue thread (8 / 12)
+  static constexpr int CG = C / NGRP;                   // channels per epilogue thread (16 / 24)
   static constexpr int WBYTES = N * K * 2;              // one weight plane (hi or lo)
   static constexpr int ABYTES = ((RP * C * 2) + 127) / 128 * 128;   // one activation row, hi or lo
   static constexpr int ALBO = RP * 16;                  // K-chunk stride of the A buffer
@@ -117,38 +118,31 @@ NMG_D void tld8(uint32_t taddr, uint32_t* r) {
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                : "r"(taddr));
 }
-NMG_D void tld4(uint32_t taddr, uint32_t* r) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"(taddr));
-}
-// tcgen05.wait::ld with 12 registers threaded through (no use can be scheduled above it)
-NMG_D void tld_wait12(uint32_t* r) {
+template <int CG>
+NMG_D void tld_wait(uint32_t* r);
+template <>
+NMG_D void tld_wait<16>(uint32_t* r) {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n"
                : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
-                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11])
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
                :
                : "memory");
 }
-NMG_D void tld_wait8(uint32_t* r) {
+template <>
+NMG_D void tld_wait<24>(uint32_t* r) {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n"
-               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7])
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]),
+                 "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23])
                :
                : "memory");
 }
-// this thread's CG columns of the three t2 slices, one wait
-template <int C, int CG>
-NMG_D void tload3(uint32_t tb, uint32_t (&r)[3][CG]) {
+// CG consecutive TMEM columns of this thread's lane
+template <int CG>
+NMG_D void tload(uint32_t taddr, uint32_t* r) {
 #pragma unroll
-  for (int t2 = 0; t2 < 3; ++t2) {
-    tld8(tb + t2 * C, r[t2]);
-    if (CG == 12) tld4(tb + t2 * C + 8, r[t2] + 8);
-  }
-#pragma unroll
-  for (int t2 = 0; t2 < 3; ++t2) {
-    if (CG == 12) tld_wait12(r[t2]);
-    else tld_wait8(r[t2]);
-  }
+  for (int j = 0; j < CG / 8; ++j) tld8(taddr + 8 * j, r + 8 * j);
+  tld_wait<CG>(r);
 }
 
 // 8 fp32 (already scaled) -> f16 hi (8) and lo (8) packed as uint4
@@ -199,9 +193,10 @@ __global__ void __launch_bounds__(NTHR, 1)
   uint64_t* dfull = empty + NSTG;                        // [2]
   uint64_t* dempty = dfull + 2;                          // [2]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + 2);
-  float* sw0 = reinterpret_cast<float*>(misc + 128);     // FIRST: w0 [C][9], b0 [C];  else w3 [C][9]
-  float* sbias = sw0 + 10 * C;                           // hidden-layer bias [C]
-  float* sxch = sbias + C;                               // !FIRST: [2][NGRP-1][128][4] partial sums
+  // FIRST: w0 transposed [t][c] then b0 [c];  else: w3 transposed [t][c]
+  float* swt = reinterpret_cast<float*>(misc + 128);
+  float* sbias = swt + 10 * C;                           // hidden-layer bias [C]
+  float* sxch = sbias + C;                               // !FIRST: [2][128][4] partial sums
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = a.n;
@@ -215,18 +210,20 @@ __global__ void __launch_bounds__(NTHR, 1)
     uint4* dl = reinterpret_cast<uint4*>(Wl);
     for (int i = tid; i < G::WBYTES / 16; i += NTHR) { dh[i] = __ldg(gh + i); dl[i] = __ldg(gl + i); }
     for (int i = tid; i < C; i += NTHR) sbias[i] = __ldg(a.bias + i);
-    if (FIRST) {
-      for (int i = tid; i < 10 * C; i += NTHR) sw0[i] = __ldg(a.w_in + i);   // w0 then b0 (contiguous)
-    } else {
-      for (int i = tid; i < 9 * C; i += NTHR) sw0[i] = __ldg(a.w_out + i);
+    const float* wsrc = FIRST ? a.w_in : a.w_out;      // [c][9]
+    for (int i = tid; i < 9 * C; i += NTHR) {
+      const int t = i / C, c = i - t * C;
+      swt[i] = __ldg(wsrc + c * 9 + t);
     }
+    if (FIRST)
+      for (int i = tid; i < C; i += NTHR) swt[9 * C + i] = __ldg(a.w_in + 9 * C + i);
   }
   if (tid == 0) {
     for (int s = 0; s < NSTG; ++s) { mb_init(&full[s], FIRST ? 5 : 1); mb_init(&empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mb_init(&dfull[s], 1); mb_init(&dempty[s], 4 * NGRP); }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  if (warp == 5) {
+  if (warp == MMAW) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tslot)),
                  "r"(G::TCOLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
@@ -239,12 +236,12 @@ __global__ void __launch_bounds__(NTHR, 1)
   // virtual input rows of a unit: [y0 - H, y1 + H - 1], H = 1 (layers 1-2) or 2 (layers 3-4)
   constexpr int H = FIRST ? 1 : 2;
 
-  if (warp < 5) {
+  if (warp >= PROD0 && warp < MMAW) {
     // ------------------------------------------------------------------ producer
     if (FIRST) {
       // thread p owns position p of the row buffer (x = X0 - 1 + p) and all C channels; a
-      // 3 x 3 window of u = b / ||b|| slides down with the rows, the next row prefetched
-      const int p = tid;
+      // 3 x 3 window of b slides down with the rows, the next row prefetched
+      const int p = tid - PROD0 * 32;
       const bool act = p < RP;
       const float sc = a.in_scale;
       int it = 0;
@@ -261,7 +258,7 @@ __global__ void __launch_bounds__(NTHR, 1)
 #pragma unroll
           for (int t1 = 0; t1 < 3; ++t1) {
             const int xx = x + t1 - 1;
-            w[t1] = (ok && xx >= 0 && xx < n) ? __ldg(row + xx) * inv : 0.f;
+            w[t1] = (ok && xx >= 0 && xx < n) ? __ldg(row + xx) : 0.f;
           }
         };
         const int r0 = max(t.y0 - H, 0), r1 = min(t.y1 + H - 1, n - 1);
@@ -272,29 +269,44 @@ __global__ void __launch_bounds__(NTHR, 1)
         for (int r = r0; r <= r1; ++r, ++it) {
           float nxt[3];
           ld3(r + 2, nxt);                       // in flight while this row is computed
+          float uu[9];
+#pragma unroll
+          for (int t2 = 0; t2 < 3; ++t2)
+#pragma unroll
+            for (int t1 = 0; t1 < 3; ++t1) uu[t2 * 3 + t1] = win[t2][t1] * inv;
           const int st = it % NSTG;
           mb_wait(&empty[st], ((uint32_t)(it / NSTG) & 1u) ^ 1u);
           if (act) {
             uint4* ah = reinterpret_cast<uint4*>(ring + st * 2 * G::ABYTES);
             uint4* al = reinterpret_cast<uint4*>(ring + st * 2 * G::ABYTES + G::ABYTES);
 #pragma unroll 1
-            for (int g = 0; g < C / 8; ++g) {
-              float v[8];
+            for (int g = 0; g < C / 16; ++g) {
+              float v[16];
 #pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const int c = g * 8 + j;
-                const float* w = sw0 + c * 9;
-                float acc = sw0[9 * C + c];
-#pragma unroll
-                for (int t2 = 0; t2 < 3; ++t2)
-#pragma unroll
-                  for (int t1 = 0; t1 < 3; ++t1) acc = fmaf(w[t2 * 3 + t1], win[t2][t1], acc);
-                v[j] = xin ? fmaxf(acc, 0.f) * sc : 0.f;
+              for (int j = 0; j < 16; j += 4) {
+                const float4 bb = *reinterpret_cast<const float4*>(swt + 9 * C + 16 * g + j);
+                v[j] = bb.x; v[j + 1] = bb.y; v[j + 2] = bb.z; v[j + 3] = bb.w;
               }
+#pragma unroll
+              for (int q9 = 0; q9 < 9; ++q9) {
+#pragma unroll
+                for (int j = 0; j < 16; j += 4) {
+                  const float4 w = *reinterpret_cast<const float4*>(swt + q9 * C + 16 * g + j);
+                  v[j] = fmaf(w.x, uu[q9], v[j]);
+                  v[j + 1] = fmaf(w.y, uu[q9], v[j + 1]);
+                  v[j + 2] = fmaf(w.z, uu[q9], v[j + 2]);
+                  v[j + 3] = fmaf(w.w, uu[q9], v[j + 3]);
+                }
+              }
+#pragma unroll
+              for (int j = 0; j < 16; ++j) v[j] = xin ? fmaxf(v[j], 0.f) * sc : 0.f;
               uint4 hi, lo;
               split8(v, hi, lo);
-              ah[g * RP + p] = hi;
-              al[g * RP + p] = lo;
+              ah[(2 * g) * RP + p] = hi;
+              al[(2 * g) * RP + p] = lo;
+              split8(v + 8, hi, lo);
+              ah[(2 * g + 1) * RP + p] = hi;
+              al[(2 * g + 1) * RP + p] = lo;
             }
           }
           asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -308,7 +320,7 @@ __global__ void __launch_bounds__(NTHR, 1)
           }
         }
       }
-    } else if (tid == 0) {
+    } else if (tid == PROD0 * 32) {
       int it = 0;
       const uint32_t bytes = 2u * (uint32_t)(RP * C * 2);
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -324,7 +336,7 @@ __global__ void __launch_bounds__(NTHR, 1)
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == MMAW) {
     // ------------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       const uint32_t wh = su32(Wh), wl = su32(Wl), rb = su32(ring);
@@ -366,10 +378,10 @@ __global__ void __launch_bounds__(NTHR, 1)
       }
     }
     __syncwarp();
-  } else if (warp >= EPI0) {
-    // ------------------------------------------------------------------ epilogue (warps 8-23)
+  } else if (warp < PROD0) {
+    // ------------------------------------------------------------------ epilogue (warps 0-7)
     const int q = warp & 3;                 // TMEM lane quarter
-    const int grp = (warp - EPI0) >> 2;     // channel group
+    const int grp = warp >> 2;              // channel half
     const int m = q * 32 + lane;            // pixel within the strip
     const int c0 = grp * CG;
     const float* bv = sbias + c0;
@@ -392,69 +404,75 @@ __global__ void __launch_bounds__(NTHR, 1)
         const bool valid = r >= 0 && r < n;
         mb_wait(&dfull[buf], (uint32_t)(k >> 1) & 1u);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        uint32_t D[3][CG];
-        if (valid) {
-          tload3<C, CG>(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * G::N + c0), D);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 3; ++i)
-#pragma unroll
-            for (int j = 0; j < CG; ++j) D[i][j] = 0u;
-        }
-        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mb_arrive(&dempty[buf]);
+        const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * G::N + c0);
         // output row r - 1 is complete: b + D_0(r - 2) + D_1(r - 1) + D_2(r)
         const int yo = r - 1;
         const bool yin = yo >= 0 && yo < n;
         float act[CG];
+        {
+          uint32_t D[CG];
+          if (valid) tload<CG>(tb + 2 * C, D);
 #pragma unroll
-        for (int j = 0; j < CG; ++j) {
-          act[j] = yin ? fmaxf(fmaf(P1[j] + __uint_as_float(D[2][j]), dsc, bv[j]), 0.f) : 0.f;
-          P1[j] = P0[j] + __uint_as_float(D[1][j]);
-          P0[j] = __uint_as_float(D[0][j]);
+          for (int j = 0; j < CG; ++j) {
+            const float d2 = valid ? __uint_as_float(D[j]) : 0.f;
+            act[j] = yin ? fmaxf(fmaf(P1[j] + d2, dsc, bv[j]), 0.f) : 0.f;
+          }
         }
+        {
+          uint32_t D[CG];
+          if (valid) tload<CG>(tb + C, D);
+#pragma unroll
+          for (int j = 0; j < CG; ++j) P1[j] = P0[j] + (valid ? __uint_as_float(D[j]) : 0.f);
+          if (valid) tload<CG>(tb, D);
+#pragma unroll
+          for (int j = 0; j < CG; ++j) P0[j] = valid ? __uint_as_float(D[j]) : 0.f;
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mb_arrive(&dempty[buf]);
         if (FIRST) {
           if (yo >= t.y0 && yo < t.y1) {
             const int64_t off = (((int64_t)t.b * n + yo) * n + x) * C + c0;
+            uint4* oh = reinterpret_cast<uint4*>(a.out_h + off);
+            uint4* ol = reinterpret_cast<uint4*>(a.out_l + off);
 #pragma unroll
-            for (int g = 0; g < CG / 4; ++g) {
+            for (int g = 0; g < CG / 8; ++g) {
               float v[8];
 #pragma unroll
-              for (int j = 0; j < 4; ++j) { v[j] = act[4 * g + j] * osc; v[4 + j] = 0.f; }
+              for (int j = 0; j < 8; ++j) v[j] = act[8 * g + j] * osc;
               uint4 hi, lo;
               split8(v, hi, lo);
-              *reinterpret_cast<uint2*>(a.out_h + off + 4 * g) = make_uint2(hi.x, hi.y);
-              *reinterpret_cast<uint2*>(a.out_l + off + 4 * g) = make_uint2(lo.x, lo.y);
+              oh[g] = hi;
+              ol[g] = lo;
             }
           }
         } else {
           // layer 4: a3 row yo feeds h rows yo + 1 (t2 = 0), yo (t2 = 1), yo - 1 (t2 = 2)
 #pragma unroll
-          for (int j = 0; j < CG; ++j) {
-            const float av = act[j];
-            const float* w = sw0 + (c0 + j) * 9;
+          for (int t2 = 0; t2 < 3; ++t2)
 #pragma unroll
-            for (int t2 = 0; t2 < 3; ++t2)
+            for (int t1 = 0; t1 < 3; ++t1) {
+              const float* w = swt + (t2 * 3 + t1) * C + c0;
+              float s4 = acc4[2 - t2][t1];
 #pragma unroll
-              for (int t1 = 0; t1 < 3; ++t1) acc4[2 - t2][t1] = fmaf(w[t2 * 3 + t1], av, acc4[2 - t2][t1]);
-          }
-          const int yh = yo - 1;               // h row yo - 1 is complete in acc4[0]
-          if (yh >= t.y0 && yh < t.y1) {       // all groups of this lane quarter take it together
-            float* xs = sxch + (erow & 1) * ((NGRP - 1) * 128 * 4);
-            if (grp > 0) {
-              *reinterpret_cast<float4*>(xs + ((grp - 1) * 128 + m) * 4) =
-                  make_float4(acc4[0][0], acc4[0][1], acc4[0][2], 0.f);
-            }
-            asm volatile("bar.sync %0, 128;\n" ::"r"(1 + q) : "memory");
-            if (grp == 0) {
-              float s0 = acc4[0][0], s1 = acc4[0][1], s2 = acc4[0][2];
-#pragma unroll
-              for (int g = 0; g < NGRP - 1; ++g) {
-                const float4 o = *reinterpret_cast<const float4*>(xs + (g * 128 + m) * 4);
-                s0 += o.x; s1 += o.y; s2 += o.z;
+              for (int j = 0; j < CG; j += 4) {
+                const float4 wv = *reinterpret_cast<const float4*>(w + j);
+                s4 = fmaf(wv.x, act[j], s4);
+                s4 = fmaf(wv.y, act[j + 1], s4);
+                s4 = fmaf(wv.z, act[j + 2], s4);
+                s4 = fmaf(wv.w, act[j + 3], s4);
               }
-              reinterpret_cast<float4*>(a.q)[((int64_t)t.b * n + yh) * n + x] = make_float4(s0, s1, s2, 0.f);
+              acc4[2 - t2][t1] = s4;
+            }
+          const int yh = yo - 1;               // h row yo - 1 is complete in acc4[0]
+          if (yh >= t.y0 && yh < t.y1) {       // both channel halves take this branch together
+            float* xs = sxch + ((erow & 1) * 128 + m) * 4;
+            if (grp == 1) *reinterpret_cast<float4*>(xs) = make_float4(acc4[0][0], acc4[0][1], acc4[0][2], 0.f);
+            asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");
+            if (grp == 0) {
+              const float4 o = *reinterpret_cast<const float4*>(xs);
+              reinterpret_cast<float4*>(a.q)[((int64_t)t.b * n + yh) * n + x] =
+                  make_float4(acc4[0][0] + o.x, acc4[0][1] + o.y, acc4[0][2] + o.z, 0.f);
             }
             ++erow;
           }
@@ -470,7 +488,7 @@ __global__ void __launch_bounds__(NTHR, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
-  if (warp == 5) {
+  if (warp == MMAW) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(G::TCOLS));
   }
 }
