@@ -92,8 +92,14 @@ struct Smooth1dArgs {
   bool accumulate;                 // x += (true) or x = (false)
   float* xh = nullptr;             // optional: tf32 hi/lo split of the updated x (for the GEMM)
   float* xl = nullptr;
+  // smooth1d_f16 only: layer-2 weights (f16 hi/lo, stacked per tap [5][2][32][8], scaled by T),
+  // a1 scale S (a1 is split as a1 S) and 1 / (S T)
+  const uint16_t* wb = nullptr;
+  float in_scale = 1.f, d_scale = 1.f;
 };
 void smooth1d(const Smooth1dArgs& a, cudaStream_t s);
+// same step with the 16 -> 16 layer on tcgen05 (FP16x3, n % 128 == 0), smooth1d_f16.cu
+void smooth1d_f16(const Smooth1dArgs& a, cudaStream_t s);
 size_t smooth1d_smem(int n);
 // same step with the 16 -> 16 layer on tcgen05 (3xTF32), smooth1d_tc.cu
 void smooth1d_tc(const Smooth1dArgs& a, cudaStream_t s);

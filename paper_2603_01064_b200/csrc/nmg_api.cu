@@ -268,7 +268,10 @@ struct nmg_hierarchy {
   std::vector<CUtensorMap> mXh, mXl;
   std::vector<char> split_fresh;                         // sxh/sxl[l] hold the split of wx[l]
   bool use_tc = true;
-  bool smooth_tc = false;                                // 1D smoother layer 2 on tcgen05 (opt-in)
+  bool smooth_tc = false;                                // 1D smoother layer 2 on tcgen05 3xTF32 (opt-in)
+  bool smooth_f16 = false;                               // 1D smoother layer 2 on tcgen05 FP16x3 (default)
+  std::vector<std::unique_ptr<DevBuf<uint16_t>>> W1b;    // per level: stacked f16 layer-2 weights
+  std::vector<float> s1d_sc;                             // per level: S1, T1
   // fp64 outer residual via int8 digit products (Ozaki-style), 1D
   bool ozaki = false;
   DevBuf<int8_t> wdig, xdig;
@@ -372,6 +375,21 @@ struct Prof {
 };
 
 // ---------------------------------------------------------------- 1D level operations
+void launch_smooth1d(nmg_hierarchy* h, int l, Smooth1dArgs& a, cudaStream_t s) {
+  if (h->smooth_f16 && a.n % 128 == 0 && h->W1b.size() > (size_t)l && h->W1b[l]->p) {
+    a.wb = h->W1b[l]->p;
+    // |u| <= 1 when normalised (||u||_2 = 1); the debug entry allows |u| <= 16
+    const float S1 = h->s1d_sc[2 * l] * (a.normalize ? 1.f : 1.f / 16.f);
+    a.in_scale = S1;
+    a.d_scale = 1.f / (S1 * h->s1d_sc[2 * l + 1]);
+    smooth1d_f16(a, s);
+  } else if (h->smooth_tc) {
+    smooth1d_tc(a, s);
+  } else {
+    smooth1d(a, s);
+  }
+}
+
 nmg_status smooth_level(nmg_hierarchy* h, int l, int nrhs, const float* b, float* x, bool accumulate,
                         cudaStream_t s) {
   Smooth1dArgs a{};
@@ -385,7 +403,7 @@ nmg_status smooth_level(nmg_hierarchy* h, int l, int nrhs, const float* b, float
   a.accumulate = accumulate;
   const bool split = x == h->wx[l]->p && h->sxh.size() > (size_t)l && h->sxh[l]->p;
   if (split) { a.xh = h->sxh[l]->p; a.xl = h->sxl[l]->p; }
-  { Prof p(h, NMG_K_SMOOTH, s); if (h->smooth_tc) smooth1d_tc(a, s); else smooth1d(a, s); }
+  { Prof p(h, NMG_K_SMOOTH, s); launch_smooth1d(h, l, a, s); }
   if (h->split_fresh.size() > (size_t)l) h->split_fresh[l] = split ? 1 : 0;
   return check_launch(h);
 }
@@ -930,6 +948,7 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
     // measured slower than the FFMA kernel (16 channels: the A tile is re-read from smem for only
     // N = 16 outputs per MMA, 32 cycles/MMA smem-bound, no overlap within the CTA): opt-in only
     h->smooth_tc = h->use_tc && (senv && std::string(senv) == "tc");
+    h->smooth_f16 = h->use_tc && !(senv && (std::string(senv) == "tc" || std::string(senv) == "ffma"));
   }
   if (d.dim == 1) {
     h->mAh.resize(h->L); h->mAl.resize(h->L); h->mAPh.resize(h->L); h->mAPl.resize(h->L);
@@ -1211,6 +1230,34 @@ nmg_status nmg_load_smoother_weights(nmg_hierarchy* h, int32_t level, const nmg_
     }
   } else {
     NMG_TRY(h->W[level - 1]->upload(params, n_params));
+    if (h->smooth_f16) {
+      // layer-2 B operand per tap t: [chunk kc][row r][j], rows 0..15 = hi(w1[o][c][t] T),
+      // rows 16..31 = lo, c = 8 kc + j; scales from |u| <= 1 and max |w1| (see conv_strip.cu)
+      const size_t L1 = (size_t)C * k + C;
+      double B1 = 0.0, wm = 0.0;
+      for (int c = 0; c < C; ++c) {
+        double acc = std::fabs((double)params[(size_t)C * k + c]);
+        for (int t = 0; t < k; ++t) acc += std::fabs((double)params[(size_t)c * k + t]);
+        B1 = std::max(B1, acc);
+      }
+      for (size_t i = 0; i < (size_t)C * C * k; ++i) wm = std::max(wm, std::fabs((double)params[L1 + i]));
+      const float S1 = pow2_scale(B1), T1 = pow2_scale(wm);
+      if (h->s1d_sc.size() < (size_t)2 * h->L) h->s1d_sc.assign((size_t)2 * h->L, 1.0f);
+      h->s1d_sc[2 * (level - 1)] = S1;
+      h->s1d_sc[2 * (level - 1) + 1] = T1;
+      std::vector<uint16_t> wb((size_t)k * 2 * 32 * 8);
+      for (int t = 0; t < k; ++t)
+        for (int o = 0; o < C; ++o)
+          for (int c = 0; c < C; ++c) {
+            const float w = params[L1 + ((size_t)o * C + c) * k + t] * T1;
+            const uint16_t hi = f16_rn(w), lo = f16_rn(w - f16_f(hi));
+            const size_t base = (size_t)t * 2 * 32 * 8 + (size_t)(c / 8) * 32 * 8 + c % 8;
+            wb[base + (size_t)o * 8] = hi;
+            wb[base + (size_t)(16 + o) * 8] = lo;
+          }
+      while (h->W1b.size() < (size_t)(h->L)) h->W1b.emplace_back(new DevBuf<uint16_t>());
+      NMG_TRY(h->W1b[level - 1]->upload(wb.data(), wb.size()));
+    }
   }
   h->w_loaded[level - 1] = 1;
   h->arch = *arch;
@@ -1435,7 +1482,7 @@ nmg_status nmg_debug_level_op(nmg_hierarchy* h, int32_t level, int32_t op, int32
       a.normalize = op == NMG_OP_SMOOTH;
       a.filter = op == NMG_OP_SMOOTH && h->d.level_filter != 0;
       a.accumulate = op == NMG_OP_SMOOTH;
-      if (h->smooth_tc) smooth1d_tc(a, s); else smooth1d(a, s);
+      launch_smooth1d(h, l, a, s);
       break;
     }
     case NMG_OP_COARSE:
