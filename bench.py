@@ -298,34 +298,39 @@ def main():
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            traffic = json.load(fh).get(dom)            # ncu dram read+write bytes per step
+            traffic = json.load(fh).get(f"cfg{cid}", {}).get(dom)   # ncu dram read+write bytes per step
     except Exception:
         pass
+    f16x3_peak = pk["bf16_tflops"] / 3.0      # f16 dense = bf16 dense rate; 3 products per fp32-accurate MAC
     if dom == "gemm64":
         peak = pk["bf16_tflops"] * FP64_NOMINAL_RATIO
         achieved = counts["gemm64"] / (step_ms * 1e-3) / 1e12
-        roof = {"kernel": "dgemm_resid_kernel (fp64 outer residual, DMMA)", "bound": "tensor", "unit": "TFLOP/s",
+        roof = {"kernel": "fp64 outer residual (Ozaki int8 tcgen05 / DMMA)", "bound": "tensor", "unit": "TFLOP/s",
                 "peak_note": "FP64 tensor: measured bf16 x nominal fp64/bf16 ratio 45/2250"}
     elif dom == "gemm32":
         peak = pk["bf16_tflops"] * TF32_NOMINAL_RATIO / 3.0
         achieved = counts["gemm32"] / (step_ms * 1e-3) / 1e12
         roof = {"kernel": "tc_gemm_kernel (3xTF32 tcgen05, all levels)", "bound": "tensor", "unit": "TFLOP/s",
                 "peak_note": "TF32 tensor (measured bf16 x 1.1/2.25) / 3 passes"}
-    elif cfg.dim == 2 and cfg.channels == 32:
-        peak = pk["bf16_tflops"] * TF32_NOMINAL_RATIO / 3.0
+    elif cfg.dim == 1:
+        peak = f16x3_peak
         achieved = counts["smooth"] / (step_ms * 1e-3) / 1e12
-        roof = {"kernel": "2D smoother: conv3x3_tc hidden layers (3xTF32 tcgen05) + FFMA first/last layers + FFT filter",
+        roof = {"kernel": "smooth1d_f16_kernel (norm, CNN with the 16->16 layer on tcgen05 FP16x3, level filter, "
+                          "update), all launches of a step",
                 "bound": "tensor", "unit": "TFLOP/s",
-                "peak_note": "TF32 tensor (measured bf16 x 1.1/2.25) / 3 passes; CNN FLOPs only"}
+                "peak_note": "FP16 dense tensor = measured bf16 dense, / 3 products per fp32-accurate MAC; "
+                             "CNN FLOPs (2880/point) only"}
     else:
-        peak = 148 * 128 * 2 * 1.965e9 / 1e12
+        peak = f16x3_peak
         achieved = counts["smooth"] / (step_ms * 1e-3) / 1e12
-        roof = {"kernel": ("smooth1d_kernel (norm + 3-layer CNN + level filter), all launches of a step"
-                           if cfg.dim == 1 else "cnn2d_kernel (FFMA 4-layer CNN) + FFT filter"),
-                "bound": "alu", "unit": "TFLOP/s",
-                "peak_note": "FP32 FFMA: 148 SM x 128 lanes x 2 FLOP x 1.965 GHz (CNN FLOPs only, 2880/point)"}
+        roof = {"kernel": "2D smoother: conv_strip_kernel (FP16x3 tcgen05, n % 128 == 0 levels), "
+                          "conv3x3_tc / cnn2d (smaller levels), FFT filter",
+                "bound": "tensor", "unit": "TFLOP/s",
+                "peak_note": "FP16 dense tensor = measured bf16 dense, / 3 products per fp32-accurate MAC; "
+                             "CNN FLOPs only"}
     roof.update({"achieved": achieved, "peak": peak, "frac": achieved / peak, "traffic": traffic,
-                 "traffic_note": "ncu dram__bytes_read+write per step, profiles/traffic.json" if traffic else None,
+                 "traffic_note": (f"ncu dram__bytes_read+write of the {dom} class per step (cfg{cid}), profiles/traffic.json"
+                                  if traffic else None),
                  "peak_source": pk["source"],
                  "share_of_step": dom_ms / tot_prof if tot_prof else None,
                  "classes_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},

@@ -89,6 +89,99 @@ NMG_D void fft_dit_inverse(float2* c, int n, const float2* __restrict__ tw, int 
   }
 }
 
+// Radix-2 stages fused R at a time in registers (R = 3, then 2 / 1 for the remainder): the
+// same butterflies with the same twiddles in the same order as fft_dif_forward /
+// fft_dit_inverse (bit-identical results), but one shared-memory pass and one barrier per R
+// stages.  Block-cooperative; each ends with __syncthreads().
+template <int R>
+NMG_D void dif_group(float2* c, int len, int g, const float2* __restrict__ tw, int tw_n) {
+  constexpr int E = 1 << R;
+  const int q = len >> R;                       // element spacing in the group
+  const int blk = g / q, pos = g - blk * q;
+  float2* base = c + blk * len + pos;
+  float2 e[E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) e[i] = base[i * q];
+#pragma unroll
+  for (int st = 0; st < R; ++st) {             // stage length len >> st, half = E >> (st + 1) elements
+    const int hs = E >> (st + 1);
+    const int step = tw_n / (len >> st);
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      if (i & hs) continue;                     // i is the upper element of its pair
+      const int posi = pos + (i & (hs - 1)) * q;   // position within the current sub-block
+      const float2 w = __ldg(tw + posi * step);
+      const float2 a = e[i], b = e[i + hs];
+      e[i] = make_float2(a.x + b.x, a.y + b.y);
+      e[i + hs] = cmul(make_float2(a.x - b.x, a.y - b.y), w);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < E; ++i) base[i * q] = e[i];
+}
+template <int R>
+NMG_D void dit_group(float2* c, int len, int g, const float2* __restrict__ tw, int tw_n) {
+  // stages len, 2 len, ..., 2^(R-1) len; group = 2^R elements spaced len/2 apart in a block of
+  // 2^(R-1) len
+  constexpr int E = 1 << R;
+  const int hq = len >> 1;
+  const int blk = g / hq, pos = g - blk * hq;
+  float2* base = c + blk * (hq << R) + pos;
+  float2 e[E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) e[i] = base[i * hq];
+#pragma unroll
+  for (int st = 0; st < R; ++st) {             // stage length len << st, pair distance 2^st elements
+    const int hs = 1 << st;
+    const int step = tw_n / (len << st);
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      if (i & hs) continue;
+      const int posi = pos + (i & (hs - 1)) * hq;
+      const float2 w = __ldg(tw + posi * step);
+      const float2 a = e[i], b = cmulc(e[i + hs], w);
+      e[i] = make_float2(a.x + b.x, a.y + b.y);
+      e[i + hs] = make_float2(a.x - b.x, a.y - b.y);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < E; ++i) base[i * hq] = e[i];
+}
+NMG_D void fft_dif_forward_fused(float2* c, int n, const float2* __restrict__ tw, int tw_n, int tid, int nthr) {
+  int len = n;
+  while (len >= 2) {
+    const int left = 31 - __clz(len);           // stages remaining
+    if (left >= 3) {
+      for (int g = tid; g < (n >> 3); g += nthr) dif_group<3>(c, len, g, tw, tw_n);
+      len >>= 3;
+    } else if (left == 2) {
+      for (int g = tid; g < (n >> 2); g += nthr) dif_group<2>(c, len, g, tw, tw_n);
+      len >>= 2;
+    } else {
+      for (int g = tid; g < (n >> 1); g += nthr) dif_group<1>(c, len, g, tw, tw_n);
+      len >>= 1;
+    }
+    __syncthreads();
+  }
+}
+NMG_D void fft_dit_inverse_fused(float2* c, int n, const float2* __restrict__ tw, int tw_n, int tid, int nthr) {
+  int len = 2;
+  while (len <= n) {
+    const int left = 31 - __clz(n / len) + 1;   // stages remaining (len .. n)
+    if (left >= 3) {
+      for (int g = tid; g < (n >> 3); g += nthr) dit_group<3>(c, len, g, tw, tw_n);
+      len <<= 3;
+    } else if (left == 2) {
+      for (int g = tid; g < (n >> 2); g += nthr) dit_group<2>(c, len, g, tw, tw_n);
+      len <<= 2;
+    } else {
+      for (int g = tid; g < (n >> 1); g += nthr) dit_group<1>(c, len, g, tw, tw_n);
+      len <<= 1;
+    }
+    __syncthreads();
+  }
+}
+
 // Level mask m'_l in natural DFT order (reading R5): sqrt(2 min(k, n-k) / n).
 NMG_D float level_mask_1d(int k, int n) {
   const int m = min(k, n - k);
@@ -104,7 +197,7 @@ NMG_D void real_level_filter(float* hbuf, int n, const float2* __restrict__ tw, 
   float2* z = reinterpret_cast<float2*>(hbuf);
   const int m = n >> 1;
   __syncthreads();
-  if (m >= 2) fft_dif_forward(z, m, tw, tw_n, tid, nthr);       // Z in bit-reversed order
+  if (m >= 2) fft_dif_forward_fused(z, m, tw, tw_n, tid, nthr);   // Z in bit-reversed order
   const int lm = (m >= 2) ? 31 - __clz(m) : 0;
   const int wstep = tw_n / n;                                     // W_n^k = tw[k * wstep]
   // pair (k, m - k): unpack H, apply the mask, repack for the inverse
@@ -138,7 +231,7 @@ NMG_D void real_level_filter(float* hbuf, int n, const float2* __restrict__ tw, 
     z[pk] = Zk2;
   }
   __syncthreads();
-  if (m >= 2) fft_dit_inverse(z, m, tw, tw_n, tid, nthr);        // natural order, unnormalised
+  if (m >= 2) fft_dit_inverse_fused(z, m, tw, tw_n, tid, nthr);  // natural order, unnormalised
 }
 
 }  // namespace nmg

@@ -1,13 +1,15 @@
 #!/usr/bin/env python
 """Aggregate an ncu CSV (metrics dram__bytes_read.sum, dram__bytes_write.sum, gpu__time_duration.sum)
 of `bench.py --steps 1` into per-kernel-class DRAM bytes of ONE step (the last `per_step` launches of
-the library) and write profiles/traffic.json.  Usage: ncu_traffic.py CSV PER_STEP_LAUNCHES OUT"""
+the library) and merge them into profiles/traffic.json under the key KEY (e.g. "cfg1").
+Usage: ncu_traffic.py CSV PER_STEP_LAUNCHES OUT KEY"""
 import collections
 import csv
 import json
 import sys
 
-CLASS = [("dgemm", "gemm64"), ("tc_gemm", "gemm32"), ("sgemm", "gemm32"), ("smooth1d", "smooth"),
+CLASS = [("dgemm", "gemm64"), ("ozaki", "gemm64"), ("row_sumsq", "misc"), ("tc_gemm", "gemm32"),
+         ("sgemm", "gemm32"), ("smooth1d", "smooth"), ("strip", "smooth"),
          ("cnn2d", "smooth"), ("conv", "smooth"), ("fft", "smooth"), ("sumsq", "smooth"),
          ("restrict", "transfer"), ("prolong", "transfer"), ("coarse", "coarse")]
 
@@ -19,7 +21,7 @@ def cls(name):
     return "misc"
 
 
-def main(path, per_step, out):
+def main(path, per_step, out, key):
     rows = list(csv.reader(open(path)))
     h = [r for r in rows if "Kernel Name" in r][0]
     hi = rows.index(h)
@@ -41,10 +43,17 @@ def main(path, per_step, out):
         c["s"] += L.get("gpu__time_duration.sum", 0)
         c["n"] += 1
     res = {k: v["bytes"] for k, v in agg.items()}
-    json.dump(res, open(out, "w"), indent=1)
+    try:
+        allres = json.load(open(out))
+    except Exception:
+        allres = {}
+    if not all(isinstance(v, dict) for v in allres.values()):
+        allres = {}
+    allres[key] = res
+    json.dump(allres, open(out, "w"), indent=1)
     for k, v in agg.items():
         print(f"{k:9s} launches {v['n']:3d}  dram {v['bytes'] / 1e6:10.1f} MB  time {v['s'] * 1e3:8.3f} ms (cold, serialised)")
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]), sys.argv[3])
+    main(sys.argv[1], int(sys.argv[2]), sys.argv[3], sys.argv[4])
