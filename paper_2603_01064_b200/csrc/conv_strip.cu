@@ -1,5 +1,6 @@
 // 2D CNN smoother (reading R7: conv(1->C) ReLU conv(C->C) ReLU conv(C->C) ReLU conv(C->1),
-// 3x3, zero "same" padding, bias) for levels with n % 128 == 0, C = 32 or 48: two persistent
+// 3x3, zero "same" padding, bias), C = 32 or 48, n % 128 == 0 (n < 128: one strip per image
+// row, the 128 - n pixels beyond the row are zero padding and not stored): two persistent
 // tcgen05 kernels with FP16x3 products on power-of-two-scaled operands (fp32-accurate).
 //
 // Pixels sit on the MMA M axis (128 consecutive pixels x = X0..X0+127 of one image row y);
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(NTHR, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = a.n;
-  const int nx = n / SEG;
+  const int nx = n >= SEG ? n / SEG : 1;   // n < 128: one strip, pixels x >= n are padding
   const int units = a.nrhs * nx * a.ysplit;
 
   {
@@ -431,7 +432,7 @@ __global__ void __launch_bounds__(NTHR, 1)
         __syncwarp();
         if (lane == 0) mb_arrive(&dempty[buf]);
         if (FIRST) {
-          if (yo >= t.y0 && yo < t.y1) {
+          if (yo >= t.y0 && yo < t.y1 && x < n) {
             const int64_t off = (((int64_t)t.b * n + yo) * n + x) * C + c0;
             uint4* oh = reinterpret_cast<uint4*>(a.out_h + off);
             uint4* ol = reinterpret_cast<uint4*>(a.out_l + off);
@@ -469,7 +470,7 @@ __global__ void __launch_bounds__(NTHR, 1)
             float* xs = sxch + ((erow & 1) * 128 + m) * 4;
             if (grp == 1) *reinterpret_cast<float4*>(xs) = make_float4(acc4[0][0], acc4[0][1], acc4[0][2], 0.f);
             asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");
-            if (grp == 0) {
+            if (grp == 0 && x < n) {
               const float4 o = *reinterpret_cast<const float4*>(xs);
               reinterpret_cast<float4*>(a.q)[((int64_t)t.b * n + yh) * n + x] =
                   make_float4(acc4[0][0] + o.x, acc4[0][1] + o.y, acc4[0][2] + o.z, 0.f);
@@ -522,7 +523,7 @@ void launch(const CUtensorMap* mh, const CUtensorMap* ml, const StripArgs& a, in
     cudaFuncSetAttribute(conv_strip_kernel<C, FIRST>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
     attr = true;
   }
-  const int units = a.nrhs * (a.n / SEG) * a.ysplit;
+  const int units = a.nrhs * (a.n >= SEG ? a.n / SEG : 1) * a.ysplit;
   const int grid = std::min(units, num_sms);
   CUtensorMap dummy{};
   conv_strip_kernel<C, FIRST><<<grid, NTHR, G::SMEM, s>>>(mh ? *mh : dummy, ml ? *ml : dummy, a);
@@ -531,7 +532,7 @@ void launch(const CUtensorMap* mh, const CUtensorMap* ml, const StripArgs& a, in
 }  // namespace
 
 int strip_ysplit(int n, int nrhs, int num_sms) {
-  const int strips = nrhs * (n / SEG);
+  const int strips = nrhs * (n >= SEG ? n / SEG : 1);
   int ys = 1;
   while (strips * ys < 4 * num_sms && ys < n / 32) ys *= 2;
   return ys;

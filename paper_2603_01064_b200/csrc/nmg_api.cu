@@ -340,6 +340,9 @@ struct nmg_hierarchy {
 
 namespace {
 
+// levels served by the column-strip CNN kernels (conv_strip.cu)
+inline bool strip_level(int n) { return n % 128 == 0 || (n >= 16 && n < 128); }
+
 nmg_status check_launch(nmg_hierarchy* h) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -560,7 +563,7 @@ nmg_status smooth2d(nmg_hierarchy* h, int l, int nrhs, const float* b, float* x,
     NMG_TRY(check_launch(h));
   }
   const bool filt = filter && h->d.level_filter != 0;
-  if (h->conv_bf && n % 128 == 0 && h->bf_C == h->arch.channels) {
+  if (h->conv_bf && strip_level(n) && h->bf_C == h->arch.channels) {
     const int C = h->arch.channels;
     const float* P = h->W[l]->p;
     const float* b1 = P + C * 9 + C + C * C * 9;
@@ -1021,7 +1024,7 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
       // the 3xTF32 kernel serves the levels the BF16 strip kernels do not (n < 128)
       int nold = 0;
       for (int l = 0; l < h->L - 1; ++l)
-        if (!(h->conv_bf && h->n[l] % 128 == 0)) nold = std::max(nold, h->n[l]);
+        if (!(h->conv_bf && strip_level(h->n[l]))) nold = std::max(nold, h->n[l]);
       const int64_t Wp = std::max(nold, 2) + 2;
       const int64_t per = Wp * Wp * 32;                         // floats per RHS per array
       const int64_t budget = (int64_t)6 << 30;                  // floats over the 2 arrays (24 GiB)
@@ -1174,7 +1177,7 @@ nmg_status nmg_load_smoother_weights(nmg_hierarchy* h, int32_t level, const nmg_
         // activation workspaces for one RHS chunk at the finest strip level
         int nmax = 0;
         for (int l = 0; l < h->L - 1; ++l)
-          if (h->n[l] % 128 == 0) nmax = std::max(nmax, h->n[l]);
+          if (strip_level(h->n[l])) nmax = std::max(nmax, h->n[l]);
         if (nmax > 0) {
           const int64_t px = (int64_t)nmax * nmax;
           const int64_t per = px * C * 4 + px * 16;                     // bytes per RHS
@@ -1187,7 +1190,7 @@ nmg_status nmg_load_smoother_weights(nmg_hierarchy* h, int32_t level, const nmg_
           NMG_TRY(h->a2l.alloc((size_t)h->bf_chunk * px * C));
           NMG_TRY(h->qbuf.alloc((size_t)h->bf_chunk * px * 4));
           for (int l = 0; l < h->L - 1; ++l) {
-            if (h->n[l] % 128 != 0) continue;
+            if (!strip_level(h->n[l])) continue;
             NMG_TRY(make_a2_map(&h->mA2h[l], h->a2h.p, h->n[l], C, h->bf_chunk));
             NMG_TRY(make_a2_map(&h->mA2l[l], h->a2l.p, h->n[l], C, h->bf_chunk));
           }
