@@ -52,6 +52,7 @@ constexpr int NTHR = 448;
 constexpr int NGRP = 2;         // epilogue channel groups
 constexpr int PROD0 = 8;        // first producer warp
 constexpr int MMAW = 13;        // MMA warp
+constexpr uint32_t IDESC4 = (1u << 4) | ((uint32_t)(16 >> 3) << 17) | ((uint32_t)(SEG >> 4) << 24);  // N = 16
 
 template <int C>
 struct Cfg {
@@ -62,9 +63,13 @@ struct Cfg {
   static constexpr int ABYTES = ((RP * C * 2) + 127) / 128 * 128;   // one activation row, hi or lo
   static constexpr int ALBO = RP * 16;                  // K-chunk stride of the A buffer
   static constexpr int BLBO = N * 16;                   // K-chunk stride of the B (weight) planes
-  static constexpr int TCOLS = 2 * N <= 256 ? 256 : 512;
-  static constexpr int MISC = 16384;                    // barriers, small params, exchange
-  static constexpr int SMEM = 2 * WBYTES + NSTG * 2 * ABYTES + MISC + 1024;
+  static constexpr int TCOLS = 2 * N + 16 <= 256 ? 256 : 512;   // D double buffer + D4 (16 columns)
+  static constexpr int A4BYTES = SEG * C * 2;           // layer-4 A tile (a3 row), hi or lo
+  static constexpr int A4LBO = SEG * 16;
+  static constexpr int W4BYTES = 16 * C * 2;            // layer-4 weights [C/8][16][8], hi or lo
+  static constexpr int W4LBO = 16 * 16;
+  static constexpr int MISC = 8192;                     // barriers, small params
+  static constexpr int SMEM = 2 * WBYTES + NSTG * 2 * ABYTES + 2 * A4BYTES + 2 * W4BYTES + MISC + 1024;
   // kind::f16, D f32, A/B f16, K-major both, N, M = 128
   static constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(SEG >> 4) << 24);
 };
@@ -188,16 +193,19 @@ __global__ void __launch_bounds__(NTHR, 1)
   uint8_t* Wh = sm;
   uint8_t* Wl = Wh + G::WBYTES;
   uint8_t* ring = Wl + G::WBYTES;                        // NSTG x (hi | lo)
-  uint8_t* misc = ring + NSTG * 2 * G::ABYTES;
+  uint8_t* A4 = ring + NSTG * 2 * G::ABYTES;             // !FIRST: a3 row (hi | lo) for layer 4
+  uint8_t* W4 = A4 + 2 * G::A4BYTES;                     // !FIRST: layer-4 weights (hi | lo)
+  uint8_t* misc = W4 + 2 * G::W4BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(misc);    // [NSTG]
   uint64_t* empty = full + NSTG;                         // [NSTG]
   uint64_t* dfull = empty + NSTG;                        // [2]
   uint64_t* dempty = dfull + 2;                          // [2]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + 2);
+  uint64_t* a4full = dempty + 2;
+  uint64_t* d4full = a4full + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(d4full + 1);
   // FIRST: w0 transposed [t][c] then b0 [c];  else: w3 transposed [t][c]
   float* swt = reinterpret_cast<float*>(misc + 128);
   float* sbias = swt + 10 * C;                           // hidden-layer bias [C]
-  float* sxch = sbias + C;                               // !FIRST: [2][128][4] partial sums
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = a.n;
@@ -211,6 +219,11 @@ __global__ void __launch_bounds__(NTHR, 1)
     uint4* dl = reinterpret_cast<uint4*>(Wl);
     for (int i = tid; i < G::WBYTES / 16; i += NTHR) { dh[i] = __ldg(gh + i); dl[i] = __ldg(gl + i); }
     for (int i = tid; i < C; i += NTHR) sbias[i] = __ldg(a.bias + i);
+    if (!FIRST) {
+      const uint4* g4 = reinterpret_cast<const uint4*>(a.w4);
+      uint4* d4 = reinterpret_cast<uint4*>(W4);
+      for (int i = tid; i < 2 * G::W4BYTES / 16; i += NTHR) d4[i] = __ldg(g4 + i);
+    }
     const float* wsrc = FIRST ? a.w_in : a.w_out;      // [c][9]
     for (int i = tid; i < 9 * C; i += NTHR) {
       const int t = i / C, c = i - t * C;
@@ -222,6 +235,8 @@ __global__ void __launch_bounds__(NTHR, 1)
   if (tid == 0) {
     for (int s = 0; s < NSTG; ++s) { mb_init(&full[s], FIRST ? 5 : 1); mb_init(&empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mb_init(&dfull[s], 1); mb_init(&dempty[s], 4 * NGRP); }
+    mb_init(a4full, 4 * NGRP);
+    mb_init(d4full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == MMAW) {
@@ -237,7 +252,7 @@ __global__ void __launch_bounds__(NTHR, 1)
   // virtual input rows of a unit: [y0 - H, y1 + H - 1], H = 1 (layers 1-2) or 2 (layers 3-4)
   constexpr int H = FIRST ? 1 : 2;
 
-  if (warp >= PROD0 && warp < MMAW) {
+  if (warp >= PROD0 && warp < (FIRST ? MMAW : MMAW - 1)) {
     // ------------------------------------------------------------------ producer
     if (FIRST) {
       // thread p owns position p of the row buffer (x = X0 - 1 + p) and all C channels; a
@@ -379,6 +394,36 @@ __global__ void __launch_bounds__(NTHR, 1)
       }
     }
     __syncwarp();
+  } else if (!FIRST && warp == MMAW - 1) {
+    // ------------------------------------------------------------------ layer-4 MMA issuer
+    // (its own thread, so the layer-3 chain of the next row never waits for the epilogue)
+    if (lane == 0) {
+      const uint32_t a4h = su32(A4), a4l = a4h + G::A4BYTES, w4h = su32(W4), w4l = w4h + G::W4BYTES;
+      const uint32_t d4 = tmem + (uint32_t)(2 * G::N);
+      int e4 = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const Unit t = unit_of(u, n, nx, a.ysplit);
+        for (int r = t.y0 - H; r <= t.y1 + H - 1; ++r, ++e4) {
+          // D4[p][t2 * 3 + t1] = sum_c a3[c](p) w3[c][t2][t1] for the a3 row the epilogue wrote
+          mb_wait(a4full, (uint32_t)e4 & 1u);
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+          uint32_t acc = 0;
+#pragma unroll
+          for (int pass = 0; pass < 3; ++pass) {
+            const uint32_t A = pass == 2 ? a4l : a4h;
+            const uint32_t Bw = pass == 1 ? w4l : w4h;
+#pragma unroll
+            for (int kc = 0; kc < C / 16; ++kc) {
+              mma_f16(d4, desc_ns(A + (uint32_t)(2 * kc * G::A4LBO), G::A4LBO),
+                      desc_ns(Bw + (uint32_t)(2 * kc * G::W4LBO), G::W4LBO), IDESC4, acc);
+              acc = 1;
+            }
+          }
+          mma_commit(d4full);
+        }
+      }
+    }
+    __syncwarp();
   } else if (warp < PROD0) {
     // ------------------------------------------------------------------ epilogue (warps 0-7)
     const int q = warp & 3;                 // TMEM lane quarter
@@ -388,14 +433,66 @@ __global__ void __launch_bounds__(NTHR, 1)
     const float* bv = sbias + c0;
     const float dsc = a.d_scale;
     const float osc = a.out_scale;
-    int k = 0, erow = 0;
+    int k = 0, e4 = 0;
+    float acc4[3][3];                        // layer 4 partial rows h(ya - 1 + i) (FIRST == false)
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) acc4[i][j] = 0.f;
+    // a3 row ya went through the layer-4 MMA: h rows ya + 1 (t2 = 0), ya (t2 = 1), ya - 1 (t2 = 2)
+    // receive its contributions; h row ya - 1 is then complete
+    auto consume_d4 = [&](const Unit& t, int x, int ya) {
+      mb_wait(d4full, (uint32_t)e4 & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      ++e4;
+      if (grp == 0) {
+        uint32_t d[16];
+        tld8(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(2 * G::N), d);
+        tld8(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(2 * G::N + 8), d + 8);
+        tld_wait<16>(d);
+        const float s4 = a.d4_scale;
+#pragma unroll
+        for (int t2 = 0; t2 < 3; ++t2)
+#pragma unroll
+          for (int t1 = 0; t1 < 3; ++t1) acc4[2 - t2][t1] = fmaf(__uint_as_float(d[t2 * 3 + t1]), s4, acc4[2 - t2][t1]);
+        const int yh = ya - 1;
+        if (yh >= t.y0 && yh < t.y1 && x < n)
+          reinterpret_cast<float4*>(a.q)[((int64_t)t.b * n + yh) * n + x] =
+              make_float4(acc4[0][0], acc4[0][1], acc4[0][2], 0.f);
+#pragma unroll
+        for (int t1 = 0; t1 < 3; ++t1) {
+          acc4[0][t1] = acc4[1][t1];
+          acc4[1][t1] = acc4[2][t1];
+          acc4[2][t1] = 0.f;
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    };
+    // this thread's CG channels of the a3 row -> A4 (scaled f16 hi / lo), then signal the MMA warp
+    auto write_a4 = [&](const float* act) {
+      uint4* ah4 = reinterpret_cast<uint4*>(A4);
+      uint4* al4 = reinterpret_cast<uint4*>(A4 + G::A4BYTES);
+      const float s3 = a.a3_scale;
+#pragma unroll
+      for (int g = 0; g < CG / 8; ++g) {
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = act[8 * g + j] * s3;
+        uint4 hi, lo;
+        split8(v, hi, lo);
+        ah4[(c0 / 8 + g) * SEG + m] = hi;
+        al4[(c0 / 8 + g) * SEG + m] = lo;
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mb_arrive(a4full);
+    };
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const Unit t = unit_of(u, n, nx, a.ysplit);
       const int x = t.X0 + m;
       float P0[CG], P1[CG];
 #pragma unroll
       for (int j = 0; j < CG; ++j) { P0[j] = 0.f; P1[j] = 0.f; }
-      float acc4[3][3];                      // layer 4 partial rows (FIRST == false)
 #pragma unroll
       for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -448,43 +545,11 @@ __global__ void __launch_bounds__(NTHR, 1)
             }
           }
         } else {
-          // layer 4: a3 row yo feeds h rows yo + 1 (t2 = 0), yo (t2 = 1), yo - 1 (t2 = 2)
-#pragma unroll
-          for (int t2 = 0; t2 < 3; ++t2)
-#pragma unroll
-            for (int t1 = 0; t1 < 3; ++t1) {
-              const float* w = swt + (t2 * 3 + t1) * C + c0;
-              float s4 = acc4[2 - t2][t1];
-#pragma unroll
-              for (int j = 0; j < CG; j += 4) {
-                const float4 wv = *reinterpret_cast<const float4*>(w + j);
-                s4 = fmaf(wv.x, act[j], s4);
-                s4 = fmaf(wv.y, act[j + 1], s4);
-                s4 = fmaf(wv.z, act[j + 2], s4);
-                s4 = fmaf(wv.w, act[j + 3], s4);
-              }
-              acc4[2 - t2][t1] = s4;
-            }
-          const int yh = yo - 1;               // h row yo - 1 is complete in acc4[0]
-          if (yh >= t.y0 && yh < t.y1) {       // both channel halves take this branch together
-            float* xs = sxch + ((erow & 1) * 128 + m) * 4;
-            if (grp == 1) *reinterpret_cast<float4*>(xs) = make_float4(acc4[0][0], acc4[0][1], acc4[0][2], 0.f);
-            asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");
-            if (grp == 0 && x < n) {
-              const float4 o = *reinterpret_cast<const float4*>(xs);
-              reinterpret_cast<float4*>(a.q)[((int64_t)t.b * n + yh) * n + x] =
-                  make_float4(acc4[0][0] + o.x, acc4[0][1] + o.y, acc4[0][2] + o.z, 0.f);
-            }
-            ++erow;
-          }
-#pragma unroll
-          for (int t1 = 0; t1 < 3; ++t1) {
-            acc4[0][t1] = acc4[1][t1];
-            acc4[1][t1] = acc4[2][t1];
-            acc4[2][t1] = 0.f;
-          }
+          if (r > t.y0 - H) consume_d4(t, x, r - 2);     // the previous iteration's a3 row
+          write_a4(act);
         }
       }
+      if (!FIRST) consume_d4(t, x, t.y1);                 // the unit's last a3 row
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");

@@ -181,6 +181,9 @@ struct StripArgs {
   uint16_t* out_h;            // l12: a2 hi/lo
   uint16_t* out_l;
   float* q;                   // l34: float4 [nrhs][n][n]
+  const uint16_t* w4;         // l34: layer-4 weights x T4, f16 hi then lo, [C/8][16][8] (row t2*3+t1)
+  float a3_scale;             // l34: S3 (a3 is split as a3 S3)
+  float d4_scale;             // l34: 1 / (S3 T4)
 };
 int strip_ysplit(int n, int nrhs, int num_sms);
 void strip_l12(const StripArgs& a, int num_sms, cudaStream_t s);

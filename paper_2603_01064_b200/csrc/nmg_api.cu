@@ -572,7 +572,7 @@ nmg_status smooth2d(nmg_hierarchy* h, int l, int nrhs, const float* b, float* x,
     const float* b3 = w3 + C * 9;
     const size_t plane = (size_t)9 * C * C;
     const uint16_t* wb = h->WB[l]->p;
-    const float* sc = &h->strip_sc[(size_t)4 * l];
+    const float* sc = &h->strip_sc[(size_t)6 * l];
     const double* nrm = normalize ? h->snorm.p : nullptr;
     for (int r0 = 0; r0 < nrhs; r0 += h->bf_chunk) {
       const int cnt = std::min(h->bf_chunk, nrhs - r0);
@@ -587,6 +587,7 @@ nmg_status smooth2d(nmg_hierarchy* h, int l, int nrhs, const float* b, float* x,
       { Prof p(h, NMG_K_SMOOTH, s); strip_l12(a, h->num_sms, s); }
       a.wh = wb + 2 * plane; a.wl = wb + 3 * plane; a.bias = b2;
       a.d_scale = 1.0f / (sc[2] * sc[3]);
+      a.w4 = wb + 4 * plane; a.a3_scale = sc[4]; a.d4_scale = 1.0f / (sc[4] * sc[5]);
       { Prof p(h, NMG_K_SMOOTH, s); strip_l34(&h->mA2h[l], &h->mA2l[l], a, h->num_sms, s); }
       { Prof p(h, NMG_K_SMOOTH, s);
         strip_combine(n, cnt, h->qbuf.p, a.norms, b3, filt ? h->Z.p + off : nullptr, x + off, accumulate, s); }
@@ -1145,16 +1146,36 @@ nmg_status nmg_load_smoother_weights(nmg_hierarchy* h, int32_t level, const nmg_
         }
         B2 = std::max(B2, sacc * B1 + std::fabs((double)params[L1 + (size_t)C * C * 9 + o]));
       }
-      for (size_t i = 0; i < (size_t)C * C * 9; ++i) wm2 = std::max(wm2, std::fabs((double)params[L2 + i]));
+      double B3 = 0.0, wm4 = 0.0;
+      for (int o = 0; o < C; ++o) {
+        double sacc = 0.0;
+        for (size_t i = 0; i < (size_t)C * 9; ++i) {
+          const double w = std::fabs((double)params[L2 + (size_t)o * C * 9 + i]);
+          sacc += w;
+          wm2 = std::max(wm2, w);
+        }
+        B3 = std::max(B3, sacc * B2 + std::fabs((double)params[L2 + (size_t)C * C * 9 + o]));
+      }
+      const size_t L3 = L2 + (size_t)C * C * 9 + C;         // w3 [1][C][3][3]
+      for (size_t i = 0; i < (size_t)C * 9; ++i) wm4 = std::max(wm4, std::fabs((double)params[L3 + i]));
       const float S1 = pow2_scale(B1), S2 = pow2_scale(B2), T1 = pow2_scale(wm1), T2 = pow2_scale(wm2);
-      if (h->strip_sc.size() < (size_t)4 * h->L) h->strip_sc.assign((size_t)4 * h->L, 1.0f);
-      float* sc = &h->strip_sc[(size_t)4 * (level - 1)];
-      sc[0] = S1; sc[1] = T1; sc[2] = S2; sc[3] = T2;
+      const float S3 = pow2_scale(B3), T4 = pow2_scale(wm4);
+      if (h->strip_sc.size() < (size_t)6 * h->L) h->strip_sc.assign((size_t)6 * h->L, 1.0f);
+      float* sc = &h->strip_sc[(size_t)6 * (level - 1)];
+      sc[0] = S1; sc[1] = T1; sc[2] = S2; sc[3] = T2; sc[4] = S3; sc[5] = T4;
       // B operand of the strip kernels: W'[n' = t2 C + o][k' = t1 C + c] = w[o][c][t2][t1] T, f16
       // hi/lo, canonical no-swizzle K-major layout: element (n', k') at ((k'/8) N + n') 8 + k' % 8
       const int N = 3 * C;
       const size_t plane = (size_t)N * N;
-      std::vector<uint16_t> wb(4 * plane);
+      std::vector<uint16_t> wb(4 * plane + 2 * 16 * (size_t)C, 0);
+      // layer 4 as an MMA B operand: rows t2 * 3 + t1 (9 of 16), K = c: [C/8][16][8]
+      for (int c = 0; c < C; ++c)
+        for (int t = 0; t < 9; ++t) {
+          const float w = params[L3 + (size_t)c * 9 + t] * T4;
+          const size_t at = 4 * plane + ((size_t)(c / 8) * 16 + t) * 8 + c % 8;
+          wb[at] = f16_rn(w);
+          wb[at + 16 * (size_t)C] = f16_rn(w - f16_f(wb[at]));
+        }
       size_t woff = L1;
       for (int layer = 0; layer < 2; ++layer) {
         uint16_t* hi = wb.data() + (2 * layer) * plane;
