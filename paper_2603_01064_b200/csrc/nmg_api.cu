@@ -582,12 +582,14 @@ nmg_status smooth2d(nmg_hierarchy* h, int l, int nrhs, const float* b, float* x,
       a.b = b + off; a.norms = nrm ? nrm + r0 : nullptr;
       a.w_in = P; a.w_out = w3;
       a.wh = wb; a.wl = wb + plane; a.bias = b1;
-      a.in_scale = sc[0]; a.out_scale = sc[2]; a.d_scale = 1.0f / (sc[0] * sc[1]);
+      // |u| <= 1 when normalised (||u||_2 = 1); the debug entry allows |u| <= 16
+      const float dbg = normalize ? 1.0f : 1.0f / 16.0f;
+      a.in_scale = sc[0] * dbg; a.out_scale = sc[2] * dbg; a.d_scale = 1.0f / (sc[0] * dbg * sc[1]);
       a.out_h = h->a2h.p; a.out_l = h->a2l.p; a.q = h->qbuf.p;
       { Prof p(h, NMG_K_SMOOTH, s); strip_l12(a, h->num_sms, s); }
       a.wh = wb + 2 * plane; a.wl = wb + 3 * plane; a.bias = b2;
-      a.d_scale = 1.0f / (sc[2] * sc[3]);
-      a.w4 = wb + 4 * plane; a.a3_scale = sc[4]; a.d4_scale = 1.0f / (sc[4] * sc[5]);
+      a.d_scale = 1.0f / (sc[2] * dbg * sc[3]);
+      a.w4 = wb + 4 * plane; a.a3_scale = sc[4] * dbg; a.d4_scale = 1.0f / (sc[4] * dbg * sc[5]);
       { Prof p(h, NMG_K_SMOOTH, s); strip_l34(&h->mA2h[l], &h->mA2l[l], a, h->num_sms, s); }
       { Prof p(h, NMG_K_SMOOTH, s);
         strip_combine(n, cnt, h->qbuf.p, a.norms, b3, filt ? h->Z.p + off : nullptr, x + off, accumulate, s); }
