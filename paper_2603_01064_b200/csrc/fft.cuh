@@ -94,14 +94,14 @@ NMG_D void fft_dit_inverse(float2* c, int n, const float2* __restrict__ tw, int 
 // fft_dit_inverse (bit-identical results), but one shared-memory pass and one barrier per R
 // stages.  Block-cooperative; each ends with __syncthreads().
 template <int R>
-NMG_D void dif_group(float2* c, int len, int g, const float2* __restrict__ tw, int tw_n) {
+NMG_D void dif_group(float2* c, int len, int g, const float2* __restrict__ tw, int tw_n, int stride = 1) {
   constexpr int E = 1 << R;
   const int q = len >> R;                       // element spacing in the group
   const int blk = g / q, pos = g - blk * q;
-  float2* base = c + blk * len + pos;
+  float2* base = c + (blk * len + pos) * stride;
   float2 e[E];
 #pragma unroll
-  for (int i = 0; i < E; ++i) e[i] = base[i * q];
+  for (int i = 0; i < E; ++i) e[i] = base[i * q * stride];
 #pragma unroll
   for (int st = 0; st < R; ++st) {             // stage length len >> st, half = E >> (st + 1) elements
     const int hs = E >> (st + 1);
@@ -117,19 +117,19 @@ NMG_D void dif_group(float2* c, int len, int g, const float2* __restrict__ tw, i
     }
   }
 #pragma unroll
-  for (int i = 0; i < E; ++i) base[i * q] = e[i];
+  for (int i = 0; i < E; ++i) base[i * q * stride] = e[i];
 }
 template <int R>
-NMG_D void dit_group(float2* c, int len, int g, const float2* __restrict__ tw, int tw_n) {
+NMG_D void dit_group(float2* c, int len, int g, const float2* __restrict__ tw, int tw_n, int stride = 1) {
   // stages len, 2 len, ..., 2^(R-1) len; group = 2^R elements spaced len/2 apart in a block of
   // 2^(R-1) len
   constexpr int E = 1 << R;
   const int hq = len >> 1;
   const int blk = g / hq, pos = g - blk * hq;
-  float2* base = c + blk * (hq << R) + pos;
+  float2* base = c + (blk * (hq << R) + pos) * stride;
   float2 e[E];
 #pragma unroll
-  for (int i = 0; i < E; ++i) e[i] = base[i * hq];
+  for (int i = 0; i < E; ++i) e[i] = base[i * hq * stride];
 #pragma unroll
   for (int st = 0; st < R; ++st) {             // stage length len << st, pair distance 2^st elements
     const int hs = 1 << st;
@@ -145,7 +145,48 @@ NMG_D void dit_group(float2* c, int len, int g, const float2* __restrict__ tw, i
     }
   }
 #pragma unroll
-  for (int i = 0; i < E; ++i) base[i * hq] = e[i];
+  for (int i = 0; i < E; ++i) base[i * hq * stride] = e[i];
+}
+// Batched fused passes over `cnt` independent length-n transforms: transform k starts at
+// c + k * kstride and its elements are `stride` apart (rows: kstride = n, stride = 1;
+// columns of an [n][G] tile: kstride = 1, stride = G).  Same arithmetic as the radix-2 loops.
+NMG_D void fft_dif_forward_batch(float2* c, int n, int cnt, int kstride, int stride, const float2* __restrict__ tw,
+                                 int tw_n, int tid, int nthr) {
+  int len = n;
+  while (len >= 2) {
+    const int left = 31 - __clz(len);
+    const int R = left >= 3 ? 3 : left;
+    const int per = n >> R;
+    for (int gg = tid; gg < cnt * per; gg += nthr) {
+      // strided (column) transforms: neighbouring threads take neighbouring transforms, so
+      // shared-memory accesses stay consecutive; rows: neighbouring groups of one transform
+      const int k = stride == 1 ? gg / per : gg % cnt, g = stride == 1 ? gg - k * per : gg / cnt;
+      float2* ck = c + k * kstride;
+      if (R == 3) dif_group<3>(ck, len, g, tw, tw_n, stride);
+      else if (R == 2) dif_group<2>(ck, len, g, tw, tw_n, stride);
+      else dif_group<1>(ck, len, g, tw, tw_n, stride);
+    }
+    len >>= R;
+    __syncthreads();
+  }
+}
+NMG_D void fft_dit_inverse_batch(float2* c, int n, int cnt, int kstride, int stride, const float2* __restrict__ tw,
+                                 int tw_n, int tid, int nthr) {
+  int len = 2;
+  while (len <= n) {
+    const int left = 31 - __clz(n / len) + 1;
+    const int R = left >= 3 ? 3 : left;
+    const int per = n >> R;
+    for (int gg = tid; gg < cnt * per; gg += nthr) {
+      const int k = stride == 1 ? gg / per : gg % cnt, g = stride == 1 ? gg - k * per : gg / cnt;
+      float2* ck = c + k * kstride;
+      if (R == 3) dit_group<3>(ck, len, g, tw, tw_n, stride);
+      else if (R == 2) dit_group<2>(ck, len, g, tw, tw_n, stride);
+      else dit_group<1>(ck, len, g, tw, tw_n, stride);
+    }
+    len <<= R;
+    __syncthreads();
+  }
 }
 NMG_D void fft_dif_forward_fused(float2* c, int n, const float2* __restrict__ tw, int tw_n, int tid, int nthr) {
   int len = n;

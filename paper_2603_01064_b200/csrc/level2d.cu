@@ -268,37 +268,12 @@ __global__ void __launch_bounds__(256) fft_rows_kernel(int n, int64_t nrows, flo
   const int tot = rows * n;
   for (int i = threadIdx.x; i < tot; i += 256) cb[i] = Z[r0 * n + i];
   __syncthreads();
-  // butterflies over all rows at once
-  const int halfn = n >> 1;
+  // butterflies over all rows at once (fused radix-8 passes, fft.cuh)
   if (!inverse) {
-    for (int len = n; len >= 2; len >>= 1) {
-      const int half = len >> 1, step = tw_n / len;
-      for (int i = threadIdx.x; i < rows * halfn; i += 256) {
-        const int row = i / halfn, ii = i - row * halfn;
-        const int pos = ii & (half - 1);
-        const int j0 = row * n + ((ii - pos) << 1) + pos, j1 = j0 + half;
-        const float2 w = __ldg(tw + pos * step);
-        const float2 u = cb[j0], v = cb[j1];
-        cb[j0] = make_float2(u.x + v.x, u.y + v.y);
-        cb[j1] = cmul(make_float2(u.x - v.x, u.y - v.y), w);
-      }
-      __syncthreads();
-    }
+    fft_dif_forward_batch(cb, n, rows, n, 1, tw, tw_n, threadIdx.x, 256);
     for (int i = threadIdx.x; i < tot; i += 256) Z[r0 * n + i] = cb[i];
   } else {
-    for (int len = 2; len <= n; len <<= 1) {
-      const int half = len >> 1, step = tw_n / len;
-      for (int i = threadIdx.x; i < rows * halfn; i += 256) {
-        const int row = i / halfn, ii = i - row * halfn;
-        const int pos = ii & (half - 1);
-        const int j0 = row * n + ((ii - pos) << 1) + pos, j1 = j0 + half;
-        const float2 w = __ldg(tw + pos * step);
-        const float2 u = cb[j0], v = cmulc(cb[j1], w);
-        cb[j0] = make_float2(u.x + v.x, u.y + v.y);
-        cb[j1] = make_float2(u.x - v.x, u.y - v.y);
-      }
-      __syncthreads();
-    }
+    fft_dit_inverse_batch(cb, n, rows, n, 1, tw, tw_n, threadIdx.x, 256);
     for (int i = threadIdx.x; i < tot; i += 256) {
       const float v = cb[i].x * scale;
       const int64_t o = r0 * n + i;
@@ -319,20 +294,7 @@ __global__ void __launch_bounds__(256) fft_cols_kernel(int n, int G, float2* __r
     cb[i] = Zb[(int64_t)r * n + k0 + c];
   }
   __syncthreads();
-  const int halfn = n >> 1;
-  for (int len = n; len >= 2; len >>= 1) {
-    const int half = len >> 1, step = tw_n / len;
-    for (int i = threadIdx.x; i < halfn * G; i += 256) {
-      const int c = i % G, ii = i / G;
-      const int pos = ii & (half - 1);
-      const int j0 = ((ii - pos) << 1) + pos, j1 = j0 + half;
-      const float2 w = __ldg(tw + pos * step);
-      const float2 u = cb[j0 * G + c], v = cb[j1 * G + c];
-      cb[j0 * G + c] = make_float2(u.x + v.x, u.y + v.y);
-      cb[j1 * G + c] = cmul(make_float2(u.x - v.x, u.y - v.y), w);
-    }
-    __syncthreads();
-  }
+  fft_dif_forward_batch(cb, n, G, 1, G, tw, tw_n, threadIdx.x, 256);
   // mask: position r holds k2 = bitrev(r); column c holds k1 = bitrev(k0 + c) (rows were DIF'd)
   for (int i = threadIdx.x; i < n * G; i += 256) {
     const int r = i / G, c = i - r * G;
@@ -343,19 +305,7 @@ __global__ void __launch_bounds__(256) fft_cols_kernel(int n, int G, float2* __r
     cb[i] = make_float2(cb[i].x * m, cb[i].y * m);
   }
   __syncthreads();
-  for (int len = 2; len <= n; len <<= 1) {
-    const int half = len >> 1, step = tw_n / len;
-    for (int i = threadIdx.x; i < halfn * G; i += 256) {
-      const int c = i % G, ii = i / G;
-      const int pos = ii & (half - 1);
-      const int j0 = ((ii - pos) << 1) + pos, j1 = j0 + half;
-      const float2 w = __ldg(tw + pos * step);
-      const float2 u = cb[j0 * G + c], v = cmulc(cb[j1 * G + c], w);
-      cb[j0 * G + c] = make_float2(u.x + v.x, u.y + v.y);
-      cb[j1 * G + c] = make_float2(u.x - v.x, u.y - v.y);
-    }
-    __syncthreads();
-  }
+  fft_dit_inverse_batch(cb, n, G, 1, G, tw, tw_n, threadIdx.x, 256);
   for (int i = threadIdx.x; i < n * G; i += 256) {
     const int r = i / G, c = i - r * G;
     Zb[(int64_t)r * n + k0 + c] = cb[i];
