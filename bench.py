@@ -191,8 +191,8 @@ def main():
         args.no_e2e = True            # 2 x 4 GiB pinned host buffers per rank: skipped
     B = cfg.nrhs
     pool = cfg.dim == 2 and B > 8     # 2D: 8 seeded RHS tiled to the batch (throughput is value-independent)
-    workload = (f"{cfg.name}_{cfg.dim}d_n{cfg.n}_L{cfg.levels}_rhs{B}_per_gpu_alpha{cfg.alpha:g}_C{cfg.channels}"
-                f"_Wseed")
+    workload = (f"{cfg.name}_{cfg.dim}d_n{cfg.n}_L{cfg.levels}_rhs{B}"
+                f"{'_total' if cid == 4 else '_per_gpu'}_alpha{cfg.alpha:g}_C{cfg.channels}_Wseed")
 
     def make_y(nrhs, start):
         if not pool:
@@ -219,7 +219,8 @@ def main():
         v = args.steps * ns / secs
         line = {"impl": "reference", "metric": f"RHS*V-cycles/s ({cfg.name}, fp64 CPU oracle)", "value": v,
                 "unit": "RHS*cycles/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True, "scaling": "weak",
+                "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
+                "scaling": "strong" if cid == 4 else "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": workload, "sample": f"{ns} RHS x 1 cycle per step"},
                 "cpu_baseline": {"value": v, "unit": "RHS*cycles/s", "cores": host_threads(), "kind": "oracle",
@@ -231,7 +232,7 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_2603_01064_b200 as nmg
-    from paper_2603_01064_b200.parallel import max_over_ranks, weak_shard
+    from paper_2603_01064_b200.parallel import max_over_ranks, shard_range, weak_shard
 
     if world > 1:
         ndev = torch.cuda.device_count()
@@ -245,13 +246,22 @@ def main():
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
 
+    # configs 0-3: weak scaling (every rank its own B-RHS shard of the seeded stream); config 4
+    # (one operator, 32 RHS): strong scaling, the 32 independent RHS split over the ranks
+    # (RHS sharding needs no exchange step)
+    strong = cid == 4
+    if strong:
+        start, B = shard_range(cfg.nrhs, world, rank)
+        global_B = cfg.nrhs
+    else:
+        start, _ = weak_shard(B, rank)
+        global_B = world * B
     factors = ni.operator_factors(cfg)
     W = ni.weights_seed(cfg)
     h = nmg.Hierarchy(cfg.dim, cfg.n, cfg.levels, cfg.alpha, factors, nu1=cfg.nu1, nu2=cfg.nu2, max_rhs=B,
                       device=local)
     for l, w in enumerate(W):
         h.load_weights(l + 1, ni.cnn_arch(cfg), w)
-    start, _ = weak_shard(B, rank)
     y_np = make_y(B, start)
     y = torch.tensor(y_np, dtype=torch.float64, device=dev)
     x = torch.zeros_like(y)
@@ -280,7 +290,7 @@ def main():
     barrier()
     launches = h.launch_count() - l0
     ms = max_over_ranks(e0.elapsed_time(e1))
-    value = world * B * args.steps / (ms / 1e3)
+    value = global_B * args.steps / (ms / 1e3)
 
     # ---- per-kernel-class device times (CUDA events on the launching stream)
     h.profile(True)
@@ -353,7 +363,7 @@ def main():
         f1.record(stream)
         torch.cuda.synchronize(dev)
         ems = max_over_ranks(f0.elapsed_time(f1))
-        e2e = {"value": world * B * args.steps / (ems / 1e3), "unit": "RHS*cycles/s",
+        e2e = {"value": global_B * args.steps / (ems / 1e3), "unit": "RHS*cycles/s",
                "h2d_bytes_per_step": 2 * 8 * B * cfg.N, "d2h_bytes_per_step": 8 * B * cfg.N}
 
     # ---- RHS solved to 1e-6 / s with converging stand-in weights (alpha = 1e-2)
@@ -391,11 +401,12 @@ def main():
         line = {"metric": f"RHS*V-cycles/s ({cfg.name}: fp64 residual + NMGF V-cycle + update per step)",
                 "value": value, "unit": "RHS*cycles/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64 outer / f32 inner",
+                "scaling": "strong" if strong else "weak", "vs_baseline": None,
+                "dtype": "f64 outer residual / fp32-accurate inner (3xTF32 GEMMs, FP16x3 CNN)",
                 "data": "synthetic (seeded RHS; W_seed Kaiming-uniform weights)",
-                "config": {"workload": workload, "global_batch": world * B, "n": cfg.n, "levels": cfg.levels,
+                "config": {"workload": workload, "global_batch": global_B, "n": cfg.n, "levels": cfg.levels,
                            "rhs": "8-RHS seeded pool tiled to the batch" if pool else "seeded, distinct",
-                           "alpha": cfg.alpha, "nu1": cfg.nu1, "nu2": cfg.nu2, "parallelism": f"rhs-shard x{world}",
+                           "alpha": cfg.alpha, "nu1": cfg.nu1, "nu2": cfg.nu2, "parallelism": f"rhs-shard x{world}" + (" (strong: 32 RHS split)" if strong else ""),
                            "l2": ("working set fits L2 (latency-bound config, no flush)" if cid == 0
                                   else "inputs larger than L2 (no flush)")},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "solve": solve,
