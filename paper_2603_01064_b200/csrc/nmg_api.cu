@@ -317,6 +317,8 @@ struct nmg_hierarchy {
   DevBuf<double> part, ynorm, relres, ywork;
   DevBuf<uint8_t> active;
   DevBuf<double> hy, hx;   // staging for nmg_vcycles_host (lazy)
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;         // copy streams of nmg_vcycles_host (lazy)
+  std::vector<cudaEvent_t> hev;                          // its chunk events
   int ntiles = 0;
   int64_t launches = 0;
   bool poisoned = false;
@@ -326,15 +328,21 @@ struct nmg_hierarchy {
   size_t ev_used = 0;
   struct Rec { int cls; cudaEvent_t a, b; };
   std::vector<Rec> recs;
-  // CUDA graph of one nmg_vcycle (keyed by nrhs, buffers and stream)
+  // CUDA graphs of one cycle, keyed by (nrhs, y, x, stream); a few entries so that the chunks
+  // of nmg_vcycles_host each replay their own graph
   bool use_graph = true;
-  int g_nrhs = -1, g_seen = 0;
-  const void* g_y = nullptr; void* g_x = nullptr; cudaStream_t g_s = nullptr;
-  cudaGraphExec_t g_exec = nullptr;
-  int64_t g_launches = 0;
+  struct GraphEntry {
+    int nrhs; const void* y; void* x; cudaStream_t s;
+    int seen; cudaGraphExec_t exec; int64_t launches; uint64_t used;
+  };
+  std::vector<GraphEntry> graphs;
+  uint64_t g_clock = 0;
   ~nmg_hierarchy() {
     for (auto e : ev_pool) cudaEventDestroy(e);
-    if (g_exec) cudaGraphExecDestroy(g_exec);
+    for (auto& g : graphs) if (g.exec) cudaGraphExecDestroy(g.exec);
+    for (auto e : hev) cudaEventDestroy(e);
+    if (s_h2d) cudaStreamDestroy(s_h2d);
+    if (s_d2h) cudaStreamDestroy(s_d2h);
   }
 };
 
@@ -799,6 +807,72 @@ nmg_status debug_2d(nmg_hierarchy* h, int l, int op, int nrhs, const float* fin,
 }  // namespace
 
 // ======================================================================= C ABI
+namespace {
+
+// One cycle through a cached CUDA graph: the first call with a given (nrhs, y, x, stream) runs
+// eagerly, the second captures the whole cycle, later calls replay it (launch-latency bound
+// small configs and coarse levels).
+nmg_status graph_cycle(nmg_hierarchy* h, int nrhs, const double* y, double* x, cudaStream_t s) {
+  auto body = [&]() -> nmg_status {
+    { Prof p(h, NMG_K_MISC, s); row_norms_f64(nrhs, (int)h->N[0], y, h->N[0], h->ynorm.p, h->ywork.p, s); }
+    return outer_step(h, nrhs, y, x, -1.0, false, s);
+  };
+  if (!h->use_graph || s == nullptr || h->prof_on) return body();
+  nmg_hierarchy::GraphEntry* g = nullptr;
+  for (auto& e : h->graphs)
+    if (e.nrhs == nrhs && e.y == y && e.x == x && e.s == s) g = &e;
+  if (!g) {
+    if (h->graphs.size() >= 8) {
+      auto old = h->graphs.begin();
+      for (auto it = h->graphs.begin(); it != h->graphs.end(); ++it)
+        if (it->used < old->used) old = it;
+      if (old->exec) cudaGraphExecDestroy(old->exec);
+      h->graphs.erase(old);
+    }
+    h->graphs.push_back({nrhs, y, x, s, 0, nullptr, 0, 0});
+    g = &h->graphs.back();
+  }
+  g->used = ++h->g_clock;
+  if (g->exec) {
+    NMG_CUDA(cudaGraphLaunch(g->exec, s));
+    h->launches += g->launches;
+    return NMG_OK;
+  }
+  if (g->seen++ == 0) return body();
+  const int64_t l0 = h->launches;
+  if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    h->use_graph = false;
+    return body();
+  }
+  nmg_status st = body();
+  cudaGraph_t gr = nullptr;
+  cudaError_t e = cudaStreamEndCapture(s, &gr);
+  if (st != NMG_OK || e != cudaSuccess || !gr) {
+    if (gr) cudaGraphDestroy(gr);
+    cudaGetLastError();
+    h->use_graph = false;
+    h->launches = l0;
+    h->poisoned = false;
+    return body();
+  }
+  g->launches = h->launches - l0;
+  h->launches = l0;
+  e = cudaGraphInstantiate(&g->exec, gr, 0);
+  cudaGraphDestroy(gr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    g->exec = nullptr;
+    h->use_graph = false;
+    return body();
+  }
+  NMG_CUDA(cudaGraphLaunch(g->exec, s));
+  h->launches += g->launches;
+  return NMG_OK;
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* nmg_last_error(void) { return g_err.c_str(); }
@@ -1313,55 +1387,7 @@ nmg_status nmg_vcycle(nmg_hierarchy* h, int32_t nrhs, const double* y, double* x
   NMG_TRY(check_ready(h, nrhs));
   if (nrhs == 0) return NMG_OK;
   if (!y || !x) return fail(NMG_ERR_INVALID_ARG, "null y/x");
-  cudaStream_t s = (cudaStream_t)stream;
-  auto body = [&]() -> nmg_status {
-    { Prof p(h, NMG_K_MISC, s); row_norms_f64(nrhs, (int)h->N[0], y, h->N[0], h->ynorm.p, h->ywork.p, s); }
-    return outer_step(h, nrhs, y, x, -1.0, false, s);
-  };
-  // CUDA graph: the first call with a given (nrhs, y, x, stream) runs eagerly, the second
-  // captures the whole cycle, later calls replay it (launch-latency bound small configs).
-  const bool key = h->g_nrhs == nrhs && h->g_y == y && h->g_x == x && h->g_s == s;
-  if (!h->use_graph || s == nullptr || h->prof_on) return body();
-  if (key && h->g_exec) {
-    NMG_CUDA(cudaGraphLaunch(h->g_exec, s));
-    h->launches += h->g_launches;
-    return NMG_OK;
-  }
-  if (!key) {
-    if (h->g_exec) { cudaGraphExecDestroy(h->g_exec); h->g_exec = nullptr; }
-    h->g_nrhs = nrhs; h->g_y = y; h->g_x = x; h->g_s = s; h->g_seen = 0;
-  }
-  if (h->g_seen++ == 0) return body();
-  const int64_t l0 = h->launches;
-  if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
-    cudaGetLastError();
-    h->use_graph = false;
-    return body();
-  }
-  nmg_status st = body();
-  cudaGraph_t g = nullptr;
-  cudaError_t e = cudaStreamEndCapture(s, &g);
-  if (st != NMG_OK || e != cudaSuccess || !g) {
-    if (g) cudaGraphDestroy(g);
-    cudaGetLastError();
-    h->use_graph = false;
-    h->launches = l0;
-    h->poisoned = false;
-    return body();
-  }
-  h->g_launches = h->launches - l0;
-  h->launches = l0;
-  e = cudaGraphInstantiate(&h->g_exec, g, 0);
-  cudaGraphDestroy(g);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    h->g_exec = nullptr;
-    h->use_graph = false;
-    return body();
-  }
-  NMG_CUDA(cudaGraphLaunch(h->g_exec, s));
-  h->launches += h->g_launches;
-  return NMG_OK;
+  return graph_cycle(h, nrhs, y, x, (cudaStream_t)stream);
 }
 
 nmg_status nmg_solve(nmg_hierarchy* h, int32_t nrhs, const double* y, double* x, double tol, int32_t max_cycles,
@@ -1440,15 +1466,47 @@ nmg_status nmg_vcycles_host(nmg_hierarchy* h, int32_t nrhs, const double* y_host
   cudaStream_t s = (cudaStream_t)stream;
   const size_t cnt = (size_t)h->d.max_rhs * h->N[0];
   if (!h->hy.p) { NMG_TRY(h->hy.alloc(cnt)); NMG_TRY(h->hx.alloc(cnt)); }
-  const size_t bytes = sizeof(double) * (size_t)nrhs * h->N[0];
-  NMG_CUDA(cudaMemcpyAsync(h->hy.p, y_host, bytes, cudaMemcpyHostToDevice, s));
-  NMG_CUDA(cudaMemcpyAsync(h->hx.p, x_host, bytes, cudaMemcpyHostToDevice, s));
-  row_norms_f64(nrhs, (int)h->N[0], h->hy.p, h->N[0], h->ynorm.p, h->ywork.p, s);
-  h->launches++;
-  for (int c = 0; c < cycles; ++c) NMG_TRY(outer_step(h, nrhs, h->hy.p, h->hx.p, -1.0, false, s));
-  if (relres_host)
-    NMG_CUDA(cudaMemcpyAsync(relres_host, h->relres.p, sizeof(double) * nrhs, cudaMemcpyDeviceToHost, s));
-  NMG_CUDA(cudaMemcpyAsync(x_host, h->hx.p, bytes, cudaMemcpyDeviceToHost, s));
+  // Pipelined over RHS chunks (the RHS are independent): host->device copies of
+  // chunk c + 1 and the device->host copy of chunk c - 1 run on two copy streams while chunk c
+  // cycles on the caller's stream.  One plain cudaMemcpyAsync per buffer and chunk.
+  const int64_t N0 = h->N[0];
+  // two chunks keep each chunk's kernels near full occupancy (measured: cfg 1 in 4 chunks of
+  // 256 RHS runs at 64% of the batch efficiency); four only for very large batches
+  int nch = nrhs < 256 ? 1 : ((int64_t)nrhs * N0 / 4 < ((int64_t)1 << 25) ? 2 : 4);
+  if (const char* ce = std::getenv("NMG_HOST_CHUNKS")) nch = std::max(1, std::min(4, std::min(nrhs, std::atoi(ce))));
+  if (!h->s_h2d) {
+    NMG_CUDA(cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking));
+    NMG_CUDA(cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking));
+    h->hev.resize(2 * 4 + 2);
+    for (auto& e : h->hev) NMG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  cudaEvent_t ev_start = h->hev[8], ev_end = h->hev[9];
+  NMG_CUDA(cudaEventRecord(ev_start, s));                 // staging buffers free after prior work on s
+  NMG_CUDA(cudaStreamWaitEvent(h->s_h2d, ev_start, 0));
+  NMG_CUDA(cudaStreamWaitEvent(h->s_d2h, ev_start, 0));
+  int off[5];
+  for (int c = 0; c <= nch; ++c) off[c] = (int)((int64_t)nrhs * c / nch);
+  for (int c = 0; c < nch; ++c) {
+    const size_t b = sizeof(double) * (size_t)(off[c + 1] - off[c]) * N0;
+    NMG_CUDA(cudaMemcpyAsync(h->hy.p + off[c] * N0, y_host + off[c] * N0, b, cudaMemcpyHostToDevice, h->s_h2d));
+    NMG_CUDA(cudaMemcpyAsync(h->hx.p + off[c] * N0, x_host + off[c] * N0, b, cudaMemcpyHostToDevice, h->s_h2d));
+    NMG_CUDA(cudaEventRecord(h->hev[c], h->s_h2d));
+  }
+  for (int c = 0; c < nch; ++c) {
+    const int cnt = off[c + 1] - off[c];
+    double* yc = h->hy.p + off[c] * N0;
+    double* xc = h->hx.p + off[c] * N0;
+    NMG_CUDA(cudaStreamWaitEvent(s, h->hev[c], 0));
+    for (int k = 0; k < cycles; ++k) NMG_TRY(graph_cycle(h, cnt, yc, xc, s));
+    if (relres_host)
+      NMG_CUDA(cudaMemcpyAsync(relres_host + off[c], h->relres.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, s));
+    NMG_CUDA(cudaEventRecord(h->hev[4 + c], s));
+    NMG_CUDA(cudaStreamWaitEvent(h->s_d2h, h->hev[4 + c], 0));
+    NMG_CUDA(cudaMemcpyAsync(x_host + off[c] * N0, xc, sizeof(double) * (size_t)cnt * N0, cudaMemcpyDeviceToHost,
+                             h->s_d2h));
+  }
+  NMG_CUDA(cudaEventRecord(ev_end, h->s_d2h));
+  NMG_CUDA(cudaStreamWaitEvent(s, ev_end, 0));
   NMG_CUDA(cudaStreamSynchronize(s));
   return NMG_OK;
 }

@@ -330,3 +330,20 @@ def test_host_entry_matches_device(cfg0):
     xh = np.zeros_like(y)
     h.vcycles_host(np.ascontiguousarray(y), xh, 3)
     assert np.array_equal(xh, xd.cpu().numpy())
+
+
+def test_host_entry_chunked_pipeline():
+    """nmg_vcycles_host splits >= 256 RHS into chunks whose copies overlap the cycles of the
+    previous chunk; per-RHS independence makes the result bitwise equal to one device call."""
+    cfg = CFG0.replace(nrhs=600)
+    f = ni.operator_factors(cfg)
+    W = weights_for(cfg, "seed")
+    h = gpu_hierarchy(cfg, f, W, max_rhs=600)
+    y, _ = ni.make_rhs(cfg, f, cfg.alpha)
+    yd = T(y, torch.float64)
+    xd = torch.zeros_like(yd)
+    for _ in range(2):
+        h.vcycle(yd, xd)
+    xh = np.zeros_like(y)
+    h.vcycles_host(np.ascontiguousarray(y), xh, 2)
+    assert np.array_equal(xh, xd.cpu().numpy())
