@@ -55,14 +55,15 @@ NMG_D uint64_t desc_sw64(uint32_t saddr) {
   d |= (uint64_t)4 << 61;
   return d;
 }
-// D s32, A/B int8 (signed), K-major, N = 64, M = 128
-constexpr uint32_t kIdescI8 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OBN >> 3) << 17) |
-                              ((uint32_t)(OBM >> 4) << 24);
-NMG_D void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+// D s32, A/B int8 (signed), K-major, M = 128, N = 64 * nd (nd stacked W digits)
+NMG_D uint32_t idesc_i8(int nd) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)((OBN * nd) >> 3) << 17) | ((uint32_t)(OBM >> 4) << 24);
+}
+NMG_D void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-      "l"(a), "l"(b), "r"(kIdescI8), "r"(acc));
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
 __global__ void __launch_bounds__(ONT, 1)
@@ -105,7 +106,7 @@ __global__ void __launch_bounds__(ONT, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {   // MMA issuer: 28 digit-pair products per 32-wide K step
+    if (lane == 0) {   // MMA issuer: 28 digit-pair products (10 MMAs) per 32-wide K step
       for (int kt = 0; kt < KT; ++kt) {
         const int s = kt % ONSTAGE;
         mb_wait(&full[s], (uint32_t)(kt / ONSTAGE) & 1u);
@@ -115,13 +116,17 @@ __global__ void __launch_bounds__(ONT, 1)
         for (int ks = 0; ks < OBK / 32; ++ks) {
 #pragma unroll
           for (int i = 1; i <= OS; ++i) {
+            // X_i times up to four consecutive W digits stacked along N (their smem planes are
+            // contiguous rows): one MMA with N = 64 nd writes the consecutive diagonal
+            // accumulators d = i + j - 2 .., so the X_i tile is read once per four digits
 #pragma unroll
-            for (int j = 1; j <= OS + 1 - i; ++j) {
-              const int d = i + j - 2;                       // accumulator 0 .. OS - 1
+            for (int j0 = 1; j0 <= OS + 1 - i; j0 += 4) {
+              const int nd = (OS + 2 - i - j0) < 4 ? (OS + 2 - i - j0) : 4;
+              const int d = i + j0 - 2;                      // first accumulator 0 .. OS - 1
               const uint64_t da = desc_sw64(xs + (i - 1) * OBM * OBK + ks * 32);
-              const uint64_t db = desc_sw64(ws + (j - 1) * OBN * OBK + ks * 32);
-              // the first product into diagonal d is the pair (i = 1, j = d + 1) at kt = ks = 0
-              mma_i8(tmem + (uint32_t)(d * OBN), da, db, (kt == 0 && ks == 0 && i == 1) ? 0u : 1u);
+              const uint64_t db = desc_sw64(ws + (j0 - 1) * OBN * OBK + ks * 32);
+              // the first products into the diagonals come from i = 1 at kt = ks = 0
+              mma_i8(tmem + (uint32_t)(d * OBN), da, db, idesc_i8(nd), (kt == 0 && ks == 0 && i == 1) ? 0u : 1u);
             }
           }
         }

@@ -114,7 +114,7 @@ NMG_D void tf32_store(float xv, float* xh, float* xl, int64_t at) {
   xl[at] = __uint_as_float(ll);
 }
 
-__global__ void __launch_bounds__(NT, 2) smooth1d_f16_kernel(Smooth1dArgs a) {
+__global__ void __launch_bounds__(NT, 3) smooth1d_f16_kernel(Smooth1dArgs a) {
   extern __shared__ __align__(1024) uint8_t smraw[];
   uint8_t* sm = smraw + ((1024u - (su32(smraw) & 1023u)) & 1023u);
   const int n = a.n, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
