@@ -10,6 +10,7 @@
 //   warp 2          : TMEM allocator (256 fp32 columns)
 //   all 4 warps     : epilogue (tcgen05.ld 32x32b.x32 -> registers -> C - acc -> global)
 #include <cuda.h>
+#include <cuda_fp16.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -25,6 +26,8 @@ template <int TBN> struct TcCfg {
   static constexpr int SMEM = TSTAGES * STAGE_BYTES + 1024 /*barriers*/ + 1024 /*align slack*/;
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TBN >> 3) << 17) |
                                     ((uint32_t)(TBM >> 4) << 24);   // D f32, A/B tf32 K-major, M=128
+  // FP16x3: the same 64-byte smem rows hold 32 f16 (K per stage 32), kind::f16 with A/B f16
+  static constexpr uint32_t IDESC16 = (1u << 4) | ((uint32_t)(TBN >> 3) << 17) | ((uint32_t)(TBM >> 4) << 24);
 };
 
 NMG_D uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -77,6 +80,15 @@ NMG_D void umma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumul
       ".reg .pred p;\n"
       "setp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+NMG_D void umma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate, uint32_t idesc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
       "}\n" ::"r"(tmem_d),
       "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
 }
@@ -143,15 +155,16 @@ NMG_D void tc_store_chunk(const TcGemmArgs& a, const uint32_t (&v)[32], int m, i
     }
   }
 
-template <int TBN>
+template <int TBN, bool F16 = false>
 __global__ void __launch_bounds__(TNT, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tXh, const __grid_constant__ CUtensorMap tXl,
                    const __grid_constant__ CUtensorMap tWh, const __grid_constant__ CUtensorMap tWl,
                    TcGemmArgs a) {
+  constexpr int KE = F16 ? 2 * TBK : TBK;    // K elements per stage (64-byte rows)
   extern __shared__ uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   constexpr int B_BYTES = TcCfg<TBN>::B_BYTES, STAGE_BYTES = TcCfg<TBN>::STAGE_BYTES;
-  constexpr uint32_t kIdesc = TcCfg<TBN>::IDESC;
+  constexpr uint32_t kIdesc = F16 ? TcCfg<TBN>::IDESC16 : TcCfg<TBN>::IDESC;
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + TSTAGES * STAGE_BYTES);
   uint64_t* empty = full + TSTAGES;
   uint64_t* done = empty + TSTAGES;
@@ -159,7 +172,7 @@ __global__ void __launch_bounds__(TNT, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int m0 = blockIdx.y * TBM, n0 = blockIdx.x * TBN;
-  const int KT = ceil_div(a.K, TBK);
+  const int KT = ceil_div(a.K, KE);
 
   if (tid == 0) {
     for (int s = 0; s < TSTAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -185,7 +198,7 @@ __global__ void __launch_bounds__(TNT, 1)
         mbar_wait(&empty[s], ph ^ 1u);
         uint8_t* st = sm + s * STAGE_BYTES;
         mbar_expect_tx(&full[s], STAGE_BYTES);
-        const int k0 = kt * TBK;
+        const int k0 = kt * KE;
         tma_load_2d(st, &tXh, &full[s], k0, m0);
         tma_load_2d(st + A_BYTES, &tXl, &full[s], k0, m0);
         tma_load_2d(st + 2 * A_BYTES, &tWh, &full[s], k0, n0);
@@ -202,15 +215,21 @@ __global__ void __launch_bounds__(TNT, 1)
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         const uint32_t st = smem_u32(sm + s * STAGE_BYTES);
 #pragma unroll
-        for (int ks = 0; ks < TBK / 8; ++ks) {
-          const uint32_t ko = ks * 32;   // 8 tf32 = 32 bytes along the 64-byte swizzled row
+        for (int ks = 0; ks < 2; ++ks) {
+          const uint32_t ko = ks * 32;   // 8 tf32 / 16 f16 = 32 bytes along the 64-byte swizzled row
           const uint64_t dxh = umma_desc_sw64(st + ko);
           const uint64_t dxl = umma_desc_sw64(st + A_BYTES + ko);
           const uint64_t dwh = umma_desc_sw64(st + 2 * A_BYTES + ko);
           const uint64_t dwl = umma_desc_sw64(st + 2 * A_BYTES + B_BYTES + ko);
-          umma_tf32(tmem, dxh, dwh, (kt | ks) ? 1u : 0u, kIdesc);
-          umma_tf32(tmem, dxh, dwl, 1u, kIdesc);
-          umma_tf32(tmem, dxl, dwh, 1u, kIdesc);
+          if (F16) {
+            umma_f16(tmem, dxh, dwh, (kt | ks) ? 1u : 0u, kIdesc);
+            umma_f16(tmem, dxh, dwl, 1u, kIdesc);
+            umma_f16(tmem, dxl, dwh, 1u, kIdesc);
+          } else {
+            umma_tf32(tmem, dxh, dwh, (kt | ks) ? 1u : 0u, kIdesc);
+            umma_tf32(tmem, dxh, dwl, 1u, kIdesc);
+            umma_tf32(tmem, dxl, dwh, 1u, kIdesc);
+          }
         }
         umma_commit(&empty[s]);      // slot reusable when these MMAs retire
       }
@@ -241,6 +260,14 @@ __global__ void __launch_bounds__(TNT, 1)
         : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
     const int nb = n0 + c * 32;
+    if (F16 && mok) {
+      const float xs = a.xinv[m];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int nn = min(nb + j, a.N - 1);
+        v[j] = __float_as_uint(__uint_as_float(v[j]) * (xs * __ldg(a.winv + nn)));
+      }
+    }
     if (mok) tc_store_chunk(a, v, m, nb, crow, drow);
     __syncwarp();
   }
@@ -266,9 +293,63 @@ __global__ void split_tf32_kernel(int64_t count, const float* __restrict__ x, fl
   lo[i] = __uint_as_float(l);
 }
 
+// ---- per-row scaled f16 hi/lo split (one CTA per row) -------------------------------
+__global__ void __launch_bounds__(256) split_f16_rows_kernel(int K, const float* __restrict__ x,
+                                                             __half* __restrict__ hi, __half* __restrict__ lo,
+                                                             float* __restrict__ xinv) {
+  __shared__ float red[8];
+  const int m = blockIdx.x;
+  const float* row = x + (int64_t)m * K;
+  float mx = 0.f;
+  for (int k = threadIdx.x; k < K; k += 256) mx = fmaxf(mx, fabsf(row[k]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  mx = red[0];
+#pragma unroll
+  for (int w = 1; w < 8; ++w) mx = fmaxf(mx, red[w]);
+  // S = 2^e with S max <= 2^14 (hi never overflows f16), exact power of two
+  int e = 0;
+  if (mx > 0.f) { frexpf(16384.f / mx, &e); e -= 1; }
+  e = max(-100, min(100, e));
+  const float S = ldexpf(1.f, e);
+  if (threadIdx.x == 0) xinv[m] = ldexpf(1.f, -e);
+  for (int k = threadIdx.x; k < K; k += 256) {
+    const float v = row[k] * S;
+    const __half h = __float2half_rn(v);
+    hi[(int64_t)m * K + k] = h;
+    lo[(int64_t)m * K + k] = __float2half_rn(v - __half2float(h));
+  }
+}
+
 }  // namespace
 
 int tc_gemm_block_m() { return TBM; }
+
+void tc_gemm_f16(const CUtensorMap* xh, const CUtensorMap* xl, const CUtensorMap* wh, const CUtensorMap* wl,
+                 const TcGemmArgs& a, cudaStream_t s, int bn) {
+  static bool attr256 = false, attr64 = false;
+  dim3 grid(ceil_div(a.N, bn), ceil_div(a.M, TBM));
+  if (bn == 256) {
+    if (!attr256) {
+      cudaFuncSetAttribute(tc_gemm_kernel<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<256>::SMEM);
+      attr256 = true;
+    }
+    tc_gemm_kernel<256, true><<<grid, TNT, TcCfg<256>::SMEM, s>>>(*xh, *xl, *wh, *wl, a);
+  } else {
+    if (!attr64) {
+      cudaFuncSetAttribute(tc_gemm_kernel<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<64>::SMEM);
+      attr64 = true;
+    }
+    tc_gemm_kernel<64, true><<<grid, TNT, TcCfg<64>::SMEM, s>>>(*xh, *xl, *wh, *wl, a);
+  }
+}
+
+void split_f16_rows(int rows, int K, const float* x, uint16_t* hi, uint16_t* lo, float* xinv, cudaStream_t s) {
+  split_f16_rows_kernel<<<rows, 256, 0, s>>>(K, x, reinterpret_cast<__half*>(hi), reinterpret_cast<__half*>(lo),
+                                             xinv);
+}
 
 void tc_gemm(const CUtensorMap* xh, const CUtensorMap* xl, const CUtensorMap* wh, const CUtensorMap* wl,
              const TcGemmArgs& a, cudaStream_t s, int bn) {

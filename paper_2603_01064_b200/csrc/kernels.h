@@ -68,10 +68,20 @@ struct TcGemmArgs {
   bool negate;
   int tblock = 0;                        // >0: transposed store within tblock x tblock blocks
   float* Dh = nullptr; float* Dl = nullptr;   // optional tf32 hi/lo split output (no C)
+  // FP16x3 variant only: X row m was split as x S_m, W row n as w T_n; xinv[m] = 1 / S_m,
+  // winv[n] = 1 / T_n (powers of two, so acc xinv winv is exact)
+  const float* xinv = nullptr;
+  const float* winv = nullptr;
 };
 // bn = 256 or 64 (tile width; W maps must use box rows = bn)
 void tc_gemm(const CUtensorMap* xh, const CUtensorMap* xl, const CUtensorMap* wh, const CUtensorMap* wl,
              const TcGemmArgs& a, cudaStream_t s, int bn);
+// same with f16 hi/lo operands (kind::f16, tensor maps with f16 elements, box {32, rows}):
+// twice the tensor rate of 3xTF32, same fp32-accurate result (2^-22 per product)
+void tc_gemm_f16(const CUtensorMap* xh, const CUtensorMap* xl, const CUtensorMap* wh, const CUtensorMap* wl,
+                 const TcGemmArgs& a, cudaStream_t s, int bn);
+// per-row power-of-two scaled f16 hi/lo split: S = 2^floor(log2(2^14 / max_k |x[m][k]|))
+void split_f16_rows(int rows, int K, const float* x, uint16_t* hi, uint16_t* lo, float* xinv, cudaStream_t s);
 int tc_gemm_block_m();
 // tile width heuristic: 256 when that already fills the GPU, else 64
 inline int tc_pick_bn(int M, int N, int num_sms) {

@@ -206,6 +206,20 @@ nmg_status make_map(CUtensorMap* m, const float* p, int64_t rows, int64_t cols, 
   return NMG_OK;
 }
 
+// f16 [rows][cols], box {32, box_rows} (64-byte rows), SWIZZLE_64B
+nmg_status make_map16(CUtensorMap* m, const uint16_t* p, int64_t rows, int64_t cols, int box_rows) {
+  NMG_TRY(get_encoder());
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2u};
+  cuuint32_t box[2] = {32u, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1u, 1u};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (void*)p, dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(NMG_ERR_CUDA, "cuTensorMapEncodeTiled (f16) failed (%d)", (int)r);
+  return NMG_OK;
+}
+
 // digit planes [S][rows][K] int8, box {64, box_rows, S}, SWIZZLE_64B
 nmg_status make_digit_map(CUtensorMap* m, const int8_t* p, int S, int64_t rows, int64_t K, int box_rows) {
   NMG_TRY(get_encoder());
@@ -267,6 +281,13 @@ struct nmg_hierarchy {
   std::vector<std::unique_ptr<DevBuf<float>>> sxh, sxl;  // X splits per level [max_rhs][n_l]
   std::vector<CUtensorMap> mXh, mXl;
   std::vector<char> split_fresh;                         // sxh/sxl[l] hold the split of wx[l]
+  // 1D inner operator applies in FP16x3 (kind::f16): per-row-scaled f16 hi/lo planes
+  bool gemm_f16 = false;
+  struct F16Op { DevBuf<uint16_t> h, l; DevBuf<float> winv; CUtensorMap m256h, m256l, m64h, m64l; };
+  std::vector<std::unique_ptr<F16Op>> A16, AP16;         // per smoothed level
+  std::vector<std::unique_ptr<DevBuf<uint16_t>>> sx16h, sx16l;
+  std::vector<std::unique_ptr<DevBuf<float>>> sxinv;
+  std::vector<CUtensorMap> mX16h, mX16l;
   bool use_tc = true;
   bool smooth_tc = false;                                // 1D smoother layer 2 on tcgen05 3xTF32 (opt-in)
   bool smooth_f16 = false;                               // 1D smoother layer 2 on tcgen05 FP16x3 (default)
@@ -412,7 +433,7 @@ nmg_status smooth_level(nmg_hierarchy* h, int l, int nrhs, const float* b, float
   a.normalize = true;
   a.filter = h->d.level_filter != 0;
   a.accumulate = accumulate;
-  const bool split = x == h->wx[l]->p && h->sxh.size() > (size_t)l && h->sxh[l]->p;
+  const bool split = !h->gemm_f16 && x == h->wx[l]->p && h->sxh.size() > (size_t)l && h->sxh[l]->p;
   if (split) { a.xh = h->sxh[l]->p; a.xl = h->sxl[l]->p; }
   { Prof p(h, NMG_K_SMOOTH, s); launch_smooth1d(h, l, a, s); }
   if (h->split_fresh.size() > (size_t)l) h->split_fresh[l] = split ? 1 : 0;
@@ -444,6 +465,22 @@ nmg_status level_resid(nmg_hierarchy* h, int l, int which, int nrhs, const float
   const float* X = h->wx[lx]->p;
   const bool tc = h->use_tc && n % 16 == 0 && K % 16 == 0 && K >= 16;
   if (!tc) return resid_gemm(h, nrhs, n, K, X, which == 0 ? h->A32[l]->p : h->AP32[l]->p, C, D, s, negate);
+  if (h->gemm_f16) {
+    { Prof p(h, NMG_K_MISC, s); split_f16_rows(nrhs, K, X, h->sx16h[lx]->p, h->sx16l[lx]->p, h->sxinv[lx]->p, s); }
+    NMG_TRY(check_launch(h));
+    const nmg_hierarchy::F16Op& W = which == 0 ? *h->A16[l] : *h->AP16[l];
+    TcGemmArgs g{};
+    g.M = nrhs; g.N = n; g.K = K;
+    g.C = C; g.ldc = n; g.D = D; g.ldd = n; g.negate = negate;
+    g.xinv = h->sxinv[lx]->p; g.winv = W.winv.p;
+    {
+      Prof p(h, NMG_K_GEMM32, s);
+      const int bn = tc_pick_bn(nrhs, n, h->num_sms);
+      tc_gemm_f16(&h->mX16h[lx], &h->mX16l[lx], bn == 256 ? &W.m256h : &W.m64h, bn == 256 ? &W.m256l : &W.m64l, g, s,
+                  bn);
+    }
+    return check_launch(h);
+  }
   if (!h->split_fresh[lx]) {
     { Prof p(h, NMG_K_MISC, s); split_tf32((int64_t)nrhs * K, X, h->sxh[lx]->p, h->sxl[lx]->p, s); }
     NMG_TRY(check_launch(h));
@@ -471,7 +508,7 @@ nmg_status cycle_level_1d(nmg_hierarchy* h, int l, int nrhs, cudaStream_t s) {
   float* y = h->wy[l]->p;
   float* x = h->wx[l]->p;
   if (l == h->L - 1) {
-    float* xh = (h->sxh.size() > (size_t)l && h->sxh[l]->p && h->nc <= 128) ? h->sxh[l]->p : nullptr;
+    float* xh = (!h->gemm_f16 && h->sxh.size() > (size_t)l && h->sxh[l]->p && h->nc <= 128) ? h->sxh[l]->p : nullptr;
     { Prof p(h, NMG_K_COARSE, s);
       coarse_chol_solve(h->nc, nrhs, h->Lrow.p, h->Lcol.p, y, n, x, n, s, xh, xh ? h->sxl[l]->p : nullptr); }
     h->split_fresh[l] = xh ? 1 : 0;
@@ -943,6 +980,32 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
         NMG_TRY(h->AP32h.back()->upload(hi.data(), hi.size()));
         NMG_TRY(h->AP32l.back()->upload(lo.data(), lo.size()));
       }
+      {
+        // f16 hi/lo planes with a power-of-two scale per row (FP16x3 GEMM operand W)
+        auto f16op = [&](const std::vector<double>& M, int rows, int cols) -> std::unique_ptr<nmg_hierarchy::F16Op> {
+          std::unique_ptr<nmg_hierarchy::F16Op> op(new nmg_hierarchy::F16Op());
+          std::vector<uint16_t> hi((size_t)rows * cols), lo((size_t)rows * cols);
+          std::vector<float> winv(rows);
+          for (int r = 0; r < rows; ++r) {
+            double mx = 0.0;
+            for (int c = 0; c < cols; ++c) mx = std::max(mx, std::fabs(M[(size_t)r * cols + c]));
+            const float T = pow2_scale(mx);
+            winv[r] = 1.0f / T;
+            for (int c = 0; c < cols; ++c) {
+              const float v = (float)M[(size_t)r * cols + c] * T;
+              hi[(size_t)r * cols + c] = f16_rn(v);
+              lo[(size_t)r * cols + c] = f16_rn(v - f16_f(hi[(size_t)r * cols + c]));
+            }
+          }
+          if (op->h.upload(hi.data(), hi.size()) != NMG_OK || op->l.upload(lo.data(), lo.size()) != NMG_OK ||
+              op->winv.upload(winv.data(), winv.size()) != NMG_OK)
+            return nullptr;
+          return op;
+        };
+        h->A16.push_back(f16op(A, nl, nl));
+        h->AP16.push_back(f16op(AP, nl, nl / 2));
+        if (!h->A16.back() || !h->AP16.back()) return fail(NMG_ERR_OOM, "f16 operator planes");
+      }
       host_restrict_rows(AP, nl, nl / 2, Ac);           // R A P
       A.swap(Ac);
     }
@@ -1031,14 +1094,38 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
     h->smooth_f16 = h->use_tc && !(senv && (std::string(senv) == "tc" || std::string(senv) == "ffma"));
   }
   if (d.dim == 1) {
+    const char* genv16 = std::getenv("NMG_GEMM");
+    h->gemm_f16 = h->use_tc && !(genv16 && std::string(genv16) == "tf32");
+  }
+  if (d.dim == 1) {
     h->mAh.resize(h->L); h->mAl.resize(h->L); h->mAPh.resize(h->L); h->mAPl.resize(h->L);
     h->mAh64.resize(h->L); h->mAl64.resize(h->L); h->mAPh64.resize(h->L); h->mAPl64.resize(h->L);
     h->mXh.resize(h->L); h->mXl.resize(h->L);
+    h->mX16h.resize(h->L); h->mX16l.resize(h->L);
     for (int l = 0; l < h->L; ++l) {
       const int nl = h->n[l];
       h->sxh.emplace_back(new DevBuf<float>());
       h->sxl.emplace_back(new DevBuf<float>());
+      h->sx16h.emplace_back(new DevBuf<uint16_t>());
+      h->sx16l.emplace_back(new DevBuf<uint16_t>());
+      h->sxinv.emplace_back(new DevBuf<float>());
       if (nl % 16 != 0) continue;   // small levels use the SIMT kernel
+      if (h->gemm_f16) {
+        NMG_TRY(h->sx16h.back()->alloc(B * nl));
+        NMG_TRY(h->sx16l.back()->alloc(B * nl));
+        NMG_TRY(h->sxinv.back()->alloc(B));
+        NMG_TRY(make_map16(&h->mX16h[l], h->sx16h.back()->p, (int64_t)B, nl, tc_gemm_block_m()));
+        NMG_TRY(make_map16(&h->mX16l[l], h->sx16l.back()->p, (int64_t)B, nl, tc_gemm_block_m()));
+        if (l < h->L - 1) {
+          for (auto* op : {h->A16[l].get(), h->AP16[l].get()}) {
+            const int cols = op == h->A16[l].get() ? nl : nl / 2;
+            NMG_TRY(make_map16(&op->m256h, op->h.p, nl, cols, 256));
+            NMG_TRY(make_map16(&op->m256l, op->l.p, nl, cols, 256));
+            NMG_TRY(make_map16(&op->m64h, op->h.p, nl, cols, 64));
+            NMG_TRY(make_map16(&op->m64l, op->l.p, nl, cols, 64));
+          }
+        }
+      }
       NMG_TRY(h->sxh.back()->alloc(B * nl));
       NMG_TRY(h->sxl.back()->alloc(B * nl));
       NMG_TRY(make_map(&h->mXh[l], h->sxh.back()->p, (int64_t)B, nl, tc_gemm_block_m()));
