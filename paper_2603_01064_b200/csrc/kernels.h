@@ -106,6 +106,9 @@ struct Smooth1dArgs {
   // a1 scale S (a1 is split as a1 S) and 1 / (S T)
   const uint16_t* wb = nullptr;
   float in_scale = 1.f, d_scale = 1.f;
+  uint16_t* x16h = nullptr;        // optional (filter path): per-row scaled f16 hi/lo split of the
+  uint16_t* x16l = nullptr;        // updated x and 1 / scale, as split_f16_rows
+  float* xinv = nullptr;
 };
 void smooth1d(const Smooth1dArgs& a, cudaStream_t s);
 // same step with the 16 -> 16 layer on tcgen05 (FP16x3, n % 128 == 0), smooth1d_f16.cu

@@ -433,8 +433,13 @@ nmg_status smooth_level(nmg_hierarchy* h, int l, int nrhs, const float* b, float
   a.normalize = true;
   a.filter = h->d.level_filter != 0;
   a.accumulate = accumulate;
-  const bool split = !h->gemm_f16 && x == h->wx[l]->p && h->sxh.size() > (size_t)l && h->sxh[l]->p;
+  bool split = !h->gemm_f16 && x == h->wx[l]->p && h->sxh.size() > (size_t)l && h->sxh[l]->p;
   if (split) { a.xh = h->sxh[l]->p; a.xl = h->sxl[l]->p; }
+  if (h->gemm_f16 && a.filter && x == h->wx[l]->p && h->smooth_f16 && a.n % 128 == 0 && h->sx16h.size() > (size_t)l &&
+      h->sx16h[l]->p) {
+    a.x16h = h->sx16h[l]->p; a.x16l = h->sx16l[l]->p; a.xinv = h->sxinv[l]->p;
+    split = true;
+  }
   { Prof p(h, NMG_K_SMOOTH, s); launch_smooth1d(h, l, a, s); }
   if (h->split_fresh.size() > (size_t)l) h->split_fresh[l] = split ? 1 : 0;
   return check_launch(h);
@@ -466,8 +471,11 @@ nmg_status level_resid(nmg_hierarchy* h, int l, int which, int nrhs, const float
   const bool tc = h->use_tc && n % 16 == 0 && K % 16 == 0 && K >= 16;
   if (!tc) return resid_gemm(h, nrhs, n, K, X, which == 0 ? h->A32[l]->p : h->AP32[l]->p, C, D, s, negate);
   if (h->gemm_f16) {
-    { Prof p(h, NMG_K_MISC, s); split_f16_rows(nrhs, K, X, h->sx16h[lx]->p, h->sx16l[lx]->p, h->sxinv[lx]->p, s); }
-    NMG_TRY(check_launch(h));
+    if (!h->split_fresh[lx]) {
+      { Prof p(h, NMG_K_MISC, s); split_f16_rows(nrhs, K, X, h->sx16h[lx]->p, h->sx16l[lx]->p, h->sxinv[lx]->p, s); }
+      NMG_TRY(check_launch(h));
+      h->split_fresh[lx] = 1;
+    }
     const nmg_hierarchy::F16Op& W = which == 0 ? *h->A16[l] : *h->AP16[l];
     TcGemmArgs g{};
     g.M = nrhs; g.N = n; g.K = K;

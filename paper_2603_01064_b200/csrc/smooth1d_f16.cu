@@ -323,11 +323,38 @@ __global__ void __launch_bounds__(NT, 3) smooth1d_f16_kernel(Smooth1dArgs a) {
       // ---- level filter F'_l on the whole row (real-input FFT packing, see fft.cuh)
       real_level_filter(hb, n, a.twiddle, a.tw_n, tid, NT);
       const float scale = 2.0f / (float)n;   // 1/(n/2) of the half-length inverse
+      float mx = 0.f;
       for (int j = tid; j < n; j += NT) {
         const float v = hb[j] * scale;
         const float xv = a.accumulate ? xrow[j] + v : v;
         xrow[j] = xv;
         if (a.xh) tf32_store(xv, a.xh, a.xl, (int64_t)rhs * a.ldx + j);
+        if (a.x16h) { hb[j] = xv; mx = fmaxf(mx, fabsf(xv)); }
+      }
+      if (a.x16h) {
+        // f16 hi/lo split of the updated row for the next FP16x3 operator apply, with the
+        // row's power-of-two scale S (S max|x| <= 2^14), as split_f16_rows
+        __shared__ float redf[NT / 32];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (lane == 0) redf[warp] = mx;
+        __syncthreads();
+        mx = redf[0];
+#pragma unroll
+        for (int w = 1; w < NT / 32; ++w) mx = fmaxf(mx, redf[w]);
+        int e = 0;
+        if (mx > 0.f) { frexpf(16384.f / mx, &e); e -= 1; }
+        e = max(-100, min(100, e));
+        const float S = ldexpf(1.f, e);
+        if (tid == 0) a.xinv[rhs] = ldexpf(1.f, -e);
+        __half* oh = reinterpret_cast<__half*>(a.x16h) + (int64_t)rhs * a.ldx;
+        __half* ol = reinterpret_cast<__half*>(a.x16l) + (int64_t)rhs * a.ldx;
+        for (int j = tid; j < n; j += NT) {
+          const float v = hb[j] * S;
+          const __half hv = __float2half_rn(v);
+          oh[j] = hv;
+          ol[j] = __float2half_rn(v - __half2float(hv));
+        }
       }
     }
   }
