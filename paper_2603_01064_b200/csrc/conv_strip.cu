@@ -49,16 +49,25 @@ constexpr int SEG = 128;        // pixels per strip (MMA M)
 constexpr int RP = SEG + 2;     // rows of the activation buffer (x halo)
 constexpr int NSTG = 3;         // activation ring depth
 constexpr int NTHR = 448;
-constexpr int NGRP = 2;         // epilogue channel groups
-constexpr int PROD0 = 8;        // first producer warp
 constexpr int MMAW = 13;        // MMA warp
 constexpr uint32_t IDESC4 = (1u << 4) | ((uint32_t)(16 >> 3) << 17) | ((uint32_t)(SEG >> 4) << 24);  // N = 16
+// Warp roles: warps 0-7 epilogue (TMEM lane quarter w % 4, channel half w / 4), warps 8-12
+// producer (layers 1-2: FFMA a1, one position and all C channels per thread; layers 3-4:
+// warp 8 TMA, warp 12 layer-4 MMA issuer), warp 13 layer-2/3 MMA issuer.  (Nine producer
+// warps with four all-channel epilogue warps measured slower at C = 32.)
+template <int C, bool FIRST>
+struct Roles {
+  static constexpr int NG = 2;                            // epilogue channel groups
+  static constexpr int PROD0 = 4 * NG;                    // first producer warp
+  static constexpr int NPROD = MMAW - PROD0;              // producer warps (FIRST)
+  static constexpr int CH = C;                            // channels per producer item
+};
 
 template <int C>
 struct Cfg {
   static constexpr int N = 3 * C;                       // (t2, o)
   static constexpr int K = 3 * C;                       // (t1, c)
-  static constexpr int CG = C / NGRP;                   // channels per epilogue thread (16 / 24)
+
   static constexpr int WBYTES = N * K * 2;              // one weight plane (hi or lo)
   static constexpr int ABYTES = ((RP * C * 2) + 127) / 128 * 128;   // one activation row, hi or lo
   static constexpr int ALBO = RP * 16;                  // K-chunk stride of the A buffer
@@ -148,7 +157,12 @@ template <int CG>
 NMG_D void tload(uint32_t taddr, uint32_t* r) {
 #pragma unroll
   for (int j = 0; j < CG / 8; ++j) tld8(taddr + 8 * j, r + 8 * j);
-  tld_wait<CG>(r);
+  if constexpr (CG == 32) {
+    tld_wait<16>(r);
+    tld_wait<16>(r + 16);
+  } else {
+    tld_wait<CG>(r);
+  }
 }
 
 // 8 fp32 (already scaled) -> f16 hi (8) and lo (8) packed as uint4
@@ -187,7 +201,10 @@ __global__ void __launch_bounds__(NTHR, 1)
     conv_strip_kernel(const __grid_constant__ CUtensorMap mInH, const __grid_constant__ CUtensorMap mInL,
                       StripArgs a) {
   using G = Cfg<C>;
-  constexpr int CG = G::CG;
+  using RL = Roles<C, FIRST>;
+  constexpr int NGRP = RL::NG;
+  constexpr int PROD0 = RL::PROD0;
+  constexpr int CG = C / NGRP;                           // channels per epilogue thread
   extern __shared__ __align__(1024) uint8_t smraw[];
   uint8_t* sm = smraw + ((1024u - (su32(smraw) & 1023u)) & 1023u);
   uint8_t* Wh = sm;
@@ -233,7 +250,7 @@ __global__ void __launch_bounds__(NTHR, 1)
       for (int i = tid; i < C; i += NTHR) swt[9 * C + i] = __ldg(a.w_in + 9 * C + i);
   }
   if (tid == 0) {
-    for (int s = 0; s < NSTG; ++s) { mb_init(&full[s], FIRST ? 5 : 1); mb_init(&empty[s], 1); }
+    for (int s = 0; s < NSTG; ++s) { mb_init(&full[s], FIRST ? RL::NPROD : 1); mb_init(&empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mb_init(&dfull[s], 1); mb_init(&dempty[s], 4 * NGRP); }
     mb_init(a4full, 4 * NGRP);
     mb_init(d4full, 1);
@@ -255,10 +272,13 @@ __global__ void __launch_bounds__(NTHR, 1)
   if (warp >= PROD0 && warp < (FIRST ? MMAW : MMAW - 1)) {
     // ------------------------------------------------------------------ producer
     if (FIRST) {
-      // thread p owns position p of the row buffer (x = X0 - 1 + p) and all C channels; a
-      // 3 x 3 window of b slides down with the rows, the next row prefetched
-      const int p = tid - PROD0 * 32;
-      const bool act = p < RP;
+      // thread owns position p of the row buffer (x = X0 - 1 + p) and RL::CH channels
+      // starting at ch0; a 3 x 3 window of b slides down with the rows, the next row prefetched
+      const int pt = tid - PROD0 * 32;
+      constexpr int SPAN = RL::CH == C ? RL::NPROD * 32 : (RL::NPROD * 32) / 2;   // threads per channel half
+      const int p = pt % SPAN;
+      const int ch0 = (pt / SPAN) * RL::CH;
+      const bool act = p < RP && pt / SPAN < C / RL::CH;
       const float sc = a.in_scale;
       int it = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -296,7 +316,7 @@ __global__ void __launch_bounds__(NTHR, 1)
             uint4* ah = reinterpret_cast<uint4*>(ring + st * 2 * G::ABYTES);
             uint4* al = reinterpret_cast<uint4*>(ring + st * 2 * G::ABYTES + G::ABYTES);
 #pragma unroll 1
-            for (int g = 0; g < C / 16; ++g) {
+            for (int g = ch0 / 16; g < (ch0 + RL::CH) / 16; ++g) {
               float v[16];
 #pragma unroll
               for (int j = 0; j < 16; j += 4) {
@@ -468,25 +488,6 @@ __global__ void __launch_bounds__(NTHR, 1)
       }
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     };
-    // this thread's CG channels of the a3 row -> A4 (scaled f16 hi / lo), then signal the MMA warp
-    auto write_a4 = [&](const float* act) {
-      uint4* ah4 = reinterpret_cast<uint4*>(A4);
-      uint4* al4 = reinterpret_cast<uint4*>(A4 + G::A4BYTES);
-      const float s3 = a.a3_scale;
-#pragma unroll
-      for (int g = 0; g < CG / 8; ++g) {
-        float v[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = act[8 * g + j] * s3;
-        uint4 hi, lo;
-        split8(v, hi, lo);
-        ah4[(c0 / 8 + g) * SEG + m] = hi;
-        al4[(c0 / 8 + g) * SEG + m] = lo;
-      }
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mb_arrive(a4full);
-    };
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const Unit t = unit_of(u, n, nx, a.ysplit);
       const int x = t.X0 + m;
@@ -506,47 +507,58 @@ __global__ void __launch_bounds__(NTHR, 1)
         // output row r - 1 is complete: b + D_0(r - 2) + D_1(r - 1) + D_2(r)
         const int yo = r - 1;
         const bool yin = yo >= 0 && yo < n;
-        float act[CG];
-        {
-          uint32_t D[CG];
-          if (valid) tload<CG>(tb + 2 * C, D);
+        // layers 3-4: the previous a3 row's layer-4 result first (it also frees the A4 tile)
+        if (!FIRST && r > t.y0 - H) consume_d4(t, x, r - 2);
+        const bool store = FIRST && yo >= t.y0 && yo < t.y1 && x < n;
+        const int64_t off = (((int64_t)t.b * n + (store ? yo : 0)) * n + x) * C + c0;
+        // 8 channels at a time: D_2 -> this row's activation, D_1 / D_0 -> the carries
 #pragma unroll
-          for (int j = 0; j < CG; ++j) {
-            const float d2 = valid ? __uint_as_float(D[j]) : 0.f;
-            act[j] = yin ? fmaxf(fmaf(P1[j] + d2, dsc, bv[j]), 0.f) : 0.f;
+        for (int g = 0; g < CG / 8; ++g) {
+          uint32_t D[24];
+          if (valid) {
+            tld8(tb + 2 * C + 8 * g, D);
+            tld8(tb + C + 8 * g, D + 8);
+            tld8(tb + 8 * g, D + 16);
+            tld_wait<24>(D);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 24; ++j) D[j] = 0u;
           }
-        }
-        {
-          uint32_t D[CG];
-          if (valid) tload<CG>(tb + C, D);
+          float act[8];
 #pragma unroll
-          for (int j = 0; j < CG; ++j) P1[j] = P0[j] + (valid ? __uint_as_float(D[j]) : 0.f);
-          if (valid) tload<CG>(tb, D);
+          for (int j = 0; j < 8; ++j) {
+            const int c = 8 * g + j;
+            act[j] = yin ? fmaxf(fmaf(P1[c] + __uint_as_float(D[j]), dsc, bv[c]), 0.f) : 0.f;
+            P1[c] = P0[c] + __uint_as_float(D[8 + j]);
+            P0[c] = __uint_as_float(D[16 + j]);
+          }
+          if (FIRST) {
+            if (store) {
+              float v[8];
 #pragma unroll
-          for (int j = 0; j < CG; ++j) P0[j] = valid ? __uint_as_float(D[j]) : 0.f;
+              for (int j = 0; j < 8; ++j) v[j] = act[j] * osc;
+              uint4 hi, lo;
+              split8(v, hi, lo);
+              reinterpret_cast<uint4*>(a.out_h + off)[g] = hi;
+              reinterpret_cast<uint4*>(a.out_l + off)[g] = lo;
+            }
+          } else {
+            float v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = act[j] * a.a3_scale;
+            uint4 hi, lo;
+            split8(v, hi, lo);
+            reinterpret_cast<uint4*>(A4)[(c0 / 8 + g) * SEG + m] = hi;
+            reinterpret_cast<uint4*>(A4 + G::A4BYTES)[(c0 / 8 + g) * SEG + m] = lo;
+          }
         }
         asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
         __syncwarp();
         if (lane == 0) mb_arrive(&dempty[buf]);
-        if (FIRST) {
-          if (yo >= t.y0 && yo < t.y1 && x < n) {
-            const int64_t off = (((int64_t)t.b * n + yo) * n + x) * C + c0;
-            uint4* oh = reinterpret_cast<uint4*>(a.out_h + off);
-            uint4* ol = reinterpret_cast<uint4*>(a.out_l + off);
-#pragma unroll
-            for (int g = 0; g < CG / 8; ++g) {
-              float v[8];
-#pragma unroll
-              for (int j = 0; j < 8; ++j) v[j] = act[8 * g + j] * osc;
-              uint4 hi, lo;
-              split8(v, hi, lo);
-              oh[g] = hi;
-              ol[g] = lo;
-            }
-          }
-        } else {
-          if (r > t.y0 - H) consume_d4(t, x, r - 2);     // the previous iteration's a3 row
-          write_a4(act);
+        if (!FIRST) {                                    // a3 row -> layer-4 MMA
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mb_arrive(a4full);
         }
       }
       if (!FIRST) consume_d4(t, x, t.y1);                 // the unit's last a3 row
