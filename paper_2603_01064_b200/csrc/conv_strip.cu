@@ -511,18 +511,29 @@ __global__ void __launch_bounds__(NTHR, 1)
         if (!FIRST && r > t.y0 - H) consume_d4(t, x, r - 2);
         const bool store = FIRST && yo >= t.y0 && yo < t.y1 && x < n;
         const int64_t off = (((int64_t)t.b * n + (store ? yo : 0)) * n + x) * C + c0;
-        // 8 channels at a time: D_2 -> this row's activation, D_1 / D_0 -> the carries
+        // 8 channels at a time: D_2 -> this row's activation, D_1 / D_0 -> the carries.  With
+        // 16 channels per thread all 48 columns are loaded before one wait (latency once per row)
+        constexpr int GB = CG == 16 ? 2 : 1;             // chunks per TMEM wait
+        uint32_t DD[GB][24];
 #pragma unroll
         for (int g = 0; g < CG / 8; ++g) {
-          uint32_t D[24];
-          if (valid) {
-            tld8(tb + 2 * C + 8 * g, D);
-            tld8(tb + C + 8 * g, D + 8);
-            tld8(tb + 8 * g, D + 16);
-            tld_wait<24>(D);
-          } else {
+          uint32_t* D = DD[g % GB];
+          if (g % GB == 0) {
+            if (valid) {
 #pragma unroll
-            for (int j = 0; j < 24; ++j) D[j] = 0u;
+              for (int gg = 0; gg < GB; ++gg) {
+                tld8(tb + 2 * C + 8 * (g + gg), DD[gg]);
+                tld8(tb + C + 8 * (g + gg), DD[gg] + 8);
+                tld8(tb + 8 * (g + gg), DD[gg] + 16);
+              }
+#pragma unroll
+              for (int gg = 0; gg < GB; ++gg) tld_wait<24>(DD[gg]);
+            } else {
+#pragma unroll
+              for (int gg = 0; gg < GB; ++gg)
+#pragma unroll
+                for (int j = 0; j < 24; ++j) DD[gg][j] = 0u;
+            }
           }
           float act[8];
 #pragma unroll
