@@ -221,11 +221,12 @@ nmg_status make_map16(CUtensorMap* m, const uint16_t* p, int64_t rows, int64_t c
 }
 
 // digit planes [S][rows][K] int8, box {64, box_rows, S}, SWIZZLE_64B
-nmg_status make_digit_map(CUtensorMap* m, const int8_t* p, int S, int64_t rows, int64_t K, int box_rows) {
+nmg_status make_digit_map(CUtensorMap* m, const int8_t* p, int S, int64_t rows, int64_t K, int box_rows,
+                          int box_digits = 0) {
   NMG_TRY(get_encoder());
   cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)S};
   cuuint64_t strides[2] = {(cuuint64_t)K, (cuuint64_t)(rows * K)};
-  cuuint32_t box[3] = {64u, (cuuint32_t)box_rows, (cuuint32_t)S};
+  cuuint32_t box[3] = {64u, (cuuint32_t)box_rows, (cuuint32_t)(box_digits > 0 ? box_digits : S)};
   cuuint32_t es[3] = {1u, 1u, 1u};
   CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)p, dims, strides, box, es,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
@@ -1221,7 +1222,7 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
   }
   if (d.dim == 1) {
     const char* fenv = std::getenv("NMG_FP64");
-    h->ozaki = h->use_tc && n % 64 == 0 && n >= 64 && !(fenv && std::string(fenv) == "dmma");
+    h->ozaki = h->use_tc && n % 128 == 0 && /* CTA pairs along N */ !(fenv && std::string(fenv) == "dmma");
     if (h->ozaki) {
       // W digits of A (rows n, K = n), host: exponent per row, S truncation digits
       const int S = ozaki_digits();
@@ -1250,7 +1251,7 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
       NMG_TRY(h->xdig.alloc((size_t)S * B * n));
       NMG_TRY(h->xexp.alloc(B));
       NMG_TRY(make_digit_map(&h->mWd, h->wdig.p, S, n, n, 64));
-      NMG_TRY(make_digit_map(&h->mXd, h->xdig.p, S, (int64_t)B, n, 128));
+      NMG_TRY(make_digit_map(&h->mXd, h->xdig.p, S, (int64_t)B, n, 64, 1));   // half tiles, one digit per box
     }
   }
   h->split_fresh.assign(h->L, 0);

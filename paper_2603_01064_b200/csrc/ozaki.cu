@@ -47,6 +47,22 @@ NMG_D void tma3d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1,
       "l"(m), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+// multicast to the CTAs of `mask` (same smem offsets, complete_tx on each CTA's barrier)
+NMG_D void tma3d_mc(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%3, "
+      "%4, %5}], [%2], %6;\n" ::"r"(su32(dst)),
+      "l"(m), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2), "h"(mask)
+      : "memory");
+}
+NMG_D void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+NMG_D uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
 NMG_D uint64_t desc_sw64(uint32_t saddr) {
   uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
   d |= (uint64_t)1 << 16;
@@ -66,7 +82,10 @@ NMG_D void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t a
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
-__global__ void __launch_bounds__(ONT, 1)
+// CTA pairs along N share the X digit tile: each CTA loads half of its rows and multicasts
+// it to both (halving the L2 -> SM traffic of X, which every N tile re-reads); a stage is
+// refilled only after the MMAs of BOTH CTAs released it (commit multicast, count 2).
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ONT, 1)
     ozaki_resid_kernel(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mW,
                        OzakiArgs a) {
   extern __shared__ __align__(1024) uint8_t smraw[];
@@ -79,8 +98,9 @@ __global__ void __launch_bounds__(ONT, 1)
   const int m0 = blockIdx.y * OBM, n0 = blockIdx.x * OBN;
   const int KT = a.K / OBK;
 
+  const uint32_t crank = cluster_rank();
   if (tid == 0) {
-    for (int s = 0; s < ONSTAGE; ++s) { mb_init(&full[s], 1); mb_init(&empty[s], 1); }
+    for (int s = 0; s < ONSTAGE; ++s) { mb_init(&full[s], 1); mb_init(&empty[s], 2); }
     mb_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -89,7 +109,7 @@ __global__ void __launch_bounds__(ONT, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
+  cluster_sync();                                 // both CTAs' barriers exist before any multicast
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tslot;
 
@@ -99,8 +119,10 @@ __global__ void __launch_bounds__(ONT, 1)
         const int s = kt % ONSTAGE;
         mb_wait(&empty[s], ((uint32_t)(kt / ONSTAGE) & 1u) ^ 1u);
         uint8_t* st = sm + s * OSTAGE;
-        mb_expect(&full[s], OSTAGE);
-        tma3d(st, &mX, &full[s], kt * OBK, m0, 0);
+        mb_expect(&full[s], OSTAGE);                 // own W + both halves of X
+#pragma unroll
+        for (int d = 0; d < OS; ++d)                 // rows [64 r, 64 r + 64) of every X digit plane
+          tma3d_mc(st + d * OBM * OBK + crank * 64 * OBK, &mX, &full[s], kt * OBK, m0 + (int)crank * 64, d, 3);
         tma3d(st + XS_BYTES, &mW, &full[s], kt * OBK, n0, 0);
       }
     }
@@ -130,9 +152,12 @@ __global__ void __launch_bounds__(ONT, 1)
             }
           }
         }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                         su32(&empty[s]))
-                     : "memory");
+        // the stage is free when both CTAs' MMAs have read it
+        asm volatile(
+            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+                su32(&empty[s])),
+            "h"((uint16_t)3)
+            : "memory");
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(done))
                    : "memory");
@@ -182,7 +207,7 @@ __global__ void __launch_bounds__(ONT, 1)
     if (a.part) a.part[(int64_t)m * gridDim.x + blockIdx.x] = sq;
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
+  cluster_sync();                                 // no CTA leaves while its peer may still signal it
   if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
 
