@@ -242,12 +242,13 @@ __global__ void __launch_bounds__(NTHR, 1)
       for (int i = tid; i < 2 * G::W4BYTES / 16; i += NTHR) d4[i] = __ldg(g4 + i);
     }
     const float* wsrc = FIRST ? a.w_in : a.w_out;      // [c][9]
+    const float wsc = FIRST ? a.in_scale : 1.f;         // layers 1-2: w0, b0 pre-scaled by S1
     for (int i = tid; i < 9 * C; i += NTHR) {
       const int t = i / C, c = i - t * C;
-      swt[i] = __ldg(wsrc + c * 9 + t);
+      swt[i] = __ldg(wsrc + c * 9 + t) * wsc;
     }
     if (FIRST)
-      for (int i = tid; i < C; i += NTHR) swt[9 * C + i] = __ldg(a.w_in + 9 * C + i);
+      for (int i = tid; i < C; i += NTHR) swt[9 * C + i] = __ldg(a.w_in + 9 * C + i) * wsc;
   }
   if (tid == 0) {
     for (int s = 0; s < NSTG; ++s) { mb_init(&full[s], FIRST ? RL::NPROD : 1); mb_init(&empty[s], 1); }
@@ -272,88 +273,105 @@ __global__ void __launch_bounds__(NTHR, 1)
   if (warp >= PROD0 && warp < (FIRST ? MMAW : MMAW - 1)) {
     // ------------------------------------------------------------------ producer
     if (FIRST) {
-      // thread owns position p of the row buffer (x = X0 - 1 + p) and RL::CH channels
-      // starting at ch0; a 3 x 3 window of b slides down with the rows, the next row prefetched
+      // item = (position pair p, p + 65 of the row buffer (x = X0 - 1 + p), channel half);
+      // 130 items over the 160 producer threads, the weights of a tap loaded once for both
+      // positions; 3 x 3 windows of b slide down with the rows, the next row prefetched.
+      // w0 and b0 in shared memory are pre-scaled by S1 (ReLU(S z) = S ReLU(z), S > 0).
+      constexpr int HC = C / 2;                            // channels per item
+      constexpr int PP = RP / 2;                           // 65 position pairs
       const int pt = tid - PROD0 * 32;
-      constexpr int SPAN = RL::CH == C ? RL::NPROD * 32 : (RL::NPROD * 32) / 2;   // threads per channel half
-      const int p = pt % SPAN;
-      const int ch0 = (pt / SPAN) * RL::CH;
-      const bool act = p < RP && pt / SPAN < C / RL::CH;
-      const float sc = a.in_scale;
+      const int j = pt % PP, half = pt / PP;
+      const bool act = pt < 2 * PP;
+      const int c0p = half * HC;
       int it = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const Unit t = unit_of(u, n, nx, a.ysplit);
         const double s = a.norms ? a.norms[t.b] : 1.0;
         const float inv = (float)((s != 0.0) ? 1.0 / s : 0.0);
         const float* B = a.b + (int64_t)t.b * n * n;
-        const int x = t.X0 - 1 + p;
-        const bool xin = act && x >= 0 && x < n;
-        auto ld3 = [&](int yy, float* w) {
-          const bool ok = xin && yy >= 0 && yy < n;
-          const float* row = B + (int64_t)yy * n;
+        int xs[2];
+        bool xin[2];
 #pragma unroll
-          for (int t1 = 0; t1 < 3; ++t1) {
-            const int xx = x + t1 - 1;
-            w[t1] = (ok && xx >= 0 && xx < n) ? __ldg(row + xx) : 0.f;
+        for (int e = 0; e < 2; ++e) {
+          xs[e] = t.X0 - 1 + j + e * PP;
+          xin[e] = act && xs[e] >= 0 && xs[e] < n;
+        }
+        auto ld3 = [&](int yy, float (*w)[3]) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const bool ok = xin[e] && yy >= 0 && yy < n;
+            const float* row = B + (int64_t)yy * n;
+#pragma unroll
+            for (int t1 = 0; t1 < 3; ++t1) {
+              const int xx = xs[e] + t1 - 1;
+              w[e][t1] = (ok && xx >= 0 && xx < n) ? __ldg(row + xx) : 0.f;
+            }
           }
         };
         const int r0 = max(t.y0 - H, 0), r1 = min(t.y1 + H - 1, n - 1);
-        float win[3][3];
+        float win[3][2][3];
         ld3(r0 - 1, win[0]);
         ld3(r0, win[1]);
         ld3(r0 + 1, win[2]);
         for (int r = r0; r <= r1; ++r, ++it) {
-          float nxt[3];
+          float nxt[2][3];
           ld3(r + 2, nxt);                       // in flight while this row is computed
-          float uu[9];
+          float uu[2][9];
 #pragma unroll
-          for (int t2 = 0; t2 < 3; ++t2)
+          for (int e = 0; e < 2; ++e)
 #pragma unroll
-            for (int t1 = 0; t1 < 3; ++t1) uu[t2 * 3 + t1] = win[t2][t1] * inv;
+            for (int t2 = 0; t2 < 3; ++t2)
+#pragma unroll
+              for (int t1 = 0; t1 < 3; ++t1) uu[e][t2 * 3 + t1] = win[t2][e][t1] * inv;
           const int st = it % NSTG;
           mb_wait(&empty[st], ((uint32_t)(it / NSTG) & 1u) ^ 1u);
           if (act) {
             uint4* ah = reinterpret_cast<uint4*>(ring + st * 2 * G::ABYTES);
             uint4* al = reinterpret_cast<uint4*>(ring + st * 2 * G::ABYTES + G::ABYTES);
 #pragma unroll 1
-            for (int g = ch0 / 16; g < (ch0 + RL::CH) / 16; ++g) {
-              float v[16];
+            for (int g = c0p / 8; g < (c0p + HC) / 8; ++g) {
+              float v[2][8];
+              {
+                const float4 b0a = *reinterpret_cast<const float4*>(swt + 9 * C + 8 * g);
+                const float4 b0b = *reinterpret_cast<const float4*>(swt + 9 * C + 8 * g + 4);
 #pragma unroll
-              for (int j = 0; j < 16; j += 4) {
-                const float4 bb = *reinterpret_cast<const float4*>(swt + 9 * C + 16 * g + j);
-                v[j] = bb.x; v[j + 1] = bb.y; v[j + 2] = bb.z; v[j + 3] = bb.w;
-              }
-#pragma unroll
-              for (int q9 = 0; q9 < 9; ++q9) {
-#pragma unroll
-                for (int j = 0; j < 16; j += 4) {
-                  const float4 w = *reinterpret_cast<const float4*>(swt + q9 * C + 16 * g + j);
-                  v[j] = fmaf(w.x, uu[q9], v[j]);
-                  v[j + 1] = fmaf(w.y, uu[q9], v[j + 1]);
-                  v[j + 2] = fmaf(w.z, uu[q9], v[j + 2]);
-                  v[j + 3] = fmaf(w.w, uu[q9], v[j + 3]);
+                for (int e = 0; e < 2; ++e) {
+                  v[e][0] = b0a.x; v[e][1] = b0a.y; v[e][2] = b0a.z; v[e][3] = b0a.w;
+                  v[e][4] = b0b.x; v[e][5] = b0b.y; v[e][6] = b0b.z; v[e][7] = b0b.w;
                 }
               }
 #pragma unroll
-              for (int j = 0; j < 16; ++j) v[j] = xin ? fmaxf(v[j], 0.f) * sc : 0.f;
-              uint4 hi, lo;
-              split8(v, hi, lo);
-              ah[(2 * g) * RP + p] = hi;
-              al[(2 * g) * RP + p] = lo;
-              split8(v + 8, hi, lo);
-              ah[(2 * g + 1) * RP + p] = hi;
-              al[(2 * g + 1) * RP + p] = lo;
+              for (int q9 = 0; q9 < 9; ++q9) {
+                const float4 wa = *reinterpret_cast<const float4*>(swt + q9 * C + 8 * g);
+                const float4 wb = *reinterpret_cast<const float4*>(swt + q9 * C + 8 * g + 4);
+                const float w8[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+#pragma unroll
+                for (int e = 0; e < 2; ++e)
+#pragma unroll
+                  for (int c = 0; c < 8; ++c) v[e][c] = fmaf(w8[c], uu[e][q9], v[e][c]);
+              }
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+#pragma unroll
+                for (int c = 0; c < 8; ++c) v[e][c] = xin[e] ? fmaxf(v[e][c], 0.f) : 0.f;
+                uint4 hi, lo;
+                split8(v[e], hi, lo);
+                ah[g * RP + j + e * PP] = hi;
+                al[g * RP + j + e * PP] = lo;
+              }
             }
           }
           asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
           __syncwarp();
           if (lane == 0) mb_arrive(&full[st]);
 #pragma unroll
-          for (int t1 = 0; t1 < 3; ++t1) {
-            win[0][t1] = win[1][t1];
-            win[1][t1] = win[2][t1];
-            win[2][t1] = nxt[t1];
-          }
+          for (int e = 0; e < 2; ++e)
+#pragma unroll
+            for (int t1 = 0; t1 < 3; ++t1) {
+              win[0][e][t1] = win[1][e][t1];
+              win[1][e][t1] = win[2][e][t1];
+              win[2][e][t1] = nxt[e][t1];
+            }
         }
       }
     } else if (tid == PROD0 * 32) {
