@@ -194,14 +194,15 @@ __global__ void __launch_bounds__(NT, 3) smooth1d_f16_kernel(Smooth1dArgs a) {
       const int pt = tid - 128;                 // 0..127
       const int half = pt >> 6;                 // channels 8 half .. 8 half + 7
       const int r0 = pt & 63;                   // rows r0, r0 + 64, r0 + 128 (< AR)
+      // weights with u = b / s and the f16 scale S1 folded in (ReLU(S z) = S ReLU(z), S > 0)
+      const float sc = a.in_scale;
       float wr[8][KS], br[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        br[j] = b0[8 * half + j];
+        br[j] = b0[8 * half + j] * sc;
 #pragma unroll
-        for (int t = 0; t < KS; ++t) wr[j][t] = w0[(8 * half + j) * KS + t] * inv;   // u = b / s folded in
+        for (int t = 0; t < KS; ++t) wr[j][t] = w0[(8 * half + j) * KS + t] * (inv * sc);
       }
-      const float sc = a.in_scale;
       for (int k = 0; k < ntile; ++k) {
         const int st = k & 1;
         mb_wait(&aempty[st], ((uint32_t)(k >> 1) & 1u) ^ 1u);
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(NT, 3) smooth1d_f16_kernel(Smooth1dArgs a) {
               acc = fmaf(wr[j][2], x2, acc);
               acc = fmaf(wr[j][3], x3, acc);
               acc = fmaf(wr[j][4], x4, acc);
-              v[j] = fmaxf(acc, 0.f) * sc;
+              v[j] = fmaxf(acc, 0.f);
             }
           } else {
 #pragma unroll
