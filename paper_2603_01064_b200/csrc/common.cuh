@@ -33,4 +33,11 @@ NMG_D double block_sum_f64(double v, double* scratch /* >= 32 doubles */) {
   return t;
 }
 
+// 2D level-filter input, paired layout: right-hand sides 2p and 2p + 1 are the real and the
+// imaginary part of complex image p (F' is a real symmetric operator, so one complex 2D FFT
+// filters both, see filter2d).  N = n * n pixels per image.
+NMG_D void zput(float2* Z, int64_t N, int b, int64_t pix, float v) {
+  reinterpret_cast<float*>(Z)[((int64_t)(b >> 1) * N + pix) * 2 + (b & 1)] = v;
+}
+
 }  // namespace nmg

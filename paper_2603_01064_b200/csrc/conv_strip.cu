@@ -602,23 +602,27 @@ __global__ void __launch_bounds__(NTHR, 1)
 
 // h(y, x) = s (b3 + Q0(y, x - 1) + Q1(y, x) + Q2(y, x + 1))  ->  Z = (h, 0) or x (+)= h
 __global__ void strip_combine_kernel(int n, int nrhs, const float4* __restrict__ Q, const double* __restrict__ norms,
-                                     const float* __restrict__ b3, float2* __restrict__ Z, float* __restrict__ xo,
-                                     int accumulate) {
+                                     const float* __restrict__ b3, float2* __restrict__ Z, int zb0,
+                                     float* __restrict__ xo, int accumulate) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t per = (int64_t)n * n;
   if (idx >= nrhs * per) return;
   const int b = (int)(idx / per);
   const int x = (int)(idx % n);
   const double s = norms ? norms[b] : 1.0;
-  float hv = 0.f;
+  float acc = 0.f;
   if (s != 0.0) {
-    float acc = __ldg(b3) + __ldg(&Q[idx].y);
+    acc = __ldg(b3) + __ldg(&Q[idx].y);
     if (x > 0) acc += __ldg(&Q[idx - 1].x);
     if (x < n - 1) acc += __ldg(&Q[idx + 1].z);
-    hv = acc * (float)s;
   }
-  if (Z) Z[idx] = make_float2(hv, 0.f);
-  else xo[idx] = accumulate ? xo[idx] + hv : hv;
+  // the filter path takes N(u) unscaled (O(1) for every RHS, so two paired RHS of very
+  // different ||b|| do not pollute each other); filter2d multiplies by s after F'
+  if (Z) zput(Z, per, zb0 + b, idx - (int64_t)b * per, acc);
+  else {
+    const float hv = acc * (float)s;
+    xo[idx] = accumulate ? xo[idx] + hv : hv;
+  }
 }
 
 template <int C, bool FIRST>
@@ -652,11 +656,11 @@ void strip_l34(const CUtensorMap* mh, const CUtensorMap* ml, const StripArgs& a,
   if (a.C == 32) launch<32, false>(mh, ml, a, num_sms, s);
   else launch<48, false>(mh, ml, a, num_sms, s);
 }
-void strip_combine(int n, int nrhs, const float* q, const double* norms, const float* b3, float2* Z, float* x,
-                   bool accumulate, cudaStream_t s) {
+void strip_combine(int n, int nrhs, const float* q, const double* norms, const float* b3, float2* Z, int zb0,
+                   float* x, bool accumulate, cudaStream_t s) {
   const int64_t tot = (int64_t)nrhs * n * n;
   strip_combine_kernel<<<(int)ceil_div64(tot, 256), 256, 0, s>>>(n, nrhs, reinterpret_cast<const float4*>(q), norms,
-                                                                 b3, Z, x, accumulate ? 1 : 0);
+                                                                 b3, Z, zb0, x, accumulate ? 1 : 0);
 }
 
 }  // namespace nmg

@@ -369,7 +369,7 @@ constexpr int OW = 32, OH = 16, OPAD = 17;
 __global__ void __launch_bounds__(128) conv_out_kernel(int n, const float* __restrict__ ih,
                                                        const double* __restrict__ norms, const float* __restrict__ w3,
                                                        const float* __restrict__ b3, float2* __restrict__ Z,
-                                                       float* __restrict__ x, int accumulate) {
+                                                       int zb0, float* __restrict__ x, int accumulate) {
   __shared__ float tile[(OH + 2) * (OW + 2) * OPAD];
   __shared__ float ws[CC * 9];
   const int tiles_x = ceil_div(n, OW);
@@ -419,10 +419,10 @@ __global__ void __launch_bounds__(128) conv_out_kernel(int n, const float* __res
   for (int p = 0; p < 4; ++p) {
     const int xx = tx0 + lx + p;
     if (xx >= n) continue;
-    const float hv = (s == 0.0) ? 0.f : (acc[p] + b) * (float)s;
+    const float nv = (s == 0.0) ? 0.f : acc[p] + b;    // N(u); the filter path scales by s after F'
     const int64_t o = ((int64_t)rb * n + y) * n + xx;
-    if (Z) Z[o] = make_float2(hv, 0.f);
-    else x[o] = accumulate ? x[o] + hv : hv;
+    if (Z) zput(Z, (int64_t)n * n, zb0 + rb, (int64_t)y * n + xx, nv);
+    else x[o] = accumulate ? x[o] + nv * (float)s : nv * (float)s;
   }
 }
 
@@ -472,9 +472,9 @@ void conv_in(int n, int nrhs, const float* b, const double* norms, const float* 
 }
 
 void conv_out(int n, int nrhs, const float* in, const double* norms, const float* w3, const float* b3, float2* Z,
-              float* x, bool accumulate, cudaStream_t s) {
+              int zb0, float* x, bool accumulate, cudaStream_t s) {
   dim3 grid(ceil_div(n, OW) * ceil_div(n, OH), nrhs);
-  conv_out_kernel<<<grid, 128, 0, s>>>(n, in, norms, w3, b3, Z, x, accumulate ? 1 : 0);
+  conv_out_kernel<<<grid, 128, 0, s>>>(n, in, norms, w3, b3, Z, zb0, x, accumulate ? 1 : 0);
 }
 
 }  // namespace nmg

@@ -156,8 +156,13 @@ void prolong_add2d(int nrhs, int n_c, const float* c, float* f, cudaStream_t s);
 void qstencil(int nrhs, int n, int hb, float alpha, const float* Q, const float* X, const float* C, float* D,
               cudaStream_t s);
 void norms_f32(int nrhs, int64_t N, const float* x, double* part, int chunks, double* out, cudaStream_t s);
-void filter2d(int nrhs, int n, float2* Z, const float2* tw, int tw_n, float* x, bool accumulate, cudaStream_t s);
-void real_to_complex(int64_t count, const float* x, float2* Z, cudaStream_t s);
+// level filter on the paired layout written by zput (common.cuh); filter2d_prepare zeroes the
+// imaginary partner of the last image when nrhs is odd (call before the writers)
+// norms (may be null): per-RHS ||b||; the writers store N(u) and x gets ||b|| F'(N(u))
+void filter2d(int nrhs, int n, float2* Z, const float2* tw, int tw_n, float* x, bool accumulate, cudaStream_t s,
+              const double* norms);
+void filter2d_prepare(int nrhs, int n, float2* Z, cudaStream_t s);
+void real_to_complex(int nrhs, int64_t N, const float* x, float2* Z, cudaStream_t s);
 
 // ---- 2D CNN on tensor cores (conv_tc.cu), C = 32 ------------------------------------
 // Activations: padded pixel-major fp32 [b][n+2][n+2][32], zero border.
@@ -172,7 +177,7 @@ int conv_tc_smem();
 void conv_in(int n, int nrhs, const float* b, const double* norms, const float* w0, const float* b0, float* o1,
              float* z2, cudaStream_t s);   // also zeroes the borders of o1 and z2
 void conv_out(int n, int nrhs, const float* in, const double* norms, const float* w3, const float* b3, float2* Z,
-              float* x, bool accumulate, cudaStream_t s);
+              int zb0, float* x, bool accumulate, cudaStream_t s);
 void zero_border(int n, int nrhs, int C, float* buf, cudaStream_t s);
 
 // ---- 2D CNN, FP16x3 tcgen05 column-strip kernels (conv_strip.cu), n % 128 == 0, C = 32/48 --
@@ -201,7 +206,7 @@ struct StripArgs {
 int strip_ysplit(int n, int nrhs, int num_sms);
 void strip_l12(const StripArgs& a, int num_sms, cudaStream_t s);
 void strip_l34(const CUtensorMap* mh, const CUtensorMap* ml, const StripArgs& a, int num_sms, cudaStream_t s);
-void strip_combine(int n, int nrhs, const float* q, const double* norms, const float* b3, float2* Z, float* x,
-                   bool accumulate, cudaStream_t s);
+void strip_combine(int n, int nrhs, const float* q, const double* norms, const float* b3, float2* Z, int zb0,
+                   float* x, bool accumulate, cudaStream_t s);
 
 }  // namespace nmg

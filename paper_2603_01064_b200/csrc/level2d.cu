@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(256, 1) cnn2d_kernel(Cnn2dArgs a) {
       for (int i = tid; i < CT * CT; i += 256) {
         const int y = ty0 + i / CT, x = tx0 + i % CT;
         if (y < n && x < n) {
-          if (a.Z) a.Z[((int64_t)b * n + y) * n + x] = make_float2(0.f, 0.f);
+          if (a.Z) zput(a.Z, (int64_t)n * n, b, (int64_t)y * n + x, 0.f);
           else a.x[((int64_t)b * n + y) * n + x] = 0.f;
         }
       }
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(256, 1) cnn2d_kernel(Cnn2dArgs a) {
     if (gy < n && gx < n) {
       const float hv = acc * (float)s;
       const int64_t off = ((int64_t)b * n + gy) * n + gx;
-      if (a.Z) a.Z[off] = make_float2(hv, 0.f);
+      if (a.Z) zput(a.Z, (int64_t)n * n, b, (int64_t)gy * n + gx, acc);   // N(u): scaled by s after F'
       else a.x[off] = a.accumulate ? a.x[off] + hv : hv;
     }
   }
@@ -260,7 +260,8 @@ __global__ void __launch_bounds__(256, 1) cnn2d_kernel(Cnn2dArgs a) {
 // rows: R rows of length n per CTA (R*n <= 4096 complex in smem), in place in Z
 __global__ void __launch_bounds__(256) fft_rows_kernel(int n, int64_t nrows, float2* __restrict__ Z,
                                                        const float2* __restrict__ tw, int tw_n, int inverse,
-                                                       float* __restrict__ x, int accumulate, float scale) {
+                                                       float* __restrict__ x, int accumulate, float scale, int nrhs,
+                                                       const double* __restrict__ norms) {
   extern __shared__ __align__(16) float2 cb[];
   const int R = max(1, 4096 / n);
   const int64_t r0 = (int64_t)blockIdx.x * R;
@@ -274,10 +275,20 @@ __global__ void __launch_bounds__(256) fft_rows_kernel(int n, int64_t nrows, flo
     for (int i = threadIdx.x; i < tot; i += 256) Z[r0 * n + i] = cb[i];
   } else {
     fft_dit_inverse_batch(cb, n, rows, n, 1, tw, tw_n, threadIdx.x, 256);
+    // complex image p holds RHS 2p (real part) and 2p + 1 (imaginary part)
+    const int64_t N = (int64_t)n * n;
     for (int i = threadIdx.x; i < tot; i += 256) {
-      const float v = cb[i].x * scale;
-      const int64_t o = r0 * n + i;
-      x[o] = accumulate ? x[o] + v : v;
+      const int64_t R = r0 + i / n;                      // complex row
+      const int64_t p = R / n;
+      const int64_t o = (2 * p * n + (R - p * n)) * n + i % n;
+      const float s0 = norms ? (float)norms[2 * p] : 1.f;
+      const float v0 = (cb[i].x * scale) * s0;
+      x[o] = accumulate ? x[o] + v0 : v0;
+      if (2 * p + 1 < nrhs) {
+        const float s1 = norms ? (float)norms[2 * p + 1] : 1.f;
+        const float v1 = (cb[i].y * scale) * s1;
+        x[o + N] = accumulate ? x[o + N] + v1 : v1;
+      }
     }
   }
 }
@@ -312,9 +323,11 @@ __global__ void __launch_bounds__(256) fft_cols_kernel(int n, int G, float2* __r
   }
 }
 
-__global__ void real_to_complex_kernel(int64_t count, const float* __restrict__ x, float2* __restrict__ Z) {
+__global__ void real_to_complex_kernel(int nrhs, int64_t N, const float* __restrict__ x, float2* __restrict__ Z) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < count) Z[i] = make_float2(x[i], 0.f);
+  if (i >= (int64_t)nrhs * N) return;
+  const int b = (int)(i / N);
+  zput(Z, N, b, i - (int64_t)b * N, x[i]);
 }
 
 }  // namespace
@@ -349,21 +362,29 @@ void cnn2d(const Cnn2dArgs& a, cudaStream_t s) {
     cnn2d_kernel<48><<<grid, 256, smem, s>>>(a);
   }
 }
-void filter2d(int nrhs, int n, float2* Z, const float2* tw, int tw_n, float* x, bool accumulate, cudaStream_t s) {
-  const int64_t nrows = (int64_t)nrhs * n;
+void filter2d(int nrhs, int n, float2* Z, const float2* tw, int tw_n, float* x, bool accumulate, cudaStream_t s,
+              const double* norms) {
+  // paired layout: (nrhs + 1) / 2 complex images, each the real-part / imaginary-part pair of
+  // two right-hand sides; F' is real and symmetric, so Re and Im of the filtered pair are the
+  // two filtered images (the odd RHS out has a zero partner, zeroed by filter2d_prepare)
+  const int npair = (nrhs + 1) / 2;
+  const int64_t nrows = (int64_t)npair * n;
   const int R = std::max(1, 4096 / n);
   const size_t smr = sizeof(float2) * (size_t)R * n;
   cudaFuncSetAttribute(fft_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
-  fft_rows_kernel<<<nblk(nrows, R), 256, smr, s>>>(n, nrows, Z, tw, tw_n, 0, nullptr, 0, 1.f);
+  fft_rows_kernel<<<nblk(nrows, R), 256, smr, s>>>(n, nrows, Z, tw, tw_n, 0, nullptr, 0, 1.f, nrhs, nullptr);
   const int G = std::min(n, std::max(1, 16384 / n));
   const size_t smc = sizeof(float2) * (size_t)n * G;
   cudaFuncSetAttribute(fft_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
-  fft_cols_kernel<<<dim3(n / G, nrhs), 256, smc, s>>>(n, G, Z, tw, tw_n);
+  fft_cols_kernel<<<dim3(n / G, npair), 256, smc, s>>>(n, G, Z, tw, tw_n);
   fft_rows_kernel<<<nblk(nrows, R), 256, smr, s>>>(n, nrows, Z, tw, tw_n, 1, x, accumulate ? 1 : 0,
-                                                   1.0f / ((float)n * (float)n));
+                                                   1.0f / ((float)n * (float)n), nrhs, norms);
 }
-void real_to_complex(int64_t count, const float* x, float2* Z, cudaStream_t s) {
-  real_to_complex_kernel<<<nblk(count, 256), 256, 0, s>>>(count, x, Z);
+void filter2d_prepare(int nrhs, int n, float2* Z, cudaStream_t s) {
+  if (nrhs & 1) cudaMemsetAsync(Z + (int64_t)(nrhs / 2) * n * n, 0, sizeof(float2) * (size_t)n * n, s);
+}
+void real_to_complex(int nrhs, int64_t N, const float* x, float2* Z, cudaStream_t s) {
+  real_to_complex_kernel<<<nblk((int64_t)nrhs * N, 256), 256, 0, s>>>(nrhs, N, x, Z);
 }
 
 }  // namespace nmg

@@ -617,6 +617,7 @@ nmg_status smooth2d(nmg_hierarchy* h, int l, int nrhs, const float* b, float* x,
     NMG_TRY(check_launch(h));
   }
   const bool filt = filter && h->d.level_filter != 0;
+  if (filt) filter2d_prepare(nrhs, n, h->Z.p, s);
   if (h->conv_bf && strip_level(n) && h->bf_C == h->arch.channels) {
     const int C = h->arch.channels;
     const float* P = h->W[l]->p;
@@ -646,11 +647,11 @@ nmg_status smooth2d(nmg_hierarchy* h, int l, int nrhs, const float* b, float* x,
       a.w4 = wb + 4 * plane; a.a3_scale = sc[4] * dbg; a.d4_scale = 1.0f / (sc[4] * dbg * sc[5]);
       { Prof p(h, NMG_K_SMOOTH, s); strip_l34(&h->mA2h[l], &h->mA2l[l], a, h->num_sms, s); }
       { Prof p(h, NMG_K_SMOOTH, s);
-        strip_combine(n, cnt, h->qbuf.p, a.norms, b3, filt ? h->Z.p + off : nullptr, x + off, accumulate, s); }
+        strip_combine(n, cnt, h->qbuf.p, a.norms, b3, filt ? h->Z.p : nullptr, r0, x + off, accumulate, s); }
       NMG_TRY(check_launch(h));
     }
     if (filt) {
-      { Prof p(h, NMG_K_SMOOTH, s); filter2d(nrhs, n, h->Z.p, h->tw.p, h->tw_n, x, accumulate, s); }
+      { Prof p(h, NMG_K_SMOOTH, s); filter2d(nrhs, n, h->Z.p, h->tw.p, h->tw_n, x, accumulate, s, normalize ? h->snorm.p : nullptr); }
       NMG_TRY(check_launch(h));
     }
     return NMG_OK;
@@ -676,12 +677,12 @@ nmg_status smooth2d(nmg_hierarchy* h, int l, int nrhs, const float* b, float* x,
       ca.bias = b2; ca.out = h->act1.p;
       { Prof p(h, NMG_K_SMOOTH, s); conv3x3_tc(&h->mWAh[l * 2 + 1], &h->mWAl[l * 2 + 1], &h->mA2[l], ca, h->num_sms, s); }
       { Prof p(h, NMG_K_SMOOTH, s);
-        conv_out(n, cnt, h->act1.p, nrm ? nrm + r0 : nullptr, w3, b3, filt ? h->Z.p + off : nullptr, x + off,
+        conv_out(n, cnt, h->act1.p, nrm ? nrm + r0 : nullptr, w3, b3, filt ? h->Z.p : nullptr, r0, x + off,
                  accumulate, s); }
       NMG_TRY(check_launch(h));
     }
     if (filt) {
-      { Prof p(h, NMG_K_SMOOTH, s); filter2d(nrhs, n, h->Z.p, h->tw.p, h->tw_n, x, accumulate, s); }
+      { Prof p(h, NMG_K_SMOOTH, s); filter2d(nrhs, n, h->Z.p, h->tw.p, h->tw_n, x, accumulate, s, normalize ? h->snorm.p : nullptr); }
       NMG_TRY(check_launch(h));
     }
     return NMG_OK;
@@ -693,7 +694,7 @@ nmg_status smooth2d(nmg_hierarchy* h, int l, int nrhs, const float* b, float* x,
   { Prof p(h, NMG_K_SMOOTH, s); cnn2d(a, s); }
   NMG_TRY(check_launch(h));
   if (filt) {
-    { Prof p(h, NMG_K_SMOOTH, s); filter2d(nrhs, n, h->Z.p, h->tw.p, h->tw_n, x, accumulate, s); }
+    { Prof p(h, NMG_K_SMOOTH, s); filter2d(nrhs, n, h->Z.p, h->tw.p, h->tw_n, x, accumulate, s, normalize ? h->snorm.p : nullptr); }
     NMG_TRY(check_launch(h));
   }
   return NMG_OK;
@@ -827,8 +828,8 @@ nmg_status debug_2d(nmg_hierarchy* h, int l, int op, int nrhs, const float* fin,
       return check_launch(h);
     case NMG_OP_FILTER:
       if (!smoothed) return fail(NMG_ERR_INVALID_ARG, "no filter at the coarsest level");
-      { Prof p(h, NMG_K_SMOOTH, s); real_to_complex((int64_t)nrhs * n * n, fin, h->Z.p, s); }
-      { Prof p(h, NMG_K_SMOOTH, s); filter2d(nrhs, n, h->Z.p, h->tw.p, h->tw_n, fout, false, s); }
+      { Prof p(h, NMG_K_SMOOTH, s); filter2d_prepare(nrhs, n, h->Z.p, s); real_to_complex(nrhs, (int64_t)n * n, fin, h->Z.p, s); }
+      { Prof p(h, NMG_K_SMOOTH, s); filter2d(nrhs, n, h->Z.p, h->tw.p, h->tw_n, fout, false, s, nullptr); }
       return check_launch(h);
     case NMG_OP_CNN:
     case NMG_OP_SMOOTH:

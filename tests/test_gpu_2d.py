@@ -150,10 +150,13 @@ def test_homogeneity_and_batch_invariance_2d(small):
         h.vcycle(yd, xd)
         outs.append(xd.cpu().numpy() / s)
     assert np.array_equal(outs[0], outs[1])
+    # batch invariance: the 2D level filter transforms RHS pairs (2p, 2p + 1) as the real and
+    # imaginary part of one complex FFT, so a RHS run alone agrees with its
+    # batch result to rounding, not bitwise (1D and the rest of the 2D cycle are per-RHS)
     y1 = T(y[2:3], torch.float64)
     x1 = torch.zeros_like(y1)
     h.vcycle(y1, x1)
-    assert np.array_equal(x1.cpu().numpy()[0], outs[0][2])
+    assert rel_l2(x1.cpu().numpy()[0], outs[0][2]) < 1e-6
 
 
 @pytest.mark.parametrize("cfg_id,nrhs,cycles", [(2, 2, 2), (3, 1, 1), (4, 1, 1)])
