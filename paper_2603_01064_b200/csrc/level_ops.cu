@@ -44,13 +44,19 @@ __global__ void prolong_add1d_kernel(int nrhs, int n_c, const float* __restrict_
 }
 
 // ---- coarse solve: x = L^{-T} L^{-1} y with the host Cholesky factor (fp64) ----------
-// One warp per RHS; lane owns entries j = q*32 + lane.  Forward substitution walks
-// columns of L (rows of Lcol = L^T), backward walks rows of L.
+// One warp per RHS; lane owns entries j = q*32 + lane of the fp64 iterate.  Blocked
+// substitution over 32-wide diagonal blocks: inside a block the 32 sequential steps keep
+// the block's column (forward) / row (backward) of L in registers, so the dependent chain
+// per step is shfl -> mul -> fma; the off-diagonal update of the other blocks is a plain
+// accumulation of independent coalesced loads (Lcol[i*nc + j] = L[j][i]).
+NMG_D double coarse_ld(const double* p) { return __ldg(p); }
+
 template <int NQ>
 __global__ void __launch_bounds__(256) coarse_kernel(int nc, int nrhs, const double* __restrict__ Lrow,
                                                      const double* __restrict__ Lcol,
                                                      const float* __restrict__ y, int64_t ldy,
-                                                     float* __restrict__ x, int64_t ldx) {
+                                                     float* __restrict__ x, int64_t ldx,
+                                                     float* __restrict__ xh, float* __restrict__ xl) {
   const int lane = threadIdx.x & 31;
   const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (b >= nrhs) return;
@@ -63,110 +69,69 @@ __global__ void __launch_bounds__(256) coarse_kernel(int nc, int nrhs, const dou
   // forward: L z = y
 #pragma unroll
   for (int q0 = 0; q0 < NQ; ++q0) {
-    for (int il = 0; il < 32; ++il) {
-      const int i = q0 * 32 + il;
-      if (i >= nc) break;
-      double zi = __shfl_sync(0xffffffffu, z[q0], il);
-      zi = zi / Lrow[(int64_t)i * nc + i];
-      if (lane == il) z[q0] = zi;
-      const double* col = Lcol + (int64_t)i * nc;   // L[j][i] for all j
+    const int i0 = q0 * 32, jd = i0 + lane;
+    const bool okj = jd < nc;
+    double Lb[32];
 #pragma unroll
-      for (int q = q0; q < NQ; ++q) {
-        const int j = q * 32 + lane;
-        if (j > i && j < nc) z[q] = fma(-col[j], zi, z[q]);
+    for (int il = 0; il < 32; ++il)
+      Lb[il] = (okj && i0 + il < nc && il < lane) ? coarse_ld(Lcol + (int64_t)(i0 + il) * nc + jd) : 0.0;
+    const double dv = okj ? 1.0 / coarse_ld(Lcol + (int64_t)jd * nc + jd) : 1.0;
+#pragma unroll
+    for (int il = 0; il < 32; ++il) {
+      const double zi = __shfl_sync(0xffffffffu, z[q0], il) * __shfl_sync(0xffffffffu, dv, il);
+      z[q0] = (lane == il) ? zi : fma(-Lb[il], zi, z[q0]);
+    }
+#pragma unroll
+    for (int q = q0 + 1; q < NQ; ++q) {
+      const int j = q * 32 + lane;
+      double acc = z[q];
+#pragma unroll 8
+      for (int il = 0; il < 32; ++il) {
+        const double zi = __shfl_sync(0xffffffffu, z[q0], il);
+        if (j < nc && i0 + il < nc) acc = fma(-coarse_ld(Lcol + (int64_t)(i0 + il) * nc + j), zi, acc);
       }
+      z[q] = acc;
     }
   }
   // backward: L^T x = z
 #pragma unroll
   for (int q0 = NQ - 1; q0 >= 0; --q0) {
-    for (int il = 31; il >= 0; --il) {
-      const int i = q0 * 32 + il;
-      if (i >= nc) continue;
-      double xi = __shfl_sync(0xffffffffu, z[q0], il);
-      xi = xi / Lrow[(int64_t)i * nc + i];
-      if (lane == il) z[q0] = xi;
-      const double* row = Lrow + (int64_t)i * nc;   // L[i][j]
+    const int i0 = q0 * 32, jd = i0 + lane;
+    const bool okj = jd < nc;
+    double Lb[32];
 #pragma unroll
-      for (int q = 0; q <= q0; ++q) {
-        const int j = q * 32 + lane;
-        if (j < i) z[q] = fma(-row[j], xi, z[q]);
+    for (int il = 0; il < 32; ++il)
+      Lb[il] = (okj && i0 + il < nc && il > lane) ? coarse_ld(Lrow + (int64_t)(i0 + il) * nc + jd) : 0.0;
+    const double dv = okj ? 1.0 / coarse_ld(Lrow + (int64_t)jd * nc + jd) : 1.0;
+#pragma unroll
+    for (int il = 31; il >= 0; --il) {
+      const double xi = __shfl_sync(0xffffffffu, z[q0], il) * __shfl_sync(0xffffffffu, dv, il);
+      z[q0] = (lane == il) ? xi : fma(-Lb[il], xi, z[q0]);
+    }
+#pragma unroll
+    for (int q = 0; q < q0; ++q) {
+      const int j = q * 32 + lane;
+      double acc = z[q];
+#pragma unroll 8
+      for (int il = 0; il < 32; ++il) {
+        const double xi = __shfl_sync(0xffffffffu, z[q0], il);
+        if (i0 + il < nc) acc = fma(-coarse_ld(Lrow + (int64_t)(i0 + il) * nc + j), xi, acc);
       }
+      z[q] = acc;
     }
   }
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
     const int j = q * 32 + lane;
-    if (j < nc) x[(int64_t)b * ldx + j] = (float)z[q];
-  }
-}
-
-// Same solve with the factor staged in shared memory (row stride nc + 1 doubles, so the
-// column walk of the forward sweep is conflict-free) and 1 / L_ii precomputed; nc <= 128.
-template <int NQ>
-__global__ void __launch_bounds__(256) coarse_smem_kernel(int nc, int nrhs, const double* __restrict__ Lrow,
-                                                          const float* __restrict__ y, int64_t ldy,
-                                                          float* __restrict__ x, int64_t ldx,
-                                                          float* __restrict__ xh, float* __restrict__ xl) {
-  extern __shared__ double Ls[];             // [nc][nc + 1], then dinv[nc]
-  const int S = nc + 1;
-  double* dinv = Ls + (size_t)nc * S;
-  for (int i = threadIdx.x; i < nc * nc; i += blockDim.x) {
-    const int r = i / nc, c = i - r * nc;
-    Ls[r * S + c] = Lrow[i];
-  }
-  for (int i = threadIdx.x; i < nc; i += blockDim.x) dinv[i] = 1.0 / Lrow[(size_t)i * nc + i];
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int wpb = blockDim.x >> 5;
-  for (int b = blockIdx.x * wpb + (threadIdx.x >> 5); b < nrhs; b += gridDim.x * wpb) {
-    double z[NQ];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      const int j = q * 32 + lane;
-      z[q] = (j < nc) ? (double)y[(int64_t)b * ldy + j] : 0.0;
-    }
-#pragma unroll
-    for (int q0 = 0; q0 < NQ; ++q0) {
-      for (int il = 0; il < 32; ++il) {
-        const int i = q0 * 32 + il;
-        if (i >= nc) break;
-        const double zi = __shfl_sync(0xffffffffu, z[q0], il) * dinv[i];
-        if (lane == il) z[q0] = zi;
-#pragma unroll
-        for (int q = q0; q < NQ; ++q) {
-          const int j = q * 32 + lane;
-          if (j > i && j < nc) z[q] = fma(-Ls[j * S + i], zi, z[q]);
-        }
-      }
-    }
-#pragma unroll
-    for (int q0 = NQ - 1; q0 >= 0; --q0) {
-      for (int il = 31; il >= 0; --il) {
-        const int i = q0 * 32 + il;
-        if (i >= nc) continue;
-        const double xi = __shfl_sync(0xffffffffu, z[q0], il) * dinv[i];
-        if (lane == il) z[q0] = xi;
-#pragma unroll
-        for (int q = 0; q <= q0; ++q) {
-          const int j = q * 32 + lane;
-          if (j < i) z[q] = fma(-Ls[i * S + j], xi, z[q]);
-        }
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      const int j = q * 32 + lane;
-      if (j < nc) {
-        const float v = (float)z[q];
-        x[(int64_t)b * ldx + j] = v;
-        if (xh) {
-          uint32_t hh, ll;
-          asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(hh) : "f"(v));
-          asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(ll) : "f"(v - __uint_as_float(hh)));
-          xh[(int64_t)b * ldx + j] = __uint_as_float(hh);
-          xl[(int64_t)b * ldx + j] = __uint_as_float(ll);
-        }
+    if (j < nc) {
+      const float v = (float)z[q];
+      x[(int64_t)b * ldx + j] = v;
+      if (xh) {
+        uint32_t hh, ll;
+        asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(hh) : "f"(v));
+        asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(ll) : "f"(v - __uint_as_float(hh)));
+        xh[(int64_t)b * ldx + j] = __uint_as_float(hh);
+        xl[(int64_t)b * ldx + j] = __uint_as_float(ll);
       }
     }
   }
@@ -250,27 +215,8 @@ void coarse_chol_solve(int nc, int nrhs, const double* Lrow, const double* Lcol,
                        float* x, int64_t ldx, cudaStream_t s, float* xh, float* xl) {
   const int grid = ceil_div(nrhs, 8);
   const int nq = ceil_div(nc, 32);
-  if (nc <= 128) {
-    const size_t smem = sizeof(double) * ((size_t)nc * (nc + 1) + nc);
-    int sms = 148, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int g = std::min(grid, sms);
-    static bool attr[5] = {false, false, false, false, false};
-    const int full = (int)(sizeof(double) * ((size_t)128 * 129 + 128));
-#define NMG_COARSE_S(Q)                                                                                 \
-  case Q:                                                                                               \
-    if (!attr[Q]) {                                                                                     \
-      cudaFuncSetAttribute(coarse_smem_kernel<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, full);    \
-      attr[Q] = true;                                                                                   \
-    }                                                                                                   \
-    coarse_smem_kernel<Q><<<g, 256, smem, s>>>(nc, nrhs, Lrow, y, ldy, x, ldx, xh, xl);                  \
-    return;
-    switch (nq) { NMG_COARSE_S(1) NMG_COARSE_S(2) NMG_COARSE_S(3) NMG_COARSE_S(4) default: break; }
-#undef NMG_COARSE_S
-  }
 #define NMG_COARSE(Q) \
-  case Q: coarse_kernel<Q><<<grid, 256, 0, s>>>(nc, nrhs, Lrow, Lcol, y, ldy, x, ldx); break;
+  case Q: coarse_kernel<Q><<<grid, 256, 0, s>>>(nc, nrhs, Lrow, Lcol, y, ldy, x, ldx, xh, xl); break;
   switch (nq) {
     NMG_COARSE(1) NMG_COARSE(2) NMG_COARSE(3) NMG_COARSE(4)
     NMG_COARSE(5) NMG_COARSE(6) NMG_COARSE(7) NMG_COARSE(8)
