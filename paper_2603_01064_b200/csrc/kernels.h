@@ -73,6 +73,24 @@ struct TcGemmArgs {
   const float* xinv = nullptr;
   const float* winv = nullptr;
 };
+// 2D Kronecker apply passes on tcgen05 (kron_tc.cu).  A = fp32 [M][n] rows (TMA map, box
+// {16, 128}, SWIZZLE_64B), W = tf32 hi/lo [n][n] (box {16, kron_tile_n(n)}).
+enum { KRON_T = 0, KRON_RESID = 1 };
+struct KronArgs {
+  int M, n;                    // M = nrhs * n rows
+  int mode;                    // KRON_T: D = blockT(A W^T); KRON_RESID: D = Cin -/+ (blockT(A W^T) + alpha S(X))
+  float* D;                    // output [nrhs][n][n]
+  const float* X = nullptr;    // KRON_RESID: image for the mass stencil S = Q X Q^T
+  const float* Cin = nullptr;  // KRON_RESID: may be null (0), may alias D
+  const float* Q = nullptr;    // [n][n], half-bandwidth hb
+  int hb = 0;
+  float alpha = 0.f;
+  bool negate = false;
+};
+int kron_tile_n(int n);
+bool kron_supported(int n, int hb);
+void kron_tc(const CUtensorMap* A, const CUtensorMap* Wh, const CUtensorMap* Wl, const KronArgs& a, int sms,
+             cudaStream_t s);
 // bn = 256 or 64 (tile width; W maps must use box rows = bn)
 void tc_gemm(const CUtensorMap* xh, const CUtensorMap* xl, const CUtensorMap* wh, const CUtensorMap* wl,
              const TcGemmArgs& a, cudaStream_t s, int bn);

@@ -1,0 +1,338 @@
+// 2D Kronecker operator apply on the 5th-gen tensor cores (3xTF32, fp32-accurate):
+//   A_l X = Mat(hat A_l Vec X) = C_l X B_l^T + alpha Q_l X Q_l^T
+// on the row-major [i2][i1] image arrays (arr = X^T) as two GEMM passes over all RHS at once:
+//   pass 1 (KRON_T)    : T = blockT(arr C^T)                    (M = nrhs * n rows, K = n)
+//   pass 2 (KRON_RESID): D = Cin -/+ (blockT(T B^T) + alpha Q arr Q^T)
+// blockT = transposed store within each n x n image, so pass 2 again contracts along rows.
+// The banded mass term (Q_l has half-bandwidth <= 2, Q_0 = I) and the residual are computed
+// in pass 2's epilogue, so one residual costs 24 B/pixel of HBM traffic: pass 1 reads X and
+// writes T (fp32), pass 2 reads T, X, Cin and writes D.
+//
+// Kernel anatomy (persistent, one CTA per SM, 320 threads):
+//   warp 8 lane 0 : TMA producer — fp32 A tile (128 rows x 16 K) + W hi/lo tiles per stage
+//   warps 4-7     : splitters — A tile -> tf32 hi (in place) + lo (hi = rna(a), lo = rna(a - hi))
+//   warp 9 lane 0 : MMA issuer — 3 x tcgen05.mma.kind::tf32 per K=8 (hi*hi + hi*lo + lo*hi),
+//                   accumulating into one of two TMEM buffers (tile i uses buffer i & 1)
+//   warps 0-3     : epilogue — tcgen05.ld of the other buffer while the next tile's MMAs run
+// The hi/lo split of A happens in shared memory, so neither X nor T is ever written split.
+#include <cuda.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace nmg {
+namespace {
+
+constexpr int KBM = 128, KBK = 16;
+constexpr int KNT = 320;
+constexpr int A_BYTES = KBM * KBK * 4;   // 8 KB
+
+template <int TBN> struct KronCfg {
+  static constexpr int B_BYTES = TBN * KBK * 4;
+  static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;        // A (hi in place), A lo, W hi, W lo
+  static constexpr int STAGES = (200 * 1024 / STAGE) > 8 ? 8 : (200 * 1024 / STAGE);
+  static constexpr int SMEM = STAGES * STAGE + 1024 /*barriers*/ + 1024 /*align*/;
+  static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TBN >> 3) << 17) |
+                                    ((uint32_t)(KBM >> 4) << 24);   // D f32, A/B tf32 K-major, M = 128
+  static constexpr uint32_t TCOLS = 2 * TBN < 32 ? 32 : 2 * TBN;
+};
+
+NMG_D uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+NMG_D void mb_init(uint64_t* b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(c));
+}
+NMG_D void mb_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+NMG_D void mb_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
+}
+NMG_D void mb_wait(uint64_t* b, uint32_t ph) {
+  asm volatile(
+      "{\n.reg .pred P1;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE_%=;\nbra WAIT_%=;\nDONE_%=:\n}\n" ::"r"(su32(b)),
+      "r"(ph)
+      : "memory");
+}
+NMG_D void tma2d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::"r"(
+          su32(dst)),
+      "l"(m), "r"(su32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+// K-major SWIZZLE_64B operand: 64-byte rows, 8-row groups 512 B apart
+NMG_D uint64_t desc_sw64(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;
+  return d;
+}
+NMG_D void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+NMG_D void mma_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(b))
+               : "memory");
+}
+NMG_D void tld16(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+// the wait carries the loaded registers so no use can be scheduled above it
+NMG_D void tld_wait16(uint32_t* r) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+               :
+               : "memory");
+}
+NMG_D float rna_tf32(float v) {
+  uint32_t h;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(h) : "f"(v));
+  return __uint_as_float(h);
+}
+
+// stencil S[b][i2][i1] = sum_{a2, a1} Q[i2][a2] Q[i1][a1] X[b][a2][a1], |a - i| <= HB
+template <int HB>
+NMG_D float qstencil_at(const float* __restrict__ Xb, const float* __restrict__ Q, int n, int i2, int i1,
+                        const float (&q1)[2 * HB + 1]) {
+  if constexpr (HB == 0) {
+    return __ldg(Q + (int64_t)i2 * n + i2) * (q1[0] * __ldg(Xb + (int64_t)i2 * n + i1));
+  } else {
+    float acc = 0.f;
+#pragma unroll
+    for (int d2 = -HB; d2 <= HB; ++d2) {
+      const int a2 = i2 + d2;
+      if (a2 < 0 || a2 >= n) continue;
+      float t = 0.f;
+#pragma unroll
+      for (int d1 = -HB; d1 <= HB; ++d1) {
+        const int a1 = i1 + d1;
+        if (a1 >= 0 && a1 < n) t = fmaf(q1[d1 + HB], __ldg(Xb + (int64_t)a2 * n + a1), t);
+      }
+      acc = fmaf(__ldg(Q + (int64_t)i2 * n + a2), t, acc);
+    }
+    return acc;
+  }
+}
+
+template <int TBN, int HB>
+__global__ void __launch_bounds__(KNT, 1)
+    kron_tc_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tWh,
+                   const __grid_constant__ CUtensorMap tWl, KronArgs a) {
+  using Cfg = KronCfg<TBN>;
+  constexpr int ST = Cfg::STAGES, STAGE = Cfg::STAGE, B_BYTES = Cfg::B_BYTES;
+  extern __shared__ uint8_t smraw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + ST * STAGE);
+  uint64_t* split = full + ST;
+  uint64_t* empty = split + ST;
+  uint64_t* tfull = empty + ST;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n = a.n;
+  const int KT = n / KBK;
+  const int NT = (n + TBN - 1) / TBN;
+  const int MT = (a.M + KBM - 1) / KBM;
+  const int T = MT * NT;
+
+  if (tid == 0) {
+    for (int s = 0; s < ST; ++s) { mb_init(&full[s], 1); mb_init(&split[s], 4); mb_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { mb_init(&tfull[b], 1); mb_init(&tempty[b], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tA) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tWh) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tWl) : "memory");
+  }
+  if (warp == 9) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
+                 "r"(Cfg::TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 8) {
+    if (lane == 0) {   // ---------------- TMA producer
+      int it = 0;
+      for (int t = blockIdx.x; t < T; t += gridDim.x) {
+        const int m0 = (t / NT) * KBM, n0 = (t % NT) * TBN;
+        for (int kt = 0; kt < KT; ++kt, ++it) {
+          const int s = it % ST;
+          mb_wait(&empty[s], ((uint32_t)(it / ST) & 1u) ^ 1u);
+          uint8_t* st = sm + s * STAGE;
+          mb_expect(&full[s], A_BYTES + 2 * B_BYTES);
+          tma2d(st, &tA, &full[s], kt * KBK, m0);
+          tma2d(st + 2 * A_BYTES, &tWh, &full[s], kt * KBK, n0);
+          tma2d(st + 2 * A_BYTES + B_BYTES, &tWl, &full[s], kt * KBK, n0);
+        }
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {   // ---------------- splitters
+    const int ct = tid - 128;
+    int it = 0;
+    for (int t = blockIdx.x; t < T; t += gridDim.x) {
+      for (int kt = 0; kt < KT; ++kt, ++it) {
+        const int s = it % ST;
+        mb_wait(&full[s], (uint32_t)(it / ST) & 1u);
+        float4* hi = reinterpret_cast<float4*>(sm + s * STAGE);
+        float4* lo = reinterpret_cast<float4*>(sm + s * STAGE + A_BYTES);
+#pragma unroll
+        for (int e = ct; e < A_BYTES / 16; e += 128) {
+          const float4 v = hi[e];
+          float4 h, l;
+          h.x = rna_tf32(v.x); l.x = rna_tf32(v.x - h.x);
+          h.y = rna_tf32(v.y); l.y = rna_tf32(v.y - h.y);
+          h.z = rna_tf32(v.z); l.z = rna_tf32(v.z - h.z);
+          h.w = rna_tf32(v.w); l.w = rna_tf32(v.w - h.w);
+          hi[e] = h;
+          lo[e] = l;
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mb_arrive(&split[s]);
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {   // ---------------- MMA issuer
+      int it = 0, i = 0;
+      for (int t = blockIdx.x; t < T; t += gridDim.x, ++i) {
+        const int ab = i & 1;
+        mb_wait(&tempty[ab], ((uint32_t)(i >> 1) & 1u) ^ 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t d = tmem + (uint32_t)(ab * TBN);
+        for (int kt = 0; kt < KT; ++kt, ++it) {
+          const int s = it % ST;
+          const uint32_t ph = (uint32_t)(it / ST) & 1u;
+          mb_wait(&full[s], ph);
+          mb_wait(&split[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+          const uint32_t st = su32(sm + s * STAGE);
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) {
+            const uint32_t ko = ks * 32;   // 8 tf32 = 32 bytes along the 64-byte swizzled row
+            const uint64_t dah = desc_sw64(st + ko), dal = desc_sw64(st + A_BYTES + ko);
+            const uint64_t dwh = desc_sw64(st + 2 * A_BYTES + ko), dwl = desc_sw64(st + 2 * A_BYTES + B_BYTES + ko);
+            mma_tf32(d, dah, dwh, Cfg::IDESC, (kt | ks) ? 1u : 0u);
+            mma_tf32(d, dah, dwl, Cfg::IDESC, 1u);
+            mma_tf32(d, dal, dwh, Cfg::IDESC, 1u);
+          }
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&tfull[ab]);
+      }
+    }
+  } else {   // ---------------- epilogue, warps 0-3 (TMEM lanes 32 w .. 32 w + 31)
+    const int64_t nn2 = (int64_t)n * n;
+    int i = 0;
+    for (int t = blockIdx.x; t < T; t += gridDim.x, ++i) {
+      const int ab = i & 1;
+      const int m = (t / NT) * KBM + warp * 32 + lane, n0 = (t % NT) * TBN;
+      const bool mok = m < a.M;
+      const int b = m / n, r = m - (m / n) * n;   // image, row of the image (i1 of the output)
+      const int64_t base = b * nn2 + r;
+      float q1[2 * HB + 1];
+      if (a.mode == KRON_RESID && mok) {
+#pragma unroll
+        for (int d1 = -HB; d1 <= HB; ++d1) {
+          const int a1 = r + d1;
+          q1[d1 + HB] = (a1 >= 0 && a1 < n) ? __ldg(a.Q + (int64_t)r * n + a1) : 0.f;
+        }
+      }
+      mb_wait(&tfull[ab], (uint32_t)(i >> 1) & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const uint32_t tb = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(ab * TBN);
+#pragma unroll 1
+      for (int c = 0; c < TBN; c += 16) {
+        uint32_t v[16];
+        tld16(tb + c, v);
+        tld_wait16(v);
+        if (!mok) continue;
+        const int nb = n0 + c;
+        if (a.mode == KRON_T) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (nb + j < n) a.D[base + (int64_t)(nb + j) * n] = __uint_as_float(v[j]);
+        } else {
+          const float* Xb = a.X + b * nn2;
+          float o[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int i2 = min(nb + j, n - 1);
+            const float sq = qstencil_at<HB>(Xb, a.Q, n, i2, r, q1);
+            const float vv = fmaf(a.alpha, sq, __uint_as_float(v[j]));
+            const float cc = a.Cin ? a.Cin[base + (int64_t)i2 * n] : 0.f;
+            o[j] = a.negate ? cc - vv : cc + vv;
+          }
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (nb + j < n) a.D[base + (int64_t)(nb + j) * n] = o[j];
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mb_arrive(&tempty[ab]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 9) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(Cfg::TCOLS));
+  }
+}
+
+template <int TBN, int HB>
+void launch_kron(const CUtensorMap* A, const CUtensorMap* Wh, const CUtensorMap* Wl, const KronArgs& a, int sms,
+                 cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kron_tc_kernel<TBN, HB>, cudaFuncAttributeMaxDynamicSharedMemorySize, KronCfg<TBN>::SMEM);
+    attr = true;
+  }
+  const int tiles = ceil_div(a.M, KBM) * ceil_div(a.n, TBN);
+  kron_tc_kernel<TBN, HB><<<std::min(tiles, sms), KNT, KronCfg<TBN>::SMEM, s>>>(*A, *Wh, *Wl, a);
+}
+
+template <int TBN>
+void launch_kron_hb(const CUtensorMap* A, const CUtensorMap* Wh, const CUtensorMap* Wl, const KronArgs& a, int sms,
+                    cudaStream_t s) {
+  switch (a.mode == KRON_T ? 0 : a.hb) {
+    case 0: launch_kron<TBN, 0>(A, Wh, Wl, a, sms, s); break;
+    case 1: launch_kron<TBN, 1>(A, Wh, Wl, a, sms, s); break;
+    default: launch_kron<TBN, 2>(A, Wh, Wl, a, sms, s); break;
+  }
+}
+
+}  // namespace
+
+int kron_tile_n(int n) { return n >= 256 ? 256 : n; }
+
+bool kron_supported(int n, int hb) {
+  return n % 16 == 0 && n >= 32 && (n <= 256 || n % 256 == 0) && hb <= 2 && (n & (n - 1)) == 0;
+}
+
+void kron_tc(const CUtensorMap* A, const CUtensorMap* Wh, const CUtensorMap* Wl, const KronArgs& a, int sms,
+             cudaStream_t s) {
+  switch (kron_tile_n(a.n)) {
+    case 32: launch_kron_hb<32>(A, Wh, Wl, a, sms, s); break;
+    case 64: launch_kron_hb<64>(A, Wh, Wl, a, sms, s); break;
+    case 128: launch_kron_hb<128>(A, Wh, Wl, a, sms, s); break;
+    default: launch_kron_hb<256>(A, Wh, Wl, a, sms, s); break;
+  }
+}
+
+}  // namespace nmg

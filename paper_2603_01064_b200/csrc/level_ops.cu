@@ -44,82 +44,118 @@ __global__ void prolong_add1d_kernel(int nrhs, int n_c, const float* __restrict_
 }
 
 // ---- coarse solve: x = L^{-T} L^{-1} y with the host Cholesky factor (fp64) ----------
-// One warp per RHS; lane owns entries j = q*32 + lane of the fp64 iterate.  Blocked
-// substitution over 32-wide diagonal blocks: inside a block the 32 sequential steps keep
-// the block's column (forward) / row (backward) of L in registers, so the dependent chain
-// per step is shfl -> mul -> fma; the off-diagonal update of the other blocks is a plain
-// accumulation of independent coalesced loads (Lcol[i*nc + j] = L[j][i]).
-NMG_D double coarse_ld(const double* p) { return __ldg(p); }
+// One warp per RHS (8 per CTA); lane owns entries j = q*32 + lane of the fp64 iterate.
+// Blocked substitution over 32-wide diagonal blocks.  The CTA stages the 32-row panel
+// of the factor each block needs (forward: rows i0.. of Lcol = L^T, columns i0..nc;
+// backward: rows i0.. of Lrow, columns 0..i0+32) in shared memory with cp.async, double
+// buffered, so the next panel streams in while the current one is used.  Inside a block
+// the 32 sequential steps keep the block's column (forward) / row (backward) of L in
+// registers (dependent chain per step: shfl -> mul -> fma); the update of the other blocks
+// is an accumulation over independent shared-memory reads.
+NMG_D void cp_async8(double* dst, const double* src) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
+}
 
 template <int NQ>
-__global__ void __launch_bounds__(256) coarse_kernel(int nc, int nrhs, const double* __restrict__ Lrow,
+NMG_D void coarse_issue_panel(int p, int nc, const double* Lrow, const double* Lcol, double* P) {
+  constexpr int PS = NQ * 32;
+  const bool fwd = p < NQ;
+  const int q0 = fwd ? p : 2 * NQ - 1 - p;
+  const int i0 = q0 * 32;
+  const int rows = min(32, nc - i0);
+  const int len = fwd ? nc - i0 : min(i0 + 32, nc);
+  const double* src = fwd ? Lcol + (int64_t)i0 * nc + i0 : Lrow + (int64_t)i0 * nc;
+  for (int e = threadIdx.x; e < rows * len; e += blockDim.x) {
+    const int il = e / len, jj = e - il * len;
+    cp_async8(P + il * PS + jj, src + (int64_t)il * nc + jj);
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
+constexpr int kCoarseWarps = 4;   // RHS per CTA: few, so that many SMs share the issue load
+
+template <int NQ>
+__global__ void __launch_bounds__(kCoarseWarps * 32) coarse_kernel(int nc, int nrhs, const double* __restrict__ Lrow,
                                                      const double* __restrict__ Lcol,
                                                      const float* __restrict__ y, int64_t ldy,
                                                      float* __restrict__ x, int64_t ldx,
                                                      float* __restrict__ xh, float* __restrict__ xl) {
-  const int lane = threadIdx.x & 31;
-  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (b >= nrhs) return;
+  constexpr int PS = NQ * 32;
+  extern __shared__ double Pbuf[];   // 2 x [32][PS] panels, dinv[NQ*32], zs[warps][32]
+  double* dinv = Pbuf + 2 * 32 * PS;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* zs = dinv + PS + warp * 32;
+  const int b = blockIdx.x * kCoarseWarps + warp;
+  const bool live = b < nrhs;
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) dinv[i] = 1.0 / Lrow[(int64_t)i * nc + i];
   double z[NQ];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
     const int j = q * 32 + lane;
-    z[q] = (j < nc) ? (double)y[(int64_t)b * ldy + j] : 0.0;
+    z[q] = (live && j < nc) ? (double)y[(int64_t)b * ldy + j] : 0.0;
   }
-  // forward: L z = y
+  coarse_issue_panel<NQ>(0, nc, Lrow, Lcol, Pbuf);
+  // forward: L z = y.  Within a block the undivided values z'_i are broadcast and the
+  // column is pre-scaled by 1 / L_ii (z_j -= (L_ji / L_ii) z'_i), so a step is shfl -> fma.
 #pragma unroll
   for (int q0 = 0; q0 < NQ; ++q0) {
-    const int i0 = q0 * 32, jd = i0 + lane;
-    const bool okj = jd < nc;
+    const int p = q0;
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    coarse_issue_panel<NQ>(p + 1, nc, Lrow, Lcol, Pbuf + ((p + 1) & 1) * 32 * PS);
+    const double* P = Pbuf + (p & 1) * 32 * PS;   // P[il][jj] = L[i0 + jj][i0 + il]
+    const int i0 = q0 * 32;
+    const bool okj = i0 + lane < nc;
     double Lb[32];
 #pragma unroll
-    for (int il = 0; il < 32; ++il)
-      Lb[il] = (okj && i0 + il < nc && il < lane) ? coarse_ld(Lcol + (int64_t)(i0 + il) * nc + jd) : 0.0;
-    const double dv = okj ? 1.0 / coarse_ld(Lcol + (int64_t)jd * nc + jd) : 1.0;
+    for (int il = 0; il < 32; ++il) Lb[il] = (okj && il < lane) ? P[il * PS + lane] * dinv[i0 + il] : 0.0;
 #pragma unroll
-    for (int il = 0; il < 32; ++il) {
-      const double zi = __shfl_sync(0xffffffffu, z[q0], il) * __shfl_sync(0xffffffffu, dv, il);
-      z[q0] = (lane == il) ? zi : fma(-Lb[il], zi, z[q0]);
-    }
+    for (int il = 0; il < 32; ++il) z[q0] = fma(-Lb[il], __shfl_sync(0xffffffffu, z[q0], il), z[q0]);
+    if (okj) z[q0] *= dinv[i0 + lane];
+    zs[lane] = z[q0];
+    __syncwarp();
 #pragma unroll
     for (int q = q0 + 1; q < NQ; ++q) {
-      const int j = q * 32 + lane;
+      const int jj = (q - q0) * 32 + lane;
+      const bool ok = q * 32 + lane < nc;
       double acc = z[q];
-#pragma unroll 8
-      for (int il = 0; il < 32; ++il) {
-        const double zi = __shfl_sync(0xffffffffu, z[q0], il);
-        if (j < nc && i0 + il < nc) acc = fma(-coarse_ld(Lcol + (int64_t)(i0 + il) * nc + j), zi, acc);
-      }
+#pragma unroll
+      for (int il = 0; il < 32; ++il)
+        if (ok) acc = fma(-P[il * PS + jj], zs[il], acc);
       z[q] = acc;
     }
   }
-  // backward: L^T x = z
+  // backward: L^T x = z, same scheme on the rows of L
 #pragma unroll
   for (int q0 = NQ - 1; q0 >= 0; --q0) {
-    const int i0 = q0 * 32, jd = i0 + lane;
-    const bool okj = jd < nc;
+    const int p = 2 * NQ - 1 - q0;
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    if (p + 1 < 2 * NQ) coarse_issue_panel<NQ>(p + 1, nc, Lrow, Lcol, Pbuf + ((p + 1) & 1) * 32 * PS);
+    const double* P = Pbuf + (p & 1) * 32 * PS;   // P[il][j] = L[i0 + il][j]
+    const int i0 = q0 * 32;
+    const bool okj = i0 + lane < nc;
     double Lb[32];
 #pragma unroll
     for (int il = 0; il < 32; ++il)
-      Lb[il] = (okj && i0 + il < nc && il > lane) ? coarse_ld(Lrow + (int64_t)(i0 + il) * nc + jd) : 0.0;
-    const double dv = okj ? 1.0 / coarse_ld(Lrow + (int64_t)jd * nc + jd) : 1.0;
+      Lb[il] = (okj && il > lane && i0 + il < nc) ? P[il * PS + i0 + lane] * dinv[i0 + il] : 0.0;
 #pragma unroll
-    for (int il = 31; il >= 0; --il) {
-      const double xi = __shfl_sync(0xffffffffu, z[q0], il) * __shfl_sync(0xffffffffu, dv, il);
-      z[q0] = (lane == il) ? xi : fma(-Lb[il], xi, z[q0]);
-    }
+    for (int il = 31; il >= 0; --il) z[q0] = fma(-Lb[il], __shfl_sync(0xffffffffu, z[q0], il), z[q0]);
+    if (okj) z[q0] *= dinv[i0 + lane];
+    zs[lane] = z[q0];
+    __syncwarp();
+    const int rows = min(32, nc - i0);
 #pragma unroll
     for (int q = 0; q < q0; ++q) {
-      const int j = q * 32 + lane;
       double acc = z[q];
-#pragma unroll 8
-      for (int il = 0; il < 32; ++il) {
-        const double xi = __shfl_sync(0xffffffffu, z[q0], il);
-        if (i0 + il < nc) acc = fma(-coarse_ld(Lrow + (int64_t)(i0 + il) * nc + j), xi, acc);
-      }
+#pragma unroll
+      for (int il = 0; il < 32; ++il)
+        if (il < rows) acc = fma(-P[il * PS + q * 32 + lane], zs[il], acc);
       z[q] = acc;
     }
   }
+  if (!live) return;
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
     const int j = q * 32 + lane;
@@ -213,10 +249,18 @@ void prolong_add1d(int nrhs, int n_c, const float* c, int64_t ldc, float* f, int
 
 void coarse_chol_solve(int nc, int nrhs, const double* Lrow, const double* Lcol, const float* y, int64_t ldy,
                        float* x, int64_t ldx, cudaStream_t s, float* xh, float* xl) {
-  const int grid = ceil_div(nrhs, 8);
+  const int grid = ceil_div(nrhs, kCoarseWarps);
   const int nq = ceil_div(nc, 32);
-#define NMG_COARSE(Q) \
-  case Q: coarse_kernel<Q><<<grid, 256, 0, s>>>(nc, nrhs, Lrow, Lcol, y, ldy, x, ldx, xh, xl); break;
+  static bool attr[9] = {};
+#define NMG_COARSE(Q)                                                                                   \
+  case Q: {                                                                                             \
+    const int smem = (2 * 32 * Q * 32 + Q * 32 + kCoarseWarps * 32) * (int)sizeof(double);           \
+    if (!attr[Q]) {                                                                                     \
+      cudaFuncSetAttribute(coarse_kernel<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);       \
+      attr[Q] = true;                                                                                   \
+    }                                                                                                   \
+    coarse_kernel<Q><<<grid, kCoarseWarps * 32, smem, s>>>(nc, nrhs, Lrow, Lcol, y, ldy, x, ldx, xh, xl);           \
+  } break;
   switch (nq) {
     NMG_COARSE(1) NMG_COARSE(2) NMG_COARSE(3) NMG_COARSE(4)
     NMG_COARSE(5) NMG_COARSE(6) NMG_COARSE(7) NMG_COARSE(8)

@@ -304,6 +304,8 @@ struct nmg_hierarchy {
   std::vector<int> qhb;                                  // Q_l half-bandwidth
   std::vector<CUtensorMap> mBh, mBl, mCh, mCl, mTh, mTl;
   std::vector<CUtensorMap> mBh64, mBl64, mCh64, mCl64;
+  std::vector<CUtensorMap> mKBh, mKBl, mKCh, mKCl;      // W maps for kron_tc (box rows kron_tile_n)
+  bool use_kron = false;
   std::vector<std::unique_ptr<DevBuf<float>>> tth, ttl;  // step-1 output (transposed blocks), hi/lo
   DevBuf<float2> Z;                                      // filter spectrum workspace
   DevBuf<double> snorm, spart;                           // smoother norms
@@ -569,6 +571,20 @@ nmg_status apply2d(nmg_hierarchy* h, int l, int nrhs, const float* X, const floa
                    bool negate = true) {
   const int n = h->n[l];
   const int M = nrhs * n;
+  if (h->use_kron && kron_supported(n, h->qhb[l])) {
+    // fused path (kron_tc.cu): pass 1 T = blockT(arr C^T); pass 2 D = Cin -/+ (blockT(T B^T) + alpha QXQ^T)
+    CUtensorMap mx;
+    NMG_TRY(make_map(&mx, X, (int64_t)M, n, tc_gemm_block_m()));
+    KronArgs k{};
+    k.M = M; k.n = n; k.mode = KRON_T; k.D = h->tth[l]->p;
+    { Prof p(h, NMG_K_GEMM32, s); kron_tc(&mx, &h->mKCh[l], &h->mKCl[l], k, h->num_sms, s); }
+    NMG_TRY(check_launch(h));
+    KronArgs k2{};
+    k2.M = M; k2.n = n; k2.mode = KRON_RESID; k2.D = D; k2.X = X; k2.Cin = Cin; k2.Q = h->Q32[l]->p;
+    k2.hb = h->qhb[l]; k2.alpha = (float)h->d.alpha; k2.negate = negate;
+    { Prof p(h, NMG_K_GEMM32, s); kron_tc(&h->mTh[l], &h->mKBh[l], &h->mKBl[l], k2, h->num_sms, s); }
+    return check_launch(h);
+  }
   const bool tc = h->use_tc && n % 16 == 0;
   if (tc) {
     { Prof p(h, NMG_K_MISC, s); split_tf32((int64_t)M * n, X, h->sxh[l]->p, h->sxl[l]->p, s); }
@@ -1158,6 +1174,11 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
     h->mBh.resize(h->L); h->mBl.resize(h->L); h->mCh.resize(h->L); h->mCl.resize(h->L);
     h->mTh.resize(h->L); h->mTl.resize(h->L); h->mXh.resize(h->L); h->mXl.resize(h->L);
     h->mBh64.resize(h->L); h->mBl64.resize(h->L); h->mCh64.resize(h->L); h->mCl64.resize(h->L);
+    h->mKBh.resize(h->L); h->mKBl.resize(h->L); h->mKCh.resize(h->L); h->mKCl.resize(h->L);
+    {
+      const char* env = std::getenv("NMG_KRON");
+      h->use_kron = h->use_tc && !(env && std::string(env) == "0");
+    }
     for (int l = 0; l < h->L; ++l) {
       const int nl = h->n[l];
       for (auto* v : {&h->sxh, &h->sxl, &h->tth, &h->ttl}) {
@@ -1178,6 +1199,13 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
       NMG_TRY(make_map(&h->mBl64[l], h->B32l[l]->p, nl, nl, 64));
       NMG_TRY(make_map(&h->mCh64[l], h->C32h[l]->p, nl, nl, 64));
       NMG_TRY(make_map(&h->mCl64[l], h->C32l[l]->p, nl, nl, 64));
+      if (kron_supported(nl, h->qhb[l])) {
+        const int kb = kron_tile_n(nl);
+        NMG_TRY(make_map(&h->mKBh[l], h->B32h[l]->p, nl, nl, kb));
+        NMG_TRY(make_map(&h->mKBl[l], h->B32l[l]->p, nl, nl, kb));
+        NMG_TRY(make_map(&h->mKCh[l], h->C32h[l]->p, nl, nl, kb));
+        NMG_TRY(make_map(&h->mKCl[l], h->C32l[l]->p, nl, nl, kb));
+      }
     }
     NMG_TRY(h->Z.alloc(B * (size_t)h->N[0]));
     NMG_TRY(h->snorm.alloc(B));
