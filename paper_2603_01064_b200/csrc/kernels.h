@@ -109,6 +109,11 @@ inline int tc_pick_bn(int M, int N, int num_sms) {
 void split_tf32(int64_t count, const float* x, float* hi, float* lo, cudaStream_t s);
 
 // ---- 1D smoother: norm -> CNN (3 layers, C=16, k=5) -> F' -> update ----------
+// 1D smoother weights by value (smooth1d_f16 reads them as constant-bank operands):
+// w0 [16][5], b0 [16] (pre-multiplied by in_scale), b1 [16], w2 [16][5], b2 (state_dict order)
+struct Smooth1dW {
+  float w0[80], b0[16], b1[16], w2[80], b2;
+};
 struct Smooth1dArgs {
   int n, nrhs;
   const float* b; int64_t ldb;     // input rows
@@ -127,6 +132,7 @@ struct Smooth1dArgs {
   uint16_t* x16h = nullptr;        // optional (filter path): per-row scaled f16 hi/lo split of the
   uint16_t* x16l = nullptr;        // updated x and 1 / scale, as split_f16_rows
   float* xinv = nullptr;
+  Smooth1dW w{};                   // smooth1d_f16 only
 };
 void smooth1d(const Smooth1dArgs& a, cudaStream_t s);
 // same step with the 16 -> 16 layer on tcgen05 (FP16x3, n % 128 == 0), smooth1d_f16.cu

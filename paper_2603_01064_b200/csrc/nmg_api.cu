@@ -294,6 +294,7 @@ struct nmg_hierarchy {
   bool smooth_f16 = false;                               // 1D smoother layer 2 on tcgen05 FP16x3 (default)
   std::vector<std::unique_ptr<DevBuf<uint16_t>>> W1b;    // per level: stacked f16 layer-2 weights
   std::vector<float> s1d_sc;                             // per level: S1, T1
+  std::vector<Smooth1dW> s1d_w;                          // per level: host copy of the 1D CNN weights
   // fp64 outer residual via int8 digit products (Ozaki-style), 1D
   bool ozaki = false;
   DevBuf<int8_t> wdig, xdig;
@@ -417,6 +418,8 @@ void launch_smooth1d(nmg_hierarchy* h, int l, Smooth1dArgs& a, cudaStream_t s) {
     const float S1 = h->s1d_sc[2 * l] * (a.normalize ? 1.f : 1.f / 16.f);
     a.in_scale = S1;
     a.d_scale = 1.f / (S1 * h->s1d_sc[2 * l + 1]);
+    a.w = h->s1d_w[l];
+    for (int c = 0; c < 16; ++c) a.w.b0[c] *= S1;
     smooth1d_f16(a, s);
   } else if (h->smooth_tc) {
     smooth1d_tc(a, s);
@@ -1480,6 +1483,16 @@ nmg_status nmg_load_smoother_weights(nmg_hierarchy* h, int32_t level, const nmg_
             wb[base + (size_t)o * 8] = hi;
             wb[base + (size_t)(16 + o) * 8] = lo;
           }
+      if (h->s1d_w.size() < (size_t)h->L) h->s1d_w.resize(h->L);
+      {
+        Smooth1dW& hw = h->s1d_w[level - 1];
+        const float* P = params;
+        for (int i = 0; i < C * k; ++i) hw.w0[i] = P[i];
+        for (int c = 0; c < C; ++c) hw.b0[c] = P[C * k + c];
+        for (int c = 0; c < C; ++c) hw.b1[c] = P[L1 + (size_t)C * C * k + c];
+        for (int i = 0; i < C * k; ++i) hw.w2[i] = P[L1 + (size_t)C * C * k + C + i];
+        hw.b2 = P[L1 + (size_t)C * C * k + C + C * k];
+      }
       while (h->W1b.size() < (size_t)(h->L)) h->W1b.emplace_back(new DevBuf<uint16_t>());
       NMG_TRY(h->W1b[level - 1]->upload(wb.data(), wb.size()));
     }

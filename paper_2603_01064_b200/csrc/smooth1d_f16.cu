@@ -10,16 +10,23 @@
 // layout [2 chunks][136 rows][8 x f16] (16-byte rows, 8-row core matrices contiguous), so
 // tap t is a +16 t byte shift of the A descriptor start: no im2col buffer.  FP16x3 with
 // power-of-two scales (see conv_strip.cu): per tap one N = 32 MMA multiplies the hi part of
-// a1 by the stacked [W_hi; W_lo] weights and one N = 16 MMA multiplies the lo part by W_hi,
-// so the A tile is read from shared memory twice per tap instead of three times
-// (D[:, 0:16] = Ah Wh + Al Wh, D[:, 16:32] = Ah Wl; the epilogue adds the halves).
+// a1 by the stacked [W_hi; W_lo] weights and one N = 16 MMA multiplies the lo part by W_hi
+// (D[:, 0:16] = Ah Wh + Al Wh, D[:, 16:32] = Ah Wl; the epilogue adds the halves).  Each MMA
+// streams its 128 x 16 A tile from shared memory, which makes shared-memory bandwidth the
+// tile pipeline's limit: two A reads per tap, not three.
+// The CNN weights travel by value in the kernel arguments, so every FFMA of layers 1 and 3
+// takes its weight as a constant-bank (uniform-register) operand: no weight registers, no
+// shared-memory loads.
 // Layer 3 (16 -> 1, k = 5) is split per tap in the epilogue: q_t(p) = sum_c w2[c][t] a2[c](p),
 // written to a 512-position ring, and h(p) = b2 + sum_t q_t(p + t - 2) is assembled after the
 // next barrier (positions outside [0, n) read zeros) -- no layer-2 halo is recomputed.
 //
-// Warps: 0-3 epilogue (TMEM lanes = positions), 4-7 layer-1 producer, 8 MMA issuer; the
-// norm, filter and update phases use all 288 threads.  Two CTAs per SM overlap the serial
-// phases of one right-hand side with the tile pipeline of another.
+// Warps: 0-3 epilogue (TMEM lanes = positions), 4-7 layer-1 producer, 8 MMA issuer (the whole
+// warp converged, one elected lane issuing, so the stage arithmetic stays in uniform
+// registers); the norm, filter and update phases use all 288 threads.  Three CTAs per SM
+// overlap the serial phases of one right-hand side with the tile pipelines of the others.
+// The level filter is a swizzled Stockham FFT (level_filter_row) and x* is prefetched with
+// cp.async while it runs.
 #include <cuda_fp16.h>
 
 #include <algorithm>
@@ -39,8 +46,9 @@ constexpr int ALBO = AR * 16;           // K-chunk stride of the a1 buffer (byte
 constexpr int ABYTES = 2 * ALBO;        // one a1 tile, hi or lo (2 chunks)
 constexpr int BLBO = 32 * 16;           // K-chunk stride of a stacked weight tap [2][32][8]
 constexpr int BTAP = 2 * BLBO;          // bytes per tap
-constexpr int UPAD = 4;
 constexpr int QR = 512;                 // q ring (positions)
+constexpr int UPAD = 4;
+constexpr int NSD = 4;                  // accumulator stages (TMEM, 32 columns each)
 constexpr uint32_t IDESC32 = (1u << 4) | ((uint32_t)(32 >> 3) << 17) | ((uint32_t)(TP >> 4) << 24);
 constexpr uint32_t IDESC16 = (1u << 4) | ((uint32_t)(16 >> 3) << 17) | ((uint32_t)(TP >> 4) << 24);
 
@@ -54,10 +62,20 @@ NMG_D void mb_arrive(uint64_t* b) {
 NMG_D void mb_wait(uint64_t* b, uint32_t ph) {
   asm volatile(
       "{\n.reg .pred P1;\nWAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
       "@P1 bra DONE_%=;\nbra WAIT_%=;\nDONE_%=:\n}\n" ::"r"(su32(b)),
-      "r"(ph)
+      "r"(ph), "r"(0x989680)
       : "memory");
+}
+NMG_D bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n.reg .b32 %%rx;\n.reg .pred %%px;\n"
+      "elect.sync %%rx|%%px, %1;\n"
+      "@%%px mov.s32 %0, 1;\n}\n"
+      : "+r"(pred)
+      : "r"(0xffffffffu));
+  return pred != 0;
 }
 NMG_D uint64_t desc_ns(uint32_t saddr, uint32_t lbo) {
   uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
@@ -76,17 +94,14 @@ NMG_D void mma_commit(uint64_t* b) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(b))
                : "memory");
 }
-NMG_D void tld32(uint32_t taddr, uint32_t* r) {
+NMG_D void tld16(uint32_t taddr, uint32_t* r) {
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
 }
-// wait::ld with the 32 destination registers threaded through in two groups of 16
+// wait::ld with the destination registers threaded through
 NMG_D void tld_wait16(uint32_t* r) {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n"
                : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
@@ -114,28 +129,247 @@ NMG_D void tf32_store(float xv, float* xh, float* xl, int64_t at) {
   xl[at] = __uint_as_float(ll);
 }
 
-__global__ void __launch_bounds__(NT, 3) smooth1d_f16_kernel(Smooth1dArgs a) {
+// ---- level filter F'_l (reading R5) on the row held in shared memory -----------
+// Same mathematics as fft.cuh's real_level_filter (one n/2-point complex FFT of the packed
+// row z[k] = h[2k] + i h[2k+1], the mask on the unpacked half spectrum, one inverse), but
+// as Stockham autosort passes (natural order in and out, ping-pong between the row buffer
+// and a scratch buffer) on a swizzled layout: complex element i lives at sw(i) =
+// i ^ ((i >> 3) & 15), a permutation inside aligned 128-element blocks that makes every
+// pass's loads and stores, the unpack's (k, m - k) pairs and the row-order accesses of the
+// epilogue and update free of shared-memory bank conflicts.
+// a1 stages, reused after the tile loop as the FFT scratch (n/2 complex)
+NMG_HD int abuf_bytes(int nsa, int n) { return max(2 * nsa * ABYTES, 4 * n); }
+NMG_D int sw(int i) { return i ^ ((i >> 3) & 15); }
+NMG_D int hsw(int p) { return 2 * sw(p >> 1) + (p & 1); }   // real position p of the row
+
+NMG_D float2 twid(const float2* __restrict__ tw, int tw_n, int k) {   // exp(-2 pi i k / tw_n), k < tw_n
+  const int h = tw_n >> 1;
+  const float2 w = __ldg(tw + (k & (h - 1)));   // branch-free, so all loads of a pass issue together
+  const float sg = k < h ? 1.f : -1.f;
+  return make_float2(sg * w.x, sg * w.y);
+}
+template <bool INV>
+NMG_D float2 rot_mi(float2 a) { return INV ? make_float2(-a.y, a.x) : make_float2(a.y, -a.x); }   // a * (-/+ i)
+// R-point DFT in registers, natural order in and out (radix-2 DIF, outputs unscrambled)
+template <int R, bool INV>
+NMG_D void dft_r(float2 (&v)[R]) {
+  if constexpr (R == 2) {
+    const float2 a = v[0], b = v[1];
+    v[0] = make_float2(a.x + b.x, a.y + b.y);
+    v[1] = make_float2(a.x - b.x, a.y - b.y);
+  } else if constexpr (R == 4) {
+    float2 t[4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const float2 a = v[i], b = v[i + 2];
+      t[i] = make_float2(a.x + b.x, a.y + b.y);
+      t[i + 2] = make_float2(a.x - b.x, a.y - b.y);
+    }
+    t[3] = rot_mi<INV>(t[3]);
+    v[0] = make_float2(t[0].x + t[1].x, t[0].y + t[1].y);
+    v[2] = make_float2(t[0].x - t[1].x, t[0].y - t[1].y);
+    v[1] = make_float2(t[2].x + t[3].x, t[2].y + t[3].y);
+    v[3] = make_float2(t[2].x - t[3].x, t[2].y - t[3].y);
+  } else {
+    constexpr float h = 0.70710678118654752440f;
+    float2 t[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 a = v[i], b = v[i + 4];
+      t[i] = make_float2(a.x + b.x, a.y + b.y);
+      t[i + 4] = make_float2(a.x - b.x, a.y - b.y);
+    }
+    // t[4 + i] *= W8^i
+    t[5] = INV ? make_float2(h * (t[5].x - t[5].y), h * (t[5].x + t[5].y))
+               : make_float2(h * (t[5].x + t[5].y), h * (t[5].y - t[5].x));
+    t[6] = rot_mi<INV>(t[6]);
+    t[7] = INV ? make_float2(-h * (t[7].x + t[7].y), h * (t[7].x - t[7].y))
+               : make_float2(h * (t[7].y - t[7].x), -h * (t[7].x + t[7].y));
+    float2 u[8];
+#pragma unroll
+    for (int g = 0; g < 8; g += 4) {
+      const float2 a0 = t[g], a1 = t[g + 1], b0 = t[g + 2], b1 = t[g + 3];
+      u[g] = make_float2(a0.x + b0.x, a0.y + b0.y);
+      u[g + 1] = make_float2(a1.x + b1.x, a1.y + b1.y);
+      u[g + 2] = make_float2(a0.x - b0.x, a0.y - b0.y);
+      u[g + 3] = rot_mi<INV>(make_float2(a1.x - b1.x, a1.y - b1.y));
+    }
+    // last stage; DIF output index bitrev3: V[0]=u0+u1, V[4]=u0-u1, V[2]=u2+u3, V[6]=u2-u3, ...
+    v[0] = make_float2(u[0].x + u[1].x, u[0].y + u[1].y);
+    v[4] = make_float2(u[0].x - u[1].x, u[0].y - u[1].y);
+    v[2] = make_float2(u[2].x + u[3].x, u[2].y + u[3].y);
+    v[6] = make_float2(u[2].x - u[3].x, u[2].y - u[3].y);
+    v[1] = make_float2(u[4].x + u[5].x, u[4].y + u[5].y);
+    v[5] = make_float2(u[4].x - u[5].x, u[4].y - u[5].y);
+    v[3] = make_float2(u[6].x + u[7].x, u[6].y + u[7].y);
+    v[7] = make_float2(u[6].x - u[7].x, u[6].y - u[7].y);
+  }
+}
+// one Stockham radix-R pass: sub-transforms of length Ns -> Ns R (ends with __syncthreads)
+template <int R, bool INV>
+NMG_D void stockham_pass(const float2* src, float2* dst, int m, int Ns, const float2* __restrict__ tw, int tw_n,
+                         int tid, int nthr) {
+  const int q = m / R, tstep = tw_n / (Ns * R);
+  for (int j = tid; j < q; j += nthr) {
+    const int jm = j & (Ns - 1);
+    float2 w[R], v[R];
+    if (Ns > 1) {   // twiddles first: independent of the data, their latency overlaps the loads
+#pragma unroll
+      for (int r = 1; r < R; ++r) w[r] = twid(tw, tw_n, jm * r * tstep);
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = src[sw(j + r * q)];
+    if (Ns > 1) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[r] = INV ? cmulc(v[r], w[r]) : cmul(v[r], w[r]);
+    }
+    dft_r<R, INV>(v);
+    const int d = (j - jm) * R + jm;
+#pragma unroll
+    for (int r = 0; r < R; ++r) dst[sw(d + r * Ns)] = v[r];
+  }
+  __syncthreads();
+}
+// m-point FFT (m a power of two >= 2), natural order; returns the buffer holding the result
+template <bool INV>
+NMG_D float2* stockham_fft(float2* a, float2* b, int m, const float2* __restrict__ tw, int tw_n, int tid, int nthr) {
+  for (int Ns = 1; Ns < m;) {
+    const int rem = m / Ns;
+    if (rem >= 8) { stockham_pass<8, INV>(a, b, m, Ns, tw, tw_n, tid, nthr); Ns *= 8; }
+    else if (rem == 4) { stockham_pass<4, INV>(a, b, m, Ns, tw, tw_n, tid, nthr); Ns *= 4; }
+    else { stockham_pass<2, INV>(a, b, m, Ns, tw, tw_n, tid, nthr); Ns *= 2; }
+    float2* c = a; a = b; b = c;
+  }
+  return a;
+}
+// F'(h) of the real row in z (swizzled, n reals = n/2 complex); scratch t of n/2 complex.
+// Result (times n/2, unnormalised) back in z.  Starts and ends with __syncthreads().
+NMG_D void level_filter_row(float2* z, float2* t, int n, const float2* __restrict__ tw, int tw_n, int tid,
+                            int nthr) {
+  const int m = n >> 1;
+  __syncthreads();
+  float2* Z = stockham_fft<false>(z, t, m, tw, tw_n, tid, nthr);
+  const int wstep = tw_n / n;   // W_n^k = tw[k * wstep]
+  // pair (k, m - k): unpack H, apply the mask, repack for the inverse (as real_level_filter)
+  constexpr int UNP = 4;
+  for (int k0 = tid; k0 <= (m >> 1); k0 += UNP * nthr) {
+    float2 Wv[UNP], W2v[UNP];
+#pragma unroll
+    for (int u = 0; u < UNP; ++u) {   // twiddle loads of all iterations first
+      const int k = min(k0 + u * nthr, m >> 1);
+      Wv[u] = __ldg(tw + k * wstep);
+      W2v[u] = __ldg(tw + ((m - k) & (m - 1)) * wstep);
+    }
+#pragma unroll
+    for (int u = 0; u < UNP; ++u) {
+    const int k = k0 + u * nthr;
+    if (k > (m >> 1)) break;
+    const int kk = (m - k) & (m - 1);
+    const float2 Zk = Z[sw(k)], Zc = Z[sw(kk)];
+    const float mk = sqrtf((float)(2 * k) / (float)n);
+    const float mc = sqrtf((float)(2 * (m - k)) / (float)n);
+    const float sp = 0.5f * (mk + mc), sm = 0.5f * (mk - mc);
+    float2 E = make_float2(0.5f * (Zk.x + Zc.x), 0.5f * (Zk.y - Zc.y));
+    float2 O = make_float2(0.5f * (Zk.y + Zc.y), -0.5f * (Zk.x - Zc.x));
+    float2 W = Wv[u];
+    float2 WO = cmul(W, O);
+    float2 Eg = make_float2(sp * E.x + sm * WO.x, sp * E.y + sm * WO.y);
+    float2 WcE = cmulc(E, W);
+    float2 Og = make_float2(sm * WcE.x + sp * O.x, sm * WcE.y + sp * O.y);
+    const float2 Zk2 = make_float2(Eg.x - Og.y, Eg.y + Og.x);
+    if (kk != k) {
+      float2 E2 = make_float2(0.5f * (Zc.x + Zk.x), 0.5f * (Zc.y - Zk.y));
+      float2 O2 = make_float2(0.5f * (Zc.y + Zk.y), -0.5f * (Zc.x - Zk.x));
+      float2 W2 = W2v[u];
+      float2 WO2 = cmul(W2, O2);
+      float2 Eg2 = make_float2(sp * E2.x - sm * WO2.x, sp * E2.y - sm * WO2.y);
+      float2 WcE2 = cmulc(E2, W2);
+      float2 Og2 = make_float2(-sm * WcE2.x + sp * O2.x, -sm * WcE2.y + sp * O2.y);
+      Z[sw(kk)] = make_float2(Eg2.x - Og2.y, Eg2.y + Og2.x);
+    }
+    Z[sw(k)] = Zk2;
+    }
+  }
+  __syncthreads();
+  float2* other = Z == z ? t : z;
+  stockham_fft<true>(Z, other, m, tw, tw_n, tid, nthr);   // equal pass counts: ends in z
+}
+
+// layer-1 producer for channels 8 H .. 8 H + 7 (H compile-time, so the weights are
+// constant-bank operands): rows r0, r0 + 64, r0 + 128 of each a1 tile
+template <int H>
+NMG_D void a1_row(const Smooth1dArgs& a, const float* u, int p, int n, uint4& hi, uint4& lo) {
+  float v[8];
+  if (p >= 0 && p < n) {
+    const float* up = u + p - 2;   // u = b S1 / ||b|| with zero padding
+    const float x0 = up[0], x1 = up[1], x2 = up[2], x3 = up[3], x4 = up[4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float* w = a.w.w0 + (8 * H + j) * KS;
+      float acc = a.w.b0[8 * H + j];
+      acc = fmaf(w[0], x0, acc);
+      acc = fmaf(w[1], x1, acc);
+      acc = fmaf(w[2], x2, acc);
+      acc = fmaf(w[3], x3, acc);
+      acc = fmaf(w[4], x4, acc);
+      v[j] = fmaxf(acc, 0.f);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = 0.f;
+  }
+  split8(v, hi, lo);
+}
+
+// Layer-1 producer for channels 8 H .. 8 H + 7 (H compile-time, so the weights are
+// constant-bank operands).  Buffer row r of tile k holds position k TP - 2 + r; rows 0..131
+// are read by the five tap-shifted MMAs.  Each thread computes rows 4 + r0 and 68 + r0
+// (two rows, r0 < 64); rows 0..3 of tile k are rows 128..131 of tile k - 1, which the
+// threads r0 = 60..63 carry over in registers (tile 0 computes them).
+template <int H, int NSA>
+NMG_D void produce_a1(const Smooth1dArgs& a, uint8_t* Abuf, uint64_t* aempty, uint64_t* afull, const float* u,
+                      int r0, int ntile, int n, int lane) {
+  const bool carry = r0 >= 60;
+  uint4 ch, cl;
+  if (carry) a1_row<H>(a, u, r0 - 60 - 2, n, ch, cl);   // tile 0 rows 0..3
+  for (int k = 0; k < ntile; ++k) {
+    const int st = k % NSA;
+    const int Q0 = k * TP;
+    uint4 h0, l0, h1, l1;
+    a1_row<H>(a, u, Q0 + 2 + r0, n, h0, l0);
+    a1_row<H>(a, u, Q0 + 66 + r0, n, h1, l1);
+    mb_wait(&aempty[st], ((uint32_t)(k / NSA) & 1u) ^ 1u);
+    uint4* ah = reinterpret_cast<uint4*>(Abuf + (2 * st) * ABYTES) + H * AR;
+    uint4* al = reinterpret_cast<uint4*>(Abuf + (2 * st + 1) * ABYTES) + H * AR;
+    ah[4 + r0] = h0; al[4 + r0] = l0;
+    ah[68 + r0] = h1; al[68 + r0] = l1;
+    if (carry) {
+      ah[r0 - 60] = ch; al[r0 - 60] = cl;
+      ch = h1; cl = l1;
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncwarp();
+    if (lane == 0) mb_arrive(&afull[st]);
+  }
+}
+
+template <int NSA>
+__global__ void __launch_bounds__(NT, 3) smooth1d_f16_kernel(const __grid_constant__ Smooth1dArgs a) {
   extern __shared__ __align__(1024) uint8_t smraw[];
   uint8_t* sm = smraw + ((1024u - (su32(smraw) & 1023u)) & 1023u);
   const int n = a.n, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int rhs = blockIdx.x;
   uint8_t* Abuf = sm;                                          // [2 stages][hi | lo] ABYTES each
-  uint8_t* Bw = Abuf + 4 * ABYTES;                             // [5 taps][2][32][8] f16
-  float* par = reinterpret_cast<float*>(Bw + KS * BTAP);       // w0 [c][5], b0, b1, w2t [t][c], b2
-  float* w0 = par;
-  float* b0 = w0 + C * KS;
-  float* b1 = b0 + C;
-  float* w2t = b1 + C;
-  float* b2 = w2t + KS * C;
-  float* qs = par + 256;                                       // [5][QR]
-  float* u = qs + KS * QR;                                     // n + 2 UPAD
-  float* hb = u + n + 2 * UPAD;                                // n (filter buffer)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(hb + n);        // afull[2] aempty[2] dfull[2] dempty[2]
+  uint8_t* Bw = Abuf + abuf_bytes(NSA, n);                     // [5 taps][2][32][8] f16
+  float* qs = reinterpret_cast<float*>(Bw + KS * BTAP);        // [5][QR]
+  float* hb = qs + KS * QR;                                    // n (filter buffer)
+  float* u = hb + n;                                           // n + 2 UPAD (input row, then x*)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(u + n + 2 * UPAD);        // afull[2] aempty[2] dfull[2] dempty[2]
   uint64_t* afull = bars;
-  uint64_t* aempty = bars + 2;
-  uint64_t* dfull = bars + 4;
-  uint64_t* dempty = bars + 6;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 8);
+  uint64_t* aempty = afull + NSA;
+  uint64_t* dfull = aempty + NSA;
+  uint64_t* dempty = dfull + NSD;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + NSD);
   __shared__ double red[32];
 
   // ---------------------------------------------------------------- setup (all threads)
@@ -143,35 +377,32 @@ __global__ void __launch_bounds__(NT, 3) smooth1d_f16_kernel(Smooth1dArgs a) {
     const uint4* g = reinterpret_cast<const uint4*>(a.wb);
     uint4* d = reinterpret_cast<uint4*>(Bw);
     for (int i = tid; i < KS * BTAP / 16; i += NT) d[i] = __ldg(g + i);
-    const float* P = a.params;   // w0 [16][1][5], b0 [16], w1 [16][16][5], b1 [16], w2 [1][16][5], b2
-    for (int i = tid; i < C * KS + C; i += NT) w0[i] = __ldg(P + i);
-    for (int i = tid; i < C; i += NT) b1[i] = __ldg(P + C * KS + C + C * C * KS + i);
-    for (int i = tid; i < KS * C; i += NT) {
-      const int t = i / C, c = i - t * C;
-      w2t[i] = __ldg(P + C * KS + C + C * C * KS + C + c * KS + t);
-    }
-    if (tid == 0) b2[0] = __ldg(P + C * KS + C + C * C * KS + C + C * KS);
   }
   if (tid == 0) {
-    for (int s = 0; s < 2; ++s) {
-      mb_init(&afull[s], 4); mb_init(&aempty[s], 1); mb_init(&dfull[s], 1); mb_init(&dempty[s], 4);
-    }
+    for (int s = 0; s < NSA; ++s) { mb_init(&afull[s], 4); mb_init(&aempty[s], 1); }
+    for (int s = 0; s < NSD; ++s) { mb_init(&dfull[s], 1); mb_init(&dempty[s], 4); }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 8) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tslot)), "r"(64));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tslot)), "r"(32 * NSD));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   const float* brow = a.b + (int64_t)rhs * a.ldb;
+  if (tid < UPAD) { u[tid] = 0.f; u[UPAD + n + tid] = 0.f; }
   double ss = 0.0;
   for (int j = tid; j < n; j += NT) {
     const float v = brow[j];
     u[UPAD + j] = v;
     ss += (double)v * (double)v;
   }
-  if (tid < UPAD) { u[tid] = 0.f; u[UPAD + n + tid] = 0.f; }
   double s = 1.0;
   if (a.normalize) s = sqrt(block_sum_f64(ss, red));   // block-wide, ends with all threads holding s
+  if (s != 0.0) {
+    // u = b / s with the f16 scale S1 folded in (ReLU(S z) = S ReLU(z), S > 0)
+    const float isc = (float)(1.0 / s) * a.in_scale;
+    __syncthreads();
+    for (int j = tid; j < n; j += NT) u[UPAD + j] *= isc;
+  }
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
@@ -186,92 +417,54 @@ __global__ void __launch_bounds__(NT, 3) smooth1d_f16_kernel(Smooth1dArgs a) {
       if (a.xh) tf32_store(xv, a.xh, a.xl, (int64_t)rhs * a.ldx + j);
     }
   } else {
-    const float inv = (float)(1.0 / s);
     const float sf = (float)s;
     const int ntile = n / TP;
     if (warp >= 4 && warp < 8) {
       // ---------------------------------------------------------- layer-1 producer
       const int pt = tid - 128;                 // 0..127
-      const int half = pt >> 6;                 // channels 8 half .. 8 half + 7
-      const int r0 = pt & 63;                   // rows r0, r0 + 64, r0 + 128 (< AR)
-      // weights with u = b / s and the f16 scale S1 folded in (ReLU(S z) = S ReLU(z), S > 0)
-      const float sc = a.in_scale;
-      float wr[8][KS], br[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        br[j] = b0[8 * half + j] * sc;
-#pragma unroll
-        for (int t = 0; t < KS; ++t) wr[j][t] = w0[(8 * half + j) * KS + t] * (inv * sc);
-      }
-      for (int k = 0; k < ntile; ++k) {
-        const int st = k & 1;
-        mb_wait(&aempty[st], ((uint32_t)(k >> 1) & 1u) ^ 1u);
-        uint4* ah = reinterpret_cast<uint4*>(Abuf + (2 * st) * ABYTES) + half * AR;
-        uint4* al = reinterpret_cast<uint4*>(Abuf + (2 * st + 1) * ABYTES) + half * AR;
-        const int Q0 = k * TP;
-        for (int r = r0; r < AR; r += 64) {
-          const int p = Q0 - 2 + r;             // a1 position of buffer row r
-          float v[8];
-          if (r < TP + 4 && p >= 0 && p < n) {
-            const float* up = u + UPAD + p - 2;
-            const float x0 = up[0], x1 = up[1], x2 = up[2], x3 = up[3], x4 = up[4];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              float acc = br[j];
-              acc = fmaf(wr[j][0], x0, acc);
-              acc = fmaf(wr[j][1], x1, acc);
-              acc = fmaf(wr[j][2], x2, acc);
-              acc = fmaf(wr[j][3], x3, acc);
-              acc = fmaf(wr[j][4], x4, acc);
-              v[j] = fmaxf(acc, 0.f);
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) v[j] = 0.f;
-          }
-          uint4 hi, lo;
-          split8(v, hi, lo);
-          ah[r] = hi;
-          al[r] = lo;
-        }
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mb_arrive(&afull[st]);
-      }
+      const int r0 = pt & 63;                   // rows 4 + r0 and 68 + r0 (see produce_a1)
+      // u holds b / s times the f16 scale S1 (ReLU(S z) = S ReLU(z), S > 0); b0 arrives
+      // pre-multiplied by S1
+      if (pt < 64) produce_a1<0, NSA>(a, Abuf, aempty, afull, u + UPAD, r0, ntile, n, lane);
+      else produce_a1<1, NSA>(a, Abuf, aempty, afull, u + UPAD, r0, ntile, n, lane);
     } else if (warp == 8) {
       // ---------------------------------------------------------- MMA issuer
-      if (lane == 0) {
-        const uint32_t ab = su32(Abuf), bb = su32(Bw);
-        for (int k = 0; k < ntile; ++k) {
-          const int st = k & 1;
-          mb_wait(&afull[st], (uint32_t)(k >> 1) & 1u);
-          mb_wait(&dempty[st], ((uint32_t)(k >> 1) & 1u) ^ 1u);
-          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-          const uint32_t d = tmem + (uint32_t)(st * 32);
-          const uint32_t ah = ab + (2 * st) * ABYTES, al = ah + ABYTES;
+      // The whole warp runs the loop converged (waits, stage arithmetic and descriptors stay
+      // warp-uniform, so they live in uniform registers); one elected lane issues.
+      const uint32_t ab = su32(Abuf), bb = su32(Bw);
+      const uint64_t db0 = desc_ns(bb, BLBO), da0 = desc_ns(ab, ALBO);
+      for (int k = 0; k < ntile; ++k) {
+        const int st = k % NSA, sd = k % NSD;
+        mb_wait(&afull[st], (uint32_t)(k / NSA) & 1u);
+        mb_wait(&dempty[sd], ((uint32_t)(k / NSD) & 1u) ^ 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        if (elect_one()) {
+          const uint32_t d = tmem + (uint32_t)(sd * 32);
+          // descriptor start addresses are in 16-byte units: + 1 per tap row shift
+          const uint64_t dah = da0 + (uint64_t)((2 * st) * ABYTES >> 4), dal = dah + (ABYTES >> 4);
 #pragma unroll
           for (int t = 0; t < KS; ++t) {
-            const uint64_t db = desc_ns(bb + t * BTAP, BLBO);
-            mma_f16(d, desc_ns(ah + 16 * t, ALBO), db, IDESC32, t > 0 ? 1u : 0u);
-            mma_f16(d, desc_ns(al + 16 * t, ALBO), db, IDESC16, 1u);
+            const uint64_t db = db0 + (uint64_t)(t * BTAP >> 4);
+            mma_f16(d, dah + t, db, IDESC32, t > 0 ? 1u : 0u);
+            mma_f16(d, dal + t, db, IDESC16, 1u);
           }
           mma_commit(&aempty[st]);
-          mma_commit(&dfull[st]);
+          mma_commit(&dfull[sd]);
         }
+        __syncwarp();
       }
-      __syncwarp();
     } else if (warp < 4) {
       // ---------------------------------------------------------- epilogue: layer 3 per tap
       const int m = tid;                        // TMEM lane = position within the tile
       const float dsc = a.d_scale;
-      const float b2v = b2[0];
+      const float b2v = a.w.b2;
       if (m < 2) {
 #pragma unroll
         for (int t = 0; t < KS; ++t) qs[t * QR + ((QR - 2 + m) & (QR - 1))] = 0.f;   // positions -2, -1
       }
       auto emit = [&](int p, float hv) {
         if (a.filter) {
-          hb[p] = hv;
+          hb[hsw(p)] = hv;
         } else {
           const float xv = a.accumulate ? xrow[p] + hv : hv;
           xrow[p] = xv;
@@ -285,24 +478,25 @@ __global__ void __launch_bounds__(NT, 3) smooth1d_f16_kernel(Smooth1dArgs a) {
         emit(p, acc * sf);
       };
       for (int k = 0; k < ntile; ++k) {
-        const int st = k & 1;
-        mb_wait(&dfull[st], (uint32_t)(k >> 1) & 1u);
+        const int sd = k % NSD;
+        mb_wait(&dfull[sd], (uint32_t)(k / NSD) & 1u);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         uint32_t d[32];
-        tld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(st * 32), d);
+        tld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(sd * 32), d);
+        tld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(sd * 32 + 16), d + 16);
         tld_wait16(d);
         tld_wait16(d + 16);
         asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
         __syncwarp();
-        if (lane == 0) mb_arrive(&dempty[st]);
+        if (lane == 0) mb_arrive(&dempty[sd]);
         float q[KS];
 #pragma unroll
         for (int t = 0; t < KS; ++t) q[t] = 0.f;
 #pragma unroll
         for (int c = 0; c < C; ++c) {
-          const float a2 = fmaxf(fmaf(__uint_as_float(d[c]) + __uint_as_float(d[16 + c]), dsc, b1[c]), 0.f);
+          const float a2 = fmaxf(fmaf(__uint_as_float(d[c]) + __uint_as_float(d[16 + c]), dsc, a.w.b1[c]), 0.f);
 #pragma unroll
-          for (int t = 0; t < KS; ++t) q[t] = fmaf(w2t[t * C + c], a2, q[t]);
+          for (int t = 0; t < KS; ++t) q[t] = fmaf(a.w.w2[c * KS + t], a2, q[t]);
         }
         const int Q0 = k * TP;
 #pragma unroll
@@ -321,16 +515,28 @@ __global__ void __launch_bounds__(NT, 3) smooth1d_f16_kernel(Smooth1dArgs a) {
     }
     __syncthreads();
     if (a.filter) {
-      // ---- level filter F'_l on the whole row (real-input FFT packing, see fft.cuh)
-      real_level_filter(hb, n, a.twiddle, a.tw_n, tid, NT);
+      // ---- level filter F'_l on the whole row (see level_filter_row); prefetch x* into the (now free) input-row buffer while the FFT runs
+      const bool pre = a.accumulate;
+      if (pre) {
+        for (int j = 4 * tid; j < n; j += 4 * NT)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(su32(u + UPAD + j)), "l"(xrow + j)
+                       : "memory");
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+      }
+      level_filter_row(reinterpret_cast<float2*>(hb), reinterpret_cast<float2*>(Abuf), n, a.twiddle, a.tw_n,
+                       tid, NT);
+      if (pre) {
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        __syncthreads();
+      }
       const float scale = 2.0f / (float)n;   // 1/(n/2) of the half-length inverse
       float mx = 0.f;
       for (int j = tid; j < n; j += NT) {
-        const float v = hb[j] * scale;
-        const float xv = a.accumulate ? xrow[j] + v : v;
+        const float v = hb[hsw(j)] * scale;
+        const float xv = a.accumulate ? (pre ? u[UPAD + j] : xrow[j]) + v : v;
         xrow[j] = xv;
         if (a.xh) tf32_store(xv, a.xh, a.xl, (int64_t)rhs * a.ldx + j);
-        if (a.x16h) { hb[j] = xv; mx = fmaxf(mx, fabsf(xv)); }
+        if (a.x16h) { hb[hsw(j)] = xv; mx = fmaxf(mx, fabsf(xv)); }
       }
       if (a.x16h) {
         // f16 hi/lo split of the updated row for the next FP16x3 operator apply, with the
@@ -351,7 +557,7 @@ __global__ void __launch_bounds__(NT, 3) smooth1d_f16_kernel(Smooth1dArgs a) {
         __half* oh = reinterpret_cast<__half*>(a.x16h) + (int64_t)rhs * a.ldx;
         __half* ol = reinterpret_cast<__half*>(a.x16l) + (int64_t)rhs * a.ldx;
         for (int j = tid; j < n; j += NT) {
-          const float v = hb[j] * S;
+          const float v = hb[hsw(j)] * S;
           const __half hv = __float2half_rn(v);
           oh[j] = hv;
           ol[j] = __float2half_rn(v - __half2float(hv));
@@ -361,23 +567,27 @@ __global__ void __launch_bounds__(NT, 3) smooth1d_f16_kernel(Smooth1dArgs a) {
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
-  if (warp == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(64));
+  if (warp == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(32 * NSD));
+}
+
+constexpr int kNSA = 2;   // a1 stages: more buy nothing once shared-memory bandwidth binds
+
+size_t smem_of(int n) {
+  return 1024 + abuf_bytes(kNSA, n) + KS * BTAP + sizeof(float) * (KS * QR + n + n + 2 * UPAD) +
+         8 * (2 * kNSA + 2 * NSD) + 16;
 }
 
 }  // namespace
 
-size_t smooth1d_f16_smem(int n) {
-  return 1024 + 4 * ABYTES + KS * BTAP + sizeof(float) * (256 + KS * QR + n + 2 * UPAD + n) + 8 * 8 + 16;
-}
+size_t smooth1d_f16_smem(int n) { return smem_of(n); }
 
 void smooth1d_f16(const Smooth1dArgs& a, cudaStream_t s) {
-  static size_t attr = 0;
-  const size_t smem = smooth1d_f16_smem(a.n);
-  if (smem > attr) {
-    cudaFuncSetAttribute(smooth1d_f16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smooth1d_f16_smem(8192));
-    attr = smooth1d_f16_smem(8192);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(smooth1d_f16_kernel<kNSA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_of(8192));
+    attr = true;
   }
-  smooth1d_f16_kernel<<<a.nrhs, NT, smem, s>>>(a);
+  smooth1d_f16_kernel<kNSA><<<a.nrhs, NT, smem_of(a.n), s>>>(a);
 }
 
 }  // namespace nmg

@@ -75,6 +75,30 @@ def test_apply_2d(which, small, small_cos):
         assert rel_l2(r.cpu().numpy(), y - want) < 1e-5
 
 
+@pytest.mark.parametrize("n,levels,nrhs", [(128, 4, 3), (512, 6, 2)])
+def test_kron_apply_levels(n, levels, nrhs):
+    """kron_tc (the 2D Kronecker apply on tcgen05) at every level it serves: mass stencil
+    half-bandwidths 0, 1, 2 (Q_0 = I, Q_l = R Q_{l-1} P), ragged 128-row tiles (M = nrhs n),
+    and n = 512 (two 256-wide N tiles per row block).  Element-wise against the oracle's
+    A_l X = C X B^T + alpha Q X Q^T."""
+    cfg = ni.CONFIGS[2].replace(n=n, levels=levels, nrhs=nrhs)
+    f, W, H, h = _both(cfg, max_rhs=nrhs)
+    rng = np.random.default_rng(7)
+    for lvl in range(1, levels):
+        m = n >> (lvl - 1)
+        x = rng.standard_normal((nrhs, m, m)).astype(np.float32)
+        want = O.apply_A(H, lvl - 1, x.astype(np.float64))
+        out = torch.zeros(nrhs, m, m, device=DEV)
+        h.debug_op(lvl, nmg.OP_APPLY, T(x), out)
+        got = out.cpu().numpy().astype(np.float64)
+        scale = np.abs(want).max()
+        assert np.abs(got - want).max() <= 1e-5 * scale, (lvl, np.abs(got - want).max() / scale)
+        y = rng.standard_normal((nrhs, m, m)).astype(np.float32)
+        r = T(y)
+        h.debug_op(lvl, nmg.OP_RESIDUAL, T(x), r)
+        assert np.abs(r.cpu().numpy() - (y - want)).max() <= 1e-5 * max(scale, 1.0), lvl
+
+
 def test_filter_2d(small):
     _, _, H, h = small
     rng = np.random.default_rng(2)

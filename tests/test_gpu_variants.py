@@ -93,10 +93,11 @@ def test_paper_form_operator_2d():
 
 
 @pytest.mark.parametrize("env", ["NMG_GEMM=simt", "NMG_CONV=ffma", "NMG_CONV=tf32", "NMG_SMOOTH1D=tc",
-                                 "NMG_SMOOTH1D=ffma", "NMG_FP64=dmma", "NMG_GRAPH=0"])
+                                 "NMG_SMOOTH1D=ffma", "NMG_FP64=dmma", "NMG_GRAPH=0",
+                                 "NMG_KRON=0"])
 def test_fallback_kernels_match(env, tmp_path):
     """The alternative kernels (SIMT GEMM, FFMA / 3xTF32 2D CNN, 3xTF32 / FFMA 1D smoother,
-    DMMA fp64 residual, no CUDA graph) agree with the oracle too; run in a subprocess so the
+    DMMA fp64 residual, no CUDA graph, separate split/GEMM/stencil 2D apply) agree with the oracle too; run in a subprocess so the
     env switch applies."""
     code = (
         "import sys; sys.path.insert(0, '.');"
