@@ -172,6 +172,9 @@ def main():
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--slab", choices=["auto", "on", "off"], default="auto",
+                    help="config 4 at N > 1: row-shard the single operator over the ranks (SURVEY §8(e)); "
+                         "auto = on for config 4 with N > 1 over NCCL")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
@@ -250,7 +253,19 @@ def main():
     # (one operator, 32 RHS): strong scaling, the 32 independent RHS split over the ranks
     # (RHS sharding needs no exchange step)
     strong = cid == 4
-    if strong:
+    # config 4 over several GPUs: the single 1024^2 operator is row-sharded (slab mode, one
+    # all-gather of the Kronecker intermediate per apply, all-to-all transposes in the level
+    # filter); every rank holds its slab of all 32 RHS
+    slab = (cfg.dim == 2 and world > 1 and args.slab == "on") or (
+        args.slab == "auto" and cid == 4 and world > 1 and os.environ.get("NMG_DIST_BACKEND", "nccl") == "nccl")
+    comm = None
+    if slab:
+        from paper_2603_01064_b200.parallel import split_slabs
+        start, global_B = 0, cfg.nrhs
+        obj = [nmg.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = nmg.Comm.nccl(world, rank, obj[0], local)
+    elif strong:
         start, B = shard_range(cfg.nrhs, world, rank)
         global_B = cfg.nrhs
     else:
@@ -259,10 +274,12 @@ def main():
     factors = ni.operator_factors(cfg)
     W = ni.weights_seed(cfg)
     h = nmg.Hierarchy(cfg.dim, cfg.n, cfg.levels, cfg.alpha, factors, nu1=cfg.nu1, nu2=cfg.nu2, max_rhs=B,
-                      device=local)
+                      device=local, comm=comm)
     for l, w in enumerate(W):
         h.load_weights(l + 1, ni.cnn_arch(cfg), w)
     y_np = make_y(B, start)
+    if slab:
+        y_np = np.ascontiguousarray(split_slabs(y_np, cfg.n, world)[rank])
     y = torch.tensor(y_np, dtype=torch.float64, device=dev)
     x = torch.zeros_like(y)
     stream = torch.cuda.Stream(dev)          # non-default stream: the library replays a CUDA graph
@@ -353,14 +370,24 @@ def main():
         xh = torch.zeros(y.shape, dtype=torch.float64).pin_memory()
         yh.copy_(torch.from_numpy(y_np))
         yhn, xhn = yh.numpy(), xh.numpy()
+        def host_step():
+            if not slab:
+                h.vcycles_host(yhn, xhn, 1, stream=stream)
+                return
+            # slab mode: the rank's slab of y and x host -> device, one cycle, x device -> host
+            y.copy_(yh, non_blocking=True)
+            x.copy_(xh, non_blocking=True)
+            h.vcycle(y, x, stream)
+            xh.copy_(x, non_blocking=True)
+
         for _ in range(2):                                   # eager run, then graph capture
-            h.vcycles_host(yhn, xhn, 1, stream=stream)
+            host_step()
         barrier()
         torch.cuda.synchronize(dev)
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         for _ in range(args.steps):
-            h.vcycles_host(yhn, xhn, 1, stream=stream)
+            host_step()
         f1.record(stream)
         torch.cuda.synchronize(dev)
         ems = max_over_ranks(f0.elapsed_time(f1))
@@ -407,12 +434,17 @@ def main():
                 "data": "synthetic (seeded RHS; W_seed Kaiming-uniform weights)",
                 "config": {"workload": workload, "global_batch": global_B, "n": cfg.n, "levels": cfg.levels,
                            "rhs": "8-RHS seeded pool tiled to the batch" if pool else "seeded, distinct",
-                           "alpha": cfg.alpha, "nu1": cfg.nu1, "nu2": cfg.nu2, "parallelism": f"rhs-shard x{world}" + (" (strong: 32 RHS split)" if strong else ""),
+                           "alpha": cfg.alpha, "nu1": cfg.nu1, "nu2": cfg.nu2,
+                           "parallelism": (f"operator slab-shard x{world} (NCCL all-gather per apply)" if slab else
+                                           f"rhs-shard x{world}" + (" (strong: 32 RHS split)" if strong else "")),
                            "l2": ("working set fits L2 (latency-bound config, no flush)" if cid == 0
                                   else "inputs larger than L2 (no flush)")},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "solve": solve,
                 "gpu_launches": launches, "clocks": clk.summary()}
         print(json.dumps(line))
+    if comm is not None:
+        h.close()
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -170,6 +170,44 @@ enum {
 nmg_status nmg_profile(nmg_hierarchy *h, int32_t enable);
 nmg_status nmg_profile_query(nmg_hierarchy *h, int32_t kclass, double *total_ms, int64_t *launches);
 
+/* ---------------------------------------------------------------------------------------
+ * Slab-sharded single-system mode (BASELINE config 4: one 2D operator
+ * row-sharded over W ranks).  Each rank owns the rows i2 in [rank R, rank R + R), R = n / W,
+ * of every right-hand side, i.e. the columns i2 of the column-major n x n matrix X.
+ * Per cycle and level: the Kronecker apply A_l X = C_l X B_l^T + alpha Q_l X Q_l^T
+ * computes T = C_l X[:, slab] locally, all-gathers T and finishes its own slab of rows of
+ * T B_l^T (one all-gather of the intermediate per apply, also for the fp64 outer residual);
+ * the CNN smoother runs on the slab plus 4 halo rows per side (its receptive field); the level
+ * filter F'_l transforms rows locally and columns after an all-to-all
+ * transpose; norms ||b_l|| and ||y - A x|| are summed over the ranks; levels whose
+ * slab would be thinner than 32 rows (or n_l < 128) run replicated on every rank after one
+ * all-gather of the restricted right-hand side.  2D only; strip-kernel CNN (C = 32 / 48).
+ * --------------------------------------------------------------------------------------- */
+typedef struct nmg_comm nmg_comm;   /* opaque communicator (one per rank)                     */
+#define NMG_COMM_ID_BYTES 128
+/* NCCL unique id for nmg_comm_create_nccl (call on rank 0, broadcast the 128 bytes). */
+nmg_status nmg_comm_nccl_unique_id(void *out_id);
+/* One rank of a W-rank NCCL communicator (one process per GPU; libnccl.so.2 is dlopen'ed).
+ * Errors: INVALID_ARG, UNSUPPORTED (no libnccl), CUDA (NCCL failure). */
+nmg_status nmg_comm_create_nccl(int32_t world, int32_t rank, const void *id, int32_t device,
+                                nmg_comm **out);
+/* W emulated ranks in ONE process on one device: out[0..world-1] receive one communicator
+ * per rank.  Each rank must be driven by its own host thread (its own stream); ranks meet at
+ * host barriers and exchange data with stream-ordered device copies (no device-side waits).
+ * Used by the tests to run the multi-rank path on a single GPU. */
+nmg_status nmg_comm_create_emulated(int32_t world, nmg_comm **out);
+/* Destroy a communicator (after every hierarchy that uses it). */
+void nmg_comm_destroy(nmg_comm *c);
+/* Build this rank's part of a slab-sharded hierarchy (desc.dim must be 2; n / world must be
+ * a multiple of 32 and >= 32; the caller keeps `comm` alive).  Afterwards nmg_vcycle,
+ * nmg_solve and nmg_residual take this rank's slab: y, x device fp64 [nrhs][R][n] holding
+ * rows i2 = rank R .. rank R + R - 1 of each RHS (same row-major [i2][i1] order); every rank
+ * must make the same calls with the same nrhs (collectives).  Relative residuals, norms and
+ * convergence decisions are global and identical on every rank.  nmg_vcycles_host and
+ * nmg_debug_level_op return NMG_ERR_UNSUPPORTED on a slab handle.
+ * Errors: as nmg_create_hierarchy, plus UNSUPPORTED for 1D / shapes the slab mode lacks. */
+nmg_status nmg_create_hierarchy_slab(const nmg_problem_desc *desc, const double *factors,
+                                     nmg_comm *comm, nmg_hierarchy **out);
 /* Number of the library's own kernel launches enqueued since the handle was created
  * (bench evidence, "gpu_launches"). */
 int64_t nmg_launch_count(const nmg_hierarchy *h);

@@ -6,6 +6,6 @@ only).  There is no CPU fallback: importing the binding without the built
 library raises.
 """
 from .binding import (  # noqa: F401
-    NmgError, Hierarchy, OP_APPLY, OP_RESIDUAL, OP_RESTRICT, OP_PROLONG, OP_FILTER,
+    NmgError, Hierarchy, Comm, nccl_unique_id, OP_APPLY, OP_RESIDUAL, OP_RESTRICT, OP_PROLONG, OP_FILTER,
     OP_CNN, OP_SMOOTH, OP_COARSE, OP_CYCLE0, lib_path, load_library,
 )

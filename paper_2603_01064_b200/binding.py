@@ -20,7 +20,9 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "SHAPE", 3: "NOT_SPD", 4: "NO_WEIGHTS", 
 
 EXPORTS = ["nmg_create_hierarchy", "nmg_load_smoother_weights", "nmg_vcycle", "nmg_solve",
            "nmg_vcycles_host", "nmg_residual", "nmg_debug_level_op", "nmg_launch_count",
-           "nmg_destroy_hierarchy", "nmg_last_error", "nmg_version", "nmg_profile", "nmg_profile_query"]
+           "nmg_destroy_hierarchy", "nmg_last_error", "nmg_version", "nmg_profile", "nmg_profile_query",
+           "nmg_comm_nccl_unique_id", "nmg_comm_create_nccl", "nmg_comm_create_emulated", "nmg_comm_destroy",
+           "nmg_create_hierarchy_slab"]
 
 KERNEL_CLASSES = ["gemm64", "gemm32", "smooth", "transfer", "coarse", "misc"]
 
@@ -78,8 +80,15 @@ def load_library(path: Optional[str] = None):
     lib.nmg_destroy_hierarchy.restype = None
     lib.nmg_last_error.restype = C.c_char_p
     lib.nmg_version.restype = C.c_char_p
+    lib.nmg_comm_nccl_unique_id.argtypes = [vp]
+    lib.nmg_comm_create_nccl.argtypes = [i32, i32, vp, i32, C.POINTER(vp)]
+    lib.nmg_comm_create_emulated.argtypes = [i32, C.POINTER(vp)]
+    lib.nmg_comm_destroy.argtypes = [vp]
+    lib.nmg_comm_destroy.restype = None
+    lib.nmg_create_hierarchy_slab.argtypes = [C.POINTER(ProblemDesc), vp, vp, C.POINTER(vp)]
     for f in ("nmg_create_hierarchy", "nmg_load_smoother_weights", "nmg_vcycle", "nmg_solve",
-              "nmg_vcycles_host", "nmg_residual", "nmg_debug_level_op"):
+              "nmg_vcycles_host", "nmg_residual", "nmg_debug_level_op", "nmg_comm_nccl_unique_id",
+              "nmg_comm_create_nccl", "nmg_comm_create_emulated", "nmg_create_hierarchy_slab"):
         getattr(lib, f).restype = C.c_int
     _LIB = lib
     return lib
@@ -108,18 +117,60 @@ def _stream(stream) -> Optional[int]:
     return getattr(stream, "cuda_stream", stream)
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (nmg_comm_nccl_unique_id), to broadcast from rank 0."""
+    lib = load_library()
+    buf = C.create_string_buffer(128)
+    _check(lib.nmg_comm_nccl_unique_id(C.cast(buf, C.c_void_p)))
+    return buf.raw
+
+
+class Comm:
+    """One rank's communicator of the slab-sharded mode (nmg_comm)."""
+
+    def __init__(self, handle, world: int, rank: int, keep=None):
+        self._c, self.world, self.rank, self._keep = handle, world, rank, keep
+
+    @classmethod
+    def nccl(cls, world: int, rank: int, uid: bytes, device: int = 0) -> "Comm":
+        lib = load_library()
+        c = C.c_void_p()
+        buf = C.create_string_buffer(uid, 128)
+        _check(lib.nmg_comm_create_nccl(world, rank, C.cast(buf, C.c_void_p), device, C.byref(c)))
+        return cls(c, world, rank)
+
+    @classmethod
+    def emulated(cls, world: int) -> list:
+        """`world` ranks in this process on one device; drive each from its own thread."""
+        lib = load_library()
+        arr = (C.c_void_p * world)()
+        _check(lib.nmg_comm_create_emulated(world, arr))
+        return [cls(C.c_void_p(arr[r]), world, r) for r in range(world)]
+
+    def close(self):
+        if getattr(self, "_c", None):
+            _LIB.nmg_comm_destroy(self._c)
+            self._c = None
+
+
 class Hierarchy:
-    """Owns an nmg_hierarchy handle (C ABI nmg_create_hierarchy ... nmg_destroy_hierarchy)."""
+    """Owns an nmg_hierarchy handle (C ABI nmg_create_hierarchy ... nmg_destroy_hierarchy).
+    With `comm`, the handle is this rank's part of a slab-sharded 2D hierarchy
+    (nmg_create_hierarchy_slab): vectors are the rank's slab [nrhs][n / world][n]."""
 
     def __init__(self, dim: int, n: int, levels: int, alpha: float, factors: Sequence[np.ndarray],
                  nu1: int = 1, nu2: int = 1, level_filter: bool = True, max_rhs: int = 1,
-                 device: int = 0):
+                 device: int = 0, comm: Optional[Comm] = None):
         lib = load_library()
         d = ProblemDesc(dim, n, levels, float(alpha), nu1, nu2, int(level_filter), max_rhs, device)
         fac = np.ascontiguousarray(np.concatenate([np.asarray(f, np.float64).ravel() for f in factors]))
         h = C.c_void_p()
-        _check(lib.nmg_create_hierarchy(C.byref(d), fac.ctypes.data, C.byref(h)))
+        if comm is None:
+            _check(lib.nmg_create_hierarchy(C.byref(d), fac.ctypes.data, C.byref(h)))
+        else:
+            _check(lib.nmg_create_hierarchy_slab(C.byref(d), fac.ctypes.data, comm._c, C.byref(h)))
         self._h = h
+        self.comm = comm
         self.dim, self.n, self.levels, self.alpha = dim, n, levels, alpha
         self.max_rhs = max_rhs
         self.N = n if dim == 1 else n * n

@@ -182,16 +182,17 @@ NMG_D void split8(const float* v, uint4& hi, uint4& lo) {
 struct Unit {
   int b, X0, y0, y1;
 };
-NMG_D Unit unit_of(int u, int n, int nx, int ys) {
+// hg = image height (rows), n = width
+NMG_D Unit unit_of(int u, int hg, int nx, int ys) {
   Unit t;
   const int per = nx * ys;
   t.b = u / per;
   const int r = u - t.b * per;
   const int yi = r / nx, xi = r - yi * nx;
   t.X0 = xi * SEG;
-  const int rows = (n + ys - 1) / ys;
+  const int rows = (hg + ys - 1) / ys;
   t.y0 = yi * rows;
-  t.y1 = min(n, t.y0 + rows);
+  t.y1 = min(hg, t.y0 + rows);
   return t;
 }
 
@@ -226,6 +227,10 @@ __global__ void __launch_bounds__(NTHR, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = a.n;
+  const int hg = a.h ? a.h : n;              // stored rows per image (slab mode: R + 2 halo rows)
+  // rows [ylo, yhi) are the image; the rest is zero padding of EVERY layer's input (a slab at
+  // the top / bottom image border has its outer halo rows outside the image)
+  const int ylo = a.ylo, yhi = a.yhi ? a.yhi : hg;
   const int nx = n >= SEG ? n / SEG : 1;   // n < 128: one strip, pixels x >= n are padding
   const int units = a.nrhs * nx * a.ysplit;
 
@@ -285,10 +290,10 @@ __global__ void __launch_bounds__(NTHR, 1)
       const int c0p = half * HC;
       int it = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const Unit t = unit_of(u, n, nx, a.ysplit);
+        const Unit t = unit_of(u, hg, nx, a.ysplit);
         const double s = a.norms ? a.norms[t.b] : 1.0;
         const float inv = (float)((s != 0.0) ? 1.0 / s : 0.0);
-        const float* B = a.b + (int64_t)t.b * n * n;
+        const float* B = a.b + (int64_t)t.b * hg * n;
         int xs[2];
         bool xin[2];
 #pragma unroll
@@ -299,7 +304,7 @@ __global__ void __launch_bounds__(NTHR, 1)
         auto ld3 = [&](int yy, float (*w)[3]) {
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const bool ok = xin[e] && yy >= 0 && yy < n;
+            const bool ok = xin[e] && yy >= ylo && yy < yhi;
             const float* row = B + (int64_t)yy * n;
 #pragma unroll
             for (int t1 = 0; t1 < 3; ++t1) {
@@ -308,7 +313,7 @@ __global__ void __launch_bounds__(NTHR, 1)
             }
           }
         };
-        const int r0 = max(t.y0 - H, 0), r1 = min(t.y1 + H - 1, n - 1);
+        const int r0 = max(t.y0 - H, ylo), r1 = min(t.y1 + H - 1, yhi - 1);
         float win[3][2][3];
         ld3(r0 - 1, win[0]);
         ld3(r0, win[1]);
@@ -378,8 +383,8 @@ __global__ void __launch_bounds__(NTHR, 1)
       int it = 0;
       const uint32_t bytes = 2u * (uint32_t)(RP * C * 2);
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const Unit t = unit_of(u, n, nx, a.ysplit);
-        const int r0 = max(t.y0 - H, 0), r1 = min(t.y1 + H - 1, n - 1);
+        const Unit t = unit_of(u, hg, nx, a.ysplit);
+        const int r0 = max(t.y0 - H, ylo), r1 = min(t.y1 + H - 1, yhi - 1);
         for (int r = r0; r <= r1; ++r, ++it) {
           const int st = it % NSTG;
           mb_wait(&empty[st], ((uint32_t)(it / NSTG) & 1u) ^ 1u);
@@ -396,11 +401,11 @@ __global__ void __launch_bounds__(NTHR, 1)
       const uint32_t wh = su32(Wh), wl = su32(Wl), rb = su32(ring);
       int it = 0, k = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const Unit t = unit_of(u, n, nx, a.ysplit);
+        const Unit t = unit_of(u, hg, nx, a.ysplit);
         for (int r = t.y0 - H; r <= t.y1 + H - 1; ++r, ++k) {
           const int buf = k & 1;
           mb_wait(&dempty[buf], ((uint32_t)(k >> 1) & 1u) ^ 1u);
-          if (r < 0 || r >= n) {          // zero-padding row: nothing to multiply
+          if (r < ylo || r >= yhi) {      // zero-padding row: nothing to multiply
             mb_arrive(&dfull[buf]);
             continue;
           }
@@ -440,7 +445,7 @@ __global__ void __launch_bounds__(NTHR, 1)
       const uint32_t d4 = tmem + (uint32_t)(2 * G::N);
       int e4 = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const Unit t = unit_of(u, n, nx, a.ysplit);
+        const Unit t = unit_of(u, hg, nx, a.ysplit);
         for (int r = t.y0 - H; r <= t.y1 + H - 1; ++r, ++e4) {
           // D4[p][t2 * 3 + t1] = sum_c a3[c](p) w3[c][t2][t1] for the a3 row the epilogue wrote
           mb_wait(a4full, (uint32_t)e4 & 1u);
@@ -495,7 +500,7 @@ __global__ void __launch_bounds__(NTHR, 1)
           for (int t1 = 0; t1 < 3; ++t1) acc4[2 - t2][t1] = fmaf(__uint_as_float(d[t2 * 3 + t1]), s4, acc4[2 - t2][t1]);
         const int yh = ya - 1;
         if (yh >= t.y0 && yh < t.y1 && x < n)
-          reinterpret_cast<float4*>(a.q)[((int64_t)t.b * n + yh) * n + x] =
+          reinterpret_cast<float4*>(a.q)[((int64_t)t.b * hg + yh) * n + x] =
               make_float4(acc4[0][0], acc4[0][1], acc4[0][2], 0.f);
 #pragma unroll
         for (int t1 = 0; t1 < 3; ++t1) {
@@ -507,7 +512,7 @@ __global__ void __launch_bounds__(NTHR, 1)
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     };
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const Unit t = unit_of(u, n, nx, a.ysplit);
+      const Unit t = unit_of(u, hg, nx, a.ysplit);
       const int x = t.X0 + m;
       float P0[CG], P1[CG];
 #pragma unroll
@@ -518,17 +523,17 @@ __global__ void __launch_bounds__(NTHR, 1)
         for (int j = 0; j < 3; ++j) acc4[i][j] = 0.f;
       for (int r = t.y0 - H; r <= t.y1 + H - 1; ++r, ++k) {
         const int buf = k & 1;
-        const bool valid = r >= 0 && r < n;
+        const bool valid = r >= ylo && r < yhi;
         mb_wait(&dfull[buf], (uint32_t)(k >> 1) & 1u);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * G::N + c0);
         // output row r - 1 is complete: b + D_0(r - 2) + D_1(r - 1) + D_2(r)
         const int yo = r - 1;
-        const bool yin = yo >= 0 && yo < n;
+        const bool yin = yo >= ylo && yo < yhi;
         // layers 3-4: the previous a3 row's layer-4 result first (it also frees the A4 tile)
         if (!FIRST && r > t.y0 - H) consume_d4(t, x, r - 2);
         const bool store = FIRST && yo >= t.y0 && yo < t.y1 && x < n;
-        const int64_t off = (((int64_t)t.b * n + (store ? yo : 0)) * n + x) * C + c0;
+        const int64_t off = (((int64_t)t.b * hg + (store ? yo : 0)) * n + x) * C + c0;
         // 8 channels at a time: D_2 -> this row's activation, D_1 / D_0 -> the carries.  With
         // 16 channels per thread all 48 columns are loaded before one wait (latency once per row)
         constexpr int GB = CG == 16 ? 2 : 1;             // chunks per TMEM wait
@@ -601,14 +606,17 @@ __global__ void __launch_bounds__(NTHR, 1)
 }
 
 // h(y, x) = s (b3 + Q0(y, x - 1) + Q1(y, x) + Q2(y, x + 1))  ->  Z = (h, 0) or x (+)= h
+// slab mode: images of hg rows whose first and last hh rows are halo (not written)
 __global__ void strip_combine_kernel(int n, int nrhs, const float4* __restrict__ Q, const double* __restrict__ norms,
                                      const float* __restrict__ b3, float2* __restrict__ Z, int zb0,
-                                     float* __restrict__ xo, int accumulate) {
+                                     float* __restrict__ xo, int accumulate, int hg, int hh) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t per = (int64_t)n * n;
+  const int64_t per = (int64_t)hg * n;
   if (idx >= nrhs * per) return;
   const int b = (int)(idx / per);
   const int x = (int)(idx % n);
+  const int row = (int)((idx - (int64_t)b * per) / n);
+  if (row < hh || row >= hg - hh) return;
   const double s = norms ? norms[b] : 1.0;
   float acc = 0.f;
   if (s != 0.0) {
@@ -618,7 +626,7 @@ __global__ void strip_combine_kernel(int n, int nrhs, const float4* __restrict__
   }
   // the filter path takes N(u) unscaled (O(1) for every RHS, so two paired RHS of very
   // different ||b|| do not pollute each other); filter2d multiplies by s after F'
-  if (Z) zput(Z, per, zb0 + b, idx - (int64_t)b * per, acc);
+  if (Z) zput(Z, (int64_t)(hg - 2 * hh) * n, zb0 + b, (int64_t)(row - hh) * n + x, acc);
   else {
     const float hv = acc * (float)s;
     xo[idx] = accumulate ? xo[idx] + hv : hv;
@@ -641,10 +649,11 @@ void launch(const CUtensorMap* mh, const CUtensorMap* ml, const StripArgs& a, in
 
 }  // namespace
 
-int strip_ysplit(int n, int nrhs, int num_sms) {
+int strip_ysplit(int n, int nrhs, int num_sms, int hg) {
   const int strips = nrhs * (n >= SEG ? n / SEG : 1);
+  if (hg <= 0) hg = n;
   int ys = 1;
-  while (strips * ys < 4 * num_sms && ys < n / 32) ys *= 2;
+  while (strips * ys < 4 * num_sms && ys < hg / 32) ys *= 2;
   return ys;
 }
 
@@ -657,10 +666,11 @@ void strip_l34(const CUtensorMap* mh, const CUtensorMap* ml, const StripArgs& a,
   else launch<48, false>(mh, ml, a, num_sms, s);
 }
 void strip_combine(int n, int nrhs, const float* q, const double* norms, const float* b3, float2* Z, int zb0,
-                   float* x, bool accumulate, cudaStream_t s) {
-  const int64_t tot = (int64_t)nrhs * n * n;
+                   float* x, bool accumulate, cudaStream_t s, int hg, int hh) {
+  if (hg <= 0) hg = n;
+  const int64_t tot = (int64_t)nrhs * hg * n;
   strip_combine_kernel<<<(int)ceil_div64(tot, 256), 256, 0, s>>>(n, nrhs, reinterpret_cast<const float4*>(q), norms,
-                                                                 b3, Z, zb0, x, accumulate ? 1 : 0);
+                                                                 b3, Z, zb0, x, accumulate ? 1 : 0, hg, hh);
 }
 
 }  // namespace nmg

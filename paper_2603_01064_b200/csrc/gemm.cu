@@ -254,10 +254,13 @@ __global__ void __launch_bounds__(DNT) dgemm_resid_kernel(Gemm64Args a) {
           double v = a.negate ? -acc[i][j][e] : acc[i][j][e];
           if (a.tblock) {
             const int64_t tb = a.tblock;
-            const int64_t off = (m / tb) * tb * tb + (int64_t)n * tb + (m % tb);
+            const int64_t R = a.tb_R ? a.tb_R : tb, S = a.tb_S ? a.tb_S : tb;
+            const int64_t img = a.tb_img ? a.tb_img : tb * tb;
+            const int64_t bi = m / R, rr = m - bi * R;
+            const int64_t off = bi * img + (int64_t)n * S + rr;
             if (a.Y) v = a.Y[off] + v;
             if (a.ax) v = fma(-a.alpha, a.ax[off], v);
-            if (a.r32) a.r32[off] = (float)v;
+            if (a.r32) a.r32[a.r32_img ? bi * a.r32_img + a.r32_off + (int64_t)n * S + rr : off] = (float)v;
             if (a.r64) a.r64[off] = v;
           } else {
             if (a.Y) v = a.Y[(int64_t)m * a.ldy + n] + v;

@@ -39,6 +39,11 @@ struct Gemm64Args {
                                           //     Y, ax, r32, r64 all use that mapping with ld = tb
   const double* ax = nullptr;             // optional: R -= alpha * ax (same location as R)
   double alpha = 0.0;
+  // generalised block mapping (slab mode; 0 = tblock defaults): output (m, n) at
+  // (m / tb_R) tb_img + n tb_S + m % tb_R; r32 (when r32_img != 0) at
+  // (m / tb_R) r32_img + r32_off + n tb_S + m % tb_R (a halo'd fp32 slab)
+  int tb_R = 0, tb_S = 0;
+  int64_t tb_img = 0, r32_img = 0, r32_off = 0;
 };
 int gemm_f64_ntiles(int N);
 void gemm_f64(const Gemm64Args& a, cudaStream_t s);
@@ -86,6 +91,13 @@ struct KronArgs {
   int hb = 0;
   float alpha = 0.f;
   bool negate = false;
+  // slab-sharded mode (0 = whole image): each image is stored as R rows (global rows r0 ..
+  // r0 + R - 1) plus H halo rows above and below; img = per-image stride of X / Cin / D.
+  // Pass 1 reads all R + 2H stored rows (M = nrhs (R + 2H)) and writes T[b][i1][R] for its
+  // slab only; pass 2 (A = the gathered T, M = nrhs n) computes the slab's R output rows
+  // (W rows r0 .. r0 + R - 1, W map box rows kron_tile_n(R)).
+  int R = 0, H = 0, r0 = 0;
+  int64_t img = 0;
 };
 int kron_tile_n(int n);
 bool kron_supported(int n, int hb);
@@ -185,7 +197,17 @@ void norms_f32(int nrhs, int64_t N, const float* x, double* part, int chunks, do
 // norms (may be null): per-RHS ||b||; the writers store N(u) and x gets ||b|| F'(N(u))
 void filter2d(int nrhs, int n, float2* Z, const float2* tw, int tw_n, float* x, bool accumulate, cudaStream_t s,
               const double* norms);
-void filter2d_prepare(int nrhs, int n, float2* Z, cudaStream_t s);
+void filter2d_prepare(int nrhs, int n, float2* Z, cudaStream_t s, int rows = 0);
+// per-RHS sum of squares (no sqrt) of N values at x + b img + off
+void sumsq_f32(int nrhs, int64_t N, const float* x, int64_t img, int64_t off, double* part, int chunks, double* out,
+               cudaStream_t s);
+// slab-sharded level filter (level2d.cu; steps in the comment there)
+void filter2d_slab_rows(int n, int npair, int R, float2* Zs, const float2* tw, int tw_n, cudaStream_t s);
+void filter2d_slab_pack(int n, int npair, int R, int W, float2* Zs, float2* buf, bool unpack, cudaStream_t s);
+void filter2d_slab_cols(int n, int npair, int R, int W, int rank, float2* buf, const float2* tw, int tw_n,
+                        cudaStream_t s);
+void filter2d_slab_inverse(int n, int nrhs, int R, float2* Zs, const float2* tw, int tw_n, float* x, int64_t ximg,
+                           int64_t xoff, bool accumulate, const double* norms, cudaStream_t s);
 void real_to_complex(int nrhs, int64_t N, const float* x, float2* Z, cudaStream_t s);
 
 // ---- 2D CNN on tensor cores (conv_tc.cu), C = 32 ------------------------------------
@@ -226,11 +248,31 @@ struct StripArgs {
   const uint16_t* w4;         // l34: layer-4 weights x T4, f16 hi then lo, [C/8][16][8] (row t2*3+t1)
   float a3_scale;             // l34: S3 (a3 is split as a3 S3)
   float d4_scale;             // l34: 1 / (S3 T4)
+  int h = 0;                  // stored rows per image (0: n); slab mode: R + 2 halo rows (the
+                              // halo rows' outputs are discarded)
+  int ylo = 0, yhi = 0;       // image rows [ylo, yhi) (yhi 0: h); rows outside are the zero
+                              // padding of every layer (slabs at the image's top / bottom edge)
 };
-int strip_ysplit(int n, int nrhs, int num_sms);
+int strip_ysplit(int n, int nrhs, int num_sms, int hg = 0);
 void strip_l12(const StripArgs& a, int num_sms, cudaStream_t s);
 void strip_l34(const CUtensorMap* mh, const CUtensorMap* ml, const StripArgs& a, int num_sms, cudaStream_t s);
 void strip_combine(int n, int nrhs, const float* q, const double* norms, const float* b3, float2* Z, int zb0,
-                   float* x, bool accumulate, cudaStream_t s);
+                   float* x, bool accumulate, cudaStream_t s, int hg = 0, int hh = 0);
+
+
+// ---- slab-sharded single-system mode (slab.cu): slabs of R rows + H halo rows per image --
+void restrict_slab(int nrhs, int n_c, int Rc, int r0c, const float* f, int64_t fimg, int64_t foff, float* c,
+                   int64_t cimg, int64_t coff, cudaStream_t s);
+void prolong_slab(int nrhs, int n_c, int Rf, int r0f, const float* c, int64_t cimg, int64_t coff, float* f,
+                  int64_t fimg, int64_t foff, cudaStream_t s);
+void halo_pack(int nrhs, int n, int R, int H, const float* x, float* send, cudaStream_t s);
+void halo_unpack(int nrhs, int n, int R, int H, int rank, int W, const float* recv, float* x, cudaStream_t s);
+void update_slab(int nrhs, int64_t N, double* x, const float* d, int64_t img, int64_t off, const uint8_t* active,
+                 cudaStream_t s);
+void part_sums(int nrhs, int64_t cnt, const double* part, double* out, cudaStream_t s);
+void relres_sums(int nrhs, const double* rsq, const double* ysq, double* relres, double tol, uint8_t* active,
+                 cudaStream_t s);
+void sqrt_inplace(int n, double* v, cudaStream_t s);
+void sumsq_f64(int nrhs, int64_t N, const double* y, double* part /*[nrhs][64]*/, double* out, cudaStream_t s);
 
 }  // namespace nmg

@@ -144,7 +144,10 @@ __global__ void __launch_bounds__(KNT, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = a.n;
   const int KT = n / KBK;
-  const int NT = (n + TBN - 1) / TBN;
+  // slab mode (R < n): pass 1 rows are the rank's halo'd image rows, pass 2 columns its slab
+  const int R = a.R ? a.R : n;
+  const int NT = ((a.mode == KRON_T ? n : R) + TBN - 1) / TBN;
+  const int wrow0 = a.mode == KRON_T ? 0 : a.r0;
   const int MT = (a.M + KBM - 1) / KBM;
   const int T = MT * NT;
 
@@ -177,8 +180,8 @@ __global__ void __launch_bounds__(KNT, 1)
           uint8_t* st = sm + s * STAGE;
           mb_expect(&full[s], A_BYTES + 2 * B_BYTES);
           tma2d(st, &tA, &full[s], kt * KBK, m0);
-          tma2d(st + 2 * A_BYTES, &tWh, &full[s], kt * KBK, n0);
-          tma2d(st + 2 * A_BYTES + B_BYTES, &tWl, &full[s], kt * KBK, n0);
+          tma2d(st + 2 * A_BYTES, &tWh, &full[s], kt * KBK, wrow0 + n0);
+          tma2d(st + 2 * A_BYTES + B_BYTES, &tWl, &full[s], kt * KBK, wrow0 + n0);
         }
       }
     }
@@ -237,14 +240,18 @@ __global__ void __launch_bounds__(KNT, 1)
       }
     }
   } else {   // ---------------- epilogue, warps 0-3 (TMEM lanes 32 w .. 32 w + 31)
-    const int64_t nn2 = (int64_t)n * n;
+    const int64_t img = a.img ? a.img : (int64_t)n * n;   // per-image stride of X, Cin, D
+    const int AH = R + 2 * a.H;                            // pass-1 A rows per image
     int i = 0;
     for (int t = blockIdx.x; t < T; t += gridDim.x, ++i) {
       const int ab = i & 1;
       const int m = (t / NT) * KBM + warp * 32 + lane, n0 = (t % NT) * TBN;
-      const bool mok = m < a.M;
-      const int b = m / n, r = m - (m / n) * n;   // image, row of the image (i1 of the output)
-      const int64_t base = b * nn2 + r;
+      // pass 1: image b, stored row e (slab row e - H; halo rows are not stored);
+      // pass 2: image b, row r = i1 of the output
+      const int b = a.mode == KRON_T ? m / AH : m / n;
+      const int r = a.mode == KRON_T ? m - b * AH - a.H : m - b * n;
+      const bool mok = m < a.M && (a.mode != KRON_T || (r >= 0 && r < R));
+      const int64_t base = a.mode == KRON_T ? (int64_t)b * n * R + r : b * img + (int64_t)a.H * n + r;
       float q1[2 * HB + 1];
       if (a.mode == KRON_RESID && mok) {
 #pragma unroll
@@ -266,21 +273,22 @@ __global__ void __launch_bounds__(KNT, 1)
         if (a.mode == KRON_T) {
 #pragma unroll
           for (int j = 0; j < 16; ++j)
-            if (nb + j < n) a.D[base + (int64_t)(nb + j) * n] = __uint_as_float(v[j]);
+            if (nb + j < n) a.D[base + (int64_t)(nb + j) * R] = __uint_as_float(v[j]);
         } else {
-          const float* Xb = a.X + b * nn2;
+          // X rows addressed by their global index i2 (the slab's halo holds i2 +- hb)
+          const float* Xb = a.X + b * img + (int64_t)(a.H - a.r0) * n;
           float o[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
-            const int i2 = min(nb + j, n - 1);
-            const float sq = qstencil_at<HB>(Xb, a.Q, n, i2, r, q1);
+            const int jj = min(nb + j, R - 1);
+            const float sq = qstencil_at<HB>(Xb, a.Q, n, a.r0 + jj, r, q1);
             const float vv = fmaf(a.alpha, sq, __uint_as_float(v[j]));
-            const float cc = a.Cin ? a.Cin[base + (int64_t)i2 * n] : 0.f;
+            const float cc = a.Cin ? a.Cin[base + (int64_t)jj * n] : 0.f;
             o[j] = a.negate ? cc - vv : cc + vv;
           }
 #pragma unroll
           for (int j = 0; j < 16; ++j)
-            if (nb + j < n) a.D[base + (int64_t)(nb + j) * n] = o[j];
+            if (nb + j < R) a.D[base + (int64_t)(nb + j) * n] = o[j];
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -303,7 +311,8 @@ void launch_kron(const CUtensorMap* A, const CUtensorMap* Wh, const CUtensorMap*
     cudaFuncSetAttribute(kron_tc_kernel<TBN, HB>, cudaFuncAttributeMaxDynamicSharedMemorySize, KronCfg<TBN>::SMEM);
     attr = true;
   }
-  const int tiles = ceil_div(a.M, KBM) * ceil_div(a.n, TBN);
+  const int cols = a.mode == KRON_T ? a.n : (a.R ? a.R : a.n);
+  const int tiles = ceil_div(a.M, KBM) * ceil_div(cols, TBN);
   kron_tc_kernel<TBN, HB><<<std::min(tiles, sms), KNT, KronCfg<TBN>::SMEM, s>>>(*A, *Wh, *Wl, a);
 }
 
@@ -327,7 +336,7 @@ bool kron_supported(int n, int hb) {
 
 void kron_tc(const CUtensorMap* A, const CUtensorMap* Wh, const CUtensorMap* Wl, const KronArgs& a, int sms,
              cudaStream_t s) {
-  switch (kron_tile_n(a.n)) {
+  switch (kron_tile_n(a.mode == KRON_T ? a.n : (a.R ? a.R : a.n))) {
     case 32: launch_kron_hb<32>(A, Wh, Wl, a, sms, s); break;
     case 64: launch_kron_hb<64>(A, Wh, Wl, a, sms, s); break;
     case 128: launch_kron_hb<128>(A, Wh, Wl, a, sms, s); break;

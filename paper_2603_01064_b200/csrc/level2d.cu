@@ -80,23 +80,24 @@ __global__ void qstencil_kernel(int nrhs, int n, int hb, float alpha, const floa
 
 // per-RHS sum of squares, fp64, two stages (fixed order => deterministic)
 __global__ void __launch_bounds__(256) sumsq_partial_kernel(int64_t N, int chunks, const float* __restrict__ x,
-                                                            double* __restrict__ part) {
+                                                            double* __restrict__ part, int64_t img, int64_t off) {
   __shared__ double red[32];
   const int b = blockIdx.y, ch = blockIdx.x;
   const int64_t len = ceil_div64(N, chunks);
   const int64_t lo = ch * len, hi = min(N, lo + len);
-  const float* r = x + (int64_t)b * N;
+  const float* r = x + (int64_t)b * img + off;
   double s = 0.0;
   for (int64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) s += (double)r[j] * (double)r[j];
   s = block_sum_f64(s, red);
   if (threadIdx.x == 0) part[(int64_t)b * chunks + ch] = s;
 }
-__global__ void sumsq_final_kernel(int nrhs, int chunks, const double* __restrict__ part, double* __restrict__ out) {
+__global__ void sumsq_final_kernel(int nrhs, int chunks, const double* __restrict__ part, double* __restrict__ out,
+                                   int take_sqrt) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= nrhs) return;
   double s = 0.0;
   for (int c = 0; c < chunks; ++c) s += part[(int64_t)b * chunks + c];
-  out[b] = sqrt(s);
+  out[b] = take_sqrt ? sqrt(s) : s;
 }
 
 // ------------------------------------------------------------------ fused 2D CNN (FFMA)
@@ -258,10 +259,13 @@ __global__ void __launch_bounds__(256, 1) cnn2d_kernel(Cnn2dArgs a) {
 
 // ------------------------------------------------------------------ 2D FFT filter passes
 // rows: R rows of length n per CTA (R*n <= 4096 complex in smem), in place in Z
+// inverse: complex row Rr = p * rows + r of pair p writes x at b * ximg + xoff + r * n + col
+// (rows = n, ximg = n n, xoff = 0 for whole images; slab mode: the rank's R rows of a halo'd slab)
 __global__ void __launch_bounds__(256) fft_rows_kernel(int n, int64_t nrows, float2* __restrict__ Z,
                                                        const float2* __restrict__ tw, int tw_n, int inverse,
                                                        float* __restrict__ x, int accumulate, float scale, int nrhs,
-                                                       const double* __restrict__ norms) {
+                                                       const double* __restrict__ norms, int rpi, int64_t ximg,
+                                                       int64_t xoff) {
   extern __shared__ __align__(16) float2 cb[];
   const int R = max(1, 4096 / n);
   const int64_t r0 = (int64_t)blockIdx.x * R;
@@ -276,11 +280,11 @@ __global__ void __launch_bounds__(256) fft_rows_kernel(int n, int64_t nrows, flo
   } else {
     fft_dit_inverse_batch(cb, n, rows, n, 1, tw, tw_n, threadIdx.x, 256);
     // complex image p holds RHS 2p (real part) and 2p + 1 (imaginary part)
-    const int64_t N = (int64_t)n * n;
+    const int64_t N = ximg;
     for (int i = threadIdx.x; i < tot; i += 256) {
       const int64_t R = r0 + i / n;                      // complex row
-      const int64_t p = R / n;
-      const int64_t o = (2 * p * n + (R - p * n)) * n + i % n;
+      const int64_t p = R / rpi;
+      const int64_t o = 2 * p * ximg + xoff + (R - p * rpi) * n + i % n;
       const float s0 = norms ? (float)norms[2 * p] : 1.f;
       const float v0 = (cb[i].x * scale) * s0;
       x[o] = accumulate ? x[o] + v0 : v0;
@@ -323,6 +327,55 @@ __global__ void __launch_bounds__(256) fft_cols_kernel(int n, int G, float2* __r
   }
 }
 
+// slab columns: buf = [W][npair][R][cw] (chunk q = rows q R .. q R + R - 1 of this rank's
+// columns); CTA = (group of G local columns, pair); mask with global position k1base + c
+__global__ void __launch_bounds__(256) fft_cols_slab_kernel(int n, int G, int R, int cw, int npair, float2* __restrict__ Z,
+                                                            const float2* __restrict__ tw, int tw_n, int k1base) {
+  extern __shared__ __align__(16) float2 cb[];   // [n][G]
+  const int p = blockIdx.y, k0 = blockIdx.x * G;
+  const int log2n = 31 - __clz(n);
+  const int64_t qstride = (int64_t)npair * R * cw;
+  auto at = [&](int r, int c) -> int64_t {
+    const int q = r / R;
+    return q * qstride + ((int64_t)p * R + (r - q * R)) * cw + k0 + c;
+  };
+  for (int i = threadIdx.x; i < n * G; i += 256) {
+    const int r = i / G, c = i - r * G;
+    cb[i] = Z[at(r, c)];
+  }
+  __syncthreads();
+  fft_dif_forward_batch(cb, n, G, 1, G, tw, tw_n, threadIdx.x, 256);
+  for (int i = threadIdx.x; i < n * G; i += 256) {
+    const int r = i / G, c = i - r * G;
+    const int a2 = bitrev(r, log2n), a1 = bitrev(k1base + k0 + c, log2n);
+    const float q2 = (float)(2 * min(a2, n - a2)) / (float)n;
+    const float q1 = (float)(2 * min(a1, n - a1)) / (float)n;
+    const float m = sqrtf(fmaxf(q1, q2));
+    cb[i] = make_float2(cb[i].x * m, cb[i].y * m);
+  }
+  __syncthreads();
+  fft_dit_inverse_batch(cb, n, G, 1, G, tw, tw_n, threadIdx.x, 256);
+  for (int i = threadIdx.x; i < n * G; i += 256) {
+    const int r = i / G, c = i - r * G;
+    Z[at(r, c)] = cb[i];
+  }
+}
+
+// dir 0: send[d][p][r][c] = Zs[p][r][d cw + c];  dir 1: Zs[p][r][d cw + c] = send[d][p][r][c]
+__global__ void a2a_pack_kernel(int n, int npair, int R, int W, float2* __restrict__ Zs, float2* __restrict__ buf,
+                                int dir) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t tot = (int64_t)npair * R * n;
+  if (i >= tot) return;
+  const int cw = n / W;
+  const int col = (int)(i % n);
+  const int64_t pr = i / n;                 // p * R + r
+  const int d = col / cw, c = col - d * cw;
+  const int64_t j = ((int64_t)d * npair * R + pr) * cw + c;
+  if (dir == 0) buf[j] = Zs[i];
+  else Zs[i] = buf[j];
+}
+
 __global__ void real_to_complex_kernel(int nrhs, int64_t N, const float* __restrict__ x, float2* __restrict__ Z) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)nrhs * N) return;
@@ -344,8 +397,13 @@ void qstencil(int nrhs, int n, int hb, float alpha, const float* Q, const float*
   qstencil_kernel<<<nblk((int64_t)nrhs * n * n, 256), 256, 0, s>>>(nrhs, n, hb, alpha, Q, X, C, D);
 }
 void norms_f32(int nrhs, int64_t N, const float* x, double* part, int chunks, double* out, cudaStream_t s) {
-  sumsq_partial_kernel<<<dim3(chunks, nrhs), 256, 0, s>>>(N, chunks, x, part);
-  sumsq_final_kernel<<<nblk(nrhs, 128), 128, 0, s>>>(nrhs, chunks, part, out);
+  sumsq_partial_kernel<<<dim3(chunks, nrhs), 256, 0, s>>>(N, chunks, x, part, N, 0);
+  sumsq_final_kernel<<<nblk(nrhs, 128), 128, 0, s>>>(nrhs, chunks, part, out, 1);
+}
+void sumsq_f32(int nrhs, int64_t N, const float* x, int64_t img, int64_t off, double* part, int chunks, double* out,
+               cudaStream_t s) {
+  sumsq_partial_kernel<<<dim3(chunks, nrhs), 256, 0, s>>>(N, chunks, x, part, img, off);
+  sumsq_final_kernel<<<nblk(nrhs, 128), 128, 0, s>>>(nrhs, chunks, part, out, 0);
 }
 int cnn2d_smem(int C) {
   return (C == 32 ? Cnn2dSmem<32>::FLOATS : Cnn2dSmem<48>::FLOATS) * (int)sizeof(float);
@@ -372,16 +430,56 @@ void filter2d(int nrhs, int n, float2* Z, const float2* tw, int tw_n, float* x, 
   const int R = std::max(1, 4096 / n);
   const size_t smr = sizeof(float2) * (size_t)R * n;
   cudaFuncSetAttribute(fft_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
-  fft_rows_kernel<<<nblk(nrows, R), 256, smr, s>>>(n, nrows, Z, tw, tw_n, 0, nullptr, 0, 1.f, nrhs, nullptr);
+  fft_rows_kernel<<<nblk(nrows, R), 256, smr, s>>>(n, nrows, Z, tw, tw_n, 0, nullptr, 0, 1.f, nrhs, nullptr, n,
+                                                   (int64_t)n * n, 0);
   const int G = std::min(n, std::max(1, 16384 / n));
   const size_t smc = sizeof(float2) * (size_t)n * G;
   cudaFuncSetAttribute(fft_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
   fft_cols_kernel<<<dim3(n / G, npair), 256, smc, s>>>(n, G, Z, tw, tw_n);
   fft_rows_kernel<<<nblk(nrows, R), 256, smr, s>>>(n, nrows, Z, tw, tw_n, 1, x, accumulate ? 1 : 0,
-                                                   1.0f / ((float)n * (float)n), nrhs, norms);
+                                                   1.0f / ((float)n * (float)n), nrhs, norms, n, (int64_t)n * n, 0);
 }
-void filter2d_prepare(int nrhs, int n, float2* Z, cudaStream_t s) {
-  if (nrhs & 1) cudaMemsetAsync(Z + (int64_t)(nrhs / 2) * n * n, 0, sizeof(float2) * (size_t)n * n, s);
+
+// ---------------------------------------------------------------- slab-sharded level filter
+// Rank `rank` of W holds rows [rank R, rank R + R) of every pair image: Zs [npair][R][n].
+//   1. row FFTs of the local rows (DIF, bit-reversed positions)
+//   2. pack: send chunk d = columns [d cw, d cw + cw) of every local row, [d][p][R][cw]
+//   3. all-to-all (caller): recv chunk q = rank q's rows of this rank's columns
+//   4. column FFT over i2 = (q, r), mask with the global column position, inverse (in place)
+//   5. all-to-all back (caller), unpack into Zs, inverse row FFTs + scale + update of x.
+void filter2d_slab_rows(int n, int npair, int R, float2* Zs, const float2* tw, int tw_n, cudaStream_t s) {
+  const int64_t nrows = (int64_t)npair * R;
+  const int RR = std::max(1, 4096 / n);
+  const size_t smr = sizeof(float2) * (size_t)RR * n;
+  cudaFuncSetAttribute(fft_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
+  fft_rows_kernel<<<nblk(nrows, RR), 256, smr, s>>>(n, nrows, Zs, tw, tw_n, 0, nullptr, 0, 1.f, 0, nullptr, R,
+                                                    (int64_t)R * n, 0);
+}
+void filter2d_slab_inverse(int n, int nrhs, int R, float2* Zs, const float2* tw, int tw_n, float* x, int64_t ximg,
+                           int64_t xoff, bool accumulate, const double* norms, cudaStream_t s) {
+  const int npair = (nrhs + 1) / 2;
+  const int64_t nrows = (int64_t)npair * R;
+  const int RR = std::max(1, 4096 / n);
+  const size_t smr = sizeof(float2) * (size_t)RR * n;
+  cudaFuncSetAttribute(fft_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
+  fft_rows_kernel<<<nblk(nrows, RR), 256, smr, s>>>(n, nrows, Zs, tw, tw_n, 1, x, accumulate ? 1 : 0,
+                                                    1.0f / ((float)n * (float)n), nrhs, norms, R, ximg, xoff);
+}
+
+void filter2d_slab_pack(int n, int npair, int R, int W, float2* Zs, float2* buf, bool unpack, cudaStream_t s) {
+  a2a_pack_kernel<<<nblk((int64_t)npair * R * n, 256), 256, 0, s>>>(n, npair, R, W, Zs, buf, unpack ? 1 : 0);
+}
+void filter2d_slab_cols(int n, int npair, int R, int W, int rank, float2* buf, const float2* tw, int tw_n,
+                        cudaStream_t s) {
+  const int cw = n / W;
+  const int G = std::min(cw, std::max(1, 16384 / n));
+  const size_t smc = sizeof(float2) * (size_t)n * G;
+  cudaFuncSetAttribute(fft_cols_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
+  fft_cols_slab_kernel<<<dim3(cw / G, npair), 256, smc, s>>>(n, G, R, cw, npair, buf, tw, tw_n, rank * cw);
+}
+void filter2d_prepare(int nrhs, int n, float2* Z, cudaStream_t s, int rows) {
+  if (rows <= 0) rows = n;
+  if (nrhs & 1) cudaMemsetAsync(Z + (int64_t)(nrhs / 2) * rows * n, 0, sizeof(float2) * (size_t)rows * n, s);
 }
 void real_to_complex(int nrhs, int64_t N, const float* x, float2* Z, cudaStream_t s) {
   real_to_complex_kernel<<<nblk((int64_t)nrhs * N, 256), 256, 0, s>>>(nrhs, N, x, Z);

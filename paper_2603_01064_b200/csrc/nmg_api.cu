@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "../../include/nmg.h"
+#include "comm.h"
 #include "kernels.h"
 
 using namespace nmg;
@@ -45,6 +46,20 @@ nmg_status fail(nmg_status st, const char* fmt, ...) {
   g_err = buf;
   return st;
 }
+
+}  // namespace
+
+nmg_status nmg::comm_fail(nmg_status st, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+namespace {
 
 #define NMG_CUDA(expr)                                                                     \
   do {                                                                                     \
@@ -252,10 +267,11 @@ nmg_status make_act_map(CUtensorMap* m, const float* p, int64_t rows, int Wp) {
 // a2 activations f16 [rhs][y][x][C] viewed as 5D {8 ch, x, C/8 chunk, y, rhs}; box
 // {8, 130, C/8, 1, 1} lands as the canonical no-swizzle K-major row buffer [C/8][130][8];
 // x = -1 and x = n are out of bounds and zero-filled (the conv's zero padding).
-nmg_status make_a2_map(CUtensorMap* m, const uint16_t* p, int n, int C, int64_t nrhs) {
+nmg_status make_a2_map(CUtensorMap* m, const uint16_t* p, int n, int C, int64_t nrhs, int hg = 0) {
   NMG_TRY(get_encoder());
-  cuuint64_t dims[5] = {8u, (cuuint64_t)n, (cuuint64_t)(C / 8), (cuuint64_t)n, (cuuint64_t)nrhs};
-  cuuint64_t strides[4] = {(cuuint64_t)C * 2u, 16u, (cuuint64_t)n * C * 2u, (cuuint64_t)n * n * C * 2u};
+  if (hg <= 0) hg = n;   // image height (slab mode: R + 2 halo rows)
+  cuuint64_t dims[5] = {8u, (cuuint64_t)n, (cuuint64_t)(C / 8), (cuuint64_t)hg, (cuuint64_t)nrhs};
+  cuuint64_t strides[4] = {(cuuint64_t)C * 2u, 16u, (cuuint64_t)n * C * 2u, (cuuint64_t)hg * n * C * 2u};
   cuuint32_t box[5] = {8u, 130u, (cuuint32_t)(C / 8), 1u, 1u};
   cuuint32_t es[5] = {1u, 1u, 1u, 1u, 1u};
   CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, (void*)p, dims, strides, box, es,
@@ -323,6 +339,7 @@ struct nmg_hierarchy {
   // 2D CNN on tcgen05 FP16x3 column-strip kernels (levels with n % 128 == 0, C = 32 / 48)
   bool conv_bf = false;
   int bf_C = 0, bf_chunk = 0;
+  int64_t bf_px = 0;                                     // pixels per RHS the a2 / q workspaces hold
   std::vector<float> strip_sc;                           // per level: S1, T1, S2, T2
   DevBuf<uint16_t> a2h, a2l;                             // [chunk][n][n][C] f16 hi / lo (scaled by S2)
   DevBuf<float> qbuf;                                    // [chunk][n][n][4]
@@ -362,6 +379,17 @@ struct nmg_hierarchy {
   };
   std::vector<GraphEntry> graphs;
   uint64_t g_clock = 0;
+  // slab-sharded single-system mode (nmg_create_hierarchy_slab)
+  bool slab = false;
+  nmg_comm* comm = nullptr;                              // not owned
+  int nw = 1, rank = 0, Ls = 0;                          // world; levels 0..Ls-1 sharded, the rest replicated
+  static constexpr int HS = 4;                           // halo rows (the 4-layer 3x3 CNN's reach)
+  std::vector<int> R;                                    // slab rows per sharded level
+  std::vector<std::unique_ptr<DevBuf<float>>> sy, sx, sr, sb;   // [B][R + 2 HS][n_l] per sharded level
+  std::vector<CUtensorMap> mKBhS, mKBlS;                 // B_l hi/lo maps, box rows kron_tile_n(R_l)
+  DevBuf<float> tsend, trecv, hsend, hrecv, csend, crecv;
+  DevBuf<double> t64send, t64recv, dscratch, ssum, rsum, ysq;
+  DevBuf<float2> zs, za, zb;
   ~nmg_hierarchy() {
     for (auto e : ev_pool) cudaEventDestroy(e);
     for (auto& g : graphs) if (g.exec) cudaGraphExecDestroy(g.exec);
@@ -753,7 +781,209 @@ nmg_status cycle_level_2d(nmg_hierarchy* h, int l, int nrhs, cudaStream_t s) {
   return NMG_OK;
 }
 
+// ---------------------------------------------------------------- slab-sharded mode (§8(e))
+// Every sharded level keeps its vectors as this rank's slab of R_l rows plus HS halo rows per
+// side, [b][R_l + 2 HS][n_l]; "global row g" of image b lives at slab + b img + (HS - r0 + g) n.
+inline int64_t slab_img(const nmg_hierarchy* h, int l) { return (int64_t)(h->R[l] + 2 * h->HS) * h->n[l]; }
+
+// fill the halo rows of x (level l) from the neighbouring ranks (zeros at the image borders)
+nmg_status halo_exchange(nmg_hierarchy* h, int l, int nrhs, float* x, cudaStream_t s) {
+  const int n = h->n[l], R = h->R[l], H = h->HS;
+  { Prof p(h, NMG_K_MISC, s); halo_pack(nrhs, n, R, H, x, h->hsend.p, s); }
+  NMG_TRY(check_launch(h));
+  NMG_TRY(h->comm->all_gather(h->hsend.p, h->hrecv.p, sizeof(float) * (size_t)2 * nrhs * H * n, s));
+  { Prof p(h, NMG_K_MISC, s); halo_unpack(nrhs, n, R, H, h->rank, h->nw, h->hrecv.p, x, s); }
+  return check_launch(h);
+}
+
+// recv = [W][rows_per_rank] blocks of `width` elements per row -> full rows: dst row m, columns
+// q w .. q w + w - 1 = rank q's block row m  (unpack of an all-gathered slab-major array)
+template <typename T>
+nmg_status unpack_gathered(nmg_hierarchy* h, const T* recv, T* dst, int64_t rows, int64_t width, int64_t dpitch,
+                           cudaStream_t s) {
+  for (int q = 0; q < h->nw; ++q)
+    NMG_CUDA(cudaMemcpy2DAsync(dst + q * width, sizeof(T) * dpitch, recv + (int64_t)q * rows * width, sizeof(T) * width,
+                               sizeof(T) * width, rows, cudaMemcpyDeviceToDevice, s));
+  return NMG_OK;
+}
+
+// D = Cin -/+ A_l X on the slab (X's halo rows must hold the neighbours' rows when hb > 0):
+// pass 1 T = C_l X[:, slab] (local), all-gather T, pass 2 D[:, slab] = T B_l[slab]^T + alpha QXQ^T
+nmg_status apply_slab(nmg_hierarchy* h, int l, int nrhs, const float* X, const float* Cin, float* D, cudaStream_t s,
+                      bool negate = true) {
+  const int n = h->n[l], R = h->R[l], H = h->HS;
+  CUtensorMap mx;
+  NMG_TRY(make_map(&mx, X, (int64_t)nrhs * (R + 2 * H), n, tc_gemm_block_m()));
+  KronArgs k{};
+  k.M = nrhs * (R + 2 * H); k.n = n; k.mode = KRON_T; k.D = h->tsend.p;
+  k.R = R; k.H = H; k.r0 = h->rank * R; k.img = slab_img(h, l);
+  { Prof p(h, NMG_K_GEMM32, s); kron_tc(&mx, &h->mKCh[l], &h->mKCl[l], k, h->num_sms, s); }
+  NMG_TRY(check_launch(h));
+  NMG_TRY(h->comm->all_gather(h->tsend.p, h->trecv.p, sizeof(float) * (size_t)nrhs * n * R, s));
+  NMG_TRY(unpack_gathered<float>(h, h->trecv.p, h->tth[l]->p, (int64_t)nrhs * n, R, n, s));
+  KronArgs k2{};
+  k2.M = nrhs * n; k2.n = n; k2.mode = KRON_RESID; k2.D = D; k2.X = X; k2.Cin = Cin; k2.Q = h->Q32[l]->p;
+  k2.hb = h->qhb[l]; k2.alpha = (float)h->d.alpha; k2.negate = negate;
+  k2.R = R; k2.H = H; k2.r0 = h->rank * R; k2.img = slab_img(h, l);
+  { Prof p(h, NMG_K_GEMM32, s); kron_tc(&h->mTh[l], &h->mKBhS[l], &h->mKBlS[l], k2, h->num_sms, s); }
+  return check_launch(h);
+}
+
+// x = x* + F'(||b|| N(b/||b||)) on the slab; b's halo rows are filled here (CNN reach 4 rows)
+nmg_status smooth_slab(nmg_hierarchy* h, int l, int nrhs, float* b, float* x, bool accumulate, cudaStream_t s) {
+  const int n = h->n[l], R = h->R[l], H = h->HS, C = h->arch.channels;
+  const int64_t img = slab_img(h, l);
+  if (!(h->conv_bf && h->bf_C == C && strip_level(n)))
+    return fail(NMG_ERR_UNSUPPORTED, "slab mode needs the strip-kernel CNN (C = 32 / 48, n %% 128 == 0)");
+  // ||b|| over the whole image: local sums of squares, summed over the ranks (fixed order)
+  {
+    const int chunks = (int)std::min<int64_t>(64, std::max<int64_t>(1, (int64_t)R * n / 4096));
+    { Prof p(h, NMG_K_SMOOTH, s); sumsq_f32(nrhs, (int64_t)R * n, b, img, (int64_t)H * n, h->spart.p, chunks, h->snorm.p, s); }
+    NMG_TRY(check_launch(h));
+    NMG_TRY(h->comm->sum_f64(h->snorm.p, nrhs, h->dscratch.p, s));
+    { Prof p(h, NMG_K_MISC, s); sqrt_inplace(nrhs, h->snorm.p, s); }
+  }
+  NMG_TRY(halo_exchange(h, l, nrhs, b, s));
+  const bool filt = h->d.level_filter != 0;
+  if (filt) filter2d_prepare(nrhs, n, h->zs.p, s, R);
+  const float* P = h->W[l]->p;
+  const float* b1 = P + C * 9 + C + C * C * 9;
+  const float* b2 = b1 + C + C * C * 9;
+  const float* w3 = b2 + C;
+  const float* b3 = w3 + C * 9;
+  const size_t plane = (size_t)9 * C * C;
+  const uint16_t* wb = h->WB[l]->p;
+  const float* sc = &h->strip_sc[(size_t)6 * l];
+  const int hg = R + 2 * H;
+  // RHS per CNN chunk: the a2 / q workspaces hold bf_chunk images of bf_px pixels
+  const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(h->bf_chunk, h->bf_chunk * h->bf_px / ((int64_t)hg * n)));
+  CUtensorMap m2h, m2l;
+  NMG_TRY(make_a2_map(&m2h, h->a2h.p, n, C, chunk, hg));
+  NMG_TRY(make_a2_map(&m2l, h->a2l.p, n, C, chunk, hg));
+  for (int c0 = 0; c0 < nrhs; c0 += chunk) {
+    const int cnt = std::min(chunk, nrhs - c0);
+    const int64_t off = (int64_t)c0 * img;
+    StripArgs a{};
+    a.n = n; a.h = hg; a.nrhs = cnt; a.C = C; a.ysplit = strip_ysplit(n, cnt, h->num_sms, hg);
+    a.ylo = h->rank == 0 ? H : 0;                       // the global image border is zero padding
+    a.yhi = h->rank == h->nw - 1 ? hg - H : hg;
+    a.b = b + off; a.norms = h->snorm.p + c0;
+    a.w_in = P; a.w_out = w3;
+    a.wh = wb; a.wl = wb + plane; a.bias = b1;
+    a.in_scale = sc[0]; a.out_scale = sc[2]; a.d_scale = 1.0f / (sc[0] * sc[1]);
+    a.out_h = h->a2h.p; a.out_l = h->a2l.p; a.q = h->qbuf.p;
+    { Prof p(h, NMG_K_SMOOTH, s); strip_l12(a, h->num_sms, s); }
+    a.wh = wb + 2 * plane; a.wl = wb + 3 * plane; a.bias = b2;
+    a.d_scale = 1.0f / (sc[2] * sc[3]);
+    a.w4 = wb + 4 * plane; a.a3_scale = sc[4]; a.d4_scale = 1.0f / (sc[4] * sc[5]);
+    { Prof p(h, NMG_K_SMOOTH, s); strip_l34(&m2h, &m2l, a, h->num_sms, s); }
+    { Prof p(h, NMG_K_SMOOTH, s);
+      strip_combine(n, cnt, h->qbuf.p, a.norms, b3, filt ? h->zs.p : nullptr, c0, x + off, accumulate, s, hg, H); }
+    NMG_TRY(check_launch(h));
+  }
+  if (filt) {
+    // rows local; columns after an all-to-all transpose; back; inverse rows + update
+    const int npair = (nrhs + 1) / 2;
+    const size_t chunk = sizeof(float2) * (size_t)npair * R * (n / h->nw);
+    { Prof p(h, NMG_K_SMOOTH, s); filter2d_slab_rows(n, npair, R, h->zs.p, h->tw.p, h->tw_n, s); }
+    { Prof p(h, NMG_K_MISC, s); filter2d_slab_pack(n, npair, R, h->nw, h->zs.p, h->za.p, false, s); }
+    NMG_TRY(check_launch(h));
+    NMG_TRY(h->comm->all_to_all(h->za.p, h->zb.p, chunk, s));
+    { Prof p(h, NMG_K_SMOOTH, s); filter2d_slab_cols(n, npair, R, h->nw, h->rank, h->zb.p, h->tw.p, h->tw_n, s); }
+    NMG_TRY(check_launch(h));
+    NMG_TRY(h->comm->all_to_all(h->zb.p, h->za.p, chunk, s));
+    { Prof p(h, NMG_K_MISC, s); filter2d_slab_pack(n, npair, R, h->nw, h->zs.p, h->za.p, true, s); }
+    { Prof p(h, NMG_K_SMOOTH, s);
+      filter2d_slab_inverse(n, nrhs, R, h->zs.p, h->tw.p, h->tw_n, x, img, (int64_t)H * n, accumulate, h->snorm.p, s); }
+    NMG_TRY(check_launch(h));
+  }
+  return NMG_OK;
+}
+
+nmg_status cycle_level_2d(nmg_hierarchy* h, int l, int nrhs, cudaStream_t s);
+
+// NMGF(0, y_l) on the slab of sharded level l: input sy[l] (own rows), output sx[l] (own rows)
+nmg_status cycle_slab(nmg_hierarchy* h, int l, int nrhs, cudaStream_t s) {
+  const int n = h->n[l], R = h->R[l], H = h->HS, r0 = h->rank * R;
+  const int64_t img = slab_img(h, l);
+  float* y = h->sy[l]->p;
+  float* x = h->sx[l]->p;
+  float* r = h->sr[l]->p;
+  float* b = h->sb[l]->p;
+  const bool hx = h->qhb[l] > 0;   // the mass stencil reads x rows +- hb
+  if (h->d.nu1 >= 1) {
+    NMG_TRY(smooth_slab(h, l, nrhs, y, x, false, s));
+    for (int k = 1; k < h->d.nu1; ++k) {
+      if (hx) NMG_TRY(halo_exchange(h, l, nrhs, x, s));
+      NMG_TRY(apply_slab(h, l, nrhs, x, y, b, s));
+      NMG_TRY(smooth_slab(h, l, nrhs, b, x, true, s));
+    }
+    if (hx) NMG_TRY(halo_exchange(h, l, nrhs, x, s));
+    NMG_TRY(apply_slab(h, l, nrhs, x, y, r, s));
+  } else {
+    NMG_CUDA(cudaMemsetAsync(x, 0, sizeof(float) * (size_t)nrhs * img, s));
+    NMG_CUDA(cudaMemcpyAsync(r, y, sizeof(float) * (size_t)nrhs * img, cudaMemcpyDeviceToDevice, s));
+  }
+  NMG_TRY(halo_exchange(h, l, nrhs, r, s));   // full weighting reads fine rows 2 j2 - 1 .. 2 j2 + 2
+  const int nc = n / 2, Rc = R / 2, r0c = r0 / 2;
+  const int64_t foff = (int64_t)(H - r0) * n;
+  if (l + 1 < h->Ls) {
+    { Prof p(h, NMG_K_TRANSFER, s);
+      restrict_slab(nrhs, nc, Rc, r0c, r, img, foff, h->sy[l + 1]->p, slab_img(h, l + 1), (int64_t)H * nc, s); }
+    NMG_TRY(check_launch(h));
+    NMG_TRY(cycle_slab(h, l + 1, nrhs, s));
+    NMG_TRY(halo_exchange(h, l + 1, nrhs, h->sx[l + 1]->p, s));
+    { Prof p(h, NMG_K_TRANSFER, s);
+      prolong_slab(nrhs, nc, R, r0, h->sx[l + 1]->p, slab_img(h, l + 1), (int64_t)(H - r0c) * nc, x, img,
+                   (int64_t)H * n, s); }
+  } else {
+    // replicated coarse sub-cycle: gather the restricted RHS, run the levels >= l + 1 on every rank
+    const int Rq = nc / h->nw;
+    { Prof p(h, NMG_K_TRANSFER, s);
+      restrict_slab(nrhs, nc, Rq, h->rank * Rq, r, img, foff, h->csend.p, (int64_t)Rq * nc, 0, s); }
+    NMG_TRY(check_launch(h));
+    NMG_TRY(h->comm->all_gather(h->csend.p, h->crecv.p, sizeof(float) * (size_t)nrhs * Rq * nc, s));
+    NMG_TRY(unpack_gathered<float>(h, h->crecv.p, h->wy[l + 1]->p, nrhs, (int64_t)Rq * nc, (int64_t)nc * nc, s));
+    NMG_TRY(cycle_level_2d(h, l + 1, nrhs, s));
+    { Prof p(h, NMG_K_TRANSFER, s);
+      prolong_slab(nrhs, nc, R, r0, h->wx[l + 1]->p, (int64_t)nc * nc, 0, x, img, (int64_t)H * n, s); }
+  }
+  NMG_TRY(check_launch(h));
+  for (int k = 0; k < h->d.nu2; ++k) {
+    if (hx) NMG_TRY(halo_exchange(h, l, nrhs, x, s));
+    NMG_TRY(apply_slab(h, l, nrhs, x, y, b, s));
+    NMG_TRY(smooth_slab(h, l, nrhs, b, x, true, s));
+  }
+  return NMG_OK;
+}
+
+// fp64 outer residual on the slab: pass 1 T = C X[:, slab] (DMMA), all-gather T, pass 2
+// r[:, slab] = y - (T B[slab]^T + alpha x); r32 -> sy[0] (own rows), ||r||^2 partials -> part
+nmg_status outer_residual_slab(nmg_hierarchy* h, int nrhs, const double* y, const double* x, double* r64,
+                               bool want_part, cudaStream_t s) {
+  const int n = h->n[0], R = h->R[0], H = h->HS, r0 = h->rank * R;
+  Gemm64Args g{};
+  g.M = nrhs * R; g.N = n; g.K = n;
+  g.X = x; g.ldx = n; g.W = h->C64.p; g.ldw = n;
+  g.Y = nullptr; g.r32 = nullptr; g.r64 = h->t64send.p; g.part = nullptr; g.negate = false;
+  g.tblock = n; g.tb_R = R; g.tb_S = R; g.tb_img = (int64_t)n * R;
+  { Prof p(h, NMG_K_GEMM64, s); gemm_f64(g, s); }
+  NMG_TRY(check_launch(h));
+  NMG_TRY(h->comm->all_gather(h->t64send.p, h->t64recv.p, sizeof(double) * (size_t)nrhs * n * R, s));
+  NMG_TRY(unpack_gathered<double>(h, h->t64recv.p, h->T64.p, (int64_t)nrhs * n, R, n, s));
+  Gemm64Args q{};
+  q.M = nrhs * n; q.N = R; q.K = n;
+  q.X = h->T64.p; q.ldx = n; q.W = h->B64.p + (int64_t)r0 * n; q.ldw = n;
+  q.Y = y; q.r32 = h->sy[0]->p; q.r64 = r64; q.part = want_part ? h->part.p : nullptr;
+  q.negate = true; q.ax = x; q.alpha = h->d.alpha;
+  q.tblock = n; q.tb_R = n; q.tb_S = n; q.tb_img = (int64_t)R * n;
+  q.r32_img = slab_img(h, 0); q.r32_off = (int64_t)H * n;
+  { Prof p(h, NMG_K_GEMM64, s); gemm_f64(q, s); }
+  return check_launch(h);
+}
+
 nmg_status inner_cycle(nmg_hierarchy* h, int nrhs, cudaStream_t s) {
+  if (h->slab) return cycle_slab(h, 0, nrhs, s);
   if (h->d.dim == 1) return cycle_level_1d(h, 0, nrhs, s);
   return cycle_level_2d(h, 0, nrhs, s);
 }
@@ -761,6 +991,7 @@ nmg_status inner_cycle(nmg_hierarchy* h, int nrhs, cudaStream_t s) {
 // fp64 residual at level 1: r32 = y - A x -> wy[0]; optional r64; norm partials -> part
 nmg_status outer_residual(nmg_hierarchy* h, int nrhs, const double* y, const double* x, double* r64,
                           bool want_part, cudaStream_t s) {
+  if (h->slab) return outer_residual_slab(h, nrhs, y, x, r64, want_part, s);
   if (h->d.dim == 2) {
     const int n = h->n[0];
     Gemm64Args g{};
@@ -806,6 +1037,41 @@ nmg_status outer_residual(nmg_hierarchy* h, int nrhs, const double* y, const dou
   return check_launch(h);
 }
 
+// ||y|| per RHS (slab mode: local sums of squares summed over the ranks)
+nmg_status ynorms(nmg_hierarchy* h, int nrhs, const double* y, cudaStream_t s) {
+  if (!h->slab) {
+    { Prof p(h, NMG_K_MISC, s); row_norms_f64(nrhs, (int)h->N[0], y, h->N[0], h->ynorm.p, h->ywork.p, s); }
+    return check_launch(h);
+  }
+  { Prof p(h, NMG_K_MISC, s); sumsq_f64(nrhs, (int64_t)h->R[0] * h->n[0], y, h->ywork.p, h->ysq.p, s); }
+  NMG_TRY(check_launch(h));
+  return h->comm->sum_f64(h->ysq.p, nrhs, h->dscratch.p, s);
+}
+// relres = ||r|| / ||y|| from the outer residual's partials; active = relres > tol
+nmg_status relres_fin(nmg_hierarchy* h, int nrhs, double tol, uint8_t* active, double* relres, cudaStream_t s) {
+  if (!h->slab) {
+    { Prof p(h, NMG_K_MISC, s); relres_finalize(nrhs, h->ntiles, h->part.p, h->ynorm.p, relres, tol, active, s, h->rows_per_rhs); }
+    return check_launch(h);
+  }
+  const int64_t cnt = (int64_t)gemm_f64_ntiles(h->R[0]) * h->n[0];
+  { Prof p(h, NMG_K_MISC, s); part_sums(nrhs, cnt, h->part.p, h->rsum.p, s); }
+  NMG_TRY(check_launch(h));
+  NMG_TRY(h->comm->sum_f64(h->rsum.p, nrhs, h->dscratch.p, s));
+  { Prof p(h, NMG_K_MISC, s); relres_sums(nrhs, h->rsum.p, h->ysq.p, relres, tol, active, s); }
+  return check_launch(h);
+}
+// x += inner correction (fp64)
+nmg_status outer_update(nmg_hierarchy* h, int nrhs, double* x, const uint8_t* active, cudaStream_t s) {
+  if (!h->slab) {
+    const int64_t N = h->N[0];
+    { Prof p(h, NMG_K_MISC, s); update_x(nrhs, (int)N, x, N, h->wx[0]->p, N, active, s); }
+    return check_launch(h);
+  }
+  { Prof p(h, NMG_K_MISC, s);
+    update_slab(nrhs, (int64_t)h->R[0] * h->n[0], x, h->sx[0]->p, slab_img(h, 0), (int64_t)h->HS * h->n[0], active, s); }
+  return check_launch(h);
+}
+
 nmg_status check_ready(nmg_hierarchy* h, int nrhs) {
   if (!h) return fail(NMG_ERR_INVALID_ARG, "null handle");
   if (h->poisoned) return fail(NMG_ERR_CUDA, "handle poisoned by an earlier CUDA error");
@@ -819,13 +1085,10 @@ nmg_status check_ready(nmg_hierarchy* h, int nrhs) {
 // one outer step: residual (+relres/active), inner cycle, masked update
 nmg_status outer_step(nmg_hierarchy* h, int nrhs, const double* y, double* x, double tol, bool use_active,
                       cudaStream_t s) {
-  const int64_t N = h->N[0];
   NMG_TRY(outer_residual(h, nrhs, y, x, nullptr, true, s));
-  { Prof p(h, NMG_K_MISC, s); relres_finalize(nrhs, h->ntiles, h->part.p, h->ynorm.p, h->relres.p, tol, h->active.p, s, h->rows_per_rhs); }
-  NMG_TRY(check_launch(h));
+  NMG_TRY(relres_fin(h, nrhs, tol, h->active.p, h->relres.p, s));
   NMG_TRY(inner_cycle(h, nrhs, s));
-  { Prof p(h, NMG_K_MISC, s); update_x(nrhs, (int)N, x, N, h->wx[0]->p, N, use_active ? h->active.p : nullptr, s); }
-  return check_launch(h);
+  return outer_update(h, nrhs, x, use_active ? h->active.p : nullptr, s);
 }
 
 nmg_status debug_2d(nmg_hierarchy* h, int l, int op, int nrhs, const float* fin, float* fout, cudaStream_t s) {
@@ -880,10 +1143,10 @@ namespace {
 // small configs and coarse levels).
 nmg_status graph_cycle(nmg_hierarchy* h, int nrhs, const double* y, double* x, cudaStream_t s) {
   auto body = [&]() -> nmg_status {
-    { Prof p(h, NMG_K_MISC, s); row_norms_f64(nrhs, (int)h->N[0], y, h->N[0], h->ynorm.p, h->ywork.p, s); }
+    NMG_TRY(ynorms(h, nrhs, y, s));
     return outer_step(h, nrhs, y, x, -1.0, false, s);
   };
-  if (!h->use_graph || s == nullptr || h->prof_on) return body();
+  if (!h->use_graph || h->slab || s == nullptr || h->prof_on) return body();
   nmg_hierarchy::GraphEntry* g = nullptr;
   for (auto& e : h->graphs)
     if (e.nrhs == nrhs && e.y == y && e.x == x && e.s == s) g = &e;
@@ -1298,6 +1561,69 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
   return NMG_OK;
 }
 
+nmg_status nmg_create_hierarchy_slab(const nmg_problem_desc* desc, const double* factors, nmg_comm* comm,
+                                     nmg_hierarchy** out) {
+  g_err.clear();
+  if (!desc || !factors || !comm || !out) return fail(NMG_ERR_INVALID_ARG, "null argument");
+  *out = nullptr;
+  if (desc->dim != 2) return fail(NMG_ERR_UNSUPPORTED, "the slab-sharded mode is 2D only");
+  const int W = comm->world;
+  if (desc->n % W != 0 || desc->n / W < 32 || (desc->n / W) % 32 != 0)
+    return fail(NMG_ERR_UNSUPPORTED, "slab mode needs n / world to be a multiple of 32 (n = %d, world = %d)", desc->n, W);
+  nmg_hierarchy* raw = nullptr;
+  NMG_TRY(nmg_create_hierarchy(desc, factors, &raw));
+  std::unique_ptr<nmg_hierarchy> h(raw);
+  if (!h->use_kron) return fail(NMG_ERR_UNSUPPORTED, "slab mode needs the tcgen05 Kronecker apply (NMG_KRON != 0)");
+  h->slab = true;
+  h->comm = comm;
+  h->nw = W;
+  h->rank = comm->rank;
+  h->use_graph = false;
+  // sharded levels: smoothed levels whose slab keeps >= 32 rows and whose width the strip CNN serves
+  h->Ls = 0;
+  for (int l = 0; l < h->L - 1; ++l) {
+    const int nl = h->n[l];
+    if (nl % W != 0 || nl / W < 32 || nl % 128 != 0 || !kron_supported(nl, h->qhb[l]) || (nl / 2) % W != 0) break;
+    h->R.push_back(nl / W);
+    h->Ls = l + 1;
+  }
+  if (h->Ls == 0) return fail(NMG_ERR_UNSUPPORTED, "no level can be sharded (n = %d, world = %d)", desc->n, W);
+  const size_t B = (size_t)h->d.max_rhs;
+  const int H = h->HS;
+  const int n0 = h->n[0], R0 = h->R[0];
+  h->mKBhS.resize(h->Ls); h->mKBlS.resize(h->Ls);
+  for (int l = 0; l < h->Ls; ++l) {
+    const int nl = h->n[l], R = h->R[l];
+    for (auto* v : {&h->sy, &h->sx, &h->sr, &h->sb}) {
+      v->emplace_back(new DevBuf<float>());
+      NMG_TRY(v->back()->alloc(B * (size_t)(R + 2 * H) * nl));
+      NMG_CUDA(cudaMemset(v->back()->p, 0, sizeof(float) * v->back()->n));
+    }
+    NMG_TRY(make_map(&h->mKBhS[l], h->B32h[l]->p, nl, nl, kron_tile_n(R)));
+    NMG_TRY(make_map(&h->mKBlS[l], h->B32l[l]->p, nl, nl, kron_tile_n(R)));
+  }
+  NMG_TRY(h->tsend.alloc(B * n0 * R0));
+  NMG_TRY(h->trecv.alloc(B * n0 * n0));
+  NMG_TRY(h->t64send.alloc(B * n0 * R0));
+  NMG_TRY(h->t64recv.alloc(B * n0 * n0));
+  NMG_TRY(h->hsend.alloc(2 * B * H * n0));
+  NMG_TRY(h->hrecv.alloc((size_t)W * 2 * B * H * n0));
+  const size_t np = (B + 1) / 2;
+  NMG_TRY(h->zs.alloc(np * R0 * n0));
+  NMG_TRY(h->za.alloc(np * R0 * n0));
+  NMG_TRY(h->zb.alloc(np * R0 * n0));
+  const int nq = h->n[h->Ls];
+  NMG_TRY(h->csend.alloc(B * (nq / W) * nq));
+  NMG_TRY(h->crecv.alloc(B * nq * nq));
+  NMG_TRY(h->dscratch.alloc((size_t)W * B));
+  NMG_TRY(h->ssum.alloc(B));
+  NMG_TRY(h->rsum.alloc(B));
+  NMG_TRY(h->ysq.alloc(B));
+  NMG_CUDA(cudaDeviceSynchronize());
+  *out = h.release();
+  return NMG_OK;
+}
+
 nmg_status nmg_load_smoother_weights(nmg_hierarchy* h, int32_t level, const nmg_cnn_arch* arch,
                                      const float* params, size_t n_params) {
   g_err.clear();
@@ -1404,13 +1730,15 @@ nmg_status nmg_load_smoother_weights(nmg_hierarchy* h, int32_t level, const nmg_
         for (int l = 0; l < h->L - 1; ++l)
           if (strip_level(h->n[l])) nmax = std::max(nmax, h->n[l]);
         if (nmax > 0) {
-          const int64_t px = (int64_t)nmax * nmax;
+          int64_t px = (int64_t)nmax * nmax;
+          if (h->slab) px = std::max<int64_t>(px, (int64_t)(h->R[0] + 2 * h->HS) * h->n[0]);   // halo'd slab image
           const int64_t per = px * C * 4 + px * 16;                     // bytes per RHS
           const int64_t budget = (int64_t)16 << 30;
           const int64_t B = h->d.max_rhs;
           const int64_t cmax = std::max<int64_t>(1, std::min<int64_t>(B, budget / per));
           const int64_t nch = (B + cmax - 1) / cmax;
           h->bf_chunk = (int)((B + nch - 1) / nch);
+          h->bf_px = px;
           NMG_TRY(h->a2h.alloc((size_t)h->bf_chunk * px * C));
           NMG_TRY(h->a2l.alloc((size_t)h->bf_chunk * px * C));
           NMG_TRY(h->qbuf.alloc((size_t)h->bf_chunk * px * 4));
@@ -1513,9 +1841,8 @@ nmg_status nmg_residual(nmg_hierarchy* h, int32_t nrhs, const double* y, const d
   cudaStream_t s = (cudaStream_t)stream;
   NMG_TRY(outer_residual(h, nrhs, y, x, r, relres != nullptr, s));
   if (relres) {
-    row_norms_f64(nrhs, (int)h->N[0], y, h->N[0], h->ynorm.p, h->ywork.p, s);
-    relres_finalize(nrhs, h->ntiles, h->part.p, h->ynorm.p, relres, -1.0, nullptr, s, h->rows_per_rhs);
-    h->launches += 2;
+    NMG_TRY(ynorms(h, nrhs, y, s));
+    NMG_TRY(relres_fin(h, nrhs, -1.0, nullptr, relres, s));
   }
   return check_launch(h);
 }
@@ -1546,11 +1873,9 @@ nmg_status nmg_solve(nmg_hierarchy* h, int32_t nrhs, const double* y, double* x,
   NMG_CUDA(cudaEventCreate(&e0));
   NMG_CUDA(cudaEventCreate(&e1));
   NMG_CUDA(cudaEventRecord(e0, s));
-  row_norms_f64(nrhs, (int)N, y, N, h->ynorm.p, h->ywork.p, s);
+  NMG_TRY(ynorms(h, nrhs, y, s));
   NMG_TRY(outer_residual(h, nrhs, y, x, nullptr, true, s));
-  relres_finalize(nrhs, h->ntiles, h->part.p, h->ynorm.p, h->relres.p, tol, h->active.p, s, h->rows_per_rhs);
-  h->launches += 2;
-  NMG_TRY(check_launch(h));
+  NMG_TRY(relres_fin(h, nrhs, tol, h->active.p, h->relres.p, s));
   nmg_status st = NMG_OK;
   int tau = 0;
   for (;; ++tau) {
@@ -1569,14 +1894,10 @@ nmg_status nmg_solve(nmg_hierarchy* h, int32_t nrhs, const double* y, double* x,
     }
     if (st != NMG_OK || nact == 0 || tau == max_cycles) break;
     NMG_TRY(inner_cycle(h, nrhs, s));
-    update_x(nrhs, (int)N, x, N, h->wx[0]->p, N, h->active.p, s);
-    h->launches++;
-    NMG_TRY(check_launch(h));
+    NMG_TRY(outer_update(h, nrhs, x, h->active.p, s));
     for (int b = 0; b < nrhs; ++b) if (act[b]) cyc[b] = tau + 1;
     NMG_TRY(outer_residual(h, nrhs, y, x, nullptr, true, s));
-    relres_finalize(nrhs, h->ntiles, h->part.p, h->ynorm.p, h->relres.p, tol, h->active.p, s, h->rows_per_rhs);
-    h->launches++;
-    NMG_TRY(check_launch(h));
+    NMG_TRY(relres_fin(h, nrhs, tol, h->active.p, h->relres.p, s));
   }
   NMG_CUDA(cudaEventRecord(e1, s));
   NMG_CUDA(cudaEventSynchronize(e1));
@@ -1601,6 +1922,7 @@ nmg_status nmg_vcycles_host(nmg_hierarchy* h, int32_t nrhs, const double* y_host
   NMG_TRY(check_ready(h, nrhs));
   if (nrhs == 0) return NMG_OK;
   if (!y_host || !x_host || cycles < 0) return fail(NMG_ERR_INVALID_ARG, "bad arguments");
+  if (h->slab) return fail(NMG_ERR_UNSUPPORTED, "nmg_vcycles_host: not available on a slab-sharded handle");
   cudaStream_t s = (cudaStream_t)stream;
   const size_t cnt = (size_t)h->d.max_rhs * h->N[0];
   if (!h->hy.p) { NMG_TRY(h->hy.alloc(cnt)); NMG_TRY(h->hx.alloc(cnt)); }
@@ -1653,6 +1975,7 @@ nmg_status nmg_debug_level_op(nmg_hierarchy* h, int32_t level, int32_t op, int32
                               void* stream) {
   g_err.clear();
   if (!h) return fail(NMG_ERR_INVALID_ARG, "null handle");
+  if (h->slab) return fail(NMG_ERR_UNSUPPORTED, "nmg_debug_level_op: not available on a slab-sharded handle");
   if (level < 1 || level > h->L) return fail(NMG_ERR_INVALID_ARG, "level %d outside 1..%d", level, h->L);
   if (nrhs < 0 || nrhs > h->d.max_rhs) return fail(NMG_ERR_INVALID_ARG, "bad nrhs");
   if (nrhs == 0) return NMG_OK;
