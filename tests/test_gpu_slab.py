@@ -155,3 +155,32 @@ def test_slab_homogeneity_bitwise(prob2):
     res = run_ranks(2, CFG2, f, W, y, body)
     for r in range(2):
         assert np.array_equal(res[r][0], res[r][1])
+
+
+def test_slab_full_config4_w8_vs_unsharded():
+    """BASELINE config 4 at full size (1024^2, 7 levels) over 8 emulated ranks (slabs of 128,
+    64 and 32 rows; replicated from 128^2 down): one cycle equals the unsharded GPU path."""
+    cfg = ni.CONFIGS[4].replace(nrhs=2)
+    f = ni.operator_factors(cfg)
+    W = weights_for(cfg, "seed")
+    y, _ = ni.make_rhs(cfg, f, cfg.alpha, nrhs=2)
+
+    def body(r, h, yd):
+        xd = torch.zeros_like(yd)
+        h.vcycle(yd, xd)
+        rr = torch.zeros(yd.shape[0], dtype=torch.float64, device=DEV)
+        h.residual(yd, xd, None, rr)
+        return xd.cpu().numpy(), rr.cpu().numpy()
+
+    res = run_ranks(8, cfg, f, W, y, body)
+    xs = join_slabs([res[r][0] for r in range(8)], cfg.n)
+    h = gpu_hierarchy(cfg, f, W, max_rhs=2)
+    yd = torch.tensor(y, dtype=torch.float64, device=DEV)
+    xd = torch.zeros_like(yd)
+    h.vcycle(yd, xd)
+    rr = torch.zeros(2, dtype=torch.float64, device=DEV)
+    h.residual(yd, xd, None, rr)
+    d = rel_l2(xs, xd.cpu().numpy().reshape(xs.shape))
+    print("slab W=8 vs unsharded: x rel diff", d, "relres", res[0][1], rr.cpu().numpy())
+    assert d < 1e-5
+    assert np.allclose(res[0][1], rr.cpu().numpy(), rtol=1e-5)
