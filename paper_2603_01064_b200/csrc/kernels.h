@@ -57,6 +57,13 @@ struct OzakiArgs {
   double* part;                          // may be null; [M][N/64]
   const int* ex;                         // [M] row exponents of X
   const int* ew;                         // [N] row exponents of W
+  // 2D Kronecker passes: tblock > 0 = transposed store within tblock x tblock blocks (Y, ax,
+  // r32, r64 all at that location); plus: store +X W^T (pass 1) instead of Y - X W^T;
+  // ax: optional -alpha ax term (pass 2)
+  int tblock = 0;
+  bool plus = false;
+  const double* ax = nullptr;
+  double alpha = 0.0;
 };
 int ozaki_digits();
 // digit planes [S][plane / K rows][K]: plane = (rows allocated per plane) * K

@@ -6,6 +6,8 @@
 //   * norms_f32                  : ||B_l||_2 Frobenius per RHS in fp64 (R10)
 //   * cnn2d_kernel               : fused 4-layer 3x3 CNN smoother N_theta (R7), FFMA
 //   * fft2d_*                    : level filter hat F'_l = Re(IDFT2(M' (.) DFT2(.)))
+#include <cstdlib>
+
 #include "common.cuh"
 #include "fft.cuh"
 #include "kernels.h"
@@ -432,7 +434,11 @@ void filter2d(int nrhs, int n, float2* Z, const float2* tw, int tw_n, float* x, 
   cudaFuncSetAttribute(fft_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
   fft_rows_kernel<<<nblk(nrows, R), 256, smr, s>>>(n, nrows, Z, tw, tw_n, 0, nullptr, 0, 1.f, nrhs, nullptr, n,
                                                    (int64_t)n * n, 0);
-  const int G = std::min(n, std::max(1, 16384 / n));
+  static const int cols_elems = [] {   // complex elements per column-pass CTA (dev knob)
+    const char* e = std::getenv("NMG_FFT_COLS_KB");
+    return (e ? std::atoi(e) : 32) * 1024 / 8;
+  }();
+  const int G = std::min(n, std::max(1, cols_elems / n));
   const size_t smc = sizeof(float2) * (size_t)n * G;
   cudaFuncSetAttribute(fft_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
   fft_cols_kernel<<<dim3(n / G, npair), 256, smc, s>>>(n, G, Z, tw, tw_n);

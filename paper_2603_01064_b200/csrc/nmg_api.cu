@@ -96,6 +96,30 @@ struct DevBuf {
   }
 };
 
+// ---------------------------------------------------------------- host Ozaki digits
+// rows of A (n x n, row-major): exponent e_r with max_k |a_rk| < 2^{e_r}, then S truncation
+// digits of a 2^{-e_r} (ozaki.cu); dig [S][n][n]
+void host_digits(const std::vector<double>& A, int n, int S, std::vector<int8_t>& dig, std::vector<int>& ew) {
+  dig.assign((size_t)S * n * n, 0);
+  ew.assign(n, 0);
+  for (int r = 0; r < n; ++r) {
+    double mx = 0.0;
+    for (int k = 0; k < n; ++k) mx = std::max(mx, std::fabs(A[(size_t)r * n + k]));
+    int e = 0;
+    if (mx > 0.0) std::frexp(mx, &e);
+    ew[r] = e;
+    for (int k = 0; k < n; ++k) {
+      double v = std::ldexp(A[(size_t)r * n + k], -e);
+      for (int i = 0; i < S; ++i) {
+        v *= 128.0;
+        const double dg = std::trunc(v);
+        v -= dg;
+        dig[((size_t)i * n + r) * n + k] = (int8_t)(int)dg;
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- host fp64 transfers
 // R (n_f/2 x n_f) applied to the rows of a column block: out = R * A  (A: n_f x cols)
 void host_restrict_rows(const std::vector<double>& A, int n_f, int cols, std::vector<double>& out) {
@@ -316,6 +340,11 @@ struct nmg_hierarchy {
   DevBuf<int8_t> wdig, xdig;
   DevBuf<int> wexp, xexp;
   CUtensorMap mWd{}, mXd{};
+  // 2D: the Kronecker pair (C then B) of the fp64 outer residual on the same int8 scheme
+  bool ozaki2d = false;
+  DevBuf<int8_t> wdigB;
+  DevBuf<int> wexpB;
+  CUtensorMap mWdB{};
   // 2D: A_l = B_l (x) C_l + alpha Q_l (x) Q_l; fp32 factors (SIMT), tf32 hi/lo (tcgen05)
   std::vector<std::unique_ptr<DevBuf<float>>> B32, C32, B32h, B32l, C32h, C32l, Q32;
   std::vector<int> qhb;                                  // Q_l half-bandwidth
@@ -992,6 +1021,28 @@ nmg_status inner_cycle(nmg_hierarchy* h, int nrhs, cudaStream_t s) {
 nmg_status outer_residual(nmg_hierarchy* h, int nrhs, const double* y, const double* x, double* r64,
                           bool want_part, cudaStream_t s) {
   if (h->slab) return outer_residual_slab(h, nrhs, y, x, r64, want_part, s);
+  if (h->d.dim == 2 && h->ozaki2d) {
+    const int n = h->n[0];
+    const int M = nrhs * n;
+    const int64_t plane = (int64_t)h->d.max_rhs * n * n;
+    { Prof p(h, NMG_K_GEMM64, s); ozaki_split_rows(M, n, x, n, h->xdig.p, plane, h->xexp.p, s); }
+    NMG_TRY(check_launch(h));
+    OzakiArgs o{};
+    o.M = M; o.N = n; o.K = n;
+    o.r64 = h->T64.p; o.tblock = n; o.plus = true;
+    o.ex = h->xexp.p; o.ew = h->wexp.p;
+    { Prof p(h, NMG_K_GEMM64, s); ozaki_resid(&h->mXd, &h->mWd, o, s); }
+    NMG_TRY(check_launch(h));
+    { Prof p(h, NMG_K_GEMM64, s); ozaki_split_rows(M, n, h->T64.p, n, h->xdig.p, plane, h->xexp.p, s); }
+    NMG_TRY(check_launch(h));
+    OzakiArgs q{};
+    q.M = M; q.N = n; q.K = n;
+    q.Y = y; q.r32 = h->wy[0]->p; q.r64 = r64; q.part = want_part ? h->part.p : nullptr;
+    q.tblock = n; q.ax = x; q.alpha = h->d.alpha;
+    q.ex = h->xexp.p; q.ew = h->wexpB.p;
+    { Prof p(h, NMG_K_GEMM64, s); ozaki_resid(&h->mXd, &h->mWdB, q, s); }
+    return check_launch(h);
+  }
   if (h->d.dim == 2) {
     const int n = h->n[0];
     Gemm64Args g{};
@@ -1523,30 +1574,38 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
       const int S = ozaki_digits();
       std::vector<double> A(factors, factors + nn);
       for (int i = 0; i < n; ++i) A[(size_t)i * n + i] += d.alpha;
-      std::vector<int8_t> dig((size_t)S * nn);
-      std::vector<int> ew(n);
-      for (int r = 0; r < n; ++r) {
-        double mx = 0.0;
-        for (int k = 0; k < n; ++k) mx = std::max(mx, std::fabs(A[(size_t)r * n + k]));
-        int e = 0;
-        if (mx > 0.0) std::frexp(mx, &e);
-        ew[r] = e;
-        for (int k = 0; k < n; ++k) {
-          double v = std::ldexp(A[(size_t)r * n + k], -e);
-          for (int i = 0; i < S; ++i) {
-            v *= 128.0;
-            const double dg = std::trunc(v);
-            v -= dg;
-            dig[((size_t)i * n + r) * n + k] = (int8_t)(int)dg;
-          }
-        }
-      }
+      std::vector<int8_t> dig;
+      std::vector<int> ew;
+      host_digits(A, n, S, dig, ew);
       NMG_TRY(h->wdig.upload(dig.data(), dig.size()));
       NMG_TRY(h->wexp.upload(ew.data(), ew.size()));
       NMG_TRY(h->xdig.alloc((size_t)S * B * n));
       NMG_TRY(h->xexp.alloc(B));
       NMG_TRY(make_digit_map(&h->mWd, h->wdig.p, S, n, n, 64));
       NMG_TRY(make_digit_map(&h->mXd, h->xdig.p, S, (int64_t)B, n, 64, 1));   // half tiles, one digit per box
+    }
+  }
+  if (d.dim == 2) {
+    // fp64 outer residual as two Ozaki int8 passes (T = X C^T, then y - T B^T - alpha x);
+    // NMG_FP64=dmma keeps the DMMA kernel
+    const char* fenv = std::getenv("NMG_FP64");
+    h->ozaki2d = h->use_tc && n % 128 == 0 && !(fenv && std::string(fenv) == "dmma");
+    if (h->ozaki2d) {
+      const int S = ozaki_digits();
+      std::vector<int8_t> dig;
+      std::vector<int> ew;
+      std::vector<double> Bm(factors, factors + nn), Cm(factors + nn, factors + 2 * nn);
+      host_digits(Cm, n, S, dig, ew);
+      NMG_TRY(h->wdig.upload(dig.data(), dig.size()));
+      NMG_TRY(h->wexp.upload(ew.data(), ew.size()));
+      host_digits(Bm, n, S, dig, ew);
+      NMG_TRY(h->wdigB.upload(dig.data(), dig.size()));
+      NMG_TRY(h->wexpB.upload(ew.data(), ew.size()));
+      NMG_TRY(h->xdig.alloc((size_t)S * B * nn));
+      NMG_TRY(h->xexp.alloc(B * n));
+      NMG_TRY(make_digit_map(&h->mWd, h->wdig.p, S, n, n, 64));
+      NMG_TRY(make_digit_map(&h->mWdB, h->wdigB.p, S, n, n, 64));
+      NMG_TRY(make_digit_map(&h->mXd, h->xdig.p, S, (int64_t)B * n, n, 64, 1));
     }
   }
   h->split_fresh.assign(h->L, 0);

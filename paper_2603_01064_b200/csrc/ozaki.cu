@@ -165,6 +165,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ONT, 1)
     __syncwarp();
   }
   // ---------------- epilogue: warp w owns rows 32 w .. 32 w + 31 (TMEM lanes)
+  if (a.tblock && (a.Y || a.ax)) {
+    // 2D pass 2: pull the tile's y and x columns into L2 while the MMAs run (the epilogue
+    // reads them column by column; a warp's 32 rows of one column are 256 contiguous bytes)
+    const int64_t tb = a.tblock;
+    const int mw = m0 + warp * 32;
+    if (mw < a.M && (lane & 15) == 0) {
+      const int64_t base = (int64_t)(mw / a.tblock) * tb * tb + (mw % a.tblock) + (lane >> 4) * 16;
+      for (int c = 0; c < OBN; ++c) {
+        const int64_t off = base + (int64_t)(n0 + c) * tb;
+        if (a.Y) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(a.Y + off));
+        if (a.ax) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(a.ax + off));
+      }
+    }
+  }
   mb_wait(done, 0);
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const int m = m0 + warp * 32 + lane;
@@ -192,7 +206,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ONT, 1)
     }
   }
   double sq = 0.0;
-  if (m < a.M) {
+  if (m < a.M && a.tblock) {
+    // 2D Kronecker passes: transposed store within tb x tb blocks (consecutive rows m of a
+    // warp write consecutive addresses); pass 1 stores +X W^T, pass 2 y - X W^T - alpha x
+    const int exm = a.ex[m];
+    const int64_t tb = a.tblock;
+    const int64_t base = (int64_t)(m / a.tblock) * tb * tb + (m % a.tblock);
+    // batches of 8 columns: all loads of a batch issue before any store (the stores could
+    // alias y / x as far as the compiler knows, which would serialise load latencies)
+#pragma unroll
+    for (int c0 = 0; c0 < OBN; c0 += 8) {
+      double yv[8], xv[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int64_t off = base + (int64_t)(n0 + c0 + j) * tb;
+        yv[j] = (!a.plus && a.Y) ? __ldg(a.Y + off) : 0.0;
+        xv[j] = a.ax ? __ldg(a.ax + off) : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int c = c0 + j;
+        const int64_t off = base + (int64_t)(n0 + c) * tb;
+        const double p = ldexp(acc[c], exm + a.ew[n0 + c]);
+        double v = a.plus ? p : yv[j] - p;
+        if (a.ax) v = fma(-a.alpha, xv[j], v);
+        if (a.r32) a.r32[off] = (float)v;
+        if (a.r64) a.r64[off] = v;
+        sq += v * v;
+      }
+    }
+    if (a.part) a.part[(int64_t)m * gridDim.x + blockIdx.x] = sq;
+  } else if (m < a.M) {
     const int exm = a.ex[m];
     const double* yr = a.Y + (int64_t)m * a.ldy + n0;
     float* r32 = a.r32 ? a.r32 + (int64_t)m * a.ldr32 + n0 : nullptr;
@@ -248,13 +292,43 @@ __global__ void __launch_bounds__(256) ozaki_split_rows_kernel(int M, int K, con
   }
 }
 
+// same digits, one warp per row (short rows, K < 2048): 8 rows per CTA
+__global__ void __launch_bounds__(256) ozaki_split_rows_warp_kernel(int M, int K, const double* __restrict__ X,
+                                                                    int64_t ldx, int8_t* __restrict__ dig,
+                                                                    int64_t plane, int* __restrict__ ex) {
+  const int m = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (m >= M) return;
+  const double* xr = X + (int64_t)m * ldx;
+  double mx = 0.0;
+  for (int k = lane; k < K; k += 32) mx = fmax(mx, fabs(xr[k]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  int e = 0;
+  if (mx > 0.0) { frexp(mx, &e); }
+  if (lane == 0) ex[m] = e;
+  for (int k = 2 * lane; k < K; k += 64) {      // two digits per byte pair store
+    double r0 = ldexp(xr[k], -e), r1 = ldexp(xr[k + 1], -e);
+#pragma unroll
+    for (int i = 0; i < OS; ++i) {
+      r0 *= 128.0;
+      r1 *= 128.0;
+      const double d0 = trunc(r0), d1 = trunc(r1);
+      r0 -= d0;
+      r1 -= d1;
+      const uint32_t pk = ((uint32_t)(uint8_t)(int8_t)(int)d0) | ((uint32_t)(uint8_t)(int8_t)(int)d1 << 8);
+      *reinterpret_cast<uint16_t*>(dig + (int64_t)i * plane + (int64_t)m * K + k) = (uint16_t)pk;
+    }
+  }
+}
+
 }  // namespace
 
 int ozaki_digits() { return OS; }
 
 void ozaki_split_rows(int M, int K, const double* X, int64_t ldx, int8_t* dig, int64_t plane, int* ex,
                       cudaStream_t s) {
-  ozaki_split_rows_kernel<<<M, 256, 0, s>>>(M, K, X, ldx, dig, plane, ex);
+  if (K < 2048 && K % 2 == 0) ozaki_split_rows_warp_kernel<<<ceil_div(M, 8), 256, 0, s>>>(M, K, X, ldx, dig, plane, ex);
+  else ozaki_split_rows_kernel<<<M, 256, 0, s>>>(M, K, X, ldx, dig, plane, ex);
 }
 
 void ozaki_resid(const CUtensorMap* mx, const CUtensorMap* mw, const OzakiArgs& a, cudaStream_t s) {

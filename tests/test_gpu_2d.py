@@ -217,3 +217,24 @@ def test_cnn_strip_kernels(C, n, nrhs):
     hv = O.cnn_forward(H.weights[0], b / s) * s
     want = x0 + O.level_filter(H, 0, hv)
     assert rel_l2(xs.cpu().numpy() - x0, want - x0) < 1e-5
+
+
+@pytest.mark.parametrize("cfg_id,n", [(2, 256), (4, 256), (3, 512)])
+def test_outer_residual_2d_ozaki(cfg_id, n):
+    """fp64 outer residual of the 2D path at n % 128 == 0 (two Ozaki int8 tcgen05 passes,
+    T = X C^T then y - T B^T - alpha x) against the oracle's fp64 A x (1e-12, north_star)."""
+    cfg = ni.CONFIGS[cfg_id].replace(n=n, levels=int(np.log2(n)) - 3, nrhs=3)
+    f = ni.operator_factors(cfg)
+    H = O.build_hierarchy(2, f, cfg.alpha, cfg.levels)
+    h = nmg.Hierarchy(2, n, cfg.levels, cfg.alpha, f, max_rhs=3)
+    rng = np.random.default_rng(6)
+    y = rng.standard_normal((3, n, n))
+    x = rng.standard_normal((3, n, n)) * np.array([1.0, 1e-3, 1e3])[:, None, None]
+    r = torch.zeros(3, n, n, dtype=torch.float64, device=DEV)
+    rr = torch.zeros(3, dtype=torch.float64, device=DEV)
+    h.residual(T(y, torch.float64), T(x, torch.float64), r, rr)
+    want = y - O.apply_A(H, 0, x)
+    for b in range(3):
+        assert rel_l2(r.cpu().numpy()[b], want[b]) < 1e-12, b
+    nrm = np.sqrt((want ** 2).sum(axis=(1, 2))) / np.sqrt((y ** 2).sum(axis=(1, 2)))
+    assert np.allclose(rr.cpu().numpy(), nrm, rtol=1e-12)
