@@ -335,28 +335,36 @@ __global__ void __launch_bounds__(NTHR, 1)
             uint4* al = reinterpret_cast<uint4*>(ring + st * 2 * G::ABYTES + G::ABYTES);
 #pragma unroll 1
             for (int g = c0p / 8; g < (c0p + HC) / 8; ++g) {
-              float v[2][8];
+              // channel pairs in packed fp32 (FFMA2: two FMAs per issue slot, each lane
+              // rounded exactly as a scalar fmaf, same order => same bits)
+              float2 v2[2][4];
               {
                 const float4 b0a = *reinterpret_cast<const float4*>(swt + 9 * C + 8 * g);
                 const float4 b0b = *reinterpret_cast<const float4*>(swt + 9 * C + 8 * g + 4);
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
-                  v[e][0] = b0a.x; v[e][1] = b0a.y; v[e][2] = b0a.z; v[e][3] = b0a.w;
-                  v[e][4] = b0b.x; v[e][5] = b0b.y; v[e][6] = b0b.z; v[e][7] = b0b.w;
+                  v2[e][0] = make_float2(b0a.x, b0a.y); v2[e][1] = make_float2(b0a.z, b0a.w);
+                  v2[e][2] = make_float2(b0b.x, b0b.y); v2[e][3] = make_float2(b0b.z, b0b.w);
                 }
               }
 #pragma unroll
               for (int q9 = 0; q9 < 9; ++q9) {
                 const float4 wa = *reinterpret_cast<const float4*>(swt + q9 * C + 8 * g);
                 const float4 wb = *reinterpret_cast<const float4*>(swt + q9 * C + 8 * g + 4);
-                const float w8[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+                const float2 w2[4] = {make_float2(wa.x, wa.y), make_float2(wa.z, wa.w), make_float2(wb.x, wb.y),
+                                      make_float2(wb.z, wb.w)};
 #pragma unroll
-                for (int e = 0; e < 2; ++e)
+                for (int e = 0; e < 2; ++e) {
+                  const float2 u2 = make_float2(uu[e][q9], uu[e][q9]);
 #pragma unroll
-                  for (int c = 0; c < 8; ++c) v[e][c] = fmaf(w8[c], uu[e][q9], v[e][c]);
+                  for (int c = 0; c < 4; ++c) v2[e][c] = __ffma2_rn(w2[c], u2, v2[e][c]);
+                }
               }
+              float v[2][8];
 #pragma unroll
               for (int e = 0; e < 2; ++e) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) { v[e][2 * c] = v2[e][c].x; v[e][2 * c + 1] = v2[e][c].y; }
 #pragma unroll
                 for (int c = 0; c < 8; ++c) v[e][c] = xin[e] ? fmaxf(v[e][c], 0.f) : 0.f;
                 uint4 hi, lo;
@@ -514,9 +522,9 @@ __global__ void __launch_bounds__(NTHR, 1)
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const Unit t = unit_of(u, hg, nx, a.ysplit);
       const int x = t.X0 + m;
-      float P0[CG], P1[CG];
+      float2 P0[CG / 2], P1[CG / 2];              // channel pairs (packed fp32 adds)
 #pragma unroll
-      for (int j = 0; j < CG; ++j) { P0[j] = 0.f; P1[j] = 0.f; }
+      for (int j = 0; j < CG / 2; ++j) { P0[j] = make_float2(0.f, 0.f); P1[j] = make_float2(0.f, 0.f); }
 #pragma unroll
       for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -559,18 +567,27 @@ __global__ void __launch_bounds__(NTHR, 1)
             }
           }
           float act[8];
+          const float2 dsc2 = make_float2(dsc, dsc);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
+          for (int j = 0; j < 8; j += 2) {
             const int c = 8 * g + j;
-            act[j] = yin ? fmaxf(fmaf(P1[c] + __uint_as_float(D[j]), dsc, bv[c]), 0.f) : 0.f;
-            P1[c] = P0[c] + __uint_as_float(D[8 + j]);
-            P0[c] = __uint_as_float(D[16 + j]);
+            const float2 d2 = make_float2(__uint_as_float(D[j]), __uint_as_float(D[j + 1]));
+            const float2 t = __ffma2_rn(__fadd2_rn(P1[c / 2], d2), dsc2, make_float2(bv[c], bv[c + 1]));
+            act[j] = yin ? fmaxf(t.x, 0.f) : 0.f;
+            act[j + 1] = yin ? fmaxf(t.y, 0.f) : 0.f;
+            P1[c / 2] = __fadd2_rn(P0[c / 2], make_float2(__uint_as_float(D[8 + j]), __uint_as_float(D[9 + j])));
+            P0[c / 2] = make_float2(__uint_as_float(D[16 + j]), __uint_as_float(D[17 + j]));
           }
           if (FIRST) {
             if (store) {
               float v[8];
+              const float2 o2 = make_float2(osc, osc);
 #pragma unroll
-              for (int j = 0; j < 8; ++j) v[j] = act[j] * osc;
+              for (int j = 0; j < 8; j += 2) {
+                const float2 t = __fmul2_rn(make_float2(act[j], act[j + 1]), o2);
+                v[j] = t.x;
+                v[j + 1] = t.y;
+              }
               uint4 hi, lo;
               split8(v, hi, lo);
               reinterpret_cast<uint4*>(a.out_h + off)[g] = hi;
@@ -578,8 +595,13 @@ __global__ void __launch_bounds__(NTHR, 1)
             }
           } else {
             float v[8];
+            const float2 s3 = make_float2(a.a3_scale, a.a3_scale);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) v[j] = act[j] * a.a3_scale;
+            for (int j = 0; j < 8; j += 2) {
+              const float2 t = __fmul2_rn(make_float2(act[j], act[j + 1]), s3);
+              v[j] = t.x;
+              v[j + 1] = t.y;
+            }
             uint4 hi, lo;
             split8(v, hi, lo);
             reinterpret_cast<uint4*>(A4)[(c0 / 8 + g) * SEG + m] = hi;
