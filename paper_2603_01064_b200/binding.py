@@ -11,7 +11,8 @@ from typing import Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(HERE, "libnmg.so")
+# NMG_LIB: alternative build of the same library (dev experiments with compile-time variants)
+lib_path = os.environ.get("NMG_LIB") or os.path.join(HERE, "libnmg.so")
 
 OP_APPLY, OP_RESIDUAL, OP_RESTRICT, OP_PROLONG, OP_FILTER, OP_CNN, OP_SMOOTH, OP_COARSE, OP_CYCLE0 = range(9)
 

@@ -47,7 +47,6 @@ namespace {
 
 constexpr int SEG = 128;        // pixels per strip (MMA M)
 constexpr int RP = SEG + 2;     // rows of the activation buffer (x halo)
-constexpr int NSTG = 3;         // activation ring depth
 constexpr int NTHR = 448;
 constexpr int MMAW = 13;        // MMA warp
 constexpr uint32_t IDESC4 = (1u << 4) | ((uint32_t)(16 >> 3) << 17) | ((uint32_t)(SEG >> 4) << 24);  // N = 16
@@ -72,7 +71,19 @@ struct Cfg {
   static constexpr int ABYTES = ((RP * C * 2) + 127) / 128 * 128;   // one activation row, hi or lo
   static constexpr int ALBO = RP * 16;                  // K-chunk stride of the A buffer
   static constexpr int BLBO = N * 16;                   // K-chunk stride of the B (weight) planes
-  static constexpr int TCOLS = 2 * N + 16 <= 256 ? 256 : 512;   // D double buffer + D4 (16 columns)
+  // pipeline depths (dev knobs NMG_STRIP_*): activation ring and TMEM D buffers
+#ifndef NMG_STRIP_NSTG32
+#define NMG_STRIP_NSTG32 5
+#endif
+#ifndef NMG_STRIP_NSTG48
+#define NMG_STRIP_NSTG48 3
+#endif
+#ifndef NMG_STRIP_NDB
+#define NMG_STRIP_NDB 2
+#endif
+  static constexpr int NSTG = C == 32 ? NMG_STRIP_NSTG32 : NMG_STRIP_NSTG48;
+  static constexpr int NDB = NMG_STRIP_NDB;
+  static constexpr int TCOLS = NDB * N + 16 <= 256 ? 256 : 512;   // D buffers + D4 (16 columns)
   static constexpr int A4BYTES = SEG * C * 2;           // layer-4 A tile (a3 row), hi or lo
   static constexpr int A4LBO = SEG * 16;
   static constexpr int W4BYTES = 16 * C * 2;            // layer-4 weights [C/8][16][8], hi or lo
@@ -203,6 +214,7 @@ __global__ void __launch_bounds__(NTHR, 1)
                       StripArgs a) {
   using G = Cfg<C>;
   using RL = Roles<C, FIRST>;
+  constexpr int NSTG = G::NSTG, NDB = G::NDB;
   constexpr int NGRP = RL::NG;
   constexpr int PROD0 = RL::PROD0;
   constexpr int CG = C / NGRP;                           // channels per epilogue thread
@@ -216,13 +228,13 @@ __global__ void __launch_bounds__(NTHR, 1)
   uint8_t* misc = W4 + 2 * G::W4BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(misc);    // [NSTG]
   uint64_t* empty = full + NSTG;                         // [NSTG]
-  uint64_t* dfull = empty + NSTG;                        // [2]
-  uint64_t* dempty = dfull + 2;                          // [2]
-  uint64_t* a4full = dempty + 2;
+  uint64_t* dfull = empty + NSTG;                        // [NDB]
+  uint64_t* dempty = dfull + NDB;                        // [NDB]
+  uint64_t* a4full = dempty + NDB;
   uint64_t* d4full = a4full + 1;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(d4full + 1);
   // FIRST: w0 transposed [t][c] then b0 [c];  else: w3 transposed [t][c]
-  float* swt = reinterpret_cast<float*>(misc + 128);
+  float* swt = reinterpret_cast<float*>(misc + 512);
   float* sbias = swt + 10 * C;                           // hidden-layer bias [C]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -257,7 +269,7 @@ __global__ void __launch_bounds__(NTHR, 1)
   }
   if (tid == 0) {
     for (int s = 0; s < NSTG; ++s) { mb_init(&full[s], FIRST ? RL::NPROD : 1); mb_init(&empty[s], 1); }
-    for (int s = 0; s < 2; ++s) { mb_init(&dfull[s], 1); mb_init(&dempty[s], 4 * NGRP); }
+    for (int s = 0; s < NDB; ++s) { mb_init(&dfull[s], 1); mb_init(&dempty[s], 4 * NGRP); }
     mb_init(a4full, 4 * NGRP);
     mb_init(d4full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -411,8 +423,8 @@ __global__ void __launch_bounds__(NTHR, 1)
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const Unit t = unit_of(u, hg, nx, a.ysplit);
         for (int r = t.y0 - H; r <= t.y1 + H - 1; ++r, ++k) {
-          const int buf = k & 1;
-          mb_wait(&dempty[buf], ((uint32_t)(k >> 1) & 1u) ^ 1u);
+          const int buf = k % NDB;
+          mb_wait(&dempty[buf], ((uint32_t)(k / NDB) & 1u) ^ 1u);
           if (r < ylo || r >= yhi) {      // zero-padding row: nothing to multiply
             mb_arrive(&dfull[buf]);
             continue;
@@ -450,7 +462,7 @@ __global__ void __launch_bounds__(NTHR, 1)
     // (its own thread, so the layer-3 chain of the next row never waits for the epilogue)
     if (lane == 0) {
       const uint32_t a4h = su32(A4), a4l = a4h + G::A4BYTES, w4h = su32(W4), w4l = w4h + G::W4BYTES;
-      const uint32_t d4 = tmem + (uint32_t)(2 * G::N);
+      const uint32_t d4 = tmem + (uint32_t)(NDB * G::N);
       int e4 = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const Unit t = unit_of(u, hg, nx, a.ysplit);
@@ -498,8 +510,8 @@ __global__ void __launch_bounds__(NTHR, 1)
       ++e4;
       if (grp == 0) {
         uint32_t d[16];
-        tld8(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(2 * G::N), d);
-        tld8(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(2 * G::N + 8), d + 8);
+        tld8(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(NDB * G::N), d);
+        tld8(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(NDB * G::N + 8), d + 8);
         tld_wait<16>(d);
         const float s4 = a.d4_scale;
 #pragma unroll
@@ -530,9 +542,9 @@ __global__ void __launch_bounds__(NTHR, 1)
 #pragma unroll
         for (int j = 0; j < 3; ++j) acc4[i][j] = 0.f;
       for (int r = t.y0 - H; r <= t.y1 + H - 1; ++r, ++k) {
-        const int buf = k & 1;
+        const int buf = k % NDB;
         const bool valid = r >= ylo && r < yhi;
-        mb_wait(&dfull[buf], (uint32_t)(k >> 1) & 1u);
+        mb_wait(&dfull[buf], (uint32_t)(k / NDB) & 1u);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * G::N + c0);
         // output row r - 1 is complete: b + D_0(r - 2) + D_1(r - 1) + D_2(r)

@@ -1,5 +1,5 @@
-timeout 600 python -m pytest tests/test_gpu_2d.py -q -x -k "ozaki or outer or history" 2>&1 | tail -2
-for c in 2 4 3; do
-  timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"ozaki|dgemm" --csv python tools/profile_cfg.py $c 32 1 2>/dev/null | grep -E "ozaki|dgemm" | awk -F'","' '{print $5, $NF}' | head -4
-  NMG_FP64=dmma timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"ozaki|dgemm" --csv python tools/profile_cfg.py $c 32 1 2>/dev/null | grep -E "ozaki|dgemm" | awk -F'","' '{print $5, $NF}' | head -2
+for v in s5 s6 s7 s8; do
+  export NMG_LIB=$PWD/paper_2603_01064_b200/variants/libnmg_$v.so
+  echo "== $v $(timeout 300 python -m pytest tests/test_gpu_2d.py -q -k strip 2>&1 | tail -1)"
+  for c in 2 4; do timeout 300 python tools/profile_cfg.py $c | grep -E "ms/step|smooth"; done
 done
