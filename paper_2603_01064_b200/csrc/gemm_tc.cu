@@ -155,7 +155,27 @@ NMG_D void tc_store_chunk(const TcGemmArgs& a, const uint32_t (&v)[32], int m, i
     }
   }
 
-template <int TBN, bool F16 = false>
+NMG_D void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%3, "
+      "%4}], [%2], %5;\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+NMG_D void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+NMG_D uint32_t cta_rank_in_cluster() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+
+// MC: CTA pairs along M (cluster 1 x 2) share the W tile -- each loads half of its rows and
+// multicasts them to both (W maps with box rows TBN / 2), halving the L2 -> SM traffic of
+// the operator, which every M tile re-reads; a stage is refilled only after the MMAs of BOTH
+// CTAs released it (commit multicast, empty count 2)
+template <int TBN, bool F16 = false, bool MC = false>
 __global__ void __launch_bounds__(TNT, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tXh, const __grid_constant__ CUtensorMap tXl,
                    const __grid_constant__ CUtensorMap tWh, const __grid_constant__ CUtensorMap tWl,
@@ -174,8 +194,9 @@ __global__ void __launch_bounds__(TNT, 1)
   const int m0 = blockIdx.y * TBM, n0 = blockIdx.x * TBN;
   const int KT = ceil_div(a.K, KE);
 
+  const uint32_t crank = MC ? cta_rank_in_cluster() : 0u;
   if (tid == 0) {
-    for (int s = 0; s < TSTAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < TSTAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], MC ? 2 : 1); }
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     prefetch_tmap(&tXh); prefetch_tmap(&tXl); prefetch_tmap(&tWh); prefetch_tmap(&tWl);
@@ -186,7 +207,8 @@ __global__ void __launch_bounds__(TNT, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
+  if (MC) cluster_sync_all();                  // both CTAs' barriers exist before any multicast
+  else __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
@@ -201,8 +223,15 @@ __global__ void __launch_bounds__(TNT, 1)
         const int k0 = kt * KE;
         tma_load_2d(st, &tXh, &full[s], k0, m0);
         tma_load_2d(st + A_BYTES, &tXl, &full[s], k0, m0);
-        tma_load_2d(st + 2 * A_BYTES, &tWh, &full[s], k0, n0);
-        tma_load_2d(st + 2 * A_BYTES + B_BYTES, &tWl, &full[s], k0, n0);
+        if (MC) {
+          const int hr = TBN / 2;
+          tma_load_2d_mc(st + 2 * A_BYTES + crank * (B_BYTES / 2), &tWh, &full[s], k0, n0 + (int)crank * hr, 3);
+          tma_load_2d_mc(st + 2 * A_BYTES + B_BYTES + crank * (B_BYTES / 2), &tWl, &full[s], k0, n0 + (int)crank * hr,
+                         3);
+        } else {
+          tma_load_2d(st + 2 * A_BYTES, &tWh, &full[s], k0, n0);
+          tma_load_2d(st + 2 * A_BYTES + B_BYTES, &tWl, &full[s], k0, n0);
+        }
       }
     }
     __syncwarp();
@@ -231,7 +260,14 @@ __global__ void __launch_bounds__(TNT, 1)
             umma_tf32(tmem, dxl, dwh, 1u, kIdesc);
           }
         }
-        umma_commit(&empty[s]);      // slot reusable when these MMAs retire
+        if (MC)   // slot reusable when both CTAs' MMAs retired
+          asm volatile(
+              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+                  smem_u32(&empty[s])),
+              "h"((uint16_t)3)
+              : "memory");
+        else
+          umma_commit(&empty[s]);    // slot reusable when these MMAs retire
       }
       umma_commit(done);             // accumulator complete
     }
@@ -272,7 +308,8 @@ __global__ void __launch_bounds__(TNT, 1)
     __syncwarp();
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
+  if (MC) cluster_sync_all();                  // no CTA leaves while its peer may still signal it
+  else __syncthreads();
   if (warp == 2) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TBN));
   }
@@ -331,7 +368,27 @@ void tc_gemm_f16(const CUtensorMap* xh, const CUtensorMap* xl, const CUtensorMap
                  const TcGemmArgs& a, cudaStream_t s, int bn) {
   static bool attr256 = false, attr64 = false;
   dim3 grid(ceil_div(a.N, bn), ceil_div(a.M, TBM));
-  if (bn == 256) {
+  if (bn == 256 && a.wh_mc && grid.y % 2 == 0) {
+    static bool attrmc = false;
+    if (!attrmc) {
+      cudaFuncSetAttribute(tc_gemm_kernel<256, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           TcCfg<256>::SMEM);
+      attrmc = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(TNT);
+    cfg.dynamicSmemBytes = TcCfg<256>::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 1;
+    at[0].val.clusterDim.y = 2;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, tc_gemm_kernel<256, true, true>, *xh, *xl, *a.wh_mc, *a.wl_mc, a);
+  } else if (bn == 256) {
     if (!attr256) {
       cudaFuncSetAttribute(tc_gemm_kernel<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<256>::SMEM);
       attr256 = true;

@@ -84,6 +84,10 @@ struct TcGemmArgs {
   // winv[n] = 1 / T_n (powers of two, so acc xinv winv is exact)
   const float* xinv = nullptr;
   const float* winv = nullptr;
+  // FP16x3, 256-wide tiles: W maps with box rows 128 (host pointers) -> CTA pairs along M
+  // multicast the W tile (cluster 1 x 2), when the number of M tiles is even
+  const CUtensorMap* wh_mc = nullptr;
+  const CUtensorMap* wl_mc = nullptr;
 };
 // 2D Kronecker apply passes on tcgen05 (kron_tc.cu).  A = fp32 [M][n] rows (TMA map, box
 // {16, 128}, SWIZZLE_64B), W = tf32 hi/lo [n][n] (box {16, kron_tile_n(n)}).

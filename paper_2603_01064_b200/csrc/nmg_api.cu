@@ -324,7 +324,8 @@ struct nmg_hierarchy {
   std::vector<char> split_fresh;                         // sxh/sxl[l] hold the split of wx[l]
   // 1D inner operator applies in FP16x3 (kind::f16): per-row-scaled f16 hi/lo planes
   bool gemm_f16 = false;
-  struct F16Op { DevBuf<uint16_t> h, l; DevBuf<float> winv; CUtensorMap m256h, m256l, m64h, m64l; };
+  struct F16Op { DevBuf<uint16_t> h, l; DevBuf<float> winv; CUtensorMap m256h, m256l, m64h, m64l, m128h, m128l; };
+  bool gemm_mc = true;                                   // NMG_GEMM_MC=0: no W multicast in the FP16x3 GEMM
   std::vector<std::unique_ptr<F16Op>> A16, AP16;         // per smoothed level
   std::vector<std::unique_ptr<DevBuf<uint16_t>>> sx16h, sx16l;
   std::vector<std::unique_ptr<DevBuf<float>>> sxinv;
@@ -544,6 +545,7 @@ nmg_status level_resid(nmg_hierarchy* h, int l, int which, int nrhs, const float
     g.M = nrhs; g.N = n; g.K = K;
     g.C = C; g.ldc = n; g.D = D; g.ldd = n; g.negate = negate;
     g.xinv = h->sxinv[lx]->p; g.winv = W.winv.p;
+    if (h->gemm_mc) { g.wh_mc = &W.m128h; g.wl_mc = &W.m128l; }
     {
       Prof p(h, NMG_K_GEMM32, s);
       const int bn = tc_pick_bn(nrhs, n, h->num_sms);
@@ -1466,6 +1468,8 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
             NMG_TRY(make_map16(&op->m256l, op->l.p, nl, cols, 256));
             NMG_TRY(make_map16(&op->m64h, op->h.p, nl, cols, 64));
             NMG_TRY(make_map16(&op->m64l, op->l.p, nl, cols, 64));
+            NMG_TRY(make_map16(&op->m128h, op->h.p, nl, cols, 128));
+            NMG_TRY(make_map16(&op->m128l, op->l.p, nl, cols, 128));
           }
         }
       }
@@ -1569,6 +1573,8 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
   if (d.dim == 1) {
     const char* fenv = std::getenv("NMG_FP64");
     h->ozaki = h->use_tc && n % 128 == 0 && /* CTA pairs along N */ !(fenv && std::string(fenv) == "dmma");
+    const char* menv = std::getenv("NMG_GEMM_MC");
+    h->gemm_mc = !(menv && std::string(menv) == "0");
     if (h->ozaki) {
       // W digits of A (rows n, K = n), host: exponent per row, S truncation digits
       const int S = ozaki_digits();
