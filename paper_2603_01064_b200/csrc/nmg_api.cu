@@ -409,6 +409,12 @@ struct nmg_hierarchy {
   };
   std::vector<GraphEntry> graphs;
   uint64_t g_clock = 0;
+  // RHS lanes: a second hierarchy (same operators and weights) cycles the second half of a
+  // large batch on a forked stream, so the two halves' kernels overlap (fills the last wave of
+  // each launch and the small coarse-level grids); both halves are captured in one graph
+  std::unique_ptr<nmg_hierarchy> lane2;
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t evf = nullptr, evj = nullptr;
   // slab-sharded single-system mode (nmg_create_hierarchy_slab)
   bool slab = false;
   nmg_comm* comm = nullptr;                              // not owned
@@ -421,6 +427,9 @@ struct nmg_hierarchy {
   DevBuf<double> t64send, t64recv, dscratch, ssum, rsum, ysq;
   DevBuf<float2> zs, za, zb;
   ~nmg_hierarchy() {
+    if (s2) cudaStreamDestroy(s2);
+    if (evf) cudaEventDestroy(evf);
+    if (evj) cudaEventDestroy(evj);
     for (auto e : ev_pool) cudaEventDestroy(e);
     for (auto& g : graphs) if (g.exec) cudaGraphExecDestroy(g.exec);
     for (auto e : hev) cudaEventDestroy(e);
@@ -1196,8 +1205,26 @@ namespace {
 // small configs and coarse levels).
 nmg_status graph_cycle(nmg_hierarchy* h, int nrhs, const double* y, double* x, cudaStream_t s) {
   auto body = [&]() -> nmg_status {
-    NMG_TRY(ynorms(h, nrhs, y, s));
-    return outer_step(h, nrhs, y, x, -1.0, false, s);
+    nmg_hierarchy* h2 = h->lane2.get();
+    if (!h2 || h->prof_on || nrhs < 2 * 128 || s == nullptr) {
+      NMG_TRY(ynorms(h, nrhs, y, s));
+      return outer_step(h, nrhs, y, x, -1.0, false, s);
+    }
+    // two lanes: RHS [0, n0) on s, [n0, nrhs) on the forked stream s2 (RHS are independent)
+    const int n0 = (nrhs / 2 + 127) / 128 * 128;
+    const int n1 = nrhs - n0;
+    const int64_t N = h->N[0];
+    NMG_CUDA(cudaEventRecord(h->evf, s));
+    NMG_CUDA(cudaStreamWaitEvent(h->s2, h->evf, 0));
+    const int64_t l2 = h2->launches;
+    NMG_TRY(ynorms(h2, n1, y + n0 * N, h->s2));
+    NMG_TRY(outer_step(h2, n1, y + n0 * N, x + n0 * N, -1.0, false, h->s2));
+    h->launches += h2->launches - l2;
+    NMG_TRY(ynorms(h, n0, y, s));
+    NMG_TRY(outer_step(h, n0, y, x, -1.0, false, s));
+    NMG_CUDA(cudaEventRecord(h->evj, h->s2));
+    NMG_CUDA(cudaStreamWaitEvent(s, h->evj, 0));
+    return NMG_OK;
   };
   if (!h->use_graph || h->slab || s == nullptr || h->prof_on) return body();
   nmg_hierarchy::GraphEntry* g = nullptr;
@@ -1621,6 +1648,22 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
   NMG_TRY(h->ywork.alloc(B * 64));
   NMG_TRY(h->relres.alloc(B));
   NMG_TRY(h->active.alloc(B));
+  {
+    const char* le = std::getenv("NMG_LANES");
+    if (d.dim == 1 && d.max_rhs >= 512 && !(le && std::string(le) == "1")) {
+      nmg_problem_desc d2 = d;
+      d2.max_rhs = d.max_rhs / 2;
+      setenv("NMG_LANES", "1", 1);                       // the lane itself has no lanes
+      nmg_hierarchy* raw = nullptr;
+      const nmg_status st = nmg_create_hierarchy(&d2, factors, &raw);
+      if (le) setenv("NMG_LANES", le, 1); else unsetenv("NMG_LANES");
+      NMG_TRY(st);
+      h->lane2.reset(raw);
+      NMG_CUDA(cudaStreamCreateWithFlags(&h->s2, cudaStreamNonBlocking));
+      NMG_CUDA(cudaEventCreateWithFlags(&h->evf, cudaEventDisableTiming));
+      NMG_CUDA(cudaEventCreateWithFlags(&h->evj, cudaEventDisableTiming));
+    }
+  }
   NMG_CUDA(cudaDeviceSynchronize());
   *out = h.release();
   return NMG_OK;
@@ -1891,6 +1934,7 @@ nmg_status nmg_load_smoother_weights(nmg_hierarchy* h, int32_t level, const nmg_
     }
   }
   h->w_loaded[level - 1] = 1;
+  if (h->lane2) NMG_TRY(nmg_load_smoother_weights(h->lane2.get(), level, arch, params, n_params));
   h->arch = *arch;
   return NMG_OK;
 }

@@ -347,3 +347,30 @@ def test_host_entry_chunked_pipeline():
     xh = np.zeros_like(y)
     h.vcycles_host(np.ascontiguousarray(y), xh, 2)
     assert np.array_equal(xh, xd.cpu().numpy())
+
+
+def test_rhs_lanes_bitwise(monkeypatch):
+    """Batches >= 256 RHS on a handle with max_rhs >= 512 run as two RHS lanes on forked
+    streams (nmg_vcycle); the NMGF cycle is per-RHS, so the result is bitwise the one-lane result."""
+    cfg = ni.CONFIGS[1].replace(n=1024, levels=4, nrhs=512)
+    f = ni.operator_factors(cfg)
+    W = ni.weights_seed(cfg)
+    y, _ = ni.make_rhs(cfg, f, cfg.alpha, nrhs=512)
+    outs = []
+    for lanes in ("1", None):
+        if lanes:
+            monkeypatch.setenv("NMG_LANES", lanes)
+        else:
+            monkeypatch.delenv("NMG_LANES", raising=False)
+        h = nmg.Hierarchy(1, cfg.n, cfg.levels, cfg.alpha, f, nu1=1, nu2=1, max_rhs=512)
+        for l, w in enumerate(W):
+            h.load_weights(l + 1, ni.cnn_arch(cfg), w)
+        yd = torch.tensor(y, dtype=torch.float64, device=DEV)
+        xd = torch.zeros_like(yd)
+        st = torch.cuda.Stream()
+        for _ in range(3):                     # eager, capture, replay
+            h.vcycle(yd, xd, st)
+        torch.cuda.synchronize()
+        outs.append(xd.cpu().numpy())
+        h.close()
+    assert np.array_equal(outs[0], outs[1])
