@@ -275,13 +275,33 @@ __global__ void __launch_bounds__(KNT, 1)
           for (int j = 0; j < 16; ++j)
             if (nb + j < n) a.D[base + (int64_t)(nb + j) * R] = __uint_as_float(v[j]);
         } else {
-          // X rows addressed by their global index i2 (the slab's halo holds i2 +- hb)
+          // X rows addressed by their global index i2 (the slab's halo holds i2 +- hb).
+          // Mass stencil S = Q X Q^T of the chunk: horizontal pass over the rows i2 - HB ..
+          // i2 + 15 + HB, then the vertical pass in registers; every load is unconditional
+          // (clamped address, out-of-range terms weighted by 0 or dropped by select), so the
+          // loads of a chunk issue back to back instead of one dependent miss at a time.
+          // Same fma order as qstencil_at (bitwise the same sums).
           const float* Xb = a.X + b * img + (int64_t)(a.H - a.r0) * n;
+          constexpr int NR = 16 + 2 * HB;
+          float hs[NR];
+#pragma unroll
+          for (int k = 0; k < NR; ++k) {
+            const int a2 = a.r0 + nb - HB + k;
+            const float* xrow = Xb + (int64_t)min(max(a2, 0), n - 1) * n;
+            float t = 0.f;
+#pragma unroll
+            for (int d1 = -HB; d1 <= HB; ++d1) t = fmaf(q1[d1 + HB], __ldg(xrow + min(max(r + d1, 0), n - 1)), t);
+            hs[k] = (a2 >= 0 && a2 < n) ? t : 0.f;
+          }
           float o[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const int jj = min(nb + j, R - 1);
-            const float sq = qstencil_at<HB>(Xb, a.Q, n, a.r0 + jj, r, q1);
+            const int i2 = a.r0 + jj;
+            float sq = 0.f;
+#pragma unroll
+            for (int d2 = -HB; d2 <= HB; ++d2)
+              sq = fmaf(__ldg(a.Q + (int64_t)i2 * n + min(max(i2 + d2, 0), n - 1)), hs[jj - nb + d2 + HB], sq);
             const float vv = fmaf(a.alpha, sq, __uint_as_float(v[j]));
             const float cc = a.Cin ? a.Cin[base + (int64_t)jj * n] : 0.f;
             o[j] = a.negate ? cc - vv : cc + vv;
