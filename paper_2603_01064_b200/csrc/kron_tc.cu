@@ -102,30 +102,6 @@ NMG_D float rna_tf32(float v) {
   return __uint_as_float(h);
 }
 
-// stencil S[b][i2][i1] = sum_{a2, a1} Q[i2][a2] Q[i1][a1] X[b][a2][a1], |a - i| <= HB
-template <int HB>
-NMG_D float qstencil_at(const float* __restrict__ Xb, const float* __restrict__ Q, int n, int i2, int i1,
-                        const float (&q1)[2 * HB + 1]) {
-  if constexpr (HB == 0) {
-    return __ldg(Q + (int64_t)i2 * n + i2) * (q1[0] * __ldg(Xb + (int64_t)i2 * n + i1));
-  } else {
-    float acc = 0.f;
-#pragma unroll
-    for (int d2 = -HB; d2 <= HB; ++d2) {
-      const int a2 = i2 + d2;
-      if (a2 < 0 || a2 >= n) continue;
-      float t = 0.f;
-#pragma unroll
-      for (int d1 = -HB; d1 <= HB; ++d1) {
-        const int a1 = i1 + d1;
-        if (a1 >= 0 && a1 < n) t = fmaf(q1[d1 + HB], __ldg(Xb + (int64_t)a2 * n + a1), t);
-      }
-      acc = fmaf(__ldg(Q + (int64_t)i2 * n + a2), t, acc);
-    }
-    return acc;
-  }
-}
-
 template <int TBN, int HB>
 __global__ void __launch_bounds__(KNT, 1)
     kron_tc_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tWh,
@@ -280,7 +256,7 @@ __global__ void __launch_bounds__(KNT, 1)
           // i2 + 15 + HB, then the vertical pass in registers; every load is unconditional
           // (clamped address, out-of-range terms weighted by 0 or dropped by select), so the
           // loads of a chunk issue back to back instead of one dependent miss at a time.
-          // Same fma order as qstencil_at (bitwise the same sums).
+          // S[b][i2][i1] = sum_{a2} Q[i2][a2] (sum_{a1} Q[i1][a1] X[b][a2][a1]), |a - i| <= HB.
           const float* Xb = a.X + b * img + (int64_t)(a.H - a.r0) * n;
           constexpr int NR = 16 + 2 * HB;
           float hs[NR];
