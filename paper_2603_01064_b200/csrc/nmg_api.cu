@@ -413,6 +413,8 @@ struct nmg_hierarchy {
   // large batch on a forked stream, so the two halves' kernels overlap (fills the last wave of
   // each launch and the small coarse-level grids); both halves are captured in one graph
   std::unique_ptr<nmg_hierarchy> lane2;
+  int lane_mult = 1;                                     // 2 while both lanes run (GEMM tile choice)
+  bool lane_tiles = true;                                // NMG_LANE_TILES=0: per-lane tile choice
   cudaStream_t s2 = nullptr;
   cudaEvent_t evf = nullptr, evj = nullptr;
   // slab-sharded single-system mode (nmg_create_hierarchy_slab)
@@ -557,7 +559,7 @@ nmg_status level_resid(nmg_hierarchy* h, int l, int which, int nrhs, const float
     if (h->gemm_mc) { g.wh_mc = &W.m128h; g.wl_mc = &W.m128l; }
     {
       Prof p(h, NMG_K_GEMM32, s);
-      const int bn = tc_pick_bn(nrhs, n, h->num_sms);
+      const int bn = tc_pick_bn(nrhs * h->lane_mult, n, h->num_sms);
       tc_gemm_f16(&h->mX16h[lx], &h->mX16l[lx], bn == 256 ? &W.m256h : &W.m64h, bn == 256 ? &W.m256l : &W.m64l, g, s,
                   bn);
     }
@@ -573,7 +575,7 @@ nmg_status level_resid(nmg_hierarchy* h, int l, int which, int nrhs, const float
   g.C = C; g.ldc = n; g.D = D; g.ldd = n; g.negate = negate;
   {
     Prof p(h, NMG_K_GEMM32, s);
-    const int bn = tc_pick_bn(nrhs, n, h->num_sms);
+    const int bn = tc_pick_bn(nrhs * h->lane_mult, n, h->num_sms);
     if (which == 0)
       tc_gemm(&h->mXh[lx], &h->mXl[lx], bn == 256 ? &h->mAh[l] : &h->mAh64[l], bn == 256 ? &h->mAl[l] : &h->mAl64[l],
               g, s, bn);
@@ -1217,11 +1219,15 @@ nmg_status graph_cycle(nmg_hierarchy* h, int nrhs, const double* y, double* x, c
     NMG_CUDA(cudaEventRecord(h->evf, s));
     NMG_CUDA(cudaStreamWaitEvent(h->s2, h->evf, 0));
     const int64_t l2 = h2->launches;
-    NMG_TRY(ynorms(h2, n1, y + n0 * N, h->s2));
-    NMG_TRY(outer_step(h2, n1, y + n0 * N, x + n0 * N, -1.0, false, h->s2));
+    // the two lanes' GEMMs run concurrently: pick the tile width for the whole batch
+    h->lane_mult = h2->lane_mult = h->lane_tiles ? 2 : 1;
+    nmg_status st = ynorms(h2, n1, y + n0 * N, h->s2);
+    if (st == NMG_OK) st = outer_step(h2, n1, y + n0 * N, x + n0 * N, -1.0, false, h->s2);
     h->launches += h2->launches - l2;
-    NMG_TRY(ynorms(h, n0, y, s));
-    NMG_TRY(outer_step(h, n0, y, x, -1.0, false, s));
+    if (st == NMG_OK) st = ynorms(h, n0, y, s);
+    if (st == NMG_OK) st = outer_step(h, n0, y, x, -1.0, false, s);
+    h->lane_mult = h2->lane_mult = 1;
+    NMG_TRY(st);
     NMG_CUDA(cudaEventRecord(h->evj, h->s2));
     NMG_CUDA(cudaStreamWaitEvent(s, h->evj, 0));
     return NMG_OK;
@@ -1659,6 +1665,8 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
       if (le) setenv("NMG_LANES", le, 1); else unsetenv("NMG_LANES");
       NMG_TRY(st);
       h->lane2.reset(raw);
+      const char* lt = std::getenv("NMG_LANE_TILES");
+      h->lane_tiles = !(lt && std::string(lt) == "0");
       NMG_CUDA(cudaStreamCreateWithFlags(&h->s2, cudaStreamNonBlocking));
       NMG_CUDA(cudaEventCreateWithFlags(&h->evf, cudaEventDisableTiming));
       NMG_CUDA(cudaEventCreateWithFlags(&h->evj, cudaEventDisableTiming));

@@ -1,3 +1,4 @@
-timeout 900 python -m pytest tests/test_gpu_2d.py tests/test_gpu_slab.py tests/test_gpu_variants.py -q -x 2>&1 | tail -1
-for c in 2 4; do timeout 300 python tools/profile_cfg.py $c | grep -E "ms/step|gemm32"; done
-timeout 300 python tools/profile_cfg.py 3 256 2 | grep -E "ms/step|gemm32"
+timeout 600 python -m pytest tests/test_gpu_1d.py -q -x 2>&1 | tail -1
+for lt in 1 0 1 0; do
+  echo "lane_tiles $lt: $(NMG_LANE_TILES=$lt timeout 300 python bench.py --config 1 --steps 100 --no-cpu --no-e2e --no-solve | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["ms_per_step"], d["value"])')"
+done
