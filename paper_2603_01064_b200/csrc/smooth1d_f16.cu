@@ -30,6 +30,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cstdio>
 
 #include "common.cuh"
 #include "fft.cuh"
@@ -353,8 +354,21 @@ NMG_D void produce_a1(const Smooth1dArgs& a, uint8_t* Abuf, uint64_t* aempty, ui
   }
 }
 
+#ifdef NMG_S1D_PHASES
+#define S1D_TS(i) do { if (threadIdx.x == 0 && blockIdx.x == 0) ts[i] = clock64(); } while (0)
+#else
+#define S1D_TS(i) do { } while (0)
+#endif
+
 template <int NSA>
-__global__ void __launch_bounds__(NT, 3) smooth1d_f16_kernel(const __grid_constant__ Smooth1dArgs a) {
+#ifndef NMG_S1D_MINB
+#define NMG_S1D_MINB 4
+#endif
+__global__ void __launch_bounds__(NT, NMG_S1D_MINB) smooth1d_f16_kernel(const __grid_constant__ Smooth1dArgs a) {
+#ifdef NMG_S1D_PHASES
+  long long ts[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
+  S1D_TS(0);
   extern __shared__ __align__(1024) uint8_t smraw[];
   uint8_t* sm = smraw + ((1024u - (su32(smraw) & 1023u)) & 1023u);
   const int n = a.n, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -419,6 +433,7 @@ __global__ void __launch_bounds__(NT, 3) smooth1d_f16_kernel(const __grid_consta
   } else {
     const float sf = (float)s;
     const int ntile = n / TP;
+    S1D_TS(1);
     if (warp >= 4 && warp < 8) {
       // ---------------------------------------------------------- layer-1 producer
       const int pt = tid - 128;                 // 0..127
@@ -514,6 +529,7 @@ __global__ void __launch_bounds__(NT, 3) smooth1d_f16_kernel(const __grid_consta
       if (m < 2) assemble(n - 2 + m);
     }
     __syncthreads();
+    S1D_TS(2);
     if (a.filter) {
       // ---- level filter F'_l on the whole row (see level_filter_row); prefetch x* into the (now free) input-row buffer while the FFT runs
       const bool pre = a.accumulate;
@@ -525,6 +541,7 @@ __global__ void __launch_bounds__(NT, 3) smooth1d_f16_kernel(const __grid_consta
       }
       level_filter_row(reinterpret_cast<float2*>(hb), reinterpret_cast<float2*>(Abuf), n, a.twiddle, a.tw_n,
                        tid, NT);
+      S1D_TS(3);
       if (pre) {
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         __syncthreads();
@@ -567,6 +584,12 @@ __global__ void __launch_bounds__(NT, 3) smooth1d_f16_kernel(const __grid_consta
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
+  S1D_TS(4);
+#ifdef NMG_S1D_PHASES
+  if (threadIdx.x == 0 && blockIdx.x == 0)
+    printf("s1d n=%d: setup+norm %lld  tiles %lld  filter %lld  update %lld  (cycles)\n", n, ts[1] - ts[0],
+           ts[2] - ts[1], ts[3] - ts[2], ts[4] - ts[3]);
+#endif
   if (warp == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(32 * NSD));
 }
 
