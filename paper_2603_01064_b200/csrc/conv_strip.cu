@@ -32,8 +32,9 @@
 // dropped Al Bl term and the representation error are ~2^-22 relative per product (BF16x3
 // would be 2^-17, which the filtered smoothing increment amplifies past 1e-5).
 //
-// Warp roles (448 threads, one CTA per SM): warps 0-7 epilogue (warp w reads TMEM lanes
-// 32 (w % 4).., channel half w / 4), warps 8-12 producer, warp 13 MMA issuer.
+// Warp roles (448 threads, one CTA per SM): warps 0 .. 4 NG - 1 epilogue (warp w reads TMEM
+// lanes 32 (w % 4).., channel group w / 4), warps 4 NG .. 12 producer, warp 13 MMA issuer;
+// NG = 1 for layers 1-2 at C = 32 (9 producer warps), else 2.
 #include <cuda.h>
 #include <cuda_fp16.h>
 
@@ -56,10 +57,17 @@ constexpr uint32_t IDESC4 = (1u << 4) | ((uint32_t)(16 >> 3) << 17) | ((uint32_t
 // warps with four all-channel epilogue warps measured slower at C = 32.)
 template <int C, bool FIRST>
 struct Roles {
-  static constexpr int NG = 2;                            // epilogue channel groups
+#ifndef NMG_STRIP_NG32
+#define NMG_STRIP_NG32 1
+#endif
+  // epilogue channel groups: layers 1-2 at C = 32 are producer-bound, so 4 all-channel
+  // epilogue warps leave 9 warps to the FFMA producer; layers 3-4 are epilogue-bound (8 warps)
+  static constexpr int NG = (FIRST && C == 32) ? NMG_STRIP_NG32 : 2;
+  // channel groups per producer item (position pair): the 130 row positions x NQ groups
+  // spread over the producer threads
+  static constexpr int NQ = NG == 1 ? 4 : 2;
   static constexpr int PROD0 = 4 * NG;                    // first producer warp
   static constexpr int NPROD = MMAW - PROD0;              // producer warps (FIRST)
-  static constexpr int CH = C;                            // channels per producer item
 };
 
 template <int C>
@@ -294,11 +302,11 @@ __global__ void __launch_bounds__(NTHR, 1)
       // 130 items over the 160 producer threads, the weights of a tap loaded once for both
       // positions; 3 x 3 windows of b slide down with the rows, the next row prefetched.
       // w0 and b0 in shared memory are pre-scaled by S1 (ReLU(S z) = S ReLU(z), S > 0).
-      constexpr int HC = C / 2;                            // channels per item
+      constexpr int HC = C / RL::NQ;                       // channels per item
       constexpr int PP = RP / 2;                           // 65 position pairs
       const int pt = tid - PROD0 * 32;
       const int j = pt % PP, half = pt / PP;
-      const bool act = pt < 2 * PP;
+      const bool act = pt < RL::NQ * PP;
       const int c0p = half * HC;
       int it = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {

@@ -1,5 +1,6 @@
-timeout 600 python -m pytest tests/test_gpu_1d.py -q -x 2>&1 | tail -1
-for v in base m5 base m5; do
+export NMG_LIB=$PWD/paper_2603_01064_b200/variants/libnmg_g1.so
+echo "g1 $(timeout 300 python -m pytest tests/test_gpu_2d.py -q -k strip 2>&1 | tail -1)"
+for v in base g1 base g1; do
   if [ $v = base ]; then unset NMG_LIB; else export NMG_LIB=$PWD/paper_2603_01064_b200/variants/libnmg_$v.so; fi
-  echo "$v: $(timeout 300 python bench.py --config 1 --steps 100 --no-cpu --no-e2e --no-solve | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["ms_per_step"], d["roofline"]["classes_ms_per_step"]["smooth"])')"
+  for c in 2 4; do echo "$v $(timeout 300 python tools/profile_cfg.py $c | grep -E 'ms/step|smooth' | tr '\n' ' ')"; done
 done
