@@ -48,13 +48,11 @@ namespace {
 
 constexpr int SEG = 128;        // pixels per strip (MMA M)
 constexpr int RP = SEG + 2;     // rows of the activation buffer (x halo)
-constexpr int NTHR = 448;
-constexpr int MMAW = 13;        // MMA warp
 constexpr uint32_t IDESC4 = (1u << 4) | ((uint32_t)(16 >> 3) << 17) | ((uint32_t)(SEG >> 4) << 24);  // N = 16
-// Warp roles: warps 0-7 epilogue (TMEM lane quarter w % 4, channel half w / 4), warps 8-12
-// producer (layers 1-2: FFMA a1, one position and all C channels per thread; layers 3-4:
-// warp 8 TMA, warp 12 layer-4 MMA issuer), warp 13 layer-2/3 MMA issuer.  (Nine producer
-// warps with four all-channel epilogue warps measured slower at C = 32.)
+// Warp roles: epilogue warps 0 .. 4 NG - 1 (TMEM lane quarter w % 4, channel group w / 4);
+// layers 1-2: producer warps 4 NG .. 12 (FFMA a1, a position pair and C / NQ channels per
+// thread), warp 13 MMA issuer; layers 3-4: warp 4 NG TMA, warp 4 NG + 1 layer-4 MMA issuer,
+// warp 4 NG + 2 layer-3 MMA issuer.
 template <int C, bool FIRST>
 struct Roles {
 #ifndef NMG_STRIP_NG32
@@ -62,11 +60,18 @@ struct Roles {
 #endif
   // epilogue channel groups: layers 1-2 at C = 32 are producer-bound, so 4 all-channel
   // epilogue warps leave 9 warps to the FFMA producer; layers 3-4 are epilogue-bound (8 warps)
-  static constexpr int NG = (FIRST && C == 32) ? NMG_STRIP_NG32 : 2;
+#ifndef NMG_STRIP_NG48L34
+#define NMG_STRIP_NG48L34 2
+#endif
+  static constexpr int NG = (FIRST && C == 32) ? NMG_STRIP_NG32 : (!FIRST && C == 48) ? NMG_STRIP_NG48L34 : 2;
   // channel groups per producer item (position pair): the 130 row positions x NQ groups
   // spread over the producer threads
   static constexpr int NQ = NG == 1 ? 4 : 2;
   static constexpr int PROD0 = 4 * NG;                    // first producer warp
+  // layers 1-2: FFMA producer warps up to warp 12; layers 3-4: one TMA warp and the layer-4
+  // MMA warp only (the rest of the threads go to the epilogue)
+  static constexpr int MMAW = FIRST ? 13 : PROD0 + 2;     // MMA issuer warp
+  static constexpr int NTHR = 32 * (MMAW + 1);
   static constexpr int NPROD = MMAW - PROD0;              // producer warps (FIRST)
 };
 
@@ -217,12 +222,13 @@ NMG_D Unit unit_of(int u, int hg, int nx, int ys) {
 
 // ------------------------------------------------------------------------------------------
 template <int C, bool FIRST>
-__global__ void __launch_bounds__(NTHR, 1)
+__global__ void __launch_bounds__(Roles<C, FIRST>::NTHR, 1)
     conv_strip_kernel(const __grid_constant__ CUtensorMap mInH, const __grid_constant__ CUtensorMap mInL,
                       StripArgs a) {
   using G = Cfg<C>;
   using RL = Roles<C, FIRST>;
   constexpr int NSTG = G::NSTG, NDB = G::NDB;
+  constexpr int MMAW = RL::MMAW, NTHR = RL::NTHR;
   constexpr int NGRP = RL::NG;
   constexpr int PROD0 = RL::PROD0;
   constexpr int CG = C / NGRP;                           // channels per epilogue thread
@@ -686,7 +692,7 @@ void launch(const CUtensorMap* mh, const CUtensorMap* ml, const StripArgs& a, in
   const int units = a.nrhs * (a.n >= SEG ? a.n / SEG : 1) * a.ysplit;
   const int grid = std::min(units, num_sms);
   CUtensorMap dummy{};
-  conv_strip_kernel<C, FIRST><<<grid, NTHR, G::SMEM, s>>>(mh ? *mh : dummy, ml ? *ml : dummy, a);
+  conv_strip_kernel<C, FIRST><<<grid, Roles<C, FIRST>::NTHR, G::SMEM, s>>>(mh ? *mh : dummy, ml ? *ml : dummy, a);
 }
 
 }  // namespace

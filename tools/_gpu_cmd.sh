@@ -1,6 +1,6 @@
-export NMG_LIB=$PWD/paper_2603_01064_b200/variants/libnmg_g1.so
-echo "g1 $(timeout 300 python -m pytest tests/test_gpu_2d.py -q -k strip 2>&1 | tail -1)"
-for v in base g1 base g1; do
+echo "base $(timeout 300 python -m pytest tests/test_gpu_2d.py -q -k "strip or full" 2>&1 | tail -1)"
+for v in base ng2 base ng2; do
   if [ $v = base ]; then unset NMG_LIB; else export NMG_LIB=$PWD/paper_2603_01064_b200/variants/libnmg_$v.so; fi
-  for c in 2 4; do echo "$v $(timeout 300 python tools/profile_cfg.py $c | grep -E 'ms/step|smooth' | tr '\n' ' ')"; done
+  echo "$v $(timeout 300 python tools/profile_cfg.py 3 256 2 | grep -E 'ms/step|smooth' | tr '\n' ' ')"
+  echo "$v $(timeout 300 python tools/profile_cfg.py 2 | grep -E 'ms/step|smooth' | tr '\n' ' ')"
 done
