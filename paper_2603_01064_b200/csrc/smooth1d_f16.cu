@@ -215,8 +215,17 @@ NMG_D void stockham_pass(const float2* src, float2* dst, int m, int Ns, const fl
     const int jm = j & (Ns - 1);
     float2 w[R], v[R];
     if (Ns > 1) {   // twiddles first: independent of the data, their latency overlaps the loads
+#ifndef NMG_S1D_TWTABLE
+      // computed twiddles (no dependent table loads; accurate sincospif, exact arguments): w1 = exp(-2 pi i jm / (Ns R)) (argument exact), powers by products
+      float sn, cs;
+      sincospif(-2.0f * (float)jm / (float)(Ns * R), &sn, &cs);
+      w[1] = make_float2(cs, sn);
+#pragma unroll
+      for (int r = 2; r < R; ++r) w[r] = cmul(w[r - 1], w[1]);
+#else
 #pragma unroll
       for (int r = 1; r < R; ++r) w[r] = twid(tw, tw_n, jm * r * tstep);
+#endif
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) v[r] = src[sw(j + r * q)];
@@ -258,8 +267,18 @@ NMG_D void level_filter_row(float2* z, float2* t, int n, const float2* __restric
 #pragma unroll
     for (int u = 0; u < UNP; ++u) {   // twiddle loads of all iterations first
       const int k = min(k0 + u * nthr, m >> 1);
+#ifndef NMG_S1D_TWTABLE
+      {
+        float sn, cs;
+        sincospif(-2.0f * (float)k / (float)n, &sn, &cs);
+        Wv[u] = make_float2(cs, sn);
+        sincospif(-2.0f * (float)((m - k) & (m - 1)) / (float)n, &sn, &cs);
+        W2v[u] = make_float2(cs, sn);
+      }
+#else
       Wv[u] = __ldg(tw + k * wstep);
       W2v[u] = __ldg(tw + ((m - k) & (m - 1)) * wstep);
+#endif
     }
 #pragma unroll
     for (int u = 0; u < UNP; ++u) {
