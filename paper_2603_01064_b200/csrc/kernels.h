@@ -172,6 +172,9 @@ void prolong_add1d(int nrhs, int n_c, const float* c, int64_t ldc, float* f, int
 void filter1d(int n, int nrhs, const float* in, float* out, const float2* tw, int tw_n, cudaStream_t s);
 
 // ---- coarse solve: Cholesky factor applied by forward/back substitution ---------
+// same result with the explicit fp64 inverse A_L^{-1} (symmetric [nc][nc], nc <= 256)
+void coarse_inv_apply(int nc, int nrhs, const double* Ainv, const float* y, int64_t ldy, float* x, int64_t ldx,
+                      cudaStream_t s, float* xh = nullptr, float* xl = nullptr);
 void coarse_chol_solve(int nc, int nrhs, const double* Lrow, const double* Lcol,
                        const float* y, int64_t ldy, float* x, int64_t ldx, cudaStream_t s,
                        float* xh = nullptr, float* xl = nullptr);

@@ -75,6 +75,59 @@ NMG_D void coarse_issue_panel(int p, int nc, const double* Lrow, const double* L
 
 constexpr int kCoarseWarps = 4;   // RHS per CTA: few, so that many SMs share the issue load
 
+// x = A_L^{-1} y with the explicit fp64 inverse (symmetric, computed once from the Cholesky
+// factor at setup): thread j forms x_j for CR right-hand sides; the Ainv[k][j] loads of a warp
+// are coalesced and independent of the accumulation, so there is no sequential substitution
+// chain.  Fixed summation order k = 0 .. nc - 1 (deterministic).
+constexpr int kCoarseRhs = 8;
+__global__ void __launch_bounds__(256) coarse_inv_kernel(int nc, int nrhs, const double* __restrict__ Ainv,
+                                                         const float* __restrict__ y, int64_t ldy,
+                                                         float* __restrict__ x, int64_t ldx,
+                                                         float* __restrict__ xh, float* __restrict__ xl) {
+  __shared__ double ys[kCoarseRhs][256];
+  const int b0 = blockIdx.x * kCoarseRhs;
+  for (int i = threadIdx.x; i < kCoarseRhs * nc; i += blockDim.x) {
+    const int r = i / nc, k = i - r * nc;
+    ys[r][k] = (b0 + r < nrhs) ? (double)y[(int64_t)(b0 + r) * ldy + k] : 0.0;
+  }
+  __syncthreads();
+  const int j = blockIdx.y * blockDim.x + threadIdx.x;   // output index (column slice per CTA)
+  if (j < nc) {
+    double acc[kCoarseRhs];
+#pragma unroll
+    for (int r = 0; r < kCoarseRhs; ++r) acc[r] = 0.0;
+    // register double buffer: the next 8 Ainv values are in flight while 8 are used
+    double av[8], an[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) av[i] = __ldg(Ainv + (int64_t)min(i, nc - 1) * nc + j);
+    for (int k0 = 0; k0 < nc; k0 += 8) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) an[i] = __ldg(Ainv + (int64_t)min(k0 + 8 + i, nc - 1) * nc + j);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (k0 + i >= nc) break;
+#pragma unroll
+        for (int r = 0; r < kCoarseRhs; ++r) acc[r] = fma(av[i], ys[r][k0 + i], acc[r]);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) av[i] = an[i];
+    }
+#pragma unroll
+    for (int r = 0; r < kCoarseRhs; ++r) {
+      if (b0 + r >= nrhs) break;
+      const float v = (float)acc[r];
+      x[(int64_t)(b0 + r) * ldx + j] = v;
+      if (xh) {
+        uint32_t hh, ll;
+        asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(hh) : "f"(v));
+        asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(ll) : "f"(v - __uint_as_float(hh)));
+        xh[(int64_t)(b0 + r) * ldx + j] = __uint_as_float(hh);
+        xl[(int64_t)(b0 + r) * ldx + j] = __uint_as_float(ll);
+      }
+    }
+  }
+}
+
 template <int NQ>
 __global__ void __launch_bounds__(kCoarseWarps * 32) coarse_kernel(int nc, int nrhs, const double* __restrict__ Lrow,
                                                      const double* __restrict__ Lcol,
@@ -245,6 +298,13 @@ void restrict1d(int nrhs, int n_f, const float* f, int64_t ldf, float* c, int64_
 
 void prolong_add1d(int nrhs, int n_c, const float* c, int64_t ldc, float* f, int64_t ldf, cudaStream_t s) {
   prolong_add1d_kernel<<<nblk((int64_t)nrhs * 2 * n_c, 256), 256, 0, s>>>(nrhs, n_c, c, ldc, f, ldf);
+}
+
+void coarse_inv_apply(int nc, int nrhs, const double* Ainv, const float* y, int64_t ldy, float* x, int64_t ldx,
+                      cudaStream_t s, float* xh, float* xl) {
+  const int bt = std::min(64, ceil_div(nc, 32) * 32);
+  coarse_inv_kernel<<<dim3(ceil_div(nrhs, kCoarseRhs), ceil_div(nc, bt)), bt, 0, s>>>(nc, nrhs, Ainv, y, ldy, x, ldx,
+                                                                                     xh, xl);
 }
 
 void coarse_chol_solve(int nc, int nrhs, const double* Lrow, const double* Lcol, const float* y, int64_t ldy,

@@ -377,6 +377,8 @@ struct nmg_hierarchy {
   std::vector<std::unique_ptr<DevBuf<uint16_t>>> WB;     // per level: hidden 1 hi, lo, hidden 2 hi, lo
   // coarse Cholesky factor (row-major L and L^T)
   DevBuf<double> Lrow, Lcol;
+  DevBuf<double> Ainv;                                   // explicit A_L^{-1} (default coarse apply)
+  bool coarse_inv = true;
   int nc = 0;
   // smoother weights per level
   std::vector<std::unique_ptr<DevBuf<float>>> W;
@@ -444,6 +446,12 @@ namespace {
 
 // levels served by the column-strip CNN kernels (conv_strip.cu)
 inline bool strip_level(int n) { return n % 128 == 0 || (n >= 16 && n < 128); }
+
+void coarse_solve(nmg_hierarchy* h, int nrhs, const float* y, int64_t ldy, float* x, int64_t ldx, cudaStream_t s,
+                  float* xh = nullptr, float* xl = nullptr) {
+  if (h->coarse_inv) coarse_inv_apply(h->nc, nrhs, h->Ainv.p, y, ldy, x, ldx, s, xh, xl);
+  else coarse_chol_solve(h->nc, nrhs, h->Lrow.p, h->Lcol.p, y, ldy, x, ldx, s, xh, xl);
+}
 
 nmg_status check_launch(nmg_hierarchy* h) {
   cudaError_t e = cudaGetLastError();
@@ -594,7 +602,7 @@ nmg_status cycle_level_1d(nmg_hierarchy* h, int l, int nrhs, cudaStream_t s) {
   if (l == h->L - 1) {
     float* xh = (!h->gemm_f16 && h->sxh.size() > (size_t)l && h->sxh[l]->p && h->nc <= 128) ? h->sxh[l]->p : nullptr;
     { Prof p(h, NMG_K_COARSE, s);
-      coarse_chol_solve(h->nc, nrhs, h->Lrow.p, h->Lcol.p, y, n, x, n, s, xh, xh ? h->sxl[l]->p : nullptr); }
+      coarse_solve(h, nrhs, y, n, x, n, s, xh, xh ? h->sxl[l]->p : nullptr); }
     h->split_fresh[l] = xh ? 1 : 0;
     return check_launch(h);
   }
@@ -794,7 +802,7 @@ nmg_status cycle_level_2d(nmg_hierarchy* h, int l, int nrhs, cudaStream_t s) {
   float* y = h->wy[l]->p;
   float* x = h->wx[l]->p;
   if (l == h->L - 1) {
-    { Prof p(h, NMG_K_COARSE, s); coarse_chol_solve(h->nc, nrhs, h->Lrow.p, h->Lcol.p, y, h->nc, x, h->nc, s); }
+    { Prof p(h, NMG_K_COARSE, s); coarse_solve(h, nrhs, y, h->nc, x, h->nc, s); }
     return check_launch(h);
   }
   float* r = h->wr[l]->p;
@@ -1183,7 +1191,7 @@ nmg_status debug_2d(nmg_hierarchy* h, int l, int op, int nrhs, const float* fin,
       return smooth2d(h, l, nrhs, fin, fout, op == NMG_OP_SMOOTH, s, op == NMG_OP_SMOOTH, op == NMG_OP_SMOOTH);
     case NMG_OP_COARSE:
       if (smoothed) return fail(NMG_ERR_INVALID_ARG, "COARSE needs level == L");
-      { Prof p(h, NMG_K_COARSE, s); coarse_chol_solve(h->nc, nrhs, h->Lrow.p, h->Lcol.p, fin, h->nc, fout, h->nc, s); }
+      { Prof p(h, NMG_K_COARSE, s); coarse_solve(h, nrhs, fin, h->nc, fout, h->nc, s); }
       return check_launch(h);
     case NMG_OP_CYCLE0:
       for (int q = l; q < h->L - 1; ++q)
@@ -1437,6 +1445,33 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
     for (int j = 0; j < Nc; ++j) Lt[(size_t)j * Nc + i] = Acoarse[(size_t)i * Nc + j];
   NMG_TRY(h->Lrow.upload(Acoarse.data(), Acoarse.size()));
   NMG_TRY(h->Lcol.upload(Lt.data(), Lt.size()));
+  {
+    // explicit inverse A_L^{-1} = L^{-T} L^{-1} (fp64, symmetric), column by column
+    const char* ce = std::getenv("NMG_COARSE");
+    h->coarse_inv = !(ce && std::string(ce) == "chol");
+    if (h->coarse_inv) {
+      std::vector<double> inv((size_t)Nc * Nc), z(Nc);
+      for (int j = 0; j < Nc; ++j) {
+        for (int i = 0; i < Nc; ++i) {           // L z = e_j
+          double v = (i == j) ? 1.0 : 0.0;
+          for (int k = 0; k < i; ++k) v -= Acoarse[(size_t)i * Nc + k] * z[k];
+          z[i] = v / Acoarse[(size_t)i * Nc + i];
+        }
+        for (int i = Nc - 1; i >= 0; --i) {      // L^T x = z
+          double v = z[i];
+          for (int k = i + 1; k < Nc; ++k) v -= Acoarse[(size_t)k * Nc + i] * z[k];
+          z[i] = v / Acoarse[(size_t)i * Nc + i];
+        }
+        for (int i = 0; i < Nc; ++i) inv[(size_t)i * Nc + j] = z[i];
+      }
+      for (int i = 0; i < Nc; ++i)               // symmetrise (exact inverse is symmetric)
+        for (int j = i + 1; j < Nc; ++j) {
+          const double v = 0.5 * (inv[(size_t)i * Nc + j] + inv[(size_t)j * Nc + i]);
+          inv[(size_t)i * Nc + j] = inv[(size_t)j * Nc + i] = v;
+        }
+      NMG_TRY(h->Ainv.upload(inv.data(), inv.size()));
+    }
+  }
 
   // twiddles exp(-2 pi i k / tw_n), k < tw_n / 2
   h->tw_n = n;
@@ -2149,7 +2184,7 @@ nmg_status nmg_debug_level_op(nmg_hierarchy* h, int32_t level, int32_t op, int32
     }
     case NMG_OP_COARSE:
       if (smoothed) return fail(NMG_ERR_INVALID_ARG, "COARSE needs level == L");
-      coarse_chol_solve(h->nc, nrhs, h->Lrow.p, h->Lcol.p, fin, n, fout, n, s);
+      coarse_solve(h, nrhs, fin, n, fout, n, s);
       break;
     case NMG_OP_CYCLE0: {
       for (int q = l; q < h->L - 1; ++q)
