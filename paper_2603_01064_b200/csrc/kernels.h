@@ -210,7 +210,12 @@ void norms_f32(int nrhs, int64_t N, const float* x, double* part, int chunks, do
 // imaginary partner of the last image when nrhs is odd (call before the writers)
 // norms (may be null): per-RHS ||b||; the writers store N(u) and x gets ||b|| F'(N(u))
 void filter2d(int nrhs, int n, float2* Z, const float2* tw, int tw_n, float* x, bool accumulate, cudaStream_t s,
-              const double* norms);
+              const double* norms, bool rows_done = false);
+// strip_combine for RHS pairs fused with filter2d's forward row FFTs: Z rows of the chunk's pairs
+// (pairs zb0 / 2 ..) hold the row-transformed N(u) (0 where ||b|| = 0); zb0 and nrhs even
+// unless the chunk ends the batch
+void combine_rows_fft(int n, int nrhs, const float* q, const double* norms, const float* b3, float2* Z, int zb0,
+                      const float2* tw, int tw_n, cudaStream_t s);
 void filter2d_prepare(int nrhs, int n, float2* Z, cudaStream_t s, int rows = 0);
 // per-RHS sum of squares (no sqrt) of N values at x + b img + off
 void sumsq_f32(int nrhs, int64_t N, const float* x, int64_t img, int64_t off, double* part, int chunks, double* out,

@@ -299,6 +299,45 @@ __global__ void __launch_bounds__(256) fft_rows_kernel(int n, int64_t nrows, flo
   }
 }
 
+// combine + forward row FFT: CTA = R rows of one pair image; h(y, x) = b3 + Q0(x-1) + Q1(x) + Q2(x+1)
+// of RHS 2p (real part) and 2p + 1 (imaginary part), 0 for a RHS with ||b|| = 0 or beyond nrhs
+__global__ void __launch_bounds__(256) combine_rows_fft_kernel(int n, int nrhs, const float4* __restrict__ Q,
+                                                               const double* __restrict__ norms,
+                                                               const float* __restrict__ b3, float2* __restrict__ Z,
+                                                               int zp0, const float2* __restrict__ tw, int tw_n) {
+  extern __shared__ __align__(16) float2 cb[];
+  const int R = max(1, 4096 / n);
+  const int rpi = (n + R - 1) / R;                         // CTAs per pair image
+  const int p = blockIdx.x / rpi, y0 = (blockIdx.x - p * rpi) * R;
+  const int rows = min(R, n - y0);
+  const float bias = __ldg(b3);
+  const int b0 = 2 * p, b1 = 2 * p + 1;
+  const bool on0 = b0 < nrhs && (norms ? norms[b0] != 0.0 : true);
+  const bool on1 = b1 < nrhs && (norms ? norms[b1] != 0.0 : true);
+  const int64_t per = (int64_t)n * n;
+  for (int i = threadIdx.x; i < rows * n; i += 256) {
+    const int y = y0 + i / n, x = i % n;
+    float h[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const bool on = e ? on1 : on0;
+      float acc = 0.f;
+      if (on) {
+        const int64_t idx = (int64_t)(e ? b1 : b0) * per + (int64_t)y * n + x;
+        acc = bias + __ldg(&Q[idx].y);
+        if (x > 0) acc += __ldg(&Q[idx - 1].x);
+        if (x < n - 1) acc += __ldg(&Q[idx + 1].z);
+      }
+      h[e] = acc;
+    }
+    cb[i] = make_float2(h[0], h[1]);
+  }
+  __syncthreads();
+  fft_dif_forward_batch(cb, n, rows, n, 1, tw, tw_n, threadIdx.x, 256);
+  float2* Zp = Z + (int64_t)(zp0 + p) * per + (int64_t)y0 * n;
+  for (int i = threadIdx.x; i < rows * n; i += 256) Zp[i] = cb[i];
+}
+
 // columns: CTA = (group of G columns, RHS); DIF forward along i2, mask, DIT inverse
 __global__ void __launch_bounds__(256) fft_cols_kernel(int n, int G, float2* __restrict__ Z,
                                                        const float2* __restrict__ tw, int tw_n) {
@@ -423,7 +462,7 @@ void cnn2d(const Cnn2dArgs& a, cudaStream_t s) {
   }
 }
 void filter2d(int nrhs, int n, float2* Z, const float2* tw, int tw_n, float* x, bool accumulate, cudaStream_t s,
-              const double* norms) {
+              const double* norms, bool rows_done) {
   // paired layout: (nrhs + 1) / 2 complex images, each the real-part / imaginary-part pair of
   // two right-hand sides; F' is real and symmetric, so Re and Im of the filtered pair are the
   // two filtered images (the odd RHS out has a zero partner, zeroed by filter2d_prepare)
@@ -432,8 +471,9 @@ void filter2d(int nrhs, int n, float2* Z, const float2* tw, int tw_n, float* x, 
   const int R = std::max(1, 4096 / n);
   const size_t smr = sizeof(float2) * (size_t)R * n;
   cudaFuncSetAttribute(fft_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
-  fft_rows_kernel<<<nblk(nrows, R), 256, smr, s>>>(n, nrows, Z, tw, tw_n, 0, nullptr, 0, 1.f, nrhs, nullptr, n,
-                                                   (int64_t)n * n, 0);
+  if (!rows_done)
+    fft_rows_kernel<<<nblk(nrows, R), 256, smr, s>>>(n, nrows, Z, tw, tw_n, 0, nullptr, 0, 1.f, nrhs, nullptr, n,
+                                                     (int64_t)n * n, 0);
   static const int cols_elems = [] {   // complex elements per column-pass CTA (dev knob)
     const char* e = std::getenv("NMG_FFT_COLS_KB");
     return (e ? std::atoi(e) : 32) * 1024 / 8;
@@ -482,6 +522,15 @@ void filter2d_slab_cols(int n, int npair, int R, int W, int rank, float2* buf, c
   const size_t smc = sizeof(float2) * (size_t)n * G;
   cudaFuncSetAttribute(fft_cols_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
   fft_cols_slab_kernel<<<dim3(cw / G, npair), 256, smc, s>>>(n, G, R, cw, npair, buf, tw, tw_n, rank * cw);
+}
+void combine_rows_fft(int n, int nrhs, const float* q, const double* norms, const float* b3, float2* Z, int zb0,
+                      const float2* tw, int tw_n, cudaStream_t s) {
+  const int R = std::max(1, 4096 / n);
+  const int npair = (nrhs + 1) / 2;
+  const size_t smr = sizeof(float2) * (size_t)R * n;
+  cudaFuncSetAttribute(combine_rows_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
+  combine_rows_fft_kernel<<<npair * ceil_div(n, R), 256, smr, s>>>(n, nrhs, reinterpret_cast<const float4*>(q), norms,
+                                                                   b3, Z, zb0 / 2, tw, tw_n);
 }
 void filter2d_prepare(int nrhs, int n, float2* Z, cudaStream_t s, int rows) {
   if (rows <= 0) rows = n;

@@ -369,6 +369,7 @@ struct nmg_hierarchy {
   // 2D CNN on tcgen05 FP16x3 column-strip kernels (levels with n % 128 == 0, C = 32 / 48)
   bool conv_bf = false;
   int bf_C = 0, bf_chunk = 0;
+  bool fuse_combine = true;                              // NMG_FUSE_COMBINE=0: separate combine + row FFT
   int64_t bf_px = 0;                                     // pixels per RHS the a2 / q workspaces hold
   std::vector<float> strip_sc;                           // per level: S1, T1, S2, T2
   DevBuf<uint16_t> a2h, a2l;                             // [chunk][n][n][C] f16 hi / lo (scaled by S2)
@@ -743,12 +744,20 @@ nmg_status smooth2d(nmg_hierarchy* h, int l, int nrhs, const float* b, float* x,
       a.d_scale = 1.0f / (sc[2] * dbg * sc[3]);
       a.w4 = wb + 4 * plane; a.a3_scale = sc[4] * dbg; a.d4_scale = 1.0f / (sc[4] * dbg * sc[5]);
       { Prof p(h, NMG_K_SMOOTH, s); strip_l34(&h->mA2h[l], &h->mA2l[l], a, h->num_sms, s); }
-      { Prof p(h, NMG_K_SMOOTH, s);
-        strip_combine(n, cnt, h->qbuf.p, a.norms, b3, filt ? h->Z.p : nullptr, r0, x + off, accumulate, s); }
+      if (filt && h->fuse_combine) {
+        // h = s (b3 + Q0 + Q1 + Q2) for the chunk's RHS pairs, straight into the forward row FFT
+        { Prof p(h, NMG_K_SMOOTH, s);
+          combine_rows_fft(n, cnt, h->qbuf.p, a.norms, b3, h->Z.p, r0, h->tw.p, h->tw_n, s); }
+      } else {
+        { Prof p(h, NMG_K_SMOOTH, s);
+          strip_combine(n, cnt, h->qbuf.p, a.norms, b3, filt ? h->Z.p : nullptr, r0, x + off, accumulate, s); }
+      }
       NMG_TRY(check_launch(h));
     }
     if (filt) {
-      { Prof p(h, NMG_K_SMOOTH, s); filter2d(nrhs, n, h->Z.p, h->tw.p, h->tw_n, x, accumulate, s, normalize ? h->snorm.p : nullptr); }
+      { Prof p(h, NMG_K_SMOOTH, s);
+        filter2d(nrhs, n, h->Z.p, h->tw.p, h->tw_n, x, accumulate, s, normalize ? h->snorm.p : nullptr,
+                 h->fuse_combine); }
       NMG_TRY(check_launch(h));
     }
     return NMG_OK;
@@ -1607,6 +1616,8 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
       // FP16x3 column-strip kernels for levels with n % 128 == 0 (NMG_CONV=tf32 keeps the
       // older 3xTF32 pixel-N kernel at every level, C = 32 only)
       h->conv_bf = h->conv_tc && !(env && std::string(env) == "tf32");
+      const char* fe = std::getenv("NMG_FUSE_COMBINE");
+      h->fuse_combine = !(fe && std::string(fe) == "0");
       int sms = 0;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d.device);
       h->num_sms = sms > 0 ? sms : 148;
@@ -1889,6 +1900,7 @@ nmg_status nmg_load_smoother_weights(nmg_hierarchy* h, int32_t level, const nmg_
           const int64_t cmax = std::max<int64_t>(1, std::min<int64_t>(B, budget / per));
           const int64_t nch = (B + cmax - 1) / cmax;
           h->bf_chunk = (int)((B + nch - 1) / nch);
+          if (h->bf_chunk > 1 && h->bf_chunk < B) h->bf_chunk &= ~1;   // even: filter pairs never straddle chunks
           h->bf_px = px;
           NMG_TRY(h->a2h.alloc((size_t)h->bf_chunk * px * C));
           NMG_TRY(h->a2l.alloc((size_t)h->bf_chunk * px * C));

@@ -1,2 +1,4 @@
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"conv_strip" -c 2 -o gpurun_out/ncu_strip4 -f python tools/profile_cfg.py 2 256 1 > /dev/null 2>&1; echo "ncu2 $?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"conv_strip" -c 2 -o gpurun_out/ncu_strip48 -f python tools/profile_cfg.py 3 64 1 > /dev/null 2>&1; echo "ncu3 $?"
+timeout 900 python -m pytest tests/test_gpu_2d.py tests/test_gpu_slab.py tests/test_gpu_variants.py -q -x 2>&1 | tail -1
+for f in 1 0 1 0; do
+  for c in 2 4; do echo "fuse $f $(NMG_FUSE_COMBINE=$f timeout 300 python tools/profile_cfg.py $c | grep -E 'ms/step|smooth' | tr '\n' ' ')"; done
+done
