@@ -184,3 +184,46 @@ def test_slab_full_config4_w8_vs_unsharded():
     print("slab W=8 vs unsharded: x rel diff", d, "relres", res[0][1], rr.cpu().numpy())
     assert d < 1e-5
     assert np.allclose(res[0][1], rr.cpu().numpy(), rtol=1e-5)
+
+
+@pytest.mark.parametrize("filt,nu1,nu2", [(False, 1, 1), (True, 1, 0), (True, 0, 1)])
+def test_slab_variants_vs_unsharded(filt, nu1, nu2, prob2):
+    """Cycle variants on the sharded path (filter off, no post-smoothing, no pre-smoothing) with
+    an odd batch (the last level-filter pair has a zero partner): one cycle equals the unsharded
+    GPU path (same kernels; rank sums in a fixed order)."""
+    f, W, y, H = prob2
+    cfg = CFG2.replace(nu1=nu1, nu2=nu2)
+    comms = nmg.Comm.emulated(2)
+    ys = split_slabs(y, cfg.n, 2)
+    out, errs = [None, None], []
+
+    def rank_main(r):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                h = nmg.Hierarchy(2, cfg.n, cfg.levels, cfg.alpha, f, nu1=nu1, nu2=nu2, level_filter=filt,
+                                  max_rhs=3, comm=comms[r])
+                for l, w in enumerate(W):
+                    h.load_weights(l + 1, ni.cnn_arch(cfg), w)
+                yd = torch.tensor(np.ascontiguousarray(ys[r]), dtype=torch.float64, device=DEV)
+                xd = torch.zeros_like(yd)
+                h.vcycle(yd, xd)
+                torch.cuda.synchronize()
+                out[r] = xd.cpu().numpy()
+                h.close()
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    ts = [threading.Thread(target=rank_main, args=(r,)) for r in range(2)]
+    [t.start() for t in ts]
+    [t.join(timeout=600) for t in ts]
+    [c.close() for c in comms]
+    assert not errs, errs
+    xs = join_slabs(out, cfg.n)
+    h = nmg.Hierarchy(2, cfg.n, cfg.levels, cfg.alpha, f, nu1=nu1, nu2=nu2, level_filter=filt, max_rhs=3)
+    for l, w in enumerate(W):
+        h.load_weights(l + 1, ni.cnn_arch(cfg), w)
+    yd = torch.tensor(y, dtype=torch.float64, device=DEV)
+    xd = torch.zeros_like(yd)
+    h.vcycle(yd, xd)
+    assert rel_l2(xs, xd.cpu().numpy().reshape(xs.shape)) < 1e-6
