@@ -415,11 +415,12 @@ struct nmg_hierarchy {
   // RHS lanes: a second hierarchy (same operators and weights) cycles the second half of a
   // large batch on a forked stream, so the two halves' kernels overlap (fills the last wave of
   // each launch and the small coarse-level grids); both halves are captured in one graph
-  std::unique_ptr<nmg_hierarchy> lane2;
-  int lane_mult = 1;                                     // 2 while both lanes run (GEMM tile choice)
+  std::vector<std::unique_ptr<nmg_hierarchy>> lanes;     // lanes 1 .. K-1 (lane 0 is this handle)
+  int lane_mult = 1;                                     // K while the lanes run (GEMM tile choice)
   bool lane_tiles = true;                                // NMG_LANE_TILES=0: per-lane tile choice
-  cudaStream_t s2 = nullptr;
-  cudaEvent_t evf = nullptr, evj = nullptr;
+  std::vector<cudaStream_t> ls;                          // one forked stream per extra lane
+  cudaEvent_t evf = nullptr;
+  std::vector<cudaEvent_t> evj;
   // slab-sharded single-system mode (nmg_create_hierarchy_slab)
   bool slab = false;
   nmg_comm* comm = nullptr;                              // not owned
@@ -432,9 +433,9 @@ struct nmg_hierarchy {
   DevBuf<double> t64send, t64recv, dscratch, ssum, rsum, ysq;
   DevBuf<float2> zs, za, zb;
   ~nmg_hierarchy() {
-    if (s2) cudaStreamDestroy(s2);
+    for (auto x : ls) cudaStreamDestroy(x);
     if (evf) cudaEventDestroy(evf);
-    if (evj) cudaEventDestroy(evj);
+    for (auto e : evj) cudaEventDestroy(e);
     for (auto e : ev_pool) cudaEventDestroy(e);
     for (auto& g : graphs) if (g.exec) cudaGraphExecDestroy(g.exec);
     for (auto e : hev) cudaEventDestroy(e);
@@ -1224,29 +1225,41 @@ namespace {
 // small configs and coarse levels).
 nmg_status graph_cycle(nmg_hierarchy* h, int nrhs, const double* y, double* x, cudaStream_t s) {
   auto body = [&]() -> nmg_status {
-    nmg_hierarchy* h2 = h->lane2.get();
-    if (!h2 || h->prof_on || nrhs < 2 * 128 || s == nullptr) {
+    const int K = (int)h->lanes.size() + 1;
+    if (K == 1 || h->prof_on || nrhs < K * 128 || s == nullptr) {
       NMG_TRY(ynorms(h, nrhs, y, s));
       return outer_step(h, nrhs, y, x, -1.0, false, s);
     }
-    // two lanes: RHS [0, n0) on s, [n0, nrhs) on the forked stream s2 (RHS are independent)
-    const int n0 = (nrhs / 2 + 127) / 128 * 128;
-    const int n1 = nrhs - n0;
+    // K lanes: RHS [off_k, off_k+1) on lane k (lane 0 = this handle on s, lane k > 0 on its
+    // forked stream); the RHS are independent, so the lanes' kernels overlap
+    int off[9];
+    for (int k = 0; k <= K; ++k) off[k] = std::min(nrhs, (nrhs * k / K + 127) / 128 * 128);
+    off[K] = nrhs;
     const int64_t N = h->N[0];
     NMG_CUDA(cudaEventRecord(h->evf, s));
-    NMG_CUDA(cudaStreamWaitEvent(h->s2, h->evf, 0));
-    const int64_t l2 = h2->launches;
-    // the two lanes' GEMMs run concurrently: pick the tile width for the whole batch
-    h->lane_mult = h2->lane_mult = h->lane_tiles ? 2 : 1;
-    nmg_status st = ynorms(h2, n1, y + n0 * N, h->s2);
-    if (st == NMG_OK) st = outer_step(h2, n1, y + n0 * N, x + n0 * N, -1.0, false, h->s2);
-    h->launches += h2->launches - l2;
-    if (st == NMG_OK) st = ynorms(h, n0, y, s);
-    if (st == NMG_OK) st = outer_step(h, n0, y, x, -1.0, false, s);
-    h->lane_mult = h2->lane_mult = 1;
+    nmg_status st = NMG_OK;
+    const int mult = h->lane_tiles ? K : 1;     // concurrent GEMMs: tile width for the whole batch
+    h->lane_mult = mult;
+    for (int k = 1; k < K && st == NMG_OK; ++k) {
+      nmg_hierarchy* hk = h->lanes[k - 1].get();
+      const int cnt = off[k + 1] - off[k];
+      if (cnt <= 0) continue;
+      NMG_CUDA(cudaStreamWaitEvent(h->ls[k - 1], h->evf, 0));
+      const int64_t l0 = hk->launches;
+      hk->lane_mult = mult;
+      st = ynorms(hk, cnt, y + off[k] * N, h->ls[k - 1]);
+      if (st == NMG_OK) st = outer_step(hk, cnt, y + off[k] * N, x + off[k] * N, -1.0, false, h->ls[k - 1]);
+      hk->lane_mult = 1;
+      h->launches += hk->launches - l0;
+    }
+    if (st == NMG_OK) st = ynorms(h, off[1], y, s);
+    if (st == NMG_OK) st = outer_step(h, off[1], y, x, -1.0, false, s);
+    h->lane_mult = 1;
     NMG_TRY(st);
-    NMG_CUDA(cudaEventRecord(h->evj, h->s2));
-    NMG_CUDA(cudaStreamWaitEvent(s, h->evj, 0));
+    for (int k = 1; k < K; ++k) {
+      NMG_CUDA(cudaEventRecord(h->evj[k - 1], h->ls[k - 1]));
+      NMG_CUDA(cudaStreamWaitEvent(s, h->evj[k - 1], 0));
+    }
     return NMG_OK;
   };
   if (!h->use_graph || h->slab || s == nullptr || h->prof_on) return body();
@@ -1702,20 +1715,32 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
   NMG_TRY(h->active.alloc(B));
   {
     const char* le = std::getenv("NMG_LANES");
-    if (d.dim == 1 && d.max_rhs >= 512 && !(le && std::string(le) == "1")) {
+    int K = le ? std::max(1, std::min(8, std::atoi(le))) : 4;
+    if (d.dim != 1) K = 1;
+    while (K > 1 && d.max_rhs < K * 256) --K;            // lanes of >= 256 RHS
+    if (K > 1) {
       nmg_problem_desc d2 = d;
-      d2.max_rhs = d.max_rhs / 2;
-      setenv("NMG_LANES", "1", 1);                       // the lane itself has no lanes
-      nmg_hierarchy* raw = nullptr;
-      const nmg_status st = nmg_create_hierarchy(&d2, factors, &raw);
+      d2.max_rhs = (d.max_rhs + K - 1) / K + 128;         // a lane's share (rounded to 128-RHS tiles)
+      setenv("NMG_LANES", "1", 1);                       // a lane itself has no lanes
+      nmg_status st = NMG_OK;
+      for (int k = 1; k < K && st == NMG_OK; ++k) {
+        nmg_hierarchy* raw = nullptr;
+        st = nmg_create_hierarchy(&d2, factors, &raw);
+        if (st == NMG_OK) h->lanes.emplace_back(raw);
+      }
       if (le) setenv("NMG_LANES", le, 1); else unsetenv("NMG_LANES");
       NMG_TRY(st);
-      h->lane2.reset(raw);
       const char* lt = std::getenv("NMG_LANE_TILES");
       h->lane_tiles = !(lt && std::string(lt) == "0");
-      NMG_CUDA(cudaStreamCreateWithFlags(&h->s2, cudaStreamNonBlocking));
       NMG_CUDA(cudaEventCreateWithFlags(&h->evf, cudaEventDisableTiming));
-      NMG_CUDA(cudaEventCreateWithFlags(&h->evj, cudaEventDisableTiming));
+      for (int k = 1; k < K; ++k) {
+        cudaStream_t x;
+        cudaEvent_t e;
+        NMG_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+        h->ls.push_back(x);
+        NMG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        h->evj.push_back(e);
+      }
     }
   }
   NMG_CUDA(cudaDeviceSynchronize());
@@ -1989,7 +2014,7 @@ nmg_status nmg_load_smoother_weights(nmg_hierarchy* h, int32_t level, const nmg_
     }
   }
   h->w_loaded[level - 1] = 1;
-  if (h->lane2) NMG_TRY(nmg_load_smoother_weights(h->lane2.get(), level, arch, params, n_params));
+  for (auto& hk : h->lanes) NMG_TRY(nmg_load_smoother_weights(hk.get(), level, arch, params, n_params));
   h->arch = *arch;
   return NMG_OK;
 }

@@ -1,4 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu_2d.py tests/test_gpu_slab.py tests/test_gpu_variants.py -q -x 2>&1 | tail -1
-for f in 1 0 1 0; do
-  for c in 2 4; do echo "fuse $f $(NMG_FUSE_COMBINE=$f timeout 300 python tools/profile_cfg.py $c | grep -E 'ms/step|smooth' | tr '\n' ' ')"; done
-done
+timeout 600 python -m pytest tests/test_gpu_1d.py -q -x -k "lanes or cycle" 2>&1 | tail -1
+for ln in 2 3 4 2 3 4; do echo "lanes $ln: $(NMG_LANES=$ln timeout 300 python bench.py --config 1 --steps 100 --no-cpu --no-e2e --no-solve | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["ms_per_step"], d["value"])')"; done
