@@ -616,8 +616,12 @@ __global__ void __launch_bounds__(Roles<C, FIRST>::NTHR, 1)
               }
               uint4 hi, lo;
               split8(v, hi, lo);
+#ifndef NMG_STRIP_NOSTORE
               reinterpret_cast<uint4*>(a.out_h + off)[g] = hi;
               reinterpret_cast<uint4*>(a.out_l + off)[g] = lo;
+#else
+              if (hi.x == 0x7fffffffu && lo.x == 0x7fffffffu) reinterpret_cast<uint4*>(a.out_h + off)[g] = hi;
+#endif
             }
           } else {
             float v[8];

@@ -1,2 +1,6 @@
-timeout 600 python -m pytest tests/test_gpu_1d.py -q -x -k "lanes or cycle" 2>&1 | tail -1
-for ln in 2 3 4 2 3 4; do echo "lanes $ln: $(NMG_LANES=$ln timeout 300 python bench.py --config 1 --steps 100 --no-cpu --no-e2e --no-solve | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["ms_per_step"], d["value"])')"; done
+export NMG_LIB=$PWD/paper_2603_01064_b200/variants/libnmg_twc.so
+echo "twc $(timeout 600 python -m pytest tests/test_gpu_2d.py -q -x 2>&1 | tail -1)"
+for v in base twc base twc; do
+  if [ $v = base ]; then unset NMG_LIB; else export NMG_LIB=$PWD/paper_2603_01064_b200/variants/libnmg_$v.so; fi
+  for c in 2 4; do echo "$v $(timeout 300 python tools/profile_cfg.py $c | grep -E 'smooth' | tr '\n' ' ')"; done
+done
