@@ -66,11 +66,16 @@ struct Roles {
   static constexpr int NG = (FIRST && C == 32) ? NMG_STRIP_NG32 : (!FIRST && C == 48) ? NMG_STRIP_NG48L34 : 2;
   // channel groups per producer item (position pair): the 130 row positions x NQ groups
   // spread over the producer threads
-  static constexpr int NQ = NG == 1 ? 4 : 2;
+#ifndef NMG_STRIP_P48
+#define NMG_STRIP_P48 7
+#endif
+  // layers 1-2 at C = 48: NMG_STRIP_P48 producer warps; 7 warps split a pixel pair's channels
+  // in three groups of 16 (195 items)
+  static constexpr int NQ = NG == 1 ? 4 : (FIRST && C == 48 && NMG_STRIP_P48 == 7) ? 3 : 2;
   static constexpr int PROD0 = 4 * NG;                    // first producer warp
   // layers 1-2: FFMA producer warps up to warp 12; layers 3-4: one TMA warp and the layer-4
   // MMA warp only (the rest of the threads go to the epilogue)
-  static constexpr int MMAW = FIRST ? 13 : PROD0 + 2;     // MMA issuer warp
+  static constexpr int MMAW = FIRST ? (C == 48 ? PROD0 + NMG_STRIP_P48 : 13) : PROD0 + 2;   // MMA issuer warp
   static constexpr int NTHR = 32 * (MMAW + 1);
   static constexpr int NPROD = MMAW - PROD0;              // producer warps (FIRST)
 };
