@@ -44,6 +44,59 @@ __global__ void restrict2d_kernel(int nrhs, int n_c, const float* __restrict__ f
 
 NMG_D float p1d(float cj, float ck) { return __fadd_rn(__fmul_rn(0.75f, cj), __fmul_rn(0.25f, ck)); }
 
+// vectorised restriction: thread = coarse (j2, 2s), (j2, 2s + 1) from 4 fine rows x fine columns
+// 4s - 1 .. 4s + 4 (a float4 + two scalars per row); same expression order (bitwise)
+__global__ void restrict2d_x2_kernel(int nrhs, int n_c, const float* __restrict__ f, float* __restrict__ c) {
+  const int hc = n_c >> 1;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t per = (int64_t)n_c * hc;
+  if (idx >= nrhs * per) return;
+  const int b = (int)(idx / per);
+  const int rem = (int)(idx - b * per);
+  const int j2 = rem / hc, sidx = rem - j2 * hc;
+  const int n_f = 2 * n_c;
+  const float* F = f + (int64_t)b * n_f * n_f;
+  const int c2[4] = {max(2 * j2 - 1, 0), 2 * j2, 2 * j2 + 1, min(2 * j2 + 2, n_f - 1)};
+  const int xm = max(4 * sidx - 1, 0), xp = min(4 * sidx + 4, n_f - 1);
+  float r0[4], r1[4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const float* row = F + (int64_t)c2[a] * n_f;
+    const float4 m = *reinterpret_cast<const float4*>(row + 4 * sidx);
+    r0[a] = r1d(row[xm], m.x, m.y, m.z);
+    r1[a] = r1d(m.y, m.z, m.w, row[xp]);
+  }
+  *reinterpret_cast<float2*>(c + ((int64_t)b * n_c + j2) * n_c + 2 * sidx) =
+      make_float2(r1d(r0[0], r0[1], r0[2], r0[3]), r1d(r1[0], r1[1], r1[2], r1[3]));
+}
+
+// vectorised prolongation: thread = fine (i2, 4t .. 4t + 3) from coarse rows j2, k2 and
+// coarse columns 2t - 1 .. 2t + 2 (bitwise prolong_add2d)
+__global__ void prolong_add2d_x4_kernel(int nrhs, int n_c, const float* __restrict__ c, float* __restrict__ f) {
+  const int q = n_c >> 1;
+  const int n_f = 2 * n_c;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t per = (int64_t)n_f * q;
+  if (idx >= nrhs * per) return;
+  const int b = (int)(idx / per);
+  const int rem = (int)(idx - b * per);
+  const int i2 = rem / q, t = rem - i2 * q;
+  const int j2 = i2 >> 1, k2 = min(max((i2 & 1) ? j2 + 1 : j2 - 1, 0), n_c - 1);
+  const float* C = c + (int64_t)b * n_c * n_c;
+  const int cm = max(2 * t - 1, 0), cp = min(2 * t + 2, n_c - 1);
+  const float* Rj = C + (int64_t)j2 * n_c;
+  const float* Rk = C + (int64_t)k2 * n_c;
+  const float j0 = Rj[2 * t], j1 = Rj[2 * t + 1], jm = Rj[cm], jp = Rj[cp];
+  const float k0 = Rk[2 * t], k1 = Rk[2 * t + 1], km = Rk[cm], kp = Rk[cp];
+  float4* fq = reinterpret_cast<float4*>(f + ((int64_t)b * n_f + i2) * n_f) + t;
+  float4 v = *fq;
+  v.x = __fadd_rn(v.x, p1d(p1d(j0, jm), p1d(k0, km)));
+  v.y = __fadd_rn(v.y, p1d(p1d(j0, j1), p1d(k0, k1)));
+  v.z = __fadd_rn(v.z, p1d(p1d(j1, j0), p1d(k1, k0)));
+  v.w = __fadd_rn(v.w, p1d(p1d(j1, jp), p1d(k1, kp)));
+  *fq = v;
+}
+
 __global__ void prolong_add2d_kernel(int nrhs, int n_c, const float* __restrict__ c, float* __restrict__ f) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int n_f = 2 * n_c;
@@ -428,10 +481,16 @@ __global__ void real_to_complex_kernel(int nrhs, int64_t N, const float* __restr
 
 void restrict2d(int nrhs, int n_f, const float* f, float* c, cudaStream_t s) {
   const int n_c = n_f / 2;
-  restrict2d_kernel<<<nblk((int64_t)nrhs * n_c * n_c, 256), 256, 0, s>>>(nrhs, n_c, f, c);
+  if (n_c % 2 == 0 && ((uintptr_t)f & 15) == 0 && ((uintptr_t)c & 7) == 0)
+    restrict2d_x2_kernel<<<nblk((int64_t)nrhs * n_c * (n_c / 2), 256), 256, 0, s>>>(nrhs, n_c, f, c);
+  else
+    restrict2d_kernel<<<nblk((int64_t)nrhs * n_c * n_c, 256), 256, 0, s>>>(nrhs, n_c, f, c);
 }
 void prolong_add2d(int nrhs, int n_c, const float* c, float* f, cudaStream_t s) {
-  prolong_add2d_kernel<<<nblk((int64_t)nrhs * 4 * n_c * n_c, 256), 256, 0, s>>>(nrhs, n_c, c, f);
+  if (n_c % 2 == 0 && ((uintptr_t)f & 15) == 0)
+    prolong_add2d_x4_kernel<<<nblk((int64_t)nrhs * 2 * n_c * (n_c / 2), 256), 256, 0, s>>>(nrhs, n_c, c, f);
+  else
+    prolong_add2d_kernel<<<nblk((int64_t)nrhs * 4 * n_c * n_c, 256), 256, 0, s>>>(nrhs, n_c, c, f);
 }
 void qstencil(int nrhs, int n, int hb, float alpha, const float* Q, const float* X, const float* C, float* D,
               cudaStream_t s) {

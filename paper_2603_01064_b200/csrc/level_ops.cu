@@ -28,7 +28,45 @@ __global__ void restrict1d_kernel(int nrhs, int n_c, const float* __restrict__ f
   c[(int64_t)b * ldc + j] = __fmul_rn(__fadd_rn(outer, inner), 0.125f);
 }
 
+// vectorised: thread = coarse outputs 2s, 2s + 1 from fine 4s - 1 .. 4s + 4 (one float4 load
+// + two scalars); same expression order as restrict1d_kernel (bitwise)
+__global__ void restrict1d_x2_kernel(int nrhs, int n_c, const float* __restrict__ f, int64_t ldf,
+                                     float* __restrict__ c, int64_t ldc) {
+  const int hc = n_c >> 1;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)nrhs * hc) return;
+  const int b = (int)(idx / hc), sidx = (int)(idx - (int64_t)b * hc);
+  const int n_f = 2 * n_c;
+  const float* fr = f + (int64_t)b * ldf;
+  const float4 m = *reinterpret_cast<const float4*>(fr + 4 * sidx);
+  const float fm = fr[max(4 * sidx - 1, 0)];
+  const float fp = fr[min(4 * sidx + 4, n_f - 1)];
+  float2 o;
+  o.x = __fmul_rn(__fadd_rn(__fadd_rn(fm, m.z), __fmul_rn(3.0f, __fadd_rn(m.x, m.y))), 0.125f);
+  o.y = __fmul_rn(__fadd_rn(__fadd_rn(m.y, fp), __fmul_rn(3.0f, __fadd_rn(m.z, m.w))), 0.125f);
+  *reinterpret_cast<float2*>(c + (int64_t)b * ldc + 2 * sidx) = o;
+}
+
 // ---- interpolation I_{l+1}^l and correction: f[i] += 3/4 c[i>>1] + 1/4 c[k] ----------
+// vectorised: thread = fine 4t .. 4t + 3 from coarse 2t - 1 .. 2t + 2 (bitwise prolong_add1d)
+__global__ void prolong_add1d_x4_kernel(int nrhs, int n_c, const float* __restrict__ c, int64_t ldc,
+                                        float* __restrict__ f, int64_t ldf) {
+  const int q = n_c >> 1;                          // fine quads per row
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)nrhs * q) return;
+  const int b = (int)(idx / q), t = (int)(idx - (int64_t)b * q);
+  const float* cr = c + (int64_t)b * ldc;
+  const float c0 = cr[2 * t], c1 = cr[2 * t + 1];
+  const float cm = cr[max(2 * t - 1, 0)], cp = cr[min(2 * t + 2, n_c - 1)];
+  float4* fq = reinterpret_cast<float4*>(f + (int64_t)b * ldf) + t;
+  float4 v = *fq;
+  v.x = __fadd_rn(v.x, __fadd_rn(__fmul_rn(0.75f, c0), __fmul_rn(0.25f, cm)));
+  v.y = __fadd_rn(v.y, __fadd_rn(__fmul_rn(0.75f, c0), __fmul_rn(0.25f, c1)));
+  v.z = __fadd_rn(v.z, __fadd_rn(__fmul_rn(0.75f, c1), __fmul_rn(0.25f, c0)));
+  v.w = __fadd_rn(v.w, __fadd_rn(__fmul_rn(0.75f, c1), __fmul_rn(0.25f, cp)));
+  *fq = v;
+}
+
 __global__ void prolong_add1d_kernel(int nrhs, int n_c, const float* __restrict__ c, int64_t ldc,
                                      float* __restrict__ f, int64_t ldf) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -293,11 +331,17 @@ inline int nblk(int64_t n, int t) { return (int)ceil_div64(n, t); }
 
 void restrict1d(int nrhs, int n_f, const float* f, int64_t ldf, float* c, int64_t ldc, cudaStream_t s) {
   const int n_c = n_f / 2;
-  restrict1d_kernel<<<nblk((int64_t)nrhs * n_c, 256), 256, 0, s>>>(nrhs, n_c, f, ldf, c, ldc);
+  if (n_c % 2 == 0 && ldf % 4 == 0 && ldc % 2 == 0 && ((uintptr_t)f & 15) == 0 && ((uintptr_t)c & 7) == 0)
+    restrict1d_x2_kernel<<<nblk((int64_t)nrhs * (n_c / 2), 256), 256, 0, s>>>(nrhs, n_c, f, ldf, c, ldc);
+  else
+    restrict1d_kernel<<<nblk((int64_t)nrhs * n_c, 256), 256, 0, s>>>(nrhs, n_c, f, ldf, c, ldc);
 }
 
 void prolong_add1d(int nrhs, int n_c, const float* c, int64_t ldc, float* f, int64_t ldf, cudaStream_t s) {
-  prolong_add1d_kernel<<<nblk((int64_t)nrhs * 2 * n_c, 256), 256, 0, s>>>(nrhs, n_c, c, ldc, f, ldf);
+  if (n_c % 2 == 0 && ldf % 4 == 0 && ((uintptr_t)f & 15) == 0)
+    prolong_add1d_x4_kernel<<<nblk((int64_t)nrhs * (n_c / 2), 256), 256, 0, s>>>(nrhs, n_c, c, ldc, f, ldf);
+  else
+    prolong_add1d_kernel<<<nblk((int64_t)nrhs * 2 * n_c, 256), 256, 0, s>>>(nrhs, n_c, c, ldc, f, ldf);
 }
 
 void coarse_inv_apply(int nc, int nrhs, const double* Ainv, const float* y, int64_t ldy, float* x, int64_t ldx,
