@@ -138,11 +138,23 @@ __global__ void __launch_bounds__(256) sumsq_partial_kernel(int64_t N, int chunk
                                                             double* __restrict__ part, int64_t img, int64_t off) {
   __shared__ double red[32];
   const int b = blockIdx.y, ch = blockIdx.x;
-  const int64_t len = ceil_div64(N, chunks);
-  const int64_t lo = ch * len, hi = min(N, lo + len);
   const float* r = x + (int64_t)b * img + off;
   double s = 0.0;
-  for (int64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) s += (double)r[j] * (double)r[j];
+  if ((N & 3) == 0 && (((uintptr_t)r) & 15) == 0) {
+    // float4 loads: chunk boundaries on multiples of 4 elements
+    const int64_t N4 = N >> 2, len = ceil_div64(N4, chunks);
+    const int64_t lo = ch * len, hi = min(N4, lo + len);
+    const float4* r4 = reinterpret_cast<const float4*>(r);
+    for (int64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) {
+      const float4 v = r4[j];
+      s += (double)v.x * (double)v.x + (double)v.y * (double)v.y + (double)v.z * (double)v.z +
+           (double)v.w * (double)v.w;
+    }
+  } else {
+    const int64_t len = ceil_div64(N, chunks);
+    const int64_t lo = ch * len, hi = min(N, lo + len);
+    for (int64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) s += (double)r[j] * (double)r[j];
+  }
   s = block_sum_f64(s, red);
   if (threadIdx.x == 0) part[(int64_t)b * chunks + ch] = s;
 }
