@@ -1,2 +1,1 @@
-timeout 1200 python -m pytest tests/test_gpu_2d.py tests/test_gpu_slab.py tests/test_gpu_variants.py -q -x 2>&1 | tail -1
-for c in 2 4; do echo "$(timeout 300 python tools/profile_cfg.py $c | grep -E 'ms/step|smooth' | tr '\n' ' ')"; done
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:kron_tc --launch-skip 3 -c 1 -o gpurun_out/ncu_kron1 -f python tools/profile_cfg.py 4 32 1 > /dev/null 2>&1; echo "ncu $?"
