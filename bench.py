@@ -259,15 +259,16 @@ def main():
     # config 4 over several GPUs: the single 1024^2 operator is row-sharded (slab mode, one
     # all-gather of the Kronecker intermediate per apply, all-to-all transposes in the level
     # filter); every rank holds its slab of all 32 RHS
-    slab = (cfg.dim == 2 and world > 1 and args.slab == "on") or (
+    slab = (cfg.dim == 2 and args.slab == "on") or (
         args.slab == "auto" and cid == 4 and world > 1 and os.environ.get("NMG_DIST_BACKEND", "nccl") == "nccl")
     comm = None
     if slab:
         from paper_2603_01064_b200.parallel import split_slabs
         start, global_B = 0, cfg.nrhs
         obj = [nmg.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        comm = nmg.Comm.nccl(world, rank, obj[0], local)
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0)
+        comm = nmg.Comm.nccl(world, rank, obj[0], local)   # world 1: a one-rank NCCL communicator
     elif strong:
         start, B = shard_range(cfg.nrhs, world, rank)
         global_B = cfg.nrhs
