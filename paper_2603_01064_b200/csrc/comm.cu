@@ -111,7 +111,7 @@ struct EmuGroup {
       cv.notify_all();
       return true;
     }
-    if (!cv.wait_for(lk, std::chrono::seconds(300), [&] { return gen != g || broken; }) || broken) {
+    if (!cv.wait_for(lk, std::chrono::seconds(120), [&] { return gen != g || broken; }) || broken) {
       broken = true;
       cv.notify_all();
       return false;

@@ -64,6 +64,11 @@ struct OzakiArgs {
   bool plus = false;
   const double* ax = nullptr;
   double alpha = 0.0;
+  // slab mode: generalised block mapping (as Gemm64Args: (m / tb_R) tb_img + col tb_S + m % tb_R,
+  // r32 at (m / tb_R) r32_img + r32_off + ...) and the first W row (rows wrow0 .. wrow0 + N)
+  int tb_R = 0, tb_S = 0;
+  int64_t tb_img = 0, r32_img = 0, r32_off = 0;
+  int wrow0 = 0;
 };
 int ozaki_digits();
 // digit planes [S][plane / K rows][K]: plane = (rows allocated per plane) * K

@@ -1022,6 +1022,32 @@ nmg_status cycle_slab(nmg_hierarchy* h, int l, int nrhs, cudaStream_t s) {
 nmg_status outer_residual_slab(nmg_hierarchy* h, int nrhs, const double* y, const double* x, double* r64,
                                bool want_part, cudaStream_t s) {
   const int n = h->n[0], R = h->R[0], H = h->HS, r0 = h->rank * R;
+  if (h->ozaki2d && R % 128 == 0) {
+    // the same two passes on the int8 tensor cores (Ozaki digits, as outer_residual 2D)
+    const int64_t plane = (int64_t)h->d.max_rhs * n * n;
+    { Prof p(h, NMG_K_GEMM64, s); ozaki_split_rows(nrhs * R, n, x, n, h->xdig.p, plane, h->xexp.p, s); }
+    NMG_TRY(check_launch(h));
+    OzakiArgs o{};
+    o.M = nrhs * R; o.N = n; o.K = n;
+    o.r64 = h->t64send.p; o.plus = true;
+    o.tblock = n; o.tb_R = R; o.tb_S = R; o.tb_img = (int64_t)n * R;
+    o.ex = h->xexp.p; o.ew = h->wexp.p;
+    { Prof p(h, NMG_K_GEMM64, s); ozaki_resid(&h->mXd, &h->mWd, o, s); }
+    NMG_TRY(check_launch(h));
+    NMG_TRY(h->comm->all_gather(h->t64send.p, h->t64recv.p, sizeof(double) * (size_t)nrhs * n * R, s));
+    NMG_TRY(unpack_gathered<double>(h, h->t64recv.p, h->T64.p, (int64_t)nrhs * n, R, n, s));
+    { Prof p(h, NMG_K_GEMM64, s); ozaki_split_rows(nrhs * n, n, h->T64.p, n, h->xdig.p, plane, h->xexp.p, s); }
+    NMG_TRY(check_launch(h));
+    OzakiArgs q{};
+    q.M = nrhs * n; q.N = R; q.K = n;
+    q.Y = y; q.ax = x; q.alpha = h->d.alpha;
+    q.r32 = h->sy[0]->p; q.r32_img = slab_img(h, 0); q.r32_off = (int64_t)H * n;
+    q.r64 = r64; q.part = want_part ? h->part.p : nullptr;
+    q.tblock = n; q.tb_R = n; q.tb_S = n; q.tb_img = (int64_t)R * n;
+    q.ex = h->xexp.p; q.ew = h->wexpB.p; q.wrow0 = r0;
+    { Prof p(h, NMG_K_GEMM64, s); ozaki_resid(&h->mXd, &h->mWdB, q, s); }
+    return check_launch(h);
+  }
   Gemm64Args g{};
   g.M = nrhs * R; g.N = n; g.K = n;
   g.X = x; g.ldx = n; g.W = h->C64.p; g.ldw = n;

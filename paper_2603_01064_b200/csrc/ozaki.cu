@@ -85,6 +85,8 @@ NMG_D void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t a
 // CTA pairs along N share the X digit tile: each CTA loads half of its rows and multicasts
 // it to both (halving the L2 -> SM traffic of X, which every N tile re-reads); a stage is
 // refilled only after the MMAs of BOTH CTAs released it (commit multicast, count 2).
+// GEN: the slab mode's general output mapping and W row offset (else the whole-image mapping)
+template <bool GEN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ONT, 1)
     ozaki_resid_kernel(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mW,
                        OzakiArgs a) {
@@ -123,7 +125,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ONT, 1)
 #pragma unroll
         for (int d = 0; d < OS; ++d)                 // rows [64 r, 64 r + 64) of every X digit plane
           tma3d_mc(st + d * OBM * OBK + crank * 64 * OBK, &mX, &full[s], kt * OBK, m0 + (int)crank * 64, d, 3);
-        tma3d(st + XS_BYTES, &mW, &full[s], kt * OBK, n0, 0);
+        tma3d(st + XS_BYTES, &mW, &full[s], kt * OBK, (GEN ? a.wrow0 : 0) + n0, 0);
       }
     }
     __syncwarp();
@@ -168,12 +170,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ONT, 1)
   if (a.tblock && (a.Y || a.ax)) {
     // 2D pass 2: pull the tile's y and x columns into L2 while the MMAs run (the epilogue
     // reads them column by column; a warp's 32 rows of one column are 256 contiguous bytes)
-    const int64_t tb = a.tblock;
+    const int R = GEN ? a.tb_R : a.tblock;                  // 32-bit divisions
+    const int64_t S = GEN ? a.tb_S : a.tblock;
+    const int64_t img = GEN ? a.tb_img : (int64_t)a.tblock * a.tblock;
     const int mw = m0 + warp * 32;
     if (mw < a.M && (lane & 15) == 0) {
-      const int64_t base = (int64_t)(mw / a.tblock) * tb * tb + (mw % a.tblock) + (lane >> 4) * 16;
+      const int bw = mw / R;
+      const int64_t base = (int64_t)bw * img + (mw - bw * R) + (lane >> 4) * 16;
       for (int c = 0; c < OBN; ++c) {
-        const int64_t off = base + (int64_t)(n0 + c) * tb;
+        const int64_t off = base + (int64_t)(n0 + c) * S;
         if (a.Y) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(a.Y + off));
         if (a.ax) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(a.ax + off));
       }
@@ -210,8 +215,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ONT, 1)
     // 2D Kronecker passes: transposed store within tb x tb blocks (consecutive rows m of a
     // warp write consecutive addresses); pass 1 stores +X W^T, pass 2 y - X W^T - alpha x
     const int exm = a.ex[m];
-    const int64_t tb = a.tblock;
-    const int64_t base = (int64_t)(m / a.tblock) * tb * tb + (m % a.tblock);
+    // block mapping: output (m, col) at (m / R) img + col S + m % R (R = S = tb, img = tb^2 by
+    // default; the slab mode passes its own); r32 may live in a halo'd slab (r32_img, r32_off)
+    const int R = GEN ? a.tb_R : a.tblock;                  // 32-bit divisions
+    const int64_t S = GEN ? a.tb_S : a.tblock;
+    const int64_t img = GEN ? a.tb_img : (int64_t)a.tblock * a.tblock;
+    const int bi = m / R;
+    const int64_t base = (int64_t)bi * img + (m - bi * R);
+    const int64_t d32 = (GEN && a.r32_img) ? bi * (a.r32_img - img) + a.r32_off : 0;   // r32 offset - output offset
     // batches of 8 columns: all loads of a batch issue before any store (the stores could
     // alias y / x as far as the compiler knows, which would serialise load latencies)
 #pragma unroll
@@ -219,18 +230,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ONT, 1)
       double yv[8], xv[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const int64_t off = base + (int64_t)(n0 + c0 + j) * tb;
+        const int64_t off = base + (int64_t)(n0 + c0 + j) * S;
         yv[j] = (!a.plus && a.Y) ? __ldg(a.Y + off) : 0.0;
         xv[j] = a.ax ? __ldg(a.ax + off) : 0.0;
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int c = c0 + j;
-        const int64_t off = base + (int64_t)(n0 + c) * tb;
-        const double p = ldexp(acc[c], exm + a.ew[n0 + c]);
+        const int64_t off = base + (int64_t)(n0 + c) * S;
+        const double p = ldexp(acc[c], exm + a.ew[(GEN ? a.wrow0 : 0) + n0 + c]);
         double v = a.plus ? p : yv[j] - p;
         if (a.ax) v = fma(-a.alpha, xv[j], v);
-        if (a.r32) a.r32[off] = (float)v;
+        if (a.r32) a.r32[off + d32] = (float)v;
         if (a.r64) a.r64[off] = v;
         sq += v * v;
       }
@@ -332,13 +343,26 @@ void ozaki_split_rows(int M, int K, const double* X, int64_t ldx, int8_t* dig, i
 }
 
 void ozaki_resid(const CUtensorMap* mx, const CUtensorMap* mw, const OzakiArgs& a, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(ozaki_resid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM);
-    attr = true;
-  }
+  static bool attr0 = false, attr1 = false;
+  const bool gen = a.tb_R || a.tb_S || a.tb_img || a.r32_img || a.wrow0;
   dim3 grid(a.N / OBN, ceil_div(a.M, OBM));
-  ozaki_resid_kernel<<<grid, ONT, OZ_SMEM, s>>>(*mx, *mw, a);
+  if (gen) {
+    if (!attr1) {
+      cudaFuncSetAttribute(ozaki_resid_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM);
+      attr1 = true;
+    }
+    OzakiArgs g = a;   // the general mapping needs every field set
+    if (!g.tb_R) g.tb_R = g.tblock;
+    if (!g.tb_S) g.tb_S = g.tblock;
+    if (!g.tb_img) g.tb_img = (int64_t)g.tblock * g.tblock;
+    ozaki_resid_kernel<true><<<grid, ONT, OZ_SMEM, s>>>(*mx, *mw, g);
+  } else {
+    if (!attr0) {
+      cudaFuncSetAttribute(ozaki_resid_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM);
+      attr0 = true;
+    }
+    ozaki_resid_kernel<false><<<grid, ONT, OZ_SMEM, s>>>(*mx, *mw, a);
+  }
 }
 
 }  // namespace nmg
