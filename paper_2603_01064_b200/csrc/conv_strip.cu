@@ -56,10 +56,13 @@ constexpr uint32_t IDESC4 = (1u << 4) | ((uint32_t)(16 >> 3) << 17) | ((uint32_t
 template <int C, bool FIRST>
 struct Roles {
 #ifndef NMG_STRIP_NG32
-#define NMG_STRIP_NG32 1
+#define NMG_STRIP_NG32 2
 #endif
-  // epilogue channel groups: layers 1-2 at C = 32 are producer-bound, so 4 all-channel
-  // epilogue warps leave 9 warps to the FFMA producer; layers 3-4 are epilogue-bound (8 warps)
+#ifndef NMG_STRIP_P32
+#define NMG_STRIP_P32 9
+#endif
+  // layers 1-2 at C = 32: 8 epilogue warps (two 16-channel groups) and 9 FFMA producer warps
+  // with four 8-channel groups per pixel pair (576 threads); layers 3-4: 8 epilogue warps
 #ifndef NMG_STRIP_NG48L34
 #define NMG_STRIP_NG48L34 2
 #endif
@@ -71,11 +74,13 @@ struct Roles {
 #endif
   // layers 1-2 at C = 48: NMG_STRIP_P48 producer warps; 7 warps split a pixel pair's channels
   // in three groups of 16 (195 items)
-  static constexpr int NQ = NG == 1 ? 4 : (FIRST && C == 48 && NMG_STRIP_P48 == 7) ? 3 : 2;
+  static constexpr int NQ = (NG == 1 || (FIRST && C == 32 && NMG_STRIP_P32 >= 9)) ? 4
+                            : (FIRST && C == 48 && NMG_STRIP_P48 == 7) ? 3 : 2;
   static constexpr int PROD0 = 4 * NG;                    // first producer warp
   // layers 1-2: FFMA producer warps up to warp 12; layers 3-4: one TMA warp and the layer-4
   // MMA warp only (the rest of the threads go to the epilogue)
-  static constexpr int MMAW = FIRST ? (C == 48 ? PROD0 + NMG_STRIP_P48 : 13) : PROD0 + 2;   // MMA issuer warp
+  static constexpr int MMAW = FIRST ? (C == 48 ? PROD0 + NMG_STRIP_P48 : (NMG_STRIP_P32 ? PROD0 + NMG_STRIP_P32 : 13))
+                                    : PROD0 + 2;   // MMA issuer warp
   static constexpr int NTHR = 32 * (MMAW + 1);
   static constexpr int NPROD = MMAW - PROD0;              // producer warps (FIRST)
 };
