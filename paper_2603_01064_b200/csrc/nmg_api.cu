@@ -1252,14 +1252,15 @@ namespace {
 nmg_status graph_cycle(nmg_hierarchy* h, int nrhs, const double* y, double* x, cudaStream_t s) {
   auto body = [&]() -> nmg_status {
     const int K = (int)h->lanes.size() + 1;
-    if (K == 1 || h->prof_on || nrhs < K * 128 || s == nullptr) {
+    const int gr = h->d.dim == 1 ? 128 : 2;             // lane granularity (GEMM M tiles / filter pairs)
+    if (K == 1 || h->prof_on || nrhs < K * gr || s == nullptr) {
       NMG_TRY(ynorms(h, nrhs, y, s));
       return outer_step(h, nrhs, y, x, -1.0, false, s);
     }
     // K lanes: RHS [off_k, off_k+1) on lane k (lane 0 = this handle on s, lane k > 0 on its
     // forked stream); the RHS are independent, so the lanes' kernels overlap
     int off[9];
-    for (int k = 0; k <= K; ++k) off[k] = std::min(nrhs, (nrhs * k / K + 127) / 128 * 128);
+    for (int k = 0; k <= K; ++k) off[k] = std::min(nrhs, (nrhs * k / K + gr - 1) / gr * gr);
     off[K] = nrhs;
     const int64_t N = h->N[0];
     NMG_CUDA(cudaEventRecord(h->evf, s));
@@ -1742,11 +1743,15 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
   {
     const char* le = std::getenv("NMG_LANES");
     int K = le ? std::max(1, std::min(8, std::atoi(le))) : 4;
-    if (d.dim != 1) K = 1;
-    while (K > 1 && d.max_rhs < K * 256) --K;            // lanes of >= 256 RHS
+    if (d.dim != 1) {                                     // 2D lanes: opt-in (NMG_LANES2D=K)
+      const char* l2 = std::getenv("NMG_LANES2D");
+      K = (l2 && !(le && std::string(le) == "1")) ? std::max(1, std::min(8, std::atoi(l2))) : 1;
+      while (K > 1 && d.max_rhs < K * 16) --K;            // lanes of >= 16 RHS
+    }
+    while (d.dim == 1 && K > 1 && d.max_rhs < K * 256) --K;   // 1D lanes of >= 256 RHS
     if (K > 1) {
       nmg_problem_desc d2 = d;
-      d2.max_rhs = (d.max_rhs + K - 1) / K + 128;         // a lane's share (rounded to 128-RHS tiles)
+      d2.max_rhs = (d.max_rhs + K - 1) / K + (d.dim == 1 ? 128 : 2);   // a lane's share (rounded up)
       setenv("NMG_LANES", "1", 1);                       // a lane itself has no lanes
       nmg_status st = NMG_OK;
       for (int k = 1; k < K && st == NMG_OK; ++k) {
