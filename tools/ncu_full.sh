@@ -11,6 +11,6 @@ run() {  # tag config kernel-regex count
       -o gpurun_out/ncu_$1 -f $B --config $2 > gpurun_out/ncu_$1.log 2>&1
   echo "NCU $1 $?"
 }
-run s1d 1 smooth1d_f16 1
-run ozaki 1 ozaki_resid 1
+NMG_LANES=1 run s1d 1 smooth1d_f16 1     # one lane: the full 1024-RHS launches
+NMG_LANES=1 run ozaki 1 ozaki_resid 1
 run strip2 2 "conv_strip|fft_cols|fft_rows" 4
