@@ -18,12 +18,16 @@
 namespace nmg {
 namespace {
 
-constexpr int TBM = 128, TBK = 16, TSTAGES = 4, TNT = 128;
+#ifndef NMG_GEMM_STAGES64
+#define NMG_GEMM_STAGES64 4
+#endif
+constexpr int TBM = 128, TBK = 16, TNT = 128;
 constexpr int A_BYTES = TBM * TBK * 4;                    // 8 KB
 template <int TBN> struct TcCfg {
   static constexpr int B_BYTES = TBN * TBK * 4;                     // 16 KB at N = 256
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;     // 48 KB at N = 256
-  static constexpr int SMEM = TSTAGES * STAGE_BYTES + 1024 /*barriers*/ + 1024 /*align slack*/;
+  static constexpr int NST = TBN == 256 ? 4 : NMG_GEMM_STAGES64;   // TMA ring depth
+  static constexpr int SMEM = NST * STAGE_BYTES + 1024 /*barriers*/ + 1024 /*align slack*/;
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TBN >> 3) << 17) |
                                     ((uint32_t)(TBM >> 4) << 24);   // D f32, A/B tf32 K-major, M=128
   // FP16x3: the same 64-byte smem rows hold 32 f16 (K per stage 32), kind::f16 with A/B f16
@@ -184,6 +188,7 @@ __global__ void __launch_bounds__(TNT, 1)
   extern __shared__ uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   constexpr int B_BYTES = TcCfg<TBN>::B_BYTES, STAGE_BYTES = TcCfg<TBN>::STAGE_BYTES;
+  constexpr int TSTAGES = TcCfg<TBN>::NST;
   constexpr uint32_t kIdesc = F16 ? TcCfg<TBN>::IDESC16 : TcCfg<TBN>::IDESC;
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + TSTAGES * STAGE_BYTES);
   uint64_t* empty = full + TSTAGES;
