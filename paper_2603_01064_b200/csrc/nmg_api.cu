@@ -1116,7 +1116,7 @@ nmg_status outer_residual(nmg_hierarchy* h, int nrhs, const double* y, const dou
     { Prof p(h, NMG_K_GEMM64, s); gemm_f64(q, s); }
     return check_launch(h);
   }
-  if (h->ozaki) {
+  if (h->ozaki && nrhs > 64) {   // small batches: one DMMA tile row beats the digit pipeline
     const int n = h->n[0];
     { Prof p(h, NMG_K_GEMM64, s);
       ozaki_split_rows(nrhs, n, x, n, h->xdig.p, (int64_t)h->d.max_rhs * n, h->xexp.p, s); }

@@ -161,10 +161,12 @@ def test_coarse_solve(cfg0):
     assert rel_l2(out.cpu().numpy(), O.coarse_solve(H, y.astype(np.float64))) < 1e-6
 
 
-def test_outer_residual_fp64(cfg0, cfg1):
+@pytest.mark.parametrize("nrhs", [5, 72])
+def test_outer_residual_fp64(cfg0, cfg1, nrhs):
+    """fp64 outer residual within 1e-12: DMMA for small batches (nrhs <= 64), exact int8 digit
+    products on tcgen05 (Ozaki) above."""
     for cfg, (f, W, H, h) in ((CFG0, cfg0), (CFG1, cfg1)):
         rng = np.random.default_rng(5)
-        nrhs = 5
         y = rng.standard_normal((nrhs, cfg.n))
         x = rng.standard_normal((nrhs, cfg.n))
         r = torch.zeros(nrhs, cfg.n, dtype=torch.float64, device=DEV)
@@ -181,7 +183,7 @@ def test_outer_residual_wide_dynamic_range(cfg1):
     1e-12 of the fp64 oracle, relative to ||y|| + ||A|| ||x||."""
     f, W, H, h = cfg1
     rng = np.random.default_rng(6)
-    nrhs = 3
+    nrhs = 72                                   # > 64: the Ozaki path
     x = rng.standard_normal((nrhs, CFG1.n)) * 10.0 ** rng.uniform(-8, 3, size=(nrhs, CFG1.n))
     y = O.apply_A(H, 0, x) + 1e-6 * rng.standard_normal((nrhs, CFG1.n))   # near-converged
     r = torch.zeros(nrhs, CFG1.n, dtype=torch.float64, device=DEV)
