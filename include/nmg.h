@@ -124,7 +124,8 @@ nmg_status nmg_solve(nmg_hierarchy *h, int32_t nrhs, const double *y, double *x,
 /* Same as nmg_vcycle repeated `cycles` times, but y and x are HOST buffers: the call
  * copies y and x host->device, runs the cycles and copies x back (end-to-end path).
  * relres (host, may be NULL) receives [nrhs] fp64 relative residuals of the input x
- * measured before the last cycle.  Synchronous. */
+ * measured before the last cycle.  The copies are pipelined with the cycles (per RHS lane
+ * on a handle with lanes, else per RHS chunk).  Synchronous. */
 nmg_status nmg_vcycles_host(nmg_hierarchy *h, int32_t nrhs, const double *y_host, double *x_host,
                             int32_t cycles, double *relres_host, void *stream);
 

@@ -1191,10 +1191,12 @@ nmg_status check_ready(nmg_hierarchy* h, int nrhs) {
 }
 
 // one outer step: residual (+relres/active), inner cycle, masked update
+// (relres: where the relative residuals go, default h->relres; a lane writes its slice of the
+// parent's array)
 nmg_status outer_step(nmg_hierarchy* h, int nrhs, const double* y, double* x, double tol, bool use_active,
-                      cudaStream_t s) {
+                      cudaStream_t s, double* relres = nullptr) {
   NMG_TRY(outer_residual(h, nrhs, y, x, nullptr, true, s));
-  NMG_TRY(relres_fin(h, nrhs, tol, h->active.p, h->relres.p, s));
+  NMG_TRY(relres_fin(h, nrhs, tol, h->active.p, relres ? relres : h->relres.p, s));
   NMG_TRY(inner_cycle(h, nrhs, s));
   return outer_update(h, nrhs, x, use_active ? h->active.p : nullptr, s);
 }
@@ -1275,7 +1277,8 @@ nmg_status graph_cycle(nmg_hierarchy* h, int nrhs, const double* y, double* x, c
       const int64_t l0 = hk->launches;
       hk->lane_mult = mult;
       st = ynorms(hk, cnt, y + off[k] * N, h->ls[k - 1]);
-      if (st == NMG_OK) st = outer_step(hk, cnt, y + off[k] * N, x + off[k] * N, -1.0, false, h->ls[k - 1]);
+      if (st == NMG_OK)
+        st = outer_step(hk, cnt, y + off[k] * N, x + off[k] * N, -1.0, false, h->ls[k - 1], h->relres.p + off[k]);
       hk->lane_mult = 1;
       h->launches += hk->launches - l0;
     }
@@ -2146,24 +2149,71 @@ nmg_status nmg_vcycles_host(nmg_hierarchy* h, int32_t nrhs, const double* y_host
   cudaStream_t s = (cudaStream_t)stream;
   const size_t cnt = (size_t)h->d.max_rhs * h->N[0];
   if (!h->hy.p) { NMG_TRY(h->hy.alloc(cnt)); NMG_TRY(h->hx.alloc(cnt)); }
+  const int64_t N0 = h->N[0];
+  if (!h->s_h2d) {
+    NMG_CUDA(cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking));
+    NMG_CUDA(cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking));
+    h->hev.resize(2 * 8 + 2);
+    for (auto& e : h->hev) NMG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  cudaEvent_t ev_start = h->hev[16], ev_end = h->hev[17];
+  NMG_CUDA(cudaEventRecord(ev_start, s));                 // staging buffers free after prior work on s
+  NMG_CUDA(cudaStreamWaitEvent(h->s_h2d, ev_start, 0));
+  NMG_CUDA(cudaStreamWaitEvent(h->s_d2h, ev_start, 0));
+  const int K = (int)h->lanes.size() + 1;
+  const int gr = h->d.dim == 1 ? 128 : 2;
+  const char* hl = std::getenv("NMG_HOST_LANES");
+  if (K > 1 && nrhs >= K * gr && !h->prof_on && s != nullptr && !(hl && std::string(hl) == "0")) {
+    // Lane-pipelined (the RHS are independent): lane k's RHS are copied in on s_h2d,
+    // its stream starts cycling as soon as they land (the lanes overlap on the GPU while later
+    // lanes are still in flight over PCIe), and its x goes back on s_d2h when it finishes.
+    int off[9];
+    for (int k = 0; k <= K; ++k) off[k] = std::min(nrhs, (nrhs * k / K + gr - 1) / gr * gr);
+    off[K] = nrhs;
+    for (int k = 0; k < K; ++k) {
+      const size_t b = sizeof(double) * (size_t)(off[k + 1] - off[k]) * N0;
+      if (!b) continue;
+      NMG_CUDA(cudaMemcpyAsync(h->hy.p + off[k] * N0, y_host + off[k] * N0, b, cudaMemcpyHostToDevice, h->s_h2d));
+      NMG_CUDA(cudaMemcpyAsync(h->hx.p + off[k] * N0, x_host + off[k] * N0, b, cudaMemcpyHostToDevice, h->s_h2d));
+      NMG_CUDA(cudaEventRecord(h->hev[k], h->s_h2d));
+    }
+    const int mult = h->lane_tiles ? K : 1;
+    for (int k = 0; k < K; ++k) {
+      const int cnt = off[k + 1] - off[k];
+      if (cnt <= 0) continue;
+      nmg_hierarchy* hk = k == 0 ? h : h->lanes[k - 1].get();
+      cudaStream_t sk = k == 0 ? s : h->ls[k - 1];
+      const double* yc = h->hy.p + off[k] * N0;
+      double* xc = h->hx.p + off[k] * N0;
+      NMG_CUDA(cudaStreamWaitEvent(sk, h->hev[k], 0));
+      const int64_t l0 = hk->launches;
+      hk->lane_mult = mult;
+      nmg_status st = NMG_OK;
+      // a lane's batch is below the lane threshold, so graph_cycle runs (and caches) it as one
+      // plain graph on the lane's own handle and stream
+      for (int c = 0; c < cycles && st == NMG_OK; ++c) st = graph_cycle(hk, cnt, yc, xc, sk);
+      hk->lane_mult = 1;
+      if (k > 0) h->launches += hk->launches - l0;
+      NMG_TRY(st);
+      if (relres_host && cycles > 0)
+        NMG_CUDA(cudaMemcpyAsync(relres_host + off[k], hk->relres.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, sk));
+      NMG_CUDA(cudaEventRecord(h->hev[8 + k], sk));
+      NMG_CUDA(cudaStreamWaitEvent(h->s_d2h, h->hev[8 + k], 0));
+      NMG_CUDA(cudaMemcpyAsync(x_host + off[k] * N0, xc, sizeof(double) * (size_t)cnt * N0, cudaMemcpyDeviceToHost,
+                               h->s_d2h));
+    }
+    NMG_CUDA(cudaEventRecord(ev_end, h->s_d2h));
+    NMG_CUDA(cudaStreamWaitEvent(s, ev_end, 0));
+    NMG_CUDA(cudaStreamSynchronize(s));
+    return NMG_OK;
+  }
   // Pipelined over RHS chunks (the RHS are independent): host->device copies of
   // chunk c + 1 and the device->host copy of chunk c - 1 run on two copy streams while chunk c
   // cycles on the caller's stream.  One plain cudaMemcpyAsync per buffer and chunk.
-  const int64_t N0 = h->N[0];
   // two chunks keep each chunk's kernels near full occupancy (measured: cfg 1 in 4 chunks of
   // 256 RHS runs at 64% of the batch efficiency); four only for very large batches
   int nch = nrhs < 256 ? 1 : ((int64_t)nrhs * N0 / 4 < ((int64_t)1 << 25) ? 2 : 4);
   if (const char* ce = std::getenv("NMG_HOST_CHUNKS")) nch = std::max(1, std::min(4, std::min(nrhs, std::atoi(ce))));
-  if (!h->s_h2d) {
-    NMG_CUDA(cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking));
-    NMG_CUDA(cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking));
-    h->hev.resize(2 * 4 + 2);
-    for (auto& e : h->hev) NMG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  }
-  cudaEvent_t ev_start = h->hev[8], ev_end = h->hev[9];
-  NMG_CUDA(cudaEventRecord(ev_start, s));                 // staging buffers free after prior work on s
-  NMG_CUDA(cudaStreamWaitEvent(h->s_h2d, ev_start, 0));
-  NMG_CUDA(cudaStreamWaitEvent(h->s_d2h, ev_start, 0));
   int off[5];
   for (int c = 0; c <= nch; ++c) off[c] = (int)((int64_t)nrhs * c / nch);
   for (int c = 0; c < nch; ++c) {
@@ -2180,8 +2230,8 @@ nmg_status nmg_vcycles_host(nmg_hierarchy* h, int32_t nrhs, const double* y_host
     for (int k = 0; k < cycles; ++k) NMG_TRY(graph_cycle(h, cnt, yc, xc, s));
     if (relres_host)
       NMG_CUDA(cudaMemcpyAsync(relres_host + off[c], h->relres.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, s));
-    NMG_CUDA(cudaEventRecord(h->hev[4 + c], s));
-    NMG_CUDA(cudaStreamWaitEvent(h->s_d2h, h->hev[4 + c], 0));
+    NMG_CUDA(cudaEventRecord(h->hev[8 + c], s));
+    NMG_CUDA(cudaStreamWaitEvent(h->s_d2h, h->hev[8 + c], 0));
     NMG_CUDA(cudaMemcpyAsync(x_host + off[c] * N0, xc, sizeof(double) * (size_t)cnt * N0, cudaMemcpyDeviceToHost,
                              h->s_d2h));
   }

@@ -351,6 +351,38 @@ def test_host_entry_chunked_pipeline():
     assert np.array_equal(xh, xd.cpu().numpy())
 
 
+@pytest.mark.parametrize("host_lanes", ["1", "0"])
+def test_host_entry_lanes(monkeypatch, host_lanes):
+    """On a handle with RHS lanes (max_rhs 1024: four lanes of 256) nmg_vcycles_host either
+    pipelines the copies per lane (default: a lane cycles as soon as its RHS land) or per chunk
+    (NMG_HOST_LANES=0, lanes inside each chunk); x is bitwise the device-entry result and relres
+    (the relative residual before the last cycle, every lane's slice) matches nmg_residual."""
+    monkeypatch.delenv("NMG_LANES", raising=False)
+    monkeypatch.setenv("NMG_HOST_LANES", host_lanes)
+    cfg = ni.CONFIGS[1].replace(n=1024, levels=4, nrhs=1024)
+    f = ni.operator_factors(cfg)
+    W = ni.weights_seed(cfg)
+    y, _ = ni.make_rhs(cfg, f, cfg.alpha, nrhs=1024)
+    h = nmg.Hierarchy(1, cfg.n, cfg.levels, cfg.alpha, f, nu1=1, nu2=1, max_rhs=1024)
+    for l, w in enumerate(W):
+        h.load_weights(l + 1, ni.cnn_arch(cfg), w)
+    yd = torch.tensor(y, dtype=torch.float64, device=DEV)
+    xd = torch.zeros_like(yd)
+    st = torch.cuda.Stream()
+    h.vcycle(yd, xd, st)
+    h.vcycle(yd, xd, st)
+    rr_ref = torch.empty(1024, dtype=torch.float64, device=DEV)
+    h.residual(yd, xd, relres=rr_ref, stream=st)
+    h.vcycle(yd, xd, st)
+    torch.cuda.synchronize()
+    xh = np.zeros_like(y)
+    rr = np.zeros(1024)
+    h.vcycles_host(np.ascontiguousarray(y), xh, 3, relres=rr, stream=st)
+    assert np.array_equal(xh, xd.cpu().numpy())
+    np.testing.assert_allclose(rr, rr_ref.cpu().numpy(), rtol=1e-12, atol=0)
+    h.close()
+
+
 def test_rhs_lanes_bitwise(monkeypatch):
     """Batches >= 256 RHS on a handle with max_rhs >= 512 run as two RHS lanes on forked
     streams (nmg_vcycle); the NMGF cycle is per-RHS, so the result is bitwise the one-lane result."""
