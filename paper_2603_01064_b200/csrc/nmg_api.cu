@@ -2213,8 +2213,8 @@ nmg_status nmg_vcycles_host(nmg_hierarchy* h, int32_t nrhs, const double* y_host
   // two chunks keep each chunk's kernels near full occupancy (measured: cfg 1 in 4 chunks of
   // 256 RHS runs at 64% of the batch efficiency); four only for very large batches
   int nch = nrhs < 256 ? 1 : ((int64_t)nrhs * N0 / 4 < ((int64_t)1 << 25) ? 2 : 4);
-  if (const char* ce = std::getenv("NMG_HOST_CHUNKS")) nch = std::max(1, std::min(4, std::min(nrhs, std::atoi(ce))));
-  int off[5];
+  if (const char* ce = std::getenv("NMG_HOST_CHUNKS")) nch = std::max(1, std::min(8, std::min(nrhs, std::atoi(ce))));
+  int off[9];
   for (int c = 0; c <= nch; ++c) off[c] = (int)((int64_t)nrhs * c / nch);
   for (int c = 0; c < nch; ++c) {
     const size_t b = sizeof(double) * (size_t)(off[c + 1] - off[c]) * N0;
