@@ -1248,6 +1248,9 @@ nmg_status debug_2d(nmg_hierarchy* h, int l, int op, int nrhs, const float* fin,
 // ======================================================================= C ABI
 namespace {
 
+// set while nmg_create_hierarchy builds a lane or a slab handle: no RHS lanes of its own
+thread_local bool t_no_lanes = false;
+
 // One cycle through a cached CUDA graph: the first call with a given (nrhs, y, x, stream) runs
 // eagerly, the second captures the whole cycle, later calls replay it (launch-latency bound
 // small configs and coarse levels).
@@ -1745,24 +1748,27 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
   NMG_TRY(h->active.alloc(B));
   {
     const char* le = std::getenv("NMG_LANES");
-    int K = le ? std::max(1, std::min(8, std::atoi(le))) : 4;
-    if (d.dim != 1) {                                     // 2D lanes: opt-in (NMG_LANES2D=K)
+    int K = t_no_lanes ? 1 : le ? std::max(1, std::min(8, std::atoi(le))) : 4;
+    if (d.dim != 1 && K > 1) {
+      // 2D: two lanes by default while the batch is small enough that a second set of lane
+      // workspaces is cheap (cfg 2, 4: same device time, the host entry overlaps more); NMG_LANES2D=K
       const char* l2 = std::getenv("NMG_LANES2D");
-      K = (l2 && !(le && std::string(le) == "1")) ? std::max(1, std::min(8, std::atoi(l2))) : 1;
+      K = l2 ? std::max(1, std::min(8, std::atoi(l2))) : ((int64_t)d.max_rhs * h->N[0] <= ((int64_t)1 << 26) ? 2 : 1);
+      if (le && std::string(le) == "1") K = 1;
       while (K > 1 && d.max_rhs < K * 16) --K;            // lanes of >= 16 RHS
     }
     while (d.dim == 1 && K > 1 && d.max_rhs < K * 256) --K;   // 1D lanes of >= 256 RHS
     if (K > 1) {
       nmg_problem_desc d2 = d;
       d2.max_rhs = (d.max_rhs + K - 1) / K + (d.dim == 1 ? 128 : 2);   // a lane's share (rounded up)
-      setenv("NMG_LANES", "1", 1);                       // a lane itself has no lanes
+      t_no_lanes = true;                                 // a lane itself has no lanes
       nmg_status st = NMG_OK;
       for (int k = 1; k < K && st == NMG_OK; ++k) {
         nmg_hierarchy* raw = nullptr;
         st = nmg_create_hierarchy(&d2, factors, &raw);
         if (st == NMG_OK) h->lanes.emplace_back(raw);
       }
-      if (le) setenv("NMG_LANES", le, 1); else unsetenv("NMG_LANES");
+      t_no_lanes = false;
       NMG_TRY(st);
       const char* lt = std::getenv("NMG_LANE_TILES");
       h->lane_tiles = !(lt && std::string(lt) == "0");
@@ -1792,7 +1798,10 @@ nmg_status nmg_create_hierarchy_slab(const nmg_problem_desc* desc, const double*
   if (desc->n % W != 0 || desc->n / W < 32 || (desc->n / W) % 32 != 0)
     return fail(NMG_ERR_UNSUPPORTED, "slab mode needs n / world to be a multiple of 32 (n = %d, world = %d)", desc->n, W);
   nmg_hierarchy* raw = nullptr;
-  NMG_TRY(nmg_create_hierarchy(desc, factors, &raw));
+  t_no_lanes = true;                                     // the slab cycle has no RHS lanes
+  const nmg_status cst = nmg_create_hierarchy(desc, factors, &raw);
+  t_no_lanes = false;
+  NMG_TRY(cst);
   std::unique_ptr<nmg_hierarchy> h(raw);
   if (!h->use_kron) return fail(NMG_ERR_UNSUPPORTED, "slab mode needs the tcgen05 Kronecker apply (NMG_KRON != 0)");
   h->slab = true;

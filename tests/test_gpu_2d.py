@@ -238,3 +238,35 @@ def test_outer_residual_2d_ozaki(cfg_id, n):
         assert rel_l2(r.cpu().numpy()[b], want[b]) < 1e-12, b
     nrm = np.sqrt((want ** 2).sum(axis=(1, 2))) / np.sqrt((y ** 2).sum(axis=(1, 2)))
     assert np.allclose(rr.cpu().numpy(), nrm, rtol=1e-12)
+
+
+@pytest.mark.parametrize("nrhs", [37, 64])
+def test_rhs_lanes_bitwise_2d(monkeypatch, nrhs):
+    """2D handles with max_rhs * n^2 <= 2^26 cycle their batch as two RHS lanes on forked streams
+    (lane boundaries on even RHS, so the level filter's RHS pairs are the same); the result is
+    bitwise the one-lane result, through the device entry and the lane-pipelined host entry."""
+    cfg = SMALL.replace(nrhs=nrhs)
+    f = ni.operator_factors(cfg)
+    W = weights_for(cfg, "seed")
+    y, _ = ni.make_rhs(cfg, f, cfg.alpha, nrhs=nrhs)
+    outs = []
+    for lanes in ("1", None):
+        if lanes:
+            monkeypatch.setenv("NMG_LANES", lanes)
+        else:
+            monkeypatch.delenv("NMG_LANES", raising=False)
+        monkeypatch.delenv("NMG_LANES2D", raising=False)
+        h = gpu_hierarchy(cfg, f, W, max_rhs=64)
+        yd = T(y, torch.float64)
+        xd = torch.zeros_like(yd)
+        st = torch.cuda.Stream()
+        for _ in range(3):                     # eager, capture, replay
+            h.vcycle(yd, xd, st)
+        torch.cuda.synchronize()
+        outs.append(xd.cpu().numpy())
+        xh = np.zeros_like(y)
+        h.vcycles_host(np.ascontiguousarray(y), xh, 3, stream=st)
+        outs.append(xh)
+        h.close()
+    for o in outs[1:]:
+        assert np.array_equal(outs[0], o)
