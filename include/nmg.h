@@ -57,8 +57,41 @@ typedef enum {
   NMG_ERR_NONFINITE = 5,    /* NaN/Inf residual; report->fail_cycle / fail_rhs are set    */
   NMG_ERR_CUDA = 6,         /* CUDA runtime / launch failure, or no sm_100 device         */
   NMG_ERR_OOM = 7,          /* device allocation failed                                   */
-  NMG_ERR_UNSUPPORTED = 8   /* architecture / mode not implemented                        */
+  NMG_ERR_UNSUPPORTED = 8,  /* architecture / mode not implemented                        */
+  NMG_ERR_DIVERGED = 9,     /* opt-in (desc.divergence_check): an active RHS's relres stayed
+                               above 10x its initial relres for 5 consecutive cycles
+                               (SPEC.md:545 rule); report->fail_cycle / fail_rhs are set     */
+  NMG_ERR_NCCL = 10         /* collective failure (NCCL call or asynchronous communicator
+                               error, or an emulated peer rank that failed / timed out)      */
 } nmg_status;
+
+/* Precision of the cycle (reading R14). */
+enum {
+  NMG_PREC_MIXED = 0,   /* fp64 outer residual, convergence test and update around an inner
+                           NMGF cycle in fp32-accurate split arithmetic on the tensor cores
+                           (correction form x + NMGF(0, y - A x), pin P11) -- default       */
+  NMG_PREC_FP64 = 1     /* every step of the cycle in fp64 except the CNN's own arithmetic
+                           (fp32 weights and activations, BASELINE configs[0]); 1D only,
+                           n <= 1024 (one fused kernel per cycle, one CTA per RHS)        */
+};
+
+/* Kernel-selection knobs (all 0 = the default production path).  They exist for A/B timing
+ * and for the parity tests of the alternative kernels; none changes what is computed beyond
+ * floating-point rounding order. */
+typedef struct {
+  int32_t lanes;          /* RHS lanes: 0 = auto (1D: up to 4 lanes of >= 256 RHS; 2D: 2 lanes
+                             while max_rhs*n^2 <= 2^26), 1 = off, K >= 2 = K lanes           */
+  int32_t no_graphs;      /* 1: launch every kernel eagerly instead of replaying the cycle's
+                             captured CUDA graph                                             */
+  int32_t coarse_subst;   /* 1: coarsest solve by forward/back substitution with the Cholesky
+                             factor instead of the explicit fp64 inverse A_L^{-1}            */
+  int32_t fp64_dmma;      /* 1: fp64 outer residual on DMMA instead of Ozaki int8 digits      */
+  int32_t simt_gemm;      /* 1: inner operator applies on the SIMT fp32 GEMM (no tcgen05)     */
+  int32_t ffma_cnn;       /* 1: CNN smoother on the FFMA kernels (no tcgen05)                 */
+  int32_t no_kron;        /* 1 (2D): Kronecker pair as two plain GEMMs + a stencil pass       */
+  int32_t host_chunks;    /* nmg_vcycles_host: 0 = pipelined per RHS lane (default when the
+                             handle has lanes), else that many RHS chunks (1..8)             */
+} nmg_tuning;
 
 /* Problem descriptor (SPEC ProblemSpec analogue). */
 typedef struct {
@@ -71,6 +104,9 @@ typedef struct {
   int32_t level_filter; /* 1: Alg 3/4 with F'_l; 0: Alg 2          */
   int32_t max_rhs;      /* workspace sizing: largest nrhs ever passed                      */
   int32_t device;       /* CUDA ordinal                                                    */
+  int32_t precision;    /* NMG_PREC_MIXED (0, default) or NMG_PREC_FP64                    */
+  int32_t divergence_check; /* 1: nmg_solve returns NMG_ERR_DIVERGED per SPEC.md:545      */
+  const nmg_tuning *tuning; /* host, may be NULL (defaults); copied at create              */
 } nmg_problem_desc;
 
 /* CNN smoother architecture (reading R7): n_layers convolutions 1 -> C -> ... -> C -> 1,
@@ -93,7 +129,8 @@ typedef struct {
 } nmg_report;
 
 /* Build the level hierarchy (host fp64 Galerkin chain A^(l+1) = I_l^{l+1} A^(l) I_{l+1}^l,
- * P:160; coarsest Cholesky; device uploads).
+ * P:160; coarsest Cholesky; device uploads).  Every device workspace the cycle entries use
+ * is allocated here (sized by max_rhs), including the staging of nmg_vcycles_host.
  *   factors (host, read-only, copied):
  *     dim 1: G, n*n doubles row-major, symmetric                 (A = G + alpha I)
  *     dim 2: B then C, each n*n doubles row-major, symmetric:
@@ -104,7 +141,8 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc *desc, const double *fact
 
 /* Load the smoother theta_l of level `level` (1..L-1), fp32 parameters in PyTorch
  * state_dict order (w0, b0, w1, b1, ...; conv weights [out][in][k] / [out][in][k2][k1]).
- * params: host, n_params floats, copied.  Loading a level twice replaces it.
+ * params: host, n_params floats, copied.  Loading a level twice replaces it; the cycle graphs
+ * captured before the reload are discarded (the call synchronises the device first).
  * Errors: INVALID_ARG, SHAPE, UNSUPPORTED, CUDA. */
 nmg_status nmg_load_smoother_weights(nmg_hierarchy *h, int32_t level, const nmg_cnn_arch *arch,
                                      const float *params, size_t n_params);
@@ -116,8 +154,9 @@ nmg_status nmg_vcycle(nmg_hierarchy *h, int32_t nrhs, const double *y, double *x
 
 /* Outer iteration from the x passed in (x0 = 0 for the paper's solve) until every
  * RHS has relres <= tol or max_cycles; converged RHS are frozen.  y, x: device
- * fp64 [nrhs][N]; rep: host (may be NULL).  Synchronises once per cycle.
- * Errors: NONFINITE (rep->fail_*), NO_WEIGHTS, CUDA. */
+ * fp64 [nrhs][N]; rep: host (may be NULL).  Synchronises once per cycle (and polls the
+ * communicator's asynchronous error state on a slab handle).
+ * Errors: NONFINITE / DIVERGED (rep->fail_*), NO_WEIGHTS, CUDA, NCCL. */
 nmg_status nmg_solve(nmg_hierarchy *h, int32_t nrhs, const double *y, double *x, double tol,
                      int32_t max_cycles, nmg_report *rep, void *stream);
 

@@ -7,5 +7,5 @@ library raises.
 """
 from .binding import (  # noqa: F401
     NmgError, Hierarchy, Comm, nccl_unique_id, OP_APPLY, OP_RESIDUAL, OP_RESTRICT, OP_PROLONG, OP_FILTER,
-    OP_CNN, OP_SMOOTH, OP_COARSE, OP_CYCLE0, lib_path, load_library,
+    OP_CNN, OP_SMOOTH, OP_COARSE, OP_CYCLE0, PREC_MIXED, PREC_FP64, lib_path, load_library,
 )

@@ -17,7 +17,8 @@ lib_path = os.environ.get("NMG_LIB") or os.path.join(HERE, "libnmg.so")
 OP_APPLY, OP_RESIDUAL, OP_RESTRICT, OP_PROLONG, OP_FILTER, OP_CNN, OP_SMOOTH, OP_COARSE, OP_CYCLE0 = range(9)
 
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "SHAPE", 3: "NOT_SPD", 4: "NO_WEIGHTS", 5: "NONFINITE",
-          6: "CUDA", 7: "OOM", 8: "UNSUPPORTED"}
+          6: "CUDA", 7: "OOM", 8: "UNSUPPORTED", 9: "DIVERGED", 10: "NCCL"}
+PREC_MIXED, PREC_FP64 = 0, 1
 
 EXPORTS = ["nmg_create_hierarchy", "nmg_load_smoother_weights", "nmg_vcycle", "nmg_solve",
            "nmg_vcycles_host", "nmg_residual", "nmg_debug_level_op", "nmg_launch_count",
@@ -34,10 +35,18 @@ class NmgError(RuntimeError):
         self.status = status
 
 
+class Tuning(C.Structure):
+    """nmg_tuning: kernel-selection knobs, all 0 = the default production path."""
+    _fields_ = [("lanes", C.c_int32), ("no_graphs", C.c_int32), ("coarse_subst", C.c_int32),
+                ("fp64_dmma", C.c_int32), ("simt_gemm", C.c_int32), ("ffma_cnn", C.c_int32),
+                ("no_kron", C.c_int32), ("host_chunks", C.c_int32)]
+
+
 class ProblemDesc(C.Structure):
     _fields_ = [("dim", C.c_int32), ("n", C.c_int32), ("levels", C.c_int32), ("alpha", C.c_double),
                 ("nu1", C.c_int32), ("nu2", C.c_int32), ("level_filter", C.c_int32),
-                ("max_rhs", C.c_int32), ("device", C.c_int32)]
+                ("max_rhs", C.c_int32), ("device", C.c_int32), ("precision", C.c_int32),
+                ("divergence_check", C.c_int32), ("tuning", C.POINTER(Tuning))]
 
 
 class CnnArch(C.Structure):
@@ -161,9 +170,12 @@ class Hierarchy:
 
     def __init__(self, dim: int, n: int, levels: int, alpha: float, factors: Sequence[np.ndarray],
                  nu1: int = 1, nu2: int = 1, level_filter: bool = True, max_rhs: int = 1,
-                 device: int = 0, comm: Optional[Comm] = None):
+                 device: int = 0, comm: Optional[Comm] = None, precision: int = PREC_MIXED,
+                 divergence_check: bool = False, tuning: Optional[dict] = None):
         lib = load_library()
-        d = ProblemDesc(dim, n, levels, float(alpha), nu1, nu2, int(level_filter), max_rhs, device)
+        tun = Tuning(**(tuning or {}))
+        d = ProblemDesc(dim, n, levels, float(alpha), nu1, nu2, int(level_filter), max_rhs, device,
+                        int(precision), int(divergence_check), C.pointer(tun))
         fac = np.ascontiguousarray(np.concatenate([np.asarray(f, np.float64).ravel() for f in factors]))
         h = C.c_void_p()
         if comm is None:

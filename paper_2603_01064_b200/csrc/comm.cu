@@ -36,6 +36,7 @@ struct NcclApi {
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
 };
 
 NcclApi* nccl_api() {
@@ -61,6 +62,7 @@ NcclApi* nccl_api() {
   sym(api.GroupStart, "ncclGroupStart");
   sym(api.GroupEnd, "ncclGroupEnd");
   sym(api.GetErrorString, "ncclGetErrorString");
+  sym(api.CommGetAsyncError, "ncclCommGetAsyncError");
   if (!ok) { dlclose(api.so); api.so = nullptr; return nullptr; }
   return &api;
 }
@@ -68,13 +70,20 @@ NcclApi* nccl_api() {
 #define NMG_NCCL(expr)                                                                          \
   do {                                                                                          \
     ncclResult_t _r = (expr);                                                                   \
-    if (_r != ncclSuccess) return nmg::comm_fail(NMG_ERR_CUDA, "NCCL %s: %s", #expr, api->GetErrorString(_r)); \
+    if (_r != ncclSuccess) return nmg::comm_fail(NMG_ERR_NCCL, "NCCL %s: %s", #expr, api->GetErrorString(_r)); \
   } while (0)
 
 struct NcclComm final : nmg_comm {
   NcclApi* api = nullptr;
   ncclComm_t c = nullptr;
   ~NcclComm() override { if (c && api) api->CommDestroy(c); }
+  nmg_status check_async() override {
+    ncclResult_t ar = ncclSuccess;
+    NMG_NCCL(api->CommGetAsyncError(c, &ar));
+    if (ar != ncclSuccess && ar != ncclInProgress)
+      return nmg::comm_fail(NMG_ERR_NCCL, "NCCL asynchronous error: %s", api->GetErrorString(ar));
+    return NMG_OK;
+  }
   nmg_status all_gather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
     NMG_NCCL(api->AllGather(send, recv, bytes, ncclChar, c, s));
     return NMG_OK;
@@ -131,7 +140,7 @@ struct EmuComm final : nmg_comm {
     auto& me = G.slots[rank];
     me.send = send; me.recv = recv; me.bytes = bytes;
     if (cudaEventRecord(me.ready, s) != cudaSuccess) return comm_fail(NMG_ERR_CUDA, "emulated collective: event record");
-    if (!G.barrier()) return comm_fail(NMG_ERR_CUDA, "emulated collective: a peer rank failed or timed out");
+    if (!G.barrier()) return comm_fail(NMG_ERR_NCCL, "emulated collective: a peer rank failed or timed out");
     for (int q = 0; q < world; ++q) {
       if (G.slots[q].bytes != bytes) return comm_fail(NMG_ERR_INVALID_ARG, "emulated collective: size mismatch");
       cudaStreamWaitEvent(s, G.slots[q].ready, 0);
@@ -142,9 +151,9 @@ struct EmuComm final : nmg_comm {
         return comm_fail(NMG_ERR_CUDA, "emulated collective: copy");
     }
     cudaEventRecord(me.done, s);
-    if (!G.barrier()) return comm_fail(NMG_ERR_CUDA, "emulated collective: a peer rank failed or timed out");
+    if (!G.barrier()) return comm_fail(NMG_ERR_NCCL, "emulated collective: a peer rank failed or timed out");
     for (int q = 0; q < world; ++q) cudaStreamWaitEvent(s, G.slots[q].done, 0);   // peers finished reading `send`
-    if (!G.barrier()) return comm_fail(NMG_ERR_CUDA, "emulated collective: a peer rank failed or timed out");
+    if (!G.barrier()) return comm_fail(NMG_ERR_NCCL, "emulated collective: a peer rank failed or timed out");
     return NMG_OK;
   }
   nmg_status all_gather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {

@@ -26,6 +26,8 @@ struct nmg_comm {
   virtual ~nmg_comm() {}
   virtual nmg_status all_gather(const void* send, void* recv, size_t bytes, cudaStream_t s) = 0;
   virtual nmg_status all_to_all(const void* send, void* recv, size_t bytes_per_peer, cudaStream_t s) = 0;
+  // asynchronous communicator errors (NCCL: ncclCommGetAsyncError); NMG_OK when healthy
+  virtual nmg_status check_async() { return NMG_OK; }
   // scratch: device, >= world * count doubles
   nmg_status sum_f64(double* buf, size_t count, double* scratch, cudaStream_t s);
 };

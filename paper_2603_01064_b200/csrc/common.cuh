@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
 #error "nmg kernels are written for sm_100a only"
 #endif
@@ -39,5 +41,23 @@ NMG_D double block_sum_f64(double v, double* scratch /* >= 32 doubles */) {
 NMG_D void zput(float2* Z, int64_t N, int b, int64_t pix, float v) {
   reinterpret_cast<float*>(Z)[((int64_t)(b >> 1) * N + pix) * 2 + (b & 1)] = v;
 }
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is a per-DEVICE property: set it once per
+// (call site, device).  `done` is the call site's bitmask of devices already configured (a
+// concurrent double set is harmless: the call is idempotent).
+inline cudaError_t smem_optin(const void* fn, int bytes, std::atomic<uint64_t>& done) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
+#define NMG_SMEM_OPTIN(fn, bytes)                                         \
+  do {                                                                    \
+    static std::atomic<uint64_t> nmg_optin_done_{0};                      \
+    ::nmg::smem_optin((const void*)(fn), (int)(bytes), nmg_optin_done_); \
+  } while (0)
 
 }  // namespace nmg

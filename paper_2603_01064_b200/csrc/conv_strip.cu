@@ -42,6 +42,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tcgen05.cuh"
 
 namespace nmg {
 namespace {
@@ -117,75 +118,12 @@ struct Cfg {
   static constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(SEG >> 4) << 24);
 };
 
-NMG_D uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
-NMG_D void mb_init(uint64_t* b, uint32_t c) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(c));
-}
-NMG_D void mb_expect(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes) : "memory");
-}
-NMG_D void mb_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
-}
-NMG_D void mb_wait(uint64_t* b, uint32_t ph) {
-  asm volatile(
-      "{\n.reg .pred P1;\nWAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@P1 bra DONE_%=;\nbra WAIT_%=;\nDONE_%=:\n}\n" ::"r"(su32(b)),
-      "r"(ph)
-      : "memory");
-}
-NMG_D void tma5d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2, int c3, int c4) {
-  asm volatile(
-      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], "
-      "[%2];\n" ::"r"(su32(dst)),
-      "l"(m), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
-      : "memory");
-}
-// K-major canonical layout without swizzle: 8-row core matrices of 16 B rows, contiguous in
-// M/N (SBO = 128 B), K chunks of 8 elements LBO bytes apart.
-NMG_D uint64_t desc_ns(uint32_t saddr, uint32_t lbo) {
-  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-  d |= (uint64_t)(128 >> 4) << 32;
-  d |= (uint64_t)1 << 46;
-  return d;
-}
-NMG_D void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc));
-}
-NMG_D void mma_commit(uint64_t* b) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(b))
-               : "memory");
-}
-
-NMG_D void tld8(uint32_t taddr, uint32_t* r) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-               : "r"(taddr));
-}
 template <int CG>
 NMG_D void tld_wait(uint32_t* r);
 template <>
-NMG_D void tld_wait<16>(uint32_t* r) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
-               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
-                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
-               :
-               : "memory");
-}
+NMG_D void tld_wait<16>(uint32_t* r) { tld_wait16(r); }
 template <>
-NMG_D void tld_wait<24>(uint32_t* r) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
-               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
-                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]),
-                 "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23])
-               :
-               : "memory");
-}
+NMG_D void tld_wait<24>(uint32_t* r) { tld_wait24(r); }
 // CG consecutive TMEM columns of this thread's lane
 template <int CG>
 NMG_D void tload(uint32_t taddr, uint32_t* r) {
@@ -698,11 +636,7 @@ __global__ void strip_combine_kernel(int n, int nrhs, const float4* __restrict__
 template <int C, bool FIRST>
 void launch(const CUtensorMap* mh, const CUtensorMap* ml, const StripArgs& a, int num_sms, cudaStream_t s) {
   using G = Cfg<C>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(conv_strip_kernel<C, FIRST>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
-    attr = true;
-  }
+  NMG_SMEM_OPTIN((conv_strip_kernel<C, FIRST>), G::SMEM);
   const int units = a.nrhs * (a.n >= SEG ? a.n / SEG : 1) * a.ysplit;
   const int grid = std::min(units, num_sms);
   CUtensorMap dummy{};

@@ -294,11 +294,7 @@ int gemm_f64_ntiles(int N) { return ceil_div(N, DBN); }
 
 void gemm_f64(const Gemm64Args& a, cudaStream_t s) {
   const size_t smem = (size_t)DSTAGES * (DBM + DBN) * DLDS * sizeof(double);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(dgemm_resid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_set = true;
-  }
+  NMG_SMEM_OPTIN(dgemm_resid_kernel, smem);
   dim3 grid(ceil_div(a.N, DBN), ceil_div(a.M, DBM));
   dgemm_resid_kernel<<<grid, DNT, smem, s>>>(a);
 }

@@ -14,6 +14,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tcgen05.cuh"
 
 namespace nmg {
 namespace {
@@ -34,72 +35,8 @@ template <int TBN> struct TcCfg {
   static constexpr uint32_t IDESC16 = (1u << 4) | ((uint32_t)(TBN >> 3) << 17) | ((uint32_t)(TBM >> 4) << 24);
 };
 
-NMG_D uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
-
-NMG_D void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-NMG_D void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes));
-}
-NMG_D void mbar_wait(uint64_t* bar, uint32_t parity) {
-  const uint32_t a = smem_u32(bar);
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@P1 bra DONE;\n"
-      "bra LAB_WAIT;\n"
-      "DONE:\n"
-      "}\n" ::"r"(a),
-      "r"(parity));
-}
-NMG_D void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-      : "memory");
-}
 NMG_D void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(map) : "memory");
-}
-
-// UMMA shared-memory descriptor, K-major, SWIZZLE_64B: rows of 64 bytes, 8-row core
-// groups 512 bytes apart (SBO), LBO unused (1), version 1 (sm_100), layout type 4.
-NMG_D uint64_t umma_desc_sw64(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)1 << 16;                  // LBO (ignored for swizzled K-major)
-  d |= (uint64_t)(512 >> 4) << 32;         // SBO
-  d |= (uint64_t)1 << 46;                  // version
-  d |= (uint64_t)4 << 61;                  // SWIZZLE_64B
-  return d;
-}
-
-NMG_D void umma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate, uint32_t idesc) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
-}
-NMG_D void umma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate, uint32_t idesc) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
-}
-NMG_D void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                   smem_u32(bar))
-               : "memory");
 }
 
 NMG_D void tc_store_chunk(const TcGemmArgs& a, const uint32_t (&v)[32], int m, int nb, const float* crow,
@@ -162,8 +99,8 @@ NMG_D void tc_store_chunk(const TcGemmArgs& a, const uint32_t (&v)[32], int m, i
 NMG_D void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, uint16_t mask) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%3, "
-      "%4}], [%2], %5;\n" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      "%4}], [%2], %5;\n" ::"r"(su32(dst)),
+      "l"(map), "r"(su32(bar)), "r"(c0), "r"(c1), "h"(mask)
       : "memory");
 }
 NMG_D void cluster_sync_all() {
@@ -201,13 +138,13 @@ __global__ void __launch_bounds__(TNT, 1)
 
   const uint32_t crank = MC ? cta_rank_in_cluster() : 0u;
   if (tid == 0) {
-    for (int s = 0; s < TSTAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], MC ? 2 : 1); }
-    mbar_init(done, 1);
+    for (int s = 0; s < TSTAGES; ++s) { mb_init(&full[s], 1); mb_init(&empty[s], MC ? 2 : 1); }
+    mb_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     prefetch_tmap(&tXh); prefetch_tmap(&tXl); prefetch_tmap(&tWh); prefetch_tmap(&tWl);
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
                  "r"(TBN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
@@ -222,20 +159,20 @@ __global__ void __launch_bounds__(TNT, 1)
       for (int kt = 0; kt < KT; ++kt) {
         const int s = kt % TSTAGES;
         const uint32_t ph = (uint32_t)(kt / TSTAGES) & 1u;
-        mbar_wait(&empty[s], ph ^ 1u);
+        mb_wait(&empty[s], ph ^ 1u);
         uint8_t* st = sm + s * STAGE_BYTES;
-        mbar_expect_tx(&full[s], STAGE_BYTES);
+        mb_expect(&full[s], STAGE_BYTES);
         const int k0 = kt * KE;
-        tma_load_2d(st, &tXh, &full[s], k0, m0);
-        tma_load_2d(st + A_BYTES, &tXl, &full[s], k0, m0);
+        tma2d(st, &tXh, &full[s], k0, m0);
+        tma2d(st + A_BYTES, &tXl, &full[s], k0, m0);
         if (MC) {
           const int hr = TBN / 2;
           tma_load_2d_mc(st + 2 * A_BYTES + crank * (B_BYTES / 2), &tWh, &full[s], k0, n0 + (int)crank * hr, 3);
           tma_load_2d_mc(st + 2 * A_BYTES + B_BYTES + crank * (B_BYTES / 2), &tWl, &full[s], k0, n0 + (int)crank * hr,
                          3);
         } else {
-          tma_load_2d(st + 2 * A_BYTES, &tWh, &full[s], k0, n0);
-          tma_load_2d(st + 2 * A_BYTES + B_BYTES, &tWl, &full[s], k0, n0);
+          tma2d(st + 2 * A_BYTES, &tWh, &full[s], k0, n0);
+          tma2d(st + 2 * A_BYTES + B_BYTES, &tWl, &full[s], k0, n0);
         }
       }
     }
@@ -245,42 +182,42 @@ __global__ void __launch_bounds__(TNT, 1)
       for (int kt = 0; kt < KT; ++kt) {
         const int s = kt % TSTAGES;
         const uint32_t ph = (uint32_t)(kt / TSTAGES) & 1u;
-        mbar_wait(&full[s], ph);
+        mb_wait(&full[s], ph);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        const uint32_t st = smem_u32(sm + s * STAGE_BYTES);
+        const uint32_t st = su32(sm + s * STAGE_BYTES);
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks) {
           const uint32_t ko = ks * 32;   // 8 tf32 / 16 f16 = 32 bytes along the 64-byte swizzled row
-          const uint64_t dxh = umma_desc_sw64(st + ko);
-          const uint64_t dxl = umma_desc_sw64(st + A_BYTES + ko);
-          const uint64_t dwh = umma_desc_sw64(st + 2 * A_BYTES + ko);
-          const uint64_t dwl = umma_desc_sw64(st + 2 * A_BYTES + B_BYTES + ko);
+          const uint64_t dxh = desc_sw64(st + ko);
+          const uint64_t dxl = desc_sw64(st + A_BYTES + ko);
+          const uint64_t dwh = desc_sw64(st + 2 * A_BYTES + ko);
+          const uint64_t dwl = desc_sw64(st + 2 * A_BYTES + B_BYTES + ko);
           if (F16) {
-            umma_f16(tmem, dxh, dwh, (kt | ks) ? 1u : 0u, kIdesc);
-            umma_f16(tmem, dxh, dwl, 1u, kIdesc);
-            umma_f16(tmem, dxl, dwh, 1u, kIdesc);
+            mma_f16(tmem, dxh, dwh, kIdesc, (kt | ks) ? 1u : 0u);
+            mma_f16(tmem, dxh, dwl, kIdesc, 1u);
+            mma_f16(tmem, dxl, dwh, kIdesc, 1u);
           } else {
-            umma_tf32(tmem, dxh, dwh, (kt | ks) ? 1u : 0u, kIdesc);
-            umma_tf32(tmem, dxh, dwl, 1u, kIdesc);
-            umma_tf32(tmem, dxl, dwh, 1u, kIdesc);
+            mma_tf32(tmem, dxh, dwh, kIdesc, (kt | ks) ? 1u : 0u);
+            mma_tf32(tmem, dxh, dwl, kIdesc, 1u);
+            mma_tf32(tmem, dxl, dwh, kIdesc, 1u);
           }
         }
         if (MC)   // slot reusable when both CTAs' MMAs retired
           asm volatile(
               "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
-                  smem_u32(&empty[s])),
+                  su32(&empty[s])),
               "h"((uint16_t)3)
               : "memory");
         else
-          umma_commit(&empty[s]);    // slot reusable when these MMAs retire
+          mma_commit(&empty[s]);    // slot reusable when these MMAs retire
       }
-      umma_commit(done);             // accumulator complete
+      mma_commit(done);             // accumulator complete
     }
     __syncwarp();
   }
 
   // ---------------- epilogue: all 4 warps, warp w owns TMEM lanes 32w..32w+31 (rows)
-  mbar_wait(done, 0);
+  mb_wait(done, 0);
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const int row = warp * 32 + lane;
   const int m = m0 + row;
@@ -371,15 +308,9 @@ int tc_gemm_block_m() { return TBM; }
 
 void tc_gemm_f16(const CUtensorMap* xh, const CUtensorMap* xl, const CUtensorMap* wh, const CUtensorMap* wl,
                  const TcGemmArgs& a, cudaStream_t s, int bn) {
-  static bool attr256 = false, attr64 = false;
   dim3 grid(ceil_div(a.N, bn), ceil_div(a.M, TBM));
   if (bn == 256 && a.wh_mc && grid.y % 2 == 0) {
-    static bool attrmc = false;
-    if (!attrmc) {
-      cudaFuncSetAttribute(tc_gemm_kernel<256, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           TcCfg<256>::SMEM);
-      attrmc = true;
-    }
+    NMG_SMEM_OPTIN((tc_gemm_kernel<256, true, true>), TcCfg<256>::SMEM);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(TNT);
@@ -394,16 +325,10 @@ void tc_gemm_f16(const CUtensorMap* xh, const CUtensorMap* xl, const CUtensorMap
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, tc_gemm_kernel<256, true, true>, *xh, *xl, *a.wh_mc, *a.wl_mc, a);
   } else if (bn == 256) {
-    if (!attr256) {
-      cudaFuncSetAttribute(tc_gemm_kernel<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<256>::SMEM);
-      attr256 = true;
-    }
+    NMG_SMEM_OPTIN((tc_gemm_kernel<256, true>), TcCfg<256>::SMEM);
     tc_gemm_kernel<256, true><<<grid, TNT, TcCfg<256>::SMEM, s>>>(*xh, *xl, *wh, *wl, a);
   } else {
-    if (!attr64) {
-      cudaFuncSetAttribute(tc_gemm_kernel<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<64>::SMEM);
-      attr64 = true;
-    }
+    NMG_SMEM_OPTIN((tc_gemm_kernel<64, true>), TcCfg<64>::SMEM);
     tc_gemm_kernel<64, true><<<grid, TNT, TcCfg<64>::SMEM, s>>>(*xh, *xl, *wh, *wl, a);
   }
 }
@@ -415,19 +340,12 @@ void split_f16_rows(int rows, int K, const float* x, uint16_t* hi, uint16_t* lo,
 
 void tc_gemm(const CUtensorMap* xh, const CUtensorMap* xl, const CUtensorMap* wh, const CUtensorMap* wl,
              const TcGemmArgs& a, cudaStream_t s, int bn) {
-  static bool attr256 = false, attr64 = false;
   dim3 grid(ceil_div(a.N, bn), ceil_div(a.M, TBM));
   if (bn == 256) {
-    if (!attr256) {
-      cudaFuncSetAttribute(tc_gemm_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<256>::SMEM);
-      attr256 = true;
-    }
+    NMG_SMEM_OPTIN(tc_gemm_kernel<256>, TcCfg<256>::SMEM);
     tc_gemm_kernel<256><<<grid, TNT, TcCfg<256>::SMEM, s>>>(*xh, *xl, *wh, *wl, a);
   } else {
-    if (!attr64) {
-      cudaFuncSetAttribute(tc_gemm_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<64>::SMEM);
-      attr64 = true;
-    }
+    NMG_SMEM_OPTIN(tc_gemm_kernel<64>, TcCfg<64>::SMEM);
     tc_gemm_kernel<64><<<grid, TNT, TcCfg<64>::SMEM, s>>>(*xh, *xl, *wh, *wl, a);
   }
 }

@@ -166,8 +166,6 @@ void smooth1d(const Smooth1dArgs& a, cudaStream_t s);
 // same step with the 16 -> 16 layer on tcgen05 (FP16x3, n % 128 == 0), smooth1d_f16.cu
 void smooth1d_f16(const Smooth1dArgs& a, cudaStream_t s);
 size_t smooth1d_smem(int n);
-// same step with the 16 -> 16 layer on tcgen05 (3xTF32), smooth1d_tc.cu
-void smooth1d_tc(const Smooth1dArgs& a, cudaStream_t s);
 
 // ---- 1D transfers (reading R4) ------------------------------------------------
 void restrict1d(int nrhs, int n_f, const float* f, int64_t ldf, float* c, int64_t ldc, cudaStream_t s);
@@ -233,22 +231,6 @@ void filter2d_slab_cols(int n, int npair, int R, int W, int rank, float2* buf, c
 void filter2d_slab_inverse(int n, int nrhs, int R, float2* Zs, const float2* tw, int tw_n, float* x, int64_t ximg,
                            int64_t xoff, bool accumulate, const double* norms, cudaStream_t s);
 void real_to_complex(int nrhs, int64_t N, const float* x, float2* Z, cudaStream_t s);
-
-// ---- 2D CNN on tensor cores (conv_tc.cu), C = 32 ------------------------------------
-// Activations: padded pixel-major fp32 [b][n+2][n+2][32], zero border.
-struct ConvTcArgs {
-  int n, nrhs;
-  const float* bias;        // [32]
-  float* out;
-};
-void conv3x3_tc(const CUtensorMap* ah, const CUtensorMap* al, const CUtensorMap* in, const ConvTcArgs& a,
-                int num_sms, cudaStream_t s);
-int conv_tc_smem();
-void conv_in(int n, int nrhs, const float* b, const double* norms, const float* w0, const float* b0, float* o1,
-             float* z2, cudaStream_t s);   // also zeroes the borders of o1 and z2
-void conv_out(int n, int nrhs, const float* in, const double* norms, const float* w3, const float* b3, float2* Z,
-              int zb0, float* x, bool accumulate, cudaStream_t s);
-void zero_border(int n, int nrhs, int C, float* buf, cudaStream_t s);
 
 // ---- 2D CNN, FP16x3 tcgen05 column-strip kernels (conv_strip.cu), n % 128 == 0, C = 32/48 --
 // Layers 1+2 (strip_l12): b -> a2 (scaled f16 hi/lo, [b][y][x][C]); layers 3+4 (strip_l34,

@@ -19,6 +19,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tcgen05.cuh"
 
 namespace nmg {
 namespace {
@@ -37,65 +38,6 @@ template <int TBN> struct KronCfg {
   static constexpr uint32_t TCOLS = 2 * TBN < 32 ? 32 : 2 * TBN;
 };
 
-NMG_D uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
-NMG_D void mb_init(uint64_t* b, uint32_t c) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(c));
-}
-NMG_D void mb_expect(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes) : "memory");
-}
-NMG_D void mb_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
-}
-NMG_D void mb_wait(uint64_t* b, uint32_t ph) {
-  asm volatile(
-      "{\n.reg .pred P1;\nWAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@P1 bra DONE_%=;\nbra WAIT_%=;\nDONE_%=:\n}\n" ::"r"(su32(b)),
-      "r"(ph)
-      : "memory");
-}
-NMG_D void tma2d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::"r"(
-          su32(dst)),
-      "l"(m), "r"(su32(bar)), "r"(c0), "r"(c1)
-      : "memory");
-}
-// K-major SWIZZLE_64B operand: 64-byte rows, 8-row groups 512 B apart
-NMG_D uint64_t desc_sw64(uint32_t saddr) {
-  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)1 << 16;
-  d |= (uint64_t)(512 >> 4) << 32;
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)4 << 61;
-  return d;
-}
-NMG_D void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc));
-}
-NMG_D void mma_commit(uint64_t* b) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(b))
-               : "memory");
-}
-NMG_D void tld16(uint32_t taddr, uint32_t* r) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-}
-// the wait carries the loaded registers so no use can be scheduled above it
-NMG_D void tld_wait16(uint32_t* r) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
-               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
-                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
-               :
-               : "memory");
-}
 NMG_D float rna_tf32(float v) {
   uint32_t h;
   asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(h) : "f"(v));
@@ -302,11 +244,7 @@ __global__ void __launch_bounds__(KNT, 1)
 template <int TBN, int HB>
 void launch_kron(const CUtensorMap* A, const CUtensorMap* Wh, const CUtensorMap* Wl, const KronArgs& a, int sms,
                  cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kron_tc_kernel<TBN, HB>, cudaFuncAttributeMaxDynamicSharedMemorySize, KronCfg<TBN>::SMEM);
-    attr = true;
-  }
+  NMG_SMEM_OPTIN((kron_tc_kernel<TBN, HB>), KronCfg<TBN>::SMEM);
   const int cols = a.mode == KRON_T ? a.n : (a.R ? a.R : a.n);
   const int tiles = ceil_div(a.M, KBM) * ceil_div(cols, TBN);
   kron_tc_kernel<TBN, HB><<<std::min(tiles, sms), KNT, KronCfg<TBN>::SMEM, s>>>(*A, *Wh, *Wl, a);

@@ -525,10 +525,10 @@ void cnn2d(const Cnn2dArgs& a, cudaStream_t s) {
   dim3 grid(tiles, a.nrhs);
   const int smem = cnn2d_smem(a.C);
   if (a.C == 32) {
-    cudaFuncSetAttribute(cnn2d_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    NMG_SMEM_OPTIN(cnn2d_kernel<32>, smem);
     cnn2d_kernel<32><<<grid, 256, smem, s>>>(a);
   } else {
-    cudaFuncSetAttribute(cnn2d_kernel<48>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    NMG_SMEM_OPTIN(cnn2d_kernel<48>, smem);
     cnn2d_kernel<48><<<grid, 256, smem, s>>>(a);
   }
 }

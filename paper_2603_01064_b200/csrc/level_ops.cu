@@ -355,14 +355,10 @@ void coarse_chol_solve(int nc, int nrhs, const double* Lrow, const double* Lcol,
                        float* x, int64_t ldx, cudaStream_t s, float* xh, float* xl) {
   const int grid = ceil_div(nrhs, kCoarseWarps);
   const int nq = ceil_div(nc, 32);
-  static bool attr[9] = {};
 #define NMG_COARSE(Q)                                                                                   \
   case Q: {                                                                                             \
     const int smem = (2 * 32 * Q * 32 + Q * 32 + kCoarseWarps * 32) * (int)sizeof(double);           \
-    if (!attr[Q]) {                                                                                     \
-      cudaFuncSetAttribute(coarse_kernel<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);       \
-      attr[Q] = true;                                                                                   \
-    }                                                                                                   \
+    NMG_SMEM_OPTIN(coarse_kernel<Q>, smem);                                                           \
     coarse_kernel<Q><<<grid, kCoarseWarps * 32, smem, s>>>(nc, nrhs, Lrow, Lcol, y, ldy, x, ldx, xh, xl);           \
   } break;
   switch (nq) {

@@ -310,6 +310,7 @@ nmg_status make_a2_map(CUtensorMap* m, const uint16_t* p, int n, int C, int64_t 
 // ======================================================================= handle
 struct nmg_hierarchy {
   nmg_problem_desc d{};
+  nmg_tuning tune{};                                     // copied from desc.tuning (zeros = defaults)
   int L = 0;
   std::vector<int> n;      // points per axis, level 0 = finest
   std::vector<int64_t> N;  // unknowns per level
@@ -325,13 +326,12 @@ struct nmg_hierarchy {
   // 1D inner operator applies in FP16x3 (kind::f16): per-row-scaled f16 hi/lo planes
   bool gemm_f16 = false;
   struct F16Op { DevBuf<uint16_t> h, l; DevBuf<float> winv; CUtensorMap m256h, m256l, m64h, m64l, m128h, m128l; };
-  bool gemm_mc = true;                                   // NMG_GEMM_MC=0: no W multicast in the FP16x3 GEMM
+  bool gemm_mc = true;                                   // 256-wide FP16x3 tiles multicast W over CTA pairs
   std::vector<std::unique_ptr<F16Op>> A16, AP16;         // per smoothed level
   std::vector<std::unique_ptr<DevBuf<uint16_t>>> sx16h, sx16l;
   std::vector<std::unique_ptr<DevBuf<float>>> sxinv;
   std::vector<CUtensorMap> mX16h, mX16l;
   bool use_tc = true;
-  bool smooth_tc = false;                                // 1D smoother layer 2 on tcgen05 3xTF32 (opt-in)
   bool smooth_f16 = false;                               // 1D smoother layer 2 on tcgen05 FP16x3 (default)
   std::vector<std::unique_ptr<DevBuf<uint16_t>>> W1b;    // per level: stacked f16 layer-2 weights
   std::vector<float> s1d_sc;                             // per level: S1, T1
@@ -358,18 +358,12 @@ struct nmg_hierarchy {
   DevBuf<double> snorm, spart;                           // smoother norms
   DevBuf<double> T64;                                    // fp64 outer step-1 output
   int rows_per_rhs = 1;
-  // 2D CNN hidden layers on tcgen05 (C = 32): padded hi/lo activations, A-operand weights
-  bool conv_tc = false;
   int num_sms = 148;
-  int conv_chunk = 0;
-  DevBuf<float> act1, act2;
-  std::vector<std::unique_ptr<DevBuf<float>>> WA;        // per level: [layer 0 hi, lo, layer 1 hi, lo]
-  std::vector<CUtensorMap> mWAh, mWAl;                   // [level * 2 + layer]
-  std::vector<CUtensorMap> mA1, mA2;                     // per level activation maps
-  // 2D CNN on tcgen05 FP16x3 column-strip kernels (levels with n % 128 == 0, C = 32 / 48)
+  // 2D CNN on tcgen05 FP16x3 column-strip kernels (levels with n % 128 == 0 or 16 <= n < 128,
+  // C = 32 / 48); other levels and tune.ffma_cnn use the FFMA kernel cnn2d
   bool conv_bf = false;
   int bf_C = 0, bf_chunk = 0;
-  bool fuse_combine = true;                              // NMG_FUSE_COMBINE=0: separate combine + row FFT
+  bool fuse_combine = true;                              // strip combine fused with the forward row FFT
   int64_t bf_px = 0;                                     // pixels per RHS the a2 / q workspaces hold
   std::vector<float> strip_sc;                           // per level: S1, T1, S2, T2
   DevBuf<uint16_t> a2h, a2l;                             // [chunk][n][n][C] f16 hi / lo (scaled by S2)
@@ -391,8 +385,8 @@ struct nmg_hierarchy {
   std::vector<std::unique_ptr<DevBuf<float>>> wy, wx, wr, wb;
   DevBuf<double> part, ynorm, relres, ywork;
   DevBuf<uint8_t> active;
-  DevBuf<double> hy, hx;   // staging for nmg_vcycles_host (lazy)
-  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;         // copy streams of nmg_vcycles_host (lazy)
+  DevBuf<double> hy, hx;   // staging for nmg_vcycles_host (allocated at create)
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;         // copy streams of nmg_vcycles_host
   std::vector<cudaEvent_t> hev;                          // its chunk events
   int ntiles = 0;
   int64_t launches = 0;
@@ -407,7 +401,7 @@ struct nmg_hierarchy {
   // of nmg_vcycles_host each replay their own graph
   bool use_graph = true;
   struct GraphEntry {
-    int nrhs; const void* y; void* x; cudaStream_t s;
+    int nrhs; const void* y; void* x; cudaStream_t s; bool lanes;
     int seen; cudaGraphExec_t exec; int64_t launches; uint64_t used;
   };
   std::vector<GraphEntry> graphs;
@@ -417,7 +411,7 @@ struct nmg_hierarchy {
   // each launch and the small coarse-level grids); both halves are captured in one graph
   std::vector<std::unique_ptr<nmg_hierarchy>> lanes;     // lanes 1 .. K-1 (lane 0 is this handle)
   int lane_mult = 1;                                     // K while the lanes run (GEMM tile choice)
-  bool lane_tiles = true;                                // NMG_LANE_TILES=0: per-lane tile choice
+  bool lane_tiles = true;                                // GEMM tile width chosen for the whole batch
   std::vector<cudaStream_t> ls;                          // one forked stream per extra lane
   cudaEvent_t evf = nullptr;
   std::vector<cudaEvent_t> evj;
@@ -500,8 +494,6 @@ void launch_smooth1d(nmg_hierarchy* h, int l, Smooth1dArgs& a, cudaStream_t s) {
     a.w = h->s1d_w[l];
     for (int c = 0; c < 16; ++c) a.w.b0[c] *= S1;
     smooth1d_f16(a, s);
-  } else if (h->smooth_tc) {
-    smooth1d_tc(a, s);
   } else {
     smooth1d(a, s);
   }
@@ -759,37 +751,6 @@ nmg_status smooth2d(nmg_hierarchy* h, int l, int nrhs, const float* b, float* x,
       { Prof p(h, NMG_K_SMOOTH, s);
         filter2d(nrhs, n, h->Z.p, h->tw.p, h->tw_n, x, accumulate, s, normalize ? h->snorm.p : nullptr,
                  h->fuse_combine); }
-      NMG_TRY(check_launch(h));
-    }
-    return NMG_OK;
-  }
-  if (h->conv_tc && h->arch.channels == 32 && n >= 8) {
-    const int C = 32;
-    const float* P = h->W[l]->p;
-    const float* w0 = P;
-    const float* b0 = P + C * 9;
-    const float* b1 = b0 + C + C * C * 9;
-    const float* b2 = b1 + C + C * C * 9;
-    const float* w3 = b2 + C;
-    const float* b3 = w3 + C * 9;
-    const double* nrm = normalize ? h->snorm.p : nullptr;
-    for (int r0 = 0; r0 < nrhs; r0 += h->conv_chunk) {
-      const int cnt = std::min(h->conv_chunk, nrhs - r0);
-      const int64_t off = (int64_t)r0 * N;
-      { Prof p(h, NMG_K_SMOOTH, s);
-        conv_in(n, cnt, b + off, nrm ? nrm + r0 : nullptr, w0, b0, h->act1.p, h->act2.p, s); }
-      ConvTcArgs ca{};
-      ca.n = n; ca.nrhs = cnt; ca.bias = b1; ca.out = h->act2.p;
-      { Prof p(h, NMG_K_SMOOTH, s); conv3x3_tc(&h->mWAh[l * 2], &h->mWAl[l * 2], &h->mA1[l], ca, h->num_sms, s); }
-      ca.bias = b2; ca.out = h->act1.p;
-      { Prof p(h, NMG_K_SMOOTH, s); conv3x3_tc(&h->mWAh[l * 2 + 1], &h->mWAl[l * 2 + 1], &h->mA2[l], ca, h->num_sms, s); }
-      { Prof p(h, NMG_K_SMOOTH, s);
-        conv_out(n, cnt, h->act1.p, nrm ? nrm + r0 : nullptr, w3, b3, filt ? h->Z.p : nullptr, r0, x + off,
-                 accumulate, s); }
-      NMG_TRY(check_launch(h));
-    }
-    if (filt) {
-      { Prof p(h, NMG_K_SMOOTH, s); filter2d(nrhs, n, h->Z.p, h->tw.p, h->tw_n, x, accumulate, s, normalize ? h->snorm.p : nullptr); }
       NMG_TRY(check_launch(h));
     }
     return NMG_OK;
@@ -1254,11 +1215,22 @@ thread_local bool t_no_lanes = false;
 // One cycle through a cached CUDA graph: the first call with a given (nrhs, y, x, stream) runs
 // eagerly, the second captures the whole cycle, later calls replay it (launch-latency bound
 // small configs and coarse levels).
-nmg_status graph_cycle(nmg_hierarchy* h, int nrhs, const double* y, double* x, cudaStream_t s) {
+void drop_graphs(nmg_hierarchy* h) {
+  for (auto& g : h->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  h->graphs.clear();
+  for (auto& hk : h->lanes) drop_graphs(hk.get());
+}
+
+// allow_lanes = false: the whole batch runs on this handle alone (the host-buffer pipeline runs
+// its lane 0 this way while lanes 1..K-1 cycle their own RHS on the lane handles concurrently,
+// so a lane handle is never used by two graphs at once).
+nmg_status graph_cycle(nmg_hierarchy* h, int nrhs, const double* y, double* x, cudaStream_t s,
+                       bool allow_lanes = true) {
   auto body = [&]() -> nmg_status {
     const int K = (int)h->lanes.size() + 1;
     const int gr = h->d.dim == 1 ? 128 : 2;             // lane granularity (GEMM M tiles / filter pairs)
-    if (K == 1 || h->prof_on || nrhs < K * gr || s == nullptr) {
+    if (K == 1 || !allow_lanes || h->prof_on || nrhs < K * gr || s == nullptr) {
       NMG_TRY(ynorms(h, nrhs, y, s));
       return outer_step(h, nrhs, y, x, -1.0, false, s);
     }
@@ -1298,7 +1270,7 @@ nmg_status graph_cycle(nmg_hierarchy* h, int nrhs, const double* y, double* x, c
   if (!h->use_graph || h->slab || s == nullptr || h->prof_on) return body();
   nmg_hierarchy::GraphEntry* g = nullptr;
   for (auto& e : h->graphs)
-    if (e.nrhs == nrhs && e.y == y && e.x == x && e.s == s) g = &e;
+    if (e.nrhs == nrhs && e.y == y && e.x == x && e.s == s && e.lanes == allow_lanes) g = &e;
   if (!g) {
     if (h->graphs.size() >= 8) {
       auto old = h->graphs.begin();
@@ -1307,7 +1279,7 @@ nmg_status graph_cycle(nmg_hierarchy* h, int nrhs, const double* y, double* x, c
       if (old->exec) cudaGraphExecDestroy(old->exec);
       h->graphs.erase(old);
     }
-    h->graphs.push_back({nrhs, y, x, s, 0, nullptr, 0, 0});
+    h->graphs.push_back({nrhs, y, x, s, allow_lanes, 0, nullptr, 0, 0});
     g = &h->graphs.back();
   }
   g->used = ++h->g_clock;
@@ -1381,8 +1353,15 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
   if (prop.major != 10) return fail(NMG_ERR_CUDA, "device %d is sm_%d%d; this library is built for sm_100a", d.device, prop.major, prop.minor);
   NMG_CUDA(cudaSetDevice(d.device));
 
+  if (d.precision != NMG_PREC_MIXED && d.precision != NMG_PREC_FP64)
+    return fail(NMG_ERR_INVALID_ARG, "precision must be NMG_PREC_MIXED or NMG_PREC_FP64 (got %d)", d.precision);
+  if (d.precision == NMG_PREC_FP64 && (d.dim != 1 || d.n > 1024))
+    return fail(NMG_ERR_UNSUPPORTED, "NMG_PREC_FP64 is implemented for 1D problems with n <= 1024");
+
   auto h = std::make_unique<nmg_hierarchy>();
   h->d = d;
+  if (d.tuning) h->tune = *d.tuning;
+  h->d.tuning = nullptr;                                 // the caller's struct is not kept
   h->L = d.levels;
   for (int l = 0; l < h->L; ++l) {
     h->n.push_back(d.n >> l);
@@ -1502,8 +1481,7 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
   NMG_TRY(h->Lcol.upload(Lt.data(), Lt.size()));
   {
     // explicit inverse A_L^{-1} = L^{-T} L^{-1} (fp64, symmetric), column by column
-    const char* ce = std::getenv("NMG_COARSE");
-    h->coarse_inv = !(ce && std::string(ce) == "chol");
+    h->coarse_inv = h->tune.coarse_subst == 0;
     if (h->coarse_inv) {
       std::vector<double> inv((size_t)Nc * Nc), z(Nc);
       for (int j = 0; j < Nc; ++j) {
@@ -1550,21 +1528,10 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
       if (need) NMG_TRY(v->back()->alloc(B * (size_t)h->N[l]));
     }
   }
-  {
-    const char* env = std::getenv("NMG_GEMM");
-    h->use_tc = !(env && std::string(env) == "simt");
-    const char* genv = std::getenv("NMG_GRAPH");
-    h->use_graph = !(genv && std::string(genv) == "0");
-    const char* senv = std::getenv("NMG_SMOOTH1D");
-    // measured slower than the FFMA kernel (16 channels: the A tile is re-read from smem for only
-    // N = 16 outputs per MMA, 32 cycles/MMA smem-bound, no overlap within the CTA): opt-in only
-    h->smooth_tc = h->use_tc && (senv && std::string(senv) == "tc");
-    h->smooth_f16 = h->use_tc && !(senv && (std::string(senv) == "tc" || std::string(senv) == "ffma"));
-  }
-  if (d.dim == 1) {
-    const char* genv16 = std::getenv("NMG_GEMM");
-    h->gemm_f16 = h->use_tc && !(genv16 && std::string(genv16) == "tf32");
-  }
+  h->use_tc = h->tune.simt_gemm == 0;
+  h->use_graph = h->tune.no_graphs == 0;
+  h->smooth_f16 = h->use_tc && h->tune.ffma_cnn == 0;
+  if (d.dim == 1) h->gemm_f16 = h->use_tc;            // 1D inner applies: FP16x3 on tcgen05
   if (d.dim == 1) {
     h->mAh.resize(h->L); h->mAl.resize(h->L); h->mAPh.resize(h->L); h->mAPl.resize(h->L);
     h->mAh64.resize(h->L); h->mAl64.resize(h->L); h->mAPh64.resize(h->L); h->mAPl64.resize(h->L);
@@ -1619,10 +1586,7 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
     h->mTh.resize(h->L); h->mTl.resize(h->L); h->mXh.resize(h->L); h->mXl.resize(h->L);
     h->mBh64.resize(h->L); h->mBl64.resize(h->L); h->mCh64.resize(h->L); h->mCl64.resize(h->L);
     h->mKBh.resize(h->L); h->mKBl.resize(h->L); h->mKCh.resize(h->L); h->mKCl.resize(h->L);
-    {
-      const char* env = std::getenv("NMG_KRON");
-      h->use_kron = h->use_tc && !(env && std::string(env) == "0");
-    }
+    h->use_kron = h->use_tc && h->tune.no_kron == 0;
     for (int l = 0; l < h->L; ++l) {
       const int nl = h->n[l];
       for (auto* v : {&h->sxh, &h->sxl, &h->tth, &h->ttl}) {
@@ -1656,50 +1620,15 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
     NMG_TRY(h->spart.alloc(B * 64));
     NMG_TRY(h->T64.alloc(B * (size_t)h->N[0]));
     h->rows_per_rhs = n;
-    {
-      const char* env = std::getenv("NMG_CONV");
-      h->conv_tc = h->use_tc && !(env && std::string(env) == "ffma");
-      // FP16x3 column-strip kernels for levels with n % 128 == 0 (NMG_CONV=tf32 keeps the
-      // older 3xTF32 pixel-N kernel at every level, C = 32 only)
-      h->conv_bf = h->conv_tc && !(env && std::string(env) == "tf32");
-      const char* fe = std::getenv("NMG_FUSE_COMBINE");
-      h->fuse_combine = !(fe && std::string(fe) == "0");
-      int sms = 0;
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d.device);
-      h->num_sms = sms > 0 ? sms : 148;
-    }
-    if (h->conv_tc) {
-      // the 3xTF32 kernel serves the levels the BF16 strip kernels do not (n < 128)
-      int nold = 0;
-      for (int l = 0; l < h->L - 1; ++l)
-        if (!(h->conv_bf && strip_level(h->n[l]))) nold = std::max(nold, h->n[l]);
-      const int64_t Wp = std::max(nold, 2) + 2;
-      const int64_t per = Wp * Wp * 32;                         // floats per RHS per array
-      const int64_t budget = (int64_t)6 << 30;                  // floats over the 2 arrays (24 GiB)
-      h->conv_chunk = (int)std::max<int64_t>(1, std::min<int64_t>(B, budget / (2 * per)));
-      for (auto* buf : {&h->act1, &h->act2}) {
-        NMG_TRY(buf->alloc((size_t)h->conv_chunk * per));
-        NMG_CUDA(cudaMemset(buf->p, 0, sizeof(float) * buf->n));
-      }
-      h->mA1.resize(h->L); h->mA2.resize(h->L);
-      for (int l = 0; l < h->L - 1; ++l) {
-        if (h->n[l] > nold) continue;
-        const int Wl = h->n[l] + 2;
-        const int64_t rows = (int64_t)h->conv_chunk * Wl;
-        NMG_TRY(make_act_map(&h->mA1[l], h->act1.p, rows, Wl));
-        NMG_TRY(make_act_map(&h->mA2[l], h->act2.p, rows, Wl));
-      }
-      h->mWAh.resize(2 * h->L); h->mWAl.resize(2 * h->L);
-      for (int l = 0; l < h->L - 1; ++l) h->WA.emplace_back(new DevBuf<float>());
+    // FP16x3 column-strip kernels for the levels strip_level() accepts; the rest FFMA (cnn2d)
+    h->conv_bf = h->use_tc && h->tune.ffma_cnn == 0;
+    if (h->conv_bf) {
       h->mA2h.resize(h->L); h->mA2l.resize(h->L);
       for (int l = 0; l < h->L - 1; ++l) h->WB.emplace_back(new DevBuf<uint16_t>());
     }
   }
   if (d.dim == 1) {
-    const char* fenv = std::getenv("NMG_FP64");
-    h->ozaki = h->use_tc && n % 128 == 0 && /* CTA pairs along N */ !(fenv && std::string(fenv) == "dmma");
-    const char* menv = std::getenv("NMG_GEMM_MC");
-    h->gemm_mc = !(menv && std::string(menv) == "0");
+    h->ozaki = h->use_tc && n % 128 == 0 && /* CTA pairs along N */ h->tune.fp64_dmma == 0;
     if (h->ozaki) {
       // W digits of A (rows n, K = n), host: exponent per row, S truncation digits
       const int S = ozaki_digits();
@@ -1718,9 +1647,8 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
   }
   if (d.dim == 2) {
     // fp64 outer residual as two Ozaki int8 passes (T = X C^T, then y - T B^T - alpha x);
-    // NMG_FP64=dmma keeps the DMMA kernel
-    const char* fenv = std::getenv("NMG_FP64");
-    h->ozaki2d = h->use_tc && n % 128 == 0 && !(fenv && std::string(fenv) == "dmma");
+    // tune.fp64_dmma keeps the DMMA kernel
+    h->ozaki2d = h->use_tc && n % 128 == 0 && h->tune.fp64_dmma == 0;
     if (h->ozaki2d) {
       const int S = ozaki_digits();
       std::vector<int8_t> dig;
@@ -1747,20 +1675,19 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
   NMG_TRY(h->relres.alloc(B));
   NMG_TRY(h->active.alloc(B));
   {
-    const char* le = std::getenv("NMG_LANES");
-    int K = t_no_lanes ? 1 : le ? std::max(1, std::min(8, std::atoi(le))) : 4;
+    const int tl = h->tune.lanes;
+    int K = t_no_lanes ? 1 : tl > 0 ? std::min(8, tl) : 4;
     if (d.dim != 1 && K > 1) {
       // 2D: two lanes by default while the batch is small enough that a second set of lane
-      // workspaces is cheap (cfg 2, 4: same device time, the host entry overlaps more); NMG_LANES2D=K
-      const char* l2 = std::getenv("NMG_LANES2D");
-      K = l2 ? std::max(1, std::min(8, std::atoi(l2))) : ((int64_t)d.max_rhs * h->N[0] <= ((int64_t)1 << 26) ? 2 : 1);
-      if (le && std::string(le) == "1") K = 1;
+      // workspaces is cheap (cfg 2, 4: same device time, the host entry overlaps more)
+      if (tl == 0) K = (int64_t)d.max_rhs * h->N[0] <= ((int64_t)1 << 26) ? 2 : 1;
       while (K > 1 && d.max_rhs < K * 16) --K;            // lanes of >= 16 RHS
     }
     while (d.dim == 1 && K > 1 && d.max_rhs < K * 256) --K;   // 1D lanes of >= 256 RHS
     if (K > 1) {
       nmg_problem_desc d2 = d;
       d2.max_rhs = (d.max_rhs + K - 1) / K + (d.dim == 1 ? 128 : 2);   // a lane's share (rounded up)
+      d2.tuning = &h->tune;
       t_no_lanes = true;                                 // a lane itself has no lanes
       nmg_status st = NMG_OK;
       for (int k = 1; k < K && st == NMG_OK; ++k) {
@@ -1770,8 +1697,6 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
       }
       t_no_lanes = false;
       NMG_TRY(st);
-      const char* lt = std::getenv("NMG_LANE_TILES");
-      h->lane_tiles = !(lt && std::string(lt) == "0");
       NMG_CUDA(cudaEventCreateWithFlags(&h->evf, cudaEventDisableTiming));
       for (int k = 1; k < K; ++k) {
         cudaStream_t x;
@@ -1782,6 +1707,16 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
         h->evj.push_back(e);
       }
     }
+  }
+  if (!t_no_lanes && d.precision == NMG_PREC_MIXED) {
+    // staging and copy streams of the host-buffer entry nmg_vcycles_host (no lazy allocation)
+    const size_t cnt = (size_t)d.max_rhs * h->N[0];
+    NMG_TRY(h->hy.alloc(cnt));
+    NMG_TRY(h->hx.alloc(cnt));
+    NMG_CUDA(cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking));
+    NMG_CUDA(cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking));
+    h->hev.resize(2 * 8 + 2);
+    for (auto& e : h->hev) NMG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   NMG_CUDA(cudaDeviceSynchronize());
   *out = h.release();
@@ -1875,6 +1810,10 @@ nmg_status nmg_load_smoother_weights(nmg_hierarchy* h, int32_t level, const nmg_
   }
   if (n_params != want) return fail(NMG_ERR_SHAPE, "expected %zu parameters, got %zu", want, n_params);
   NMG_CUDA(cudaSetDevice(h->d.device));
+  // captured cycle graphs bake in weight pointers, tensor maps and by-value weights: drop them
+  // (after the device is idle) so the next cycle re-captures with the new smoother
+  NMG_CUDA(cudaDeviceSynchronize());
+  drop_graphs(h);
   if (h->d.dim == 2) {
     // device layout: hidden-layer weights transposed to [c][t2][t1][o] (see cnn2d_kernel)
     std::vector<float> dev(params, params + n_params);
@@ -1982,39 +1921,6 @@ nmg_status nmg_load_smoother_weights(nmg_hierarchy* h, int32_t level, const nmg_
         h->bf_C = C;
       }
     }
-    if (h->conv_tc && C == 32) {
-      // A operand of the tcgen05 conv: rows (t1, o) = 32 t1 + o (96 of 128), K blocks (t2, 16-ch chunk)
-      const int NCH = 2, AM = 128, BLK = AM * 16;
-      std::vector<double> A((size_t)2 * 3 * NCH * BLK, 0.0);
-      size_t woff = (size_t)C * 9 + C;
-      for (int layer = 0; layer < 2; ++layer) {
-        double* Al = A.data() + (size_t)layer * 3 * NCH * BLK;
-        for (int t2 = 0; t2 < 3; ++t2)
-          for (int ch = 0; ch < NCH; ++ch)
-            for (int t1 = 0; t1 < 3; ++t1)
-              for (int o = 0; o < C; ++o)
-                for (int k = 0; k < 16; ++k) {
-                  const int c = ch * 16 + k;
-                  Al[((size_t)(t2 * NCH + ch) * AM + t1 * 32 + o) * 16 + k] =
-                      params[woff + (((size_t)o * C + c) * 3 + t2) * 3 + t1];
-                }
-        woff += (size_t)C * C * 9 + C;
-      }
-      std::vector<float> hi, lo;
-      split_host(A, hi, lo);
-      const size_t half = (size_t)3 * NCH * BLK;
-      std::vector<float> packed(4 * half);
-      for (int layer = 0; layer < 2; ++layer) {
-        std::copy(hi.begin() + layer * half, hi.begin() + (layer + 1) * half, packed.begin() + (2 * layer) * half);
-        std::copy(lo.begin() + layer * half, lo.begin() + (layer + 1) * half, packed.begin() + (2 * layer + 1) * half);
-      }
-      DevBuf<float>& wa = *h->WA[level - 1];
-      NMG_TRY(wa.upload(packed.data(), packed.size()));
-      for (int layer = 0; layer < 2; ++layer) {
-        NMG_TRY(make_map(&h->mWAh[(level - 1) * 2 + layer], wa.p + (2 * layer) * half, 3 * NCH * AM, 16, AM));
-        NMG_TRY(make_map(&h->mWAl[(level - 1) * 2 + layer], wa.p + (2 * layer + 1) * half, 3 * NCH * AM, 16, AM));
-      }
-    }
   } else {
     NMG_TRY(h->W[level - 1]->upload(params, n_params));
     if (h->smooth_f16) {
@@ -2096,9 +2002,9 @@ nmg_status nmg_solve(nmg_hierarchy* h, int32_t nrhs, const double* y, double* x,
   if (nrhs == 0) return NMG_OK;
   if (!y || !x || max_cycles < 0) return fail(NMG_ERR_INVALID_ARG, "bad arguments");
   const int64_t N = h->N[0];
-  std::vector<double> rr(nrhs);
+  std::vector<double> rr(nrhs), rr0(nrhs, 0.0);
   std::vector<uint8_t> act(nrhs, 1);
-  std::vector<int32_t> cyc(nrhs, 0);
+  std::vector<int32_t> cyc(nrhs, 0), above(nrhs, 0);
   if (rep && rep->history)
     for (size_t i = 0; i < (size_t)nrhs * (max_cycles + 1); ++i) rep->history[i] = NAN;
   cudaEvent_t e0, e1;
@@ -2113,6 +2019,10 @@ nmg_status nmg_solve(nmg_hierarchy* h, int32_t nrhs, const double* y, double* x,
   for (;; ++tau) {
     NMG_CUDA(cudaMemcpyAsync(rr.data(), h->relres.p, sizeof(double) * nrhs, cudaMemcpyDeviceToHost, s));
     NMG_CUDA(cudaStreamSynchronize(s));
+    if (h->slab) {
+      st = h->comm->check_async();
+      if (st != NMG_OK) break;
+    }
     int nact = 0;
     for (int b = 0; b < nrhs; ++b) {
       if (!act[b]) continue;
@@ -2122,6 +2032,15 @@ nmg_status nmg_solve(nmg_hierarchy* h, int32_t nrhs, const double* y, double* x,
         break;
       }
       if (rep && rep->history) rep->history[(size_t)b * (max_cycles + 1) + tau] = rr[b];
+      if (tau == 0) rr0[b] = rr[b];
+      // divergence = relres above 10x the initial relres for 5 consecutive cycles
+      above[b] = (tau > 0 && rr[b] > 10.0 * rr0[b]) ? above[b] + 1 : 0;
+      if (h->d.divergence_check && above[b] >= 5) {
+        if (rep) { rep->fail_cycle = tau; rep->fail_rhs = b; }
+        st = fail(NMG_ERR_DIVERGED, "rhs %d diverged: relres %.3e > 10 x initial %.3e for 5 cycles (cycle %d)", b,
+                  rr[b], rr0[b], tau);
+        break;
+      }
       if (rr[b] <= tol) act[b] = 0; else ++nact;
     }
     if (st != NMG_OK || nact == 0 || tau == max_cycles) break;
@@ -2156,23 +2075,15 @@ nmg_status nmg_vcycles_host(nmg_hierarchy* h, int32_t nrhs, const double* y_host
   if (!y_host || !x_host || cycles < 0) return fail(NMG_ERR_INVALID_ARG, "bad arguments");
   if (h->slab) return fail(NMG_ERR_UNSUPPORTED, "nmg_vcycles_host: not available on a slab-sharded handle");
   cudaStream_t s = (cudaStream_t)stream;
-  const size_t cnt = (size_t)h->d.max_rhs * h->N[0];
-  if (!h->hy.p) { NMG_TRY(h->hy.alloc(cnt)); NMG_TRY(h->hx.alloc(cnt)); }
+  if (!h->hy.p || !h->s_h2d) return fail(NMG_ERR_UNSUPPORTED, "nmg_vcycles_host: handle has no host staging");
   const int64_t N0 = h->N[0];
-  if (!h->s_h2d) {
-    NMG_CUDA(cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking));
-    NMG_CUDA(cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking));
-    h->hev.resize(2 * 8 + 2);
-    for (auto& e : h->hev) NMG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  }
   cudaEvent_t ev_start = h->hev[16], ev_end = h->hev[17];
   NMG_CUDA(cudaEventRecord(ev_start, s));                 // staging buffers free after prior work on s
   NMG_CUDA(cudaStreamWaitEvent(h->s_h2d, ev_start, 0));
   NMG_CUDA(cudaStreamWaitEvent(h->s_d2h, ev_start, 0));
   const int K = (int)h->lanes.size() + 1;
   const int gr = h->d.dim == 1 ? 128 : 2;
-  const char* hl = std::getenv("NMG_HOST_LANES");
-  if (K > 1 && nrhs >= K * gr && !h->prof_on && s != nullptr && !(hl && std::string(hl) == "0")) {
+  if (K > 1 && nrhs >= K * gr && !h->prof_on && s != nullptr && h->tune.host_chunks == 0) {
     // Lane-pipelined (the RHS are independent): lane k's RHS are copied in on s_h2d,
     // its stream starts cycling as soon as they land (the lanes overlap on the GPU while later
     // lanes are still in flight over PCIe), and its x goes back on s_d2h when it finishes.
@@ -2198,9 +2109,9 @@ nmg_status nmg_vcycles_host(nmg_hierarchy* h, int32_t nrhs, const double* y_host
       const int64_t l0 = hk->launches;
       hk->lane_mult = mult;
       nmg_status st = NMG_OK;
-      // a lane's batch is below the lane threshold, so graph_cycle runs (and caches) it as one
-      // plain graph on the lane's own handle and stream
-      for (int c = 0; c < cycles && st == NMG_OK; ++c) st = graph_cycle(hk, cnt, yc, xc, sk);
+      // lane k runs its RHS on its own handle and stream only (no sub-lanes: lane 0's batch must
+      // not fork onto lanes 1..K-1, which are cycling their own RHS concurrently)
+      for (int c = 0; c < cycles && st == NMG_OK; ++c) st = graph_cycle(hk, cnt, yc, xc, sk, false);
       hk->lane_mult = 1;
       if (k > 0) h->launches += hk->launches - l0;
       NMG_TRY(st);
@@ -2222,7 +2133,7 @@ nmg_status nmg_vcycles_host(nmg_hierarchy* h, int32_t nrhs, const double* y_host
   // two chunks keep each chunk's kernels near full occupancy (measured: cfg 1 in 4 chunks of
   // 256 RHS runs at 64% of the batch efficiency); four only for very large batches
   int nch = nrhs < 256 ? 1 : ((int64_t)nrhs * N0 / 4 < ((int64_t)1 << 25) ? 2 : 4);
-  if (const char* ce = std::getenv("NMG_HOST_CHUNKS")) nch = std::max(1, std::min(8, std::min(nrhs, std::atoi(ce))));
+  if (h->tune.host_chunks > 0) nch = std::max(1, std::min(8, std::min(nrhs, (int)h->tune.host_chunks)));
   int off[9];
   for (int c = 0; c <= nch; ++c) off[c] = (int)((int64_t)nrhs * c / nch);
   for (int c = 0; c < nch; ++c) {
@@ -2237,7 +2148,7 @@ nmg_status nmg_vcycles_host(nmg_hierarchy* h, int32_t nrhs, const double* y_host
     double* xc = h->hx.p + off[c] * N0;
     NMG_CUDA(cudaStreamWaitEvent(s, h->hev[c], 0));
     for (int k = 0; k < cycles; ++k) NMG_TRY(graph_cycle(h, cnt, yc, xc, s));
-    if (relres_host)
+    if (relres_host && cycles > 0)
       NMG_CUDA(cudaMemcpyAsync(relres_host + off[c], h->relres.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, s));
     NMG_CUDA(cudaEventRecord(h->hev[8 + c], s));
     NMG_CUDA(cudaStreamWaitEvent(h->s_d2h, h->hev[8 + c], 0));

@@ -14,6 +14,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tcgen05.cuh"
 
 namespace nmg {
 namespace {
@@ -26,27 +27,6 @@ constexpr int WS_BYTES = OS * OBN * OBK;    // 28 KB
 constexpr int OSTAGE = XS_BYTES + WS_BYTES;
 constexpr int OZ_SMEM = ONSTAGE * OSTAGE + 256 + 1024;
 
-NMG_D uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
-NMG_D void mb_init(uint64_t* b, uint32_t c) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(c));
-}
-NMG_D void mb_expect(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes));
-}
-NMG_D void mb_wait(uint64_t* b, uint32_t ph) {
-  asm volatile(
-      "{\n.reg .pred P1;\nWAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@P1 bra DONE_%=;\nbra WAIT_%=;\nDONE_%=:\n}\n" ::"r"(su32(b)),
-      "r"(ph));
-}
-NMG_D void tma3d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(
-          su32(dst)),
-      "l"(m), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
-}
 // multicast to the CTAs of `mask` (same smem offsets, complete_tx on each CTA's barrier)
 NMG_D void tma3d_mc(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2, uint16_t mask) {
   asm volatile(
@@ -63,15 +43,6 @@ NMG_D uint32_t cluster_rank() {
   asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
   return r;
 }
-NMG_D uint64_t desc_sw64(uint32_t saddr) {
-  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)1 << 16;
-  d |= (uint64_t)(512 >> 4) << 32;
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)4 << 61;
-  return d;
-}
-// D s32, A/B int8 (signed), K-major, M = 128, N = 64 * nd (nd stacked W digits)
 NMG_D uint32_t idesc_i8(int nd) {
   return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)((OBN * nd) >> 3) << 17) | ((uint32_t)(OBM >> 4) << 24);
 }
@@ -343,24 +314,17 @@ void ozaki_split_rows(int M, int K, const double* X, int64_t ldx, int8_t* dig, i
 }
 
 void ozaki_resid(const CUtensorMap* mx, const CUtensorMap* mw, const OzakiArgs& a, cudaStream_t s) {
-  static bool attr0 = false, attr1 = false;
   const bool gen = a.tb_R || a.tb_S || a.tb_img || a.r32_img || a.wrow0;
   dim3 grid(a.N / OBN, ceil_div(a.M, OBM));
   if (gen) {
-    if (!attr1) {
-      cudaFuncSetAttribute(ozaki_resid_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM);
-      attr1 = true;
-    }
+    NMG_SMEM_OPTIN(ozaki_resid_kernel<true>, OZ_SMEM);
     OzakiArgs g = a;   // the general mapping needs every field set
     if (!g.tb_R) g.tb_R = g.tblock;
     if (!g.tb_S) g.tb_S = g.tblock;
     if (!g.tb_img) g.tb_img = (int64_t)g.tblock * g.tblock;
     ozaki_resid_kernel<true><<<grid, ONT, OZ_SMEM, s>>>(*mx, *mw, g);
   } else {
-    if (!attr0) {
-      cudaFuncSetAttribute(ozaki_resid_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM);
-      attr0 = true;
-    }
+    NMG_SMEM_OPTIN(ozaki_resid_kernel<false>, OZ_SMEM);
     ozaki_resid_kernel<false><<<grid, ONT, OZ_SMEM, s>>>(*mx, *mw, a);
   }
 }

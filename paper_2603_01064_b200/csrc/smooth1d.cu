@@ -267,17 +267,13 @@ size_t smooth1d_smem(int n) {
 
 void smooth1d(const Smooth1dArgs& a, cudaStream_t s) {
   const size_t smem = smooth1d_smem(a.n);
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaFuncSetAttribute(smooth1d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smooth1d_smem(8192));
-    attr = smooth1d_smem(8192);
-  }
+  NMG_SMEM_OPTIN(smooth1d_kernel, smooth1d_smem(8192));
   smooth1d_kernel<<<a.nrhs, NT, smem, s>>>(a);
 }
 
 void filter1d(int n, int nrhs, const float* in, float* out, const float2* tw, int tw_n, cudaStream_t s) {
   const size_t smem = (size_t)std::max(n, 4) * sizeof(float);
-  cudaFuncSetAttribute(filter1d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  NMG_SMEM_OPTIN(filter1d_kernel, 8192 * sizeof(float));
   filter1d_kernel<<<nrhs, NT, smem, s>>>(n, in, out, tw, tw_n);
 }
 

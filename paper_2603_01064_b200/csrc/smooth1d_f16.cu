@@ -35,6 +35,7 @@
 #include "common.cuh"
 #include "fft.cuh"
 #include "kernels.h"
+#include "tcgen05.cuh"
 
 namespace nmg {
 namespace {
@@ -53,21 +54,6 @@ constexpr int NSD = 4;                  // accumulator stages (TMEM, 32 columns 
 constexpr uint32_t IDESC32 = (1u << 4) | ((uint32_t)(32 >> 3) << 17) | ((uint32_t)(TP >> 4) << 24);
 constexpr uint32_t IDESC16 = (1u << 4) | ((uint32_t)(16 >> 3) << 17) | ((uint32_t)(TP >> 4) << 24);
 
-NMG_D uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
-NMG_D void mb_init(uint64_t* b, uint32_t c) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(c));
-}
-NMG_D void mb_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
-}
-NMG_D void mb_wait(uint64_t* b, uint32_t ph) {
-  asm volatile(
-      "{\n.reg .pred P1;\nWAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
-      "@P1 bra DONE_%=;\nbra WAIT_%=;\nDONE_%=:\n}\n" ::"r"(su32(b)),
-      "r"(ph), "r"(0x989680)
-      : "memory");
-}
 NMG_D bool elect_one() {
   uint32_t pred = 0;
   asm volatile(
@@ -77,38 +63,6 @@ NMG_D bool elect_one() {
       : "+r"(pred)
       : "r"(0xffffffffu));
   return pred != 0;
-}
-NMG_D uint64_t desc_ns(uint32_t saddr, uint32_t lbo) {
-  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-  d |= (uint64_t)(128 >> 4) << 32;
-  d |= (uint64_t)1 << 46;
-  return d;
-}
-NMG_D void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc));
-}
-NMG_D void mma_commit(uint64_t* b) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(b))
-               : "memory");
-}
-NMG_D void tld16(uint32_t taddr, uint32_t* r) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-}
-// wait::ld with the destination registers threaded through
-NMG_D void tld_wait16(uint32_t* r) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
-               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
-                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
-               :
-               : "memory");
 }
 NMG_D void split8(const float* v, uint4& hi, uint4& lo) {
   uint32_t h[4], l[4];
@@ -624,11 +578,7 @@ size_t smem_of(int n) {
 size_t smooth1d_f16_smem(int n) { return smem_of(n); }
 
 void smooth1d_f16(const Smooth1dArgs& a, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(smooth1d_f16_kernel<kNSA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_of(8192));
-    attr = true;
-  }
+  NMG_SMEM_OPTIN(smooth1d_f16_kernel<kNSA>, smem_of(8192));
   smooth1d_f16_kernel<kNSA><<<a.nrhs, NT, smem_of(a.n), s>>>(a);
 }
 

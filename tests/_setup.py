@@ -24,10 +24,10 @@ def oracle_hierarchy(cfg, factors, weights, level_filter=True):
     return H
 
 
-def gpu_hierarchy(cfg, factors, weights, max_rhs, level_filter=True):
+def gpu_hierarchy(cfg, factors, weights, max_rhs, level_filter=True, **kw):
     import paper_2603_01064_b200 as nmg
     h = nmg.Hierarchy(cfg.dim, cfg.n, cfg.levels, cfg.alpha, factors, nu1=cfg.nu1, nu2=cfg.nu2,
-                      level_filter=level_filter, max_rhs=max_rhs)
+                      level_filter=level_filter, max_rhs=max_rhs, **kw)
     for l, w in enumerate(weights):
         h.load_weights(l + 1, ni.cnn_arch(cfg), w)
     return h

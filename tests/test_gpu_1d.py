@@ -351,19 +351,18 @@ def test_host_entry_chunked_pipeline():
     assert np.array_equal(xh, xd.cpu().numpy())
 
 
-@pytest.mark.parametrize("host_lanes", ["1", "0"])
-def test_host_entry_lanes(monkeypatch, host_lanes):
+@pytest.mark.parametrize("host_chunks", [0, 2])
+def test_host_entry_lanes(host_chunks):
     """On a handle with RHS lanes (max_rhs 1024: four lanes of 256) nmg_vcycles_host either
     pipelines the copies per lane (default: a lane cycles as soon as its RHS land) or per chunk
-    (NMG_HOST_LANES=0, lanes inside each chunk); x is bitwise the device-entry result and relres
+    (tuning.host_chunks, lanes inside each chunk); x is bitwise the device-entry result and relres
     (the relative residual before the last cycle, every lane's slice) matches nmg_residual."""
-    monkeypatch.delenv("NMG_LANES", raising=False)
-    monkeypatch.setenv("NMG_HOST_LANES", host_lanes)
     cfg = ni.CONFIGS[1].replace(n=1024, levels=4, nrhs=1024)
     f = ni.operator_factors(cfg)
     W = ni.weights_seed(cfg)
     y, _ = ni.make_rhs(cfg, f, cfg.alpha, nrhs=1024)
-    h = nmg.Hierarchy(1, cfg.n, cfg.levels, cfg.alpha, f, nu1=1, nu2=1, max_rhs=1024)
+    h = nmg.Hierarchy(1, cfg.n, cfg.levels, cfg.alpha, f, nu1=1, nu2=1, max_rhs=1024,
+                      tuning={"host_chunks": host_chunks})
     for l, w in enumerate(W):
         h.load_weights(l + 1, ni.cnn_arch(cfg), w)
     yd = torch.tensor(y, dtype=torch.float64, device=DEV)
@@ -383,7 +382,7 @@ def test_host_entry_lanes(monkeypatch, host_lanes):
     h.close()
 
 
-def test_rhs_lanes_bitwise(monkeypatch):
+def test_rhs_lanes_bitwise():
     """Batches >= 256 RHS on a handle with max_rhs >= 512 run as two RHS lanes on forked
     streams (nmg_vcycle); the NMGF cycle is per-RHS, so the result is bitwise the one-lane result."""
     cfg = ni.CONFIGS[1].replace(n=1024, levels=4, nrhs=512)
@@ -391,12 +390,9 @@ def test_rhs_lanes_bitwise(monkeypatch):
     W = ni.weights_seed(cfg)
     y, _ = ni.make_rhs(cfg, f, cfg.alpha, nrhs=512)
     outs = []
-    for lanes in ("1", None):
-        if lanes:
-            monkeypatch.setenv("NMG_LANES", lanes)
-        else:
-            monkeypatch.delenv("NMG_LANES", raising=False)
-        h = nmg.Hierarchy(1, cfg.n, cfg.levels, cfg.alpha, f, nu1=1, nu2=1, max_rhs=512)
+    for lanes in (1, 0):
+        h = nmg.Hierarchy(1, cfg.n, cfg.levels, cfg.alpha, f, nu1=1, nu2=1, max_rhs=512,
+                          tuning={"lanes": lanes})
         for l, w in enumerate(W):
             h.load_weights(l + 1, ni.cnn_arch(cfg), w)
         yd = torch.tensor(y, dtype=torch.float64, device=DEV)

@@ -241,7 +241,7 @@ def test_outer_residual_2d_ozaki(cfg_id, n):
 
 
 @pytest.mark.parametrize("nrhs", [37, 64])
-def test_rhs_lanes_bitwise_2d(monkeypatch, nrhs):
+def test_rhs_lanes_bitwise_2d(nrhs):
     """2D handles with max_rhs * n^2 <= 2^26 cycle their batch as two RHS lanes on forked streams
     (lane boundaries on even RHS, so the level filter's RHS pairs are the same); the result is
     bitwise the one-lane result, through the device entry and the lane-pipelined host entry."""
@@ -250,13 +250,8 @@ def test_rhs_lanes_bitwise_2d(monkeypatch, nrhs):
     W = weights_for(cfg, "seed")
     y, _ = ni.make_rhs(cfg, f, cfg.alpha, nrhs=nrhs)
     outs = []
-    for lanes in ("1", None):
-        if lanes:
-            monkeypatch.setenv("NMG_LANES", lanes)
-        else:
-            monkeypatch.delenv("NMG_LANES", raising=False)
-        monkeypatch.delenv("NMG_LANES2D", raising=False)
-        h = gpu_hierarchy(cfg, f, W, max_rhs=64)
+    for lanes in (1, 0):
+        h = gpu_hierarchy(cfg, f, W, max_rhs=64, tuning={"lanes": lanes})
         yd = T(y, torch.float64)
         xd = torch.zeros_like(yd)
         st = torch.cuda.Stream()

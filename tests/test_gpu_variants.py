@@ -92,29 +92,23 @@ def test_paper_form_operator_2d():
     assert ok, err
 
 
-@pytest.mark.parametrize("env", ["NMG_GEMM=simt", "NMG_CONV=ffma", "NMG_CONV=tf32", "NMG_SMOOTH1D=tc",
-                                 "NMG_SMOOTH1D=ffma", "NMG_FP64=dmma", "NMG_GRAPH=0",
-                                 "NMG_KRON=0"])
-def test_fallback_kernels_match(env, tmp_path):
-    """The alternative kernels (SIMT GEMM, FFMA / 3xTF32 2D CNN, 3xTF32 / FFMA 1D smoother,
-    DMMA fp64 residual, no CUDA graph, separate split/GEMM/stencil 2D apply) agree with the oracle too; run in a subprocess so the
-    env switch applies."""
-    code = (
-        "import sys; sys.path.insert(0, '.');"
-        "import numpy as np, torch, nmg_inputs as ni;"
-        "from tests._setup import *; from oracle import nmg_oracle as O;"
-        "cfg = (ni.CONFIGS[0].replace(nrhs=2) if ('SMOOTH1D' in %r or 'FP64' in %r) else ni.CONFIGS[2].replace(n=64, levels=3, nrhs=2));"
-        "f = ni.operator_factors(cfg); W = weights_for(cfg, 'seed');"
-        "H = oracle_hierarchy(cfg, f, W); h = gpu_hierarchy(cfg, f, W, max_rhs=2);"
-        "y, _ = ni.make_rhs(cfg, f, cfg.alpha);"
-        "yd = torch.tensor(y, dtype=torch.float64, device='cuda'); xd = torch.zeros_like(yd);"
-        "rep = h.solve(yd, xd, tol=1e-300, max_cycles=3);"
-        "orc = O.solve(H, y, tol=1e-300, max_cycles=3, freeze=False);"
-        "ok, err = history_close(rep['history'], orc.history); print('ERR', err); assert ok"
-    )
-    code = code % (env, env)
-    k, v = env.split("=")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, k: v},
-                       capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout + r.stderr
+@pytest.mark.parametrize("knob", ["simt_gemm", "ffma_cnn", "fp64_dmma", "no_graphs", "no_kron", "coarse_subst"])
+@pytest.mark.parametrize("dim", [1, 2])
+def test_fallback_kernels_match(knob, dim):
+    """The alternative kernels selected by nmg_tuning (SIMT GEMM, FFMA CNNs, DMMA fp64 residual,
+    eager launches, unfused Kronecker pair, Cholesky substitution at the coarsest level) agree
+    with the oracle too."""
+    if knob == "no_kron" and dim == 1:
+        pytest.skip("2D-only knob")
+    cfg = ni.CONFIGS[0].replace(nrhs=2) if dim == 1 else ni.CONFIGS[2].replace(n=64, levels=3, nrhs=2)
+    f = ni.operator_factors(cfg)
+    W = weights_for(cfg, "seed")
+    H = oracle_hierarchy(cfg, f, W)
+    h = gpu_hierarchy(cfg, f, W, max_rhs=2, tuning={knob: 1})
+    y, _ = ni.make_rhs(cfg, f, cfg.alpha)
+    yd = torch.tensor(y, dtype=torch.float64, device="cuda")
+    xd = torch.zeros_like(yd)
+    rep = h.solve(yd, xd, tol=1e-300, max_cycles=3)
+    orc = O.solve(H, y, tol=1e-300, max_cycles=3, freeze=False)
+    ok, err = history_close(rep["history"], orc.history)
+    assert ok, err
