@@ -1,23 +1,26 @@
 #!/usr/bin/env python
 """Benchmark of the batched NMGF solve phase (arxiv 2603.01064) on B200.
 
-Workload (BASELINE.json configs[1], the metric's configuration): 1D, n = 4096,
-sigma = 0.02, alpha = 1e-3 (default; --alpha), 6 levels (4096 -> 128),
-1024 RHS per GPU, CNN 3x16 k5 smoothers (W_seed), nu1 = nu2 = 1, level filter on.
+Default workload (--config 3): BASELINE.json configs[3], the largest configuration that fits
+one GPU -- 2D 512 x 512, sigma = 0.02, alpha = 1e-3 (--alpha 1e-4 for the other sweep point),
+6 levels (512^2 -> 16^2), 2048 RHS sharded over the ranks, CNN 4 x 48 3x3 smoothers (W_seed),
+nu1 = nu2 = 1, level filter on.  --config 0..4 selects the other BASELINE rows.
 
 One "step" = one pass of the whole hot path over the batch: fp64 outer residual and
 convergence test, one NMGF V-cycle (all levels), fp64 update.
-  value = RHS * V-cycles / s, whole job (all ranks), device-timed (CUDA events, max
-          over ranks).  Weak scaling: every rank solves its own 1024-RHS shard.
-  e2e   = the same metric through the C ABI host-buffer entry nmg_vcycles_host
-          (H2D of y and x, one cycle, D2H of x inside the timed region).
-  solve = RHS solved to 1e-6 relative residual per second with the converging
-          W_lin stand-in weights at alpha = 1e-2.
-Inputs are larger than L2 (fp64 A 128 MiB + fp32 level operators 128 MiB streamed
-per step), so no explicit L2 flush is needed between steps.
+  value = RHS * V-cycles / s, whole job (all ranks), device-timed (CUDA events, max over
+          ranks).  Configs 1-4 split the configuration's own RHS batch over the ranks
+          (strong scaling); config 0 runs replicas; config 4 row-shards its
+          single operator (slab mode) over NCCL.
+  e2e   = the same metric through the C ABI host-buffer entry nmg_vcycles_host (H2D of y
+          and x from pinned host memory, one cycle, D2H of x inside the timed region),
+          checked afterwards against the device entry.
+  solve = RHS solved to 1e-6 relative residual per second with the converging W_lin
+          stand-in weights (1D configs only).
+Inputs are larger than L2 (cfg 3: 4 GiB fp64 y and x), so no explicit L2 flush is needed.
 
---impl reference times the fp64 CPU oracle (oracle/) on a bounded sample of the
-same workload on this host's cores.
+--impl reference times the fp64 CPU oracle (oracle/) on a bounded sample of the same
+workload on this host's cores (the reference arm: /root/reference holds only the paper).
 """
 from __future__ import annotations
 
@@ -154,6 +157,7 @@ def oracle_rate(cfg, factors, weights, y, nrhs, cycles):
 
 
 def host_threads():
+    """Threads the oracle's numpy/BLAS actually uses on this host."""
     try:
         from threadpoolctl import threadpool_info
         th = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"]
@@ -162,15 +166,33 @@ def host_threads():
         return os.cpu_count()
 
 
+def host_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+def metric_name(cfg):
+    """Identical on both arms (the driver divides the two values)."""
+    return f"RHS*V-cycles/s ({cfg.name})"
+
+
 # ------------------------------------------------------------------ main
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=None)
-    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4])
+    ap.add_argument("--config", type=int, default=3, choices=[0, 1, 2, 3, 4])
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--alpha", type=float, default=1e-3)
+    ap.add_argument("--alpha", type=float, default=None, help="override the config's alpha (sweep points)")
     ap.add_argument("--nrhs", type=int, default=None)
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -187,18 +209,16 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     cid = args.config
     cfg = ni.CONFIGS[cid]
-    if cid == 1 or args.alpha != 1e-3:
-        cfg = cfg.replace(alpha=args.alpha if cid == 1 else cfg.alpha)
+    if args.alpha is not None:
+        cfg = cfg.replace(alpha=args.alpha)
     if args.nrhs:
         cfg = cfg.replace(nrhs=args.nrhs)
     if args.steps is None:
-        args.steps = {0: 5000, 1: 400, 2: 60, 3: 3, 4: 30}[cid]   # >= ~0.5 s timed (clock samples)
-    if cid == 3:
-        args.no_e2e = True            # 2 x 4 GiB pinned host buffers per rank: skipped
+        args.steps = {0: 5000, 1: 400, 2: 60, 3: 5, 4: 30}[cid]   # >= ~0.5 s timed (clock samples)
     B = cfg.nrhs
     pool = cfg.dim == 2 and B > 8     # 2D: 8 seeded RHS tiled to the batch (throughput is value-independent)
     workload = (f"{cfg.name}_{cfg.dim}d_n{cfg.n}_L{cfg.levels}_rhs{B}"
-                f"{'_total' if cid == 4 else '_per_gpu'}_alpha{cfg.alpha:g}_C{cfg.channels}_Wseed")
+                f"{'_per_gpu' if cid == 0 else '_total'}_alpha{cfg.alpha:g}_C{cfg.channels}_Wseed")
 
     def make_y(nrhs, start):
         if not pool:
@@ -211,26 +231,26 @@ def main():
             return
         factors = ni.operator_factors(cfg)
         W = ni.weights_seed(cfg)
+        # bounded sample per step (every --steps / --warmup step runs): 1D 16 RHS x 1 cycle,
+        # 2D 1 RHS x 1 cycle (cfg 3: ~3 s per step on 16 host threads)
         ns = 16 if cfg.dim == 1 else 1
         y, _ = ni.make_rhs(cfg, factors, cfg.alpha, nrhs=ns)
-        rates, secs = [], 0.0
-        for _ in range(min(args.warmup, 1)):
-            oracle_rate(cfg, factors, W, y, min(ns, 4), 1)
-        ref_steps = min(args.steps, 200) if cfg.dim == 1 else min(args.steps, 3)
-        for _ in range(ref_steps):
-            r, dt = oracle_rate(cfg, factors, W, y, ns, 1)
-            rates.append(r)
+        secs = 0.0
+        for _ in range(args.warmup):
+            oracle_rate(cfg, factors, W, y, ns, 1)
+        for _ in range(args.steps):
+            _, dt = oracle_rate(cfg, factors, W, y, ns, 1)
             secs += dt
-        args.steps = ref_steps
         v = args.steps * ns / secs
-        line = {"impl": "reference", "metric": f"RHS*V-cycles/s ({cfg.name}, fp64 CPU oracle)", "value": v,
+        sample = f"{ns} RHS x 1 cycle per step of the {cfg.name} workload"
+        line = {"impl": "reference", "metric": metric_name(cfg), "value": v,
                 "unit": "RHS*cycles/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
-                "scaling": "strong" if cid == 4 else "weak",
+                "scaling": "weak" if cid == 0 else "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": workload, "sample": f"{ns} RHS x 1 cycle per step"},
+                "config": {"workload": workload, "sample": sample},
                 "cpu_baseline": {"value": v, "unit": "RHS*cycles/s", "cores": host_threads(), "kind": "oracle",
-                                 "sample": f"{ns} RHS x 1 cycle per step of the {cfg.name} workload"},
+                                 "sample": sample, **host_info()},
                 "e2e": {"value": v, "unit": "RHS*cycles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
         return
@@ -252,10 +272,10 @@ def main():
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
 
-    # configs 0-3: weak scaling (every rank its own B-RHS shard of the seeded stream); config 4
-    # (one operator, 32 RHS): strong scaling, the 32 independent RHS split over the ranks
-    # (RHS sharding needs no exchange step)
-    strong = cid == 4
+    # configs 1-4: strong scaling -- the configuration's own RHS batch is split over the ranks
+    # (RHS sharding needs no exchange step; config 4 at N > 1 row-shards its single
+    # operator instead).  Config 0 (8 RHS, latency-bound) runs one replica per rank (weak).
+    strong = cid != 0
     # config 4 over several GPUs: the single 1024^2 operator is row-sharded (slab mode, one
     # all-gather of the Kronecker intermediate per apply, all-to-all transposes in the level
     # filter); every rank holds its slab of all 32 RHS
@@ -277,6 +297,8 @@ def main():
         global_B = world * B
     factors = ni.operator_factors(cfg)
     W = ni.weights_seed(cfg)
+    if B == 0:
+        raise SystemExit(f"rank {rank}: no RHS left for this rank ({cfg.nrhs} RHS over {world} ranks)")
     h = nmg.Hierarchy(cfg.dim, cfg.n, cfg.levels, cfg.alpha, factors, nu1=cfg.nu1, nu2=cfg.nu2, max_rhs=B,
                       device=local, comm=comm)
     for l, w in enumerate(W):
@@ -352,14 +374,18 @@ def main():
                 "bound": "tensor", "unit": "TFLOP/s",
                 "peak_note": "FP16 dense tensor = measured bf16 dense, / 3 products per fp32-accurate MAC; "
                              "CNN FLOPs (2880/point) only"}
-    else:
+    elif dom == "smooth":
         peak = f16x3_peak
         achieved = counts["smooth"] / (step_ms * 1e-3) / 1e12
-        roof = {"kernel": "2D smoother: conv_strip_kernel (FP16x3 tcgen05, n % 128 == 0 levels), "
-                          "conv3x3_tc / cnn2d (smaller levels), FFT filter",
+        roof = {"kernel": "conv_strip_kernel<C,1> + <C,0> (2D CNN layers 1-2 / 3-4, FP16x3 tcgen05), all launches "
+                          "of a step",
                 "bound": "tensor", "unit": "TFLOP/s",
                 "peak_note": "FP16 dense tensor = measured bf16 dense, / 3 products per fp32-accurate MAC; "
-                             "CNN FLOPs only"}
+                             "CNN FLOPs (2 (9C + 18C^2 + 9C) per pixel) only"}
+    else:
+        peak = pk["hbm_gbs"] / 1e3
+        achieved = (counts.get(dom + "_bytes") or float("nan")) / (step_ms * 1e-3) / 1e12
+        roof = {"kernel": dom, "bound": "hbm", "unit": "TB/s"}
     roof.update({"achieved": achieved, "peak": peak, "frac": achieved / peak, "traffic": traffic,
                  "traffic_note": (f"ncu dram__bytes_read+write of the {dom} class per step (cfg{cid}), profiles/traffic.json"
                                   if traffic else None),
@@ -396,8 +422,20 @@ def main():
         f1.record(stream)
         torch.cuda.synchronize(dev)
         ems = max_over_ranks(f0.elapsed_time(f1))
+        # correctness check of the path just timed: one host-entry cycle from x = 0 against one
+        # device-entry cycle from x = 0 (same kernels; RHS chunking changes no per-RHS arithmetic)
+        xh.zero_()
+        host_step()
+        torch.cuda.synchronize(dev)
+        xd = torch.zeros_like(y)
+        h.vcycle(y, xd, stream)
+        torch.cuda.synchronize(dev)
+        xdh = xd.cpu()
+        diff = float((xh - xdh).abs().max() / xdh.abs().max().clamp_min(1e-300))
         e2e = {"value": global_B * args.steps / (ems / 1e3), "unit": "RHS*cycles/s",
-               "h2d_bytes_per_step": 2 * 8 * B * cfg.N, "d2h_bytes_per_step": 8 * B * cfg.N}
+               "h2d_bytes_per_step": 2 * 8 * B * cfg.N, "d2h_bytes_per_step": 8 * B * cfg.N,
+               "check_vs_device_entry_max_rel_diff": diff}
+        del yh, xh, xd
 
     # ---- RHS solved to 1e-6 / s with converging stand-in weights (alpha = 1e-2)
     solve = None
@@ -428,20 +466,22 @@ def main():
         nr, nc = {0: (8, 200), 1: (128, 8), 2: (4, 2), 3: (1, 1), 4: (1, 1)}[cid]
         rate, dt = oracle_rate(cfg, factors, W, y_np, nr, nc)
         cpu = {"value": rate, "unit": "RHS*cycles/s", "cores": host_threads(), "kind": "oracle",
-               "sample": f"{nr} RHS x {nc} cycles of the same workload ({dt:.1f} s)"}
+               "sample": f"{nr} RHS x {nc} cycles of the same workload ({dt:.1f} s)", **host_info()}
 
     if rank == 0:
-        line = {"metric": f"RHS*V-cycles/s ({cfg.name}: fp64 residual + NMGF V-cycle + update per step)",
+        line = {"metric": metric_name(cfg),
                 "value": value, "unit": "RHS*cycles/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "strong" if strong else "weak", "vs_baseline": None,
-                "dtype": "f64 outer residual / fp32-accurate inner (3xTF32 GEMMs, FP16x3 CNN)",
+                "dtype": ("f64 outer residual (Ozaki int8 tcgen05) + fp32-accurate inner cycle (FP16x3 tcgen05 "
+                          + ("CNN and operator applies)" if cfg.dim == 1 else "CNN, 3xTF32 tcgen05 Kronecker applies)")),
                 "data": "synthetic (seeded RHS; W_seed Kaiming-uniform weights)",
                 "config": {"workload": workload, "global_batch": global_B, "n": cfg.n, "levels": cfg.levels,
                            "rhs": "8-RHS seeded pool tiled to the batch" if pool else "seeded, distinct",
                            "alpha": cfg.alpha, "nu1": cfg.nu1, "nu2": cfg.nu2,
                            "parallelism": (f"operator slab-shard x{world} (NCCL all-gather per apply)" if slab else
-                                           f"rhs-shard x{world}" + (" (strong: 32 RHS split)" if strong else "")),
+                                           f"rhs-shard x{world}" + (f" (strong: {cfg.nrhs} RHS split)" if strong
+                                                                    else " (replicas)")),
                            "l2": ("working set fits L2 (latency-bound config, no flush)" if cid == 0
                                   else "inputs larger than L2 (no flush)")},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "solve": solve,

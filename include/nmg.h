@@ -201,11 +201,12 @@ nmg_status nmg_debug_level_op(nmg_hierarchy *h, int32_t level, int32_t op, int32
 enum {
   NMG_K_GEMM64 = 0,    /* fp64 outer residual GEMM (+ norm partials)           */
   NMG_K_GEMM32 = 1,    /* fp32-accurate inner operator applies                  */
-  NMG_K_SMOOTH = 2,    /* fused norm + CNN + level filter + update              */
+  NMG_K_SMOOTH = 2,    /* 1D: fused norm + CNN + level filter + update; 2D: CNN  */
   NMG_K_TRANSFER = 3,  /* restriction / prolongation                            */
   NMG_K_COARSE = 4,    /* coarsest Cholesky solve                               */
   NMG_K_MISC = 5,      /* relres, update, norms, conversions                    */
-  NMG_K_COUNT = 6
+  NMG_K_FILTER = 6,    /* 2D: smoother norms, strip combine + level-filter FFTs */
+  NMG_K_COUNT = 7
 };
 nmg_status nmg_profile(nmg_hierarchy *h, int32_t enable);
 nmg_status nmg_profile_query(nmg_hierarchy *h, int32_t kclass, double *total_ms, int64_t *launches);

@@ -26,7 +26,7 @@ EXPORTS = ["nmg_create_hierarchy", "nmg_load_smoother_weights", "nmg_vcycle", "n
            "nmg_comm_nccl_unique_id", "nmg_comm_create_nccl", "nmg_comm_create_emulated", "nmg_comm_destroy",
            "nmg_create_hierarchy_slab"]
 
-KERNEL_CLASSES = ["gemm64", "gemm32", "smooth", "transfer", "coarse", "misc"]
+KERNEL_CLASSES = ["gemm64", "gemm32", "smooth", "transfer", "coarse", "misc", "filter"]
 
 
 class NmgError(RuntimeError):

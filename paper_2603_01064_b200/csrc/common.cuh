@@ -35,11 +35,13 @@ NMG_D double block_sum_f64(double v, double* scratch /* >= 32 doubles */) {
   return t;
 }
 
-// 2D level-filter input, paired layout: right-hand sides 2p and 2p + 1 are the real and the
-// imaginary part of complex image p (F' is a real symmetric operator, so one complex 2D FFT
-// filters both, see filter2d).  N = n * n pixels per image.
-NMG_D void zput(float2* Z, int64_t N, int b, int64_t pix, float v) {
-  reinterpret_cast<float*>(Z)[((int64_t)(b >> 1) * N + pix) * 2 + (b & 1)] = v;
+// 2D level-filter input, per-RHS packing: rows 2r and 2r + 1 of RHS b's image (`rows` x n real
+// values, rows even) are the real and the imaginary part of complex row r of its spectrum
+// buffer Z_b = [rows / 2][n] complex (one real 2D DFT done as n/2 complex row FFTs plus a
+// Hermitian unmixing in the column pass, see level2d.cu).  Each RHS keeps its own buffer, so
+// right-hand sides never share a transform (per-RHS independence, SURVEY pin P14).
+NMG_D void zput(float2* Z, int rows, int n, int b, int y, int x, float v) {
+  reinterpret_cast<float*>(Z)[(int64_t)b * rows * n + (int64_t)(y >> 1) * 2 * n + 2 * x + (y & 1)] = v;
 }
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is a per-DEVICE property: set it once per

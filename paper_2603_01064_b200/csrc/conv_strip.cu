@@ -624,9 +624,8 @@ __global__ void strip_combine_kernel(int n, int nrhs, const float4* __restrict__
     if (x > 0) acc += __ldg(&Q[idx - 1].x);
     if (x < n - 1) acc += __ldg(&Q[idx + 1].z);
   }
-  // the filter path takes N(u) unscaled (O(1) for every RHS, so two paired RHS of very
-  // different ||b|| do not pollute each other); filter2d multiplies by s after F'
-  if (Z) zput(Z, (int64_t)(hg - 2 * hh) * n, zb0 + b, (int64_t)(row - hh) * n + x, acc);
+  // the filter path takes N(u) unscaled; filter2d multiplies by s after F'
+  if (Z) zput(Z, hg - 2 * hh, n, zb0 + b, row - hh, x, acc);
   else {
     const float hv = acc * (float)s;
     xo[idx] = accumulate ? xo[idx] + hv : hv;

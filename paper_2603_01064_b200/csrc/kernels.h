@@ -209,28 +209,27 @@ void prolong_add2d(int nrhs, int n_c, const float* c, float* f, cudaStream_t s);
 void qstencil(int nrhs, int n, int hb, float alpha, const float* Q, const float* X, const float* C, float* D,
               cudaStream_t s);
 void norms_f32(int nrhs, int64_t N, const float* x, double* part, int chunks, double* out, cudaStream_t s);
-// level filter on the paired layout written by zput (common.cuh); filter2d_prepare zeroes the
-// imaginary partner of the last image when nrhs is odd (call before the writers)
+// level filter hat F'_l on the per-RHS layout written by zput (common.cuh): Z_b = [n/2][n] complex.
 // norms (may be null): per-RHS ||b||; the writers store N(u) and x gets ||b|| F'(N(u))
 void filter2d(int nrhs, int n, float2* Z, const float2* tw, int tw_n, float* x, bool accumulate, cudaStream_t s,
               const double* norms, bool rows_done = false);
-// strip_combine for RHS pairs fused with filter2d's forward row FFTs: Z rows of the chunk's pairs
-// (pairs zb0 / 2 ..) hold the row-transformed N(u) (0 where ||b|| = 0); zb0 and nrhs even
-// unless the chunk ends the batch
+// strip_combine fused with filter2d's forward row FFTs: Z_b (b = zb0 ..) of the chunk's RHS hold
+// the row-transformed N(u) (0 where ||b|| = 0)
 void combine_rows_fft(int n, int nrhs, const float* q, const double* norms, const float* b3, float2* Z, int zb0,
                       const float2* tw, int tw_n, cudaStream_t s);
-void filter2d_prepare(int nrhs, int n, float2* Z, cudaStream_t s, int rows = 0);
 // per-RHS sum of squares (no sqrt) of N values at x + b img + off
 void sumsq_f32(int nrhs, int64_t N, const float* x, int64_t img, int64_t off, double* part, int chunks, double* out,
                cudaStream_t s);
-// slab-sharded level filter (level2d.cu; steps in the comment there)
-void filter2d_slab_rows(int n, int npair, int R, float2* Zs, const float2* tw, int tw_n, cudaStream_t s);
-void filter2d_slab_pack(int n, int npair, int R, int W, float2* Zs, float2* buf, bool unpack, cudaStream_t s);
-void filter2d_slab_cols(int n, int npair, int R, int W, int rank, float2* buf, const float2* tw, int tw_n,
+// slab-sharded level filter (level2d.cu; steps in the comment there): Zs [nrhs][R/2][n];
+// all-to-all chunks of filter2d_slab_chunk(n, W) complex slots per (RHS, local complex row)
+int filter2d_slab_chunk(int n, int W);
+void filter2d_slab_rows(int n, int nrhs, int R, float2* Zs, const float2* tw, int tw_n, cudaStream_t s);
+void filter2d_slab_pack(int n, int nrhs, int R, int W, float2* Zs, float2* buf, bool unpack, cudaStream_t s);
+void filter2d_slab_cols(int n, int nrhs, int R, int W, int rank, float2* buf, const float2* tw, int tw_n,
                         cudaStream_t s);
 void filter2d_slab_inverse(int n, int nrhs, int R, float2* Zs, const float2* tw, int tw_n, float* x, int64_t ximg,
                            int64_t xoff, bool accumulate, const double* norms, cudaStream_t s);
-void real_to_complex(int nrhs, int64_t N, const float* x, float2* Z, cudaStream_t s);
+void real_to_complex(int nrhs, int n, const float* x, float2* Z, cudaStream_t s);
 
 // ---- 2D CNN, FP16x3 tcgen05 column-strip kernels (conv_strip.cu), n % 128 == 0, C = 32/48 --
 // Layers 1+2 (strip_l12): b -> a2 (scaled f16 hi/lo, [b][y][x][C]); layers 3+4 (strip_l34,

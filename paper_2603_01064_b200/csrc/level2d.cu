@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(256, 1) cnn2d_kernel(Cnn2dArgs a) {
       for (int i = tid; i < CT * CT; i += 256) {
         const int y = ty0 + i / CT, x = tx0 + i % CT;
         if (y < n && x < n) {
-          if (a.Z) zput(a.Z, (int64_t)n * n, b, (int64_t)y * n + x, 0.f);
+          if (a.Z) zput(a.Z, n, n, b, y, x, 0.f);
           else a.x[((int64_t)b * n + y) * n + x] = 0.f;
         }
       }
@@ -318,19 +318,31 @@ __global__ void __launch_bounds__(256, 1) cnn2d_kernel(Cnn2dArgs a) {
     if (gy < n && gx < n) {
       const float hv = acc * (float)s;
       const int64_t off = ((int64_t)b * n + gy) * n + gx;
-      if (a.Z) zput(a.Z, (int64_t)n * n, b, (int64_t)gy * n + gx, acc);   // N(u): scaled by s after F'
+      if (a.Z) zput(a.Z, n, n, b, gy, gx, acc);   // N(u): scaled by s after F'
       else a.x[off] = a.accumulate ? a.x[off] + hv : hv;
     }
   }
 }
 
 // ------------------------------------------------------------------ 2D FFT filter passes
-// rows: R rows of length n per CTA (R*n <= 4096 complex in smem), in place in Z
-// inverse: complex row Rr = p * rows + r of pair p writes x at b * ximg + xoff + r * n + col
-// (rows = n, ximg = n n, xoff = 0 for whole images; slab mode: the rank's R rows of a halo'd slab)
+// hat F'_l(h) = Re(IDFT2(M' (.) DFT2(h))) of each REAL image h (rows x n) on its own.
+// Rows 2r and 2r + 1 travel as one complex row z_r = h_2r + i h_2r+1 (zput, common.cuh):
+//   1. forward row FFTs of the rows/2 complex rows (natural-order spectra Z_r[k1]);
+//   2. column pass per frequency pair (k1, n - k1), k1 = 0 .. n/2: unmix the two real rows'
+//      spectra  H_2r[k1] = (Z_r[k1] + conj Z_r[n-k1]) / 2,  H_2r+1[k1] = (Z_r[k1] - conj Z_r[n-k1]) / 2i
+//      (Hermitian symmetry of real rows), FFT along i2, mask M'(k1, k2), inverse FFT along i2,
+//      and re-pack  W_r[k1] = Y_2r[k1] + i Y_2r+1[k1],  W_r[n-k1] = conj Y_2r[k1] + i conj Y_2r+1[k1]
+//      (the filtered image is real, so Y[n-k1] = conj Y[k1]);
+//   3. inverse row FFTs of W_r give y_2r + i y_2r+1 -> scale 1/n^2 (and ||b||) -> x.
+// The work equals one complex 2D FFT per RHS PAIR, but no two right-hand sides share a buffer.
+
+// rows: R complex rows of length n per CTA (R n <= 4096 complex in smem), in place in Z.
+// forward: natural in, natural out (the DIF result is read back through bitrev).
+// inverse: natural in (loaded bit-reversed for the DIT pass); complex row Rr = b rpi + r of
+// RHS b writes real rows 2r and 2r + 1 of x at b ximg + xoff + (2r) n + col (rpi = rows / 2).
 __global__ void __launch_bounds__(256) fft_rows_kernel(int n, int64_t nrows, float2* __restrict__ Z,
                                                        const float2* __restrict__ tw, int tw_n, int inverse,
-                                                       float* __restrict__ x, int accumulate, float scale, int nrhs,
+                                                       float* __restrict__ x, int accumulate, float scale,
                                                        const double* __restrict__ norms, int rpi, int64_t ximg,
                                                        int64_t xoff) {
   extern __shared__ __align__(16) float2 cb[];
@@ -338,57 +350,59 @@ __global__ void __launch_bounds__(256) fft_rows_kernel(int n, int64_t nrows, flo
   const int64_t r0 = (int64_t)blockIdx.x * R;
   const int rows = (int)min((int64_t)R, nrows - r0);
   const int tot = rows * n;
-  for (int i = threadIdx.x; i < tot; i += 256) cb[i] = Z[r0 * n + i];
-  __syncthreads();
-  // butterflies over all rows at once (fused radix-8 passes, fft.cuh)
+  const int log2n = 31 - __clz(n);
   if (!inverse) {
+    for (int i = threadIdx.x; i < tot; i += 256) cb[i] = Z[r0 * n + i];
+    __syncthreads();
     fft_dif_forward_batch(cb, n, rows, n, 1, tw, tw_n, threadIdx.x, 256);
-    for (int i = threadIdx.x; i < tot; i += 256) Z[r0 * n + i] = cb[i];
-  } else {
-    fft_dit_inverse_batch(cb, n, rows, n, 1, tw, tw_n, threadIdx.x, 256);
-    // complex image p holds RHS 2p (real part) and 2p + 1 (imaginary part)
-    const int64_t N = ximg;
     for (int i = threadIdx.x; i < tot; i += 256) {
-      const int64_t R = r0 + i / n;                      // complex row
-      const int64_t p = R / rpi;
-      const int64_t o = 2 * p * ximg + xoff + (R - p * rpi) * n + i % n;
-      const float s0 = norms ? (float)norms[2 * p] : 1.f;
-      const float v0 = (cb[i].x * scale) * s0;
-      x[o] = accumulate ? x[o] + v0 : v0;
-      if (2 * p + 1 < nrhs) {
-        const float s1 = norms ? (float)norms[2 * p + 1] : 1.f;
-        const float v1 = (cb[i].y * scale) * s1;
-        x[o + N] = accumulate ? x[o + N] + v1 : v1;
-      }
+      const int r = i / n, k = i - r * n;
+      Z[r0 * n + i] = cb[r * n + bitrev(k, log2n)];
     }
+    return;
+  }
+  for (int i = threadIdx.x; i < tot; i += 256) {
+    const int r = i / n, k = i - r * n;
+    cb[r * n + bitrev(k, log2n)] = Z[r0 * n + i];
+  }
+  __syncthreads();
+  fft_dit_inverse_batch(cb, n, rows, n, 1, tw, tw_n, threadIdx.x, 256);
+  for (int i = threadIdx.x; i < tot; i += 256) {
+    const int64_t Rr = r0 + i / n;                     // complex row
+    const int64_t b = Rr / rpi, r = Rr - b * rpi;
+    const int col = i % n;
+    const int64_t o = b * ximg + xoff + 2 * r * n + col;
+    const float sb = norms ? (float)norms[b] : 1.f;
+    const float v0 = (cb[i].x * scale) * sb, v1 = (cb[i].y * scale) * sb;
+    x[o] = accumulate ? x[o] + v0 : v0;
+    x[o + n] = accumulate ? x[o + n] + v1 : v1;
   }
 }
 
-// combine + forward row FFT: CTA = R rows of one pair image; h(y, x) = b3 + Q0(x-1) + Q1(x) + Q2(x+1)
-// of RHS 2p (real part) and 2p + 1 (imaginary part), 0 for a RHS with ||b|| = 0 or beyond nrhs
+// combine + forward row FFT: CTA = R complex rows of one RHS; complex row r = (h(2r, .), h(2r+1, .))
+// with h(y, x) = b3 + Q0(y, x-1) + Q1(y, x) + Q2(y, x+1), 0 for a RHS with ||b|| = 0
 __global__ void __launch_bounds__(256) combine_rows_fft_kernel(int n, int nrhs, const float4* __restrict__ Q,
                                                                const double* __restrict__ norms,
                                                                const float* __restrict__ b3, float2* __restrict__ Z,
-                                                               int zp0, const float2* __restrict__ tw, int tw_n) {
+                                                               int zb0, const float2* __restrict__ tw, int tw_n) {
   extern __shared__ __align__(16) float2 cb[];
   const int R = max(1, 4096 / n);
-  const int rpi = (n + R - 1) / R;                         // CTAs per pair image
-  const int p = blockIdx.x / rpi, y0 = (blockIdx.x - p * rpi) * R;
-  const int rows = min(R, n - y0);
+  const int half = n / 2;
+  const int rpi = (half + R - 1) / R;                      // CTAs per RHS
+  const int b = blockIdx.x / rpi, r0 = (blockIdx.x - b * rpi) * R;
+  const int rows = min(R, half - r0);
   const float bias = __ldg(b3);
-  const int b0 = 2 * p, b1 = 2 * p + 1;
-  const bool on0 = b0 < nrhs && (norms ? norms[b0] != 0.0 : true);
-  const bool on1 = b1 < nrhs && (norms ? norms[b1] != 0.0 : true);
+  const bool on = norms ? norms[b] != 0.0 : true;
   const int64_t per = (int64_t)n * n;
+  const int log2n = 31 - __clz(n);
   for (int i = threadIdx.x; i < rows * n; i += 256) {
-    const int y = y0 + i / n, x = i % n;
+    const int r = r0 + i / n, x = i % n;
     float h[2];
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
-      const bool on = e ? on1 : on0;
       float acc = 0.f;
       if (on) {
-        const int64_t idx = (int64_t)(e ? b1 : b0) * per + (int64_t)y * n + x;
+        const int64_t idx = (int64_t)b * per + (int64_t)(2 * r + e) * n + x;
         acc = bias + __ldg(&Q[idx].y);
         if (x > 0) acc += __ldg(&Q[idx - 1].x);
         if (x < n - 1) acc += __ldg(&Q[idx + 1].z);
@@ -399,94 +413,148 @@ __global__ void __launch_bounds__(256) combine_rows_fft_kernel(int n, int nrhs, 
   }
   __syncthreads();
   fft_dif_forward_batch(cb, n, rows, n, 1, tw, tw_n, threadIdx.x, 256);
-  float2* Zp = Z + (int64_t)(zp0 + p) * per + (int64_t)y0 * n;
-  for (int i = threadIdx.x; i < rows * n; i += 256) Zp[i] = cb[i];
+  float2* Zp = Z + (int64_t)(zb0 + b) * per / 2 + (int64_t)r0 * n;
+  for (int i = threadIdx.x; i < rows * n; i += 256) {
+    const int r = i / n, k = i - r * n;
+    Zp[i] = cb[r * n + bitrev(k, log2n)];
+  }
 }
 
-// columns: CTA = (group of G columns, RHS); DIF forward along i2, mask, DIT inverse
+NMG_D float mask2d(int k1, int k2, int n) {
+  const float q2 = (float)(2 * min(k2, n - k2)) / (float)n;
+  const float q1 = (float)(2 * min(k1, n - k1)) / (float)n;
+  return sqrtf(fmaxf(q1, q2));
+}
+
+// Column pass on a shared-memory tile cb[i2][c] (n x G): forward along i2, mask M'(k1[c], k2),
+// inverse along i2 (unnormalised; the 1/n^2 is applied by the inverse row pass).
+NMG_D void cols_filter_tile(float2* cb, int n, int G, const int* k1s, const float2* __restrict__ tw, int tw_n) {
+  const int log2n = 31 - __clz(n);
+  fft_dif_forward_batch(cb, n, G, 1, G, tw, tw_n, threadIdx.x, 256);
+  for (int i = threadIdx.x; i < n * G; i += 256) {
+    const int r = i / G, c = i - r * G;
+    const float m = mask2d(k1s[c], bitrev(r, log2n), n);     // rows were DIF'd: position r holds k2 = bitrev(r)
+    cb[i] = make_float2(cb[i].x * m, cb[i].y * m);
+  }
+  __syncthreads();
+  fft_dit_inverse_batch(cb, n, G, 1, G, tw, tw_n, threadIdx.x, 256);
+}
+
+// unmix (step 2): A = Z_r[k1], B = Z_r[n - k1] -> H_2r[k1], H_2r+1[k1]
+NMG_D void unmix(float2 A, float2 B, float2& h0, float2& h1) {
+  // (A + conj B) / 2 and (A - conj B) / 2i
+  h0 = make_float2(0.5f * (A.x + B.x), 0.5f * (A.y - B.y));
+  h1 = make_float2(0.5f * (A.y + B.y), -0.5f * (A.x - B.x));
+}
+// re-pack (step 2): W[k1] = Y0 + i Y1, W[n - k1] = conj Y0 + i conj Y1
+NMG_D float2 pack_k(float2 y0, float2 y1) { return make_float2(y0.x - y1.y, y0.y + y1.x); }
+NMG_D float2 pack_mirror(float2 y0, float2 y1) { return make_float2(y0.x + y1.y, y1.x - y0.y); }
+
+// whole images: Z_b = [n/2][n]; CTA = (group of G frequencies k1 = g G .. g G + G - 1 of
+// 0 .. n/2 - 1, or the single k1 = n/2 column for the last group, RHS b)
 __global__ void __launch_bounds__(256) fft_cols_kernel(int n, int G, float2* __restrict__ Z,
                                                        const float2* __restrict__ tw, int tw_n) {
-  extern __shared__ __align__(16) float2 cb[];   // [n][G]
-  const int b = blockIdx.y, k0 = blockIdx.x * G;
-  float2* Zb = Z + (int64_t)b * n * n;
-  const int log2n = 31 - __clz(n);
-  for (int i = threadIdx.x; i < n * G; i += 256) {
-    const int r = i / G, c = i - r * G;
-    cb[i] = Zb[(int64_t)r * n + k0 + c];
+  extern __shared__ __align__(16) float2 cb[];   // [n][Gc]
+  __shared__ int k1s[64];
+  const int b = blockIdx.y, half = n / 2;
+  const int ng = half / G;                        // full groups; group ng = the k1 = n/2 column
+  const int Gc = blockIdx.x < ng ? G : 1;
+  const int k0 = blockIdx.x < ng ? blockIdx.x * G : half;
+  float2* Zb = Z + (int64_t)b * half * n;
+  for (int c = threadIdx.x; c < Gc; c += 256) k1s[c] = k0 + c;
+  for (int i = threadIdx.x; i < half * Gc; i += 256) {
+    const int r = i / Gc, c = i - r * Gc;
+    const int k = k0 + c, km = (n - k) & (n - 1);
+    float2 h0, h1;
+    unmix(Zb[(int64_t)r * n + k], Zb[(int64_t)r * n + km], h0, h1);
+    cb[(2 * r) * Gc + c] = h0;
+    cb[(2 * r + 1) * Gc + c] = h1;
   }
   __syncthreads();
-  fft_dif_forward_batch(cb, n, G, 1, G, tw, tw_n, threadIdx.x, 256);
-  // mask: position r holds k2 = bitrev(r); column c holds k1 = bitrev(k0 + c) (rows were DIF'd)
-  for (int i = threadIdx.x; i < n * G; i += 256) {
-    const int r = i / G, c = i - r * G;
-    const int a2 = bitrev(r, log2n), a1 = bitrev(k0 + c, log2n);
-    const float q2 = (float)(2 * min(a2, n - a2)) / (float)n;
-    const float q1 = (float)(2 * min(a1, n - a1)) / (float)n;
-    const float m = sqrtf(fmaxf(q1, q2));
-    cb[i] = make_float2(cb[i].x * m, cb[i].y * m);
-  }
-  __syncthreads();
-  fft_dit_inverse_batch(cb, n, G, 1, G, tw, tw_n, threadIdx.x, 256);
-  for (int i = threadIdx.x; i < n * G; i += 256) {
-    const int r = i / G, c = i - r * G;
-    Zb[(int64_t)r * n + k0 + c] = cb[i];
+  cols_filter_tile(cb, n, Gc, k1s, tw, tw_n);
+  for (int i = threadIdx.x; i < half * Gc; i += 256) {
+    const int r = i / Gc, c = i - r * Gc;
+    const int k = k0 + c;
+    const float2 y0 = cb[(2 * r) * Gc + c], y1 = cb[(2 * r + 1) * Gc + c];
+    Zb[(int64_t)r * n + k] = pack_k(y0, y1);
+    if (k != 0 && k != half) Zb[(int64_t)r * n + (n - k)] = pack_mirror(y0, y1);
   }
 }
 
-// slab columns: buf = [W][npair][R][cw] (chunk q = rows q R .. q R + R - 1 of this rank's
-// columns); CTA = (group of G local columns, pair); mask with global position k1base + c
-__global__ void __launch_bounds__(256) fft_cols_slab_kernel(int n, int G, int R, int cw, int npair, float2* __restrict__ Z,
-                                                            const float2* __restrict__ tw, int tw_n, int k1base) {
-  extern __shared__ __align__(16) float2 cb[];   // [n][G]
-  const int p = blockIdx.y, k0 = blockIdx.x * G;
-  const int log2n = 31 - __clz(n);
-  const int64_t qstride = (int64_t)npair * R * cw;
-  auto at = [&](int r, int c) -> int64_t {
-    const int q = r / R;
-    return q * qstride + ((int64_t)p * R + (r - q * R)) * cw + k0 + c;
-  };
-  for (int i = threadIdx.x; i < n * G; i += 256) {
-    const int r = i / G, c = i - r * G;
-    cb[i] = Z[at(r, c)];
-  }
-  __syncthreads();
-  fft_dif_forward_batch(cb, n, G, 1, G, tw, tw_n, threadIdx.x, 256);
-  for (int i = threadIdx.x; i < n * G; i += 256) {
-    const int r = i / G, c = i - r * G;
-    const int a2 = bitrev(r, log2n), a1 = bitrev(k1base + k0 + c, log2n);
-    const float q2 = (float)(2 * min(a2, n - a2)) / (float)n;
-    const float q1 = (float)(2 * min(a1, n - a1)) / (float)n;
-    const float m = sqrtf(fmaxf(q1, q2));
-    cb[i] = make_float2(cb[i].x * m, cb[i].y * m);
-  }
-  __syncthreads();
-  fft_dit_inverse_batch(cb, n, G, 1, G, tw, tw_n, threadIdx.x, 256);
-  for (int i = threadIdx.x; i < n * G; i += 256) {
-    const int r = i / G, c = i - r * G;
-    Z[at(r, c)] = cb[i];
-  }
+// ---- slab mode: rank q holds image rows [q R, q R + R) of every RHS: Zs_b = [R/2][n].
+// The frequency columns are dealt to the ranks in mirror-closed chunks of CW = 2 h + 1 slots
+// (h = n / (2 W)): rank d gets k1 = d h + j (slot j < h), its mirror n - k1 (slot h + j; empty
+// for k1 = 0) and, on the last rank, k1 = n/2 (slot 2h; empty elsewhere).
+NMG_D int slab_col_of_slot(int d, int j, int h, int n, int W) {   // frequency of slot j, -1 if empty
+  if (j < h) return d * h + j;
+  if (j < 2 * h) { const int k = d * h + (j - h); return k == 0 ? -1 : n - k; }
+  return d == W - 1 ? n / 2 : -1;
 }
-
-// dir 0: send[d][p][r][c] = Zs[p][r][d cw + c];  dir 1: Zs[p][r][d cw + c] = send[d][p][r][c]
-__global__ void a2a_pack_kernel(int n, int npair, int R, int W, float2* __restrict__ Zs, float2* __restrict__ buf,
+// dir 0 (pack): buf[d][b][r][j] = Zs[b][r][col(d, j)] (0 for empty slots);  dir 1: the reverse
+__global__ void a2a_pack_kernel(int n, int nrhs, int R2, int W, float2* __restrict__ Zs, float2* __restrict__ buf,
                                 int dir) {
+  const int h = n / (2 * W), CW = 2 * h + 1;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t tot = (int64_t)npair * R * n;
-  if (i >= tot) return;
-  const int cw = n / W;
-  const int col = (int)(i % n);
-  const int64_t pr = i / n;                 // p * R + r
-  const int d = col / cw, c = col - d * cw;
-  const int64_t j = ((int64_t)d * npair * R + pr) * cw + c;
-  if (dir == 0) buf[j] = Zs[i];
-  else Zs[i] = buf[j];
+  const int64_t rows = (int64_t)nrhs * R2;                 // (b, r) pairs
+  if (i >= (int64_t)W * rows * CW) return;
+  const int j = (int)(i % CW);
+  const int64_t br = (i / CW) % rows;
+  const int d = (int)(i / (CW * rows));
+  const int k = slab_col_of_slot(d, j, h, n, W);
+  if (dir == 0) buf[i] = k >= 0 ? Zs[br * n + k] : make_float2(0.f, 0.f);
+  else if (k >= 0) Zs[br * n + k] = buf[i];
+}
+// columns after the all-to-all: buf = [W][nrhs][R2][CW] (chunk q = rank q's complex rows of this
+// rank's slots); CTA = (group of G slot pairs j, j + h; RHS b); the last rank's slot 2h (k1 = n/2)
+// is one extra group of one column.  Global complex row of (q, r) = q R2 + r.
+__global__ void __launch_bounds__(256) fft_cols_slab_kernel(int n, int G, int R2, int W, int rank, int nrhs,
+                                                            float2* __restrict__ buf, const float2* __restrict__ tw,
+                                                            int tw_n) {
+  extern __shared__ __align__(16) float2 cb[];   // [n][Gc]
+  __shared__ int k1s[64];
+  const int h = n / (2 * W), CW = 2 * h + 1;
+  const int b = blockIdx.y;
+  const int ng = h / G;
+  const bool last = blockIdx.x >= ng;             // the k1 = n/2 slot (last rank only)
+  const int Gc = last ? 1 : G;
+  const int j0 = last ? 2 * h : blockIdx.x * G;
+  const int64_t qstride = (int64_t)nrhs * R2 * CW;
+  auto at = [&](int rr, int j) -> int64_t {       // global complex row rr, slot j
+    const int q = rr / R2;
+    return q * qstride + ((int64_t)b * R2 + (rr - q * R2)) * CW + j;
+  };
+  for (int c = threadIdx.x; c < Gc; c += 256) k1s[c] = last ? n / 2 : rank * h + j0 + c;
+  const int half = n / 2;
+  for (int i = threadIdx.x; i < half * Gc; i += 256) {
+    const int r = i / Gc, c = i - r * Gc;
+    const int j = j0 + c;
+    const int k = last ? n / 2 : rank * h + j;
+    const float2 A = buf[at(r, j)];
+    const float2 B = (last || k == 0) ? A : buf[at(r, j + h)];
+    float2 h0, h1;
+    unmix(A, B, h0, h1);
+    cb[(2 * r) * Gc + c] = h0;
+    cb[(2 * r + 1) * Gc + c] = h1;
+  }
+  __syncthreads();
+  cols_filter_tile(cb, n, Gc, k1s, tw, tw_n);
+  for (int i = threadIdx.x; i < half * Gc; i += 256) {
+    const int r = i / Gc, c = i - r * Gc;
+    const int j = j0 + c;
+    const int k = last ? n / 2 : rank * h + j;
+    const float2 y0 = cb[(2 * r) * Gc + c], y1 = cb[(2 * r + 1) * Gc + c];
+    buf[at(r, j)] = pack_k(y0, y1);
+    if (!last && k != 0) buf[at(r, j + h)] = pack_mirror(y0, y1);
+  }
 }
 
-__global__ void real_to_complex_kernel(int nrhs, int64_t N, const float* __restrict__ x, float2* __restrict__ Z) {
+__global__ void real_to_complex_kernel(int nrhs, int n, const float* __restrict__ x, float2* __restrict__ Z) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t N = (int64_t)n * n;
   if (i >= (int64_t)nrhs * N) return;
   const int b = (int)(i / N);
-  zput(Z, N, b, i - (int64_t)b * N, x[i]);
+  const int64_t p = i - (int64_t)b * N;
+  zput(Z, n, n, b, (int)(p / n), (int)(p % n), x[i]);
 }
 
 }  // namespace
@@ -534,81 +602,66 @@ void cnn2d(const Cnn2dArgs& a, cudaStream_t s) {
 }
 void filter2d(int nrhs, int n, float2* Z, const float2* tw, int tw_n, float* x, bool accumulate, cudaStream_t s,
               const double* norms, bool rows_done) {
-  // paired layout: (nrhs + 1) / 2 complex images, each the real-part / imaginary-part pair of
-  // two right-hand sides; F' is real and symmetric, so Re and Im of the filtered pair are the
-  // two filtered images (the odd RHS out has a zero partner, zeroed by filter2d_prepare)
-  const int npair = (nrhs + 1) / 2;
-  const int64_t nrows = (int64_t)npair * n;
+  // per-RHS buffers Z_b = [n/2][n] complex (zput); three passes (rows, columns, inverse rows)
+  const int64_t nrows = (int64_t)nrhs * (n / 2);
   const int R = std::max(1, 4096 / n);
   const size_t smr = sizeof(float2) * (size_t)R * n;
-  cudaFuncSetAttribute(fft_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
   if (!rows_done)
-    fft_rows_kernel<<<nblk(nrows, R), 256, smr, s>>>(n, nrows, Z, tw, tw_n, 0, nullptr, 0, 1.f, nrhs, nullptr, n,
+    fft_rows_kernel<<<nblk(nrows, R), 256, smr, s>>>(n, nrows, Z, tw, tw_n, 0, nullptr, 0, 1.f, nullptr, n / 2,
                                                      (int64_t)n * n, 0);
-  static const int cols_elems = [] {   // complex elements per column-pass CTA (dev knob)
-    const char* e = std::getenv("NMG_FFT_COLS_KB");
-    return (e ? std::atoi(e) : 32) * 1024 / 8;
-  }();
-  const int G = std::min(n, std::max(1, cols_elems / n));
+  const int G = std::min(std::max(1, n / 2), std::min(64, std::max(1, 4096 / n)));   // 32 KB of columns
   const size_t smc = sizeof(float2) * (size_t)n * G;
-  cudaFuncSetAttribute(fft_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
-  fft_cols_kernel<<<dim3(n / G, npair), 256, smc, s>>>(n, G, Z, tw, tw_n);
+  NMG_SMEM_OPTIN(fft_cols_kernel, 65536);
+  fft_cols_kernel<<<dim3(std::max(1, (n / 2) / G) + 1, nrhs), 256, smc, s>>>(n, G, Z, tw, tw_n);
   fft_rows_kernel<<<nblk(nrows, R), 256, smr, s>>>(n, nrows, Z, tw, tw_n, 1, x, accumulate ? 1 : 0,
-                                                   1.0f / ((float)n * (float)n), nrhs, norms, n, (int64_t)n * n, 0);
+                                                   1.0f / ((float)n * (float)n), norms, n / 2, (int64_t)n * n, 0);
 }
 
 // ---------------------------------------------------------------- slab-sharded level filter
-// Rank `rank` of W holds rows [rank R, rank R + R) of every pair image: Zs [npair][R][n].
-//   1. row FFTs of the local rows (DIF, bit-reversed positions)
-//   2. pack: send chunk d = columns [d cw, d cw + cw) of every local row, [d][p][R][cw]
-//   3. all-to-all (caller): recv chunk q = rank q's rows of this rank's columns
-//   4. column FFT over i2 = (q, r), mask with the global column position, inverse (in place)
+// Rank `rank` of W holds rows [rank R, rank R + R) of every image: Zs [nrhs][R/2][n].
+//   1. row FFTs of the local complex rows (natural-order spectra)
+//   2. pack: send chunk d = rank d's mirror-closed frequency slots of every local row
+//   3. all-to-all (caller): recv chunk q = rank q's rows of this rank's slots
+//   4. unmix, column FFT over i2, mask, inverse, re-pack (in place)
 //   5. all-to-all back (caller), unpack into Zs, inverse row FFTs + scale + update of x.
-void filter2d_slab_rows(int n, int npair, int R, float2* Zs, const float2* tw, int tw_n, cudaStream_t s) {
-  const int64_t nrows = (int64_t)npair * R;
+int filter2d_slab_chunk(int n, int W) { return n / W + 1; }   // slots per rank (2 h + 1)
+void filter2d_slab_rows(int n, int nrhs, int R, float2* Zs, const float2* tw, int tw_n, cudaStream_t s) {
+  const int64_t nrows = (int64_t)nrhs * (R / 2);
   const int RR = std::max(1, 4096 / n);
   const size_t smr = sizeof(float2) * (size_t)RR * n;
-  cudaFuncSetAttribute(fft_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
-  fft_rows_kernel<<<nblk(nrows, RR), 256, smr, s>>>(n, nrows, Zs, tw, tw_n, 0, nullptr, 0, 1.f, 0, nullptr, R,
+  fft_rows_kernel<<<nblk(nrows, RR), 256, smr, s>>>(n, nrows, Zs, tw, tw_n, 0, nullptr, 0, 1.f, nullptr, R / 2,
                                                     (int64_t)R * n, 0);
 }
 void filter2d_slab_inverse(int n, int nrhs, int R, float2* Zs, const float2* tw, int tw_n, float* x, int64_t ximg,
                            int64_t xoff, bool accumulate, const double* norms, cudaStream_t s) {
-  const int npair = (nrhs + 1) / 2;
-  const int64_t nrows = (int64_t)npair * R;
+  const int64_t nrows = (int64_t)nrhs * (R / 2);
   const int RR = std::max(1, 4096 / n);
   const size_t smr = sizeof(float2) * (size_t)RR * n;
-  cudaFuncSetAttribute(fft_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
   fft_rows_kernel<<<nblk(nrows, RR), 256, smr, s>>>(n, nrows, Zs, tw, tw_n, 1, x, accumulate ? 1 : 0,
-                                                    1.0f / ((float)n * (float)n), nrhs, norms, R, ximg, xoff);
+                                                    1.0f / ((float)n * (float)n), norms, R / 2, ximg, xoff);
 }
-
-void filter2d_slab_pack(int n, int npair, int R, int W, float2* Zs, float2* buf, bool unpack, cudaStream_t s) {
-  a2a_pack_kernel<<<nblk((int64_t)npair * R * n, 256), 256, 0, s>>>(n, npair, R, W, Zs, buf, unpack ? 1 : 0);
+void filter2d_slab_pack(int n, int nrhs, int R, int W, float2* Zs, float2* buf, bool unpack, cudaStream_t s) {
+  const int64_t tot = (int64_t)W * nrhs * (R / 2) * filter2d_slab_chunk(n, W);
+  a2a_pack_kernel<<<nblk(tot, 256), 256, 0, s>>>(n, nrhs, R / 2, W, Zs, buf, unpack ? 1 : 0);
 }
-void filter2d_slab_cols(int n, int npair, int R, int W, int rank, float2* buf, const float2* tw, int tw_n,
+void filter2d_slab_cols(int n, int nrhs, int R, int W, int rank, float2* buf, const float2* tw, int tw_n,
                         cudaStream_t s) {
-  const int cw = n / W;
-  const int G = std::min(cw, std::max(1, 16384 / n));
+  const int h = n / (2 * W);
+  const int G = std::min(h, std::min(64, std::max(1, 4096 / n)));
   const size_t smc = sizeof(float2) * (size_t)n * G;
-  cudaFuncSetAttribute(fft_cols_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
-  fft_cols_slab_kernel<<<dim3(cw / G, npair), 256, smc, s>>>(n, G, R, cw, npair, buf, tw, tw_n, rank * cw);
+  NMG_SMEM_OPTIN(fft_cols_slab_kernel, 65536);
+  const int groups = h / G + (rank == W - 1 ? 1 : 0);
+  fft_cols_slab_kernel<<<dim3(groups, nrhs), 256, smc, s>>>(n, G, R / 2, W, rank, nrhs, buf, tw, tw_n);
 }
 void combine_rows_fft(int n, int nrhs, const float* q, const double* norms, const float* b3, float2* Z, int zb0,
                       const float2* tw, int tw_n, cudaStream_t s) {
   const int R = std::max(1, 4096 / n);
-  const int npair = (nrhs + 1) / 2;
   const size_t smr = sizeof(float2) * (size_t)R * n;
-  cudaFuncSetAttribute(combine_rows_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
-  combine_rows_fft_kernel<<<npair * ceil_div(n, R), 256, smr, s>>>(n, nrhs, reinterpret_cast<const float4*>(q), norms,
-                                                                   b3, Z, zb0 / 2, tw, tw_n);
+  combine_rows_fft_kernel<<<nrhs * ceil_div(n / 2, R), 256, smr, s>>>(n, nrhs, reinterpret_cast<const float4*>(q),
+                                                                      norms, b3, Z, zb0, tw, tw_n);
 }
-void filter2d_prepare(int nrhs, int n, float2* Z, cudaStream_t s, int rows) {
-  if (rows <= 0) rows = n;
-  if (nrhs & 1) cudaMemsetAsync(Z + (int64_t)(nrhs / 2) * rows * n, 0, sizeof(float2) * (size_t)rows * n, s);
-}
-void real_to_complex(int nrhs, int64_t N, const float* x, float2* Z, cudaStream_t s) {
-  real_to_complex_kernel<<<nblk((int64_t)nrhs * N, 256), 256, 0, s>>>(nrhs, N, x, Z);
+void real_to_complex(int nrhs, int n, const float* x, float2* Z, cudaStream_t s) {
+  real_to_complex_kernel<<<nblk((int64_t)nrhs * n * n, 256), 256, 0, s>>>(nrhs, n, x, Z);
 }
 
 }  // namespace nmg

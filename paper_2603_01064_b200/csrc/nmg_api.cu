@@ -395,7 +395,7 @@ struct nmg_hierarchy {
   bool prof_on = false;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
-  struct Rec { int cls; cudaEvent_t a, b; };
+  struct Rec { int cls, nk; cudaEvent_t a, b; };
   std::vector<Rec> recs;
   // CUDA graphs of one cycle, keyed by (nrhs, y, x, stream); a few entries so that the chunks
   // of nmg_vcycles_host each replay their own graph
@@ -467,11 +467,12 @@ cudaEvent_t prof_event(nmg_hierarchy* h) {
   return h->ev_pool[h->ev_used++];
 }
 
-// Counts one library launch of class `cls`; when profiling, brackets it with events.
+// Counts the `nk` library kernel launches of one launcher call of class `cls`; when profiling,
+// brackets them with events.
 struct Prof {
-  nmg_hierarchy* h; int cls; cudaStream_t s; cudaEvent_t a = nullptr;
-  Prof(nmg_hierarchy* h_, int cls_, cudaStream_t s_) : h(h_), cls(cls_), s(s_) {
-    h->launches++;
+  nmg_hierarchy* h; int cls; cudaStream_t s; int nk; cudaEvent_t a = nullptr;
+  Prof(nmg_hierarchy* h_, int cls_, cudaStream_t s_, int nk_ = 1) : h(h_), cls(cls_), s(s_), nk(nk_) {
+    h->launches += nk;
     if (h->prof_on && (a = prof_event(h))) cudaEventRecord(a, s);
   }
   ~Prof() {
@@ -479,7 +480,7 @@ struct Prof {
     cudaEvent_t b = prof_event(h);
     if (!b) return;
     cudaEventRecord(b, s);
-    h->recs.push_back({cls, a, b});
+    h->recs.push_back({cls, nk, a, b});
   }
 };
 
@@ -704,11 +705,10 @@ nmg_status smooth2d(nmg_hierarchy* h, int l, int nrhs, const float* b, float* x,
   const int64_t N = (int64_t)n * n;
   const int chunks = (int)std::min<int64_t>(64, std::max<int64_t>(1, N / 4096));
   if (normalize) {
-    { Prof p(h, NMG_K_SMOOTH, s); norms_f32(nrhs, N, b, h->spart.p, chunks, h->snorm.p, s); }
+    { Prof p(h, NMG_K_FILTER, s, 2); norms_f32(nrhs, N, b, h->spart.p, chunks, h->snorm.p, s); }
     NMG_TRY(check_launch(h));
   }
   const bool filt = filter && h->d.level_filter != 0;
-  if (filt) filter2d_prepare(nrhs, n, h->Z.p, s);
   if (h->conv_bf && strip_level(n) && h->bf_C == h->arch.channels) {
     const int C = h->arch.channels;
     const float* P = h->W[l]->p;
@@ -739,16 +739,16 @@ nmg_status smooth2d(nmg_hierarchy* h, int l, int nrhs, const float* b, float* x,
       { Prof p(h, NMG_K_SMOOTH, s); strip_l34(&h->mA2h[l], &h->mA2l[l], a, h->num_sms, s); }
       if (filt && h->fuse_combine) {
         // h = s (b3 + Q0 + Q1 + Q2) for the chunk's RHS pairs, straight into the forward row FFT
-        { Prof p(h, NMG_K_SMOOTH, s);
+        { Prof p(h, NMG_K_FILTER, s);
           combine_rows_fft(n, cnt, h->qbuf.p, a.norms, b3, h->Z.p, r0, h->tw.p, h->tw_n, s); }
       } else {
-        { Prof p(h, NMG_K_SMOOTH, s);
+        { Prof p(h, NMG_K_FILTER, s);
           strip_combine(n, cnt, h->qbuf.p, a.norms, b3, filt ? h->Z.p : nullptr, r0, x + off, accumulate, s); }
       }
       NMG_TRY(check_launch(h));
     }
     if (filt) {
-      { Prof p(h, NMG_K_SMOOTH, s);
+      { Prof p(h, NMG_K_FILTER, s, h->fuse_combine ? 2 : 3);
         filter2d(nrhs, n, h->Z.p, h->tw.p, h->tw_n, x, accumulate, s, normalize ? h->snorm.p : nullptr,
                  h->fuse_combine); }
       NMG_TRY(check_launch(h));
@@ -762,7 +762,7 @@ nmg_status smooth2d(nmg_hierarchy* h, int l, int nrhs, const float* b, float* x,
   { Prof p(h, NMG_K_SMOOTH, s); cnn2d(a, s); }
   NMG_TRY(check_launch(h));
   if (filt) {
-    { Prof p(h, NMG_K_SMOOTH, s); filter2d(nrhs, n, h->Z.p, h->tw.p, h->tw_n, x, accumulate, s, normalize ? h->snorm.p : nullptr); }
+    { Prof p(h, NMG_K_FILTER, s, 3); filter2d(nrhs, n, h->Z.p, h->tw.p, h->tw_n, x, accumulate, s, normalize ? h->snorm.p : nullptr); }
     NMG_TRY(check_launch(h));
   }
   return NMG_OK;
@@ -859,14 +859,13 @@ nmg_status smooth_slab(nmg_hierarchy* h, int l, int nrhs, float* b, float* x, bo
   // ||b|| over the whole image: local sums of squares, summed over the ranks (fixed order)
   {
     const int chunks = (int)std::min<int64_t>(64, std::max<int64_t>(1, (int64_t)R * n / 4096));
-    { Prof p(h, NMG_K_SMOOTH, s); sumsq_f32(nrhs, (int64_t)R * n, b, img, (int64_t)H * n, h->spart.p, chunks, h->snorm.p, s); }
+    { Prof p(h, NMG_K_FILTER, s, 2); sumsq_f32(nrhs, (int64_t)R * n, b, img, (int64_t)H * n, h->spart.p, chunks, h->snorm.p, s); }
     NMG_TRY(check_launch(h));
     NMG_TRY(h->comm->sum_f64(h->snorm.p, nrhs, h->dscratch.p, s));
     { Prof p(h, NMG_K_MISC, s); sqrt_inplace(nrhs, h->snorm.p, s); }
   }
   NMG_TRY(halo_exchange(h, l, nrhs, b, s));
   const bool filt = h->d.level_filter != 0;
-  if (filt) filter2d_prepare(nrhs, n, h->zs.p, s, R);
   const float* P = h->W[l]->p;
   const float* b1 = P + C * 9 + C + C * C * 9;
   const float* b2 = b1 + C + C * C * 9;
@@ -898,23 +897,22 @@ nmg_status smooth_slab(nmg_hierarchy* h, int l, int nrhs, float* b, float* x, bo
     a.d_scale = 1.0f / (sc[2] * sc[3]);
     a.w4 = wb + 4 * plane; a.a3_scale = sc[4]; a.d4_scale = 1.0f / (sc[4] * sc[5]);
     { Prof p(h, NMG_K_SMOOTH, s); strip_l34(&m2h, &m2l, a, h->num_sms, s); }
-    { Prof p(h, NMG_K_SMOOTH, s);
+    { Prof p(h, NMG_K_FILTER, s);
       strip_combine(n, cnt, h->qbuf.p, a.norms, b3, filt ? h->zs.p : nullptr, c0, x + off, accumulate, s, hg, H); }
     NMG_TRY(check_launch(h));
   }
   if (filt) {
     // rows local; columns after an all-to-all transpose; back; inverse rows + update
-    const int npair = (nrhs + 1) / 2;
-    const size_t chunk = sizeof(float2) * (size_t)npair * R * (n / h->nw);
-    { Prof p(h, NMG_K_SMOOTH, s); filter2d_slab_rows(n, npair, R, h->zs.p, h->tw.p, h->tw_n, s); }
-    { Prof p(h, NMG_K_MISC, s); filter2d_slab_pack(n, npair, R, h->nw, h->zs.p, h->za.p, false, s); }
+    const size_t chunk = sizeof(float2) * (size_t)nrhs * (R / 2) * filter2d_slab_chunk(n, h->nw);
+    { Prof p(h, NMG_K_FILTER, s); filter2d_slab_rows(n, nrhs, R, h->zs.p, h->tw.p, h->tw_n, s); }
+    { Prof p(h, NMG_K_MISC, s); filter2d_slab_pack(n, nrhs, R, h->nw, h->zs.p, h->za.p, false, s); }
     NMG_TRY(check_launch(h));
     NMG_TRY(h->comm->all_to_all(h->za.p, h->zb.p, chunk, s));
-    { Prof p(h, NMG_K_SMOOTH, s); filter2d_slab_cols(n, npair, R, h->nw, h->rank, h->zb.p, h->tw.p, h->tw_n, s); }
+    { Prof p(h, NMG_K_FILTER, s); filter2d_slab_cols(n, nrhs, R, h->nw, h->rank, h->zb.p, h->tw.p, h->tw_n, s); }
     NMG_TRY(check_launch(h));
     NMG_TRY(h->comm->all_to_all(h->zb.p, h->za.p, chunk, s));
-    { Prof p(h, NMG_K_MISC, s); filter2d_slab_pack(n, npair, R, h->nw, h->zs.p, h->za.p, true, s); }
-    { Prof p(h, NMG_K_SMOOTH, s);
+    { Prof p(h, NMG_K_MISC, s); filter2d_slab_pack(n, nrhs, R, h->nw, h->zs.p, h->za.p, true, s); }
+    { Prof p(h, NMG_K_FILTER, s);
       filter2d_slab_inverse(n, nrhs, R, h->zs.p, h->tw.p, h->tw_n, x, img, (int64_t)H * n, accumulate, h->snorm.p, s); }
     NMG_TRY(check_launch(h));
   }
@@ -1109,10 +1107,10 @@ nmg_status outer_residual(nmg_hierarchy* h, int nrhs, const double* y, const dou
 // ||y|| per RHS (slab mode: local sums of squares summed over the ranks)
 nmg_status ynorms(nmg_hierarchy* h, int nrhs, const double* y, cudaStream_t s) {
   if (!h->slab) {
-    { Prof p(h, NMG_K_MISC, s); row_norms_f64(nrhs, (int)h->N[0], y, h->N[0], h->ynorm.p, h->ywork.p, s); }
+    { Prof p(h, NMG_K_MISC, s, 2); row_norms_f64(nrhs, (int)h->N[0], y, h->N[0], h->ynorm.p, h->ywork.p, s); }
     return check_launch(h);
   }
-  { Prof p(h, NMG_K_MISC, s); sumsq_f64(nrhs, (int64_t)h->R[0] * h->n[0], y, h->ywork.p, h->ysq.p, s); }
+  { Prof p(h, NMG_K_MISC, s, 2); sumsq_f64(nrhs, (int64_t)h->R[0] * h->n[0], y, h->ywork.p, h->ysq.p, s); }
   NMG_TRY(check_launch(h));
   return h->comm->sum_f64(h->ysq.p, nrhs, h->dscratch.p, s);
 }
@@ -1181,8 +1179,8 @@ nmg_status debug_2d(nmg_hierarchy* h, int l, int op, int nrhs, const float* fin,
       return check_launch(h);
     case NMG_OP_FILTER:
       if (!smoothed) return fail(NMG_ERR_INVALID_ARG, "no filter at the coarsest level");
-      { Prof p(h, NMG_K_SMOOTH, s); filter2d_prepare(nrhs, n, h->Z.p, s); real_to_complex(nrhs, (int64_t)n * n, fin, h->Z.p, s); }
-      { Prof p(h, NMG_K_SMOOTH, s); filter2d(nrhs, n, h->Z.p, h->tw.p, h->tw_n, fout, false, s, nullptr); }
+      { Prof p(h, NMG_K_FILTER, s); real_to_complex(nrhs, n, fin, h->Z.p, s); }
+      { Prof p(h, NMG_K_FILTER, s, 3); filter2d(nrhs, n, h->Z.p, h->tw.p, h->tw_n, fout, false, s, nullptr); }
       return check_launch(h);
     case NMG_OP_CNN:
     case NMG_OP_SMOOTH:
@@ -1229,7 +1227,7 @@ nmg_status graph_cycle(nmg_hierarchy* h, int nrhs, const double* y, double* x, c
                        bool allow_lanes = true) {
   auto body = [&]() -> nmg_status {
     const int K = (int)h->lanes.size() + 1;
-    const int gr = h->d.dim == 1 ? 128 : 2;             // lane granularity (GEMM M tiles / filter pairs)
+    const int gr = h->d.dim == 1 ? 128 : 2;             // lane granularity (1D: GEMM M tiles)
     if (K == 1 || !allow_lanes || h->prof_on || nrhs < K * gr || s == nullptr) {
       NMG_TRY(ynorms(h, nrhs, y, s));
       return outer_step(h, nrhs, y, x, -1.0, false, s);
@@ -1615,7 +1613,7 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
         NMG_TRY(make_map(&h->mKCl[l], h->C32l[l]->p, nl, nl, kb));
       }
     }
-    NMG_TRY(h->Z.alloc(B * (size_t)h->N[0]));
+    NMG_TRY(h->Z.alloc(B * (size_t)h->N[0] / 2));          // level filter: [B][n/2][n] complex
     NMG_TRY(h->snorm.alloc(B));
     NMG_TRY(h->spart.alloc(B * 64));
     NMG_TRY(h->T64.alloc(B * (size_t)h->N[0]));
@@ -1773,10 +1771,10 @@ nmg_status nmg_create_hierarchy_slab(const nmg_problem_desc* desc, const double*
   NMG_TRY(h->t64recv.alloc(B * n0 * n0));
   NMG_TRY(h->hsend.alloc(2 * B * H * n0));
   NMG_TRY(h->hrecv.alloc((size_t)W * 2 * B * H * n0));
-  const size_t np = (B + 1) / 2;
-  NMG_TRY(h->zs.alloc(np * R0 * n0));
-  NMG_TRY(h->za.alloc(np * R0 * n0));
-  NMG_TRY(h->zb.alloc(np * R0 * n0));
+  // level filter: per-RHS [R/2][n] complex rows; all-to-all chunks of n / W + 1 slots per rank
+  NMG_TRY(h->zs.alloc(B * (R0 / 2) * n0));
+  NMG_TRY(h->za.alloc((size_t)W * B * (R0 / 2) * filter2d_slab_chunk(n0, W)));
+  NMG_TRY(h->zb.alloc((size_t)W * B * (R0 / 2) * filter2d_slab_chunk(n0, W)));
   const int nq = h->n[h->Ls];
   NMG_TRY(h->csend.alloc(B * (nq / W) * nq));
   NMG_TRY(h->crecv.alloc(B * nq * nq));
@@ -1907,7 +1905,6 @@ nmg_status nmg_load_smoother_weights(nmg_hierarchy* h, int32_t level, const nmg_
           const int64_t cmax = std::max<int64_t>(1, std::min<int64_t>(B, budget / per));
           const int64_t nch = (B + cmax - 1) / cmax;
           h->bf_chunk = (int)((B + nch - 1) / nch);
-          if (h->bf_chunk > 1 && h->bf_chunk < B) h->bf_chunk &= ~1;   // even: filter pairs never straddle chunks
           h->bf_px = px;
           NMG_TRY(h->a2h.alloc((size_t)h->bf_chunk * px * C));
           NMG_TRY(h->a2l.alloc((size_t)h->bf_chunk * px * C));
@@ -2256,7 +2253,7 @@ nmg_status nmg_profile_query(nmg_hierarchy* h, int32_t kclass, double* total_ms,
     float ms = 0.f;
     NMG_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
     tot += ms;
-    ++cnt;
+    cnt += r.nk;
   }
   *total_ms = tot;
   *launches = cnt;
