@@ -1,0 +1,171 @@
+"""GPU parity at the benchmark's exact launch configurations (bench.py): full BASELINE batches on
+handles sized like the bench's (1D: max_rhs 1024 -> four RHS lanes, 256-wide multicast FP16x3
+GEMM tiles, Ozaki fp64 residual; 2D: the 8-RHS seeded pool tiled to the full batch, the strip-
+kernel CNN in RHS chunks, Ozaki 2D residual, Kronecker applies).
+
+Expected values: the fp64 oracle, precomputed by tools/make_oracle_goldens.py (calls only
+oracle/ and nmg_inputs) into tests/golden/oracle_*.npz.  Tolerances (BASELINE.json north_star):
+per-operator 1e-5 relative L2 PER RHS, residual histories 1e-3 relative until 1e-6, stopping
+cycles equal (+-1 only when the oracle residual is within 1e-3 of the tolerance, reading R13).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import nmg_inputs as ni
+from tests._setup import gpu_hierarchy, history_close, oracle_hierarchy, weights_for
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2603_01064_b200 as nmg  # noqa: E402
+from oracle import nmg_oracle as O  # noqa: E402
+
+DEV = torch.device("cuda:0")
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+CFG1 = ni.CONFIGS[1]
+
+
+def T(a, dtype=torch.float32):
+    return torch.tensor(np.ascontiguousarray(a), dtype=dtype, device=DEV)
+
+
+def rel_rows(a, b):
+    """Relative L2 error of every RHS (row) separately."""
+    a = np.asarray(a, np.float64).reshape(a.shape[0], -1)
+    b = np.asarray(b, np.float64).reshape(b.shape[0], -1)
+    nb = np.linalg.norm(b, axis=1)
+    return np.linalg.norm(a - b, axis=1) / np.where(nb > 0, nb, 1.0)
+
+
+def gold(name):
+    return np.load(os.path.join(GOLD, name))
+
+
+@pytest.fixture(scope="module")
+def cfg1_bench():
+    """The bench's config-1 handle: 1024 RHS, default lanes (four lanes of 256 RHS)."""
+    f = ni.operator_factors(CFG1)
+    W = weights_for(CFG1, "seed")
+    return f, W, oracle_hierarchy(CFG1, f, W), gpu_hierarchy(CFG1, f, W, max_rhs=CFG1.nrhs)
+
+
+@pytest.mark.parametrize("lvl", [1, 2])
+def test_cfg1_operator_full_batch_per_rhs(cfg1_bench, lvl):
+    """OP_APPLY / OP_RESIDUAL with the full 1024-RHS batch: level 1 runs the 256-wide FP16x3 GEMM
+    with the operator tile multicast over CTA pairs (tc_gemm_kernel<256, f16, MC>), level 2 the
+    64-wide tiles; every RHS within 1e-5 on its own."""
+    _, _, H, h = cfg1_bench
+    n = CFG1.n >> (lvl - 1)
+    rng = np.random.default_rng(40 + lvl)
+    x = rng.standard_normal((1024, n)).astype(np.float32)
+    x *= np.logspace(-3, 3, 1024, dtype=np.float32)[:, None]        # per-RHS scales (per-row f16 split)
+    y = rng.standard_normal((1024, n)).astype(np.float32)
+    want = O.apply_A(H, lvl - 1, x.astype(np.float64))
+    out = torch.zeros(1024, n, device=DEV)
+    h.debug_op(lvl, nmg.OP_APPLY, T(x), out)
+    assert rel_rows(out.cpu().numpy(), want).max() < 1e-5
+    yy = y * np.abs(want).max(axis=1, keepdims=True).astype(np.float32)
+    r = T(yy)
+    h.debug_op(lvl, nmg.OP_RESIDUAL, T(x), r)
+    assert rel_rows(r.cpu().numpy(), yy - want).max() < 1e-5
+
+
+@pytest.mark.parametrize("alpha", ni.ALPHAS[1])
+def test_cfg1_full_batch_wseed_alpha_sweep(alpha):
+    """The bench's config-1 launch (1024 RHS, four lanes, Ozaki residual) for every alpha of the
+    sweep: 10 W_seed cycles; 16 sampled RHS (lane edges 255/256, 511/512, 767/768 included)
+    against the oracle's histories."""
+    cfg = CFG1.replace(alpha=alpha)
+    f = ni.operator_factors(cfg)
+    W = weights_for(cfg, "seed")
+    h = gpu_hierarchy(cfg, f, W, max_rhs=cfg.nrhs)
+    y, _ = ni.make_rhs(cfg, f, alpha)
+    yd = T(y, torch.float64)
+    xd = torch.zeros_like(yd)
+    rep = h.solve(yd, xd, tol=1e-300, max_cycles=cfg.cycles)
+    g = gold("oracle_cfg1_wseed.npz")
+    idx = g["idx"]
+    ok, err = history_close(rep["history"][idx], g[f"hist_{alpha:g}"])
+    assert ok, err
+    h.close()
+
+
+@pytest.mark.parametrize("alpha", [1e-2, 1e-3])
+def test_cfg1_wlin_solve_stopping_cycles(alpha):
+    """RHS solved to 1e-6 (the bench's `solve` figure) with the converging W_lin stand-in:
+    each sampled RHS stops at the oracle's cycle (+-1 only per reading R13) and its history
+    matches until 1e-6."""
+    cfg = CFG1.replace(alpha=alpha)
+    f = ni.operator_factors(cfg)
+    W = weights_for(cfg, "lin")
+    h = gpu_hierarchy(cfg, f, W, max_rhs=cfg.nrhs)
+    y, _ = ni.make_rhs(cfg, f, alpha)
+    yd = T(y, torch.float64)
+    xd = torch.zeros_like(yd)
+    rep = h.solve(yd, xd, tol=1e-6, max_cycles=100)
+    assert rep["converged"].all()
+    g = gold("oracle_cfg1_wlin.npz")
+    idx = g["idx"]
+    oc, oh = g[f"cycles_{alpha:g}"], g[f"hist_{alpha:g}"]
+    assert g[f"conv_{alpha:g}"].all()
+    ok, err = history_close(rep["history"][idx], oh)
+    assert ok, err
+    for k, b in enumerate(idx):
+        d = abs(int(rep["cycles"][b]) - int(oc[k]))
+        if d:
+            c = min(int(rep["cycles"][b]), int(oc[k]))
+            assert d == 1 and abs(oh[k, c] - 1e-6) <= 1e-3 * 1e-6, (b, rep["cycles"][b], oc[k])
+    h.close()
+
+
+POOL = {"cfg2": (2, 1e-3), "cfg3_a1e-3": (3, 1e-3), "cfg3_a1e-4": (3, 1e-4), "cfg4": (4, 1e-4)}
+
+
+@pytest.mark.parametrize("key", list(POOL))
+def test_2d_bench_batch_tiled_pool(key):
+    """The bench's 2D launch: the configuration's full batch (256 / 2048 / 32 RHS) built by tiling
+    the 8-RHS seeded pool, on a handle with max_rhs = batch (RHS chunks of the strip CNN, lanes
+    where the bench has them).  3 cycles; every batch RHS is bitwise its pool member's result
+    (per-RHS independence), and the pool members' histories match the oracle's."""
+    cid, alpha = POOL[key]
+    cfg = ni.CONFIGS[cid].replace(alpha=alpha)
+    f = ni.operator_factors(cfg)
+    W = weights_for(cfg, "seed")
+    B = cfg.nrhs
+    pool, _ = ni.make_rhs(cfg, f, alpha, nrhs=8, start=0)
+    y = np.ascontiguousarray(np.concatenate([pool] * (-(-B // 8)))[:B])
+    h = gpu_hierarchy(cfg, f, W, max_rhs=B)
+    yd = T(y, torch.float64)
+    del y
+    xd = torch.zeros_like(yd)
+    rep = h.solve(yd, xd, tol=1e-300, max_cycles=3)
+    hist = rep["history"]
+    x = xd.view(B, -1)
+    for b in range(8, B):
+        assert np.array_equal(hist[b], hist[b % 8]), b
+    for b in range(8, B, max(1, B // 64)):
+        assert torch.equal(x[b], x[b % 8]), b
+    g = gold("oracle_2d_pool.npz")[f"hist_{key}"]
+    ok, err = history_close(hist[:g.shape[0]], g)
+    assert ok, err
+    h.close()
+    del xd, yd
+    torch.cuda.empty_cache()
+
+
+def test_coarse_substitution_cfg1(cfg1_bench):
+    """tuning.coarse_subst (Cholesky forward/back substitution, the north-star form of the
+    coarsest solve) at config 1: same histories as the explicit-inverse default."""
+    f, W, H, _ = cfg1_bench
+    h = gpu_hierarchy(CFG1.replace(nrhs=4), f, W, max_rhs=4, tuning={"coarse_subst": 1})
+    y, _ = ni.make_rhs(CFG1, f, CFG1.alpha, nrhs=4)
+    yd = T(y, torch.float64)
+    rep = h.solve(yd, torch.zeros_like(yd), tol=1e-300, max_cycles=4)
+    orc = O.solve(H, y, tol=1e-300, max_cycles=4, freeze=False)
+    ok, err = history_close(rep["history"], orc.history)
+    assert ok, err
