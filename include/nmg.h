@@ -116,6 +116,17 @@ typedef struct {
   int32_t n_layers, channels, ksize;
 } nmg_cnn_arch;
 
+/* FNO smoother architecture (the paper's own smoother: PAPER.md section 3.1 P:208-216,
+ * Appendix A; per-grid values in Table 6): lift 1 -> width (pointwise),
+ * n_layers Fourier layers GELU(DFT^{-1}(R (.) DFT(Z)) + W * Z + B) with R a complex width x width
+ * mixing of the `modes` lowest frequencies per axis (2D: i1-modes 0..modes-1 x i2-modes
+ * 0..modes-1 and n-modes..n-1) and W a ksize (x ksize) convolution with zero "same" padding,
+ * then proj width -> 1 (pointwise).  Constraints: width <= 64, 1 <= n_layers <= 8, ksize odd
+ * <= 7, modes a power of two <= n_l / 4. */
+typedef struct {
+  int32_t width, n_layers, modes, ksize;
+} nmg_fno_arch;
+
 /* Solve report (SPEC SolveReport analogue), caller-allocated HOST memory. */
 typedef struct {
   int32_t *cycles;       /* [nrhs] cycles applied to each RHS                              */
@@ -146,6 +157,16 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc *desc, const double *fact
  * Errors: INVALID_ARG, SHAPE, UNSUPPORTED, CUDA. */
 nmg_status nmg_load_smoother_weights(nmg_hierarchy *h, int32_t level, const nmg_cnn_arch *arch,
                                      const float *params, size_t n_params);
+
+/* Load an FNO smoother theta_l for level `level` (1..L-1) instead of a CNN; params: host fp32,
+ * copied, in the order lift.w [c][1], lift.b [c]; per Fourier layer: R as (re, im) pairs
+ * [modes][c_in][c_out][2] (1D) or [2 modes][modes][c_in][c_out][2] (2D; i2-mode rows 0..modes-1
+ * then n-modes..n-1), W [c_out][c_in][ksize](x ksize), B [c]; proj.w [1][c], proj.b [1].
+ * Allocates the level's FNO workspaces (sized by max_rhs, RHS-chunked); replaces whatever
+ * smoother the level had; drops captured cycle graphs.  Errors: INVALID_ARG, SHAPE,
+ * UNSUPPORTED, OOM, CUDA. */
+nmg_status nmg_load_fno_weights(nmg_hierarchy *h, int32_t level, const nmg_fno_arch *arch,
+                                const float *params, size_t n_params);
 
 /* One cycle x <- NMGF(x, y) for nrhs right-hand sides (one tau step), computed in
  * correction form x + NMGF(0, y - A x) (pin P11): fp64 outer residual, fp32-accurate

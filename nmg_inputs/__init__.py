@@ -330,3 +330,74 @@ def weights_lin(cfg: Config, scale: Optional[float] = None, g1=None, alpha: Opti
 
 def cnn_arch(cfg: Config) -> Tuple[int, int, int]:
     return (cfg.n_layers, cfg.channels, cfg.ksize)
+
+
+# --------------------------------------------------------------------------
+# FNO smoother (Appendix A, Table 6)
+# --------------------------------------------------------------------------
+# Table 6 (tab:network_structures): per grid h = 1/n the width c, Fourier layers L, retained
+# modes k and W-convolution kernel size.  Grids outside the table take the nearest row with
+# k capped at n/4 (reading R23 in DESIGN.md).
+FNO_TABLE = {
+    1: {64: (64, 4, 16, 5), 128: (64, 4, 32, 5), 256: (64, 5, 64, 7), 512: (64, 6, 128, 7), 1024: (64, 6, 128, 7)},
+    2: {64: (64, 4, 16, 3), 128: (64, 4, 32, 3), 256: (64, 5, 32, 5), 512: (64, 6, 64, 7), 1024: (64, 6, 64, 7)},
+}
+
+
+def fno_arch(dim: int, n: int, width: Optional[int] = None) -> Tuple[int, int, int, int]:
+    """(c, L, k, ksize) for a level with n points per axis (Table 6, nearest row)."""
+    rows = FNO_TABLE[dim]
+    key = min(rows, key=lambda r: abs(math.log2(r) - math.log2(n)))
+    c, L, k, ks = rows[key]
+    k = max(1, min(k, n // 4))
+    return (width or c, L, k, ks)
+
+
+def fno_param_shapes(dim: int, c: int, L: int, k: int, ks: int) -> List[Tuple[str, Tuple[int, ...]]]:
+    """Flat parameter order (the ABI's, nmg.h nmg_load_fno_weights):
+    lift.w [c][1], lift.b [c]; per Fourier layer: spectral R ([k][c_in][c_out][re,im] in 1D,
+    [2k][k][c_in][c_out][re,im] in 2D: i2-mode rows 0..k-1 then n-k..n-1, i1-modes 0..k-1),
+    conv W [c_out][c_in][ks](x ks), bias [c]; proj.w [1][c], proj.b [1]."""
+    spec = (k, c, c, 2) if dim == 1 else (2 * k, k, c, c, 2)
+    conv = (c, c, ks) if dim == 1 else (c, c, ks, ks)
+    out = [("lift_w", (c, 1)), ("lift_b", (c,))]
+    for i in range(L):
+        out += [(f"spec{i}", spec), (f"conv{i}", conv), (f"bias{i}", (c,))]
+    out += [("proj_w", (1, c)), ("proj_b", (1,))]
+    return out
+
+
+def fno_n_params(dim, c, L, k, ks) -> int:
+    return sum(int(np.prod(sh)) for _, sh in fno_param_shapes(dim, c, L, k, ks))
+
+
+def fno_unflatten(dim, c, L, k, ks, flat: np.ndarray) -> dict:
+    out, o = {}, 0
+    for name, sh in fno_param_shapes(dim, c, L, k, ks):
+        m = int(np.prod(sh))
+        out[name] = np.asarray(flat[o:o + m]).reshape(sh)
+        o += m
+    assert o == flat.size
+    return out
+
+
+def fno_weights_seed(cfg: Config, seed: int = 0, width: Optional[int] = None) -> List[np.ndarray]:
+    """W_seed for FNO smoothers, one flat fp32 vector per smoothed level (arch from fno_arch):
+    PyTorch-default-style bounds -- lift / proj / conv U(+-1/sqrt(fan_in)) weights and biases,
+    spectral weights (1/(c c)) U(0, 1) for the real and imaginary parts (the FNO reference
+    initialisation)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for lvl in range(cfg.levels - 1):
+        n = cfg.n >> lvl
+        c, L, k, ks = fno_arch(cfg.dim, n, width)
+        parts = []
+        for name, sh in fno_param_shapes(cfg.dim, c, L, k, ks):
+            if name.startswith("spec"):
+                parts.append(rng.uniform(0.0, 1.0, size=sh) / (c * c))
+            else:
+                fan_in = {"lift_w": 1, "lift_b": 1, "proj_w": c, "proj_b": c}.get(name, c * ks ** cfg.dim)
+                bd = 1.0 / math.sqrt(fan_in)
+                parts.append(rng.uniform(-bd, bd, size=sh))
+        out.append(np.concatenate([p.ravel() for p in parts]).astype(np.float32))
+    return out

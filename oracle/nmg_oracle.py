@@ -144,7 +144,11 @@ def build_hierarchy(dim: int, factors: Sequence[np.ndarray], alpha: float, level
 
 
 def load_weights(H: Hierarchy, level: int, layers) -> None:
-    """Smoother parameters theta_l for level l (1-based, l < L); layers = [(W, b)]."""
+    """Smoother parameters theta_l for level l (1-based, l < L): a CNN as layers = [(W, b)],
+    or an FNO as the dict of fno_params()."""
+    if isinstance(layers, dict):
+        H.weights[level - 1] = layers
+        return
     H.weights[level - 1] = [(np.asarray(w, np.float64), np.asarray(b, np.float64)) for w, b in layers]
 
 
@@ -309,6 +313,86 @@ def cnn_forward(layers, u: np.ndarray) -> np.ndarray:
 
 
 # ==========================================================================
+# FNO smoother (section 3.1; Appendix A; Table 6)
+# ==========================================================================
+# N(u) = proj o f_L o ... o f_1 o lift (u), with the Fourier layer (Appendix A)
+#   f(Z) = sigma( DFT^{-1}( R (.) DFT(Z) ) + W Z + B ),
+# R a learnable complex c x c channel mixing applied to the k lowest frequencies only (the others
+# are zeroed), W a convolution (kernel size per Table 6), B a bias, sigma = GELU (reading R24:
+# the paper leaves sigma unnamed; GELU is the activation of the FNO it builds on), lift / proj
+# pointwise fully connected layers 1 -> c and c -> 1.
+
+def fno_params(dim: int, c: int, L: int, k: int, ks: int, flat: np.ndarray) -> dict:
+    """Unpack the flat fp32 parameter vector (nmg_inputs.fno_param_shapes order) to fp64."""
+    p = {"dim": dim, "c": c, "L": L, "k": k, "ks": ks}
+    o = 0
+    flat = np.asarray(flat, np.float64)
+
+    def take(sh):
+        nonlocal o
+        m = int(np.prod(sh))
+        v = flat[o:o + m].reshape(sh)
+        o += m
+        return v
+    p["lift_w"], p["lift_b"] = take((c, 1))[:, 0], take((c,))
+    spec = (k, c, c, 2) if dim == 1 else (2 * k, k, c, c, 2)
+    conv = (c, c, ks) if dim == 1 else (c, c, ks, ks)
+    p["layers"] = []
+    for _ in range(L):
+        Rr = take(spec)
+        p["layers"].append((Rr[..., 0] + 1j * Rr[..., 1], take(conv), take((c,))))
+    p["proj_w"], p["proj_b"] = take((1, c))[0], take((1,))[0]
+    assert o == flat.size
+    return p
+
+
+def gelu(z: np.ndarray) -> np.ndarray:
+    """sigma(z) = z Phi(z) = z (1 + erf(z / sqrt 2)) / 2 (exact GELU)."""
+    from scipy.special import erf
+    return 0.5 * z * (1.0 + erf(z / math.sqrt(2.0)))
+
+
+def spectral_conv(z: np.ndarray, R: np.ndarray, k: int) -> np.ndarray:
+    """DFT^{-1}(R (.) DFT(z)) with R acting on the k lowest modes per axis only.
+
+    1D: z [B][c][n]; Z = rfft(z)[..., :k]; Y[b,o,m] = sum_c Z[b,c,m] R[m,c,o]; irfft with the
+        modes >= k zero (real output, length n).
+    2D: z [B][c][n2][n1]; Z = rfft2(z) (half spectrum along i1); the kept modes are i1-modes
+        0..k-1 and i2-modes 0..k-1 and n-k..n-1 (R[j2, m1] with j2 < k the low and j2 >= k the
+        high i2-modes); irfft2 with every other mode zero.
+    """
+    if z.ndim == 3:
+        n = z.shape[-1]
+        Z = np.fft.rfft(z, axis=-1)[..., :k]
+        Y = np.einsum("bcm,mco->bom", Z, R)
+        Yp = np.zeros((z.shape[0], R.shape[-1], n // 2 + 1), dtype=complex)
+        Yp[..., :k] = Y
+        return np.fft.irfft(Yp, n=n, axis=-1)
+    n2, n1 = z.shape[-2:]
+    Z = np.fft.rfft2(z, axes=(-2, -1))
+    Zk = np.concatenate([Z[:, :, :k, :k], Z[:, :, n2 - k:, :k]], axis=2)     # [B][c][2k][k]
+    Y = np.einsum("bcjm,jmco->bojm", Zk, R)
+    Yp = np.zeros((z.shape[0], R.shape[-1], n2, n1 // 2 + 1), dtype=complex)
+    Yp[:, :, :k, :k] = Y[:, :, :k]
+    Yp[:, :, n2 - k:, :k] = Y[:, :, k:]
+    return np.fft.irfft2(Yp, s=(n2, n1), axes=(-2, -1))
+
+
+def fno_forward(p: dict, u: np.ndarray) -> np.ndarray:
+    """N_theta(u) of the FNO smoother; u 1D [B][n] or 2D [B][n2][n1] -> same shape."""
+    ex = (None, slice(None)) + (None,) * (u.ndim - 1)
+    z = p["lift_w"][ex] * u[:, None] + p["lift_b"][ex]
+    for R, W, bias in p["layers"]:
+        z = gelu(spectral_conv(z, R, p["k"]) + conv_same(z, W, bias))
+    return np.tensordot(p["proj_w"], z, axes=([0], [1])) + p["proj_b"]
+
+
+def smoother_forward(theta, u: np.ndarray) -> np.ndarray:
+    """N_theta(u) for either smoother family (CNN: list of layers; FNO: dict)."""
+    return fno_forward(theta, u) if isinstance(theta, dict) else cnn_forward(theta, u)
+
+
+# ==========================================================================
 # NMGF cycle (Alg 3 P:315-339 / Alg 4 P:373-401)
 # ==========================================================================
 
@@ -325,7 +409,7 @@ def smoothing_step(H: Hierarchy, l: int, x: np.ndarray, y: np.ndarray) -> np.nda
     s = rhs_norm(b)
     shape = (-1,) + (1,) * (b.ndim - 1)
     safe = np.where(s > 0, s, 1.0).reshape(shape)
-    hv = cnn_forward(H.weights[l], b / safe) * safe
+    hv = smoother_forward(H.weights[l], b / safe) * safe
     hv = np.where(s.reshape(shape) > 0, hv, 0.0)
     if H.level_filter:
         hv = level_filter(H, l, hv)

@@ -24,7 +24,7 @@ EXPORTS = ["nmg_create_hierarchy", "nmg_load_smoother_weights", "nmg_vcycle", "n
            "nmg_vcycles_host", "nmg_residual", "nmg_debug_level_op", "nmg_launch_count",
            "nmg_destroy_hierarchy", "nmg_last_error", "nmg_version", "nmg_profile", "nmg_profile_query",
            "nmg_comm_nccl_unique_id", "nmg_comm_create_nccl", "nmg_comm_create_emulated", "nmg_comm_destroy",
-           "nmg_create_hierarchy_slab"]
+           "nmg_create_hierarchy_slab", "nmg_load_fno_weights"]
 
 KERNEL_CLASSES = ["gemm64", "gemm32", "smooth", "transfer", "coarse", "misc", "filter"]
 
@@ -53,6 +53,10 @@ class CnnArch(C.Structure):
     _fields_ = [("n_layers", C.c_int32), ("channels", C.c_int32), ("ksize", C.c_int32)]
 
 
+class FnoArch(C.Structure):
+    _fields_ = [("width", C.c_int32), ("n_layers", C.c_int32), ("modes", C.c_int32), ("ksize", C.c_int32)]
+
+
 class Report(C.Structure):
     _fields_ = [("cycles", C.POINTER(C.c_int32)), ("converged", C.POINTER(C.c_uint8)),
                 ("history", C.POINTER(C.c_double)), ("wall_seconds", C.c_double),
@@ -75,6 +79,7 @@ def load_library(path: Optional[str] = None):
     vp, i32, f64 = C.c_void_p, C.c_int32, C.c_double
     lib.nmg_create_hierarchy.argtypes = [C.POINTER(ProblemDesc), vp, C.POINTER(vp)]
     lib.nmg_load_smoother_weights.argtypes = [vp, i32, C.POINTER(CnnArch), vp, C.c_size_t]
+    lib.nmg_load_fno_weights.argtypes = [vp, i32, C.POINTER(FnoArch), vp, C.c_size_t]
     lib.nmg_vcycle.argtypes = [vp, i32, vp, vp, vp]
     lib.nmg_solve.argtypes = [vp, i32, vp, vp, f64, i32, C.POINTER(Report), vp]
     lib.nmg_vcycles_host.argtypes = [vp, i32, vp, vp, i32, vp, vp]
@@ -96,7 +101,7 @@ def load_library(path: Optional[str] = None):
     lib.nmg_comm_destroy.argtypes = [vp]
     lib.nmg_comm_destroy.restype = None
     lib.nmg_create_hierarchy_slab.argtypes = [C.POINTER(ProblemDesc), vp, vp, C.POINTER(vp)]
-    for f in ("nmg_create_hierarchy", "nmg_load_smoother_weights", "nmg_vcycle", "nmg_solve",
+    for f in ("nmg_create_hierarchy", "nmg_load_smoother_weights", "nmg_load_fno_weights", "nmg_vcycle", "nmg_solve",
               "nmg_vcycles_host", "nmg_residual", "nmg_debug_level_op", "nmg_comm_nccl_unique_id",
               "nmg_comm_create_nccl", "nmg_comm_create_emulated", "nmg_create_hierarchy_slab"):
         getattr(lib, f).restype = C.c_int
@@ -203,6 +208,12 @@ class Hierarchy:
         p = np.ascontiguousarray(params, dtype=np.float32)
         a = CnnArch(*arch)
         _check(_LIB.nmg_load_smoother_weights(self._h, level, C.byref(a), p.ctypes.data, p.size))
+
+    def load_fno_weights(self, level: int, arch, params: np.ndarray):
+        """arch = (width, n_layers, modes, ksize); params flat fp32 (nmg_inputs.fno_param_shapes)."""
+        p = np.ascontiguousarray(params, dtype=np.float32)
+        a = FnoArch(*arch)
+        _check(_LIB.nmg_load_fno_weights(self._h, level, C.byref(a), p.ctypes.data, p.size))
 
     def vcycle(self, y, x, stream=None):
         _check(_LIB.nmg_vcycle(self._h, y.shape[0], _ptr(y), _ptr(x), _stream(stream)))

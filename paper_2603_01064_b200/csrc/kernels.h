@@ -265,6 +265,34 @@ void strip_combine(int n, int nrhs, const float* q, const double* norms, const f
                    float* x, bool accumulate, cudaStream_t s, int hg = 0, int hh = 0);
 
 
+// ---- FNO smoother (fno.cu; Appendix A, Table 6) -------------------------------
+struct FnoLayer {
+  const float2* R;            // spectral weights [modes][c_in][c_out] complex
+  const float* W;             // W convolution [c_out][c_in][ks](x ks)
+  const float* B;             // bias [c]
+};
+struct FnoArgs {
+  int dim, n, nrhs, c, L, k, ks;
+  const float* in;            // b [nrhs][N]
+  const double* norms;        // ||b|| per RHS (null: 1, the debug CNN op)
+  const float* lift_w;        // [c]
+  const float* lift_b;        // [c]
+  const float* proj_w;        // [c]
+  float proj_b;
+  FnoLayer layer[8];
+  float* Z0; float* Z1;       // activations [nrhs][c][N]
+  float2* T;                  // 2D: [nrhs][c][n][k]
+  float2* Zh; float2* Yh;     // [nrhs][modes][c]
+  const float2* tw; int tw_n;
+  // output: 1D x (+)= ||b|| F'(h) (filter) or ||b|| h; 2D: Zf (level-filter input, zput) when set,
+  // else x (+)= ||b|| h
+  float* x; bool accumulate, filter;
+  float2* Zf = nullptr; int zb0 = 0;
+};
+void fno_forward(const FnoArgs& a, cudaStream_t s);
+int fno_launches(int dim, int L);
+size_t fno_conv_smem(int dim, int c, int ks);
+
 // ---- slab-sharded single-system mode (slab.cu): slabs of R rows + H halo rows per image --
 void restrict_slab(int nrhs, int n_c, int Rc, int r0c, const float* f, int64_t fimg, int64_t foff, float* c,
                    int64_t cimg, int64_t coff, cudaStream_t s);

@@ -375,6 +375,12 @@ struct nmg_hierarchy {
   DevBuf<double> Ainv;                                   // explicit A_L^{-1} (default coarse apply)
   bool coarse_inv = true;
   int nc = 0;
+  // FNO smoothers (nmg_load_fno_weights): per level arch + device parameters; shared workspaces
+  struct FnoLevel { nmg_fno_arch arch{}; DevBuf<float> p; float proj_b = 0.f; };
+  std::vector<std::unique_ptr<FnoLevel>> fno;            // null = the level has a CNN
+  DevBuf<float> fz0, fz1;
+  DevBuf<float2> fT, fZh, fYh;
+  int fno_chunk = 0;
   // smoother weights per level
   std::vector<std::unique_ptr<DevBuf<float>>> W;
   std::vector<int> w_loaded;
@@ -500,8 +506,63 @@ void launch_smooth1d(nmg_hierarchy* h, int l, Smooth1dArgs& a, cudaStream_t s) {
   }
 }
 
+// FNO smoother at level l (NEXT-2): x (+)= ||b|| F'_l(N(b / ||b||)) in RHS chunks (normalize =
+// false: the raw network output of the debug CNN op; filter = false: no F').  norms: ||b|| per
+// RHS already in h->snorm when normalize.
+nmg_status run_fno(nmg_hierarchy* h, int l, int nrhs, const float* b, float* x, bool normalize, bool filter,
+                   bool accumulate, cudaStream_t s) {
+  const nmg_hierarchy::FnoLevel& F = *h->fno[l];
+  const nmg_fno_arch& ar = F.arch;
+  const int dim = h->d.dim, n = h->n[l], c = ar.width, k = ar.modes, ks = ar.ksize;
+  const int64_t N = h->N[l];
+  const float* P = F.p.p;
+  FnoArgs a{};
+  a.dim = dim; a.n = n; a.c = c; a.L = ar.n_layers; a.k = k; a.ks = ks;
+  a.lift_w = P; a.lift_b = P + c;
+  size_t off = 2 * (size_t)c;
+  const size_t spec = (dim == 1 ? (size_t)k : (size_t)2 * k * k) * c * c * 2;
+  const size_t conv = (size_t)c * c * (dim == 1 ? ks : ks * ks);
+  for (int i = 0; i < ar.n_layers; ++i) {
+    a.layer[i].R = reinterpret_cast<const float2*>(P + off); off += spec;
+    a.layer[i].W = P + off; off += conv;
+    a.layer[i].B = P + off; off += c;
+  }
+  a.proj_w = P + off;
+  a.proj_b = F.proj_b;
+  a.Z0 = h->fz0.p; a.Z1 = h->fz1.p; a.T = h->fT.p; a.Zh = h->fZh.p; a.Yh = h->fYh.p;
+  a.tw = h->tw.p; a.tw_n = h->tw_n;
+  a.filter = filter && h->d.level_filter != 0;
+  a.accumulate = accumulate;
+  const bool zf = dim == 2 && a.filter;
+  for (int r0 = 0; r0 < nrhs; r0 += h->fno_chunk) {
+    const int cnt = std::min(h->fno_chunk, nrhs - r0);
+    a.nrhs = cnt;
+    a.in = b + (int64_t)r0 * N;
+    a.norms = normalize ? h->snorm.p + r0 : nullptr;
+    a.x = x + (int64_t)r0 * N;
+    a.Zf = zf ? h->Z.p : nullptr;
+    a.zb0 = r0;
+    { Prof p(h, NMG_K_SMOOTH, s, fno_launches(dim, ar.n_layers)); fno_forward(a, s); }
+    NMG_TRY(check_launch(h));
+  }
+  if (zf) {
+    { Prof p(h, NMG_K_FILTER, s, 3);
+      filter2d(nrhs, n, h->Z.p, h->tw.p, h->tw_n, x, accumulate, s, normalize ? h->snorm.p : nullptr); }
+    NMG_TRY(check_launch(h));
+  }
+  return NMG_OK;
+}
+
 nmg_status smooth_level(nmg_hierarchy* h, int l, int nrhs, const float* b, float* x, bool accumulate,
                         cudaStream_t s) {
+  if (h->fno.size() > (size_t)l && h->fno[l]) {
+    const int n = h->n[l];
+    { Prof p(h, NMG_K_FILTER, s, 2); norms_f32(nrhs, n, b, h->spart.p, 1, h->snorm.p, s); }
+    NMG_TRY(check_launch(h));
+    NMG_TRY(run_fno(h, l, nrhs, b, x, true, true, accumulate, s));
+    if (h->split_fresh.size() > (size_t)l) h->split_fresh[l] = 0;
+    return NMG_OK;
+  }
   Smooth1dArgs a{};
   a.n = h->n[l]; a.nrhs = nrhs;
   a.b = b; a.ldb = a.n;
@@ -709,6 +770,7 @@ nmg_status smooth2d(nmg_hierarchy* h, int l, int nrhs, const float* b, float* x,
     NMG_TRY(check_launch(h));
   }
   const bool filt = filter && h->d.level_filter != 0;
+  if (h->fno.size() > (size_t)l && h->fno[l]) return run_fno(h, l, nrhs, b, x, normalize, filter, accumulate, s);
   if (h->conv_bf && strip_level(n) && h->bf_C == h->arch.channels) {
     const int C = h->arch.channels;
     const float* P = h->W[l]->p;
@@ -1960,8 +2022,61 @@ nmg_status nmg_load_smoother_weights(nmg_hierarchy* h, int32_t level, const nmg_
     }
   }
   h->w_loaded[level - 1] = 1;
+  if (h->fno.size() > (size_t)(level - 1)) h->fno[level - 1].reset();   // the CNN replaces an FNO
   for (auto& hk : h->lanes) NMG_TRY(nmg_load_smoother_weights(hk.get(), level, arch, params, n_params));
   h->arch = *arch;
+  return NMG_OK;
+}
+
+nmg_status nmg_load_fno_weights(nmg_hierarchy* h, int32_t level, const nmg_fno_arch* arch, const float* params,
+                                size_t n_params) {
+  g_err.clear();
+  if (!h || !arch || !params) return fail(NMG_ERR_INVALID_ARG, "null argument");
+  if (level < 1 || level > h->L - 1) return fail(NMG_ERR_INVALID_ARG, "level %d outside 1..%d", level, h->L - 1);
+  if (h->slab) return fail(NMG_ERR_UNSUPPORTED, "FNO smoothers are not available on a slab-sharded handle");
+  const int dim = h->d.dim, n = h->n[level - 1];
+  const int c = arch->width, L = arch->n_layers, k = arch->modes, ks = arch->ksize;
+  if (c < 1 || c > 64 || L < 1 || L > 8 || ks < 1 || ks > 7 || (ks & 1) == 0 || k < 1 || (k & (k - 1)) ||
+      4 * k > n || n > 4096)
+    return fail(NMG_ERR_UNSUPPORTED, "FNO arch (width %d, layers %d, modes %d, ksize %d) not supported at n = %d", c, L,
+                k, ks, n);
+  const size_t spec = (dim == 1 ? (size_t)k : (size_t)2 * k * k) * c * c * 2;
+  const size_t conv = (size_t)c * c * (dim == 1 ? ks : ks * ks);
+  const size_t want = 2 * (size_t)c + L * (spec + conv + c) + c + 1;
+  if (n_params != want) return fail(NMG_ERR_SHAPE, "expected %zu FNO parameters, got %zu", want, n_params);
+  NMG_CUDA(cudaSetDevice(h->d.device));
+  NMG_CUDA(cudaDeviceSynchronize());
+  drop_graphs(h);
+  if (h->fno.size() < (size_t)h->L) h->fno.resize(h->L);
+  std::unique_ptr<nmg_hierarchy::FnoLevel> F(new nmg_hierarchy::FnoLevel());
+  F->arch = *arch;
+  F->proj_b = params[n_params - 1];
+  NMG_TRY(F->p.upload(params, n_params));
+  h->fno[level - 1] = std::move(F);
+  // workspaces for the largest FNO level: RHS chunks with <= 2 GiB of activations per buffer
+  int64_t per = 0, tper = 0, hper = 0;
+  for (int l = 0; l < h->L - 1; ++l) {
+    if (!h->fno[l]) continue;
+    const nmg_fno_arch& a = h->fno[l]->arch;
+    per = std::max<int64_t>(per, (int64_t)a.width * h->N[l]);
+    if (dim == 2) tper = std::max<int64_t>(tper, (int64_t)a.width * h->n[l] * a.modes);
+    hper = std::max<int64_t>(hper, (int64_t)a.width * (dim == 1 ? a.modes : 2 * a.modes * a.modes));
+  }
+  const int64_t B = h->d.max_rhs;
+  const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(B, ((int64_t)1 << 29) / per));
+  if (chunk != h->fno_chunk || (int64_t)h->fz0.n < chunk * per || (int64_t)h->fZh.n < chunk * hper ||
+      (int64_t)h->fT.n < chunk * tper) {
+    h->fno_chunk = chunk;
+    NMG_TRY(h->fz0.alloc((size_t)chunk * per));
+    NMG_TRY(h->fz1.alloc((size_t)chunk * per));
+    NMG_TRY(h->fZh.alloc((size_t)chunk * hper));
+    NMG_TRY(h->fYh.alloc((size_t)chunk * hper));
+    if (tper) NMG_TRY(h->fT.alloc((size_t)chunk * tper));
+  }
+  if (!h->snorm.p) NMG_TRY(h->snorm.alloc(B));
+  if (!h->spart.p) NMG_TRY(h->spart.alloc(B * 64));
+  h->w_loaded[level - 1] = 1;
+  for (auto& hk : h->lanes) NMG_TRY(nmg_load_fno_weights(hk.get(), level, arch, params, n_params));
   return NMG_OK;
 }
 
@@ -2208,6 +2323,10 @@ nmg_status nmg_debug_level_op(nmg_hierarchy* h, int32_t level, int32_t op, int32
     case NMG_OP_CNN:
     case NMG_OP_SMOOTH: {
       if (!smoothed || !h->w_loaded[l]) return fail(NMG_ERR_NO_WEIGHTS, "no smoother at level %d", level);
+      if (h->fno.size() > (size_t)l && h->fno[l]) {
+        if (op == NMG_OP_SMOOTH) return smooth_level(h, l, nrhs, fin, fout, true, s);
+        return run_fno(h, l, nrhs, fin, fout, false, false, false, s);
+      }
       Smooth1dArgs a{};
       a.n = n; a.nrhs = nrhs; a.b = fin; a.ldb = n; a.x = fout; a.ldx = n;
       a.params = h->W[l]->p; a.twiddle = h->tw.p; a.tw_n = h->tw_n;

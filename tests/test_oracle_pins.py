@@ -466,3 +466,100 @@ def test_cfg0_wlin_converges_wseed_stagnates():
     H2, _ = _hier(cfg, weights="seed")
     rep2 = O.solve(H2, y, max_cycles=10, freeze=False)
     assert np.all(rep2.history[:, 10] > 1e-4)
+
+
+# ------------------------------------------------------------------ FNO smoother (NEXT-2)
+def _dft_spectral_bruteforce_1d(z, R, k):
+    """DFT^{-1}(R (.) DFT(z)) from the DFT definition: Z_m = sum_p z_p e^{-2 pi i m p / n} for the
+    kept modes m < k, Y_m = sum_c Z_m[c] R[m, c, o], and the real inverse of the Hermitian
+    spectrum that has Y at +m, conj(Y) at -m and zeros elsewhere:
+    x_p = (Re Y_0 + 2 sum_{0<m<k} Re(Y_m e^{2 pi i m p / n})) / n."""
+    B, c, n = z.shape
+    out = np.zeros((B, R.shape[2], n))
+    for b in range(B):
+        for m in range(k):
+            Zm = np.array([sum(z[b, ch, p] * np.exp(-2j * np.pi * m * p / n) for p in range(n)) for ch in range(c)])
+            Ym = Zm @ R[m]
+            for p in range(n):
+                w = 1.0 if m == 0 else 2.0
+                out[b, :, p] += w * np.real(Ym * np.exp(2j * np.pi * m * p / n)) / n
+    return out
+
+
+def test_fno_spectral_conv_1d_bruteforce():
+    rng = np.random.default_rng(21)
+    z = rng.standard_normal((2, 3, 8))
+    R = rng.standard_normal((3, 3, 2)) + 1j * rng.standard_normal((3, 3, 2))
+    got = O.spectral_conv(z, R, 3)
+    want = _dft_spectral_bruteforce_1d(z, R, 3)
+    assert np.abs(got - want).max() < 1e-12
+
+
+def test_fno_spectral_conv_2d_bruteforce():
+    """2D: kept modes i1 in {0..k-1} x i2 in {0..k-1} U {n-k..n-1}; brute force over the full
+    complex 2D DFT with the Hermitian completion (i1-mode -m1 paired with i2-mode -m2)."""
+    rng = np.random.default_rng(22)
+    n, k, c = 8, 2, 2
+    z = rng.standard_normal((1, c, n, n))
+    R = rng.standard_normal((2 * k, k, c, 2)) + 1j * rng.standard_normal((2 * k, k, c, 2))
+    got = O.spectral_conv(z, R, k)
+    i2 = np.arange(n)[:, None]
+    i1 = np.arange(n)[None, :]
+    full = np.zeros((2, n, n), dtype=complex)      # full spectrum of the output channels
+    for j2 in range(2 * k):
+        m2 = j2 if j2 < k else n - 2 * k + j2
+        for m1 in range(k):
+            E = np.exp(-2j * np.pi * (m2 * i2 + m1 * i1) / n)
+            Zm = np.array([(z[0, ch] * E).sum() for ch in range(c)])
+            Y = Zm @ R[j2, m1]
+            full[:, m2, m1] += Y
+            if m1 > 0:      # Hermitian partner of an i1-mode > 0 (not stored in the half spectrum)
+                full[:, (-m2) % n, (-m1) % n] += np.conj(Y)
+    # the i1-mode-0 column keeps only its real-symmetric part (irfft drops Im of that column's
+    # inverse along i1): (Y + conj Y(-m2)) / 2 per i2-mode pair
+    col0 = full[:, :, 0].copy()
+    full[:, :, 0] = 0.5 * (col0 + np.conj(col0[:, (-np.arange(n)) % n]))
+    want = np.zeros((2, n, n))
+    for m2 in range(n):
+        for m1 in range(n):
+            want += np.real(full[:, m2, m1][:, None, None] * np.exp(2j * np.pi * (m2 * i2 + m1 * i1) / n)) / n ** 2
+    assert np.abs(got[0] - want).max() < 1e-12
+
+
+@pytest.mark.parametrize("dim", [1, 2])
+def test_fno_forward_vs_torch(dim):
+    """The oracle FNO (numpy FFTs, tensordot convs, erf GELU) against an independent torch
+    composition (torch.fft, conv1d/conv2d, torch GELU) on seeded weights."""
+    torch = pytest.importorskip("torch")
+    import torch.nn.functional as F
+    n = 32 if dim == 1 else 16
+    c, L, k, ks = (8, 2, 5, 5) if dim == 1 else (6, 2, 3, 3)
+    cfg = ni.CONFIGS[0 if dim == 1 else 2].replace(n=n, levels=2)
+    flat = ni.fno_weights_seed(cfg, seed=5, width=c)[0]
+    c0, L0, k0, ks0 = ni.fno_arch(dim, n, c)
+    P = ni.fno_unflatten(dim, c0, L0, k0, ks0, flat)
+    p = O.fno_params(dim, c0, L0, k0, ks0, flat)
+    rng = np.random.default_rng(3)
+    u = rng.standard_normal((2,) + (n,) * dim)
+    ours = O.fno_forward(p, u)
+    t = lambda a: torch.tensor(np.asarray(a, np.float64))   # noqa: E731
+    z = F.linear(t(u)[..., None], t(P["lift_w"]), t(P["lift_b"])).movedim(-1, 1)
+    for i in range(L0):
+        Rr = t(P[f"spec{i}"])
+        Rc = torch.complex(Rr[..., 0], Rr[..., 1])
+        if dim == 1:
+            Z = torch.fft.rfft(z, dim=-1)[..., :k0]
+            Yp = torch.zeros(z.shape[0], c0, n // 2 + 1, dtype=torch.complex128)
+            Yp[..., :k0] = torch.einsum("bcm,mco->bom", Z, Rc)
+            s = torch.fft.irfft(Yp, n=n, dim=-1)
+            w = F.conv1d(z, t(P[f"conv{i}"]), t(P[f"bias{i}"]), padding=ks0 // 2)
+        else:
+            Z = torch.fft.rfft2(z)
+            Yp = torch.zeros(z.shape[0], c0, n, n // 2 + 1, dtype=torch.complex128)
+            Yp[:, :, :k0, :k0] = torch.einsum("bcjm,jmco->bojm", Z[:, :, :k0, :k0], Rc[:k0])
+            Yp[:, :, n - k0:, :k0] = torch.einsum("bcjm,jmco->bojm", Z[:, :, n - k0:, :k0], Rc[k0:])
+            s = torch.fft.irfft2(Yp, s=(n, n))
+            w = F.conv2d(z, t(P[f"conv{i}"]), t(P[f"bias{i}"]), padding=ks0 // 2)
+        z = F.gelu(s + w)
+    ref = (F.linear(z.movedim(1, -1), t(P["proj_w"]), t(P["proj_b"]))[..., 0]).numpy()
+    assert np.abs(ours - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max())
