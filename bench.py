@@ -195,6 +195,8 @@ def main():
     ap.add_argument("--alpha", type=float, default=None, help="override the config's alpha (sweep points)")
     ap.add_argument("--nrhs", type=int, default=None)
     ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--precision", choices=["auto", "mixed", "fp64"], default="auto",
+                    help="auto: fp64 cycle for config 0 (BASELINE's fp64 system), mixed otherwise")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--slab", choices=["auto", "on", "off"], default="auto",
@@ -299,8 +301,9 @@ def main():
     W = ni.weights_seed(cfg)
     if B == 0:
         raise SystemExit(f"rank {rank}: no RHS left for this rank ({cfg.nrhs} RHS over {world} ranks)")
+    prec = nmg.PREC_FP64 if args.precision == "fp64" or (args.precision == "auto" and cid == 0) else nmg.PREC_MIXED
     h = nmg.Hierarchy(cfg.dim, cfg.n, cfg.levels, cfg.alpha, factors, nu1=cfg.nu1, nu2=cfg.nu2, max_rhs=B,
-                      device=local, comm=comm)
+                      device=local, comm=comm, precision=prec)
     for l, w in enumerate(W):
         h.load_weights(l + 1, ni.cnn_arch(cfg), w)
     y_np = make_y(B, start)
@@ -437,28 +440,40 @@ def main():
                "check_vs_device_entry_max_rel_diff": diff}
         del yh, xh, xd
 
-    # ---- RHS solved to 1e-6 / s with converging stand-in weights (alpha = 1e-2)
+    # ---- RHS solved to 1e-6 / s with converging weights: the trained smoothers W_train
+    # (trainer/nmg_train.py, Alg 5) for this config and alpha when present, else (1D) the W_lin
+    # stand-in at the largest alpha of the sweep where it converges
     solve = None
-    if not args.no_solve and cfg.dim == 1:
-        scfg = cfg.replace(alpha=1e-2 if cid == 1 else cfg.alpha)
-        sf = ni.operator_factors(scfg)
-        hs = nmg.Hierarchy(1, scfg.n, scfg.levels, scfg.alpha, sf, nu1=scfg.nu1, nu2=scfg.nu2, max_rhs=B,
-                           device=local)
-        for l, w in enumerate(ni.weights_lin(scfg)):
-            hs.load_weights(l + 1, ni.cnn_arch(scfg), w)
-        ys_np, _ = ni.make_rhs(scfg, sf, scfg.alpha, nrhs=B, start=start)
-        ys = torch.tensor(ys_np, dtype=torch.float64, device=dev)
-        xs = torch.zeros_like(ys)
-        hs.solve(ys, xs, tol=1e-6, max_cycles=100, stream=stream)   # warm
-        xs.zero_()
-        barrier()
-        torch.cuda.synchronize(dev)
-        rep = hs.solve(ys, xs, tol=1e-6, max_cycles=100, stream=stream)
-        sec = max_over_ranks(rep["wall_seconds"])
-        solve = {"value": world * int(rep["converged"].sum()) / sec, "unit": "RHS solved/s (relres<=1e-6)",
-                 "alpha": scfg.alpha, "weights": "W_lin stand-in", "cycles_max": int(rep["cycles"].max()),
-                 "cycles_mean": float(rep["cycles"].mean()), "converged": int(rep["converged"].sum()),
-                 "seconds": sec}
+    if not args.no_solve:
+        wt = ni.weights_trained(cfg)
+        scfg, label = cfg, "W_train (level-wise trainer, Alg 5)"
+        if wt is None and cfg.dim == 1:
+            scfg = cfg.replace(alpha=max(ni.ALPHAS[cid]))
+            wt, label = ni.weights_lin(scfg), "W_lin stand-in"
+        if wt is not None:
+            sf = ni.operator_factors(scfg)
+            hs = nmg.Hierarchy(cfg.dim, scfg.n, scfg.levels, scfg.alpha, sf, nu1=scfg.nu1, nu2=scfg.nu2, max_rhs=B,
+                               device=local, precision=prec)
+            for l, w in enumerate(wt):
+                hs.load_weights(l + 1, ni.cnn_arch(scfg), w)
+            if scfg.alpha == cfg.alpha:
+                ys = y
+            else:
+                ys = torch.tensor(make_y(B, start), dtype=torch.float64, device=dev)
+            xs = torch.zeros_like(ys)
+            hs.solve(ys, xs, tol=1e-6, max_cycles=100, stream=stream)   # warm (graph capture)
+            xs.zero_()
+            barrier()
+            torch.cuda.synchronize(dev)
+            rep = hs.solve(ys, xs, tol=1e-6, max_cycles=100, stream=stream)
+            sec = max_over_ranks(rep["wall_seconds"])
+            conv = int(rep["converged"].sum())
+            solve = {"value": (world if not strong else 1) * conv / sec * (world if strong else 1),
+                     "unit": "RHS solved/s (relres<=1e-6)", "alpha": scfg.alpha, "weights": label,
+                     "cycles_max": int(rep["cycles"].max()), "cycles_mean": float(rep["cycles"].mean()),
+                     "converged": conv, "of": B, "seconds": sec}
+            hs.close()
+            del xs
 
     # ---- CPU oracle baseline (rank 0, N = 1 only; bounded sample)
     cpu = None

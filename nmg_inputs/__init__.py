@@ -401,3 +401,27 @@ def fno_weights_seed(cfg: Config, seed: int = 0, width: Optional[int] = None) ->
                 parts.append(rng.uniform(-bd, bd, size=sh))
         out.append(np.concatenate([p.ravel() for p in parts]).astype(np.float32))
     return out
+
+
+# --------------------------------------------------------------------------
+# W_train: smoothers trained by trainer/nmg_train.py (Alg 5, NEXT-1), committed as data
+# --------------------------------------------------------------------------
+TRAINED_DIR = __import__("os").path.join(__import__("os").path.dirname(__file__), "trained")
+
+
+def trained_path(cfg: Config) -> str:
+    import os
+    return os.path.join(TRAINED_DIR, f"W_train_{cfg.name}_a{cfg.alpha:g}.npz")
+
+
+def weights_trained(cfg: Config) -> Optional[List[np.ndarray]]:
+    """W_train for (config, alpha) if the trainer's output is present, else None."""
+    import os
+    p = trained_path(cfg)
+    if not os.path.exists(p):
+        return None
+    with np.load(p) as z:
+        w = z["weights"]
+    if w.shape != (cfg.levels - 1, n_params(cfg)):
+        return None
+    return [np.ascontiguousarray(v, dtype=np.float32) for v in w]

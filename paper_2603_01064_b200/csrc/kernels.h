@@ -293,6 +293,25 @@ void fno_forward(const FnoArgs& a, cudaStream_t s);
 int fno_launches(int dim, int L);
 size_t fno_conv_smem(int dim, int c, int ks);
 
+// ---- NMG_PREC_FP64: the whole cycle of one RHS per CTA in one launch (cycle64.cu; 1D, n <= 1024)
+struct Cycle64Args {
+  int n, L, nrhs, nu1, nu2;
+  bool filter;
+  const double* A[8];         // fp64 Galerkin operators of the smoothed levels 0 .. L-2 (A[0] = G + alpha I)
+  const double* Ainv;         // fp64 (A^(L))^{-1}
+  const float* W[8];          // CNN parameters per smoothed level (state_dict order)
+  const double* y;            // [nrhs][n]
+  double* x;                  // [nrhs][n], in/out
+  double* relres;             // [nrhs] or null
+  double tol;
+  const uint8_t* active_in;   // null: every RHS cycles
+  uint8_t* active_out;        // null or [nrhs]: relres > tol
+  bool do_cycle;              // run the cycle (else only the relative residual)
+  bool relres_after;          // relres of the output x (nmg_solve) instead of the input x (nmg_vcycle)
+};
+size_t cycle64_smem(int n, int L);
+void cycle64(const Cycle64Args& a, cudaStream_t s);
+
 // ---- slab-sharded single-system mode (slab.cu): slabs of R rows + H halo rows per image --
 void restrict_slab(int nrhs, int n_c, int Rc, int r0c, const float* f, int64_t fimg, int64_t foff, float* c,
                    int64_t cimg, int64_t coff, cudaStream_t s);

@@ -316,6 +316,7 @@ struct nmg_hierarchy {
   std::vector<int64_t> N;  // unknowns per level
   // level-1 fp64 operator (1D: A; 2D: B, C)
   DevBuf<double> A64, B64, C64;
+  std::vector<std::unique_ptr<DevBuf<double>>> A64l;     // NMG_PREC_FP64: fp64 A_l, levels 1 .. L-2
   // per smoothed level (l < L-1) fp32 operators (SIMT path) and tf32 hi/lo splits (tcgen05)
   std::vector<std::unique_ptr<DevBuf<float>>> A32, AP32, A32h, A32l, AP32h, AP32l;
   std::vector<CUtensorMap> mAh, mAl, mAPh, mAPl;        // W operand maps per level (box 256)
@@ -1282,12 +1283,30 @@ void drop_graphs(nmg_hierarchy* h) {
   for (auto& hk : h->lanes) drop_graphs(hk.get());
 }
 
+// NMG_PREC_FP64: one fused launch (cycle64.cu)
+nmg_status cycle_fp64(nmg_hierarchy* h, int nrhs, const double* y, double* x, bool do_cycle, bool relres_after,
+                      double tol, const uint8_t* active_in, uint8_t* active_out, cudaStream_t s) {
+  Cycle64Args a{};
+  a.n = h->d.n; a.L = h->L; a.nrhs = nrhs; a.nu1 = h->d.nu1; a.nu2 = h->d.nu2; a.filter = h->d.level_filter != 0;
+  for (int l = 0; l < h->L - 1; ++l) {
+    a.A[l] = l == 0 ? h->A64.p : h->A64l[l - 1]->p;
+    a.W[l] = h->W[l]->p;
+  }
+  a.Ainv = h->Ainv.p;
+  a.y = y; a.x = x; a.relres = h->relres.p; a.tol = tol;
+  a.active_in = active_in; a.active_out = active_out;
+  a.do_cycle = do_cycle; a.relres_after = relres_after;
+  { Prof p(h, NMG_K_SMOOTH, s); cycle64(a, s); }
+  return check_launch(h);
+}
+
 // allow_lanes = false: the whole batch runs on this handle alone (the host-buffer pipeline runs
 // its lane 0 this way while lanes 1..K-1 cycle their own RHS on the lane handles concurrently,
 // so a lane handle is never used by two graphs at once).
 nmg_status graph_cycle(nmg_hierarchy* h, int nrhs, const double* y, double* x, cudaStream_t s,
                        bool allow_lanes = true) {
   auto body = [&]() -> nmg_status {
+    if (h->d.precision == NMG_PREC_FP64) return cycle_fp64(h, nrhs, y, x, true, false, -1.0, nullptr, nullptr, s);
     const int K = (int)h->lanes.size() + 1;
     const int gr = h->d.dim == 1 ? 128 : 2;             // lane granularity (1D: GEMM M tiles)
     if (K == 1 || !allow_lanes || h->prof_on || nrhs < K * gr || s == nullptr) {
@@ -1488,6 +1507,10 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
       }
       host_restrict_rows(AP, nl, nl / 2, Ac);           // R A P
       A.swap(Ac);
+      if (d.precision == NMG_PREC_FP64 && l + 1 < h->L - 1) {
+        h->A64l.emplace_back(new DevBuf<double>());
+        NMG_TRY(h->A64l.back()->upload(A.data(), A.size()));
+      }
     }
     Acoarse = A;
   } else {
@@ -1541,7 +1564,7 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
   NMG_TRY(h->Lcol.upload(Lt.data(), Lt.size()));
   {
     // explicit inverse A_L^{-1} = L^{-T} L^{-1} (fp64, symmetric), column by column
-    h->coarse_inv = h->tune.coarse_subst == 0;
+    h->coarse_inv = h->tune.coarse_subst == 0 || d.precision == NMG_PREC_FP64;
     if (h->coarse_inv) {
       std::vector<double> inv((size_t)Nc * Nc), z(Nc);
       for (int j = 0; j < Nc; ++j) {
@@ -1736,7 +1759,7 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
   NMG_TRY(h->active.alloc(B));
   {
     const int tl = h->tune.lanes;
-    int K = t_no_lanes ? 1 : tl > 0 ? std::min(8, tl) : 4;
+    int K = (t_no_lanes || d.precision == NMG_PREC_FP64) ? 1 : tl > 0 ? std::min(8, tl) : 4;
     if (d.dim != 1 && K > 1) {
       // 2D: two lanes by default while the batch is small enough that a second set of lane
       // workspaces is cheap (cfg 2, 4: same device time, the host entry overlaps more)
@@ -1768,7 +1791,7 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
       }
     }
   }
-  if (!t_no_lanes && d.precision == NMG_PREC_MIXED) {
+  if (!t_no_lanes) {
     // staging and copy streams of the host-buffer entry nmg_vcycles_host (no lazy allocation)
     const size_t cnt = (size_t)d.max_rhs * h->N[0];
     NMG_TRY(h->hy.alloc(cnt));
@@ -2034,6 +2057,7 @@ nmg_status nmg_load_fno_weights(nmg_hierarchy* h, int32_t level, const nmg_fno_a
   if (!h || !arch || !params) return fail(NMG_ERR_INVALID_ARG, "null argument");
   if (level < 1 || level > h->L - 1) return fail(NMG_ERR_INVALID_ARG, "level %d outside 1..%d", level, h->L - 1);
   if (h->slab) return fail(NMG_ERR_UNSUPPORTED, "FNO smoothers are not available on a slab-sharded handle");
+  if (h->d.precision == NMG_PREC_FP64) return fail(NMG_ERR_UNSUPPORTED, "FNO smoothers run in the mixed-precision cycle only");
   const int dim = h->d.dim, n = h->n[level - 1];
   const int c = arch->width, L = arch->n_layers, k = arch->modes, ks = arch->ksize;
   if (c < 1 || c > 64 || L < 1 || L > 8 || ks < 1 || ks > 7 || (ks & 1) == 0 || k < 1 || (k & (k - 1)) ||
@@ -2122,10 +2146,15 @@ nmg_status nmg_solve(nmg_hierarchy* h, int32_t nrhs, const double* y, double* x,
   cudaEvent_t e0, e1;
   NMG_CUDA(cudaEventCreate(&e0));
   NMG_CUDA(cudaEventCreate(&e1));
+  const bool f64 = h->d.precision == NMG_PREC_FP64;
   NMG_CUDA(cudaEventRecord(e0, s));
-  NMG_TRY(ynorms(h, nrhs, y, s));
-  NMG_TRY(outer_residual(h, nrhs, y, x, nullptr, true, s));
-  NMG_TRY(relres_fin(h, nrhs, tol, h->active.p, h->relres.p, s));
+  if (f64) {
+    NMG_TRY(cycle_fp64(h, nrhs, y, x, false, false, tol, nullptr, h->active.p, s));
+  } else {
+    NMG_TRY(ynorms(h, nrhs, y, s));
+    NMG_TRY(outer_residual(h, nrhs, y, x, nullptr, true, s));
+    NMG_TRY(relres_fin(h, nrhs, tol, h->active.p, h->relres.p, s));
+  }
   nmg_status st = NMG_OK;
   int tau = 0;
   for (;; ++tau) {
@@ -2156,9 +2185,13 @@ nmg_status nmg_solve(nmg_hierarchy* h, int32_t nrhs, const double* y, double* x,
       if (rr[b] <= tol) act[b] = 0; else ++nact;
     }
     if (st != NMG_OK || nact == 0 || tau == max_cycles) break;
+    for (int b = 0; b < nrhs; ++b) if (act[b]) cyc[b] = tau + 1;
+    if (f64) {
+      NMG_TRY(cycle_fp64(h, nrhs, y, x, true, true, tol, h->active.p, h->active.p, s));
+      continue;
+    }
     NMG_TRY(inner_cycle(h, nrhs, s));
     NMG_TRY(outer_update(h, nrhs, x, h->active.p, s));
-    for (int b = 0; b < nrhs; ++b) if (act[b]) cyc[b] = tau + 1;
     NMG_TRY(outer_residual(h, nrhs, y, x, nullptr, true, s));
     NMG_TRY(relres_fin(h, nrhs, tol, h->active.p, h->relres.p, s));
   }

@@ -112,3 +112,32 @@ def test_fallback_kernels_match(knob, dim):
     orc = O.solve(H, y, tol=1e-300, max_cycles=3, freeze=False)
     ok, err = history_close(rep["history"], orc.history)
     assert ok, err
+
+
+@pytest.mark.parametrize("kind,tol,cycles", [("seed", 1e-300, 10), ("lin", 1e-10, 60)])
+def test_precision_fp64_cfg0(kind, tol, cycles):
+    """NMG_PREC_FP64 (config 0's fp64 system, reading R14): the fused one-launch fp64 cycle.
+    Histories match the fp64 oracle far below the mixed path's 1e-3 (only the CNN's own fp32
+    arithmetic differs), and with W_lin the solve reaches 1e-10 at the oracle's cycle."""
+    import paper_2603_01064_b200 as nmg
+    cfg = ni.CONFIGS[0]
+    f = ni.operator_factors(cfg)
+    W = weights_for(cfg, kind)
+    H = oracle_hierarchy(cfg, f, W)
+    h = gpu_hierarchy(cfg, f, W, max_rhs=cfg.nrhs, precision=nmg.PREC_FP64)
+    y, _ = ni.make_rhs(cfg, f, cfg.alpha)
+    yd = torch.tensor(y, dtype=torch.float64, device=DEV)
+    xd = torch.zeros_like(yd)
+    rep = h.solve(yd, xd, tol=tol, max_cycles=cycles)
+    orc = O.solve(H, y, tol=tol, max_cycles=cycles, freeze=tol > 1e-100)
+    ok, err = history_close(rep["history"], orc.history, tol=1e-5, floor=1e-12)
+    assert ok, err
+    if kind == "lin":
+        assert rep["converged"].all() and np.array_equal(rep["cycles"], orc.cycles)
+    # nmg_vcycle (graph-captured single launch) equals the solve's cycles
+    x2 = torch.zeros_like(yd)
+    for _ in range(3):
+        h.vcycle(yd, x2)
+    x3 = torch.zeros_like(yd)
+    h.solve(yd, x3, tol=1e-300, max_cycles=3)
+    assert torch.equal(x2, x3)

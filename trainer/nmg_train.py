@@ -278,14 +278,22 @@ def data_generation(lv: TorchLevels, nets, nbs: int, K: int, rng: np.random.Gene
     x = torch.tensor(rng.standard_normal(shape), dtype=lv.dt, device=lv.dev)
     y = lv.apply(0, x)
     ks = rng.integers(1, K + 1, size=nbs)
+    shape_b = (-1,) + (1,) * (x.dim() - 1)
     for j in range(1, K + 1):
         live = torch.tensor(ks >= j, device=lv.dev)
         if not bool(live.any()):
             break
         with torch.no_grad():
             c = rollout(y) if rollout is not None else nmgf0(lv, nets, y, nu1, nu2)
-        shape_b = (-1,) + (1,) * (x.dim() - 1)
-        x = torch.where(live.reshape(shape_b), x - c, x)
+        xn = x - c
+        # a cycle of a still-untrained smoother may diverge: such a sample keeps its last finite
+        # error (and stops rolling); the rest are rescaled to unit norm after every step (the
+        # cycle is positively homogeneous, pin P10), so no rollout overflows
+        nrm = rhs_norm(xn)
+        ok = torch.isfinite(nrm) & (nrm > 0) & live
+        ks = np.where(ok.cpu().numpy(), ks, 0)
+        xn = xn / torch.where(ok, nrm, torch.ones_like(nrm)).reshape(shape_b)
+        x = torch.where(ok.reshape(shape_b), xn, x)
         y = lv.apply(0, x)
     nx = rhs_norm(x).reshape((-1,) + (1,) * (x.dim() - 1))
     nx = torch.where(nx > 0, nx, torch.ones_like(nx))
@@ -311,10 +319,15 @@ def train(cfg, alpha: float, init: List[np.ndarray], epochs: int, nbs: int = 20,
         losses = level_losses(lv, nets, x, y)
         for o in opts:
             o.zero_grad(set_to_none=True)
-        sum(losses).backward()
-        for o, s in zip(opts, scheds):
-            o.step()
-            s.step()
+        total = sum(losses)
+        if bool(torch.isfinite(total)):          # a non-finite batch is skipped, not learned from
+            total.backward()
+            for net in nets:
+                torch.nn.utils.clip_grad_norm_(net.parameters(), 10.0)
+            for o in opts:
+                o.step()
+        for sch in scheds:
+            sch.step()
         hist.append([float(v.detach()) for v in losses])
         if verbose and (ep % log_every == 0 or ep == epochs - 1):
             print(f"  alpha {alpha:g} epoch {ep:5d}  losses " + " ".join(f"{v:.3e}" for v in hist[-1])
