@@ -335,16 +335,23 @@ __global__ void __launch_bounds__(256, 1) cnn2d_kernel(Cnn2dArgs a) {
 //      (the filtered image is real, so Y[n-k1] = conj Y[k1]);
 //   3. inverse row FFTs of W_r give y_2r + i y_2r+1 -> scale 1/n^2 (and ||b||) -> x.
 // The work equals one complex 2D FFT per RHS PAIR, but no two right-hand sides share a buffer.
+// Whole images keep the row spectra in the DIF's bit-reversed order (no permutation pass); the
+// mirror of frequency position p (k1 = bitrev(p)) is the reversal of p inside its dyadic block
+// [2^j, 2^(j+1)): bitrev(n - bitrev(p)) = 3 * 2^j - 1 - p (p >= 2; positions 0 and 1 hold the
+// self-mirrored k1 = 0 and n/2), so a CTA takes a contiguous group of positions and its
+// contiguous mirror group.  The slab mode stores natural-order spectra (its all-to-all deals
+// mirror-closed frequency chunks to the ranks).
 
 // rows: R complex rows of length n per CTA (R n <= 4096 complex in smem), in place in Z.
-// forward: natural in, natural out (the DIF result is read back through bitrev).
-// inverse: natural in (loaded bit-reversed for the DIT pass); complex row Rr = b rpi + r of
-// RHS b writes real rows 2r and 2r + 1 of x at b ximg + xoff + (2r) n + col (rpi = rows / 2).
+// forward: natural in; out bit-reversed (natural = 0) or natural (natural = 1).
+// inverse: in bit-reversed (natural = 0) or natural (natural = 1, loaded bit-reversed for the
+// DIT pass); complex row Rr = b rpi + r of RHS b writes real rows 2r and 2r + 1 of x at
+// b ximg + xoff + (2r) n + col (rpi = rows / 2).
 __global__ void __launch_bounds__(256) fft_rows_kernel(int n, int64_t nrows, float2* __restrict__ Z,
                                                        const float2* __restrict__ tw, int tw_n, int inverse,
                                                        float* __restrict__ x, int accumulate, float scale,
                                                        const double* __restrict__ norms, int rpi, int64_t ximg,
-                                                       int64_t xoff) {
+                                                       int64_t xoff, int natural) {
   extern __shared__ __align__(16) float2 cb[];
   const int R = max(1, 4096 / n);
   const int64_t r0 = (int64_t)blockIdx.x * R;
@@ -357,13 +364,13 @@ __global__ void __launch_bounds__(256) fft_rows_kernel(int n, int64_t nrows, flo
     fft_dif_forward_batch(cb, n, rows, n, 1, tw, tw_n, threadIdx.x, 256);
     for (int i = threadIdx.x; i < tot; i += 256) {
       const int r = i / n, k = i - r * n;
-      Z[r0 * n + i] = cb[r * n + bitrev(k, log2n)];
+      Z[r0 * n + i] = natural ? cb[r * n + bitrev(k, log2n)] : cb[i];
     }
     return;
   }
   for (int i = threadIdx.x; i < tot; i += 256) {
     const int r = i / n, k = i - r * n;
-    cb[r * n + bitrev(k, log2n)] = Z[r0 * n + i];
+    cb[natural ? r * n + bitrev(k, log2n) : i] = Z[r0 * n + i];
   }
   __syncthreads();
   fft_dit_inverse_batch(cb, n, rows, n, 1, tw, tw_n, threadIdx.x, 256);
@@ -414,10 +421,7 @@ __global__ void __launch_bounds__(256) combine_rows_fft_kernel(int n, int nrhs, 
   __syncthreads();
   fft_dif_forward_batch(cb, n, rows, n, 1, tw, tw_n, threadIdx.x, 256);
   float2* Zp = Z + (int64_t)(zb0 + b) * per / 2 + (int64_t)r0 * n;
-  for (int i = threadIdx.x; i < rows * n; i += 256) {
-    const int r = i / n, k = i - r * n;
-    Zp[i] = cb[r * n + bitrev(k, log2n)];
-  }
+  for (int i = threadIdx.x; i < rows * n; i += 256) Zp[i] = cb[i];          // bit-reversed spectra
 }
 
 NMG_D float mask2d(int k1, int k2, int n) {
@@ -450,23 +454,36 @@ NMG_D void unmix(float2 A, float2 B, float2& h0, float2& h1) {
 NMG_D float2 pack_k(float2 y0, float2 y1) { return make_float2(y0.x - y1.y, y0.y + y1.x); }
 NMG_D float2 pack_mirror(float2 y0, float2 y1) { return make_float2(y0.x + y1.y, y1.x - y0.y); }
 
-// whole images: Z_b = [n/2][n]; CTA = (group of G frequencies k1 = g G .. g G + G - 1 of
-// 0 .. n/2 - 1, or the single k1 = n/2 column for the last group, RHS b)
+// whole images: Z_b = [n/2][n] with bit-reversed row spectra.  CTA = (position group, RHS b):
+// group 0 = positions {0, 1} (k1 = 0, n/2; self-mirrored); then for each dyadic block
+// [2^j, 2^(j+1)), j >= 1, its lower half split in groups of Gs = min(G, 2^(j-1)) positions p,
+// each with the mirror positions 3 * 2^j - 1 - p of the upper half.
 __global__ void __launch_bounds__(256) fft_cols_kernel(int n, int G, float2* __restrict__ Z,
                                                        const float2* __restrict__ tw, int tw_n) {
   extern __shared__ __align__(16) float2 cb[];   // [n][Gc]
   __shared__ int k1s[64];
   const int b = blockIdx.y, half = n / 2;
-  const int ng = half / G;                        // full groups; group ng = the k1 = n/2 column
-  const int Gc = blockIdx.x < ng ? G : 1;
-  const int k0 = blockIdx.x < ng ? blockIdx.x * G : half;
+  const int log2n = 31 - __clz(n);
+  int p0 = 0, Gc = 2, S = 1;                      // S = block size (1: the self-mirrored pair)
+  {
+    int g = blockIdx.x;
+    if (g > 0) {
+      --g;
+      for (S = 2; S < n; S <<= 1) {
+        const int cnt = max(1, (S / 2) / G);
+        if (g < cnt) { Gc = min(G, S / 2); p0 = S + g * Gc; break; }
+        g -= cnt;
+      }
+    }
+  }
   float2* Zb = Z + (int64_t)b * half * n;
-  for (int c = threadIdx.x; c < Gc; c += 256) k1s[c] = k0 + c;
+  auto mirror = [&](int p) { return S == 1 ? p : 3 * S - 1 - p; };
+  for (int c = threadIdx.x; c < Gc; c += 256) k1s[c] = bitrev(p0 + c, log2n);
   for (int i = threadIdx.x; i < half * Gc; i += 256) {
     const int r = i / Gc, c = i - r * Gc;
-    const int k = k0 + c, km = (n - k) & (n - 1);
+    const int p = p0 + c;
     float2 h0, h1;
-    unmix(Zb[(int64_t)r * n + k], Zb[(int64_t)r * n + km], h0, h1);
+    unmix(Zb[(int64_t)r * n + p], Zb[(int64_t)r * n + mirror(p)], h0, h1);
     cb[(2 * r) * Gc + c] = h0;
     cb[(2 * r + 1) * Gc + c] = h1;
   }
@@ -474,10 +491,10 @@ __global__ void __launch_bounds__(256) fft_cols_kernel(int n, int G, float2* __r
   cols_filter_tile(cb, n, Gc, k1s, tw, tw_n);
   for (int i = threadIdx.x; i < half * Gc; i += 256) {
     const int r = i / Gc, c = i - r * Gc;
-    const int k = k0 + c;
+    const int p = p0 + c;
     const float2 y0 = cb[(2 * r) * Gc + c], y1 = cb[(2 * r + 1) * Gc + c];
-    Zb[(int64_t)r * n + k] = pack_k(y0, y1);
-    if (k != 0 && k != half) Zb[(int64_t)r * n + (n - k)] = pack_mirror(y0, y1);
+    Zb[(int64_t)r * n + p] = pack_k(y0, y1);
+    if (S > 1) Zb[(int64_t)r * n + mirror(p)] = pack_mirror(y0, y1);
   }
 }
 
@@ -608,13 +625,15 @@ void filter2d(int nrhs, int n, float2* Z, const float2* tw, int tw_n, float* x, 
   const size_t smr = sizeof(float2) * (size_t)R * n;
   if (!rows_done)
     fft_rows_kernel<<<nblk(nrows, R), 256, smr, s>>>(n, nrows, Z, tw, tw_n, 0, nullptr, 0, 1.f, nullptr, n / 2,
-                                                     (int64_t)n * n, 0);
-  const int G = std::min(std::max(1, n / 2), std::min(64, std::max(1, 4096 / n)));   // 32 KB of columns
-  const size_t smc = sizeof(float2) * (size_t)n * G;
+                                                     (int64_t)n * n, 0, 0);
+  const int G = std::min(std::max(1, n / 2), std::min(64, std::max(2, 4096 / n)));   // 32 KB of columns
+  const size_t smc = sizeof(float2) * (size_t)n * std::max(G, 2);
   NMG_SMEM_OPTIN(fft_cols_kernel, 65536);
-  fft_cols_kernel<<<dim3(std::max(1, (n / 2) / G) + 1, nrhs), 256, smc, s>>>(n, G, Z, tw, tw_n);
+  int groups = 1;
+  for (int S = 2; S < n; S <<= 1) groups += std::max(1, (S / 2) / G);
+  fft_cols_kernel<<<dim3(groups, nrhs), 256, smc, s>>>(n, G, Z, tw, tw_n);
   fft_rows_kernel<<<nblk(nrows, R), 256, smr, s>>>(n, nrows, Z, tw, tw_n, 1, x, accumulate ? 1 : 0,
-                                                   1.0f / ((float)n * (float)n), norms, n / 2, (int64_t)n * n, 0);
+                                                   1.0f / ((float)n * (float)n), norms, n / 2, (int64_t)n * n, 0, 0);
 }
 
 // ---------------------------------------------------------------- slab-sharded level filter
@@ -630,7 +649,7 @@ void filter2d_slab_rows(int n, int nrhs, int R, float2* Zs, const float2* tw, in
   const int RR = std::max(1, 4096 / n);
   const size_t smr = sizeof(float2) * (size_t)RR * n;
   fft_rows_kernel<<<nblk(nrows, RR), 256, smr, s>>>(n, nrows, Zs, tw, tw_n, 0, nullptr, 0, 1.f, nullptr, R / 2,
-                                                    (int64_t)R * n, 0);
+                                                    (int64_t)R * n, 0, 1);
 }
 void filter2d_slab_inverse(int n, int nrhs, int R, float2* Zs, const float2* tw, int tw_n, float* x, int64_t ximg,
                            int64_t xoff, bool accumulate, const double* norms, cudaStream_t s) {
@@ -638,7 +657,7 @@ void filter2d_slab_inverse(int n, int nrhs, int R, float2* Zs, const float2* tw,
   const int RR = std::max(1, 4096 / n);
   const size_t smr = sizeof(float2) * (size_t)RR * n;
   fft_rows_kernel<<<nblk(nrows, RR), 256, smr, s>>>(n, nrows, Zs, tw, tw_n, 1, x, accumulate ? 1 : 0,
-                                                    1.0f / ((float)n * (float)n), norms, R / 2, ximg, xoff);
+                                                    1.0f / ((float)n * (float)n), norms, R / 2, ximg, xoff, 1);
 }
 void filter2d_slab_pack(int n, int nrhs, int R, int W, float2* Zs, float2* buf, bool unpack, cudaStream_t s) {
   const int64_t tot = (int64_t)W * nrhs * (R / 2) * filter2d_slab_chunk(n, W);

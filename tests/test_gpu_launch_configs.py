@@ -169,3 +169,51 @@ def test_coarse_substitution_cfg1(cfg1_bench):
     orc = O.solve(H, y, tol=1e-300, max_cycles=4, freeze=False)
     ok, err = history_close(rep["history"], orc.history)
     assert ok, err
+
+
+def _wtrain_keys():
+    p = os.path.join(GOLD, "oracle_wtrain.npz")
+    if not os.path.exists(p):
+        return []
+    with np.load(p) as z:
+        return sorted(k[len("cycles_"):] for k in z.files if k.startswith("cycles_"))
+
+
+@pytest.mark.parametrize("key", _wtrain_keys())
+def test_wtrain_solve_matches_oracle(key):
+    """The trained smoothers W_train (trainer/nmg_train.py, Alg 5) at the bench's launch
+    configuration (full batch; 2D: the tiled pool): the oracle converged on its sample
+    (tools/make_oracle_goldens.py), every GPU RHS converges to 1e-6, and the sampled RHS stop at
+    the oracle's cycle (+-1 per reading R13) with matching histories."""
+    name, a = key.rsplit("_a", 1)
+    alpha = float(a)
+    cid = [c for c, v in ni.CONFIGS.items() if v.name == name][0]
+    cfg = ni.CONFIGS[cid].replace(alpha=alpha)
+    W = ni.weights_trained(cfg)
+    assert W is not None
+    g = gold("oracle_wtrain.npz")
+    oc, oh = g[f"cycles_{key}"], g[f"hist_{key}"]
+    assert g[f"conv_{key}"].all()
+    f = ni.operator_factors(cfg)
+    B = cfg.nrhs
+    if cfg.dim == 1:
+        y, _ = ni.make_rhs(cfg, f, alpha)
+        idx = list(gold("oracle_cfg1_wseed.npz")["idx"])
+    else:
+        pool, _ = ni.make_rhs(cfg, f, alpha, nrhs=8, start=0)
+        y = np.ascontiguousarray(np.concatenate([pool] * (-(-B // 8)))[:B])
+        idx = list(range(len(oc)))
+    h = gpu_hierarchy(cfg, f, W, max_rhs=B)
+    yd = T(y, torch.float64)
+    del y
+    xd = torch.zeros_like(yd)
+    rep = h.solve(yd, xd, tol=1e-6, max_cycles=60)
+    assert rep["converged"].all()
+    ok, err = history_close(rep["history"][idx], oh)
+    assert ok, err
+    for k, b in enumerate(idx):
+        d = abs(int(rep["cycles"][b]) - int(oc[k]))
+        if d:
+            c = min(int(rep["cycles"][b]), int(oc[k]))
+            assert d == 1 and abs(oh[k, c] - 1e-6) <= 1e-3 * 1e-6, (b, rep["cycles"][b], oc[k])
+    h.close()

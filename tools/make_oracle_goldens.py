@@ -13,7 +13,9 @@ on the GPU box.  Re-run after any change to the oracle's arithmetic or to nmg_in
   2D (configs[2], [3] at alpha 1e-3 / 1e-4, [4]): the bench's 8-RHS seeded pool (tiled to the
      batch on the GPU), 3-cycle W_seed histories of the first `m` pool members.
 
-Usage: python tools/make_oracle_goldens.py [which ...]   (which in 1d_seed 1d_lin 2d)
+  W_train (trainer/nmg_train.py output): oracle solves to 1e-6 with the trained smoothers.
+
+Usage: python tools/make_oracle_goldens.py [which ...]   (which in 1d_seed 1d_lin 2d trained)
 """
 import os
 import sys
@@ -65,6 +67,35 @@ def one_d_lin():
     np.savez_compressed(os.path.join(GOLD, "oracle_cfg1_wlin.npz"), **out)
 
 
+def trained():
+    """W_train (trainer output, nmg_inputs/trained): oracle solves to 1e-6 -- the
+    oracle's confirmation that the trained smoothers converge, and the stopping cycles the GPU
+    solve must reproduce.  1D: the IDX_1D RHS of the full batch; 2D: 4 pool members (cfg 3: 2)."""
+    out = {}
+    for cid in (1, 2, 3, 4):
+        for a in sorted(set(ni.ALPHAS[cid]) | ({1e-2} if cid in (1, 2, 3) else set()), reverse=True):
+            cfg = ni.CONFIGS[cid].replace(alpha=a)
+            W = ni.weights_trained(cfg)
+            if W is None:
+                continue
+            f = ni.operator_factors(cfg)
+            H = hierarchy(cfg, f, W)
+            t0 = time.time()
+            if cfg.dim == 1:
+                y, _ = ni.make_rhs(cfg, f, a)
+                y = y[IDX_1D]
+            else:
+                y, _ = ni.make_rhs(cfg, f, a, nrhs=2 if cid >= 3 else 4, start=0)
+            orc = O.solve(H, y, tol=1e-6, max_cycles=40)
+            key = f"{cfg.name}_a{a:g}"
+            out[f"hist_{key}"] = orc.history
+            out[f"cycles_{key}"] = orc.cycles
+            out[f"conv_{key}"] = orc.converged
+            print(f"{key}: converged {orc.converged.sum()}/{len(orc.converged)}, cycles {orc.cycles.max()} "
+                  f"({time.time() - t0:.0f} s)", flush=True)
+    np.savez_compressed(os.path.join(GOLD, "oracle_wtrain.npz"), **out)
+
+
 def two_d():
     out = {}
     for key, (cid, a, m) in POOL_2D.items():
@@ -83,5 +114,5 @@ if __name__ == "__main__":
     which = sys.argv[1:] or ["1d_seed", "1d_lin", "2d"]
     for w in which:
         t0 = time.time()
-        {"1d_seed": one_d_seed, "1d_lin": one_d_lin, "2d": two_d}[w]()
+        {"1d_seed": one_d_seed, "1d_lin": one_d_lin, "2d": two_d, "trained": trained}[w]()
         print(f"{w} done in {time.time() - t0:.0f} s", flush=True)

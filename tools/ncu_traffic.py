@@ -1,16 +1,20 @@
 #!/usr/bin/env python
 """Aggregate an ncu CSV (metrics dram__bytes_read.sum, dram__bytes_write.sum, gpu__time_duration.sum)
 of `bench.py --steps 1` into per-kernel-class DRAM bytes of ONE step (the last `per_step` launches of
-the library) and merge them into profiles/traffic.json under the key KEY (e.g. "cfg1").
+the library, PER_STEP = the bench line's real kernel count per step, sum of launches_per_step) and
+merge them into profiles/traffic.json under the key KEY (e.g. "cfg1").
 Usage: ncu_traffic.py CSV PER_STEP_LAUNCHES OUT KEY"""
 import collections
 import csv
 import json
 import sys
 
-CLASS = [("dgemm", "gemm64"), ("ozaki", "gemm64"), ("row_sumsq", "misc"), ("tc_gemm", "gemm32"),
-         ("sgemm", "gemm32"), ("smooth1d", "smooth"), ("strip", "smooth"),
-         ("cnn2d", "smooth"), ("conv", "smooth"), ("fft", "smooth"), ("sumsq", "smooth"),
+# the library's kernel classes (include/nmg.h NMG_K_*): first match wins
+CLASS = [("dgemm", "gemm64"), ("ozaki", "gemm64"), ("row_sumsq", "misc"), ("row_norms", "misc"),
+         ("tc_gemm", "gemm32"), ("kron_tc", "gemm32"), ("sgemm", "gemm32"), ("gemm_f32", "gemm32"),
+         ("smooth1d", "smooth"), ("strip_combine", "filter"), ("conv_strip", "smooth"), ("cycle64", "smooth"),
+         ("fno_", "smooth"), ("cnn2d", "smooth"), ("combine_rows_fft", "filter"), ("fft_", "filter"),
+         ("sumsq", "filter"), ("real_to_complex", "filter"),
          ("restrict", "transfer"), ("prolong", "transfer"), ("coarse", "coarse")]
 
 
