@@ -447,6 +447,12 @@ def main():
     if not args.no_solve:
         wt = ni.weights_trained(cfg)
         scfg, label = cfg, "W_train (level-wise trainer, Alg 5)"
+        if wt is None:            # the config's trained set at another alpha of the curriculum
+            for a in (1e-2, 1e-3, 1e-4):
+                if ni.weights_trained(cfg.replace(alpha=a)) is not None:
+                    scfg = cfg.replace(alpha=a)
+                    wt = ni.weights_trained(scfg)
+                    break
         if wt is None and cfg.dim == 1:
             scfg = cfg.replace(alpha=max(ni.ALPHAS[cid]))
             wt, label = ni.weights_lin(scfg), "W_lin stand-in"

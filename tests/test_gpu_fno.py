@@ -75,9 +75,14 @@ def test_fno_smoothing_step(setup):
     h.debug_op(1, nmg.OP_SMOOTH, T(b), xs)
     b32 = b.astype(np.float32).astype(np.float64)
     s = np.sqrt((b32.reshape(3, -1) ** 2).sum(1)).reshape((3,) + (1,) * cfg.dim)
-    want = O.level_filter(H, 0, O.fno_forward(H.weights[0], b32 / s) * s)
+    hv = O.fno_forward(H.weights[0], b32 / s) * s
+    want = O.level_filter(H, 0, hv)
     got = xs.cpu().numpy().astype(np.float64) - x0.astype(np.float32)
-    assert rel_rows(got, want).max() < 1e-5
+    # F' is a contraction (mask <= 1) that removes the large smooth part of h (here
+    # ||h|| / ||F'(h)|| ~ 1e3 with the bias-dominated seeded FNO), so the fp32 error of h is
+    # measured against ||h||: |F'(h_gpu) - F'(h)| <= |h_gpu - h|
+    err = np.linalg.norm((got - want).reshape(3, -1), axis=1) / np.linalg.norm(hv.reshape(3, -1), axis=1)
+    assert err.max() < 1e-5
 
 
 def test_fno_cycle_history(setup):

@@ -207,7 +207,7 @@ def test_wtrain_solve_matches_oracle(key):
     yd = T(y, torch.float64)
     del y
     xd = torch.zeros_like(yd)
-    rep = h.solve(yd, xd, tol=1e-6, max_cycles=60)
+    rep = h.solve(yd, xd, tol=1e-6, max_cycles=150)
     assert rep["converged"].all()
     ok, err = history_close(rep["history"][idx], oh)
     assert ok, err

@@ -86,7 +86,7 @@ def trained():
                 y = y[IDX_1D]
             else:
                 y, _ = ni.make_rhs(cfg, f, a, nrhs=2 if cid >= 3 else 4, start=0)
-            orc = O.solve(H, y, tol=1e-6, max_cycles=40)
+            orc = O.solve(H, y, tol=1e-6, max_cycles=150)
             key = f"{cfg.name}_a{a:g}"
             out[f"hist_{key}"] = orc.history
             out[f"cycles_{key}"] = orc.cycles

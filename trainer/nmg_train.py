@@ -307,7 +307,11 @@ def train(cfg, alpha: float, init: List[np.ndarray], epochs: int, nbs: int = 20,
     lv = TorchLevels(cfg, factors, alpha, device)
     nets = [CNN(cfg, w, out_scale=1.0 / alpha, device=device) for w in init]
     opts = [torch.optim.Adam(n.parameters(), lr=lr) for n in nets]
-    scheds = [torch.optim.lr_scheduler.CosineAnnealingLR(o, T_max=max(1, epochs), eta_min=lr * 0.02) for o in opts]
+    # linear warm-up over the first 5 % of the epochs (a curriculum stage starts from the previous
+    # alpha's smoother under a 10x larger output gain), then cosine decay to 2 % of lr
+    warm = max(1, epochs // 20)
+    sched_fn = lambda e: (e + 1) / warm if e < warm else 0.02 + 0.49 * (1 + math.cos(math.pi * (e - warm) / max(1, epochs - warm)))   # noqa: E731
+    scheds = [torch.optim.lr_scheduler.LambdaLR(o, sched_fn) for o in opts]
     ro = NmgRollout(cfg, factors, alpha, nbs) if rollout == "nmg" else None
     rng = np.random.default_rng(seed)
     hist = []
