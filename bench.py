@@ -195,6 +195,7 @@ def main():
     ap.add_argument("--alpha", type=float, default=None, help="override the config's alpha (sweep points)")
     ap.add_argument("--nrhs", type=int, default=None)
     ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--lanes", type=int, default=0, help="nmg_tuning.lanes (0 = library default, 1 = off)")
     ap.add_argument("--precision", choices=["auto", "mixed", "fp64"], default="auto",
                     help="auto: fp64 cycle for config 0 (BASELINE's fp64 system), mixed otherwise")
     ap.add_argument("--no-cpu", action="store_true")
@@ -303,7 +304,7 @@ def main():
         raise SystemExit(f"rank {rank}: no RHS left for this rank ({cfg.nrhs} RHS over {world} ranks)")
     prec = nmg.PREC_FP64 if args.precision == "fp64" or (args.precision == "auto" and cid == 0) else nmg.PREC_MIXED
     h = nmg.Hierarchy(cfg.dim, cfg.n, cfg.levels, cfg.alpha, factors, nu1=cfg.nu1, nu2=cfg.nu2, max_rhs=B,
-                      device=local, comm=comm, precision=prec)
+                      device=local, comm=comm, precision=prec, tuning={"lanes": args.lanes})
     for l, w in enumerate(W):
         h.load_weights(l + 1, ni.cnn_arch(cfg), w)
     y_np = make_y(B, start)
@@ -494,7 +495,8 @@ def main():
                 "value": value, "unit": "RHS*cycles/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "strong" if strong else "weak", "vs_baseline": None,
-                "dtype": ("f64 outer residual (Ozaki int8 tcgen05) + fp32-accurate inner cycle (FP16x3 tcgen05 "
+                "dtype": ("f64 (NMG_PREC_FP64 fused cycle; the CNN's own arithmetic fp32)" if prec == nmg.PREC_FP64 else
+                          "f64 outer residual (Ozaki int8 tcgen05) + fp32-accurate inner cycle (FP16x3 tcgen05 "
                           + ("CNN and operator applies)" if cfg.dim == 1 else "CNN, 3xTF32 tcgen05 Kronecker applies)")),
                 "data": "synthetic (seeded RHS; W_seed Kaiming-uniform weights)",
                 "config": {"workload": workload, "global_batch": global_B, "n": cfg.n, "levels": cfg.levels,

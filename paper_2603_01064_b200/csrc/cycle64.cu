@@ -25,6 +25,8 @@ constexpr int NT = 512;
 constexpr int C = 16, KS = 5, HK = 2;
 
 struct Smem {
+  float* w;         // the level's CNN parameters (1473 floats)
+  double2* tw;      // exp(-2 pi i k / n0), k < n0 / 2 (fp64 twiddles of the finest level)
   double* y[8];
   double* x[8];
   double* r;        // n
@@ -57,15 +59,15 @@ NMG_D double norm2(const double* v, int n, double* red) {
 }
 
 // fp64 complex FFT of length n in shared memory (radix 2, DIF forward natural -> bit-reversed,
-// DIT inverse bit-reversed -> natural, twiddles exp(-+2 pi i k / len) by sincospi)
-NMG_D void fft64(double2* z, int n, bool inverse) {
+// DIT inverse bit-reversed -> natural); twiddles exp(-+2 pi i pos / len) = tw[pos n0 / len]
+NMG_D void fft64(double2* z, int n, bool inverse, const double2* tw, int n0) {
   if (!inverse) {
     for (int len = n; len >= 2; len >>= 1) {
-      const int half = len >> 1;
+      const int half = len >> 1, step = n0 / len;
       for (int i = threadIdx.x; i < (n >> 1); i += NT) {
         const int pos = i & (half - 1), j0 = ((i - pos) << 1) + pos, j1 = j0 + half;
-        double s, c;
-        sincospi(-2.0 * pos / len, &s, &c);
+        const double2 w = tw[pos * step];
+        const double c = w.x, s = w.y;
         const double2 a = z[j0], b = z[j1];
         z[j0] = make_double2(a.x + b.x, a.y + b.y);
         const double dx = a.x - b.x, dy = a.y - b.y;
@@ -75,11 +77,11 @@ NMG_D void fft64(double2* z, int n, bool inverse) {
     }
   } else {
     for (int len = 2; len <= n; len <<= 1) {
-      const int half = len >> 1;
+      const int half = len >> 1, step = n0 / len;
       for (int i = threadIdx.x; i < (n >> 1); i += NT) {
         const int pos = i & (half - 1), j0 = ((i - pos) << 1) + pos, j1 = j0 + half;
-        double s, c;
-        sincospi(2.0 * pos / len, &s, &c);
+        const double2 w = tw[pos * step];
+        const double c = w.x, s = -w.y;                 // conjugate twiddle
         const double2 a = z[j0], bb = z[j1];
         const double2 b = make_double2(bb.x * c - bb.y * s, bb.x * s + bb.y * c);
         z[j0] = make_double2(a.x + b.x, a.y + b.y);
@@ -94,13 +96,16 @@ NMG_D void fft64(double2* z, int n, bool inverse) {
 NMG_D void smooth_step(const Cycle64Args& a, int l, int n, double* x, const Smem& S) {
   const double s = norm2(S.b, n, S.red);
   if (s == 0.0) return;
-  const float* P = a.W[l];                     // w0 [16][1][5], b0, w1 [16][16][5], b1, w2 [1][16][5], b2
+  // the level's parameters in shared memory: w0 [16][1][5], b0, w1 [16][16][5], b1, w2 [1][16][5], b2
+  for (int i = threadIdx.x; i < 1473; i += NT) S.w[i] = __ldg(a.W[l] + i);
+  __syncthreads();
+  const float* P = S.w;
   const float* w0 = P;
   const float* b0 = w0 + C * KS;
   const float* w1 = b0 + C;
   const float* b1 = w1 + C * C * KS;
   const float* w2 = b1 + C;
-  const float b2 = __ldg(w2 + C * KS);
+  const float b2 = w2[C * KS];
   const int np = n + 2 * HK;
   for (int j = threadIdx.x; j < np; j += NT) {
     const int p = j - HK;
@@ -111,9 +116,9 @@ NMG_D void smooth_step(const Cycle64Args& a, int l, int n, double* x, const Smem
     const int c = i / np, j = i - c * np, p = j - HK;
     float v = 0.f;
     if (p >= 0 && p < n) {
-      float acc = __ldg(b0 + c);
+      float acc = b0[c];
 #pragma unroll
-      for (int t = 0; t < KS; ++t) acc = fmaf(__ldg(w0 + c * KS + t), S.u[j + t - HK], acc);
+      for (int t = 0; t < KS; ++t) acc = fmaf(w0[c * KS + t], S.u[j + t - HK], acc);
       v = fmaxf(acc, 0.f);
     }
     S.a1[i] = v;
@@ -123,12 +128,12 @@ NMG_D void smooth_step(const Cycle64Args& a, int l, int n, double* x, const Smem
     const int o = i / np, j = i - o * np, p = j - HK;
     float v = 0.f;
     if (p >= 0 && p < n) {
-      float acc = __ldg(b1 + o);
+      float acc = b1[o];
       for (int c = 0; c < C; ++c) {
         const float* wr = w1 + (o * C + c) * KS;
         const float* ar = S.a1 + c * np + j - HK;
 #pragma unroll
-        for (int t = 0; t < KS; ++t) acc = fmaf(__ldg(wr + t), ar[t], acc);
+        for (int t = 0; t < KS; ++t) acc = fmaf(wr[t], ar[t], acc);
       }
       v = fmaxf(acc, 0.f);
     }
@@ -140,7 +145,7 @@ NMG_D void smooth_step(const Cycle64Args& a, int l, int n, double* x, const Smem
     for (int c = 0; c < C; ++c) {
       const float* ar = S.a2 + c * np + p;
 #pragma unroll
-      for (int t = 0; t < KS; ++t) acc = fmaf(__ldg(w2 + c * KS + t), ar[t], acc);
+      for (int t = 0; t < KS; ++t) acc = fmaf(w2[c * KS + t], ar[t], acc);
     }
     S.z[p] = make_double2(s * (double)acc, 0.0);
   }
@@ -150,7 +155,7 @@ NMG_D void smooth_step(const Cycle64Args& a, int l, int n, double* x, const Smem
     __syncthreads();
     return;
   }
-  fft64(S.z, n, false);                                  // bit-reversed spectrum
+  fft64(S.z, n, false, S.tw, a.n);                       // bit-reversed spectrum
   const int lg = 31 - __clz(n);
   for (int j = threadIdx.x; j < n; j += NT) {
     const int k = (int)(__brev((unsigned)j) >> (32 - lg));
@@ -158,7 +163,7 @@ NMG_D void smooth_step(const Cycle64Args& a, int l, int n, double* x, const Smem
     S.z[j] = make_double2(S.z[j].x * m, S.z[j].y * m);
   }
   __syncthreads();
-  fft64(S.z, n, true);
+  fft64(S.z, n, true, S.tw, a.n);
   for (int p = threadIdx.x; p < n; p += NT) x[p] += S.z[p].x / (double)n;   // Re(IDFT), 1/n
   __syncthreads();
 }
@@ -174,9 +179,16 @@ __global__ void __launch_bounds__(NT, 1) cycle64_kernel(const __grid_constant__ 
   S.b = p; p += n0;
   S.red = p; p += 32;
   S.z = reinterpret_cast<double2*>(p); p += 2 * n0;
+  S.tw = reinterpret_cast<double2*>(p); p += n0;
   S.u = reinterpret_cast<float*>(p);
   S.a1 = S.u + n0 + 2 * HK + 4;
   S.a2 = S.a1 + C * (n0 + 2 * HK);
+  S.w = S.a2 + C * (n0 + 2 * HK);
+  for (int k = threadIdx.x; k < n0 / 2; k += NT) {
+    double sn, cs;
+    sincospi(-2.0 * k / n0, &sn, &cs);
+    S.tw[k] = make_double2(cs, sn);
+  }
   const double* yg = a.y + (int64_t)b * n0;
   double* xg = a.x + (int64_t)b * n0;
   for (int j = threadIdx.x; j < n0; j += NT) { S.y[0][j] = yg[j]; S.x[0][j] = xg[j]; }
@@ -250,8 +262,8 @@ __global__ void __launch_bounds__(NT, 1) cycle64_kernel(const __grid_constant__ 
 size_t cycle64_smem(int n, int L) {
   size_t d = 0;
   for (int l = 0; l < L; ++l) d += 2 * (size_t)(n >> l);
-  d += 2 * (size_t)n + 32 + 2 * (size_t)n;
-  return d * sizeof(double) + sizeof(float) * ((size_t)n + 2 * HK + 4 + 2 * (size_t)C * (n + 2 * HK)) + 64;
+  d += 2 * (size_t)n + 32 + 2 * (size_t)n + (size_t)n;
+  return d * sizeof(double) + sizeof(float) * ((size_t)n + 2 * HK + 4 + 2 * (size_t)C * (n + 2 * HK) + 1476) + 64;
 }
 
 void cycle64(const Cycle64Args& a, cudaStream_t s) {

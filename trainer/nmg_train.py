@@ -378,7 +378,9 @@ def main():
     ap.add_argument("--K", type=int, default=10)
     ap.add_argument("--lr", type=float, default=1e-3)
     ap.add_argument("--rollout", choices=["nmg", "torch"], default=None)
-    ap.add_argument("--init", choices=["seed", "lin"], default="seed")
+    ap.add_argument("--init", choices=["seed", "lin", "trained"], default="seed",
+                    help="trained: start from nmg_inputs/trained at --init-alpha")
+    ap.add_argument("--init-alpha", type=float, default=None)
     ap.add_argument("--n", type=int, default=None, help="override the grid size (quick runs)")
     ap.add_argument("--levels", type=int, default=None)
     ap.add_argument("--out", default=OUT_DIR)
@@ -391,7 +393,11 @@ def main():
     torch.backends.cuda.matmul.allow_tf32 = False
     torch.backends.cudnn.allow_tf32 = False
     rollout = args.rollout or ("nmg" if dev == "cuda" else "torch")
-    w = ni.weights_seed(cfg) if args.init == "seed" else ni.weights_lin(cfg, alpha=alphas[0])
+    if args.init == "trained":
+        w = ni.weights_trained(cfg.replace(alpha=args.init_alpha))
+        assert w is not None, "no trained weights at --init-alpha"
+    else:
+        w = ni.weights_seed(cfg) if args.init == "seed" else ni.weights_lin(cfg, alpha=alphas[0])
     for a in sorted(alphas, reverse=True):
         c = cfg.replace(alpha=a)
         t0 = time.time()
