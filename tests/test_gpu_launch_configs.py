@@ -210,10 +210,52 @@ def test_wtrain_solve_matches_oracle(key):
     rep = h.solve(yd, xd, tol=1e-6, max_cycles=150)
     assert rep["converged"].all()
     ok, err = history_close(rep["history"][idx], oh)
+    if not ok:
+        hg = rep["history"][idx]
+        m = np.isfinite(oh) & (oh >= 1e-6)
+        dev = np.where(m, np.abs(hg - oh) / np.where(m, oh, 1.0), 0.0)
+        print(key, "history deviation by cycle:", np.array2string(dev.max(axis=0), precision=2))
     assert ok, err
     for k, b in enumerate(idx):
         d = abs(int(rep["cycles"][b]) - int(oc[k]))
         if d:
             c = min(int(rep["cycles"][b]), int(oc[k]))
             assert d == 1 and abs(oh[k, c] - 1e-6) <= 1e-3 * 1e-6, (b, rep["cycles"][b], oc[k])
+    h.close()
+
+
+@pytest.mark.parametrize("name,cid,alpha", [("cfg1_a1e-4", 1, 1e-4), ("cfg1_a1e-3", 1, 1e-3), ("cfg2_a1e-3", 2, 1e-3)])
+def test_wtrain_smoother_per_level(name, cid, alpha):
+    """The FP16x3 tensor-core CNN with TRAINED weights (large output gains, activations far from
+    the power-of-two scales' worst-case bounds): OP_CNN and OP_SMOOTH at every smoothed level
+    within 1e-5 per RHS (the smoothing step measured against ||h||: F' is a contraction)."""
+    cfg = ni.CONFIGS[cid].replace(alpha=alpha)
+    W = ni.weights_trained(cfg)
+    if W is None:
+        pytest.skip("no trained weights")
+    f = ni.operator_factors(cfg)
+    H = oracle_hierarchy(cfg, f, W)
+    h = gpu_hierarchy(cfg, f, W, max_rhs=8)
+    rng = np.random.default_rng(12)
+    for lvl in range(1, cfg.levels):
+        n = cfg.n >> (lvl - 1)
+        shape = (4,) + (n,) * cfg.dim
+        b = rng.standard_normal(shape) * np.logspace(-2, 2, 4).reshape((4,) + (1,) * cfg.dim)
+        b = b.astype(np.float32).astype(np.float64)
+        s = np.sqrt((b.reshape(4, -1) ** 2).sum(1)).reshape((4,) + (1,) * cfg.dim)
+        u = b / s
+        out = torch.zeros(shape, device=DEV)
+        h.debug_op(lvl, nmg.OP_CNN, T(u), out)
+        want = O.cnn_forward(H.weights[lvl - 1], u.astype(np.float32).astype(np.float64))
+        e1 = rel_rows(out.cpu().numpy(), want).max()
+        x0 = rng.standard_normal(shape).astype(np.float32)
+        xs = T(x0)
+        h.debug_op(lvl, nmg.OP_SMOOTH, T(b), xs)
+        hv = O.cnn_forward(H.weights[lvl - 1], u) * s
+        wantx = O.level_filter(H, lvl - 1, hv)
+        got = xs.cpu().numpy().astype(np.float64) - x0
+        err = np.linalg.norm((got - wantx).reshape(4, -1), axis=1) / np.linalg.norm(hv.reshape(4, -1), axis=1)
+        print(name, "level", lvl, "cnn", e1, "smooth", err.max())
+        assert e1 < 1e-5, ("cnn", lvl, e1)
+        assert err.max() < 1e-5, ("smooth", lvl, err)
     h.close()
