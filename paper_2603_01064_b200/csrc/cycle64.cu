@@ -38,16 +38,36 @@ struct Smem {
   double* red;      // 32
 };
 
-// out[i] = (sub ? y[i] : 0) - sum_j A[i][j] v[j]   (warp per row, lanes over j, fixed order)
+// out[i] = (sub ? y[i] : 0) - sum_j A[i][j] v[j]   (warp per 4 rows, lanes over j, fixed order;
+// the 4 rows' loads of 4 consecutive j-steps are issued together to hide the L2 latency)
 NMG_D void matvec(const double* __restrict__ A, int n, const double* v, const double* y, double* out) {
+  constexpr int RW = 4;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = warp; i < n; i += NT / 32) {
-    const double* Ai = A + (int64_t)i * n;
-    double acc = 0.0;
-    for (int j = lane; j < n; j += 32) acc = fma(__ldg(Ai + j), v[j], acc);
+  for (int i0 = warp * RW; i0 < n; i0 += (NT / 32) * RW) {
+    double acc[RW];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) out[i] = (y ? y[i] : 0.0) - acc;
+    for (int r = 0; r < RW; ++r) acc[r] = 0.0;
+    const int nr = min(RW, n - i0);
+    for (int j0 = 0; j0 < n; j0 += 128) {
+      double a[RW][4], vv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = j0 + 32 * q + lane;
+        vv[q] = j < n ? v[j] : 0.0;
+#pragma unroll
+        for (int r = 0; r < RW; ++r) a[r][q] = (j < n && r < nr) ? __ldg(A + (int64_t)(i0 + r) * n + j) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int r = 0; r < RW; ++r) acc[r] = fma(a[r][q], vv[q], acc[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < RW; ++r) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
+      if (lane == 0 && r < nr) out[i0 + r] = (y ? y[i0 + r] : 0.0) - acc[r];
+    }
   }
   __syncthreads();
 }
