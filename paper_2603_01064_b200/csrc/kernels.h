@@ -71,6 +71,7 @@ struct OzakiArgs {
   int wrow0 = 0;
 };
 int ozaki_digits();
+int ozaki_bk();   // K block of the digit tensor maps (box K; 32: SWIZZLE_32B, 64: SWIZZLE_64B)
 // digit planes [S][plane / K rows][K]: plane = (rows allocated per plane) * K
 void ozaki_split_rows(int M, int K, const double* X, int64_t ldx, int8_t* dig, int64_t plane, int* ex,
                       cudaStream_t s);

@@ -259,16 +259,17 @@ nmg_status make_map16(CUtensorMap* m, const uint16_t* p, int64_t rows, int64_t c
   return NMG_OK;
 }
 
-// digit planes [S][rows][K] int8, box {64, box_rows, S}, SWIZZLE_64B
+// digit planes [S][rows][K] int8, box {ozaki_bk(), box_rows, S}, SWIZZLE_32B / _64B (32- / 64-byte rows)
 nmg_status make_digit_map(CUtensorMap* m, const int8_t* p, int S, int64_t rows, int64_t K, int box_rows,
                           int box_digits = 0) {
   NMG_TRY(get_encoder());
+  const int bk = ozaki_bk();
   cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)S};
   cuuint64_t strides[2] = {(cuuint64_t)K, (cuuint64_t)(rows * K)};
-  cuuint32_t box[3] = {64u, (cuuint32_t)box_rows, (cuuint32_t)(box_digits > 0 ? box_digits : S)};
+  cuuint32_t box[3] = {(cuuint32_t)bk, (cuuint32_t)box_rows, (cuuint32_t)(box_digits > 0 ? box_digits : S)};
   cuuint32_t es[3] = {1u, 1u, 1u};
   CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)p, dims, strides, box, es,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, bk == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(NMG_ERR_CUDA, "cuTensorMapEncodeTiled (digits) failed (%d)", (int)r);
   return NMG_OK;

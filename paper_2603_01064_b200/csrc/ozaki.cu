@@ -21,9 +21,18 @@ namespace {
 
 constexpr int OS = 7;                       // digits per operand
 constexpr int NDIAG = OS;                   // diagonals d = 2 .. OS + 1
-constexpr int OBM = 128, OBN = 64, OBK = 64, ONSTAGE = 2, ONT = 128;
-constexpr int XS_BYTES = OS * OBM * OBK;    // 56 KB
-constexpr int WS_BYTES = OS * OBN * OBK;    // 28 KB
+// K block per pipeline stage: 32 int8 (one MMA K step, 32-byte rows, SWIZZLE_32B) in 4 stages of
+// 42 KB -- three stages in flight cover the TMA latency at the MMA's consumption rate, which two
+// 84 KB stages of 64-wide K blocks did not (tensor pipe 31-34 % active, ncu r02)
+#ifndef NMG_OZ_BK
+#define NMG_OZ_BK 32
+#endif
+#ifndef NMG_OZ_NST
+#define NMG_OZ_NST 4
+#endif
+constexpr int OBM = 128, OBN = 64, OBK = NMG_OZ_BK, ONSTAGE = NMG_OZ_NST, ONT = 128;
+constexpr int XS_BYTES = OS * OBM * OBK;    // 28 KB (OBK 32)
+constexpr int WS_BYTES = OS * OBN * OBK;    // 14 KB
 constexpr int OSTAGE = XS_BYTES + WS_BYTES;
 constexpr int OZ_SMEM = ONSTAGE * OSTAGE + 256 + 1024;
 
@@ -118,8 +127,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ONT, 1)
             for (int j0 = 1; j0 <= OS + 1 - i; j0 += 4) {
               const int nd = (OS + 2 - i - j0) < 4 ? (OS + 2 - i - j0) : 4;
               const int d = i + j0 - 2;                      // first accumulator 0 .. OS - 1
-              const uint64_t da = desc_sw64(xs + (i - 1) * OBM * OBK + ks * 32);
-              const uint64_t db = desc_sw64(ws + (j0 - 1) * OBN * OBK + ks * 32);
+              const uint64_t da = OBK == 32 ? desc_sw32(xs + (i - 1) * OBM * OBK) : desc_sw64(xs + (i - 1) * OBM * OBK + ks * 32);
+              const uint64_t db = OBK == 32 ? desc_sw32(ws + (j0 - 1) * OBN * OBK) : desc_sw64(ws + (j0 - 1) * OBN * OBK + ks * 32);
               // the first products into the diagonals come from i = 1 at kt = ks = 0
               mma_i8(tmem + (uint32_t)(d * OBN), da, db, idesc_i8(nd), (kt == 0 && ks == 0 && i == 1) ? 0u : 1u);
             }
@@ -305,6 +314,7 @@ __global__ void __launch_bounds__(256) ozaki_split_rows_warp_kernel(int M, int K
 
 }  // namespace
 
+int ozaki_bk() { return OBK; }
 int ozaki_digits() { return OS; }
 
 void ozaki_split_rows(int M, int K, const double* X, int64_t ldx, int8_t* dig, int64_t plane, int* ex,

@@ -70,6 +70,16 @@ NMG_D uint64_t desc_sw64(uint32_t saddr) {
   return d;
 }
 
+// K-major SWIZZLE_32B operand: 32-byte rows, 8-row groups 256 B apart (SBO), layout type 6
+NMG_D uint64_t desc_sw32(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(256 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)6 << 61;
+  return d;
+}
+
 NMG_D void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"

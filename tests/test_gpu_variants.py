@@ -114,7 +114,7 @@ def test_fallback_kernels_match(knob, dim):
     assert ok, err
 
 
-@pytest.mark.parametrize("kind,tol,cycles", [("seed", 1e-300, 10), ("lin", 1e-10, 60)])
+@pytest.mark.parametrize("kind,tol,cycles", [("seed", 1e-300, 10), ("lin", 1e-10, 120)])
 def test_precision_fp64_cfg0(kind, tol, cycles):
     """NMG_PREC_FP64 (config 0's fp64 system, reading R14): the fused one-launch fp64 cycle.
     Histories match the fp64 oracle far below the mixed path's 1e-3 (only the CNN's own fp32
