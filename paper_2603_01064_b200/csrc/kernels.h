@@ -72,6 +72,7 @@ struct OzakiArgs {
 };
 int ozaki_digits();
 int ozaki_bk();   // K block of the digit tensor maps (box K; 32: SWIZZLE_32B, 64: SWIZZLE_64B)
+int ozaki_bn();   // N tile (box rows of the W digit maps; the ||r||^2 partials per row are N / ozaki_bn())
 // digit planes [S][plane / K rows][K]: plane = (rows allocated per plane) * K
 void ozaki_split_rows(int M, int K, const double* X, int64_t ldx, int8_t* dig, int64_t plane, int* ex,
                       cudaStream_t s);

@@ -396,7 +396,8 @@ struct nmg_hierarchy {
   DevBuf<double> hy, hx;   // staging for nmg_vcycles_host (allocated at create)
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;         // copy streams of nmg_vcycles_host
   std::vector<cudaEvent_t> hev;                          // its chunk events
-  int ntiles = 0;
+  int ntiles = 0;        // ||r||^2 partials per row: DMMA residual (64-wide tiles)
+  int ntiles_oz = 0;     // ... Ozaki residual (ozaki_bn()-wide tiles)
   int64_t launches = 0;
   bool poisoned = false;
   // profiling (nmg_profile): event pairs per kernel class
@@ -1181,10 +1182,13 @@ nmg_status ynorms(nmg_hierarchy* h, int nrhs, const double* y, cudaStream_t s) {
 // relres = ||r|| / ||y|| from the outer residual's partials; active = relres > tol
 nmg_status relres_fin(nmg_hierarchy* h, int nrhs, double tol, uint8_t* active, double* relres, cudaStream_t s) {
   if (!h->slab) {
-    { Prof p(h, NMG_K_MISC, s); relres_finalize(nrhs, h->ntiles, h->part.p, h->ynorm.p, relres, tol, active, s, h->rows_per_rhs); }
+    const bool oz = h->d.dim == 1 ? (h->ozaki && nrhs > 64) : h->ozaki2d;   // as outer_residual
+    { Prof p(h, NMG_K_MISC, s);
+      relres_finalize(nrhs, oz ? h->ntiles_oz : h->ntiles, h->part.p, h->ynorm.p, relres, tol, active, s, h->rows_per_rhs); }
     return check_launch(h);
   }
-  const int64_t cnt = (int64_t)gemm_f64_ntiles(h->R[0]) * h->n[0];
+  const int64_t cnt = (int64_t)((h->ozaki2d && h->R[0] % 128 == 0) ? h->R[0] / ozaki_bn() : gemm_f64_ntiles(h->R[0])) *
+                      h->n[0];
   { Prof p(h, NMG_K_MISC, s); part_sums(nrhs, cnt, h->part.p, h->rsum.p, s); }
   NMG_TRY(check_launch(h));
   NMG_TRY(h->comm->sum_f64(h->rsum.p, nrhs, h->dscratch.p, s));
@@ -1725,7 +1729,7 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
       NMG_TRY(h->wexp.upload(ew.data(), ew.size()));
       NMG_TRY(h->xdig.alloc((size_t)S * B * n));
       NMG_TRY(h->xexp.alloc(B));
-      NMG_TRY(make_digit_map(&h->mWd, h->wdig.p, S, n, n, 64));
+      NMG_TRY(make_digit_map(&h->mWd, h->wdig.p, S, n, n, ozaki_bn()));
       NMG_TRY(make_digit_map(&h->mXd, h->xdig.p, S, (int64_t)B, n, 64, 1));   // half tiles, one digit per box
     }
   }
@@ -1746,14 +1750,15 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
       NMG_TRY(h->wexpB.upload(ew.data(), ew.size()));
       NMG_TRY(h->xdig.alloc((size_t)S * B * nn));
       NMG_TRY(h->xexp.alloc(B * n));
-      NMG_TRY(make_digit_map(&h->mWd, h->wdig.p, S, n, n, 64));
-      NMG_TRY(make_digit_map(&h->mWdB, h->wdigB.p, S, n, n, 64));
+      NMG_TRY(make_digit_map(&h->mWd, h->wdig.p, S, n, n, ozaki_bn()));
+      NMG_TRY(make_digit_map(&h->mWdB, h->wdigB.p, S, n, n, ozaki_bn()));
       NMG_TRY(make_digit_map(&h->mXd, h->xdig.p, S, (int64_t)B * n, n, 64, 1));
     }
   }
   h->split_fresh.assign(h->L, 0);
   h->ntiles = gemm_f64_ntiles(d.dim == 1 ? (int)h->N[0] : n);
-  NMG_TRY(h->part.alloc(B * h->ntiles * (size_t)h->rows_per_rhs));
+  h->ntiles_oz = (d.dim == 1 ? (int)h->N[0] : n) / ozaki_bn();
+  NMG_TRY(h->part.alloc(B * (size_t)std::max(h->ntiles, h->ntiles_oz) * (size_t)h->rows_per_rhs));
   NMG_TRY(h->ynorm.alloc(B));
   NMG_TRY(h->ywork.alloc(B * 64));
   NMG_TRY(h->relres.alloc(B));

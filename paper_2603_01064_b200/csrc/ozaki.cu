@@ -28,9 +28,16 @@ constexpr int NDIAG = OS;                   // diagonals d = 2 .. OS + 1
 #define NMG_OZ_BK 32
 #endif
 #ifndef NMG_OZ_NST
-#define NMG_OZ_NST 4
+#define NMG_OZ_NST 3
 #endif
-constexpr int OBM = 128, OBN = 64, OBK = NMG_OZ_BK, ONSTAGE = NMG_OZ_NST, ONT = 128;
+// 32-wide N tiles: 7 diagonal accumulators x 32 columns = 224 TMEM columns (256 allocated) and
+// 3 x 35 KB of stages, so TWO CTAs share an SM and one's epilogue (fp64 combine, y / x loads,
+// r stores -- ~260 KB of HBM traffic per 2D tile) overlaps the other's MMAs
+#ifndef NMG_OZ_BN
+#define NMG_OZ_BN 32
+#endif
+constexpr int OBM = 128, OBN = NMG_OZ_BN, OBK = NMG_OZ_BK, ONSTAGE = NMG_OZ_NST, ONT = 128;
+constexpr int OTCOLS = OBN == 32 ? 256 : 512;
 constexpr int XS_BYTES = OS * OBM * OBK;    // 28 KB (OBK 32)
 constexpr int WS_BYTES = OS * OBN * OBK;    // 14 KB
 constexpr int OSTAGE = XS_BYTES + WS_BYTES;
@@ -67,7 +74,7 @@ NMG_D void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t a
 // refilled only after the MMAs of BOTH CTAs released it (commit multicast, count 2).
 // GEN: the slab mode's general output mapping and W row offset (else the whole-image mapping)
 template <bool GEN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ONT, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ONT, OBN == 32 ? 2 : 1)
     ozaki_resid_kernel(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mW,
                        OzakiArgs a) {
   extern __shared__ __align__(1024) uint8_t smraw[];
@@ -87,7 +94,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ONT, 1)
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(su32(tslot)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tslot)), "n"(OTCOLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -243,7 +250,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ONT, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   cluster_sync();                                 // no CTA leaves while its peer may still signal it
-  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(OTCOLS));
 }
 
 // digits of the rows of X (fp64 [M][K]): ex[m] with max_k |x_mk| < 2^{ex[m]}, then S truncation
@@ -315,6 +322,7 @@ __global__ void __launch_bounds__(256) ozaki_split_rows_warp_kernel(int M, int K
 }  // namespace
 
 int ozaki_bk() { return OBK; }
+int ozaki_bn() { return OBN; }
 int ozaki_digits() { return OS; }
 
 void ozaki_split_rows(int M, int K, const double* X, int64_t ldx, int8_t* dig, int64_t plane, int* ex,
