@@ -21,20 +21,19 @@ namespace {
 
 constexpr int OS = 7;                       // digits per operand
 constexpr int NDIAG = OS;                   // diagonals d = 2 .. OS + 1
-// K block per pipeline stage: 32 int8 (one MMA K step, 32-byte rows, SWIZZLE_32B) in 4 stages of
-// 42 KB -- three stages in flight cover the TMA latency at the MMA's consumption rate, which two
-// 84 KB stages of 64-wide K blocks did not (tensor pipe 31-34 % active, ncu r02)
+// Tile / pipeline shape (compile-time knobs for A/B builds, tools/ab_ozaki.sh).  Measured at
+// tensor-pipe 31-34 % active (ncu r02, cfg 3); neither 32-wide K blocks in 4 stages of 42 KB
+// (SWIZZLE_32B digit maps: cfg 1 gemm64 0.423 vs 0.430 ms, cfg 3 32.7 vs 32.2 ms) nor 32-wide
+// N tiles with two CTAs per SM (epilogue of one under the MMAs of the other: cfg 1 0.68 ms,
+// cfg 3 32.9 ms) moved it, so the kernel keeps 64 x 64 tiles in two 84 KB stages.
 #ifndef NMG_OZ_BK
-#define NMG_OZ_BK 32
+#define NMG_OZ_BK 64
 #endif
 #ifndef NMG_OZ_NST
-#define NMG_OZ_NST 3
+#define NMG_OZ_NST 2
 #endif
-// 32-wide N tiles: 7 diagonal accumulators x 32 columns = 224 TMEM columns (256 allocated) and
-// 3 x 35 KB of stages, so TWO CTAs share an SM and one's epilogue (fp64 combine, y / x loads,
-// r stores -- ~260 KB of HBM traffic per 2D tile) overlaps the other's MMAs
 #ifndef NMG_OZ_BN
-#define NMG_OZ_BN 32
+#define NMG_OZ_BN 64
 #endif
 constexpr int OBM = 128, OBN = NMG_OZ_BN, OBK = NMG_OZ_BK, ONSTAGE = NMG_OZ_NST, ONT = 128;
 constexpr int OTCOLS = OBN == 32 ? 256 : 512;
