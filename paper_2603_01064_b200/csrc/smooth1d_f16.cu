@@ -25,8 +25,9 @@
 // warp converged, one elected lane issuing, so the stage arithmetic stays in uniform
 // registers); the norm, filter and update phases use all 288 threads.  Three CTAs per SM
 // overlap the serial phases of one right-hand side with the tile pipelines of the others.
-// The level filter is a swizzled Stockham FFT (level_filter_row) and x* is prefetched with
-// cp.async while it runs.
+// The level filter is a swizzled Stockham FFT (level_filter_row).  The CNN output row h is written
+// into the input-row buffer behind the layer-1 producer and moved into the freed a1 stages for
+// the filter (no separate h row: 50 KB per CTA at n = 4096, four CTAs per SM).
 #include <cuda_fp16.h>
 
 #include <algorithm>
@@ -295,6 +296,33 @@ NMG_D void a1_row(const Smooth1dArgs& a, const float* u, int p, int n, uint4& hi
   split8(v, hi, lo);
 }
 
+// the same for two positions p0, p1 at once: packed fp32 pairs (FFMA2 with the weight as a
+// broadcast operand -- half the FMA issue slots; each lane rounds exactly as the scalar fmaf,
+// same order, so the result is bitwise a1_row's)
+template <int H>
+NMG_D void a1_row2(const Smooth1dArgs& a, const float* u, int p0, int p1, int n, uint4& hi0, uint4& lo0, uint4& hi1,
+                   uint4& lo1) {
+  const bool ok0 = p0 >= 0 && p0 < n, ok1 = p1 >= 0 && p1 < n;
+  const float* u0 = u + (ok0 ? p0 : 2) - 2;   // any in-range window when the position is padding
+  const float* u1 = u + (ok1 ? p1 : 2) - 2;
+  float2 x[KS];
+#pragma unroll
+  for (int t = 0; t < KS; ++t) x[t] = make_float2(u0[t], u1[t]);
+  float v0[8], v1[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float* w = a.w.w0 + (8 * H + j) * KS;
+    const float b = a.w.b0[8 * H + j];
+    float2 acc = make_float2(b, b);
+#pragma unroll
+    for (int t = 0; t < KS; ++t) acc = __ffma2_rn(x[t], make_float2(w[t], w[t]), acc);
+    v0[j] = ok0 ? fmaxf(acc.x, 0.f) : 0.f;
+    v1[j] = ok1 ? fmaxf(acc.y, 0.f) : 0.f;
+  }
+  split8(v0, hi0, lo0);
+  split8(v1, hi1, lo1);
+}
+
 // Layer-1 producer for channels 8 H .. 8 H + 7 (H compile-time, so the weights are
 // constant-bank operands).  Buffer row r of tile k holds position k TP - 2 + r; rows 0..131
 // are read by the five tap-shifted MMAs.  Each thread computes rows 4 + r0 and 68 + r0
@@ -310,8 +338,7 @@ NMG_D void produce_a1(const Smooth1dArgs& a, uint8_t* Abuf, uint64_t* aempty, ui
     const int st = k % NSA;
     const int Q0 = k * TP;
     uint4 h0, l0, h1, l1;
-    a1_row<H>(a, u, Q0 + 2 + r0, n, h0, l0);
-    a1_row<H>(a, u, Q0 + 66 + r0, n, h1, l1);
+    a1_row2<H>(a, u, Q0 + 2 + r0, Q0 + 66 + r0, n, h0, l0, h1, l1);
     mb_wait(&aempty[st], ((uint32_t)(k / NSA) & 1u) ^ 1u);
     uint4* ah = reinterpret_cast<uint4*>(Abuf + (2 * st) * ABYTES) + H * AR;
     uint4* al = reinterpret_cast<uint4*>(Abuf + (2 * st + 1) * ABYTES) + H * AR;
@@ -349,8 +376,11 @@ __global__ void __launch_bounds__(NT, NMG_S1D_MINB) smooth1d_f16_kernel(const __
   uint8_t* Abuf = sm;                                          // [2 stages][hi | lo] ABYTES each
   uint8_t* Bw = Abuf + abuf_bytes(NSA, n);                     // [5 taps][2][32][8] f16
   float* qs = reinterpret_cast<float*>(Bw + KS * BTAP);        // [5][QR]
-  float* hb = qs + KS * QR;                                    // n (filter buffer)
-  float* u = hb + n;                                           // n + 2 UPAD (input row, then x*)
+  // the input row u (b / s) and, in place behind the producer, the CNN output h (plain order):
+  // the epilogue of tile k writes h at positions <= k TP + 125, the producer reads u only from
+  // the tile it is filling (>= k TP - 2), and tile k + 1 starts at k TP + 126
+  float* u = qs + KS * QR;                                     // n + 2 UPAD
+  float* hb = reinterpret_cast<float*>(Abuf);                  // filter row (swizzled), after the tiles
   uint64_t* bars = reinterpret_cast<uint64_t*>(u + n + 2 * UPAD);        // afull[2] aempty[2] dfull[2] dempty[2]
   uint64_t* afull = bars;
   uint64_t* aempty = afull + NSA;
@@ -452,7 +482,7 @@ __global__ void __launch_bounds__(NT, NMG_S1D_MINB) smooth1d_f16_kernel(const __
       }
       auto emit = [&](int p, float hv) {
         if (a.filter) {
-          hb[hsw(p)] = hv;
+          u[UPAD + p] = hv;
         } else {
           const float xv = a.accumulate ? xrow[p] + hv : hv;
           xrow[p] = xv;
@@ -477,15 +507,24 @@ __global__ void __launch_bounds__(NT, NMG_S1D_MINB) smooth1d_f16_kernel(const __
         asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
         __syncwarp();
         if (lane == 0) mb_arrive(&dempty[sd]);
+        // layer 3 per tap over channel pairs in packed fp32 (even / odd channel partial sums,
+        // added at the end): q[t] = sum_c w2[c][t] a2[c]
+        float2 q2[KS];
+#pragma unroll
+        for (int t = 0; t < KS; ++t) q2[t] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int c = 0; c < C; c += 2) {
+          const float2 s2 = __fadd2_rn(make_float2(__uint_as_float(d[c]), __uint_as_float(d[c + 1])),
+                                       make_float2(__uint_as_float(d[16 + c]), __uint_as_float(d[17 + c])));
+          const float2 z2 = __ffma2_rn(s2, make_float2(dsc, dsc), make_float2(a.w.b1[c], a.w.b1[c + 1]));
+          const float2 a22 = make_float2(fmaxf(z2.x, 0.f), fmaxf(z2.y, 0.f));
+#pragma unroll
+          for (int t = 0; t < KS; ++t)
+            q2[t] = __ffma2_rn(make_float2(a.w.w2[c * KS + t], a.w.w2[(c + 1) * KS + t]), a22, q2[t]);
+        }
         float q[KS];
 #pragma unroll
-        for (int t = 0; t < KS; ++t) q[t] = 0.f;
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-          const float a2 = fmaxf(fmaf(__uint_as_float(d[c]) + __uint_as_float(d[16 + c]), dsc, a.w.b1[c]), 0.f);
-#pragma unroll
-          for (int t = 0; t < KS; ++t) q[t] = fmaf(a.w.w2[c * KS + t], a2, q[t]);
-        }
+        for (int t = 0; t < KS; ++t) q[t] = q2[t].x + q2[t].y;
         const int Q0 = k * TP;
 #pragma unroll
         for (int t = 0; t < KS; ++t) qs[t * QR + ((Q0 + m) & (QR - 1))] = q[t];
@@ -504,15 +543,11 @@ __global__ void __launch_bounds__(NT, NMG_S1D_MINB) smooth1d_f16_kernel(const __
     __syncthreads();
     S1D_TS(2);
     if (a.filter) {
-      // ---- level filter F'_l on the whole row (see level_filter_row); prefetch x* into the (now free) input-row buffer while the FFT runs
-      const bool pre = a.accumulate;
-      if (pre) {
-        for (int j = 4 * tid; j < n; j += 4 * NT)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(su32(u + UPAD + j)), "l"(xrow + j)
-                       : "memory");
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
-      }
-      level_filter_row(reinterpret_cast<float2*>(hb), reinterpret_cast<float2*>(Abuf), n, a.twiddle, a.tw_n,
+      // ---- level filter F'_l on the whole row (see level_filter_row): h moves from the input-row
+      // buffer into the (now free) a1 stages in the swizzled layout; the row buffer is the scratch
+      for (int j = tid; j < n; j += NT) hb[hsw(j)] = u[UPAD + j];
+      const bool pre = false;
+      level_filter_row(reinterpret_cast<float2*>(hb), reinterpret_cast<float2*>(u + UPAD), n, a.twiddle, a.tw_n,
                        tid, NT);
       S1D_TS(3);
       if (pre) {
@@ -569,7 +604,7 @@ __global__ void __launch_bounds__(NT, NMG_S1D_MINB) smooth1d_f16_kernel(const __
 constexpr int kNSA = 2;   // a1 stages: more buy nothing once shared-memory bandwidth binds
 
 size_t smem_of(int n) {
-  return 1024 + abuf_bytes(kNSA, n) + KS * BTAP + sizeof(float) * (KS * QR + n + n + 2 * UPAD) +
+  return 1024 + abuf_bytes(kNSA, n) + KS * BTAP + sizeof(float) * (KS * QR + n + 2 * UPAD) +
          8 * (2 * kNSA + 2 * NSD) + 16;
 }
 
