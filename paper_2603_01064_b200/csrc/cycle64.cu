@@ -12,7 +12,9 @@
 // Galerkin operators A_l and A_L^{-1} are read from L2 by warp-per-row dot products (fixed
 // order, deterministic).  The level filter is an fp64 complex FFT of the real row.  For the
 // latency-bound small problems (config 0: n = 256, 8 RHS) one launch replaces the ~50 kernel
-// launches of the mixed-precision cycle.
+// launches of the mixed-precision cycle.  The same kernel runs the COARSE SUB-CYCLE of the mixed
+// path (yf / xf set): NMGF(0, y_l0) over the levels with n_l <= 512, fp32 in and out, every step
+// in between in fp64 -- one launch instead of ~8 per coarse level (latency-bound at small batches).
 #include <cmath>
 
 #include "common.cuh"
@@ -209,18 +211,22 @@ __global__ void __launch_bounds__(NT, 1) cycle64_kernel(const __grid_constant__ 
     sincospi(-2.0 * k / n0, &sn, &cs);
     S.tw[k] = make_double2(cs, sn);
   }
-  const double* yg = a.y + (int64_t)b * n0;
-  double* xg = a.x + (int64_t)b * n0;
-  for (int j = threadIdx.x; j < n0; j += NT) { S.y[0][j] = yg[j]; S.x[0][j] = xg[j]; }
+  const bool sub = a.yf != nullptr;                     // coarse sub-cycle: NMGF(0, y) of fp32 y
+  const double* yg = sub ? nullptr : a.y + (int64_t)b * n0;
+  double* xg = sub ? nullptr : a.x + (int64_t)b * n0;
+  for (int j = threadIdx.x; j < n0; j += NT) {
+    S.y[0][j] = sub ? (double)a.yf[(int64_t)b * n0 + j] : yg[j];
+    S.x[0][j] = sub ? 0.0 : xg[j];
+  }
   __syncthreads();
-  const double ny = norm2(S.y[0], n0, S.red);
+  const double ny = sub ? 1.0 : norm2(S.y[0], n0, S.red);
   auto relres = [&]() -> double {
     matvec(a.A[0], n0, S.x[0], S.y[0], S.r);
     const double nr = norm2(S.r, n0, S.red);
     return ny > 0.0 ? nr / ny : 0.0;
   };
   const bool active = a.active_in ? a.active_in[b] != 0 : true;
-  if (!a.relres_after) {
+  if (!sub && !a.relres_after) {
     const double rr = relres();
     if (threadIdx.x == 0) {
       if (a.relres) a.relres[b] = rr;
@@ -266,9 +272,12 @@ __global__ void __launch_bounds__(NT, 1) cycle64_kernel(const __grid_constant__ 
         smooth_step(a, l, n, S.x[l], S);
       }
     }
-    for (int j = threadIdx.x; j < n0; j += NT) xg[j] = S.x[0][j];
+    for (int j = threadIdx.x; j < n0; j += NT) {
+      if (sub) a.xf[(int64_t)b * n0 + j] = (float)S.x[0][j];
+      else xg[j] = S.x[0][j];
+    }
   }
-  if (a.relres_after) {
+  if (!sub && a.relres_after) {
     const double rr = relres();
     if (threadIdx.x == 0) {
       if (a.relres) a.relres[b] = rr;

@@ -310,6 +310,10 @@ struct Cycle64Args {
   uint8_t* active_out;        // null or [nrhs]: relres > tol
   bool do_cycle;              // run the cycle (else only the relative residual)
   bool relres_after;          // relres of the output x (nmg_solve) instead of the input x (nmg_vcycle)
+  // coarse sub-cycle of the mixed path: x_l0 = NMGF(0, y_l0) with fp32 y / x ([nrhs][n]); the
+  // levels of this call are the hierarchy's l0 .. L-1 (n, L, A, W, Ainv of that sub-hierarchy)
+  const float* yf = nullptr;
+  float* xf = nullptr;
 };
 size_t cycle64_smem(int n, int L);
 void cycle64(const Cycle64Args& a, cudaStream_t s);

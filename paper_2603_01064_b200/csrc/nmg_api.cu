@@ -317,7 +317,10 @@ struct nmg_hierarchy {
   std::vector<int64_t> N;  // unknowns per level
   // level-1 fp64 operator (1D: A; 2D: B, C)
   DevBuf<double> A64, B64, C64;
-  std::vector<std::unique_ptr<DevBuf<double>>> A64l;     // NMG_PREC_FP64: fp64 A_l, levels 1 .. L-2
+  std::vector<std::unique_ptr<DevBuf<double>>> A64l;     // fp64 A_l by level (1 .. L-2) for cycle64:
+                                                         // every level in NMG_PREC_FP64, the fused
+                                                         // coarse levels (n_l <= 512) in the mixed path
+  int l_fuse = -1;                                       // first level of the fused coarse sub-cycle
   // per smoothed level (l < L-1) fp32 operators (SIMT path) and tf32 hi/lo splits (tcgen05)
   std::vector<std::unique_ptr<DevBuf<float>>> A32, AP32, A32h, A32l, AP32h, AP32l;
   std::vector<CUtensorMap> mAh, mAl, mAPh, mAPl;        // W operand maps per level (box 256)
@@ -654,10 +657,32 @@ nmg_status level_resid(nmg_hierarchy* h, int l, int which, int nrhs, const float
 }
 
 // NMGF(0, y_l) at level l (0-based): input wy[l], output wx[l].
+// the coarse levels l0 .. L-1 as one fp64 sub-cycle launch (cycle64.cu): x_l0 = NMGF(0, y_l0)
+bool fused_coarse_ok(const nmg_hierarchy* h, int l) {
+  if (h->l_fuse < 0 || l != h->l_fuse) return false;
+  for (int q = l; q < h->L - 1; ++q)
+    if (h->fno.size() > (size_t)q && h->fno[q]) return false;   // CNN smoothers only
+  return true;
+}
+
 nmg_status cycle_level_1d(nmg_hierarchy* h, int l, int nrhs, cudaStream_t s) {
   const int n = h->n[l];
   float* y = h->wy[l]->p;
   float* x = h->wx[l]->p;
+  if (fused_coarse_ok(h, l)) {
+    Cycle64Args a{};
+    a.n = n; a.L = h->L - l; a.nrhs = nrhs; a.nu1 = h->d.nu1; a.nu2 = h->d.nu2;
+    a.filter = h->d.level_filter != 0;
+    for (int q = l; q < h->L - 1; ++q) {
+      a.A[q - l] = q == 0 ? h->A64.p : h->A64l[q]->p;
+      a.W[q - l] = h->W[q]->p;
+    }
+    a.Ainv = h->Ainv.p;
+    a.yf = y; a.xf = x; a.do_cycle = true;
+    { Prof p(h, NMG_K_COARSE, s); cycle64(a, s); }
+    h->split_fresh[l] = 0;
+    return check_launch(h);
+  }
   if (l == h->L - 1) {
     float* xh = (!h->gemm_f16 && h->sxh.size() > (size_t)l && h->sxh[l]->p && h->nc <= 128) ? h->sxh[l]->p : nullptr;
     { Prof p(h, NMG_K_COARSE, s);
@@ -1294,7 +1319,7 @@ nmg_status cycle_fp64(nmg_hierarchy* h, int nrhs, const double* y, double* x, bo
   Cycle64Args a{};
   a.n = h->d.n; a.L = h->L; a.nrhs = nrhs; a.nu1 = h->d.nu1; a.nu2 = h->d.nu2; a.filter = h->d.level_filter != 0;
   for (int l = 0; l < h->L - 1; ++l) {
-    a.A[l] = l == 0 ? h->A64.p : h->A64l[l - 1]->p;
+    a.A[l] = l == 0 ? h->A64.p : h->A64l[l]->p;
     a.W[l] = h->W[l]->p;
   }
   a.Ainv = h->Ainv.p;
@@ -1461,6 +1486,12 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
   const size_t nn = (size_t)n * n;
 
   std::vector<double> Acoarse;
+  if (d.dim == 1 && d.precision == NMG_PREC_MIXED && h->tune.no_fused_coarse == 0) {
+    // the coarse levels (n_l <= 512 and at least one smoothed level) run as one fused fp64
+    // sub-cycle kernel per RHS (cycle64.cu): latency-bound small grids become one launch
+    for (int l = 0; l < h->L - 1; ++l)
+      if (h->n[l] <= 512) { h->l_fuse = l; break; }
+  }
   if (d.dim == 1) {
     std::vector<double> A(factors, factors + nn);
     for (int i = 0; i < n; ++i) A[(size_t)i * n + i] += d.alpha;
@@ -1512,10 +1543,9 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
       }
       host_restrict_rows(AP, nl, nl / 2, Ac);           // R A P
       A.swap(Ac);
-      if (d.precision == NMG_PREC_FP64 && l + 1 < h->L - 1) {
-        h->A64l.emplace_back(new DevBuf<double>());
-        NMG_TRY(h->A64l.back()->upload(A.data(), A.size()));
-      }
+      while ((int)h->A64l.size() < l + 2) h->A64l.emplace_back(new DevBuf<double>());
+      if (l + 1 < h->L - 1 && (d.precision == NMG_PREC_FP64 || (h->l_fuse >= 0 && l + 1 >= h->l_fuse)))
+        NMG_TRY(h->A64l[l + 1]->upload(A.data(), A.size()));
     }
     Acoarse = A;
   } else {
@@ -1569,7 +1599,7 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
   NMG_TRY(h->Lcol.upload(Lt.data(), Lt.size()));
   {
     // explicit inverse A_L^{-1} = L^{-T} L^{-1} (fp64, symmetric), column by column
-    h->coarse_inv = h->tune.coarse_subst == 0 || d.precision == NMG_PREC_FP64;
+    h->coarse_inv = h->tune.coarse_subst == 0 || d.precision == NMG_PREC_FP64 || h->l_fuse >= 0;
     if (h->coarse_inv) {
       std::vector<double> inv((size_t)Nc * Nc), z(Nc);
       for (int j = 0; j < Nc; ++j) {

@@ -92,13 +92,13 @@ def test_paper_form_operator_2d():
     assert ok, err
 
 
-@pytest.mark.parametrize("knob", ["simt_gemm", "ffma_cnn", "fp64_dmma", "no_graphs", "no_kron", "coarse_subst"])
+@pytest.mark.parametrize("knob", ["simt_gemm", "ffma_cnn", "fp64_dmma", "no_graphs", "no_kron", "coarse_subst", "no_fused_coarse"])
 @pytest.mark.parametrize("dim", [1, 2])
 def test_fallback_kernels_match(knob, dim):
     """The alternative kernels selected by nmg_tuning (SIMT GEMM, FFMA CNNs, DMMA fp64 residual,
     eager launches, unfused Kronecker pair, Cholesky substitution at the coarsest level) agree
     with the oracle too."""
-    if knob == "no_kron" and dim == 1:
+    if (knob == "no_kron" and dim == 1) or (knob == "no_fused_coarse" and dim == 2):
         pytest.skip("2D-only knob")
     cfg = ni.CONFIGS[0].replace(nrhs=2) if dim == 1 else ni.CONFIGS[2].replace(n=64, levels=3, nrhs=2)
     f = ni.operator_factors(cfg)
