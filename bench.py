@@ -196,6 +196,7 @@ def main():
     ap.add_argument("--nrhs", type=int, default=None)
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--lanes", type=int, default=0, help="nmg_tuning.lanes (0 = library default, 1 = off)")
+    ap.add_argument("--tune", default="", help="extra nmg_tuning fields, e.g. no_fused_coarse=1,no_graphs=1")
     ap.add_argument("--precision", choices=["auto", "mixed", "fp64"], default="auto",
                     help="auto: fp64 cycle for config 0 (BASELINE's fp64 system), mixed otherwise")
     ap.add_argument("--no-cpu", action="store_true")
@@ -304,7 +305,8 @@ def main():
         raise SystemExit(f"rank {rank}: no RHS left for this rank ({cfg.nrhs} RHS over {world} ranks)")
     prec = nmg.PREC_FP64 if args.precision == "fp64" or (args.precision == "auto" and cid == 0) else nmg.PREC_MIXED
     h = nmg.Hierarchy(cfg.dim, cfg.n, cfg.levels, cfg.alpha, factors, nu1=cfg.nu1, nu2=cfg.nu2, max_rhs=B,
-                      device=local, comm=comm, precision=prec, tuning={"lanes": args.lanes})
+                      device=local, comm=comm, precision=prec,
+                      tuning={"lanes": args.lanes, **{k: int(v) for k, v in (kv.split("=") for kv in args.tune.split(",") if kv)}})
     for l, w in enumerate(W):
         h.load_weights(l + 1, ni.cnn_arch(cfg), w)
     y_np = make_y(B, start)
