@@ -91,8 +91,9 @@ typedef struct {
   int32_t no_kron;        /* 1 (2D): Kronecker pair as two plain GEMMs + a stencil pass       */
   int32_t host_chunks;    /* nmg_vcycles_host: 0 = pipelined per RHS lane (default when the
                              handle has lanes), else that many RHS chunks (1..8)             */
-  int32_t no_fused_coarse;/* 1 (1D): run the coarse levels (n_l <= 512) as separate launches
-                             instead of one fused fp64 sub-cycle kernel per RHS              */
+  int32_t fused_coarse;   /* N > 0 (1D): the levels with n_l <= N run as ONE fused fp64 sub-cycle
+                             kernel per RHS (cycle64) instead of per-level launches (opt-in:
+                             slower than the batched kernels for n_l >= 256)                  */
 } nmg_tuning;
 
 /* Problem descriptor (SPEC ProblemSpec analogue). */

@@ -1486,11 +1486,13 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
   const size_t nn = (size_t)n * n;
 
   std::vector<double> Acoarse;
-  if (d.dim == 1 && d.precision == NMG_PREC_MIXED && h->tune.no_fused_coarse == 0) {
-    // the coarse levels (n_l <= 512 and at least one smoothed level) run as one fused fp64
-    // sub-cycle kernel per RHS (cycle64.cu): latency-bound small grids become one launch
+  if (d.dim == 1 && d.precision == NMG_PREC_MIXED && h->tune.fused_coarse > 0) {
+    // opt-in: the coarse levels (n_l <= tune.fused_coarse) run as one fused fp64 sub-cycle
+    // kernel per RHS (cycle64.cu).  Measured slower for the BASELINE shapes (cfg 1, n_l <= 512:
+    // 2.57 vs 1.42 ms per step at 1024 RHS, 0.66 vs 0.58 ms at 128): one CTA per RHS streams
+    // the fp64 operator from L2 for every matvec, where the batched GEMMs read it once per tile
     for (int l = 0; l < h->L - 1; ++l)
-      if (h->n[l] <= 512) { h->l_fuse = l; break; }
+      if (h->n[l] <= h->tune.fused_coarse) { h->l_fuse = l; break; }
   }
   if (d.dim == 1) {
     std::vector<double> A(factors, factors + nn);
