@@ -424,20 +424,22 @@ __global__ void __launch_bounds__(256) combine_rows_fft_kernel(int n, int nrhs, 
   for (int i = threadIdx.x; i < rows * n; i += 256) Zp[i] = cb[i];          // bit-reversed spectra
 }
 
-NMG_D float mask2d(int k1, int k2, int n) {
-  const float q2 = (float)(2 * min(k2, n - k2)) / (float)n;
-  const float q1 = (float)(2 * min(k1, n - k1)) / (float)n;
-  return sqrtf(fmaxf(q1, q2));
-}
+// per-axis profile t[k] = sqrt(2 min(k, n - k) / n); the 2D mask is sqrt(max(q1, q2)) =
+// max(t[k1], t[k2]) (sqrt is monotone and correctly rounded, so this is the same value)
+NMG_D float mask_axis(int k, int n) { return sqrtf((float)(2 * min(k, n - k)) / (float)n); }
 
 // Column pass on a shared-memory tile cb[i2][c] (n x G): forward along i2, mask M'(k1[c], k2),
 // inverse along i2 (unnormalised; the 1/n^2 is applied by the inverse row pass).
 NMG_D void cols_filter_tile(float2* cb, int n, int G, const int* k1s, const float2* __restrict__ tw, int tw_n) {
+  __shared__ float mt[1024];                                 // the per-axis profile (n <= 1024 here)
+  __shared__ float m1s[64];
   const int log2n = 31 - __clz(n);
-  fft_dif_forward_batch(cb, n, G, 1, G, tw, tw_n, threadIdx.x, 256);
+  for (int k = threadIdx.x; k < n; k += 256) mt[bitrev(k, log2n)] = mask_axis(k, n);   // by DIF position
+  for (int c = threadIdx.x; c < G; c += 256) m1s[c] = mask_axis(k1s[c], n);
+  fft_dif_forward_batch(cb, n, G, 1, G, tw, tw_n, threadIdx.x, 256);   // ends with __syncthreads
   for (int i = threadIdx.x; i < n * G; i += 256) {
     const int r = i / G, c = i - r * G;
-    const float m = mask2d(k1s[c], bitrev(r, log2n), n);     // rows were DIF'd: position r holds k2 = bitrev(r)
+    const float m = fmaxf(m1s[c], mt[r]);                   // rows were DIF'd: position r holds k2 = bitrev(r)
     cb[i] = make_float2(cb[i].x * m, cb[i].y * m);
   }
   __syncthreads();

@@ -1453,6 +1453,7 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
   const int Nc = d.dim == 1 ? nc : nc * nc;
   if (Nc > 256) return fail(NMG_ERR_UNSUPPORTED, "coarsest system %d > 256 unknowns", Nc);
   if (d.dim == 1 && d.n > 8192) return fail(NMG_ERR_UNSUPPORTED, "1D n > 8192");
+  if (d.dim == 2 && d.n > 1024) return fail(NMG_ERR_UNSUPPORTED, "2D n > 1024");
 
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= d.device || d.device < 0)
