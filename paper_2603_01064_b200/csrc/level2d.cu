@@ -402,14 +402,28 @@ __global__ void __launch_bounds__(256) combine_rows_fft_kernel(int n, int nrhs, 
   const bool on = norms ? norms[b] != 0.0 : true;
   const int64_t per = (int64_t)n * n;
   const int log2n = 31 - __clz(n);
+  const int lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < rows * n; i += 256) {
     const int r = r0 + i / n, x = i % n;
     float h[2];
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       float acc = 0.f;
-      if (on) {
-        const int64_t idx = (int64_t)b * per + (int64_t)(2 * r + e) * n + x;
+      const int64_t idx = (int64_t)b * per + (int64_t)(2 * r + e) * n + x;
+      if (n >= 32) {
+        // a warp covers 32 consecutive x of one row: one float4 load per pixel, the x -+ 1
+        // neighbours' taps by shuffles (the two warp-edge values loaded directly)
+        const float4 q = on ? __ldg(&Q[idx]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        float left = __shfl_up_sync(0xffffffffu, q.x, 1);
+        float right = __shfl_down_sync(0xffffffffu, q.z, 1);
+        if (lane == 0) left = (on && x > 0) ? __ldg(&Q[idx - 1].x) : 0.f;
+        if (lane == 31) right = (on && x < n - 1) ? __ldg(&Q[idx + 1].z) : 0.f;
+        if (on) {
+          acc = bias + q.y;
+          if (x > 0) acc += left;
+          if (x < n - 1) acc += right;
+        }
+      } else if (on) {
         acc = bias + __ldg(&Q[idx].y);
         if (x > 0) acc += __ldg(&Q[idx - 1].x);
         if (x < n - 1) acc += __ldg(&Q[idx + 1].z);
