@@ -138,6 +138,17 @@ def operator_factors(cfg: Config, paper_form: bool = False) -> Tuple[np.ndarray,
     raise ValueError(cfg.kernel)
 
 
+def anisotropic_factors(cfg: Config, alpha: float) -> Tuple[np.ndarray]:
+    """The paper's anisotropic 1D system A = alpha D + K with D = diag(a(t_i)),
+    a(z) = 1 + 0.5 sin(2 pi z), as the G of A = G + alpha I:
+    G = K + alpha (D - I) (dense, symmetric).  Problem data only."""
+    assert cfg.dim == 1
+    K = gaussian_kernel_1d(cfg.n, cfg.sigma)
+    a = 1.0 + 0.5 * np.sin(2.0 * math.pi * grid_points(cfg.n))
+    G = K + alpha * np.diag(a - 1.0)
+    return (0.5 * (G + G.T),)
+
+
 def truncated_kernel_2d_cfg4(n: int, sigma: float, tol: float = 1e-12):
     """Direct (non-Kronecker) config-4 stencil, truncated where the unnormalised
     value exp(-|d|^2/(2 s^2)) (1 + 0.3 cos(2 pi d1)) < tol (reading R2/R17).

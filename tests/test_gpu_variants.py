@@ -143,3 +143,43 @@ def test_precision_fp64_cfg0(kind, tol, cycles):
     x3 = torch.zeros_like(yd)
     h.solve(yd, x3, tol=1e-300, max_cycles=3)
     assert torch.equal(x2, x3)
+
+
+def test_anisotropic_operator_1d():
+    """NEXT-3: the paper's anisotropic system A = alpha D + K, a(z) = 1 + 0.5 sin 2 pi z
+    (PAPER.md:517-521), passed as G = K + alpha (D - I); histories vs the oracle."""
+    cfg = ni.CONFIGS[0].replace(alpha=1e-2)
+    f = ni.anisotropic_factors(cfg, cfg.alpha)
+    W = weights_for(cfg, "seed")
+    H = oracle_hierarchy(cfg, f, W)
+    h = gpu_hierarchy(cfg, f, W, max_rhs=cfg.nrhs)
+    y, _ = ni.make_rhs(cfg, f, cfg.alpha)
+    yd = torch.tensor(y, dtype=torch.float64, device=DEV)
+    rep = h.solve(yd, torch.zeros_like(yd), tol=1e-300, max_cycles=4)
+    orc = O.solve(H, y, tol=1e-300, max_cycles=4, freeze=False)
+    ok, err = history_close(rep["history"], orc.history)
+    assert ok, err
+
+
+@pytest.mark.parametrize("Lp", [5, 6])
+def test_level_truncation_Lprime(Lp):
+    """NEXT-3: test-time truncation L': smoothers trained on the 6-level
+    config-1 hierarchy (W_train, alpha 1e-3), solved on the first L' levels with an exact solve
+    at level L' (n_L' <= 256); converges to 1e-6 at the oracle's stopping cycles."""
+    cfg = ni.CONFIGS[1].replace(alpha=1e-3)
+    W = ni.weights_trained(cfg)
+    if W is None:
+        pytest.skip("no trained weights")
+    c = cfg.replace(levels=Lp, nrhs=8)
+    f = ni.operator_factors(c)
+    Wl = W[:Lp - 1]
+    H = oracle_hierarchy(c, f, Wl)
+    h = gpu_hierarchy(c, f, Wl, max_rhs=8)
+    y, _ = ni.make_rhs(c, f, c.alpha, nrhs=8)
+    yd = torch.tensor(y, dtype=torch.float64, device=DEV)
+    rep = h.solve(yd, torch.zeros_like(yd), tol=1e-6, max_cycles=60)
+    orc = O.solve(H, y, tol=1e-6, max_cycles=60)
+    assert orc.converged.all() and rep["converged"].all()
+    ok, err = history_close(rep["history"], orc.history)
+    assert ok, err
+    assert np.abs(rep["cycles"] - orc.cycles).max() <= 1
