@@ -87,3 +87,32 @@ def test_short_training_converges_cfg0():
     assert np.all(hist[-10:].mean(axis=0) < 0.5 * hist[:10].mean(axis=0))
     h = T.eval_solve(cfg, cfg.alpha, w, nrhs=4, max_cycles=40)
     assert np.nanmax(h[:, -1]) <= 1e-6
+
+
+@pytest.mark.parametrize("dim", [1, 2])
+def test_fno_module_matches_oracle(dim):
+    """The trainer's FNO (torch.fft) equals the oracle's FNO (numpy loops over modes, Appendix A
+    P:651-657) on the same flat Table-6 parameters, and export() folds the 1/alpha gain."""
+    n = 64 if dim == 1 else 32
+    cfg = ni.CONFIGS[0] if dim == 1 else ni.CONFIGS[2].replace(n=32, levels=3, nrhs=3)
+    arch = ni.fno_arch(dim, n)
+    cfg = cfg.replace(n=n)
+    w = ni.fno_weights_seed(cfg, seed=5)[0]
+    net = T.FNO(dim, n, w, out_scale=1e3, dtype=torch.float64)
+    u = np.random.default_rng(1).standard_normal((2,) + (n,) * dim)
+    want = O.fno_forward(O.fno_params(dim, *arch, w), u)
+    assert np.abs(net(torch.tensor(u)).detach().numpy() - want).max() < 1e-10 * np.abs(want).max()
+    plain = T.FNO(dim, n, net.export(), dtype=torch.float64)
+    assert np.abs(plain(torch.tensor(u)).detach().numpy() - want).max() < 1e-5 * np.abs(want).max()
+
+
+def test_fno_short_training_converges():
+    """Level-wise training (Alg 5) of the FNO smoothers lowers the losses and the trained cycle
+    converges on config 0 (the paper's own smoother, Appendix A)."""
+    cfg = ni.CONFIGS[0]
+    torch.manual_seed(0)
+    w, hist = T.train(cfg, cfg.alpha, ni.fno_weights_seed(cfg), 40, arch="fno", verbose=False)
+    hist = np.asarray(hist)
+    assert np.all(hist[-5:].mean(0) < hist[:5].mean(0))
+    h = T.eval_solve(cfg, cfg.alpha, w, nrhs=2, max_cycles=60, arch="fno")
+    assert np.nanmax(h[:, -1]) < 1e-6

@@ -200,6 +200,63 @@ class CNN(torch.nn.Module):
         return ni.flatten_params(layers)
 
 
+class FNO(torch.nn.Module):
+    """The paper's FNO smoother (Appendix A, Table 6; readings R23/R24) for level n:
+    lift 1 -> c, L Fourier layers GELU(irfft(R . rfft(Z)_k) + W * Z + B), proj c -> 1.  Same flat
+    parameter layout as the library's nmg_load_fno_weights (nmg_inputs.fno_param_shapes)."""
+
+    def __init__(self, dim, n, flat, out_scale: float = 1.0, device="cpu", dtype=torch.float32, width=None):
+        super().__init__()
+        self.dim, self.n, self.out_scale = dim, n, out_scale
+        self.arch = ni.fno_arch(dim, n, width)
+        c, L, k, ks = self.arch
+        P = ni.fno_unflatten(dim, c, L, k, ks, np.asarray(flat, np.float64))
+        t = lambda a: torch.nn.Parameter(torch.tensor(a, dtype=dtype, device=device))   # noqa: E731
+        self.lift_w, self.lift_b = t(P["lift_w"]), t(P["lift_b"])
+        self.spec = torch.nn.ParameterList([t(P[f"spec{i}"]) for i in range(L)])
+        self.conv = torch.nn.ParameterList([t(P[f"conv{i}"]) for i in range(L)])
+        self.bias = torch.nn.ParameterList([t(P[f"bias{i}"]) for i in range(L)])
+        self.proj_w = t(P["proj_w"] / out_scale)
+        self.proj_b = t(P["proj_b"] / out_scale)
+
+    def forward(self, u):
+        c, L, k, ks = self.arch
+        n = self.n
+        z = F.linear(u[..., None], self.lift_w, self.lift_b).movedim(-1, 1)      # [B][c][...]
+        for i in range(L):
+            R = torch.complex(self.spec[i][..., 0], self.spec[i][..., 1])
+            if self.dim == 1:
+                Z = torch.fft.rfft(z, dim=-1)[..., :k]
+                Yp = torch.zeros(z.shape[0], c, n // 2 + 1, dtype=Z.dtype, device=z.device)
+                Yp[..., :k] = torch.einsum("bcm,mco->bom", Z, R)
+                sp = torch.fft.irfft(Yp, n=n, dim=-1)
+                w = F.conv1d(z, self.conv[i], self.bias[i], padding=ks // 2)
+            else:
+                Z = torch.fft.rfft2(z)
+                Yp = torch.zeros(z.shape[0], c, n, n // 2 + 1, dtype=Z.dtype, device=z.device)
+                Yp[:, :, :k, :k] = torch.einsum("bcjm,jmco->bojm", Z[:, :, :k, :k], R[:k])
+                Yp[:, :, n - k:, :k] = torch.einsum("bcjm,jmco->bojm", Z[:, :, n - k:, :k], R[k:])
+                sp = torch.fft.irfft2(Yp, s=(n, n))
+                w = F.conv2d(z, self.conv[i], self.bias[i], padding=ks // 2)
+            z = F.gelu(sp + w)
+        return F.linear(z.movedim(1, -1), self.proj_w, self.proj_b)[..., 0] * self.out_scale
+
+    def export(self) -> np.ndarray:
+        parts = [self.lift_w, self.lift_b]
+        for i in range(len(self.spec)):
+            parts += [self.spec[i], self.conv[i], self.bias[i]]
+        out = [p.detach().double().cpu().numpy().ravel() for p in parts]
+        out += [(self.proj_w.detach().double().cpu().numpy() * self.out_scale).ravel(),
+                (self.proj_b.detach().double().cpu().numpy() * self.out_scale).ravel()]
+        return np.concatenate(out).astype(np.float32)
+
+
+def make_nets(cfg, weights, arch, out_scale=1.0, device="cpu", dtype=torch.float32):
+    if arch == "fno":
+        return [FNO(cfg.dim, cfg.n >> l, w, out_scale, device, dtype) for l, w in enumerate(weights)]
+    return [CNN(cfg, w, out_scale, device, dtype) for w in weights]
+
+
 def smooth(lv: TorchLevels, nets, l, x, y):
     """One smoothing step (Alg 3): b = y - A x, h = N(b/||b||)||b||, x + F'(h)."""
     b = y - lv.apply(l, x) if x is not None else y
@@ -262,7 +319,10 @@ class NmgRollout:
 
     def load(self, nets):
         for l, net in enumerate(nets):
-            self.h.load_weights(l + 1, ni.cnn_arch(self.cfg), net.export())
+            if isinstance(net, FNO):
+                self.h.load_fno_weights(l + 1, net.arch, net.export())
+            else:
+                self.h.load_weights(l + 1, ni.cnn_arch(self.cfg), net.export())
 
     def __call__(self, y):
         yd = y.to(torch.float64).contiguous()
@@ -302,10 +362,10 @@ def data_generation(lv: TorchLevels, nets, nbs: int, K: int, rng: np.random.Gene
 
 # ------------------------------------------------------------------------------------------
 def train(cfg, alpha: float, init: List[np.ndarray], epochs: int, nbs: int = 20, K: int = 10, lr: float = 1e-3,
-          device="cpu", seed: int = 0, rollout: str = "torch", log_every: int = 100, verbose=True):
+          device="cpu", seed: int = 0, rollout: str = "torch", log_every: int = 100, verbose=True, arch="cnn"):
     factors = ni.operator_factors(cfg)
     lv = TorchLevels(cfg, factors, alpha, device)
-    nets = [CNN(cfg, w, out_scale=1.0 / alpha, device=device) for w in init]
+    nets = make_nets(cfg, init, arch, out_scale=1.0 / alpha, device=device)
     opts = [torch.optim.Adam(n.parameters(), lr=lr) for n in nets]
     # linear warm-up over the first 5 % of the epochs (a curriculum stage starts from the previous
     # alpha's smoother under a 10x larger output gain), then cosine decay to 2 % of lr
@@ -340,12 +400,12 @@ def train(cfg, alpha: float, init: List[np.ndarray], epochs: int, nbs: int = 20,
 
 
 @torch.no_grad()
-def eval_solve(cfg, alpha, weights, nrhs=16, max_cycles=100, device="cpu", tol=1e-6):
+def eval_solve(cfg, alpha, weights, nrhs=16, max_cycles=100, device="cpu", tol=1e-6, arch="cnn"):
     """Relative-residual histories of the trained cycle (transcription, fp64) on the problem's
     own seeded right-hand sides: a quick convergence check (the parity check is the oracle's)."""
     factors = ni.operator_factors(cfg)
     lv = TorchLevels(cfg, factors, alpha, device, dtype=torch.float64)
-    nets = [CNN(cfg, w, device=device, dtype=torch.float64) for w in weights]
+    nets = make_nets(cfg, weights, arch, device=device, dtype=torch.float64)
     y, _ = ni.make_rhs(cfg, factors, alpha, nrhs=nrhs)
     y = torch.tensor(y, dtype=torch.float64, device=device)
     x = torch.zeros_like(y)
@@ -361,11 +421,12 @@ def eval_solve(cfg, alpha, weights, nrhs=16, max_cycles=100, device="cpu", tol=1
     return torch.stack(hist, 1).numpy()
 
 
-def save(cfg, alpha, weights, hist, extra=None, out_dir=OUT_DIR):
+def save(cfg, alpha, weights, hist, extra=None, out_dir=OUT_DIR, arch="cnn"):
     os.makedirs(out_dir, exist_ok=True)
-    p = os.path.join(out_dir, f"W_train_{cfg.name}_a{alpha:g}.npz")
-    np.savez_compressed(p, weights=np.stack(weights), loss_history=hist, alpha=alpha, config=cfg.name,
-                        **(extra or {}))
+    tag = "" if arch == "cnn" else "_fno"
+    p = os.path.join(out_dir, f"W_train{tag}_{cfg.name}_a{alpha:g}.npz")
+    w = np.stack(weights) if arch == "cnn" else np.array(weights, dtype=object)
+    np.savez_compressed(p, weights=w, loss_history=hist, alpha=alpha, config=cfg.name, **(extra or {}))
     return p
 
 
@@ -384,6 +445,7 @@ def main():
     ap.add_argument("--n", type=int, default=None, help="override the grid size (quick runs)")
     ap.add_argument("--levels", type=int, default=None)
     ap.add_argument("--out", default=OUT_DIR)
+    ap.add_argument("--arch", choices=["cnn", "fno"], default="cnn", help="fno: the paper's smoother (Table 6)")
     args = ap.parse_args()
     cfg = ni.CONFIGS[args.config]
     if args.n:
@@ -393,7 +455,9 @@ def main():
     torch.backends.cuda.matmul.allow_tf32 = False
     torch.backends.cudnn.allow_tf32 = False
     rollout = args.rollout or ("nmg" if dev == "cuda" else "torch")
-    if args.init == "trained":
+    if args.arch == "fno":
+        w = ni.fno_weights_seed(cfg)
+    elif args.init == "trained":
         w = ni.weights_trained(cfg.replace(alpha=args.init_alpha))
         assert w is not None, "no trained weights at --init-alpha"
     else:
@@ -401,12 +465,12 @@ def main():
     for a in sorted(alphas, reverse=True):
         c = cfg.replace(alpha=a)
         t0 = time.time()
-        w, hist = train(c, a, w, args.epochs, args.nbs, args.K, args.lr, dev, rollout=rollout)
-        h = eval_solve(c, a, w, device=dev)
+        w, hist = train(c, a, w, args.epochs, args.nbs, args.K, args.lr, dev, rollout=rollout, arch=args.arch)
+        h = eval_solve(c, a, w, device=dev, arch=args.arch)
         last = h[:, -1]
         print(f"alpha {a:g}: trained in {time.time() - t0:.0f} s; eval {h.shape[1] - 1} cycles, "
               f"max final relres {np.nanmax(last):.3e}", flush=True)
-        print("saved", save(c, a, w, hist, {"eval_history": h}, args.out), flush=True)
+        print("saved", save(c, a, w, hist, {"eval_history": h}, args.out, args.arch), flush=True)
 
 
 if __name__ == "__main__":
