@@ -352,6 +352,13 @@ def main():
     tot_prof = sum(v[0] for v in prof.values())
     counts = algorithmic_counts(cfg, B)
     pk = peaks()
+    clocks = clk.summary()
+    # the burst figure for a kernel timed alone, the sustained one for a kernel inside a long
+    # step: a timed region that drove the GPU into its power cap is the condition the sustained
+    # matmul figure was measured under (MEASURED_PEAKS.json "how")
+    sustained = "sw_power_cap" in clocks["reasons"] and "bf16_tflops_sustained" in pk
+    bf16_burst = pk["bf16_tflops"]
+    bf16 = pk["bf16_tflops_sustained"] if sustained else bf16_burst
     dom = max(prof, key=lambda k: prof[k][0])
     dom_ms, dom_n = prof[dom]
     step_ms = dom_ms / psteps                           # all launches of the class in one step
@@ -361,14 +368,14 @@ def main():
             traffic = json.load(fh).get(f"cfg{cid}", {}).get(dom)   # ncu dram read+write bytes per step
     except Exception:
         pass
-    f16x3_peak = pk["bf16_tflops"] / 3.0      # f16 dense = bf16 dense rate; 3 products per fp32-accurate MAC
+    f16x3_peak = bf16 / 3.0      # f16 dense = bf16 dense rate; 3 products per fp32-accurate MAC
     if dom == "gemm64":
-        peak = pk["bf16_tflops"] * FP64_NOMINAL_RATIO
+        peak = bf16 * FP64_NOMINAL_RATIO
         achieved = counts["gemm64"] / (step_ms * 1e-3) / 1e12
         roof = {"kernel": "fp64 outer residual (Ozaki int8 tcgen05 / DMMA)", "bound": "tensor", "unit": "TFLOP/s",
                 "peak_note": "FP64 tensor: measured bf16 x nominal fp64/bf16 ratio 45/2250"}
     elif dom == "gemm32":
-        peak = pk["bf16_tflops"] * TF32_NOMINAL_RATIO / 3.0
+        peak = bf16 * TF32_NOMINAL_RATIO / 3.0
         achieved = counts["gemm32"] / (step_ms * 1e-3) / 1e12
         roof = {"kernel": "tc_gemm_kernel (3xTF32 tcgen05, all levels)", "bound": "tensor", "unit": "TFLOP/s",
                 "peak_note": "TF32 tensor (measured bf16 x 1.1/2.25) / 3 passes"}
@@ -395,7 +402,9 @@ def main():
     roof.update({"achieved": achieved, "peak": peak, "frac": achieved / peak, "traffic": traffic,
                  "traffic_note": (f"ncu dram__bytes_read+write of the {dom} class per step (cfg{cid}), profiles/traffic.json"
                                   if traffic else None),
-                 "peak_source": pk["source"],
+                 "peak_source": pk["source"] + (" bf16_tflops_sustained (run at sw_power_cap)" if sustained
+                                                else (" bf16_tflops (burst)" if roof["bound"] == "tensor" else " hbm_gbs")),
+                 "frac_vs_burst_peak": (achieved / (peak * bf16_burst / bf16)) if roof["bound"] == "tensor" else None,
                  "share_of_step": dom_ms / tot_prof if tot_prof else None,
                  "classes_ms_per_step": {k: v[0] / psteps for k, v in prof.items()},
                  "launches_per_step": {k: v[1] / psteps for k, v in prof.items()}})
@@ -510,7 +519,7 @@ def main():
                            "l2": ("working set fits L2 (latency-bound config, no flush)" if cid == 0
                                   else "inputs larger than L2 (no flush)")},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "solve": solve,
-                "gpu_launches": launches, "clocks": clk.summary()}
+                "gpu_launches": launches, "clocks": clocks}
         print(json.dumps(line))
     if comm is not None:
         h.close()

@@ -17,6 +17,7 @@ for t in ${@:-cfg3}; do
     ozaki1d) run ozaki1d 1 ozaki_resid 1 "--lanes 1" ;;
     cfg3) run cfg3 3 "conv_strip|fft_cols|fft_rows|combine_rows_fft|ozaki_resid|kron_tc|norms|sumsq" 14 ;;
     cfg2) run cfg2 2 "conv_strip|fft_cols|fft_rows|combine_rows_fft" 6 ;;
+    strip3) run strip3 3 "conv_strip" 2 ;;
     fft3) run fft3 3 "fft_cols|fft_rows|combine_rows_fft|sumsq_partial" 4 "--lanes 1" ;;
   esac
 done
