@@ -44,6 +44,19 @@ NMG_D void zput(float2* Z, int rows, int n, int b, int y, int x, float v) {
   reinterpret_cast<float*>(Z)[(int64_t)b * rows * n + (int64_t)(y >> 1) * 2 * n + 2 * x + (y & 1)] = v;
 }
 
+// 2D CNN output h(y, x) = b3 + Q0(x - 1) + Q1(x) + Q2(x + 1) (conv_strip.cu): the strip kernel
+// stores v = the sum without the terms that cross its 128-pixel strip boundary and, per (image
+// row, strip), the edge record E = {Q2(X0), Q0(X0 + 127), Q2(X0 + 1)}; this completes pixel x of
+// a row whose records start at E (the same additions in the same order as a whole-row sum)
+constexpr int kStripSeg = 128;
+NMG_D float strip_h_fix(float v, const float4* __restrict__ E, int n, int x) {
+  if (n < kStripSeg) return v;
+  const int m = x & (kStripSeg - 1), st = x / kStripSeg;
+  if (m == 0 && x > 0) return (v + __ldg(&E[st - 1].y)) + __ldg(&E[st].z);
+  if (m == kStripSeg - 1 && x < n - 1) return v + __ldg(&E[st + 1].x);
+  return v;
+}
+
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is a per-DEVICE property: set it once per
 // (call site, device).  `done` is the call site's bitmask of devices already configured (a
 // concurrent double set is harmless: the call is idempotent).

@@ -137,13 +137,16 @@ NMG_D void tload(uint32_t taddr, uint32_t* r) {
   }
 }
 
-// 8 fp32 (already scaled) -> f16 hi (8) and lo (8) packed as uint4
+// 8 fp32 (already scaled) -> f16 hi (8) and lo (8) packed as uint4; the residual v - hi of a
+// channel pair is one packed FADD2 (each lane rounds as the scalar subtraction: same bits)
 NMG_D void split8(const float* v, uint4& hi, uint4& lo) {
   uint32_t h[4], l[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const __half2 hv = __floats2half2_rn(v[2 * j], v[2 * j + 1]);
-    const __half2 lv = __floats2half2_rn(v[2 * j] - __low2float(hv), v[2 * j + 1] - __high2float(hv));
+    const float2 hf = __half22float2(hv);
+    const float2 r = __fadd2_rn(make_float2(v[2 * j], v[2 * j + 1]), make_float2(-hf.x, -hf.y));
+    const __half2 lv = __floats2half2_rn(r.x, r.y);
     h[j] = *reinterpret_cast<const uint32_t*>(&hv);
     l[j] = *reinterpret_cast<const uint32_t*>(&lv);
   }
@@ -340,11 +343,18 @@ __global__ void __launch_bounds__(Roles<C, FIRST>::NTHR, 1)
 #pragma unroll
                 for (int c = 0; c < 4; ++c) { v[e][2 * c] = v2[e][c].x; v[e][2 * c + 1] = v2[e][c].y; }
 #pragma unroll
-                for (int c = 0; c < 8; ++c) v[e][c] = xin[e] ? fmaxf(v[e][c], 0.f) : 0.f;
+                for (int c = 0; c < 8; ++c) v[e][c] = fmaxf(v[e][c], 0.f);
                 uint4 hi, lo;
                 split8(v[e], hi, lo);
-                ah[g * RP + j + e * PP] = hi;
-                al[g * RP + j + e * PP] = lo;
+                // a position outside the image is zero padding of layer 2's input: predicated
+                // zero stores instead of a select per channel
+                if (xin[e]) {
+                  ah[g * RP + j + e * PP] = hi;
+                  al[g * RP + j + e * PP] = lo;
+                } else {
+                  ah[g * RP + j + e * PP] = make_uint4(0u, 0u, 0u, 0u);
+                  al[g * RP + j + e * PP] = make_uint4(0u, 0u, 0u, 0u);
+                }
               }
             }
           }
@@ -458,6 +468,8 @@ __global__ void __launch_bounds__(Roles<C, FIRST>::NTHR, 1)
     const float* bv = sbias + c0;
     const float dsc = a.d_scale;
     const float osc = a.out_scale;
+    const float b3v = FIRST ? 0.f : __ldg(a.b3);
+    float* xch = reinterpret_cast<float*>(misc + 4096);     // [2][4 warps][Q0 of lane 31, Q2 of lane 0]
     int k = 0, e4 = 0;
     float acc4[3][3];                        // layer 4 partial rows h(ya - 1 + i) (FIRST == false)
 #pragma unroll
@@ -480,10 +492,36 @@ __global__ void __launch_bounds__(Roles<C, FIRST>::NTHR, 1)
         for (int t2 = 0; t2 < 3; ++t2)
 #pragma unroll
           for (int t1 = 0; t1 < 3; ++t1) acc4[2 - t2][t1] = fmaf(__uint_as_float(d[t2 * 3 + t1]), s4, acc4[2 - t2][t1]);
+        // h(yh, x) = b3 + Q0(x - 1) + Q1(x) + Q2(x + 1) (in this order): the x -+ 1 taps of
+        // the neighbouring pixels by shuffles inside the warp and through shared memory across
+        // the four lane-quarter warps; the strip's first and last pixel lack the term from the
+        // neighbouring strip and are finished by strip_combine / combine_rows_fft from the
+        // strip-edge records {Q2(X0), Q0(X0 + 127), Q2(X0 + 1)} (same summation order, so the
+        // result is bitwise the one of a whole-row combine)
         const int yh = ya - 1;
-        if (yh >= t.y0 && yh < t.y1 && x < n)
-          reinterpret_cast<float4*>(a.q)[((int64_t)t.b * hg + yh) * n + x] =
-              make_float4(acc4[0][0], acc4[0][1], acc4[0][2], 0.f);
+        const float Q0 = acc4[0][0], Q1 = acc4[0][1], Q2 = acc4[0][2];
+        float left = __shfl_up_sync(0xffffffffu, Q0, 1);
+        float right = __shfl_down_sync(0xffffffffu, Q2, 1);
+        float* xw = xch + 8 * (e4 & 1);
+        if (lane == 31) xw[2 * q] = Q0;
+        if (lane == 0) xw[2 * q + 1] = Q2;
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        if (lane == 0 && q > 0) left = xw[2 * (q - 1)];
+        if (lane == 31 && q < 3) right = xw[2 * (q + 1) + 1];
+        if (yh >= t.y0 && yh < t.y1 && x < n) {
+          const int64_t row = (int64_t)t.b * hg + yh;
+          float* er = reinterpret_cast<float*>(a.qe + row * nx + (t.X0 / SEG));
+          float v = b3v + Q1;
+          if (m == 0 && x > 0) {            // Q0(x - 1) belongs to the strip on the left
+            er[2] = right;
+          } else {
+            if (x > 0) v += left;
+            if (x < n - 1 && m != SEG - 1) v += right;   // else Q2(x + 1) is the right strip's
+          }
+          a.q[row * n + x] = v;
+          if (m == 0) er[0] = Q2;
+          if (m == SEG - 1) er[1] = Q0;
+        }
 #pragma unroll
         for (int t1 = 0; t1 < 3; ++t1) {
           acc4[0][t1] = acc4[1][t1];
@@ -605,10 +643,12 @@ __global__ void __launch_bounds__(Roles<C, FIRST>::NTHR, 1)
   }
 }
 
-// h(y, x) = s (b3 + Q0(y, x - 1) + Q1(y, x) + Q2(y, x + 1))  ->  Z = (h, 0) or x (+)= h
+// h(y, x) = s (b3 + Q0(y, x - 1) + Q1(y, x) + Q2(y, x + 1))  ->  Z = (h, 0) or x (+)= h.  The strip
+// kernel stored the sum without the terms that cross a 128-pixel strip boundary; the strip's
+// edge record E = {Q2(X0), Q0(X0 + 127), Q2(X0 + 1)} supplies them (strip_h_fix, common.cuh).
 // slab mode: images of hg rows whose first and last hh rows are halo (not written)
-__global__ void strip_combine_kernel(int n, int nrhs, const float4* __restrict__ Q, const double* __restrict__ norms,
-                                     const float* __restrict__ b3, float2* __restrict__ Z, int zb0,
+__global__ void strip_combine_kernel(int n, int nrhs, const float* __restrict__ q, const float4* __restrict__ qe,
+                                     const double* __restrict__ norms, float2* __restrict__ Z, int zb0,
                                      float* __restrict__ xo, int accumulate, int hg, int hh) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t per = (int64_t)hg * n;
@@ -619,11 +659,7 @@ __global__ void strip_combine_kernel(int n, int nrhs, const float4* __restrict__
   if (row < hh || row >= hg - hh) return;
   const double s = norms ? norms[b] : 1.0;
   float acc = 0.f;
-  if (s != 0.0) {
-    acc = __ldg(b3) + __ldg(&Q[idx].y);
-    if (x > 0) acc += __ldg(&Q[idx - 1].x);
-    if (x < n - 1) acc += __ldg(&Q[idx + 1].z);
-  }
+  if (s != 0.0) acc = strip_h_fix(__ldg(&q[idx]), qe + ((int64_t)b * hg + row) * (n / SEG), n, x);
   // the filter path takes N(u) unscaled; filter2d multiplies by s after F'
   if (Z) zput(Z, hg - 2 * hh, n, zb0 + b, row - hh, x, acc);
   else {
@@ -660,12 +696,12 @@ void strip_l34(const CUtensorMap* mh, const CUtensorMap* ml, const StripArgs& a,
   if (a.C == 32) launch<32, false>(mh, ml, a, num_sms, s);
   else launch<48, false>(mh, ml, a, num_sms, s);
 }
-void strip_combine(int n, int nrhs, const float* q, const double* norms, const float* b3, float2* Z, int zb0,
+void strip_combine(int n, int nrhs, const float* q, const float4* qe, const double* norms, float2* Z, int zb0,
                    float* x, bool accumulate, cudaStream_t s, int hg, int hh) {
   if (hg <= 0) hg = n;
   const int64_t tot = (int64_t)nrhs * hg * n;
-  strip_combine_kernel<<<(int)ceil_div64(tot, 256), 256, 0, s>>>(n, nrhs, reinterpret_cast<const float4*>(q), norms,
-                                                                 b3, Z, zb0, x, accumulate ? 1 : 0, hg, hh);
+  strip_combine_kernel<<<(int)ceil_div64(tot, 256), 256, 0, s>>>(n, nrhs, q, qe, norms, Z, zb0, x, accumulate ? 1 : 0,
+                                                                 hg, hh);
 }
 
 }  // namespace nmg

@@ -217,7 +217,7 @@ void filter2d(int nrhs, int n, float2* Z, const float2* tw, int tw_n, float* x, 
               const double* norms, bool rows_done = false);
 // strip_combine fused with filter2d's forward row FFTs: Z_b (b = zb0 ..) of the chunk's RHS hold
 // the row-transformed N(u) (0 where ||b|| = 0)
-void combine_rows_fft(int n, int nrhs, const float* q, const double* norms, const float* b3, float2* Z, int zb0,
+void combine_rows_fft(int n, int nrhs, const float* q, const float4* qe, const double* norms, float2* Z, int zb0,
                       const float2* tw, int tw_n, cudaStream_t s);
 // per-RHS sum of squares (no sqrt) of N values at x + b img + off
 void sumsq_f32(int nrhs, int64_t N, const float* x, int64_t img, int64_t off, double* part, int chunks, double* out,
@@ -251,7 +251,9 @@ struct StripArgs {
   float d_scale;              // 1 / (S T) of this layer
   uint16_t* out_h;            // l12: a2 hi/lo
   uint16_t* out_l;
-  float* q;                   // l34: float4 [nrhs][n][n]
+  float* q;                   // l34: the CNN output h without its strip-edge terms, [nrhs][h][n]
+  float4* qe;                 // l34: strip-edge records [nrhs][h][n / 128] (see strip_combine)
+  const float* b3;            // l34: last-layer bias (1 value)
   const uint16_t* w4;         // l34: layer-4 weights x T4, f16 hi then lo, [C/8][16][8] (row t2*3+t1)
   float a3_scale;             // l34: S3 (a3 is split as a3 S3)
   float d4_scale;             // l34: 1 / (S3 T4)
@@ -263,7 +265,7 @@ struct StripArgs {
 int strip_ysplit(int n, int nrhs, int num_sms, int hg = 0);
 void strip_l12(const StripArgs& a, int num_sms, cudaStream_t s);
 void strip_l34(const CUtensorMap* mh, const CUtensorMap* ml, const StripArgs& a, int num_sms, cudaStream_t s);
-void strip_combine(int n, int nrhs, const float* q, const double* norms, const float* b3, float2* Z, int zb0,
+void strip_combine(int n, int nrhs, const float* q, const float4* qe, const double* norms, float2* Z, int zb0,
                    float* x, bool accumulate, cudaStream_t s, int hg = 0, int hh = 0);
 
 

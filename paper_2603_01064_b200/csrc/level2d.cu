@@ -387,50 +387,53 @@ __global__ void __launch_bounds__(256) fft_rows_kernel(int n, int64_t nrows, flo
 }
 
 // combine + forward row FFT: CTA = R complex rows of one RHS; complex row r = (h(2r, .), h(2r+1, .))
-// with h(y, x) = b3 + Q0(y, x-1) + Q1(y, x) + Q2(y, x+1), 0 for a RHS with ||b|| = 0
-__global__ void __launch_bounds__(256) combine_rows_fft_kernel(int n, int nrhs, const float4* __restrict__ Q,
+// with h the strip kernel's output completed at the strip edges (strip_h_fix), 0 for a RHS with
+// ||b|| = 0.  Four consecutive pixels of both rows per thread (two float4 loads).
+__global__ void __launch_bounds__(256) combine_rows_fft_kernel(int n, int nrhs, const float* __restrict__ q,
+                                                               const float4* __restrict__ qe,
                                                                const double* __restrict__ norms,
-                                                               const float* __restrict__ b3, float2* __restrict__ Z,
-                                                               int zb0, const float2* __restrict__ tw, int tw_n) {
+                                                               float2* __restrict__ Z, int zb0,
+                                                               const float2* __restrict__ tw, int tw_n) {
   extern __shared__ __align__(16) float2 cb[];
   const int R = max(1, 4096 / n);
   const int half = n / 2;
   const int rpi = (half + R - 1) / R;                      // CTAs per RHS
   const int b = blockIdx.x / rpi, r0 = (blockIdx.x - b * rpi) * R;
   const int rows = min(R, half - r0);
-  const float bias = __ldg(b3);
   const bool on = norms ? norms[b] != 0.0 : true;
   const int64_t per = (int64_t)n * n;
-  const int log2n = 31 - __clz(n);
-  const int lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < rows * n; i += 256) {
-    const int r = r0 + i / n, x = i % n;
-    float h[2];
+  const int nx = n / kStripSeg;
+  if (n % 4 == 0) {
+    for (int i4 = threadIdx.x; i4 < rows * n / 4; i4 += 256) {
+      const int i = 4 * i4;
+      const int r = r0 + i / n, x = i % n;
+      float h[2][4];
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      float acc = 0.f;
-      const int64_t idx = (int64_t)b * per + (int64_t)(2 * r + e) * n + x;
-      if (n >= 32) {
-        // a warp covers 32 consecutive x of one row: one float4 load per pixel, the x -+ 1
-        // neighbours' taps by shuffles (the two warp-edge values loaded directly)
-        const float4 q = on ? __ldg(&Q[idx]) : make_float4(0.f, 0.f, 0.f, 0.f);
-        float left = __shfl_up_sync(0xffffffffu, q.x, 1);
-        float right = __shfl_down_sync(0xffffffffu, q.z, 1);
-        if (lane == 0) left = (on && x > 0) ? __ldg(&Q[idx - 1].x) : 0.f;
-        if (lane == 31) right = (on && x < n - 1) ? __ldg(&Q[idx + 1].z) : 0.f;
-        if (on) {
-          acc = bias + q.y;
-          if (x > 0) acc += left;
-          if (x < n - 1) acc += right;
+      for (int e = 0; e < 2; ++e) {
+        const int64_t row = (int64_t)b * n + 2 * r + e;
+        float4 v = on ? __ldg(reinterpret_cast<const float4*>(q + row * n + x)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (on && n >= kStripSeg) {
+          const float4* E = qe + row * nx;
+          v.x = strip_h_fix(v.x, E, n, x);          // x % 4 == 0: a possible strip start
+          v.w = strip_h_fix(v.w, E, n, x + 3);      // x % 4 == 3: a possible strip end
         }
-      } else if (on) {
-        acc = bias + __ldg(&Q[idx].y);
-        if (x > 0) acc += __ldg(&Q[idx - 1].x);
-        if (x < n - 1) acc += __ldg(&Q[idx + 1].z);
+        h[e][0] = v.x; h[e][1] = v.y; h[e][2] = v.z; h[e][3] = v.w;
       }
-      h[e] = acc;
+      float4* c4 = reinterpret_cast<float4*>(cb + i);
+      c4[0] = make_float4(h[0][0], h[1][0], h[0][1], h[1][1]);
+      c4[1] = make_float4(h[0][2], h[1][2], h[0][3], h[1][3]);
     }
-    cb[i] = make_float2(h[0], h[1]);
+  } else {
+    for (int i = threadIdx.x; i < rows * n; i += 256) {
+      const int r = r0 + i / n, x = i % n;
+      float h[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t row = (int64_t)b * n + 2 * r + e;
+        h[e] = on ? strip_h_fix(__ldg(&q[row * n + x]), qe + row * nx, n, x) : 0.f;
+      }
+      cb[i] = make_float2(h[0], h[1]);
+    }
   }
   __syncthreads();
   fft_dif_forward_batch(cb, n, rows, n, 1, tw, tw_n, threadIdx.x, 256);
@@ -688,12 +691,11 @@ void filter2d_slab_cols(int n, int nrhs, int R, int W, int rank, float2* buf, co
   const int groups = h / G + (rank == W - 1 ? 1 : 0);
   fft_cols_slab_kernel<<<dim3(groups, nrhs), 256, smc, s>>>(n, G, R / 2, W, rank, nrhs, buf, tw, tw_n);
 }
-void combine_rows_fft(int n, int nrhs, const float* q, const double* norms, const float* b3, float2* Z, int zb0,
+void combine_rows_fft(int n, int nrhs, const float* q, const float4* qe, const double* norms, float2* Z, int zb0,
                       const float2* tw, int tw_n, cudaStream_t s) {
   const int R = std::max(1, 4096 / n);
   const size_t smr = sizeof(float2) * (size_t)R * n;
-  combine_rows_fft_kernel<<<nrhs * ceil_div(n / 2, R), 256, smr, s>>>(n, nrhs, reinterpret_cast<const float4*>(q),
-                                                                      norms, b3, Z, zb0, tw, tw_n);
+  combine_rows_fft_kernel<<<nrhs * ceil_div(n / 2, R), 256, smr, s>>>(n, nrhs, q, qe, norms, Z, zb0, tw, tw_n);
 }
 void real_to_complex(int nrhs, int n, const float* x, float2* Z, cudaStream_t s) {
   real_to_complex_kernel<<<nblk((int64_t)nrhs * n * n, 256), 256, 0, s>>>(nrhs, n, x, Z);

@@ -372,7 +372,7 @@ struct nmg_hierarchy {
   int64_t bf_px = 0;                                     // pixels per RHS the a2 / q workspaces hold
   std::vector<float> strip_sc;                           // per level: S1, T1, S2, T2
   DevBuf<uint16_t> a2h, a2l;                             // [chunk][n][n][C] f16 hi / lo (scaled by S2)
-  DevBuf<float> qbuf;                                    // [chunk][n][n][4]
+  DevBuf<float> qbuf;                                    // CNN output h [chunk][px], then edge records
   std::vector<CUtensorMap> mA2h, mA2l;                   // per level
   std::vector<std::unique_ptr<DevBuf<uint16_t>>> WB;     // per level: hidden 1 hi, lo, hidden 2 hi, lo
   // coarse Cholesky factor (row-major L and L^T)
@@ -454,6 +454,10 @@ namespace {
 
 // levels served by the column-strip CNN kernels (conv_strip.cu)
 inline bool strip_level(int n) { return n % 128 == 0 || (n >= 16 && n < 128); }
+// strip-edge records of the CNN output (after the chunk's h images in qbuf, see strip_h_fix)
+inline float4* qedge(nmg_hierarchy* h) {
+  return reinterpret_cast<float4*>(h->qbuf.p + (size_t)h->bf_chunk * h->bf_px);
+}
 
 void coarse_solve(nmg_hierarchy* h, int nrhs, const float* y, int64_t ldy, float* x, int64_t ldx, cudaStream_t s,
                   float* xh = nullptr, float* xl = nullptr) {
@@ -821,7 +825,7 @@ nmg_status smooth2d(nmg_hierarchy* h, int l, int nrhs, const float* b, float* x,
       // |u| <= 1 when normalised (||u||_2 = 1); the debug entry allows |u| <= 16
       const float dbg = normalize ? 1.0f : 1.0f / 16.0f;
       a.in_scale = sc[0] * dbg; a.out_scale = sc[2] * dbg; a.d_scale = 1.0f / (sc[0] * dbg * sc[1]);
-      a.out_h = h->a2h.p; a.out_l = h->a2l.p; a.q = h->qbuf.p;
+      a.out_h = h->a2h.p; a.out_l = h->a2l.p; a.q = h->qbuf.p; a.qe = qedge(h); a.b3 = b3;
       { Prof p(h, NMG_K_SMOOTH, s); strip_l12(a, h->num_sms, s); }
       a.wh = wb + 2 * plane; a.wl = wb + 3 * plane; a.bias = b2;
       a.d_scale = 1.0f / (sc[2] * dbg * sc[3]);
@@ -830,10 +834,10 @@ nmg_status smooth2d(nmg_hierarchy* h, int l, int nrhs, const float* b, float* x,
       if (filt && h->fuse_combine) {
         // h = s (b3 + Q0 + Q1 + Q2) for the chunk's RHS pairs, straight into the forward row FFT
         { Prof p(h, NMG_K_FILTER, s);
-          combine_rows_fft(n, cnt, h->qbuf.p, a.norms, b3, h->Z.p, r0, h->tw.p, h->tw_n, s); }
+          combine_rows_fft(n, cnt, h->qbuf.p, a.qe, a.norms, h->Z.p, r0, h->tw.p, h->tw_n, s); }
       } else {
         { Prof p(h, NMG_K_FILTER, s);
-          strip_combine(n, cnt, h->qbuf.p, a.norms, b3, filt ? h->Z.p : nullptr, r0, x + off, accumulate, s); }
+          strip_combine(n, cnt, h->qbuf.p, a.qe, a.norms, filt ? h->Z.p : nullptr, r0, x + off, accumulate, s); }
       }
       NMG_TRY(check_launch(h));
     }
@@ -981,14 +985,14 @@ nmg_status smooth_slab(nmg_hierarchy* h, int l, int nrhs, float* b, float* x, bo
     a.w_in = P; a.w_out = w3;
     a.wh = wb; a.wl = wb + plane; a.bias = b1;
     a.in_scale = sc[0]; a.out_scale = sc[2]; a.d_scale = 1.0f / (sc[0] * sc[1]);
-    a.out_h = h->a2h.p; a.out_l = h->a2l.p; a.q = h->qbuf.p;
+    a.out_h = h->a2h.p; a.out_l = h->a2l.p; a.q = h->qbuf.p; a.qe = qedge(h); a.b3 = b3;
     { Prof p(h, NMG_K_SMOOTH, s); strip_l12(a, h->num_sms, s); }
     a.wh = wb + 2 * plane; a.wl = wb + 3 * plane; a.bias = b2;
     a.d_scale = 1.0f / (sc[2] * sc[3]);
     a.w4 = wb + 4 * plane; a.a3_scale = sc[4]; a.d4_scale = 1.0f / (sc[4] * sc[5]);
     { Prof p(h, NMG_K_SMOOTH, s); strip_l34(&m2h, &m2l, a, h->num_sms, s); }
     { Prof p(h, NMG_K_FILTER, s);
-      strip_combine(n, cnt, h->qbuf.p, a.norms, b3, filt ? h->zs.p : nullptr, c0, x + off, accumulate, s, hg, H); }
+      strip_combine(n, cnt, h->qbuf.p, a.qe, a.norms, filt ? h->zs.p : nullptr, c0, x + off, accumulate, s, hg, H); }
     NMG_TRY(check_launch(h));
   }
   if (filt) {
@@ -2023,7 +2027,7 @@ nmg_status nmg_load_smoother_weights(nmg_hierarchy* h, int32_t level, const nmg_
         if (nmax > 0) {
           int64_t px = (int64_t)nmax * nmax;
           if (h->slab) px = std::max<int64_t>(px, (int64_t)(h->R[0] + 2 * h->HS) * h->n[0]);   // halo'd slab image
-          const int64_t per = px * C * 4 + px * 16;                     // bytes per RHS
+          const int64_t per = px * C * 4 + px * 8;                      // bytes per RHS (a2 hi/lo, h + edges)
           const int64_t budget = (int64_t)16 << 30;
           const int64_t B = h->d.max_rhs;
           const int64_t cmax = std::max<int64_t>(1, std::min<int64_t>(B, budget / per));
@@ -2032,7 +2036,8 @@ nmg_status nmg_load_smoother_weights(nmg_hierarchy* h, int32_t level, const nmg_
           h->bf_px = px;
           NMG_TRY(h->a2h.alloc((size_t)h->bf_chunk * px * C));
           NMG_TRY(h->a2l.alloc((size_t)h->bf_chunk * px * C));
-          NMG_TRY(h->qbuf.alloc((size_t)h->bf_chunk * px * 4));
+          // CNN output h [chunk][px] followed by the strip-edge records (px / 32 floats per image)
+          NMG_TRY(h->qbuf.alloc((size_t)h->bf_chunk * px * 2));
           for (int l = 0; l < h->L - 1; ++l) {
             if (!strip_level(h->n[l])) continue;
             NMG_TRY(make_a2_map(&h->mA2h[l], h->a2h.p, h->n[l], C, h->bf_chunk));

@@ -70,7 +70,9 @@ NMG_D void split8(const float* v, uint4& hi, uint4& lo) {
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const __half2 hv = __floats2half2_rn(v[2 * j], v[2 * j + 1]);
-    const __half2 lv = __floats2half2_rn(v[2 * j] - __low2float(hv), v[2 * j + 1] - __high2float(hv));
+    const float2 hf = __half22float2(hv);   // v - hi per channel pair in one FADD2 (same bits)
+    const float2 r = __fadd2_rn(make_float2(v[2 * j], v[2 * j + 1]), make_float2(-hf.x, -hf.y));
+    const __half2 lv = __floats2half2_rn(r.x, r.y);
     h[j] = *reinterpret_cast<const uint32_t*>(&hv);
     l[j] = *reinterpret_cast<const uint32_t*>(&lv);
   }

@@ -1,7 +1,9 @@
 #!/bin/bash
-# A/B of conv_strip variants on config 3 (smooth class per step) -- dev tool
+# A/B of libnmg variants on a config (default 3): ms/step and the smooth / filter class times.
+# Usage: CFG=3 bash tools/ab_strip.sh [default|path/to/libnmg_X.so ...]   -- dev tool
 cd "$(dirname "$0")/.."
-for lib in "" ${@}; do
-  NMG_LIB=$lib timeout 600 python bench.py --config 3 --steps 5 --warmup 3 --no-cpu --no-e2e --no-solve 2>/dev/null | \
-    python -c "import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']['classes_ms_per_step']; print('lib=${lib:-default}', round(d['ms_per_step'],2), 'smooth', round(r['smooth'],2), 'filter', round(r['filter'],2), d['clocks']['sm_mhz'])"
+for lib in ${@:-default}; do
+  [ "$lib" = default ] && L= || L=$lib
+  NMG_LIB=$L timeout 600 python bench.py --config ${CFG:-3} --steps ${STEPS:-5} --warmup 3 --no-cpu --no-e2e --no-solve 2>/dev/null | \
+    python -c "import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']['classes_ms_per_step']; print('lib=$lib', round(d['ms_per_step'],3), ' '.join(f'{k} {v:.3f}' for k,v in r.items()), d['clocks']['sm_mhz'])"
 done
