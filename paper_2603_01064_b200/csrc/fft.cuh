@@ -92,135 +92,121 @@ NMG_D void fft_dit_inverse(float2* c, int n, const float2* __restrict__ tw, int 
 // Radix-2 stages fused R at a time in registers (R = 3, then 2 / 1 for the remainder): the
 // same butterflies with the same twiddles in the same order as fft_dif_forward /
 // fft_dit_inverse (bit-identical results), but one shared-memory pass and one barrier per R
-// stages.  Block-cooperative; each ends with __syncthreads().
+// stages.  All lengths are powers of two and passed as log2 (llen = log2 len, ltw = log2 tw_n),
+// so the index arithmetic is shifts and masks (no integer division).  Block-cooperative; each
+// batch / fused driver ends with __syncthreads().
 template <int R>
-NMG_D void dif_group(float2* c, int len, int g, const float2* __restrict__ tw, int tw_n, int stride = 1) {
+NMG_D void dif_group(float2* c, int llen, int g, const float2* __restrict__ tw, int ltw, int stride = 1) {
   constexpr int E = 1 << R;
-  const int q = len >> R;                       // element spacing in the group
-  const int blk = g / q, pos = g - blk * q;
-  float2* base = c + (blk * len + pos) * stride;
+  const int lq = llen - R;                      // element spacing q = len >> R in the group
+  const int blk = g >> lq, pos = g & ((1 << lq) - 1);
+  float2* base = c + ((blk << llen) + pos) * stride;
+  const int qs = stride << lq;
   float2 e[E];
 #pragma unroll
-  for (int i = 0; i < E; ++i) e[i] = base[i * q * stride];
+  for (int i = 0; i < E; ++i) e[i] = base[i * qs];
 #pragma unroll
   for (int st = 0; st < R; ++st) {             // stage length len >> st, half = E >> (st + 1) elements
     const int hs = E >> (st + 1);
-    const int step = tw_n / (len >> st);
+    const int lstep = ltw - (llen - st);        // twiddle stride tw_n / (len >> st)
 #pragma unroll
     for (int i = 0; i < E; ++i) {
       if (i & hs) continue;                     // i is the upper element of its pair
-      const int posi = pos + (i & (hs - 1)) * q;   // position within the current sub-block
-      const float2 w = __ldg(tw + posi * step);
+      const int posi = pos + ((i & (hs - 1)) << lq);   // position within the current sub-block
+      const float2 w = __ldg(tw + (posi << lstep));
       const float2 a = e[i], b = e[i + hs];
       e[i] = make_float2(a.x + b.x, a.y + b.y);
       e[i + hs] = cmul(make_float2(a.x - b.x, a.y - b.y), w);
     }
   }
 #pragma unroll
-  for (int i = 0; i < E; ++i) base[i * q * stride] = e[i];
+  for (int i = 0; i < E; ++i) base[i * qs] = e[i];
 }
 template <int R>
-NMG_D void dit_group(float2* c, int len, int g, const float2* __restrict__ tw, int tw_n, int stride = 1) {
+NMG_D void dit_group(float2* c, int llen, int g, const float2* __restrict__ tw, int ltw, int stride = 1) {
   // stages len, 2 len, ..., 2^(R-1) len; group = 2^R elements spaced len/2 apart in a block of
   // 2^(R-1) len
   constexpr int E = 1 << R;
-  const int hq = len >> 1;
-  const int blk = g / hq, pos = g - blk * hq;
-  float2* base = c + (blk * (hq << R) + pos) * stride;
+  const int lhq = llen - 1;
+  const int blk = g >> lhq, pos = g & ((1 << lhq) - 1);
+  float2* base = c + ((blk << (lhq + R)) + pos) * stride;
+  const int qs = stride << lhq;
   float2 e[E];
 #pragma unroll
-  for (int i = 0; i < E; ++i) e[i] = base[i * hq * stride];
+  for (int i = 0; i < E; ++i) e[i] = base[i * qs];
 #pragma unroll
   for (int st = 0; st < R; ++st) {             // stage length len << st, pair distance 2^st elements
     const int hs = 1 << st;
-    const int step = tw_n / (len << st);
+    const int lstep = ltw - (llen + st);        // twiddle stride tw_n / (len << st)
 #pragma unroll
     for (int i = 0; i < E; ++i) {
       if (i & hs) continue;
-      const int posi = pos + (i & (hs - 1)) * hq;
-      const float2 w = __ldg(tw + posi * step);
+      const int posi = pos + ((i & (hs - 1)) << lhq);
+      const float2 w = __ldg(tw + (posi << lstep));
       const float2 a = e[i], b = cmulc(e[i + hs], w);
       e[i] = make_float2(a.x + b.x, a.y + b.y);
       e[i + hs] = make_float2(a.x - b.x, a.y - b.y);
     }
   }
 #pragma unroll
-  for (int i = 0; i < E; ++i) base[i * hq * stride] = e[i];
+  for (int i = 0; i < E; ++i) base[i * qs] = e[i];
 }
+NMG_D int ilog2(int v) { return 31 - __clz(v); }
 // Batched fused passes over `cnt` independent length-n transforms: transform k starts at
 // c + k * kstride and its elements are `stride` apart (rows: kstride = n, stride = 1;
 // columns of an [n][G] tile: kstride = 1, stride = G).  Same arithmetic as the radix-2 loops.
+// Strided (column) transforms put neighbouring transforms on neighbouring threads, so the
+// shared-memory accesses stay consecutive; rows put neighbouring groups of one transform there.
+template <bool DIT>
+NMG_D void fft_batch_pass(float2* c, int ln, int cnt, int kstride, int stride, int llen, int R,
+                          const float2* __restrict__ tw, int ltw, int tid, int nthr) {
+  const int lper = ln - R;
+  const int tot = cnt << lper;
+  const bool pow2 = (cnt & (cnt - 1)) == 0;
+  const int lcnt = ilog2(max(cnt, 1));
+  for (int gg = tid; gg < tot; gg += nthr) {
+    int k, g;
+    if (stride == 1) { k = gg >> lper; g = gg & ((1 << lper) - 1); }
+    else if (pow2) { k = gg & (cnt - 1); g = gg >> lcnt; }
+    else { k = gg % cnt; g = gg / cnt; }
+    float2* ck = c + k * kstride;
+    if (DIT) {
+      if (R == 3) dit_group<3>(ck, llen, g, tw, ltw, stride);
+      else if (R == 2) dit_group<2>(ck, llen, g, tw, ltw, stride);
+      else dit_group<1>(ck, llen, g, tw, ltw, stride);
+    } else {
+      if (R == 3) dif_group<3>(ck, llen, g, tw, ltw, stride);
+      else if (R == 2) dif_group<2>(ck, llen, g, tw, ltw, stride);
+      else dif_group<1>(ck, llen, g, tw, ltw, stride);
+    }
+  }
+}
 NMG_D void fft_dif_forward_batch(float2* c, int n, int cnt, int kstride, int stride, const float2* __restrict__ tw,
                                  int tw_n, int tid, int nthr) {
-  int len = n;
-  while (len >= 2) {
-    const int left = 31 - __clz(len);
-    const int R = left >= 3 ? 3 : left;
-    const int per = n >> R;
-    for (int gg = tid; gg < cnt * per; gg += nthr) {
-      // strided (column) transforms: neighbouring threads take neighbouring transforms, so
-      // shared-memory accesses stay consecutive; rows: neighbouring groups of one transform
-      const int k = stride == 1 ? gg / per : gg % cnt, g = stride == 1 ? gg - k * per : gg / cnt;
-      float2* ck = c + k * kstride;
-      if (R == 3) dif_group<3>(ck, len, g, tw, tw_n, stride);
-      else if (R == 2) dif_group<2>(ck, len, g, tw, tw_n, stride);
-      else dif_group<1>(ck, len, g, tw, tw_n, stride);
-    }
-    len >>= R;
+  const int ln = ilog2(n), ltw = ilog2(tw_n);
+  for (int llen = ln; llen >= 1;) {
+    const int R = llen >= 3 ? 3 : llen;
+    fft_batch_pass<false>(c, ln, cnt, kstride, stride, llen, R, tw, ltw, tid, nthr);
+    llen -= R;
     __syncthreads();
   }
 }
 NMG_D void fft_dit_inverse_batch(float2* c, int n, int cnt, int kstride, int stride, const float2* __restrict__ tw,
                                  int tw_n, int tid, int nthr) {
-  int len = 2;
-  while (len <= n) {
-    const int left = 31 - __clz(n / len) + 1;
+  const int ln = ilog2(n), ltw = ilog2(tw_n);
+  for (int llen = 1; llen <= ln;) {
+    const int left = ln - llen + 1;             // stages remaining (len .. n)
     const int R = left >= 3 ? 3 : left;
-    const int per = n >> R;
-    for (int gg = tid; gg < cnt * per; gg += nthr) {
-      const int k = stride == 1 ? gg / per : gg % cnt, g = stride == 1 ? gg - k * per : gg / cnt;
-      float2* ck = c + k * kstride;
-      if (R == 3) dit_group<3>(ck, len, g, tw, tw_n, stride);
-      else if (R == 2) dit_group<2>(ck, len, g, tw, tw_n, stride);
-      else dit_group<1>(ck, len, g, tw, tw_n, stride);
-    }
-    len <<= R;
+    fft_batch_pass<true>(c, ln, cnt, kstride, stride, llen, R, tw, ltw, tid, nthr);
+    llen += R;
     __syncthreads();
   }
 }
 NMG_D void fft_dif_forward_fused(float2* c, int n, const float2* __restrict__ tw, int tw_n, int tid, int nthr) {
-  int len = n;
-  while (len >= 2) {
-    const int left = 31 - __clz(len);           // stages remaining
-    if (left >= 3) {
-      for (int g = tid; g < (n >> 3); g += nthr) dif_group<3>(c, len, g, tw, tw_n);
-      len >>= 3;
-    } else if (left == 2) {
-      for (int g = tid; g < (n >> 2); g += nthr) dif_group<2>(c, len, g, tw, tw_n);
-      len >>= 2;
-    } else {
-      for (int g = tid; g < (n >> 1); g += nthr) dif_group<1>(c, len, g, tw, tw_n);
-      len >>= 1;
-    }
-    __syncthreads();
-  }
+  fft_dif_forward_batch(c, n, 1, n, 1, tw, tw_n, tid, nthr);
 }
 NMG_D void fft_dit_inverse_fused(float2* c, int n, const float2* __restrict__ tw, int tw_n, int tid, int nthr) {
-  int len = 2;
-  while (len <= n) {
-    const int left = 31 - __clz(n / len) + 1;   // stages remaining (len .. n)
-    if (left >= 3) {
-      for (int g = tid; g < (n >> 3); g += nthr) dit_group<3>(c, len, g, tw, tw_n);
-      len <<= 3;
-    } else if (left == 2) {
-      for (int g = tid; g < (n >> 2); g += nthr) dit_group<2>(c, len, g, tw, tw_n);
-      len <<= 2;
-    } else {
-      for (int g = tid; g < (n >> 1); g += nthr) dit_group<1>(c, len, g, tw, tw_n);
-      len <<= 1;
-    }
-    __syncthreads();
-  }
+  fft_dit_inverse_batch(c, n, 1, n, 1, tw, tw_n, tid, nthr);
 }
 
 // Level mask m'_l in natural DFT order (reading R5): sqrt(2 min(k, n-k) / n).

@@ -363,21 +363,25 @@ __global__ void __launch_bounds__(256) fft_rows_kernel(int n, int64_t nrows, flo
     __syncthreads();
     fft_dif_forward_batch(cb, n, rows, n, 1, tw, tw_n, threadIdx.x, 256);
     for (int i = threadIdx.x; i < tot; i += 256) {
-      const int r = i / n, k = i - r * n;
+      const int r = i >> log2n, k = i & (n - 1);
       Z[r0 * n + i] = natural ? cb[r * n + bitrev(k, log2n)] : cb[i];
     }
     return;
   }
   for (int i = threadIdx.x; i < tot; i += 256) {
-    const int r = i / n, k = i - r * n;
+    const int r = i >> log2n, k = i & (n - 1);
     cb[natural ? r * n + bitrev(k, log2n) : i] = Z[r0 * n + i];
   }
   __syncthreads();
   fft_dit_inverse_batch(cb, n, rows, n, 1, tw, tw_n, threadIdx.x, 256);
+  // complex row Rr = r0 + i / n of RHS b = Rr / rpi (rpi = rows per image / 2, a power of two
+  // for whole images; the slab mode's R / 2 may not be)
+  const bool rp2 = (rpi & (rpi - 1)) == 0;
+  const int lrpi = 31 - __clz(rpi);
   for (int i = threadIdx.x; i < tot; i += 256) {
-    const int64_t Rr = r0 + i / n;                     // complex row
-    const int64_t b = Rr / rpi, r = Rr - b * rpi;
-    const int col = i % n;
+    const int64_t Rr = r0 + (i >> log2n);              // complex row
+    const int64_t b = rp2 ? (Rr >> lrpi) : Rr / rpi, r = Rr - b * rpi;
+    const int col = i & (n - 1);
     const int64_t o = b * ximg + xoff + 2 * r * n + col;
     const float sb = norms ? (float)norms[b] : 1.f;
     const float v0 = (cb[i].x * scale) * sb, v1 = (cb[i].y * scale) * sb;
@@ -454,8 +458,9 @@ NMG_D void cols_filter_tile(float2* cb, int n, int G, const int* k1s, const floa
   for (int k = threadIdx.x; k < n; k += 256) mt[bitrev(k, log2n)] = mask_axis(k, n);   // by DIF position
   for (int c = threadIdx.x; c < G; c += 256) m1s[c] = mask_axis(k1s[c], n);
   fft_dif_forward_batch(cb, n, G, 1, G, tw, tw_n, threadIdx.x, 256);   // ends with __syncthreads
+  const int lG = 31 - __clz(G);                              // G a power of two
   for (int i = threadIdx.x; i < n * G; i += 256) {
-    const int r = i / G, c = i - r * G;
+    const int r = i >> lG, c = i & (G - 1);
     const float m = fmaxf(m1s[c], mt[r]);                   // rows were DIF'd: position r holds k2 = bitrev(r)
     cb[i] = make_float2(cb[i].x * m, cb[i].y * m);
   }
@@ -498,8 +503,9 @@ __global__ void __launch_bounds__(256) fft_cols_kernel(int n, int G, float2* __r
   float2* Zb = Z + (int64_t)b * half * n;
   auto mirror = [&](int p) { return S == 1 ? p : 3 * S - 1 - p; };
   for (int c = threadIdx.x; c < Gc; c += 256) k1s[c] = bitrev(p0 + c, log2n);
+  const int lGc = 31 - __clz(Gc);                            // Gc a power of two
   for (int i = threadIdx.x; i < half * Gc; i += 256) {
-    const int r = i / Gc, c = i - r * Gc;
+    const int r = i >> lGc, c = i & (Gc - 1);
     const int p = p0 + c;
     float2 h0, h1;
     unmix(Zb[(int64_t)r * n + p], Zb[(int64_t)r * n + mirror(p)], h0, h1);
@@ -509,7 +515,7 @@ __global__ void __launch_bounds__(256) fft_cols_kernel(int n, int G, float2* __r
   __syncthreads();
   cols_filter_tile(cb, n, Gc, k1s, tw, tw_n);
   for (int i = threadIdx.x; i < half * Gc; i += 256) {
-    const int r = i / Gc, c = i - r * Gc;
+    const int r = i >> lGc, c = i & (Gc - 1);
     const int p = p0 + c;
     const float2 y0 = cb[(2 * r) * Gc + c], y1 = cb[(2 * r + 1) * Gc + c];
     Zb[(int64_t)r * n + p] = pack_k(y0, y1);
