@@ -510,6 +510,9 @@ void launch_smooth1d(nmg_hierarchy* h, int l, Smooth1dArgs& a, cudaStream_t s) {
     a.d_scale = 1.f / (S1 * h->s1d_sc[2 * l + 1]);
     a.w = h->s1d_w[l];
     for (int c = 0; c < 16; ++c) a.w.b0[c] *= S1;
+    // layer-2 output scale folded into layer 3 (d_scale a power of two: exact)
+    for (int c = 0; c < 16; ++c) a.w.b1[c] /= a.d_scale;
+    for (int i = 0; i < 80; ++i) a.w.w2[i] *= a.d_scale;
     smooth1d_f16(a, s);
   } else {
     smooth1d(a, s);

@@ -318,11 +318,16 @@ NMG_D void a1_row2(const Smooth1dArgs& a, const float* u, int p0, int p1, int n,
     float2 acc = make_float2(b, b);
 #pragma unroll
     for (int t = 0; t < KS; ++t) acc = __ffma2_rn(x[t], make_float2(w[t], w[t]), acc);
-    v0[j] = ok0 ? fmaxf(acc.x, 0.f) : 0.f;
-    v1[j] = ok1 ? fmaxf(acc.y, 0.f) : 0.f;
+    v0[j] = fmaxf(acc.x, 0.f);
+    v1[j] = fmaxf(acc.y, 0.f);
   }
   split8(v0, hi0, lo0);
   split8(v1, hi1, lo1);
+  // padding positions (outside [0, n)) are zeros of layer 2's input: one select per packed word
+  // instead of one per channel
+  const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+  if (!ok0) { hi0 = z; lo0 = z; }
+  if (!ok1) { hi1 = z; lo1 = z; }
 }
 
 // Layer-1 producer for channels 8 H .. 8 H + 7 (H compile-time, so the weights are
@@ -476,7 +481,6 @@ __global__ void __launch_bounds__(NT, NMG_S1D_MINB) smooth1d_f16_kernel(const __
     } else if (warp < 4) {
       // ---------------------------------------------------------- epilogue: layer 3 per tap
       const int m = tid;                        // TMEM lane = position within the tile
-      const float dsc = a.d_scale;
       const float b2v = a.w.b2;
       if (m < 2) {
 #pragma unroll
@@ -497,42 +501,62 @@ __global__ void __launch_bounds__(NT, NMG_S1D_MINB) smooth1d_f16_kernel(const __
         for (int t = 0; t < KS; ++t) acc += qs[t * QR + ((p + t - 2) & (QR - 1))];
         emit(p, acc * sf);
       };
-      for (int k = 0; k < ntile; ++k) {
-        const int sd = k % NSD;
-        mb_wait(&dfull[sd], (uint32_t)(k / NSD) & 1u);
+      // Tiles are consumed in pairs (k, k + 1): each thread holds position k TP + m and
+      // (k + 1) TP + m, so layer 3 runs in packed fp32 over the POSITION pair with the weight as
+      // a broadcast (uniform) operand.  w2 and b1 arrive scaled by the power of two d_scale
+      // (a.w.w2 = w2 d_scale, a.w.b1 = b1 / d_scale: ReLU(d s + b1) w2 = ReLU(s + b1 / d) (w2 d)
+      // exactly), so the accumulator only needs its two FP16x3 halves added.
+      for (int k = 0; k < ntile; k += 2) {
+        const bool two = k + 1 < ntile;
+        const int sa = k % NSD, sb = (k + 1) % NSD;
+        mb_wait(&dfull[sa], (uint32_t)(k / NSD) & 1u);
+        if (two) mb_wait(&dfull[sb], (uint32_t)((k + 1) / NSD) & 1u);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        uint32_t d[32];
-        tld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(sd * 32), d);
-        tld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(sd * 32 + 16), d + 16);
-        tld_wait16(d);
-        tld_wait16(d + 16);
-        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mb_arrive(&dempty[sd]);
-        // layer 3 per tap over channel pairs in packed fp32 (even / odd channel partial sums,
-        // added at the end): q[t] = sum_c w2[c][t] a2[c]
+        const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(sa * 32);
+        // an unpaired last tile reads its own columns twice (position B is never stored)
+        const uint32_t tb = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)((two ? sb : sa) * 32);
         float2 q2[KS];
 #pragma unroll
         for (int t = 0; t < KS; ++t) q2[t] = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int c = 0; c < C; c += 2) {
-          const float2 s2 = __fadd2_rn(make_float2(__uint_as_float(d[c]), __uint_as_float(d[c + 1])),
-                                       make_float2(__uint_as_float(d[16 + c]), __uint_as_float(d[17 + c])));
-          const float2 z2 = __ffma2_rn(s2, make_float2(dsc, dsc), make_float2(a.w.b1[c], a.w.b1[c + 1]));
-          const float2 a22 = make_float2(fmaxf(z2.x, 0.f), fmaxf(z2.y, 0.f));
+        for (int h4 = 0; h4 < 4; ++h4) {                 // channels 4 h4 .. 4 h4 + 3
+          // d[0..3] / d[4..7]: the two FP16x3 halves at position A; d[8..15] the same at B
+          uint32_t d[16];
+          tld4(ta + 4 * h4, d);
+          tld4(ta + 16 + 4 * h4, d + 4);
+          tld4(tb + 4 * h4, d + 8);
+          tld4(tb + 16 + 4 * h4, d + 12);
+          tld_wait16(d);
 #pragma unroll
-          for (int t = 0; t < KS; ++t)
-            q2[t] = __ffma2_rn(make_float2(a.w.w2[c * KS + t], a.w.w2[(c + 1) * KS + t]), a22, q2[t]);
+          for (int c = 0; c < 4; ++c) {
+            const int ch = 4 * h4 + c;
+            // the halves per position (scalar adds: their results pair up without moves)
+            float2 z = make_float2(__uint_as_float(d[c]) + __uint_as_float(d[4 + c]),
+                                   __uint_as_float(d[8 + c]) + __uint_as_float(d[12 + c]));
+            z = __fadd2_rn(z, make_float2(a.w.b1[ch], a.w.b1[ch]));
+            const float2 av = make_float2(fmaxf(z.x, 0.f), fmaxf(z.y, 0.f));
+#pragma unroll
+            for (int t = 0; t < KS; ++t)
+              q2[t] = __ffma2_rn(av, make_float2(a.w.w2[ch * KS + t], a.w.w2[ch * KS + t]), q2[t]);
+          }
         }
-        float q[KS];
-#pragma unroll
-        for (int t = 0; t < KS; ++t) q[t] = q2[t].x + q2[t].y;
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          mb_arrive(&dempty[sa]);
+          if (two) mb_arrive(&dempty[sb]);
+        }
         const int Q0 = k * TP;
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");   // the previous pair's assembly is done
 #pragma unroll
-        for (int t = 0; t < KS; ++t) qs[t * QR + ((Q0 + m) & (QR - 1))] = q[t];
+        for (int t = 0; t < KS; ++t) {
+          qs[t * QR + ((Q0 + m) & (QR - 1))] = q2[t].x;
+          if (two) qs[t * QR + ((Q0 + TP + m) & (QR - 1))] = q2[t].y;
+        }
         asm volatile("bar.sync 1, 128;\n" ::: "memory");
         const int p = Q0 - 2 + m;
         if (p >= 0) assemble(p);
+        if (two) assemble(Q0 + TP - 2 + m);
       }
       // positions n, n + 1 are zero padding; finish h(n - 2), h(n - 1)
       if (m < 2) {
