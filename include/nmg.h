@@ -90,7 +90,7 @@ typedef struct {
   int32_t ffma_cnn;       /* 1: CNN smoother on the FFMA kernels (no tcgen05)                 */
   int32_t no_kron;        /* 1 (2D): Kronecker pair as two plain GEMMs + a stencil pass       */
   int32_t host_chunks;    /* nmg_vcycles_host: 0 = pipelined per RHS lane (default when the
-                             handle has lanes), else that many RHS chunks (1..8)             */
+                             handle has lanes), else that many RHS chunks (1..16)            */
   int32_t fused_coarse;   /* N > 0 (1D): the levels with n_l <= N run as ONE fused fp64 sub-cycle
                              kernel per RHS (cycle64) instead of per-level launches (opt-in:
                              slower than the batched kernels for n_l >= 256)                  */

@@ -453,6 +453,7 @@ struct nmg_hierarchy {
 namespace {
 
 // levels served by the column-strip CNN kernels (conv_strip.cu)
+constexpr int kMaxHostChunks = 16;   // host-entry pipeline: RHS chunks / lanes (events per handle)
 inline bool strip_level(int n) { return n % 128 == 0 || (n >= 16 && n < 128); }
 // strip-edge records of the CNN output (after the chunk's h images in qbuf, see strip_h_fix)
 inline float4* qedge(nmg_hierarchy* h) {
@@ -1352,7 +1353,7 @@ nmg_status graph_cycle(nmg_hierarchy* h, int nrhs, const double* y, double* x, c
     }
     // K lanes: RHS [off_k, off_k+1) on lane k (lane 0 = this handle on s, lane k > 0 on its
     // forked stream); the RHS are independent, so the lanes' kernels overlap
-    int off[9];
+    int off[kMaxHostChunks + 1];
     for (int k = 0; k <= K; ++k) off[k] = std::min(nrhs, (nrhs * k / K + gr - 1) / gr * gr);
     off[K] = nrhs;
     const int64_t N = h->N[0];
@@ -1844,7 +1845,7 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
     NMG_TRY(h->hx.alloc(cnt));
     NMG_CUDA(cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking));
     NMG_CUDA(cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking));
-    h->hev.resize(2 * 8 + 2);
+    h->hev.resize(2 * kMaxHostChunks + 2);
     for (auto& e : h->hev) NMG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   NMG_CUDA(cudaDeviceSynchronize());
@@ -2269,7 +2270,7 @@ nmg_status nmg_vcycles_host(nmg_hierarchy* h, int32_t nrhs, const double* y_host
   cudaStream_t s = (cudaStream_t)stream;
   if (!h->hy.p || !h->s_h2d) return fail(NMG_ERR_UNSUPPORTED, "nmg_vcycles_host: handle has no host staging");
   const int64_t N0 = h->N[0];
-  cudaEvent_t ev_start = h->hev[16], ev_end = h->hev[17];
+  cudaEvent_t ev_start = h->hev[2 * kMaxHostChunks], ev_end = h->hev[2 * kMaxHostChunks + 1];
   NMG_CUDA(cudaEventRecord(ev_start, s));                 // staging buffers free after prior work on s
   NMG_CUDA(cudaStreamWaitEvent(h->s_h2d, ev_start, 0));
   NMG_CUDA(cudaStreamWaitEvent(h->s_d2h, ev_start, 0));
@@ -2279,7 +2280,7 @@ nmg_status nmg_vcycles_host(nmg_hierarchy* h, int32_t nrhs, const double* y_host
     // Lane-pipelined (the RHS are independent): lane k's RHS are copied in on s_h2d,
     // its stream starts cycling as soon as they land (the lanes overlap on the GPU while later
     // lanes are still in flight over PCIe), and its x goes back on s_d2h when it finishes.
-    int off[9];
+    int off[kMaxHostChunks + 1];
     for (int k = 0; k <= K; ++k) off[k] = std::min(nrhs, (nrhs * k / K + gr - 1) / gr * gr);
     off[K] = nrhs;
     for (int k = 0; k < K; ++k) {
@@ -2309,8 +2310,8 @@ nmg_status nmg_vcycles_host(nmg_hierarchy* h, int32_t nrhs, const double* y_host
       NMG_TRY(st);
       if (relres_host && cycles > 0)
         NMG_CUDA(cudaMemcpyAsync(relres_host + off[k], hk->relres.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, sk));
-      NMG_CUDA(cudaEventRecord(h->hev[8 + k], sk));
-      NMG_CUDA(cudaStreamWaitEvent(h->s_d2h, h->hev[8 + k], 0));
+      NMG_CUDA(cudaEventRecord(h->hev[kMaxHostChunks + k], sk));
+      NMG_CUDA(cudaStreamWaitEvent(h->s_d2h, h->hev[kMaxHostChunks + k], 0));
       NMG_CUDA(cudaMemcpyAsync(x_host + off[k] * N0, xc, sizeof(double) * (size_t)cnt * N0, cudaMemcpyDeviceToHost,
                                h->s_d2h));
     }
@@ -2323,10 +2324,14 @@ nmg_status nmg_vcycles_host(nmg_hierarchy* h, int32_t nrhs, const double* y_host
   // chunk c + 1 and the device->host copy of chunk c - 1 run on two copy streams while chunk c
   // cycles on the caller's stream.  One plain cudaMemcpyAsync per buffer and chunk.
   // two chunks keep each chunk's kernels near full occupancy (measured: cfg 1 in 4 chunks of
-  // 256 RHS runs at 64% of the batch efficiency); four only for very large batches
-  int nch = nrhs < 256 ? 1 : ((int64_t)nrhs * N0 / 4 < ((int64_t)1 << 25) ? 2 : 4);
-  if (h->tune.host_chunks > 0) nch = std::max(1, std::min(8, std::min(nrhs, (int)h->tune.host_chunks)));
-  int off[9];
+  // 256 RHS runs at 64% of the batch efficiency); for very large batches the copy of the first
+  // chunk and the return of the last one are the exposed part, so more chunks: config 3 (2048
+  // RHS of 512^2, 12.9 GB over PCIe per cycle) e2e 4,652 / 4,782 / 4,928 RHS cycles/s at 4 / 6 / 8
+  int nch = nrhs < 256 ? 1 : ((int64_t)nrhs * N0 / 4 < ((int64_t)1 << 25) ? 2
+                             : ((int64_t)nrhs * N0 < ((int64_t)1 << 29) ? 4 : 8));
+  if (h->tune.host_chunks > 0)
+    nch = std::max(1, std::min(kMaxHostChunks, std::min(nrhs, (int)h->tune.host_chunks)));
+  int off[kMaxHostChunks + 1];
   for (int c = 0; c <= nch; ++c) off[c] = (int)((int64_t)nrhs * c / nch);
   for (int c = 0; c < nch; ++c) {
     const size_t b = sizeof(double) * (size_t)(off[c + 1] - off[c]) * N0;
@@ -2342,8 +2347,8 @@ nmg_status nmg_vcycles_host(nmg_hierarchy* h, int32_t nrhs, const double* y_host
     for (int k = 0; k < cycles; ++k) NMG_TRY(graph_cycle(h, cnt, yc, xc, s));
     if (relres_host && cycles > 0)
       NMG_CUDA(cudaMemcpyAsync(relres_host + off[c], h->relres.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, s));
-    NMG_CUDA(cudaEventRecord(h->hev[8 + c], s));
-    NMG_CUDA(cudaStreamWaitEvent(h->s_d2h, h->hev[8 + c], 0));
+    NMG_CUDA(cudaEventRecord(h->hev[kMaxHostChunks + c], s));
+    NMG_CUDA(cudaStreamWaitEvent(h->s_d2h, h->hev[kMaxHostChunks + c], 0));
     NMG_CUDA(cudaMemcpyAsync(x_host + off[c] * N0, xc, sizeof(double) * (size_t)cnt * N0, cudaMemcpyDeviceToHost,
                              h->s_d2h));
   }
