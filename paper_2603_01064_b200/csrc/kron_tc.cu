@@ -181,52 +181,120 @@ __global__ void __launch_bounds__(KNT, 1)
       mb_wait(&tfull[ab], (uint32_t)(i >> 1) & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       const uint32_t tb = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(ab * TBN);
-#pragma unroll 1
-      for (int c = 0; c < TBN; c += 16) {
-        uint32_t v[16];
-        tld16(tb + c, v);
-        tld_wait16(v);
-        if (!mok) continue;
-        const int nb = n0 + c;
-        if (a.mode == KRON_T) {
+      if (a.mode == KRON_RESID && HB <= 1) {
+        // D = Cin -/+ (acc + alpha S), S[b][i2][i1] = sum_{a2} Q[i2][a2] (sum_{a1} Q[i1][a1] X[b][a2][a1])
+        // (|a - i| <= HB; X rows addressed by their global index i2, the slab's halo holds i2 +- HB).
+        // Per 16-column chunk: the horizontal pass over the rows i2 - HB .. i2 + 15 + HB, then the
+        // vertical pass in registers.  Software-pipelined: the X / Cin loads of chunk c + 1 are in
+        // flight while chunk c is combined with its accumulator columns and stored (one DRAM
+        // latency per tile instead of one per chunk: the epilogue was latency-bound).  Every load
+        // is unconditional (clamped address; out-of-range terms weighted by 0 or dropped by select).
+        const float* Xb = a.X + b * img + (int64_t)(a.H - a.r0) * n;
+        constexpr int NR = 16 + 2 * HB, NW = 2 * HB + 1;
+        const int nch = (min(TBN, R - n0) + 15) / 16;
+        float raw[NR][NW], cin[16];       // loads in flight (chunk c + 1)
+        float hs[NR], cc[16];             // chunk c, horizontal pass done
+        auto load = [&](int c) {
+          const int nb = n0 + 16 * c;
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (nb + j < n) a.D[base + (int64_t)(nb + j) * R] = __uint_as_float(v[j]);
-        } else {
-          // X rows addressed by their global index i2 (the slab's halo holds i2 +- hb).
-          // Mass stencil S = Q X Q^T of the chunk: horizontal pass over the rows i2 - HB ..
-          // i2 + 15 + HB, then the vertical pass in registers; every load is unconditional
-          // (clamped address, out-of-range terms weighted by 0 or dropped by select), so the
-          // loads of a chunk issue back to back instead of one dependent miss at a time.
-          // S[b][i2][i1] = sum_{a2} Q[i2][a2] (sum_{a1} Q[i1][a1] X[b][a2][a1]), |a - i| <= HB.
-          const float* Xb = a.X + b * img + (int64_t)(a.H - a.r0) * n;
-          constexpr int NR = 16 + 2 * HB;
-          float hs[NR];
+          for (int k = 0; k < NR; ++k) {
+            const float* xrow = Xb + (int64_t)min(max(a.r0 + nb - HB + k, 0), n - 1) * n;
+#pragma unroll
+            for (int d1 = -HB; d1 <= HB; ++d1) raw[k][d1 + HB] = __ldg(xrow + min(max(r + d1, 0), n - 1));
+          }
+#pragma unroll
+          for (int j = 0; j < 16; ++j) cin[j] = a.Cin ? a.Cin[base + (int64_t)min(nb + j, R - 1) * n] : 0.f;
+        };
+        auto horizontal = [&](int c) {
+          const int nb = n0 + 16 * c;
 #pragma unroll
           for (int k = 0; k < NR; ++k) {
             const int a2 = a.r0 + nb - HB + k;
-            const float* xrow = Xb + (int64_t)min(max(a2, 0), n - 1) * n;
             float t = 0.f;
 #pragma unroll
-            for (int d1 = -HB; d1 <= HB; ++d1) t = fmaf(q1[d1 + HB], __ldg(xrow + min(max(r + d1, 0), n - 1)), t);
+            for (int d1 = -HB; d1 <= HB; ++d1) t = fmaf(q1[d1 + HB], raw[k][d1 + HB], t);
             hs[k] = (a2 >= 0 && a2 < n) ? t : 0.f;
           }
-          float o[16];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int jj = min(nb + j, R - 1);
-            const int i2 = a.r0 + jj;
-            float sq = 0.f;
+          for (int j = 0; j < 16; ++j) cc[j] = cin[j];
+        };
+        if (mok && nch > 0) { load(0); horizontal(0); }
+#pragma unroll 1
+        for (int c = 0; c < nch; ++c) {
+          if (mok && c + 1 < nch) load(c + 1);
+          uint32_t v[16];
+          tld16(tb + 16 * c, v);
+          tld_wait16(v);
+          if (mok) {
+            const int nb = n0 + 16 * c;
+            float o[16];
 #pragma unroll
-            for (int d2 = -HB; d2 <= HB; ++d2)
-              sq = fmaf(__ldg(a.Q + (int64_t)i2 * n + min(max(i2 + d2, 0), n - 1)), hs[jj - nb + d2 + HB], sq);
-            const float vv = fmaf(a.alpha, sq, __uint_as_float(v[j]));
-            const float cc = a.Cin ? a.Cin[base + (int64_t)jj * n] : 0.f;
-            o[j] = a.negate ? cc - vv : cc + vv;
+            for (int j = 0; j < 16; ++j) {
+              // columns nb + j >= R are not stored (their clamped terms are never used)
+              const int i2 = a.r0 + min(nb + j, R - 1);
+              float sq = 0.f;
+#pragma unroll
+              for (int d2 = -HB; d2 <= HB; ++d2)
+                sq = fmaf(__ldg(a.Q + (int64_t)i2 * n + min(max(i2 + d2, 0), n - 1)), hs[j + d2 + HB], sq);
+              const float vv = fmaf(a.alpha, sq, __uint_as_float(v[j]));
+              o[j] = a.negate ? cc[j] - vv : cc[j] + vv;
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (nb + j < R) a.D[base + (int64_t)(nb + j) * n] = o[j];
+            if (c + 1 < nch) horizontal(c + 1);
           }
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (nb + j < R) a.D[base + (int64_t)(nb + j) * n] = o[j];
+        }
+      } else {
+        // pass 1 (KRON_T), and pass 2 at HB = 2 (levels n <= 128: the pipelined registers would
+        // spill there): one chunk at a time
+  #pragma unroll 1
+        for (int c = 0; c < TBN; c += 16) {
+          uint32_t v[16];
+          tld16(tb + c, v);
+          tld_wait16(v);
+          if (!mok) continue;
+          const int nb = n0 + c;
+          if (a.mode == KRON_T) {
+  #pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (nb + j < n) a.D[base + (int64_t)(nb + j) * R] = __uint_as_float(v[j]);
+          } else {
+            // X rows addressed by their global index i2 (the slab's halo holds i2 +- hb).
+            // Mass stencil S = Q X Q^T of the chunk: horizontal pass over the rows i2 - HB ..
+            // i2 + 15 + HB, then the vertical pass in registers; every load is unconditional
+            // (clamped address, out-of-range terms weighted by 0 or dropped by select), so the
+            // loads of a chunk issue back to back instead of one dependent miss at a time.
+            // S[b][i2][i1] = sum_{a2} Q[i2][a2] (sum_{a1} Q[i1][a1] X[b][a2][a1]), |a - i| <= HB.
+            const float* Xb = a.X + b * img + (int64_t)(a.H - a.r0) * n;
+            constexpr int NR = 16 + 2 * HB;
+            float hs[NR];
+  #pragma unroll
+            for (int k = 0; k < NR; ++k) {
+              const int a2 = a.r0 + nb - HB + k;
+              const float* xrow = Xb + (int64_t)min(max(a2, 0), n - 1) * n;
+              float t = 0.f;
+  #pragma unroll
+              for (int d1 = -HB; d1 <= HB; ++d1) t = fmaf(q1[d1 + HB], __ldg(xrow + min(max(r + d1, 0), n - 1)), t);
+              hs[k] = (a2 >= 0 && a2 < n) ? t : 0.f;
+            }
+            float o[16];
+  #pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int jj = min(nb + j, R - 1);
+              const int i2 = a.r0 + jj;
+              float sq = 0.f;
+  #pragma unroll
+              for (int d2 = -HB; d2 <= HB; ++d2)
+                sq = fmaf(__ldg(a.Q + (int64_t)i2 * n + min(max(i2 + d2, 0), n - 1)), hs[jj - nb + d2 + HB], sq);
+              const float vv = fmaf(a.alpha, sq, __uint_as_float(v[j]));
+              const float cc = a.Cin ? a.Cin[base + (int64_t)jj * n] : 0.f;
+              o[j] = a.negate ? cc - vv : cc + vv;
+            }
+  #pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (nb + j < R) a.D[base + (int64_t)(nb + j) * n] = o[j];
+          }
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
