@@ -18,8 +18,10 @@ for t in ${@:-cfg3}; do
     cfg3) run cfg3 3 "conv_strip|fft_cols|fft_rows|combine_rows_fft|ozaki_resid|kron_tc|norms|sumsq" 14 ;;
     cfg2) run cfg2 2 "conv_strip|fft_cols|fft_rows|combine_rows_fft" 6 ;;
     strip3) run strip3 3 "conv_strip" 2 ;;
+    strip2) run strip2 2 "conv_strip" 2 ;;
     fft3) run fft3 3 "fft_cols|fft_rows|combine_rows_fft|sumsq_partial" 4 "--lanes 1" ;;
     kron3) run kron3 3 "kron_tc" 4 ;;
     cols3) run cols3 3 "fft_cols|fft_rows" 2 "--lanes 1" ;;
+    comb3) run comb3 3 "combine_rows" 1 "--lanes 1" ;;
   esac
 done
