@@ -94,6 +94,9 @@ typedef struct {
   int32_t fused_coarse;   /* N > 0 (1D): the levels with n_l <= N run as ONE fused fp64 sub-cycle
                              kernel per RHS (cycle64) instead of per-level launches (opt-in:
                              slower than the batched kernels for n_l >= 256)                  */
+  int32_t no_compaction;  /* 1: nmg_solve keeps cycling the whole batch (converged RHS masked)
+                             instead of gathering the active RHS into a smaller batch; 2:
+                             gather whenever one RHS converged (parity tests)               */
 } nmg_tuning;
 
 /* Problem descriptor (SPEC ProblemSpec analogue). */
@@ -179,7 +182,11 @@ nmg_status nmg_vcycle(nmg_hierarchy *h, int32_t nrhs, const double *y, double *x
 /* Outer iteration from the x passed in (x0 = 0 for the paper's solve) until every
  * RHS has relres <= tol or max_cycles; converged RHS are frozen.  y, x: device
  * fp64 [nrhs][N]; rep: host (may be NULL).  Synchronises once per cycle (and polls the
- * communicator's asynchronous error state on a slab handle).
+ * communicator's asynchronous error state on a slab handle).  Once the converged RHS are at
+ * least 1/8 of the cycling batch (and 2^22 values), the still-active ones are gathered into the
+ * handle's staging buffers and cycle as a smaller batch (their arithmetic does not depend on the
+ * batch; nmg_tuning.no_compaction = 1 keeps the whole batch); x holds every RHS's final iterate
+ * when the call returns (not while it runs).
  * Errors: NONFINITE / DIVERGED (rep->fail_*), NO_WEIGHTS, CUDA, NCCL. */
 nmg_status nmg_solve(nmg_hierarchy *h, int32_t nrhs, const double *y, double *x, double tol,
                      int32_t max_cycles, nmg_report *rep, void *stream);

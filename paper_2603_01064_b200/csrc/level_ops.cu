@@ -316,6 +316,24 @@ __global__ void update_x_kernel(int nrhs, int N, double* __restrict__ x, int64_t
   x[(int64_t)b * ldx + j] += (double)d[(int64_t)b * ldd + j];
 }
 
+// active-set compaction of nmg_solve: dst row i = src row map[i] (gather) or dst row map[i] =
+// src row i (scatter); rows of N doubles, 16-byte vectors when N is even
+__global__ void permute_rows_kernel(int rows, int64_t N, const double* __restrict__ src, double* __restrict__ dst,
+                                    const int32_t* __restrict__ map, int scatter) {
+  const int i = blockIdx.y;
+  if (i >= rows) return;
+  const int64_t si = scatter ? i : map[i], di = scatter ? map[i] : i;
+  if (N % 2 == 0) {
+    const double2* s2 = reinterpret_cast<const double2*>(src + si * N);
+    double2* d2 = reinterpret_cast<double2*>(dst + di * N);
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < N / 2; k += (int64_t)gridDim.x * blockDim.x)
+      d2[k] = s2[k];
+  } else {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < N; k += (int64_t)gridDim.x * blockDim.x)
+      dst[di * N + k] = src[si * N + k];
+  }
+}
+
 __global__ void f64_to_f32_kernel(int64_t count, const double* __restrict__ in, float* __restrict__ out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < count) out[i] = (float)in[i];
@@ -386,6 +404,12 @@ void update_x(int nrhs, int N, double* x, int64_t ldx, const float* d, int64_t l
   update_x_kernel<<<nblk((int64_t)nrhs * N, 256), 256, 0, s>>>(nrhs, N, x, ldx, d, ldd, active);
 }
 
+void permute_rows(int rows, int64_t N, const double* src, double* dst, const int32_t* map, bool scatter,
+                  cudaStream_t s) {
+  if (rows <= 0) return;
+  const int bx = (int)std::min<int64_t>(64, (N / 2 + 255) / 256 + 1);
+  permute_rows_kernel<<<dim3(bx, rows), 256, 0, s>>>(rows, N, src, dst, map, scatter ? 1 : 0);
+}
 void f64_to_f32(int64_t count, const double* in, float* out, cudaStream_t s) {
   f64_to_f32_kernel<<<nblk(count, 256), 256, 0, s>>>(count, in, out);
 }

@@ -396,7 +396,9 @@ struct nmg_hierarchy {
   std::vector<std::unique_ptr<DevBuf<float>>> wy, wx, wr, wb;
   DevBuf<double> part, ynorm, relres, ywork;
   DevBuf<uint8_t> active;
-  DevBuf<double> hy, hx;   // staging for nmg_vcycles_host (allocated at create)
+  DevBuf<double> hy, hx;   // staging for nmg_vcycles_host (allocated at create); nmg_solve's
+                           // compacted active set reuses them
+  DevBuf<int32_t> cmap;    // nmg_solve: compacted index -> RHS
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;         // copy streams of nmg_vcycles_host
   std::vector<cudaEvent_t> hev;                          // its chunk events
   int ntiles = 0;        // ||r||^2 partials per row: DMMA residual (64-wide tiles)
@@ -1843,6 +1845,7 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
     const size_t cnt = (size_t)d.max_rhs * h->N[0];
     NMG_TRY(h->hy.alloc(cnt));
     NMG_TRY(h->hx.alloc(cnt));
+    NMG_TRY(h->cmap.alloc((size_t)d.max_rhs));
     NMG_CUDA(cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking));
     NMG_CUDA(cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking));
     h->hev.resize(2 * kMaxHostChunks + 2);
@@ -2205,32 +2208,45 @@ nmg_status nmg_solve(nmg_hierarchy* h, int32_t nrhs, const double* y, double* x,
   }
   nmg_status st = NMG_OK;
   int tau = 0;
+  // Active-set compaction (the RHS are independent; each RHS's arithmetic does not
+  // depend on the batch it runs in): once the converged RHS would leave enough work undone, the
+  // still-active ones are gathered into the handle's staging buffers and cycle as a smaller batch;
+  // x goes back to the caller's rows before each regathering and at the end.  cur = rows cycling,
+  // cmap[i] = the RHS in row i (identity while yc == y).
+  const double* yc = y;
+  double* xc = x;
+  int cur = nrhs;
+  std::vector<int32_t> map(nrhs);
+  for (int b = 0; b < nrhs; ++b) map[b] = b;
+  const bool can_compact = !f64 && !h->slab && h->hy.p && h->cmap.p && h->tune.no_compaction != 1;
   for (;; ++tau) {
-    NMG_CUDA(cudaMemcpyAsync(rr.data(), h->relres.p, sizeof(double) * nrhs, cudaMemcpyDeviceToHost, s));
+    NMG_CUDA(cudaMemcpyAsync(rr.data(), h->relres.p, sizeof(double) * cur, cudaMemcpyDeviceToHost, s));
     NMG_CUDA(cudaStreamSynchronize(s));
     if (h->slab) {
       st = h->comm->check_async();
       if (st != NMG_OK) break;
     }
     int nact = 0;
-    for (int b = 0; b < nrhs; ++b) {
+    for (int i = 0; i < cur; ++i) {
+      const int b = map[i];
       if (!act[b]) continue;
-      if (!std::isfinite(rr[b])) {
+      const double rb = rr[i];
+      if (!std::isfinite(rb)) {
         if (rep) { rep->fail_cycle = tau; rep->fail_rhs = b; }
         st = fail(NMG_ERR_NONFINITE, "non-finite residual at cycle %d, rhs %d", tau, b);
         break;
       }
-      if (rep && rep->history) rep->history[(size_t)b * (max_cycles + 1) + tau] = rr[b];
-      if (tau == 0) rr0[b] = rr[b];
+      if (rep && rep->history) rep->history[(size_t)b * (max_cycles + 1) + tau] = rb;
+      if (tau == 0) rr0[b] = rb;
       // divergence = relres above 10x the initial relres for 5 consecutive cycles
-      above[b] = (tau > 0 && rr[b] > 10.0 * rr0[b]) ? above[b] + 1 : 0;
+      above[b] = (tau > 0 && rb > 10.0 * rr0[b]) ? above[b] + 1 : 0;
       if (h->d.divergence_check && above[b] >= 5) {
         if (rep) { rep->fail_cycle = tau; rep->fail_rhs = b; }
         st = fail(NMG_ERR_DIVERGED, "rhs %d diverged: relres %.3e > 10 x initial %.3e for 5 cycles (cycle %d)", b,
-                  rr[b], rr0[b], tau);
+                  rb, rr0[b], tau);
         break;
       }
-      if (rr[b] <= tol) act[b] = 0; else ++nact;
+      if (rb <= tol) act[b] = 0; else ++nact;
     }
     if (st != NMG_OK || nact == 0 || tau == max_cycles) break;
     for (int b = 0; b < nrhs; ++b) if (act[b]) cyc[b] = tau + 1;
@@ -2238,10 +2254,38 @@ nmg_status nmg_solve(nmg_hierarchy* h, int32_t nrhs, const double* y, double* x,
       NMG_TRY(cycle_fp64(h, nrhs, y, x, true, true, tol, h->active.p, h->active.p, s));
       continue;
     }
-    NMG_TRY(inner_cycle(h, nrhs, s));
-    NMG_TRY(outer_update(h, nrhs, x, h->active.p, s));
-    NMG_TRY(outer_residual(h, nrhs, y, x, nullptr, true, s));
-    NMG_TRY(relres_fin(h, nrhs, tol, h->active.p, h->relres.p, s));
+    // compact when the converged rows are at least 1/8 of the batch and 2^22 values of work
+    // (no_compaction = 2, for the parity tests: whenever one has converged)
+    const bool compact = h->tune.no_compaction == 2
+                             ? nact < cur
+                             : nact <= cur - cur / 8 && (int64_t)(cur - nact) * N >= ((int64_t)1 << 22);
+    if (can_compact && compact) {
+      if (xc != x) permute_rows(cur, N, xc, x, h->cmap.p, true, s);            // x back to its rows
+      std::vector<int32_t> nmap;
+      nmap.reserve(nact);
+      for (int i = 0; i < cur; ++i) if (act[map[i]]) nmap.push_back(map[i]);
+      map.swap(nmap);
+      cur = nact;
+      NMG_CUDA(cudaMemcpyAsync(h->cmap.p, map.data(), sizeof(int32_t) * cur, cudaMemcpyHostToDevice, s));
+      permute_rows(cur, N, y, h->hy.p, h->cmap.p, false, s);
+      permute_rows(cur, N, x, h->hx.p, h->cmap.p, false, s);
+      NMG_TRY(check_launch(h));
+      yc = h->hy.p;
+      xc = h->hx.p;
+      // the residual of the compacted batch (the same values, now in rows 0 .. cur - 1)
+      NMG_TRY(ynorms(h, cur, yc, s));
+      NMG_TRY(outer_residual(h, cur, yc, xc, nullptr, true, s));
+      NMG_TRY(relres_fin(h, cur, tol, h->active.p, h->relres.p, s));
+      NMG_CUDA(cudaStreamSynchronize(s));   // map (pageable host memory) consumed before it changes
+    }
+    NMG_TRY(inner_cycle(h, cur, s));
+    NMG_TRY(outer_update(h, cur, xc, h->active.p, s));
+    NMG_TRY(outer_residual(h, cur, yc, xc, nullptr, true, s));
+    NMG_TRY(relres_fin(h, cur, tol, h->active.p, h->relres.p, s));
+  }
+  if (xc != x) {
+    permute_rows(cur, N, xc, x, h->cmap.p, true, s);
+    NMG_TRY(check_launch(h));
   }
   NMG_CUDA(cudaEventRecord(e1, s));
   NMG_CUDA(cudaEventSynchronize(e1));
