@@ -204,14 +204,20 @@ def test_wtrain_solve_matches_oracle(key):
     assert g[f"conv_{key}"].all()
     f = ni.operator_factors(cfg)
     B = cfg.nrhs
-    if cfg.dim == 1:
+    kw = {}
+    if cid == 0:   # all 8 RHS, in the bench's launch configuration (the fused fp64 cycle)
+        import paper_2603_01064_b200 as nmg
+        y, _ = ni.make_rhs(cfg, f, alpha)
+        idx = list(range(B))
+        kw = {"precision": nmg.PREC_FP64}
+    elif cfg.dim == 1:
         y, _ = ni.make_rhs(cfg, f, alpha)
         idx = list(gold("oracle_cfg1_wseed.npz")["idx"])
     else:
         pool, _ = ni.make_rhs(cfg, f, alpha, nrhs=8, start=0)
         y = np.ascontiguousarray(np.concatenate([pool] * (-(-B // 8)))[:B])
         idx = list(range(len(oc)))
-    h = gpu_hierarchy(cfg, f, W, max_rhs=B)
+    h = gpu_hierarchy(cfg, f, W, max_rhs=B, **kw)
     yd = T(y, torch.float64)
     del y
     xd = torch.zeros_like(yd)

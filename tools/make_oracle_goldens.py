@@ -67,13 +67,19 @@ def one_d_lin():
     np.savez_compressed(os.path.join(GOLD, "oracle_cfg1_wlin.npz"), **out)
 
 
-def trained():
+def trained(cids=(0, 1, 2, 3, 4)):
     """W_train (trainer output, nmg_inputs/trained): oracle solves to 1e-6 -- the
     oracle's confirmation that the trained smoothers converge, and the stopping cycles the GPU
-    solve must reproduce.  1D: the IDX_1D RHS of the full batch; 2D: 4 pool members (cfg 3: 2)."""
+    solve must reproduce.  Config 0: its 8 RHS; 1D: the IDX_1D RHS of the full batch; 2D: 4 pool
+    members (cfg 3: 2).  Entries of configs outside `cids` are kept from the existing file."""
     out = {}
-    for cid in (1, 2, 3, 4):
-        for a in sorted(set(ni.ALPHAS[cid]) | ({1e-2} if cid in (1, 2, 3) else set()), reverse=True):
+    p = os.path.join(GOLD, "oracle_wtrain.npz")
+    if os.path.exists(p):
+        with np.load(p) as z:
+            keep = {k: z[k] for k in z.files if int(k.split("cfg")[1][0]) not in cids}
+        out.update(keep)
+    for cid in cids:
+        for a in sorted(set(ni.ALPHAS[cid]) | ({1e-2} if cid in (0, 1, 2, 3) else set()), reverse=True):
             cfg = ni.CONFIGS[cid].replace(alpha=a)
             W = ni.weights_trained(cfg)
             if W is None:
@@ -81,7 +87,9 @@ def trained():
             f = ni.operator_factors(cfg)
             H = hierarchy(cfg, f, W)
             t0 = time.time()
-            if cfg.dim == 1:
+            if cid == 0:
+                y, _ = ni.make_rhs(cfg, f, a)
+            elif cfg.dim == 1:
                 y, _ = ni.make_rhs(cfg, f, a)
                 y = y[IDX_1D]
             else:
@@ -114,5 +122,8 @@ if __name__ == "__main__":
     which = sys.argv[1:] or ["1d_seed", "1d_lin", "2d"]
     for w in which:
         t0 = time.time()
+        if w.startswith("trained:"):        # trained:0,1 -> only those configs (merged)
+            trained(tuple(int(c) for c in w.split(":")[1].split(",")))
+            continue
         {"1d_seed": one_d_seed, "1d_lin": one_d_lin, "2d": two_d, "trained": trained}[w]()
         print(f"{w} done in {time.time() - t0:.0f} s", flush=True)
