@@ -19,8 +19,7 @@
 namespace nmg {
 namespace {
 
-constexpr int OS = 7;                       // digits per operand
-constexpr int NDIAG = OS;                   // diagonals d = 2 .. OS + 1
+constexpr int OS = 7;                       // digits per operand (diagonals d = 2 .. OS + 1)
 // Tile / pipeline shape (compile-time knobs for A/B builds, tools/ab_ozaki.sh).  Measured at
 // tensor-pipe 31-34 % active (ncu r02, cfg 3); neither 32-wide K blocks in 4 stages of 42 KB
 // (SWIZZLE_32B digit maps: cfg 1 gemm64 0.423 vs 0.430 ms, cfg 3 32.7 vs 32.2 ms) nor 32-wide
