@@ -379,6 +379,15 @@ def main():
         achieved = counts["gemm32"] / (step_ms * 1e-3) / 1e12
         roof = {"kernel": "tc_gemm_kernel (3xTF32 tcgen05, all levels)", "bound": "tensor", "unit": "TFLOP/s",
                 "peak_note": "TF32 tensor (measured bf16 x 1.1/2.25) / 3 passes"}
+    elif prec == nmg.PREC_FP64:
+        # the whole cycle in one fused launch (cycle64_kernel, one CTA per RHS): latency-bound;
+        # reported against the FP32 FFMA rate (148 SMs x 128 lanes x 2 FLOP x 1.965 GHz)
+        peak = 148 * 128 * 2 * 1.965e9 / 1e12
+        achieved = (counts["gemm64"] * 2 + counts["gemm32"] + counts["smooth"]) / (step_ms * 1e-3) / 1e12
+        roof = {"kernel": "cycle64_kernel (whole fp64 cycle per RHS, one CTA per RHS, one launch per cycle)",
+                "bound": "alu", "unit": "TFLOP/s",
+                "peak_note": "FP32 FFMA peak from unit counts and clock (DESIGN.md §6); work = fp64 operator "
+                             "applies + fp32 CNN FLOPs; the kernel is latency-bound (8 CTAs on 148 SMs)"}
     elif cfg.dim == 1:
         peak = f16x3_peak
         achieved = counts["smooth"] / (step_ms * 1e-3) / 1e12
@@ -402,8 +411,10 @@ def main():
     roof.update({"achieved": achieved, "peak": peak, "frac": achieved / peak, "traffic": traffic,
                  "traffic_note": (f"ncu dram__bytes_read+write of the {dom} class per step (cfg{cid}), profiles/traffic.json"
                                   if traffic else None),
-                 "peak_source": pk["source"] + (" bf16_tflops_sustained (run at sw_power_cap)" if sustained
-                                                else (" bf16_tflops (burst)" if roof["bound"] == "tensor" else " hbm_gbs")),
+                 "peak_source": ("derived from unit counts and clock (DESIGN.md §6)" if roof["bound"] == "alu" else
+                                 pk["source"] + (" bf16_tflops_sustained (run at sw_power_cap)" if sustained
+                                                 else (" bf16_tflops (burst)" if roof["bound"] == "tensor"
+                                                       else " hbm_gbs"))),
                  "frac_vs_burst_peak": (achieved / (peak * bf16_burst / bf16)) if roof["bound"] == "tensor" else None,
                  "share_of_step": dom_ms / tot_prof if tot_prof else None,
                  "classes_ms_per_step": {k: v[0] / psteps for k, v in prof.items()},

@@ -227,13 +227,14 @@ NMG_D void real_level_filter(float* hbuf, int n, const float2* __restrict__ tw, 
   if (m >= 2) fft_dif_forward_fused(z, m, tw, tw_n, tid, nthr);   // Z in bit-reversed order
   const int lm = (m >= 2) ? 31 - __clz(m) : 0;
   const int wstep = tw_n / n;                                     // W_n^k = tw[k * wstep]
+  const float invn = 1.0f / (float)n;                             // power of two: x invn == x / n
   // pair (k, m - k): unpack H, apply the mask, repack for the inverse
   for (int k = tid; k <= (m >> 1); k += nthr) {
     const int kk = (m - k) & (m - 1);                             // m - k (mod m)
     const int pk = lm ? bitrev(k, lm) : 0, pkk = lm ? bitrev(kk, lm) : 0;
     const float2 Zk = z[pk], Zc = z[pkk];
-    const float mk = sqrtf((float)(2 * k) / (float)n);            // mu[k],   k <= m
-    const float mc = sqrtf((float)(2 * (m - k)) / (float)n);      // mu[m-k]
+    const float mk = sqrtf((float)(2 * k) * invn);                // mu[k],   k <= m
+    const float mc = sqrtf((float)(2 * (m - k)) * invn);          // mu[m-k]
     const float sp = 0.5f * (mk + mc), sm = 0.5f * (mk - mc);
     // k side: E = (Zk + conj Zc)/2, O = -i (Zk - conj Zc)/2
     float2 E = make_float2(0.5f * (Zk.x + Zc.x), 0.5f * (Zk.y - Zc.y));

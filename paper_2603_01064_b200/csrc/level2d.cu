@@ -347,11 +347,13 @@ __global__ void __launch_bounds__(256, 1) cnn2d_kernel(Cnn2dArgs a) {
 // inverse: in bit-reversed (natural = 0) or natural (natural = 1, loaded bit-reversed for the
 // DIT pass); complex row Rr = b rpi + r of RHS b writes real rows 2r and 2r + 1 of x at
 // b ximg + xoff + (2r) n + col (rpi = rows / 2).
-__global__ void __launch_bounds__(256) fft_rows_kernel(int n, int64_t nrows, float2* __restrict__ Z,
+template <int NN>
+__global__ void __launch_bounds__(256) fft_rows_kernel(int n_, int64_t nrows, float2* __restrict__ Z,
                                                        const float2* __restrict__ tw, int tw_n, int inverse,
                                                        float* __restrict__ x, int accumulate, float scale,
                                                        const double* __restrict__ norms, int rpi, int64_t ximg,
                                                        int64_t xoff, int natural) {
+  const int n = NN > 0 ? NN : n_;   // compile-time for the level sizes (index arithmetic folds)
   extern __shared__ __align__(16) float2 cb[];
   const int R = max(1, 4096 / n);
   const int64_t r0 = (int64_t)blockIdx.x * R;
@@ -393,11 +395,13 @@ __global__ void __launch_bounds__(256) fft_rows_kernel(int n, int64_t nrows, flo
 // combine + forward row FFT: CTA = R complex rows of one RHS; complex row r = (h(2r, .), h(2r+1, .))
 // with h the strip kernel's output completed at the strip edges (strip_h_fix), 0 for a RHS with
 // ||b|| = 0.  Four consecutive pixels of both rows per thread (two float4 loads).
-__global__ void __launch_bounds__(256) combine_rows_fft_kernel(int n, int nrhs, const float* __restrict__ q,
+template <int NN>
+__global__ void __launch_bounds__(256) combine_rows_fft_kernel(int n_, int nrhs, const float* __restrict__ q,
                                                                const float4* __restrict__ qe,
                                                                const double* __restrict__ norms,
                                                                float2* __restrict__ Z, int zb0,
                                                                const float2* __restrict__ tw, int tw_n) {
+  const int n = NN > 0 ? NN : n_;   // compile-time for the level sizes (index arithmetic folds)
   extern __shared__ __align__(16) float2 cb[];
   const int R = max(1, 4096 / n);
   const int half = n / 2;
@@ -482,8 +486,10 @@ NMG_D float2 pack_mirror(float2 y0, float2 y1) { return make_float2(y0.x + y1.y,
 // group 0 = positions {0, 1} (k1 = 0, n/2; self-mirrored); then for each dyadic block
 // [2^j, 2^(j+1)), j >= 1, its lower half split in groups of Gs = min(G, 2^(j-1)) positions p,
 // each with the mirror positions 3 * 2^j - 1 - p of the upper half.
-__global__ void __launch_bounds__(256) fft_cols_kernel(int n, int G, float2* __restrict__ Z,
+template <int NN>
+__global__ void __launch_bounds__(256) fft_cols_kernel(int n_, int G, float2* __restrict__ Z,
                                                        const float2* __restrict__ tw, int tw_n) {
+  const int n = NN > 0 ? NN : n_;   // compile-time for the level sizes (index arithmetic folds)
   extern __shared__ __align__(16) float2 cb[];   // [n][Gc]
   __shared__ int k1s[64];
   const int b = blockIdx.y, half = n / 2;
@@ -642,6 +648,17 @@ void cnn2d(const Cnn2dArgs& a, cudaStream_t s) {
     cnn2d_kernel<48><<<grid, 256, smem, s>>>(a);
   }
 }
+// instantiate a kernel for the 2D level sizes (compile-time n), generic otherwise
+#define NMG_DISPATCH_N(n, ...)                                     \
+  switch (n) {                                                     \
+    case 32: { constexpr int NN = 32; __VA_ARGS__; break; }        \
+    case 64: { constexpr int NN = 64; __VA_ARGS__; break; }        \
+    case 128: { constexpr int NN = 128; __VA_ARGS__; break; }      \
+    case 256: { constexpr int NN = 256; __VA_ARGS__; break; }      \
+    case 512: { constexpr int NN = 512; __VA_ARGS__; break; }      \
+    case 1024: { constexpr int NN = 1024; __VA_ARGS__; break; }    \
+    default: { constexpr int NN = 0; __VA_ARGS__; break; }         \
+  }
 void filter2d(int nrhs, int n, float2* Z, const float2* tw, int tw_n, float* x, bool accumulate, cudaStream_t s,
               const double* norms, bool rows_done) {
   // per-RHS buffers Z_b = [n/2][n] complex (zput); three passes (rows, columns, inverse rows)
@@ -649,16 +666,17 @@ void filter2d(int nrhs, int n, float2* Z, const float2* tw, int tw_n, float* x, 
   const int R = std::max(1, 4096 / n);
   const size_t smr = sizeof(float2) * (size_t)R * n;
   if (!rows_done)
-    fft_rows_kernel<<<nblk(nrows, R), 256, smr, s>>>(n, nrows, Z, tw, tw_n, 0, nullptr, 0, 1.f, nullptr, n / 2,
-                                                     (int64_t)n * n, 0, 0);
+    NMG_DISPATCH_N(n, (fft_rows_kernel<NN><<<nblk(nrows, R), 256, smr, s>>>(n, nrows, Z, tw, tw_n, 0, nullptr, 0, 1.f,
+                                                                          nullptr, n / 2, (int64_t)n * n, 0, 0)))
   const int G = std::min(std::max(1, n / 2), std::min(64, std::max(2, 4096 / n)));   // 32 KB of columns
   const size_t smc = sizeof(float2) * (size_t)n * std::max(G, 2);
-  NMG_SMEM_OPTIN(fft_cols_kernel, 65536);
   int groups = 1;
   for (int S = 2; S < n; S <<= 1) groups += std::max(1, (S / 2) / G);
-  fft_cols_kernel<<<dim3(groups, nrhs), 256, smc, s>>>(n, G, Z, tw, tw_n);
-  fft_rows_kernel<<<nblk(nrows, R), 256, smr, s>>>(n, nrows, Z, tw, tw_n, 1, x, accumulate ? 1 : 0,
-                                                   1.0f / ((float)n * (float)n), norms, n / 2, (int64_t)n * n, 0, 0);
+  NMG_DISPATCH_N(n, NMG_SMEM_OPTIN(fft_cols_kernel<NN>, 65536);
+                 fft_cols_kernel<NN><<<dim3(groups, nrhs), 256, smc, s>>>(n, G, Z, tw, tw_n))
+  NMG_DISPATCH_N(n, (fft_rows_kernel<NN><<<nblk(nrows, R), 256, smr, s>>>(n, nrows, Z, tw, tw_n, 1, x, accumulate ? 1 : 0,
+                                                                        1.0f / ((float)n * (float)n), norms, n / 2,
+                                                                        (int64_t)n * n, 0, 0)))
 }
 
 // ---------------------------------------------------------------- slab-sharded level filter
@@ -673,16 +691,16 @@ void filter2d_slab_rows(int n, int nrhs, int R, float2* Zs, const float2* tw, in
   const int64_t nrows = (int64_t)nrhs * (R / 2);
   const int RR = std::max(1, 4096 / n);
   const size_t smr = sizeof(float2) * (size_t)RR * n;
-  fft_rows_kernel<<<nblk(nrows, RR), 256, smr, s>>>(n, nrows, Zs, tw, tw_n, 0, nullptr, 0, 1.f, nullptr, R / 2,
-                                                    (int64_t)R * n, 0, 1);
+  fft_rows_kernel<0><<<nblk(nrows, RR), 256, smr, s>>>(n, nrows, Zs, tw, tw_n, 0, nullptr, 0, 1.f, nullptr, R / 2,
+                                                       (int64_t)R * n, 0, 1);
 }
 void filter2d_slab_inverse(int n, int nrhs, int R, float2* Zs, const float2* tw, int tw_n, float* x, int64_t ximg,
                            int64_t xoff, bool accumulate, const double* norms, cudaStream_t s) {
   const int64_t nrows = (int64_t)nrhs * (R / 2);
   const int RR = std::max(1, 4096 / n);
   const size_t smr = sizeof(float2) * (size_t)RR * n;
-  fft_rows_kernel<<<nblk(nrows, RR), 256, smr, s>>>(n, nrows, Zs, tw, tw_n, 1, x, accumulate ? 1 : 0,
-                                                    1.0f / ((float)n * (float)n), norms, R / 2, ximg, xoff, 1);
+  fft_rows_kernel<0><<<nblk(nrows, RR), 256, smr, s>>>(n, nrows, Zs, tw, tw_n, 1, x, accumulate ? 1 : 0,
+                                                       1.0f / ((float)n * (float)n), norms, R / 2, ximg, xoff, 1);
 }
 void filter2d_slab_pack(int n, int nrhs, int R, int W, float2* Zs, float2* buf, bool unpack, cudaStream_t s) {
   const int64_t tot = (int64_t)W * nrhs * (R / 2) * filter2d_slab_chunk(n, W);
@@ -701,7 +719,8 @@ void combine_rows_fft(int n, int nrhs, const float* q, const float4* qe, const d
                       const float2* tw, int tw_n, cudaStream_t s) {
   const int R = std::max(1, 4096 / n);
   const size_t smr = sizeof(float2) * (size_t)R * n;
-  combine_rows_fft_kernel<<<nrhs * ceil_div(n / 2, R), 256, smr, s>>>(n, nrhs, q, qe, norms, Z, zb0, tw, tw_n);
+  NMG_DISPATCH_N(n, (combine_rows_fft_kernel<NN><<<nrhs * ceil_div(n / 2, R), 256, smr, s>>>(n, nrhs, q, qe, norms, Z,
+                                                                                           zb0, tw, tw_n)))
 }
 void real_to_complex(int nrhs, int n, const float* x, float2* Z, cudaStream_t s) {
   real_to_complex_kernel<<<nblk((int64_t)nrhs * n * n, 256), 256, 0, s>>>(nrhs, n, x, Z);

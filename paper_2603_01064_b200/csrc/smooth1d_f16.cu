@@ -163,60 +163,66 @@ NMG_D void dft_r(float2 (&v)[R]) {
     v[7] = make_float2(u[6].x - u[7].x, u[6].y - u[7].y);
   }
 }
-// one Stockham radix-R pass: sub-transforms of length Ns -> Ns R (ends with __syncthreads)
-template <int R, bool INV>
-NMG_D void stockham_pass(const float2* src, float2* dst, int m, int Ns, const float2* __restrict__ tw, int tw_n,
-                         int tid, int nthr) {
-  const int q = m / R, tstep = tw_n / (Ns * R);
-  for (int j = tid; j < q; j += nthr) {
-    const int jm = j & (Ns - 1);
+// one Stockham radix-R pass: sub-transforms of length NS -> NS R (ends with __syncthreads).
+// The transform length M and the pass (NS) are compile-time (one instantiation per level
+// size), so the group, twiddle and swizzle index arithmetic folds to shifts and masks.
+template <int R, int NS, int M, bool INV>
+NMG_D void stockham_pass(const float2* src, float2* dst, const float2* __restrict__ tw, int tw_n, int tid) {
+  constexpr int q = M / R;
+  constexpr float inv = 1.0f / (float)(NS * R);   // a power of two: x inv is bitwise x / (NS R)
+  for (int j = tid; j < q; j += NT) {
+    const int jm = j & (NS - 1);
     float2 w[R], v[R];
-    if (Ns > 1) {   // twiddles first: independent of the data, their latency overlaps the loads
+    if constexpr (NS > 1) {   // twiddles first: independent of the data, their latency overlaps the loads
 #ifndef NMG_S1D_TWTABLE
-      // computed twiddles (no dependent table loads; accurate sincospif, exact arguments): w1 = exp(-2 pi i jm / (Ns R)) (argument exact), powers by products
+      // computed twiddles (no dependent table loads; accurate sincospif, exact arguments):
+      // w1 = exp(-2 pi i jm / (NS R)), powers by products
       float sn, cs;
-      sincospif(-2.0f * (float)jm / (float)(Ns * R), &sn, &cs);
+      sincospif(-2.0f * (float)jm * inv, &sn, &cs);
       w[1] = make_float2(cs, sn);
 #pragma unroll
       for (int r = 2; r < R; ++r) w[r] = cmul(w[r - 1], w[1]);
 #else
+      const int tstep = tw_n / (NS * R);
 #pragma unroll
       for (int r = 1; r < R; ++r) w[r] = twid(tw, tw_n, jm * r * tstep);
 #endif
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) v[r] = src[sw(j + r * q)];
-    if (Ns > 1) {
+    if constexpr (NS > 1) {
 #pragma unroll
       for (int r = 1; r < R; ++r) v[r] = INV ? cmulc(v[r], w[r]) : cmul(v[r], w[r]);
     }
     dft_r<R, INV>(v);
     const int d = (j - jm) * R + jm;
 #pragma unroll
-    for (int r = 0; r < R; ++r) dst[sw(d + r * Ns)] = v[r];
+    for (int r = 0; r < R; ++r) dst[sw(d + r * NS)] = v[r];
   }
   __syncthreads();
 }
-// m-point FFT (m a power of two >= 2), natural order; returns the buffer holding the result
-template <bool INV>
-NMG_D float2* stockham_fft(float2* a, float2* b, int m, const float2* __restrict__ tw, int tw_n, int tid, int nthr) {
-  for (int Ns = 1; Ns < m;) {
-    const int rem = m / Ns;
-    if (rem >= 8) { stockham_pass<8, INV>(a, b, m, Ns, tw, tw_n, tid, nthr); Ns *= 8; }
-    else if (rem == 4) { stockham_pass<4, INV>(a, b, m, Ns, tw, tw_n, tid, nthr); Ns *= 4; }
-    else { stockham_pass<2, INV>(a, b, m, Ns, tw, tw_n, tid, nthr); Ns *= 2; }
-    float2* c = a; a = b; b = c;
+// M-point FFT (M a power of two >= 2) from pass NS on, natural order; returns the buffer
+// holding the result (a and b alternate per pass)
+template <int M, int NS, bool INV>
+NMG_D float2* stockham_fft(float2* a, float2* b, const float2* __restrict__ tw, int tw_n, int tid) {
+  if constexpr (NS >= M) {
+    return a;
+  } else {
+    constexpr int REM = M / NS;
+    constexpr int R = REM >= 8 ? 8 : (REM == 4 ? 4 : 2);
+    stockham_pass<R, NS, M, INV>(a, b, tw, tw_n, tid);
+    return stockham_fft<M, NS * R, INV>(b, a, tw, tw_n, tid);
   }
-  return a;
 }
 // F'(h) of the real row in z (swizzled, n reals = n/2 complex); scratch t of n/2 complex.
 // Result (times n/2, unnormalised) back in z.  Starts and ends with __syncthreads().
-NMG_D void level_filter_row(float2* z, float2* t, int n, const float2* __restrict__ tw, int tw_n, int tid,
-                            int nthr) {
-  const int m = n >> 1;
+template <int N>
+NMG_D void level_filter_row(float2* z, float2* t, const float2* __restrict__ tw, int tw_n, int tid) {
+  constexpr int n = N, m = N >> 1, nthr = NT;
   __syncthreads();
-  float2* Z = stockham_fft<false>(z, t, m, tw, tw_n, tid, nthr);
+  float2* Z = stockham_fft<m, 1, false>(z, t, tw, tw_n, tid);
   const int wstep = tw_n / n;   // W_n^k = tw[k * wstep]
+  constexpr float invn = 1.0f / (float)n;   // n a power of two: x invn is bitwise x / n
   // pair (k, m - k): unpack H, apply the mask, repack for the inverse (as real_level_filter)
   constexpr int UNP = 4;
   for (int k0 = tid; k0 <= (m >> 1); k0 += UNP * nthr) {
@@ -227,9 +233,9 @@ NMG_D void level_filter_row(float2* z, float2* t, int n, const float2* __restric
 #ifndef NMG_S1D_TWTABLE
       {
         float sn, cs;
-        sincospif(-2.0f * (float)k / (float)n, &sn, &cs);
+        sincospif(-2.0f * (float)k * invn, &sn, &cs);
         Wv[u] = make_float2(cs, sn);
-        sincospif(-2.0f * (float)((m - k) & (m - 1)) / (float)n, &sn, &cs);
+        sincospif(-2.0f * (float)((m - k) & (m - 1)) * invn, &sn, &cs);
         W2v[u] = make_float2(cs, sn);
       }
 #else
@@ -243,8 +249,8 @@ NMG_D void level_filter_row(float2* z, float2* t, int n, const float2* __restric
     if (k > (m >> 1)) break;
     const int kk = (m - k) & (m - 1);
     const float2 Zk = Z[sw(k)], Zc = Z[sw(kk)];
-    const float mk = sqrtf((float)(2 * k) / (float)n);
-    const float mc = sqrtf((float)(2 * (m - k)) / (float)n);
+    const float mk = sqrtf((float)(2 * k) * invn);
+    const float mc = sqrtf((float)(2 * (m - k)) * invn);
     const float sp = 0.5f * (mk + mc), sm = 0.5f * (mk - mc);
     float2 E = make_float2(0.5f * (Zk.x + Zc.x), 0.5f * (Zk.y - Zc.y));
     float2 O = make_float2(0.5f * (Zk.y + Zc.y), -0.5f * (Zk.x - Zc.x));
@@ -269,7 +275,19 @@ NMG_D void level_filter_row(float2* z, float2* t, int n, const float2* __restric
   }
   __syncthreads();
   float2* other = Z == z ? t : z;
-  stockham_fft<true>(Z, other, m, tw, tw_n, tid, nthr);   // equal pass counts: ends in z
+  stockham_fft<m, 1, true>(Z, other, tw, tw_n, tid);   // equal pass counts: ends in z
+}
+// the level sizes the kernel supports (n % 128 == 0, n <= 8192)
+NMG_D void level_filter_row(float2* z, float2* t, int n, const float2* __restrict__ tw, int tw_n, int tid) {
+  switch (n) {
+    case 128: level_filter_row<128>(z, t, tw, tw_n, tid); break;
+    case 256: level_filter_row<256>(z, t, tw, tw_n, tid); break;
+    case 512: level_filter_row<512>(z, t, tw, tw_n, tid); break;
+    case 1024: level_filter_row<1024>(z, t, tw, tw_n, tid); break;
+    case 2048: level_filter_row<2048>(z, t, tw, tw_n, tid); break;
+    case 4096: level_filter_row<4096>(z, t, tw, tw_n, tid); break;
+    default: level_filter_row<8192>(z, t, tw, tw_n, tid); break;
+  }
 }
 
 // layer-1 producer for channels 8 H .. 8 H + 7 (H compile-time, so the weights are
@@ -574,7 +592,7 @@ __global__ void __launch_bounds__(NT, NMG_S1D_MINB) smooth1d_f16_kernel(const __
       for (int j = tid; j < n; j += NT) hb[hsw(j)] = u[UPAD + j];
       const bool pre = false;
       level_filter_row(reinterpret_cast<float2*>(hb), reinterpret_cast<float2*>(u + UPAD), n, a.twiddle, a.tw_n,
-                       tid, NT);
+                       tid);
       S1D_TS(3);
       if (pre) {
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
