@@ -217,7 +217,10 @@ __global__ void __launch_bounds__(Roles<C, FIRST>::NTHR, 1)
     uint4* dh = reinterpret_cast<uint4*>(Wh);
     uint4* dl = reinterpret_cast<uint4*>(Wl);
     for (int i = tid; i < G::WBYTES / 16; i += NTHR) { dh[i] = __ldg(gh + i); dl[i] = __ldg(gl + i); }
-    for (int i = tid; i < C; i += NTHR) sbias[i] = __ldg(a.bias + i);
+    // the layer's output scale (a2 S2 / a3 S3, powers of two) folded into the bias and the
+    // accumulator scale: ReLU(d acc + b) S = ReLU((d S) acc + b S), bitwise
+    const float osc_fold = FIRST ? a.out_scale : a.a3_scale;
+    for (int i = tid; i < C; i += NTHR) sbias[i] = __ldg(a.bias + i) * osc_fold;
     if (!FIRST) {
       const uint4* g4 = reinterpret_cast<const uint4*>(a.w4);
       uint4* d4 = reinterpret_cast<uint4*>(W4);
@@ -466,8 +469,7 @@ __global__ void __launch_bounds__(Roles<C, FIRST>::NTHR, 1)
     const int m = q * 32 + lane;            // pixel within the strip
     const int c0 = grp * CG;
     const float* bv = sbias + c0;
-    const float dsc = a.d_scale;
-    const float osc = a.out_scale;
+    const float dsc = a.d_scale * (FIRST ? a.out_scale : a.a3_scale);   // output scale folded (see sbias)
     const float b3v = FIRST ? 0.f : __ldg(a.b3);
     float* xch = reinterpret_cast<float*>(misc + 4096);     // [2][4 warps][Q0 of lane 31, Q2 of lane 0]
     int k = 0, e4 = 0;
@@ -585,23 +587,17 @@ __global__ void __launch_bounds__(Roles<C, FIRST>::NTHR, 1)
             const int c = 8 * g + j;
             const float2 d2 = make_float2(__uint_as_float(D[j]), __uint_as_float(D[j + 1]));
             const float2 t = __ffma2_rn(__fadd2_rn(P1[c / 2], d2), dsc2, make_float2(bv[c], bv[c + 1]));
-            act[j] = yin ? fmaxf(t.x, 0.f) : 0.f;
-            act[j + 1] = yin ? fmaxf(t.y, 0.f) : 0.f;
+            // layers 1-2 store only rows inside the image (store implies yin); layers 3-4 feed
+            // the a3 row of a padding row to layer 4 as zeros
+            act[j] = (FIRST || yin) ? fmaxf(t.x, 0.f) : 0.f;
+            act[j + 1] = (FIRST || yin) ? fmaxf(t.y, 0.f) : 0.f;
             P1[c / 2] = __fadd2_rn(P0[c / 2], make_float2(__uint_as_float(D[8 + j]), __uint_as_float(D[9 + j])));
             P0[c / 2] = make_float2(__uint_as_float(D[16 + j]), __uint_as_float(D[17 + j]));
           }
           if (FIRST) {
             if (store) {
-              float v[8];
-              const float2 o2 = make_float2(osc, osc);
-#pragma unroll
-              for (int j = 0; j < 8; j += 2) {
-                const float2 t = __fmul2_rn(make_float2(act[j], act[j + 1]), o2);
-                v[j] = t.x;
-                v[j + 1] = t.y;
-              }
               uint4 hi, lo;
-              split8(v, hi, lo);
+              split8(act, hi, lo);
 #ifndef NMG_STRIP_NOSTORE
               reinterpret_cast<uint4*>(a.out_h + off)[g] = hi;
               reinterpret_cast<uint4*>(a.out_l + off)[g] = lo;
@@ -610,16 +606,8 @@ __global__ void __launch_bounds__(Roles<C, FIRST>::NTHR, 1)
 #endif
             }
           } else {
-            float v[8];
-            const float2 s3 = make_float2(a.a3_scale, a.a3_scale);
-#pragma unroll
-            for (int j = 0; j < 8; j += 2) {
-              const float2 t = __fmul2_rn(make_float2(act[j], act[j + 1]), s3);
-              v[j] = t.x;
-              v[j + 1] = t.y;
-            }
             uint4 hi, lo;
-            split8(v, hi, lo);
+            split8(act, hi, lo);
             reinterpret_cast<uint4*>(A4)[(c0 / 8 + g) * SEG + m] = hi;
             reinterpret_cast<uint4*>(A4 + G::A4BYTES)[(c0 / 8 + g) * SEG + m] = lo;
           }
