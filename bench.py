@@ -28,6 +28,9 @@ import argparse
 import json
 import math
 import os
+# NCCL's banner / debug lines (NCCL_DEBUG=VERSION in some images) go to stderr: stdout carries
+# only the one JSON line per run
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 import statistics
 import subprocess
 import sys
