@@ -341,11 +341,7 @@ NMG_D void a1_row2(const Smooth1dArgs& a, const float* u, int p0, int p1, int n,
   }
   split8(v0, hi0, lo0);
   split8(v1, hi1, lo1);
-  // padding positions (outside [0, n)) are zeros of layer 2's input: one select per packed word
-  // instead of one per channel
-  const uint4 z = make_uint4(0u, 0u, 0u, 0u);
-  if (!ok0) { hi0 = z; lo0 = z; }
-  if (!ok1) { hi1 = z; lo1 = z; }
+  // positions outside [0, n) are zeros of layer 2's input: the caller stores zero words there
 }
 
 // Layer-1 producer for channels 8 H .. 8 H + 7 (H compile-time, so the weights are
@@ -367,8 +363,14 @@ NMG_D void produce_a1(const Smooth1dArgs& a, uint8_t* Abuf, uint64_t* aempty, ui
     mb_wait(&aempty[st], ((uint32_t)(k / NSA) & 1u) ^ 1u);
     uint4* ah = reinterpret_cast<uint4*>(Abuf + (2 * st) * ABYTES) + H * AR;
     uint4* al = reinterpret_cast<uint4*>(Abuf + (2 * st + 1) * ABYTES) + H * AR;
+    // position Q0 + 2 + r0 is always inside the row; Q0 + 66 + r0 passes its end only in the last
+    // tile (predicated zero stores instead of selects)
     ah[4 + r0] = h0; al[4 + r0] = l0;
-    ah[68 + r0] = h1; al[68 + r0] = l1;
+    if (Q0 + 66 + r0 < n) {
+      ah[68 + r0] = h1; al[68 + r0] = l1;
+    } else {
+      ah[68 + r0] = make_uint4(0u, 0u, 0u, 0u); al[68 + r0] = make_uint4(0u, 0u, 0u, 0u);
+    }
     if (carry) {
       ah[r0 - 60] = ch; al[r0 - 60] = cl;
       ch = h1; cl = l1;

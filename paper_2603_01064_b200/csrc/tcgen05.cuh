@@ -19,14 +19,28 @@ NMG_D void mb_expect(uint64_t* b, uint32_t bytes) {
 NMG_D void mb_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
 }
-// spin on the phase parity (try_wait suspends the thread for a bounded time per probe)
+// wait for the phase parity: try_wait suspends the warp until the phase completes or a time
+// limit passes (NMG_MB_SUSPEND_NS: the suspend-time hint; without one the probe returns early and
+// the loop spins, taking issue slots from the other warps of the SM)
+#ifndef NMG_MB_SUSPEND_NS
+#define NMG_MB_SUSPEND_NS 0
+#endif
 NMG_D void mb_wait(uint64_t* b, uint32_t ph) {
+#if NMG_MB_SUSPEND_NS > 0
+  asm volatile(
+      "{\n.reg .pred P1;\nMBW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@P1 bra MBD_%=;\nbra MBW_%=;\nMBD_%=:\n}\n" ::"r"(su32(b)),
+      "r"(ph), "r"((uint32_t)NMG_MB_SUSPEND_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n.reg .pred P1;\nMBW_%=:\n"
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
       "@P1 bra MBD_%=;\nbra MBW_%=;\nMBD_%=:\n}\n" ::"r"(su32(b)),
       "r"(ph)
       : "memory");
+#endif
 }
 
 NMG_D void tma2d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
