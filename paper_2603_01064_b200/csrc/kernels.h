@@ -193,7 +193,7 @@ void update_x(int nrhs, int N, double* x, int64_t ldx, const float* d, int64_t l
               const uint8_t* active, cudaStream_t s);
 void f64_to_f32(int64_t count, const double* in, float* out, cudaStream_t s);
 void f32_to_f64(int64_t count, const float* in, double* out, cudaStream_t s);
-// rows of N doubles: dst[i] = src[map[i]] (gather) or dst[map[i]] = src[i] (scatter); rows <= 65535
+// rows of N doubles: dst[i] = src[map[i]] (gather) or dst[map[i]] = src[i] (scatter)
 void permute_rows(int rows, int64_t N, const double* src, double* dst, const int32_t* map, bool scatter,
                   cudaStream_t s);
 

@@ -320,17 +320,17 @@ __global__ void update_x_kernel(int nrhs, int N, double* __restrict__ x, int64_t
 // src row i (scatter); rows of N doubles, 16-byte vectors when N is even
 __global__ void permute_rows_kernel(int rows, int64_t N, const double* __restrict__ src, double* __restrict__ dst,
                                     const int32_t* __restrict__ map, int scatter) {
-  const int i = blockIdx.y;
-  if (i >= rows) return;
-  const int64_t si = scatter ? i : map[i], di = scatter ? map[i] : i;
-  if (N % 2 == 0) {
-    const double2* s2 = reinterpret_cast<const double2*>(src + si * N);
-    double2* d2 = reinterpret_cast<double2*>(dst + di * N);
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < N / 2; k += (int64_t)gridDim.x * blockDim.x)
-      d2[k] = s2[k];
-  } else {
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < N; k += (int64_t)gridDim.x * blockDim.x)
-      dst[di * N + k] = src[si * N + k];
+  for (int i = blockIdx.y; i < rows; i += gridDim.y) {
+    const int64_t si = scatter ? i : map[i], di = scatter ? map[i] : i;
+    if (N % 2 == 0) {
+      const double2* s2 = reinterpret_cast<const double2*>(src + si * N);
+      double2* d2 = reinterpret_cast<double2*>(dst + di * N);
+      for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < N / 2; k += (int64_t)gridDim.x * blockDim.x)
+        d2[k] = s2[k];
+    } else {
+      for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < N; k += (int64_t)gridDim.x * blockDim.x)
+        dst[di * N + k] = src[si * N + k];
+    }
   }
 }
 
@@ -408,7 +408,7 @@ void permute_rows(int rows, int64_t N, const double* src, double* dst, const int
                   cudaStream_t s) {
   if (rows <= 0) return;
   const int bx = (int)std::min<int64_t>(64, (N / 2 + 255) / 256 + 1);
-  permute_rows_kernel<<<dim3(bx, rows), 256, 0, s>>>(rows, N, src, dst, map, scatter ? 1 : 0);
+  permute_rows_kernel<<<dim3(bx, std::min(rows, 65535)), 256, 0, s>>>(rows, N, src, dst, map, scatter ? 1 : 0);
 }
 void f64_to_f32(int64_t count, const double* in, float* out, cudaStream_t s) {
   f64_to_f32_kernel<<<nblk(count, 256), 256, 0, s>>>(count, in, out);
