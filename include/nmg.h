@@ -97,6 +97,12 @@ typedef struct {
   int32_t no_compaction;  /* 1: nmg_solve keeps cycling the whole batch (converged RHS masked)
                              instead of gathering the active RHS into a smaller batch; 2:
                              gather whenever one RHS converged (parity tests)               */
+  int32_t dense_k;        /* 1: the operator contractions run every K block, including the blocks
+                             whose split operator digits are all zero (the Gaussian operators'
+                             far-off-diagonal blocks; skipping them is exact) */
+  int32_t no_balance;     /* 1: load the CNN weights as given instead of lifting hidden channels
+                             whose activation bound lies > 2^4 below their layer's largest by a
+                             power of two (an exactly equivalent network, see nmg_api.cu)    */
 } nmg_tuning;
 
 /* Problem descriptor (SPEC ProblemSpec analogue). */

@@ -40,7 +40,8 @@ class Tuning(C.Structure):
     _fields_ = [("lanes", C.c_int32), ("no_graphs", C.c_int32), ("coarse_subst", C.c_int32),
                 ("fp64_dmma", C.c_int32), ("simt_gemm", C.c_int32), ("ffma_cnn", C.c_int32),
                 ("no_kron", C.c_int32), ("host_chunks", C.c_int32), ("fused_coarse", C.c_int32),
-                ("no_compaction", C.c_int32)]
+                ("no_compaction", C.c_int32), ("dense_k", C.c_int32),
+                ("no_balance", C.c_int32)]
 
 
 class ProblemDesc(C.Structure):

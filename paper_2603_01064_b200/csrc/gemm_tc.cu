@@ -134,7 +134,21 @@ __global__ void __launch_bounds__(TNT, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int m0 = blockIdx.y * TBM, n0 = blockIdx.x * TBN;
-  const int KT = ceil_div(a.K, KE);
+  // K blocks [kb, ke): outside the union of the tile's 64-row ranges every W element is zero in
+  // both planes, so the skipped products are exact zeros (CTA pairs along M share n0: same range)
+  int kb = 0, ke = ceil_div(a.K, KE);
+  if (a.krange) {
+    int lo = a.K, hi = 0;
+#pragma unroll
+    for (int t = 0; t < TBN / 64; ++t) {
+      if (n0 + 64 * t >= a.N) break;
+      const int2 r = __ldg(&a.krange[n0 / 64 + t]);
+      lo = min(lo, r.x);
+      hi = max(hi, r.y);
+    }
+    kb = lo / KE;
+    ke = max(kb + 1, min(ke, ceil_div(hi, KE)));
+  }
 
   const uint32_t crank = MC ? cta_rank_in_cluster() : 0u;
   if (tid == 0) {
@@ -156,9 +170,9 @@ __global__ void __launch_bounds__(TNT, 1)
 
   if (warp == 0) {
     if (lane == 0) {   // ---------------- TMA producer
-      for (int kt = 0; kt < KT; ++kt) {
-        const int s = kt % TSTAGES;
-        const uint32_t ph = (uint32_t)(kt / TSTAGES) & 1u;
+      for (int kt = kb; kt < ke; ++kt) {
+        const int s = (kt - kb) % TSTAGES;
+        const uint32_t ph = (uint32_t)((kt - kb) / TSTAGES) & 1u;
         mb_wait(&empty[s], ph ^ 1u);
         uint8_t* st = sm + s * STAGE_BYTES;
         mb_expect(&full[s], STAGE_BYTES);
@@ -179,9 +193,9 @@ __global__ void __launch_bounds__(TNT, 1)
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {   // ---------------- MMA issuer
-      for (int kt = 0; kt < KT; ++kt) {
-        const int s = kt % TSTAGES;
-        const uint32_t ph = (uint32_t)(kt / TSTAGES) & 1u;
+      for (int kt = kb; kt < ke; ++kt) {
+        const int s = (kt - kb) % TSTAGES;
+        const uint32_t ph = (uint32_t)((kt - kb) / TSTAGES) & 1u;
         mb_wait(&full[s], ph);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         const uint32_t st = su32(sm + s * STAGE_BYTES);
@@ -193,11 +207,11 @@ __global__ void __launch_bounds__(TNT, 1)
           const uint64_t dwh = desc_sw64(st + 2 * A_BYTES + ko);
           const uint64_t dwl = desc_sw64(st + 2 * A_BYTES + B_BYTES + ko);
           if (F16) {
-            mma_f16(tmem, dxh, dwh, kIdesc, (kt | ks) ? 1u : 0u);
+            mma_f16(tmem, dxh, dwh, kIdesc, (kt != kb || ks) ? 1u : 0u);
             mma_f16(tmem, dxh, dwl, kIdesc, 1u);
             mma_f16(tmem, dxl, dwh, kIdesc, 1u);
           } else {
-            mma_tf32(tmem, dxh, dwh, kIdesc, (kt | ks) ? 1u : 0u);
+            mma_tf32(tmem, dxh, dwh, kIdesc, (kt != kb || ks) ? 1u : 0u);
             mma_tf32(tmem, dxh, dwl, kIdesc, 1u);
             mma_tf32(tmem, dxl, dwh, kIdesc, 1u);
           }

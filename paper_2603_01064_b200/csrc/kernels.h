@@ -69,6 +69,9 @@ struct OzakiArgs {
   int tb_R = 0, tb_S = 0;
   int64_t tb_img = 0, r32_img = 0, r32_off = 0;
   int wrow0 = 0;
+  // per ozaki_bn()-row tile of W (absolute W rows): the K blocks [x, y) (units of ozaki_bk())
+  // outside which every digit of the tile is zero; null = all K blocks
+  const int2* krange = nullptr;
 };
 int ozaki_digits();
 int ozaki_bk();   // K block of the digit tensor maps (box K; 32: SWIZZLE_32B, 64: SWIZZLE_64B)
@@ -95,6 +98,9 @@ struct TcGemmArgs {
   // multicast the W tile (cluster 1 x 2), when the number of M tiles is even
   const CUtensorMap* wh_mc = nullptr;
   const CUtensorMap* wl_mc = nullptr;
+  // optional, per 64-row tile of W: the K elements [x, y) (multiples of 32) outside which the
+  // tile's hi and lo planes are all zero (those K blocks are skipped; null = all of K)
+  const int2* krange = nullptr;
 };
 // 2D Kronecker apply passes on tcgen05 (kron_tc.cu).  A = fp32 [M][n] rows (TMA map, box
 // {16, 128}, SWIZZLE_64B), W = tf32 hi/lo [n][n] (box {16, kron_tile_n(n)}).

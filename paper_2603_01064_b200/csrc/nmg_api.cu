@@ -120,6 +120,31 @@ void host_digits(const std::vector<double>& A, int n, int S, std::vector<int8_t>
   }
 }
 
+// K-block range per row tile of digit planes dig [S][rows][K]: [first, last + 1) of the bk-wide
+// K blocks holding a nonzero digit of the tile's bn rows in any plane.  The Gaussian operators
+// decay below 2^-49 of their row maximum a few hundred points off the diagonal, where every
+// truncation digit is zero: the contraction may skip those blocks exactly (int32 zeros).  An
+// all-zero tile keeps one block so that its accumulators are written.
+std::vector<int2> digit_kranges(const std::vector<int8_t>& dig, int S, int rows, int K, int bn, int bk) {
+  std::vector<int2> kr(rows / bn);
+  for (int t = 0; t < rows / bn; ++t) {
+    int lo = K / bk, hi = 0;
+    for (int kb = 0; kb < K / bk; ++kb) {
+      bool nz = false;
+      for (int i = 0; i < S && !nz; ++i)
+        for (int r = t * bn; r < (t + 1) * bn && !nz; ++r) {
+          const int8_t* row = dig.data() + ((size_t)i * rows + r) * K + (size_t)kb * bk;
+          for (int k = 0; k < bk; ++k)
+            if (row[k]) { nz = true; break; }
+        }
+      if (nz) { lo = std::min(lo, kb); hi = kb + 1; }
+    }
+    if (hi <= lo) { lo = 0; hi = 1; }
+    kr[t] = make_int2(lo, hi);
+  }
+  return kr;
+}
+
 // ---------------------------------------------------------------- host fp64 transfers
 // R (n_f/2 x n_f) applied to the rows of a column block: out = R * A  (A: n_f x cols)
 void host_restrict_rows(const std::vector<double>& A, int n_f, int cols, std::vector<double>& out) {
@@ -330,7 +355,7 @@ struct nmg_hierarchy {
   std::vector<char> split_fresh;                         // sxh/sxl[l] hold the split of wx[l]
   // 1D inner operator applies in FP16x3 (kind::f16): per-row-scaled f16 hi/lo planes
   bool gemm_f16 = false;
-  struct F16Op { DevBuf<uint16_t> h, l; DevBuf<float> winv; CUtensorMap m256h, m256l, m64h, m64l, m128h, m128l; };
+  struct F16Op { DevBuf<uint16_t> h, l; DevBuf<float> winv; DevBuf<int2> kr; CUtensorMap m256h, m256l, m64h, m64l, m128h, m128l; };
   bool gemm_mc = true;                                   // 256-wide FP16x3 tiles multicast W over CTA pairs
   std::vector<std::unique_ptr<F16Op>> A16, AP16;         // per smoothed level
   std::vector<std::unique_ptr<DevBuf<uint16_t>>> sx16h, sx16l;
@@ -351,6 +376,8 @@ struct nmg_hierarchy {
   DevBuf<int8_t> wdigB;
   DevBuf<int> wexpB;
   CUtensorMap mWdB{};
+  // per ozaki_bn()-row tile of the W digits: the K blocks holding a nonzero digit (C / A, then B)
+  DevBuf<int2> wkr, wkrB;
   // 2D: A_l = B_l (x) C_l + alpha Q_l (x) Q_l; fp32 factors (SIMT), tf32 hi/lo (tcgen05)
   std::vector<std::unique_ptr<DevBuf<float>>> B32, C32, B32h, B32l, C32h, C32l, Q32;
   std::vector<int> qhb;                                  // Q_l half-bandwidth
@@ -636,6 +663,7 @@ nmg_status level_resid(nmg_hierarchy* h, int l, int which, int nrhs, const float
     g.M = nrhs; g.N = n; g.K = K;
     g.C = C; g.ldc = n; g.D = D; g.ldd = n; g.negate = negate;
     g.xinv = h->sxinv[lx]->p; g.winv = W.winv.p;
+    g.krange = h->tune.dense_k ? nullptr : W.kr.p;
     if (h->gemm_mc) { g.wh_mc = &W.m128h; g.wl_mc = &W.m128l; }
     {
       Prof p(h, NMG_K_GEMM32, s);
@@ -1090,7 +1118,7 @@ nmg_status outer_residual_slab(nmg_hierarchy* h, int nrhs, const double* y, cons
     o.M = nrhs * R; o.N = n; o.K = n;
     o.r64 = h->t64send.p; o.plus = true;
     o.tblock = n; o.tb_R = R; o.tb_S = R; o.tb_img = (int64_t)n * R;
-    o.ex = h->xexp.p; o.ew = h->wexp.p;
+    o.ex = h->xexp.p; o.ew = h->wexp.p; o.krange = h->tune.dense_k ? nullptr : h->wkr.p;
     { Prof p(h, NMG_K_GEMM64, s); ozaki_resid(&h->mXd, &h->mWd, o, s); }
     NMG_TRY(check_launch(h));
     NMG_TRY(h->comm->all_gather(h->t64send.p, h->t64recv.p, sizeof(double) * (size_t)nrhs * n * R, s));
@@ -1104,6 +1132,7 @@ nmg_status outer_residual_slab(nmg_hierarchy* h, int nrhs, const double* y, cons
     q.r64 = r64; q.part = want_part ? h->part.p : nullptr;
     q.tblock = n; q.tb_R = n; q.tb_S = n; q.tb_img = (int64_t)R * n;
     q.ex = h->xexp.p; q.ew = h->wexpB.p; q.wrow0 = r0;
+    q.krange = (h->tune.dense_k || r0 % (2 * ozaki_bn())) ? nullptr : h->wkrB.p;
     { Prof p(h, NMG_K_GEMM64, s); ozaki_resid(&h->mXd, &h->mWdB, q, s); }
     return check_launch(h);
   }
@@ -1146,7 +1175,7 @@ nmg_status outer_residual(nmg_hierarchy* h, int nrhs, const double* y, const dou
     OzakiArgs o{};
     o.M = M; o.N = n; o.K = n;
     o.r64 = h->T64.p; o.tblock = n; o.plus = true;
-    o.ex = h->xexp.p; o.ew = h->wexp.p;
+    o.ex = h->xexp.p; o.ew = h->wexp.p; o.krange = h->tune.dense_k ? nullptr : h->wkr.p;
     { Prof p(h, NMG_K_GEMM64, s); ozaki_resid(&h->mXd, &h->mWd, o, s); }
     NMG_TRY(check_launch(h));
     { Prof p(h, NMG_K_GEMM64, s); ozaki_split_rows(M, n, h->T64.p, n, h->xdig.p, plane, h->xexp.p, s); }
@@ -1155,7 +1184,7 @@ nmg_status outer_residual(nmg_hierarchy* h, int nrhs, const double* y, const dou
     q.M = M; q.N = n; q.K = n;
     q.Y = y; q.r32 = h->wy[0]->p; q.r64 = r64; q.part = want_part ? h->part.p : nullptr;
     q.tblock = n; q.ax = x; q.alpha = h->d.alpha;
-    q.ex = h->xexp.p; q.ew = h->wexpB.p;
+    q.ex = h->xexp.p; q.ew = h->wexpB.p; q.krange = h->tune.dense_k ? nullptr : h->wkrB.p;
     { Prof p(h, NMG_K_GEMM64, s); ozaki_resid(&h->mXd, &h->mWdB, q, s); }
     return check_launch(h);
   }
@@ -1186,7 +1215,7 @@ nmg_status outer_residual(nmg_hierarchy* h, int nrhs, const double* y, const dou
     o.r32 = h->wy[0]->p; o.ldr32 = n;
     o.r64 = r64; o.ldr64 = n;
     o.part = want_part ? h->part.p : nullptr;
-    o.ex = h->xexp.p; o.ew = h->wexp.p;
+    o.ex = h->xexp.p; o.ew = h->wexp.p; o.krange = h->tune.dense_k ? nullptr : h->wkr.p;
     { Prof p(h, NMG_K_GEMM64, s); ozaki_resid(&h->mXd, &h->mWd, o, s); }
     return check_launch(h);
   }
@@ -1545,8 +1574,24 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
               lo[(size_t)r * cols + c] = f16_rn(v - f16_f(hi[(size_t)r * cols + c]));
             }
           }
+          // per 64-row tile: the 32-element K blocks holding a nonzero hi or lo value (the
+          // Gaussian operators' far off-diagonal entries flush to zero in both f16 planes: the
+          // FP16x3 GEMM skips those blocks, whose products are exact zeros)
+          std::vector<int2> kr(rows / 64);
+          for (int t = 0; t < rows / 64; ++t) {
+            int lo_k = cols, hi_k = 0;
+            for (int r = t * 64; r < (t + 1) * 64; ++r)
+              for (int c = 0; c < cols; ++c)
+                if ((hi[(size_t)r * cols + c] | lo[(size_t)r * cols + c]) & 0x7fffu) {
+                  lo_k = std::min(lo_k, c);
+                  hi_k = std::max(hi_k, c + 1);
+                }
+            if (hi_k <= lo_k) { lo_k = 0; hi_k = 32; }
+            kr[t] = make_int2(lo_k / 32 * 32, (hi_k + 31) / 32 * 32);
+          }
           if (op->h.upload(hi.data(), hi.size()) != NMG_OK || op->l.upload(lo.data(), lo.size()) != NMG_OK ||
-              op->winv.upload(winv.data(), winv.size()) != NMG_OK)
+              op->winv.upload(winv.data(), winv.size()) != NMG_OK ||
+              (rows % 64 == 0 && op->kr.upload(kr.data(), kr.size()) != NMG_OK))
             return nullptr;
           return op;
         };
@@ -1770,6 +1815,8 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
       host_digits(A, n, S, dig, ew);
       NMG_TRY(h->wdig.upload(dig.data(), dig.size()));
       NMG_TRY(h->wexp.upload(ew.data(), ew.size()));
+      const std::vector<int2> kr = digit_kranges(dig, S, n, n, ozaki_bn(), ozaki_bk());
+      NMG_TRY(h->wkr.upload(kr.data(), kr.size()));
       NMG_TRY(h->xdig.alloc((size_t)S * B * n));
       NMG_TRY(h->xexp.alloc(B));
       NMG_TRY(make_digit_map(&h->mWd, h->wdig.p, S, n, n, ozaki_bn()));
@@ -1788,9 +1835,13 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
       host_digits(Cm, n, S, dig, ew);
       NMG_TRY(h->wdig.upload(dig.data(), dig.size()));
       NMG_TRY(h->wexp.upload(ew.data(), ew.size()));
+      std::vector<int2> kr = digit_kranges(dig, S, n, n, ozaki_bn(), ozaki_bk());
+      NMG_TRY(h->wkr.upload(kr.data(), kr.size()));
       host_digits(Bm, n, S, dig, ew);
       NMG_TRY(h->wdigB.upload(dig.data(), dig.size()));
       NMG_TRY(h->wexpB.upload(ew.data(), ew.size()));
+      kr = digit_kranges(dig, S, n, n, ozaki_bn(), ozaki_bk());
+      NMG_TRY(h->wkrB.upload(kr.data(), kr.size()));
       NMG_TRY(h->xdig.alloc((size_t)S * B * nn));
       NMG_TRY(h->xexp.alloc(B * n));
       NMG_TRY(make_digit_map(&h->mWd, h->wdig.p, S, n, n, ozaki_bn()));
@@ -1922,8 +1973,60 @@ nmg_status nmg_create_hierarchy_slab(const nmg_problem_desc* desc, const double*
   return NMG_OK;
 }
 
+// Exact rebalancing of the CNN's hidden channels before the FP16x3 splits.  ReLU is positively
+// homogeneous, so scaling hidden channel c of layer k (its weights and bias) by a power of two
+// lambda_c and the next layer's input-channel-c weights by 1 / lambda_c leaves every fp32 value
+// of the network bitwise unchanged up to the factor lambda_c on a_k[c] (power-of-two products and
+// sums round identically; exponents are clamped far from the fp32 range ends).  A channel whose
+// activation bound B_k[c] = |b_k[c]| + sum |w_k[c]| B_{k-1} lies more than 2^4 below the layer's
+// largest is lifted into the largest one's binade: the layer's split scale S_k = 2^14 / max_c
+// B_k[c] would otherwise leave such a channel only a few bits in its f16 hi/lo parts (the spread
+// moves to the next layer's weights, whose split scale comes from their actual maximum).  Layers
+// whose channels all lie within 2^4 of each other (the seeded and the trained smoothers) are
+// left as given, so their splits are unchanged.
+void balance_cnn(std::vector<float>& p, int n_layers, int C, int kk) {
+  std::vector<double> bin(1, 1.0);   // |u| <= 1 (||u||_2 = 1 after the normalisation)
+  size_t off = 0;
+  int cin = 1;
+  for (int layer = 0; layer + 1 < n_layers; ++layer) {
+    const int cout = C;
+    float* w = p.data() + off;
+    float* b = w + (size_t)cout * cin * kk;
+    const size_t next = off + (size_t)cout * cin * kk + cout;   // next layer's weights [o'][c][t]
+    const int cout_next = layer + 2 == n_layers ? 1 : C;
+    std::vector<double> bout(cout, 0.0);
+    double bmax = 0.0;
+    for (int o = 0; o < cout; ++o) {
+      double B = std::fabs((double)b[o]);
+      for (int c = 0; c < cin; ++c)
+        for (int t = 0; t < kk; ++t) B += std::fabs((double)w[((size_t)o * cin + c) * kk + t]) * bin[c];
+      bout[o] = B;
+      if (std::isfinite(B)) bmax = std::max(bmax, B);
+    }
+    int emax = 0;
+    if (bmax > 0.0) std::frexp(bmax, &emax);
+    for (int o = 0; o < cout; ++o) {
+      const double B = bout[o];
+      if (!(B > 0.0) || !(B < std::ldexp(bmax, -4))) continue;
+      int e = 0;
+      std::frexp(B, &e);
+      const int sh = std::min(40, emax - e);                     // B 2^sh in bmax's binade
+      const float lam = std::ldexp(1.0f, sh), inv = std::ldexp(1.0f, -sh);
+      for (int i = 0; i < cin * kk; ++i) w[(size_t)o * cin * kk + i] *= lam;
+      b[o] *= lam;
+      for (int o2 = 0; o2 < cout_next; ++o2)
+        for (int t = 0; t < kk; ++t) p[next + ((size_t)o2 * cout + o) * kk + t] *= inv;
+      bout[o] = std::ldexp(B, sh);
+    }
+    bin.swap(bout);
+    off = next;
+    cin = cout;
+  }
+}
+
 nmg_status nmg_load_smoother_weights(nmg_hierarchy* h, int32_t level, const nmg_cnn_arch* arch,
-                                     const float* params, size_t n_params) {
+                                     const float* params_in, size_t n_params) {
+  const float* params = params_in;
   g_err.clear();
   if (!h || !arch || !params) return fail(NMG_ERR_INVALID_ARG, "null argument");
   if (level < 1 || level > h->L - 1) return fail(NMG_ERR_INVALID_ARG, "level %d outside 1..%d", level, h->L - 1);
@@ -1942,6 +2045,11 @@ nmg_status nmg_load_smoother_weights(nmg_hierarchy* h, int32_t level, const nmg_
     cin = cout;
   }
   if (n_params != want) return fail(NMG_ERR_SHAPE, "expected %zu parameters, got %zu", want, n_params);
+  std::vector<float> balanced(params, params + n_params);
+  if (!h->tune.no_balance) {
+    balance_cnn(balanced, arch->n_layers, C, kk);
+    params = balanced.data();
+  }
   NMG_CUDA(cudaSetDevice(h->d.device));
   // captured cycle graphs bake in weight pointers, tensor maps and by-value weights: drop them
   // (after the device is idle) so the next cycle re-captures with the new smoother

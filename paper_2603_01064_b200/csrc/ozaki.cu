@@ -83,7 +83,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ONT, OBN == 32 ? 2 :
   uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int m0 = blockIdx.y * OBM, n0 = blockIdx.x * OBN;
-  const int KT = a.K / OBK;
+  // K blocks [kb, ke): the union of the two W tiles of the CTA pair (both CTAs run the same
+  // blocks: they share the multicast X stages).  Outside it every digit of both W tiles is zero,
+  // so the skipped int32 products are exact zeros and the accumulators are bitwise unchanged.
+  int kb = 0, ke = a.K / OBK;
+  if (a.krange) {
+    const int t0 = ((GEN ? a.wrow0 : 0) + (int)(blockIdx.x & ~1u) * OBN) / OBN;
+    const int2 r0 = __ldg(&a.krange[t0]), r1 = __ldg(&a.krange[t0 + 1]);
+    kb = min(r0.x, r1.x);
+    ke = max(r0.y, r1.y);
+  }
 
   const uint32_t crank = cluster_rank();
   if (tid == 0) {
@@ -102,9 +111,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ONT, OBN == 32 ? 2 :
 
   if (warp == 0) {
     if (lane == 0) {   // TMA producer: all S digit planes of X and W for one 64-wide K block
-      for (int kt = 0; kt < KT; ++kt) {
-        const int s = kt % ONSTAGE;
-        mb_wait(&empty[s], ((uint32_t)(kt / ONSTAGE) & 1u) ^ 1u);
+      for (int kt = kb; kt < ke; ++kt) {
+        const int s = (kt - kb) % ONSTAGE;
+        mb_wait(&empty[s], ((uint32_t)((kt - kb) / ONSTAGE) & 1u) ^ 1u);
         uint8_t* st = sm + s * OSTAGE;
         mb_expect(&full[s], OSTAGE);                 // own W + both halves of X
 #pragma unroll
@@ -116,9 +125,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ONT, OBN == 32 ? 2 :
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {   // MMA issuer: 28 digit-pair products (10 MMAs) per 32-wide K step
-      for (int kt = 0; kt < KT; ++kt) {
-        const int s = kt % ONSTAGE;
-        mb_wait(&full[s], (uint32_t)(kt / ONSTAGE) & 1u);
+      for (int kt = kb; kt < ke; ++kt) {
+        const int s = (kt - kb) % ONSTAGE;
+        mb_wait(&full[s], (uint32_t)((kt - kb) / ONSTAGE) & 1u);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         const uint32_t xs = su32(sm + s * OSTAGE), ws = xs + XS_BYTES;
 #pragma unroll
@@ -134,8 +143,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ONT, OBN == 32 ? 2 :
               const int d = i + j0 - 2;                      // first accumulator 0 .. OS - 1
               const uint64_t da = OBK == 32 ? desc_sw32(xs + (i - 1) * OBM * OBK) : desc_sw64(xs + (i - 1) * OBM * OBK + ks * 32);
               const uint64_t db = OBK == 32 ? desc_sw32(ws + (j0 - 1) * OBN * OBK) : desc_sw64(ws + (j0 - 1) * OBN * OBK + ks * 32);
-              // the first products into the diagonals come from i = 1 at kt = ks = 0
-              mma_i8(tmem + (uint32_t)(d * OBN), da, db, idesc_i8(nd), (kt == 0 && ks == 0 && i == 1) ? 0u : 1u);
+              // the first products into the diagonals come from i = 1 at kt = kb, ks = 0
+              mma_i8(tmem + (uint32_t)(d * OBN), da, db, idesc_i8(nd), (kt == kb && ks == 0 && i == 1) ? 0u : 1u);
             }
           }
         }
