@@ -122,6 +122,9 @@ struct KronArgs {
   // (W rows r0 .. r0 + R - 1, W map box rows kron_tile_n(R)).
   int R = 0, H = 0, r0 = 0;
   int64_t img = 0;
+  // optional, per 64-row tile of W (absolute rows): the K elements [x, y) (multiples of 16)
+  // outside which the tile's tf32 hi and lo values are all zero (skipped; null = all of K)
+  const int2* krange = nullptr;
 };
 int kron_tile_n(int n);
 bool kron_supported(int n, int hb);

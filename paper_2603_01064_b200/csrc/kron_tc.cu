@@ -68,6 +68,23 @@ __global__ void __launch_bounds__(KNT, 1)
   const int wrow0 = a.mode == KRON_T ? 0 : a.r0;
   const int MT = (a.M + KBM - 1) / KBM;
   const int T = MT * NT;
+  // K blocks of output-column tile n0: outside the union of its 64-row W ranges every W hi/lo
+  // value is zero, so those products are exact zeros (the producer, the splitters and the MMA
+  // issuer all walk the same blocks)
+  auto krange = [&](int n0, int& kb, int& ke) {
+    kb = 0;
+    ke = KT;
+    if (!a.krange) return;
+    int lo = n, hi = 0;
+    for (int t = 0; t < TBN / 64 && n0 + 64 * t < (a.mode == KRON_T ? n : R); ++t) {
+      const int2 r = __ldg(&a.krange[(wrow0 + n0) / 64 + t]);
+      lo = min(lo, r.x);
+      hi = max(hi, r.y);
+    }
+    if (hi <= lo) return;
+    kb = lo / KBK;
+    ke = max(kb + 1, min(KT, (hi + KBK - 1) / KBK));
+  };
 
   if (tid == 0) {
     for (int s = 0; s < ST; ++s) { mb_init(&full[s], 1); mb_init(&split[s], 4); mb_init(&empty[s], 1); }
@@ -92,7 +109,9 @@ __global__ void __launch_bounds__(KNT, 1)
       int it = 0;
       for (int t = blockIdx.x; t < T; t += gridDim.x) {
         const int m0 = (t / NT) * KBM, n0 = (t % NT) * TBN;
-        for (int kt = 0; kt < KT; ++kt, ++it) {
+        int kb, ke;
+        krange(n0, kb, ke);
+        for (int kt = kb; kt < ke; ++kt, ++it) {
           const int s = it % ST;
           mb_wait(&empty[s], ((uint32_t)(it / ST) & 1u) ^ 1u);
           uint8_t* st = sm + s * STAGE;
@@ -107,7 +126,9 @@ __global__ void __launch_bounds__(KNT, 1)
     const int ct = tid - 128;
     int it = 0;
     for (int t = blockIdx.x; t < T; t += gridDim.x) {
-      for (int kt = 0; kt < KT; ++kt, ++it) {
+      int kb, ke;
+      krange((t % NT) * TBN, kb, ke);
+      for (int kt = kb; kt < ke; ++kt, ++it) {
         const int s = it % ST;
         mb_wait(&full[s], (uint32_t)(it / ST) & 1u);
         float4* hi = reinterpret_cast<float4*>(sm + s * STAGE);
@@ -136,7 +157,9 @@ __global__ void __launch_bounds__(KNT, 1)
         mb_wait(&tempty[ab], ((uint32_t)(i >> 1) & 1u) ^ 1u);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         const uint32_t d = tmem + (uint32_t)(ab * TBN);
-        for (int kt = 0; kt < KT; ++kt, ++it) {
+        int kb, ke;
+        krange((t % NT) * TBN, kb, ke);
+        for (int kt = kb; kt < ke; ++kt, ++it) {
           const int s = it % ST;
           const uint32_t ph = (uint32_t)(it / ST) & 1u;
           mb_wait(&full[s], ph);
@@ -148,7 +171,7 @@ __global__ void __launch_bounds__(KNT, 1)
             const uint32_t ko = ks * 32;   // 8 tf32 = 32 bytes along the 64-byte swizzled row
             const uint64_t dah = desc_sw64(st + ko), dal = desc_sw64(st + A_BYTES + ko);
             const uint64_t dwh = desc_sw64(st + 2 * A_BYTES + ko), dwl = desc_sw64(st + 2 * A_BYTES + B_BYTES + ko);
-            mma_tf32(d, dah, dwh, Cfg::IDESC, (kt | ks) ? 1u : 0u);
+            mma_tf32(d, dah, dwh, Cfg::IDESC, (kt != kb || ks) ? 1u : 0u);
             mma_tf32(d, dah, dwl, Cfg::IDESC, 1u);
             mma_tf32(d, dal, dwh, Cfg::IDESC, 1u);
           }

@@ -145,6 +145,24 @@ std::vector<int2> digit_kranges(const std::vector<int8_t>& dig, int S, int rows,
   return kr;
 }
 
+// per 64-row tile of a split operator (hi/lo planes [rows][cols], fp32 bit patterns): the K
+// elements [first, last + 1) holding a nonzero hi or lo value, rounded out to `gran`
+std::vector<int2> zero_kranges_f32(const std::vector<float>& hi, const std::vector<float>& lo, int rows, int cols,
+                                   int gran) {
+  std::vector<int2> kr(rows / 64);
+  for (int t = 0; t < rows / 64; ++t) {
+    int a = cols, b = 0;
+    for (int r = t * 64; r < (t + 1) * 64; ++r)
+      for (int c = 0; c < cols; ++c) {
+        const size_t i = (size_t)r * cols + c;
+        if (hi[i] != 0.0f || lo[i] != 0.0f) { a = std::min(a, c); b = std::max(b, c + 1); }
+      }
+    if (b <= a) { a = 0; b = gran; }
+    kr[t] = make_int2(a / gran * gran, (b + gran - 1) / gran * gran);
+  }
+  return kr;
+}
+
 // ---------------------------------------------------------------- host fp64 transfers
 // R (n_f/2 x n_f) applied to the rows of a column block: out = R * A  (A: n_f x cols)
 void host_restrict_rows(const std::vector<double>& A, int n_f, int cols, std::vector<double>& out) {
@@ -380,6 +398,7 @@ struct nmg_hierarchy {
   DevBuf<int2> wkr, wkrB;
   // 2D: A_l = B_l (x) C_l + alpha Q_l (x) Q_l; fp32 factors (SIMT), tf32 hi/lo (tcgen05)
   std::vector<std::unique_ptr<DevBuf<float>>> B32, C32, B32h, B32l, C32h, C32l, Q32;
+  std::vector<std::unique_ptr<DevBuf<int2>>> Bkr, Ckr;   // per level: nonzero K ranges of B_l, C_l
   std::vector<int> qhb;                                  // Q_l half-bandwidth
   std::vector<CUtensorMap> mBh, mBl, mCh, mCl, mTh, mTl;
   std::vector<CUtensorMap> mBh64, mBl64, mCh64, mCl64;
@@ -780,11 +799,13 @@ nmg_status apply2d(nmg_hierarchy* h, int l, int nrhs, const float* X, const floa
     NMG_TRY(make_map(&mx, X, (int64_t)M, n, tc_gemm_block_m()));
     KronArgs k{};
     k.M = M; k.n = n; k.mode = KRON_T; k.D = h->tth[l]->p;
+    k.krange = h->tune.dense_k ? nullptr : h->Ckr[l]->p;
     { Prof p(h, NMG_K_GEMM32, s); kron_tc(&mx, &h->mKCh[l], &h->mKCl[l], k, h->num_sms, s); }
     NMG_TRY(check_launch(h));
     KronArgs k2{};
     k2.M = M; k2.n = n; k2.mode = KRON_RESID; k2.D = D; k2.X = X; k2.Cin = Cin; k2.Q = h->Q32[l]->p;
     k2.hb = h->qhb[l]; k2.alpha = (float)h->d.alpha; k2.negate = negate;
+    k2.krange = h->tune.dense_k ? nullptr : h->Bkr[l]->p;
     { Prof p(h, NMG_K_GEMM32, s); kron_tc(&h->mTh[l], &h->mKBh[l], &h->mKBl[l], k2, h->num_sms, s); }
     return check_launch(h);
   }
@@ -966,6 +987,7 @@ nmg_status apply_slab(nmg_hierarchy* h, int l, int nrhs, const float* X, const f
   KronArgs k{};
   k.M = nrhs * (R + 2 * H); k.n = n; k.mode = KRON_T; k.D = h->tsend.p;
   k.R = R; k.H = H; k.r0 = h->rank * R; k.img = slab_img(h, l);
+  k.krange = h->tune.dense_k ? nullptr : h->Ckr[l]->p;
   { Prof p(h, NMG_K_GEMM32, s); kron_tc(&mx, &h->mKCh[l], &h->mKCl[l], k, h->num_sms, s); }
   NMG_TRY(check_launch(h));
   NMG_TRY(h->comm->all_gather(h->tsend.p, h->trecv.p, sizeof(float) * (size_t)nrhs * n * R, s));
@@ -974,6 +996,7 @@ nmg_status apply_slab(nmg_hierarchy* h, int l, int nrhs, const float* X, const f
   k2.M = nrhs * n; k2.n = n; k2.mode = KRON_RESID; k2.D = D; k2.X = X; k2.Cin = Cin; k2.Q = h->Q32[l]->p;
   k2.hb = h->qhb[l]; k2.alpha = (float)h->d.alpha; k2.negate = negate;
   k2.R = R; k2.H = H; k2.r0 = h->rank * R; k2.img = slab_img(h, l);
+  k2.krange = (h->tune.dense_k || (h->rank * R) % 64) ? nullptr : h->Bkr[l]->p;
   { Prof p(h, NMG_K_GEMM32, s); kron_tc(&h->mTh[l], &h->mKBhS[l], &h->mKBlS[l], k2, h->num_sms, s); }
   return check_launch(h);
 }
@@ -1625,9 +1648,17 @@ nmg_status nmg_create_hierarchy(const nmg_problem_desc* desc, const double* fact
       split_host(B, hi, lo);
       NMG_TRY(up(h->B32h, hi.data()));
       NMG_TRY(up(h->B32l, lo.data()));
+      auto kr_up = [&](std::vector<std::unique_ptr<DevBuf<int2>>>& v) -> nmg_status {
+        v.emplace_back(new DevBuf<int2>());
+        if (nl % 64) return NMG_OK;
+        const std::vector<int2> kr = zero_kranges_f32(hi, lo, nl, nl, 16);
+        return v.back()->upload(kr.data(), kr.size());
+      };
+      NMG_TRY(kr_up(h->Bkr));
       split_host(C, hi, lo);
       NMG_TRY(up(h->C32h, hi.data()));
       NMG_TRY(up(h->C32l, lo.data()));
+      NMG_TRY(kr_up(h->Ckr));
       int hb = 0;
       for (int i = 0; i < nl; ++i)
         for (int j = 0; j < nl; ++j)
