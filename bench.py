@@ -143,12 +143,30 @@ def algorithmic_counts(cfg, B):
             "gemm64_bytes": 8.0 * (n[0] * n[0] + 3 * B * n[0])}
 
 
+def fno_flops(cfg, B):
+    """FNO smoother FLOPs per step (Appendix A / Table 6 arch per level): per Fourier layer the
+    W-convolution 2 c^2 ks^d per point and the complex mode mixing 8 c^2 per kept mode (k in 1D,
+    2k x k in 2D); lift and projection 2c per point each.  The FFTs of the kept modes are not
+    counted."""
+    tot = 0.0
+    for l in range(cfg.levels - 1):
+        n = cfg.n >> l
+        c, L, k, ks = ni.fno_arch(cfg.dim, n)
+        pts = n ** cfg.dim
+        modes = k if cfg.dim == 1 else 2 * k * k
+        tot += (cfg.nu1 + cfg.nu2) * B * (L * (2.0 * c * c * ks ** cfg.dim * pts + 8.0 * c * c * modes) + 4.0 * c * pts)
+    return tot
+
+
 # ------------------------------------------------------------------ oracle timing
-def oracle_rate(cfg, factors, weights, y, nrhs, cycles):
+def oracle_rate(cfg, factors, weights, y, nrhs, cycles, fno=False):
     from oracle import nmg_oracle as O
     H = O.build_hierarchy(cfg.dim, factors, cfg.alpha, cfg.levels, nu1=cfg.nu1, nu2=cfg.nu2)
     for l, w in enumerate(weights):
-        O.load_weights(H, l + 1, ni.unflatten_params(cfg, w))
+        if fno:
+            O.load_weights(H, l + 1, O.fno_params(cfg.dim, *ni.fno_arch(cfg.dim, cfg.n >> l), w))
+        else:
+            O.load_weights(H, l + 1, ni.unflatten_params(cfg, w))
     ys = y[:nrhs]
     x = np.zeros_like(ys)
     t0 = time.perf_counter()
@@ -202,6 +220,9 @@ def main():
     ap.add_argument("--tune", default="", help="extra nmg_tuning fields, e.g. no_fused_coarse=1,no_graphs=1")
     ap.add_argument("--precision", choices=["auto", "mixed", "fp64"], default="auto",
                     help="auto: fp64 cycle for config 0 (BASELINE's fp64 system), mixed otherwise")
+    ap.add_argument("--smoother", choices=["cnn", "fno"], default="cnn",
+                    help="cnn: BASELINE's CNN smoothers (the headline); fno: the paper's FNO smoothers "
+                         "(Table 6 hyperparameters per level, W_seed; fp32 SIMT kernels, SURVEY NEXT-2)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--slab", choices=["auto", "on", "off"], default="auto",
@@ -220,12 +241,15 @@ def main():
         cfg = cfg.replace(alpha=args.alpha)
     if args.nrhs:
         cfg = cfg.replace(nrhs=args.nrhs)
+    fno = args.smoother == "fno"
     if args.steps is None:
-        args.steps = {0: 5000, 1: 400, 2: 60, 3: 5, 4: 30}[cid]   # >= ~0.5 s timed (clock samples)
+        args.steps = ({0: 500, 1: 10, 2: 3, 3: 1, 4: 2} if fno else
+                      {0: 5000, 1: 400, 2: 60, 3: 5, 4: 30})[cid]   # >= ~0.5 s timed (clock samples)
     B = cfg.nrhs
     pool = cfg.dim == 2 and B > 8     # 2D: 8 seeded RHS tiled to the batch (throughput is value-independent)
     workload = (f"{cfg.name}_{cfg.dim}d_n{cfg.n}_L{cfg.levels}_rhs{B}"
-                f"{'_per_gpu' if cid == 0 else '_total'}_alpha{cfg.alpha:g}_C{cfg.channels}_Wseed")
+                f"{'_per_gpu' if cid == 0 else '_total'}_alpha{cfg.alpha:g}_"
+                f"{'FNO' if fno else 'C%d' % cfg.channels}_Wseed")
 
     def make_y(nrhs, start):
         if not pool:
@@ -237,16 +261,16 @@ def main():
         if rank != 0:
             return
         factors = ni.operator_factors(cfg)
-        W = ni.weights_seed(cfg)
+        W = ni.fno_weights_seed(cfg, seed=3) if fno else ni.weights_seed(cfg)
         # bounded sample per step (every --steps / --warmup step runs): 1D 16 RHS x 1 cycle,
         # 2D 1 RHS x 1 cycle (cfg 3: ~3 s per step on 16 host threads)
         ns = 16 if cfg.dim == 1 else 1
         y, _ = ni.make_rhs(cfg, factors, cfg.alpha, nrhs=ns)
         secs = 0.0
         for _ in range(args.warmup):
-            oracle_rate(cfg, factors, W, y, ns, 1)
+            oracle_rate(cfg, factors, W, y, ns, 1, fno)
         for _ in range(args.steps):
-            _, dt = oracle_rate(cfg, factors, W, y, ns, 1)
+            _, dt = oracle_rate(cfg, factors, W, y, ns, 1, fno)
             secs += dt
         v = args.steps * ns / secs
         sample = f"{ns} RHS x 1 cycle per step of the {cfg.name} workload"
@@ -303,15 +327,18 @@ def main():
         start, _ = weak_shard(B, rank)
         global_B = world * B
     factors = ni.operator_factors(cfg)
-    W = ni.weights_seed(cfg)
+    W = ni.fno_weights_seed(cfg, seed=3) if fno else ni.weights_seed(cfg)
     if B == 0:
         raise SystemExit(f"rank {rank}: no RHS left for this rank ({cfg.nrhs} RHS over {world} ranks)")
-    prec = nmg.PREC_FP64 if args.precision == "fp64" or (args.precision == "auto" and cid == 0) else nmg.PREC_MIXED
+    prec = nmg.PREC_FP64 if args.precision == "fp64" or (args.precision == "auto" and cid == 0 and not fno) else nmg.PREC_MIXED
     h = nmg.Hierarchy(cfg.dim, cfg.n, cfg.levels, cfg.alpha, factors, nu1=cfg.nu1, nu2=cfg.nu2, max_rhs=B,
                       device=local, comm=comm, precision=prec,
                       tuning={"lanes": args.lanes, **{k: int(v) for k, v in (kv.split("=") for kv in args.tune.split(",") if kv)}})
     for l, w in enumerate(W):
-        h.load_weights(l + 1, ni.cnn_arch(cfg), w)
+        if fno:
+            h.load_fno_weights(l + 1, ni.fno_arch(cfg.dim, cfg.n >> l), w)
+        else:
+            h.load_weights(l + 1, ni.cnn_arch(cfg), w)
     y_np = make_y(B, start)
     if slab:
         y_np = np.ascontiguousarray(split_slabs(y_np, cfg.n, world)[rank])
@@ -354,6 +381,8 @@ def main():
     prof = h.profile_query()
     tot_prof = sum(v[0] for v in prof.values())
     counts = algorithmic_counts(cfg, B)
+    if fno:
+        counts["smooth"] = fno_flops(cfg, B)
     pk = peaks()
     clocks = clk.summary()
     # the burst figure for a kernel timed alone, the sustained one for a kernel inside a long
@@ -372,7 +401,16 @@ def main():
     except Exception:
         pass
     f16x3_peak = bf16 / 3.0      # f16 dense = bf16 dense rate; 3 products per fp32-accurate MAC
-    if dom == "gemm64":
+    if fno and dom == "smooth":
+        # FNO smoother kernels are fp32 SIMT (fno.cu): reported against the FP32 FFMA rate
+        peak = 148 * 128 * 2 * 1.965e9 / 1e12
+        achieved = counts["smooth"] / (step_ms * 1e-3) / 1e12
+        roof = {"kernel": "fno_* (lift, row/column mode FFTs, mode mixing, W-conv + bias + GELU, projection; fp32 "
+                          "SIMT), all launches of a step",
+                "bound": "alu", "unit": "TFLOP/s",
+                "peak_note": "FP32 FFMA peak from unit counts and clock (DESIGN.md §6); FNO FLOPs = per layer "
+                             "2 c^2 ks^d per point (W-conv) + 8 c^2 per kept mode (mixing), lift and projection 2c"}
+    elif dom == "gemm64":
         peak = bf16 * FP64_NOMINAL_RATIO
         achieved = counts["gemm64"] / (step_ms * 1e-3) / 1e12
         roof = {"kernel": "fp64 outer residual (Ozaki int8 tcgen05 / DMMA)", "bound": "tensor", "unit": "TFLOP/s",
@@ -470,7 +508,7 @@ def main():
     # (trainer/nmg_train.py, Alg 5) for this config and alpha when present, else (1D) the W_lin
     # stand-in at the largest alpha of the sweep where it converges
     solve = None
-    if not args.no_solve:
+    if not args.no_solve and not fno:      # no trained FNO weights exist
         wt = ni.weights_trained(cfg)
         scfg, label = cfg, "W_train (level-wise trainer, Alg 5)"
         if wt is None:            # the config's trained set at another alpha of the curriculum
@@ -511,7 +549,9 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         nr, nc = {0: (8, 200), 1: (128, 8), 2: (4, 2), 3: (1, 1), 4: (1, 1)}[cid]
-        rate, dt = oracle_rate(cfg, factors, W, y_np, nr, nc)
+        if fno:
+            nr, nc = {0: (8, 20), 1: (16, 1), 2: (1, 1), 3: (1, 1), 4: (1, 1)}[cid]
+        rate, dt = oracle_rate(cfg, factors, W, y_np, nr, nc, fno)
         cpu = {"value": rate, "unit": "RHS*cycles/s", "cores": host_threads(), "kind": "oracle",
                "sample": f"{nr} RHS x {nc} cycles of the same workload ({dt:.1f} s)", **host_info()}
 
@@ -520,10 +560,13 @@ def main():
                 "value": value, "unit": "RHS*cycles/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "strong" if strong else "weak", "vs_baseline": None,
-                "dtype": ("f64 (NMG_PREC_FP64 fused cycle; the CNN's own arithmetic fp32)" if prec == nmg.PREC_FP64 else
+                "dtype": ("f64 outer residual (Ozaki int8 tcgen05) + fp32 inner cycle (fp32 SIMT FNO smoothers, "
+                          "tcgen05 operator applies)" if fno else
+                          "f64 (NMG_PREC_FP64 fused cycle; the CNN's own arithmetic fp32)" if prec == nmg.PREC_FP64 else
                           "f64 outer residual (Ozaki int8 tcgen05) + fp32-accurate inner cycle (FP16x3 tcgen05 "
                           + ("CNN and operator applies)" if cfg.dim == 1 else "CNN, 3xTF32 tcgen05 Kronecker applies)")),
-                "data": "synthetic (seeded RHS; W_seed Kaiming-uniform weights)",
+                "data": ("synthetic (seeded RHS; W_seed FNO weights, Table 6 arch per level)" if fno else
+                         "synthetic (seeded RHS; W_seed Kaiming-uniform weights)"),
                 "config": {"workload": workload, "global_batch": global_B, "n": cfg.n, "levels": cfg.levels,
                            "rhs": "8-RHS seeded pool tiled to the batch" if pool else "seeded, distinct",
                            "alpha": cfg.alpha, "nu1": cfg.nu1, "nu2": cfg.nu2,

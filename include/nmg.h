@@ -103,6 +103,8 @@ typedef struct {
   int32_t no_balance;     /* 1: load the CNN weights as given instead of lifting hidden channels
                              whose activation bound lies > 2^4 below their layer's largest by a
                              power of two (an exactly equivalent network, see nmg_api.cu)    */
+  int32_t simt_fno;       /* 1: FNO W-convolution on the fp32 SIMT kernels instead of the tcgen05
+                             3xTF32 implicit GEMM (fno_tc.cu)                                  */
 } nmg_tuning;
 
 /* Problem descriptor (SPEC ProblemSpec analogue). */

@@ -41,7 +41,7 @@ class Tuning(C.Structure):
                 ("fp64_dmma", C.c_int32), ("simt_gemm", C.c_int32), ("ffma_cnn", C.c_int32),
                 ("no_kron", C.c_int32), ("host_chunks", C.c_int32), ("fused_coarse", C.c_int32),
                 ("no_compaction", C.c_int32), ("dense_k", C.c_int32),
-                ("no_balance", C.c_int32)]
+                ("no_balance", C.c_int32), ("simt_fno", C.c_int32)]
 
 
 class ProblemDesc(C.Structure):

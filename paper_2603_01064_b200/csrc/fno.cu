@@ -8,6 +8,9 @@
 //   per layer      spectral forward (row FFTs in shared memory, fft.cuh; 2D: rows then columns)
 //                  -> Zh [b][mode][c] (complex) -> mode mixing Yh = Zh R -> inverse (Hermitian
 //                  completion, real output) into Z1 -> Z1 = GELU(Z1 + B + W * Z0) -> swap
+//                  (the W convolution: fno_conv_tc, 3xTF32 implicit GEMM on tcgen05 over channels-last
+//                  tf32 hi/lo copies of the layer input, fno_tc.cu; the fp32 SIMT fno_conv1d/2d
+//                  kernels below serve the shapes it does not take: c % 16 != 0, 1D n < 128, 2D n < 16)
 //   fno_proj       h = proj(Z) -> 1D: x (+)= ||b|| F'_l(h) (fused level filter); 2D: the level
 //                  filter's input buffer (zput), filter2d finishes.
 #include <algorithm>
@@ -347,10 +350,20 @@ void fno_forward(const FnoArgs& a, cudaStream_t s) {
   const int modes = a.dim == 1 ? k : 2 * k * k;
   fno_lift_kernel<<<nblk((int64_t)a.nrhs * c * N, NT), NT, 0, s>>>(a.nrhs, c, N, a.in, a.norms, a.lift_w, a.lift_b,
                                                                   a.Z0);
+  const bool tc = a.tXh[0] != nullptr;
+  FnoConvArgs ca{};
+  if (tc) {
+    fno_lift_cl(a.nrhs, c, N, a.in, a.norms, a.lift_w, a.lift_b, a.Xh[0], a.Xl[0], s);
+    int bx, by;
+    fno_tc_box(n, &bx, &by);
+    ca.dim = a.dim; ca.n = n; ca.c = c; ca.ks = ks; ca.nrhs = a.nrhs;
+    ca.lbx = 31 - __builtin_clz((unsigned)bx);
+  }
   const int R = std::max(1, 4096 / n);
   const size_t smr = sizeof(float2) * (size_t)R * n;
   const size_t smc = fno_conv_smem(a.dim, c, ks);
-  if (a.dim == 1) NMG_SMEM_OPTIN(fno_conv1d_kernel, fno_conv_smem(1, 64, 7));
+  if (tc) {}
+  else if (a.dim == 1) NMG_SMEM_OPTIN(fno_conv1d_kernel, fno_conv_smem(1, 64, 7));
   else NMG_SMEM_OPTIN(fno_conv2d_kernel, fno_conv_smem(2, 64, 7));
   float* Z0 = a.Z0;
   float* Z1 = a.Z1;
@@ -362,7 +375,14 @@ void fno_forward(const FnoArgs& a, cudaStream_t s) {
       fno_mix_kernel<<<dim3(modes, ceil_div(a.nrhs, 16)), NT, 0, s>>>(a.nrhs, modes, c, a.Zh, ly.R, a.Yh);
       fno_rows_inv_kernel<<<nblk(rows, R), NT, smr, s>>>(n, rows, k, a.Yh, c, (int64_t)k * c, c, 1, 1.0f / (float)n,
                                                          Z1, a.tw, a.tw_n);
-      fno_conv1d_kernel<<<dim3(ceil_div(n, CT1), a.nrhs), NT, smc, s>>>(n, c, ks, Z0, ly.W, ly.B, Z1);
+      if (tc) {
+        ca.bias = ly.B; ca.Z1 = Z1;
+        ca.Xh_out = l + 1 < a.L ? a.Xh[(l + 1) & 1] : nullptr;
+        ca.Xl_out = l + 1 < a.L ? a.Xl[(l + 1) & 1] : nullptr;
+        fno_conv_tc(a.tXh[l & 1], a.tXl[l & 1], ly.tWh, ly.tWl, ca, s);
+      } else {
+        fno_conv1d_kernel<<<dim3(ceil_div(n, CT1), a.nrhs), NT, smc, s>>>(n, c, ks, Z0, ly.W, ly.B, Z1);
+      }
     } else {
       const int64_t rows = (int64_t)a.nrhs * c * n;
       const int64_t per = (int64_t)c * n;
@@ -375,8 +395,15 @@ void fno_forward(const FnoArgs& a, cudaStream_t s) {
       fno_cols_inv_kernel<<<dim3(k / G, c, a.nrhs), NT, smg, s>>>(n, k, c, G, a.Yh, a.T, a.tw, a.tw_n);
       fno_rows_inv_kernel<<<nblk(rows, R), NT, smr, s>>>(n, rows, k, a.T, per, per * k, 1, k,
                                                          1.0f / ((float)n * (float)n), Z1, a.tw, a.tw_n);
-      fno_conv2d_kernel<<<dim3(ceil_div(n, CT2) * ceil_div(n, CT2), a.nrhs), NT, smc, s>>>(n, c, ks, Z0, ly.W, ly.B,
-                                                                                           Z1);
+      if (tc) {
+        ca.bias = ly.B; ca.Z1 = Z1;
+        ca.Xh_out = l + 1 < a.L ? a.Xh[(l + 1) & 1] : nullptr;
+        ca.Xl_out = l + 1 < a.L ? a.Xl[(l + 1) & 1] : nullptr;
+        fno_conv_tc(a.tXh[l & 1], a.tXl[l & 1], ly.tWh, ly.tWl, ca, s);
+      } else {
+        fno_conv2d_kernel<<<dim3(ceil_div(n, CT2) * ceil_div(n, CT2), a.nrhs), NT, smc, s>>>(n, c, ks, Z0, ly.W,
+                                                                                             ly.B, Z1);
+      }
     }
     std::swap(Z0, Z1);
   }
@@ -389,6 +416,6 @@ void fno_forward(const FnoArgs& a, cudaStream_t s) {
   }
 }
 
-int fno_launches(int dim, int L) { return 1 + L * (dim == 1 ? 4 : 6) + 1; }
+int fno_launches(int dim, int L, bool tc) { return 1 + (tc ? 1 : 0) + L * (dim == 1 ? 4 : 6) + 1; }
 
 }  // namespace nmg

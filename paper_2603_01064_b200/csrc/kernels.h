@@ -286,7 +286,24 @@ struct FnoLayer {
   const float2* R;            // spectral weights [modes][c_in][c_out] complex
   const float* W;             // W convolution [c_out][c_in][ks](x ks)
   const float* B;             // bias [c]
+  // tensor-core W-convolution (fno_tc.cu): W as [o][tap][c] tf32 hi/lo, box {16, 64}
+  const CUtensorMap* tWh = nullptr;
+  const CUtensorMap* tWl = nullptr;
 };
+// W-convolution + bias + GELU on tcgen05 (3xTF32 implicit GEMM, fno_tc.cu)
+struct FnoConvArgs {
+  int dim, n, c, ks, nrhs;
+  int lbx;                    // 2D: log2 of the output box width bx (box bx x 128 / bx pixels)
+  const float* bias;          // [c]
+  float* Z1;                  // [nrhs][c][N]: the spectral branch on entry, the layer output on exit
+  float* Xh_out; float* Xl_out;   // next layer's channels-last tf32 hi/lo input [nrhs][N][c] (null: last layer)
+};
+bool fno_tc_ok(int dim, int n, int c);
+void fno_tc_box(int n, int* bx, int* by);
+void fno_lift_cl(int nrhs, int c, int64_t N, const float* in, const double* norms, const float* lw, const float* lb,
+                 float* Xh, float* Xl, cudaStream_t s);
+void fno_conv_tc(const CUtensorMap* xh, const CUtensorMap* xl, const CUtensorMap* wh, const CUtensorMap* wl,
+                 const FnoConvArgs& a, cudaStream_t s);
 struct FnoArgs {
   int dim, n, nrhs, c, L, k, ks;
   const float* in;            // b [nrhs][N]
@@ -304,9 +321,15 @@ struct FnoArgs {
   // else x (+)= ||b|| h
   float* x; bool accumulate, filter;
   float2* Zf = nullptr; int zb0 = 0;
+  // tensor-core W-convolution: channels-last tf32 hi/lo layer inputs (ping-pong pairs) and their
+  // tensor maps; null tX: the fp32 SIMT convolution kernels
+  const CUtensorMap* tXh[2] = {nullptr, nullptr};
+  const CUtensorMap* tXl[2] = {nullptr, nullptr};
+  float* Xh[2] = {nullptr, nullptr};
+  float* Xl[2] = {nullptr, nullptr};
 };
 void fno_forward(const FnoArgs& a, cudaStream_t s);
-int fno_launches(int dim, int L);
+int fno_launches(int dim, int L, bool tc);
 size_t fno_conv_smem(int dim, int c, int ks);
 
 // ---- NMG_PREC_FP64: the whole cycle of one RHS per CTA in one launch (cycle64.cu; 1D, n <= 1024)

@@ -349,6 +349,33 @@ nmg_status make_a2_map(CUtensorMap* m, const uint16_t* p, int n, int C, int64_t 
   return NMG_OK;
 }
 
+// FNO layer input, channels-last fp32 (tf32 hi or lo plane): 1D [rhs][n][c] as {c, x, rhs} with box
+// {16, 128, 1}; 2D [rhs][n][n][c] as {c, x, y, rhs} with box {16, bx, by, 1}; SWIZZLE_64B.  Points
+// outside the image (tap shifts) are zero-filled: the convolution's "same" padding.
+nmg_status make_fno_x_map(CUtensorMap* m, const float* p, int dim, int n, int c, int64_t nrhs, int bx, int by) {
+  NMG_TRY(get_encoder());
+  CUresult r;
+  if (dim == 1) {
+    cuuint64_t dims[3] = {(cuuint64_t)c, (cuuint64_t)n, (cuuint64_t)nrhs};
+    cuuint64_t strides[2] = {(cuuint64_t)c * 4u, (cuuint64_t)n * c * 4u};
+    cuuint32_t box[3] = {16u, 128u, 1u};
+    cuuint32_t es[3] = {1u, 1u, 1u};
+    r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)p, dims, strides, box, es,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    cuuint64_t dims[4] = {(cuuint64_t)c, (cuuint64_t)n, (cuuint64_t)n, (cuuint64_t)nrhs};
+    cuuint64_t strides[3] = {(cuuint64_t)c * 4u, (cuuint64_t)n * c * 4u, (cuuint64_t)n * n * c * 4u};
+    cuuint32_t box[4] = {16u, (cuuint32_t)bx, (cuuint32_t)by, 1u};
+    cuuint32_t es[4] = {1u, 1u, 1u, 1u};
+    r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)p, dims, strides, box, es,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  if (r != CUDA_SUCCESS) return fail(NMG_ERR_CUDA, "cuTensorMapEncodeTiled (FNO input, %dD) failed (%d)", dim, (int)r);
+  return NMG_OK;
+}
+
 }  // namespace
 
 // ======================================================================= handle
@@ -427,9 +454,16 @@ struct nmg_hierarchy {
   bool coarse_inv = true;
   int nc = 0;
   // FNO smoothers (nmg_load_fno_weights): per level arch + device parameters; shared workspaces
-  struct FnoLevel { nmg_fno_arch arch{}; DevBuf<float> p; float proj_b = 0.f; };
+  struct FnoLevel {
+    nmg_fno_arch arch{}; DevBuf<float> p; float proj_b = 0.f;
+    // tensor-core W-convolution (fno_tc.cu): W as [layer][o][tap][c] tf32 hi/lo + one map per layer
+    bool tc = false;
+    DevBuf<float> w2h, w2l;
+    std::vector<CUtensorMap> mWh, mWl;
+  };
   std::vector<std::unique_ptr<FnoLevel>> fno;            // null = the level has a CNN
   DevBuf<float> fz0, fz1;
+  DevBuf<float> fXh[2], fXl[2];                          // channels-last tf32 hi/lo layer inputs (ping-pong)
   DevBuf<float2> fT, fZh, fYh;
   int fno_chunk = 0;
   // smoother weights per level
@@ -588,6 +622,18 @@ nmg_status run_fno(nmg_hierarchy* h, int l, int nrhs, const float* b, float* x, 
     a.layer[i].R = reinterpret_cast<const float2*>(P + off); off += spec;
     a.layer[i].W = P + off; off += conv;
     a.layer[i].B = P + off; off += c;
+    if (F.tc) { a.layer[i].tWh = &F.mWh[i]; a.layer[i].tWl = &F.mWl[i]; }
+  }
+  CUtensorMap mXh[2], mXl[2];
+  if (F.tc) {
+    int bx, by;
+    fno_tc_box(n, &bx, &by);
+    for (int q = 0; q < 2; ++q) {
+      NMG_TRY(make_fno_x_map(&mXh[q], h->fXh[q].p, dim, n, c, h->fno_chunk, bx, by));
+      NMG_TRY(make_fno_x_map(&mXl[q], h->fXl[q].p, dim, n, c, h->fno_chunk, bx, by));
+      a.tXh[q] = &mXh[q]; a.tXl[q] = &mXl[q];
+      a.Xh[q] = h->fXh[q].p; a.Xl[q] = h->fXl[q].p;
+    }
   }
   a.proj_w = P + off;
   a.proj_b = F.proj_b;
@@ -604,7 +650,7 @@ nmg_status run_fno(nmg_hierarchy* h, int l, int nrhs, const float* b, float* x, 
     a.x = x + (int64_t)r0 * N;
     a.Zf = zf ? h->Z.p : nullptr;
     a.zb0 = r0;
-    { Prof p(h, NMG_K_SMOOTH, s, fno_launches(dim, ar.n_layers)); fno_forward(a, s); }
+    { Prof p(h, NMG_K_SMOOTH, s, fno_launches(dim, ar.n_layers, F.tc)); fno_forward(a, s); }
     NMG_TRY(check_launch(h));
   }
   if (zf) {
@@ -2266,11 +2312,38 @@ nmg_status nmg_load_fno_weights(nmg_hierarchy* h, int32_t level, const nmg_fno_a
   F->arch = *arch;
   F->proj_b = params[n_params - 1];
   NMG_TRY(F->p.upload(params, n_params));
+  F->tc = !h->tune.simt_fno && fno_tc_ok(dim, n, c);
+  if (F->tc) {
+    // W [o][c][tap] -> [layer][o][tap][c], tf32 hi/lo (K index of the implicit GEMM = tap * c + channel)
+    const int taps = dim == 1 ? ks : ks * ks;
+    std::vector<float> wh((size_t)L * conv), wl((size_t)L * conv);
+    for (int i = 0; i < L; ++i) {
+      const float* Wi = params + 2 * (size_t)c + i * (spec + conv + c) + spec;
+      for (int o = 0; o < c; ++o)
+        for (int ch = 0; ch < c; ++ch)
+          for (int t = 0; t < taps; ++t) {
+            const float w = Wi[((size_t)o * c + ch) * taps + t];
+            const size_t at = (size_t)i * conv + ((size_t)o * taps + t) * c + ch;
+            wh[at] = tf32_rna(w);
+            wl[at] = tf32_rna(w - wh[at]);
+          }
+    }
+    NMG_TRY(F->w2h.upload(wh.data(), wh.size()));
+    NMG_TRY(F->w2l.upload(wl.data(), wl.size()));
+    F->mWh.resize(L);
+    F->mWl.resize(L);
+    for (int i = 0; i < L; ++i) {
+      NMG_TRY(make_map(&F->mWh[i], F->w2h.p + (size_t)i * conv, c, (int64_t)taps * c, 64));
+      NMG_TRY(make_map(&F->mWl[i], F->w2l.p + (size_t)i * conv, c, (int64_t)taps * c, 64));
+    }
+  }
   h->fno[level - 1] = std::move(F);
   // workspaces for the largest FNO level: RHS chunks with <= 2 GiB of activations per buffer
   int64_t per = 0, tper = 0, hper = 0;
+  bool any_tc = false;
   for (int l = 0; l < h->L - 1; ++l) {
     if (!h->fno[l]) continue;
+    any_tc = any_tc || h->fno[l]->tc;
     const nmg_fno_arch& a = h->fno[l]->arch;
     per = std::max<int64_t>(per, (int64_t)a.width * h->N[l]);
     if (dim == 2) tper = std::max<int64_t>(tper, (int64_t)a.width * h->n[l] * a.modes);
@@ -2279,8 +2352,13 @@ nmg_status nmg_load_fno_weights(nmg_hierarchy* h, int32_t level, const nmg_fno_a
   const int64_t B = h->d.max_rhs;
   const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(B, ((int64_t)1 << 29) / per));
   if (chunk != h->fno_chunk || (int64_t)h->fz0.n < chunk * per || (int64_t)h->fZh.n < chunk * hper ||
-      (int64_t)h->fT.n < chunk * tper) {
+      (int64_t)h->fT.n < chunk * tper || (any_tc && (int64_t)h->fXh[0].n < chunk * per)) {
     h->fno_chunk = chunk;
+    if (any_tc)
+      for (int q = 0; q < 2; ++q) {
+        NMG_TRY(h->fXh[q].alloc((size_t)chunk * per));
+        NMG_TRY(h->fXl[q].alloc((size_t)chunk * per));
+      }
     NMG_TRY(h->fz0.alloc((size_t)chunk * per));
     NMG_TRY(h->fz1.alloc((size_t)chunk * per));
     NMG_TRY(h->fZh.alloc((size_t)chunk * hper));

@@ -32,11 +32,12 @@ def rel_rows(a, b):
     return np.linalg.norm(a - b, axis=1) / np.linalg.norm(b, axis=1)
 
 
-def build(cfg, nrhs):
+def build(cfg, nrhs, simt=False):
     f = ni.operator_factors(cfg)
     Wf = ni.fno_weights_seed(cfg, seed=3)
     H = O.build_hierarchy(cfg.dim, f, cfg.alpha, cfg.levels, nu1=cfg.nu1, nu2=cfg.nu2)
-    h = nmg.Hierarchy(cfg.dim, cfg.n, cfg.levels, cfg.alpha, f, nu1=cfg.nu1, nu2=cfg.nu2, max_rhs=nrhs)
+    h = nmg.Hierarchy(cfg.dim, cfg.n, cfg.levels, cfg.alpha, f, nu1=cfg.nu1, nu2=cfg.nu2, max_rhs=nrhs,
+                      tuning={"simt_fno": 1} if simt else None)
     for l, w in enumerate(Wf):
         arch = ni.fno_arch(cfg.dim, cfg.n >> l)
         O.load_weights(H, l + 1, O.fno_params(cfg.dim, *arch, w))
@@ -44,10 +45,13 @@ def build(cfg, nrhs):
     return f, H, h
 
 
-@pytest.fixture(scope="module", params=["1d", "2d"])
+# default: the W-convolution on tcgen05 (3xTF32 implicit GEMM, fno_tc.cu); "-simt": the fp32 SIMT
+# convolution kernels (nmg_tuning.simt_fno), which also serve the shapes the tensor-core kernel
+# does not take
+@pytest.fixture(scope="module", params=["1d", "2d", "1d-simt", "2d-simt"])
 def setup(request):
-    cfg = C1 if request.param == "1d" else C2
-    return (cfg,) + build(cfg, 4)
+    cfg = C1 if request.param.startswith("1d") else C2
+    return (cfg,) + build(cfg, 4, simt=request.param.endswith("simt"))
 
 
 def test_fno_forward_per_level(setup):
@@ -94,6 +98,30 @@ def test_fno_cycle_history(setup):
     orc = O.solve(H, y, tol=1e-300, max_cycles=3, freeze=False)
     ok, err = history_close(rep["history"], orc.history)
     assert ok, err
+
+
+@pytest.mark.parametrize("dim,n,nrhs", [(1, 4096, 3), (1, 512, 5), (2, 256, 2), (2, 128, 3), (2, 16, 5)])
+def test_fno_forward_table6_sizes(dim, n, nrhs):
+    """Raw FNO output at the BASELINE level sizes (Table 6 rows: ks = 7 / 5 / 3, k up to 128; the
+    tensor-core convolution's 1D tiles and 2D boxes 128 x 1, 128 x 1, 16 x 8 with several tiles per
+    image and tap shifts crossing the image border), per RHS against the oracle."""
+    base = ni.CONFIGS[1] if dim == 1 else ni.CONFIGS[2]
+    levels = max(2, int(np.log2(n // (256 if dim == 1 else 16))) + 1)   # coarsest system <= 256 unknowns
+    cfg = base.replace(n=n, levels=levels, nrhs=nrhs)
+    f = ni.operator_factors(cfg)
+    arch = ni.fno_arch(dim, n)
+    w = ni.fno_weights_seed(cfg, seed=5)[0]
+    h = nmg.Hierarchy(dim, n, levels, cfg.alpha, f, max_rhs=nrhs)
+    h.load_fno_weights(1, arch, w)
+    rng = np.random.default_rng(11)
+    shape = (nrhs,) + (n,) * dim
+    u = rng.standard_normal(shape)
+    u /= np.sqrt((u.reshape(nrhs, -1) ** 2).sum(1)).reshape((nrhs,) + (1,) * dim)
+    out = torch.zeros(shape, device=DEV)
+    h.debug_op(1, nmg.OP_CNN, T(u), out)
+    want = O.fno_forward(O.fno_params(dim, *arch, w), u)
+    assert rel_rows(out.cpu().numpy(), want).max() < 1e-5
+    h.close()
 
 
 def test_fno_replaced_by_cnn_and_back():
