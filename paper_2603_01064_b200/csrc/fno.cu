@@ -50,18 +50,33 @@ __global__ void __launch_bounds__(NT) fno_rows_fwd_kernel(int n, int64_t rows, i
                                                           float2* __restrict__ out, int64_t per, int64_t ostride_b,
                                                           int64_t ostride_m, int64_t ostride_r,
                                                           const float2* __restrict__ tw, int tw_n) {
+  // real rows 2q and 2q + 1 travel as one complex row z = x_a + i x_b (half the FFT work); the kept
+  // modes are unmixed by the Hermitian symmetry of real rows: X_a[m] = (Z[m] + conj Z[n-m]) / 2,
+  // X_b[m] = (Z[m] - conj Z[n-m]) / 2i
   extern __shared__ __align__(16) float2 cb[];
-  const int R = max(1, 4096 / n);
-  const int64_t r0 = (int64_t)blockIdx.x * R;
-  const int cnt = (int)min((int64_t)R, rows - r0);
+  const int R = max(1, 4096 / n);                      // complex rows per CTA
+  const int64_t r0 = (int64_t)blockIdx.x * 2 * R;      // first real row
+  const int cnt = (int)min((int64_t)2 * R, rows - r0);
+  const int cntc = (cnt + 1) >> 1;
   const int log2n = 31 - __clz(n);
-  for (int i = threadIdx.x; i < cnt * n; i += NT) cb[i] = make_float2(Z[r0 * n + i], 0.f);
+  for (int i = threadIdx.x; i < cntc * n; i += NT) {
+    const int q = i >> log2n, p = i & (n - 1);
+    const float* za = Z + (r0 + 2 * q) * n + p;
+    cb[i] = make_float2(za[0], 2 * q + 1 < cnt ? za[n] : 0.f);
+  }
   __syncthreads();
-  fft_dif_forward_batch(cb, n, cnt, n, 1, tw, tw_n, threadIdx.x, NT);
-  for (int i = threadIdx.x; i < cnt * k; i += NT) {
-    const int r = i / k, m = i - r * k;
-    const int64_t rr = r0 + r;
-    out[(rr / per) * ostride_b + m * ostride_m + (rr % per) * ostride_r] = cb[r * n + bitrev(m, log2n)];
+  fft_dif_forward_batch(cb, n, cntc, n, 1, tw, tw_n, threadIdx.x, NT);
+  for (int i = threadIdx.x; i < cntc * k; i += NT) {
+    const int q = i / k, m = i - q * k;
+    const float2 A = cb[q * n + bitrev(m, log2n)], B = cb[q * n + bitrev((n - m) & (n - 1), log2n)];
+    const int64_t ra = r0 + 2 * q;
+    out[(ra / per) * ostride_b + m * ostride_m + (ra % per) * ostride_r] =
+        make_float2(0.5f * (A.x + B.x), 0.5f * (A.y - B.y));
+    if (2 * q + 1 < cnt) {
+      const int64_t rb = ra + 1;
+      out[(rb / per) * ostride_b + m * ostride_m + (rb % per) * ostride_r] =
+          make_float2(0.5f * (A.y + B.y), -0.5f * (A.x - B.x));
+    }
   }
 }
 
@@ -146,27 +161,37 @@ __global__ void __launch_bounds__(NT) fno_rows_inv_kernel(int n, int64_t rows, i
                                                           int64_t per, int64_t istride_b, int64_t istride_m,
                                                           int64_t istride_r, float scale, float* __restrict__ Z,
                                                           const float2* __restrict__ tw, int tw_n) {
+  // real rows 2q and 2q + 1 as one complex inverse transform of W = Y_a + i Y_b (both Hermitian
+  // completed): W[m] = Y_a[m] + i Y_b[m], W[n-m] = conj Y_a[m] + i conj Y_b[m]; y_a = Re, y_b = Im
   extern __shared__ __align__(16) float2 cb[];
-  const int R = max(1, 4096 / n);
-  const int64_t r0 = (int64_t)blockIdx.x * R;
-  const int cnt = (int)min((int64_t)R, rows - r0);
+  const int R = max(1, 4096 / n);                      // complex rows per CTA
+  const int64_t r0 = (int64_t)blockIdx.x * 2 * R;      // first real row
+  const int cnt = (int)min((int64_t)2 * R, rows - r0);
+  const int cntc = (cnt + 1) >> 1;
   const int log2n = 31 - __clz(n);
-  for (int i = threadIdx.x; i < cnt * n; i += NT) cb[i] = make_float2(0.f, 0.f);
+  for (int i = threadIdx.x; i < cntc * n; i += NT) cb[i] = make_float2(0.f, 0.f);
   __syncthreads();
-  for (int i = threadIdx.x; i < cnt * k; i += NT) {
-    const int r = i / k, m = i - r * k;
-    const int64_t rr = r0 + r;
-    float2 X = in[(rr / per) * istride_b + m * istride_m + (rr % per) * istride_r];
+  for (int i = threadIdx.x; i < cntc * k; i += NT) {
+    const int q = i / k, m = i - q * k;
+    const int64_t ra = r0 + 2 * q, rb = ra + 1;
+    const float2 A = in[(ra / per) * istride_b + m * istride_m + (ra % per) * istride_r];
+    const float2 B = 2 * q + 1 < cnt ? in[(rb / per) * istride_b + m * istride_m + (rb % per) * istride_r]
+                                     : make_float2(0.f, 0.f);
     if (m == 0) {
-      cb[r * n] = make_float2(X.x, 0.f);          // bitrev(0) = 0
+      cb[q * n] = make_float2(A.x, B.x);          // bitrev(0) = 0; DC imaginary parts dropped (irfft)
     } else {
-      cb[r * n + bitrev(m, log2n)] = X;
-      cb[r * n + bitrev(n - m, log2n)] = make_float2(X.x, -X.y);
+      cb[q * n + bitrev(m, log2n)] = make_float2(A.x - B.y, A.y + B.x);
+      cb[q * n + bitrev(n - m, log2n)] = make_float2(A.x + B.y, B.x - A.y);
     }
   }
   __syncthreads();
-  fft_dit_inverse_batch(cb, n, cnt, n, 1, tw, tw_n, threadIdx.x, NT);
-  for (int i = threadIdx.x; i < cnt * n; i += NT) Z[r0 * n + i] = cb[i].x * scale;
+  fft_dit_inverse_batch(cb, n, cntc, n, 1, tw, tw_n, threadIdx.x, NT);
+  for (int i = threadIdx.x; i < cntc * n; i += NT) {
+    const int q = i >> log2n, p = i & (n - 1);
+    float* za = Z + (r0 + 2 * q) * n + p;
+    za[0] = cb[i].x * scale;
+    if (2 * q + 1 < cnt) za[n] = cb[i].y * scale;
+  }
 }
 
 // 1D: Z1[b][o][p] = GELU(Z1[b][o][p] + B[o] + sum_{c,t} W[o][c][t] Z0[b][c][p + t - ks/2])
@@ -371,9 +396,9 @@ void fno_forward(const FnoArgs& a, cudaStream_t s) {
     const FnoLayer& ly = a.layer[l];
     if (a.dim == 1) {
       const int64_t rows = (int64_t)a.nrhs * c;
-      fno_rows_fwd_kernel<<<nblk(rows, R), NT, smr, s>>>(n, rows, k, Z0, a.Zh, c, (int64_t)k * c, c, 1, a.tw, a.tw_n);
+      fno_rows_fwd_kernel<<<nblk(rows, 2 * R), NT, smr, s>>>(n, rows, k, Z0, a.Zh, c, (int64_t)k * c, c, 1, a.tw, a.tw_n);
       fno_mix_kernel<<<dim3(modes, ceil_div(a.nrhs, 16)), NT, 0, s>>>(a.nrhs, modes, c, a.Zh, ly.R, a.Yh);
-      fno_rows_inv_kernel<<<nblk(rows, R), NT, smr, s>>>(n, rows, k, a.Yh, c, (int64_t)k * c, c, 1, 1.0f / (float)n,
+      fno_rows_inv_kernel<<<nblk(rows, 2 * R), NT, smr, s>>>(n, rows, k, a.Yh, c, (int64_t)k * c, c, 1, 1.0f / (float)n,
                                                          Z1, a.tw, a.tw_n);
       if (tc) {
         ca.bias = ly.B; ca.Z1 = Z1;
@@ -387,13 +412,13 @@ void fno_forward(const FnoArgs& a, cudaStream_t s) {
       const int64_t rows = (int64_t)a.nrhs * c * n;
       const int64_t per = (int64_t)c * n;
       // rows (b, c, i2) -> T[b][c][i2][m1]
-      fno_rows_fwd_kernel<<<nblk(rows, R), NT, smr, s>>>(n, rows, k, Z0, a.T, per, per * k, 1, k, a.tw, a.tw_n);
+      fno_rows_fwd_kernel<<<nblk(rows, 2 * R), NT, smr, s>>>(n, rows, k, Z0, a.T, per, per * k, 1, k, a.tw, a.tw_n);
       const int G = std::min(k, std::max(1, 4096 / n));
       const size_t smg = sizeof(float2) * (size_t)n * G;
       fno_cols_fwd_kernel<<<dim3(k / G, c, a.nrhs), NT, smg, s>>>(n, k, c, G, a.T, a.Zh, a.tw, a.tw_n);
       fno_mix_kernel<<<dim3(modes, ceil_div(a.nrhs, 16)), NT, 0, s>>>(a.nrhs, modes, c, a.Zh, ly.R, a.Yh);
       fno_cols_inv_kernel<<<dim3(k / G, c, a.nrhs), NT, smg, s>>>(n, k, c, G, a.Yh, a.T, a.tw, a.tw_n);
-      fno_rows_inv_kernel<<<nblk(rows, R), NT, smr, s>>>(n, rows, k, a.T, per, per * k, 1, k,
+      fno_rows_inv_kernel<<<nblk(rows, 2 * R), NT, smr, s>>>(n, rows, k, a.T, per, per * k, 1, k,
                                                          1.0f / ((float)n * (float)n), Z1, a.tw, a.tw_n);
       if (tc) {
         ca.bias = ly.B; ca.Z1 = Z1;
