@@ -222,7 +222,7 @@ def main():
                     help="auto: fp64 cycle for config 0 (BASELINE's fp64 system), mixed otherwise")
     ap.add_argument("--smoother", choices=["cnn", "fno"], default="cnn",
                     help="cnn: BASELINE's CNN smoothers (the headline); fno: the paper's FNO smoothers "
-                         "(Table 6 hyperparameters per level, W_seed; fp32 SIMT kernels, SURVEY NEXT-2)")
+                         "(Table 6 hyperparameters per level, W_seed; W-convolutions on tcgen05, SURVEY NEXT-2)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--slab", choices=["auto", "on", "off"], default="auto",
@@ -402,14 +402,18 @@ def main():
         pass
     f16x3_peak = bf16 / 3.0      # f16 dense = bf16 dense rate; 3 products per fp32-accurate MAC
     if fno and dom == "smooth":
-        # FNO smoother kernels are fp32 SIMT (fno.cu): reported against the FP32 FFMA rate
-        peak = 148 * 128 * 2 * 1.965e9 / 1e12
+        # FNO smoother: the W-convolution (the dense contraction, > 95 % of the FNO FLOPs) runs as a
+        # 3xTF32 implicit GEMM on tcgen05 (fno_tc.cu); the class also holds the mode FFTs, the mode
+        # mixing, lift and projection (fp32 SIMT), so the fraction is a whole-smoother figure
+        peak = bf16 * TF32_NOMINAL_RATIO / 3.0
         achieved = counts["smooth"] / (step_ms * 1e-3) / 1e12
-        roof = {"kernel": "fno_* (lift, row/column mode FFTs, mode mixing, W-conv + bias + GELU, projection; fp32 "
-                          "SIMT), all launches of a step",
-                "bound": "alu", "unit": "TFLOP/s",
-                "peak_note": "FP32 FFMA peak from unit counts and clock (DESIGN.md §6); FNO FLOPs = per layer "
-                             "2 c^2 ks^d per point (W-conv) + 8 c^2 per kept mode (mixing), lift and projection 2c"}
+        roof = {"kernel": "fno_conv_rows_kernel / fno_conv_tc_kernel (W-conv + bias + GELU, 3xTF32 tcgen05 implicit "
+                          "GEMM) + fno_* (lift, row/column mode FFTs, mode mixing, projection; fp32 SIMT), all "
+                          "launches of a step",
+                "bound": "tensor", "unit": "TFLOP/s",
+                "peak_note": "TF32 tensor (measured bf16 x 1.1/2.25) / 3 products per fp32-accurate MAC; FNO FLOPs "
+                             "= per layer 2 c^2 ks^d per point (W-conv) + 8 c^2 per kept mode (mixing), lift and "
+                             "projection 2c; FFTs not counted"}
     elif dom == "gemm64":
         peak = bf16 * FP64_NOMINAL_RATIO
         achieved = counts["gemm64"] / (step_ms * 1e-3) / 1e12
@@ -560,8 +564,8 @@ def main():
                 "value": value, "unit": "RHS*cycles/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "strong" if strong else "weak", "vs_baseline": None,
-                "dtype": ("f64 outer residual (Ozaki int8 tcgen05) + fp32 inner cycle (fp32 SIMT FNO smoothers, "
-                          "tcgen05 operator applies)" if fno else
+                "dtype": ("f64 outer residual (Ozaki int8 tcgen05) + fp32-accurate inner cycle (FNO smoothers: 3xTF32 "
+                          "tcgen05 W-convolutions, fp32 SIMT mode FFTs; tcgen05 operator applies)" if fno else
                           "f64 (NMG_PREC_FP64 fused cycle; the CNN's own arithmetic fp32)" if prec == nmg.PREC_FP64 else
                           "f64 outer residual (Ozaki int8 tcgen05) + fp32-accurate inner cycle (FP16x3 tcgen05 "
                           + ("CNN and operator applies)" if cfg.dim == 1 else "CNN, 3xTF32 tcgen05 Kronecker applies)")),

@@ -104,7 +104,8 @@ typedef struct {
                              whose activation bound lies > 2^4 below their layer's largest by a
                              power of two (an exactly equivalent network, see nmg_api.cu)    */
   int32_t simt_fno;       /* 1: FNO W-convolution on the fp32 SIMT kernels instead of the tcgen05
-                             3xTF32 implicit GEMM (fno_tc.cu)                                  */
+                             3xTF32 implicit GEMM (fno_tc.cu); 2: tcgen05, box variant only (no
+                             row-halo kernel for 2D n >= 128)                                  */
 } nmg_tuning;
 
 /* Problem descriptor (SPEC ProblemSpec analogue). */

@@ -383,6 +383,7 @@ void fno_forward(const FnoArgs& a, cudaStream_t s) {
     fno_tc_box(n, &bx, &by);
     ca.dim = a.dim; ca.n = n; ca.c = c; ca.ks = ks; ca.nrhs = a.nrhs;
     ca.lbx = 31 - __builtin_clz((unsigned)bx);
+    ca.rows = a.tc_rows;
   }
   const int R = std::max(1, 4096 / n);
   const size_t smr = sizeof(float2) * (size_t)R * n;

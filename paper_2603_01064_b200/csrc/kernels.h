@@ -294,11 +294,14 @@ struct FnoLayer {
 struct FnoConvArgs {
   int dim, n, c, ks, nrhs;
   int lbx;                    // 2D: log2 of the output box width bx (box bx x 128 / bx pixels)
+  bool rows;                  // 2D, n >= 128: row-halo variant (rank-5 no-swizzle input maps, x taps as
+                              // descriptor shifts)
   const float* bias;          // [c]
   float* Z1;                  // [nrhs][c][N]: the spectral branch on entry, the layer output on exit
   float* Xh_out; float* Xl_out;   // next layer's channels-last tf32 hi/lo input [nrhs][N][c] (null: last layer)
 };
 bool fno_tc_ok(int dim, int n, int c);
+bool fno_tc_rows(int dim, int n, int ks);
 void fno_tc_box(int n, int* bx, int* by);
 void fno_lift_cl(int nrhs, int c, int64_t N, const float* in, const double* norms, const float* lw, const float* lb,
                  float* Xh, float* Xl, cudaStream_t s);
@@ -327,6 +330,7 @@ struct FnoArgs {
   const CUtensorMap* tXl[2] = {nullptr, nullptr};
   float* Xh[2] = {nullptr, nullptr};
   float* Xl[2] = {nullptr, nullptr};
+  bool tc_rows = false;       // the X maps are the row-halo variant's rank-5 maps
 };
 void fno_forward(const FnoArgs& a, cudaStream_t s);
 int fno_launches(int dim, int L, bool tc);

@@ -352,10 +352,21 @@ nmg_status make_a2_map(CUtensorMap* m, const uint16_t* p, int n, int C, int64_t 
 // FNO layer input, channels-last fp32 (tf32 hi or lo plane): 1D [rhs][n][c] as {c, x, rhs} with box
 // {16, 128, 1}; 2D [rhs][n][n][c] as {c, x, y, rhs} with box {16, bx, by, 1}; SWIZZLE_64B.  Points
 // outside the image (tap shifts) are zero-filled: the convolution's "same" padding.
-nmg_status make_fno_x_map(CUtensorMap* m, const float* p, int dim, int n, int c, int64_t nrhs, int bx, int by) {
+nmg_status make_fno_x_map(CUtensorMap* m, const float* p, int dim, int n, int c, int64_t nrhs, int bx, int by,
+                          int halo_ks = 0) {
   NMG_TRY(get_encoder());
   CUresult r;
-  if (dim == 1) {
+  if (halo_ks > 0) {
+    // row-halo variant (fno_conv_rows_kernel): {4 ch, x, c/4 chunk, y, rhs}, box {4, 128 + ks - 1, 4, 1, 1}
+    // lands as the no-swizzle K-major tile [4 chunks][128 + ks - 1 pixels][4 tf32]
+    cuuint64_t dims[5] = {4u, (cuuint64_t)n, (cuuint64_t)(c / 4), (cuuint64_t)n, (cuuint64_t)nrhs};
+    cuuint64_t strides[4] = {(cuuint64_t)c * 4u, 16u, (cuuint64_t)n * c * 4u, (cuuint64_t)n * n * c * 4u};
+    cuuint32_t box[5] = {4u, (cuuint32_t)(128 + halo_ks - 1), 4u, 1u, 1u};
+    cuuint32_t es[5] = {1u, 1u, 1u, 1u, 1u};
+    r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, (void*)p, dims, strides, box, es,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else if (dim == 1) {
     cuuint64_t dims[3] = {(cuuint64_t)c, (cuuint64_t)n, (cuuint64_t)nrhs};
     cuuint64_t strides[2] = {(cuuint64_t)c * 4u, (cuuint64_t)n * c * 4u};
     cuuint32_t box[3] = {16u, 128u, 1u};
@@ -628,9 +639,11 @@ nmg_status run_fno(nmg_hierarchy* h, int l, int nrhs, const float* b, float* x, 
   if (F.tc) {
     int bx, by;
     fno_tc_box(n, &bx, &by);
+    a.tc_rows = h->tune.simt_fno != 2 && fno_tc_rows(dim, n, ks);
+    const int hks = a.tc_rows ? ks : 0;
     for (int q = 0; q < 2; ++q) {
-      NMG_TRY(make_fno_x_map(&mXh[q], h->fXh[q].p, dim, n, c, h->fno_chunk, bx, by));
-      NMG_TRY(make_fno_x_map(&mXl[q], h->fXl[q].p, dim, n, c, h->fno_chunk, bx, by));
+      NMG_TRY(make_fno_x_map(&mXh[q], h->fXh[q].p, dim, n, c, h->fno_chunk, bx, by, hks));
+      NMG_TRY(make_fno_x_map(&mXl[q], h->fXl[q].p, dim, n, c, h->fno_chunk, bx, by, hks));
       a.tXh[q] = &mXh[q]; a.tXl[q] = &mXl[q];
       a.Xh[q] = h->fXh[q].p; a.Xl[q] = h->fXl[q].p;
     }
@@ -2312,7 +2325,7 @@ nmg_status nmg_load_fno_weights(nmg_hierarchy* h, int32_t level, const nmg_fno_a
   F->arch = *arch;
   F->proj_b = params[n_params - 1];
   NMG_TRY(F->p.upload(params, n_params));
-  F->tc = !h->tune.simt_fno && fno_tc_ok(dim, n, c);
+  F->tc = h->tune.simt_fno != 1 && fno_tc_ok(dim, n, c);   // simt_fno 2: tcgen05 box variant only
   if (F->tc) {
     // W [o][c][tap] -> [layer][o][tap][c], tf32 hi/lo (K index of the implicit GEMM = tap * c + channel)
     const int taps = dim == 1 ? ks : ks * ks;
