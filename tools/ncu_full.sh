@@ -1,7 +1,7 @@
 #!/bin/bash
 # One ncu --set full capture per hot kernel (run under gpurun, one GPU), after the same
 # command has exited 0 without ncu.  Reports land in gpurun_out/ncu_<tag>.ncu-rep.
-#   bash tools/ncu_full.sh [tags...]     (tags: s1d ozaki1d cfg3 cfg2)
+#   bash tools/ncu_full.sh [tags...]     (tags: s1d ozaki1d cfg3 cfg2 ... fno1 fno2)
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 B="python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e --no-solve"
@@ -23,5 +23,7 @@ for t in ${@:-cfg3}; do
     kron3) run kron3 3 "kron_tc" 4 ;;
     cols3) run cols3 3 "fft_cols|fft_rows" 2 "--lanes 1" ;;
     comb3) run comb3 3 "combine_rows" 1 "--lanes 1" ;;
+    fno2) run fno2 2 "fno_conv_rows|fno_conv_tc|fno_rows_fwd|fno_rows_inv" 4 "--smoother fno --nrhs 64" ;;
+    fno1) run fno1 1 "fno_conv_tc|fno_rows_fwd|fno_rows_inv" 3 "--smoother fno --nrhs 256 --lanes 1" ;;
   esac
 done

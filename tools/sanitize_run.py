@@ -25,7 +25,26 @@ def run(cfg, nrhs):
     torch.cuda.synchronize()
     print(cfg.name, "history", rep["history"][:, -1])
 
+def run_fno(cfg, nrhs):
+    """FNO smoothers (tcgen05 W-convolution: box kernel, and the row-halo kernel at 2D n >= 128)."""
+    import torch
+    import paper_2603_01064_b200 as nmg
+    f = ni.operator_factors(cfg)
+    h = nmg.Hierarchy(cfg.dim, cfg.n, cfg.levels, cfg.alpha, f, nu1=cfg.nu1, nu2=cfg.nu2, max_rhs=nrhs)
+    for l, w in enumerate(ni.fno_weights_seed(cfg, seed=3)):
+        h.load_fno_weights(l + 1, ni.fno_arch(cfg.dim, cfg.n >> l), w)
+    y, _ = ni.make_rhs(cfg, f, cfg.alpha, nrhs=nrhs)
+    yd = torch.tensor(y, dtype=torch.float64, device="cuda")
+    rep = h.solve(yd, torch.zeros_like(yd), tol=1e-300, max_cycles=1)
+    torch.cuda.synchronize()
+    print(cfg.name, "fno history", rep["history"][:, -1])
+
+
 if __name__ == "__main__":
+    if "fno" in sys.argv[1:]:
+        run_fno(ni.CONFIGS[0].replace(nrhs=2), 2)
+        run_fno(ni.CONFIGS[2].replace(n=128, levels=4, nrhs=1), 1)
+        sys.exit(0)
     run(ni.CONFIGS[0], 8)
     run(ni.CONFIGS[2].replace(n=64, levels=3), 3)
     print("sanitize run done")
