@@ -1,6 +1,5 @@
 #!/bin/bash
 # Round-end GPU pass: gpu_round.sh (tests, smoke, CNN bench lines, shard timings, ncu launch lists)
-# plus the FNO-smoother bench lines / launch lists and a compute-sanitizer memcheck of small runs.
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 SHARDS=1 NCU="3 1" bash tools/gpu_round.sh 3 1 0 2 4
@@ -15,5 +14,3 @@ for spec in 1:256 2:64; do
   timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
       --csv --log-file gpurun_out/launches_fno_cfg$c.csv $CMD > gpurun_out/ncu_fno_cfg$c.log 2>&1; echo "NCU fno $c $?"
 done
-timeout 900 compute-sanitizer --tool memcheck python tools/sanitize_run.py > gpurun_out/sanitizer_memcheck.log 2>&1; echo "MEMCHECK $?"; tail -3 gpurun_out/sanitizer_memcheck.log
-timeout 900 compute-sanitizer --tool memcheck python tools/sanitize_run.py fno > gpurun_out/sanitizer_memcheck_fno.log 2>&1; echo "MEMCHECK fno $?"; tail -3 gpurun_out/sanitizer_memcheck_fno.log
