@@ -19,6 +19,11 @@ convergence test, one NMGF V-cycle (all levels), fp64 update.
           stand-in weights (1D configs only).
 Inputs are larger than L2 (cfg 3: 4 GiB fp64 y and x), so no explicit L2 flush is needed.
 
+--smoother fno runs the same cycle with the paper's FNO smoothers (Table-6 architecture per level,
+W_seed weights; W-convolutions as 3xTF32 implicit GEMMs on tcgen05) instead of BASELINE's CNNs;
+its line reports the FNO smoother class against the 3xTF32 tensor peak and has no solve figure
+(no trained FNO weights exist here).
+
 --impl reference times the fp64 CPU oracle (oracle/) on a bounded sample of the same
 workload on this host's cores (the reference arm: /root/reference holds only the paper).
 """

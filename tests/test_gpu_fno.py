@@ -100,18 +100,21 @@ def test_fno_cycle_history(setup):
     assert ok, err
 
 
-@pytest.mark.parametrize("dim,n,nrhs", [(1, 4096, 3), (1, 512, 5), (2, 256, 2), (2, 128, 3), (2, 16, 5)])
-def test_fno_forward_table6_sizes(dim, n, nrhs):
+@pytest.mark.parametrize("dim,n,nrhs,knob", [(1, 4096, 3, 0), (1, 512, 5, 0), (2, 256, 2, 0), (2, 128, 3, 0),
+                                             (2, 16, 5, 0), (2, 128, 2, 2), (2, 128, 2, 1)])
+def test_fno_forward_table6_sizes(dim, n, nrhs, knob):
     """Raw FNO output at the BASELINE level sizes (Table 6 rows: ks = 7 / 5 / 3, k up to 128; the
-    tensor-core convolution's 1D tiles and 2D boxes 128 x 1, 128 x 1, 16 x 8 with several tiles per
-    image and tap shifts crossing the image border), per RHS against the oracle."""
+    tensor-core convolution's 1D tiles, the 2D row-halo kernel at n >= 128 and the 16 x 8 pixel boxes
+    at n = 16, several tiles per image and tap shifts crossing the image border), per RHS against the
+    oracle.  knob = nmg_tuning.simt_fno: 2 = the box kernel where the row-halo kernel would run,
+    1 = the fp32 SIMT convolution."""
     base = ni.CONFIGS[1] if dim == 1 else ni.CONFIGS[2]
     levels = max(2, int(np.log2(n // (256 if dim == 1 else 16))) + 1)   # coarsest system <= 256 unknowns
     cfg = base.replace(n=n, levels=levels, nrhs=nrhs)
     f = ni.operator_factors(cfg)
     arch = ni.fno_arch(dim, n)
     w = ni.fno_weights_seed(cfg, seed=5)[0]
-    h = nmg.Hierarchy(dim, n, levels, cfg.alpha, f, max_rhs=nrhs)
+    h = nmg.Hierarchy(dim, n, levels, cfg.alpha, f, max_rhs=nrhs, tuning={"simt_fno": knob} if knob else None)
     h.load_fno_weights(1, arch, w)
     rng = np.random.default_rng(11)
     shape = (nrhs,) + (n,) * dim
