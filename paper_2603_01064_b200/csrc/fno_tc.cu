@@ -28,11 +28,23 @@
 namespace nmg {
 namespace {
 
-constexpr int FM = 128, FN = 64, FK = 16, FT = 128, FST = 4;
+#ifndef NMG_FNO_ST1D
+#define NMG_FNO_ST1D 2   // 50 KB: four CTAs per SM (the short 1D K loop is epilogue-latency-bound: 157.6 -> 144.5 ms
+                         // per cfg 1 FNO step against 4 stages / two CTAs; 3 stages 147.5)
+#endif
+#ifndef NMG_FNO_RA
+#define NMG_FNO_RA 2     // row-halo kernel rings: 2 input-row stages + 4 W stages = 70 KB, three CTAs per SM
+#endif                   // (cfg 2 FNO step 439.8 -> 427.7 ms against 3 + 6 stages / two CTAs)
+#ifndef NMG_FNO_RW
+#define NMG_FNO_RW 4
+#endif
+constexpr int FM = 128, FN = 64, FK = 16, FT = 128;
+// TMA ring depth of the box kernel (24 KB stages): 1D / 2D
+template <int DIM> struct FnoRing { static constexpr int ST = DIM == 1 ? NMG_FNO_ST1D : 4; };
 constexpr int FA_BYTES = FM * FK * 4;                         // 8 KB
 constexpr int FB_BYTES = FN * FK * 4;                         // 4 KB
 constexpr int FSTAGE = 2 * FA_BYTES + 2 * FB_BYTES;           // 24 KB
-constexpr int FSMEM = FST * FSTAGE + 1024 /*barriers*/ + 1024 /*align slack*/;
+template <int DIM> constexpr int fno_box_smem() { return FnoRing<DIM>::ST * FSTAGE + 1024 /*barriers*/ + 1024 /*align slack*/; }
 // D f32, A/B tf32 K-major, M = 128, N = 64
 constexpr uint32_t FIDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(FN >> 3) << 17) |
                             ((uint32_t)(FM >> 4) << 24);
@@ -110,6 +122,7 @@ __global__ void __launch_bounds__(FT)
     fno_conv_tc_kernel(const __grid_constant__ CUtensorMap tXh, const __grid_constant__ CUtensorMap tXl,
                        const __grid_constant__ CUtensorMap tWh, const __grid_constant__ CUtensorMap tWl,
                        FnoConvArgs a) {
+  constexpr int FST = FnoRing<DIM>::ST;
   extern __shared__ uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + FST * FSTAGE);
@@ -220,7 +233,7 @@ __global__ void __launch_bounds__(FT)
 // chunks LBO = 16 (128 + ks - 1) bytes apart); the x tap t1 is a 16 t1-byte shift of the A
 // descriptor's start address.  The layer input is read from L2 ks times instead of ks^2 times
 // (the box variant above is L2 -> SM bound at ~195 TFLOP/s); W streams through its own ring.
-constexpr int RA_ST = 3, RW_ST = 6;
+constexpr int RA_ST = NMG_FNO_RA, RW_ST = NMG_FNO_RW;
 constexpr int RA_MAX = 2 * 64 * (FM + 6);                      // hi + lo, ks <= 7: 17,152 B
 constexpr int RA_STAGE = (RA_MAX + 1023) / 1024 * 1024;           // the W ring behind it stays 1 KB-aligned (SWIZZLE_64B)
 constexpr int RW_STAGE = 2 * FB_BYTES;                          // 8 KB
@@ -378,18 +391,18 @@ void fno_lift_cl(int nrhs, int c, int64_t N, const float* in, const double* norm
 void fno_conv_tc(const CUtensorMap* xh, const CUtensorMap* xl, const CUtensorMap* wh, const CUtensorMap* wl,
                  const FnoConvArgs& a, cudaStream_t s) {
   if (a.dim == 1) {
-    NMG_SMEM_OPTIN(fno_conv_tc_kernel<1>, FSMEM);
+    NMG_SMEM_OPTIN(fno_conv_tc_kernel<1>, fno_box_smem<1>());
     const int64_t tiles = (int64_t)a.nrhs * (a.n / FM);
-    fno_conv_tc_kernel<1><<<(unsigned)tiles, FT, FSMEM, s>>>(*xh, *xl, *wh, *wl, a);
+    fno_conv_tc_kernel<1><<<(unsigned)tiles, FT, fno_box_smem<1>(), s>>>(*xh, *xl, *wh, *wl, a);
   } else if (a.rows) {
     NMG_SMEM_OPTIN(fno_conv_rows_kernel, RSMEM);
     const int64_t tiles = (int64_t)a.nrhs * a.n * (a.n / FM);
     fno_conv_rows_kernel<<<(unsigned)tiles, FT, RSMEM, s>>>(*xh, *xl, *wh, *wl, a);
   } else {
-    NMG_SMEM_OPTIN(fno_conv_tc_kernel<2>, FSMEM);
+    NMG_SMEM_OPTIN(fno_conv_tc_kernel<2>, fno_box_smem<2>());
     const int bx = 1 << a.lbx, by = FM / bx;
     const int64_t tiles = (int64_t)a.nrhs * (a.n / bx) * (a.n / by);
-    fno_conv_tc_kernel<2><<<(unsigned)tiles, FT, FSMEM, s>>>(*xh, *xl, *wh, *wl, a);
+    fno_conv_tc_kernel<2><<<(unsigned)tiles, FT, fno_box_smem<2>(), s>>>(*xh, *xl, *wh, *wl, a);
   }
 }
 
