@@ -183,3 +183,53 @@ def test_level_truncation_Lprime(Lp):
     ok, err = history_close(rep["history"], orc.history)
     assert ok, err
     assert np.abs(rep["cycles"] - orc.cycles).max() <= 1
+
+
+@pytest.mark.parametrize("dim", [1, 2])
+def test_weight_reload_matches_fresh_handle(dim):
+    """Reloading a level's smoother weights replaces them: the captured cycle graphs (which bake in
+    weight pointers, tensor maps and by-value weights) are dropped, so cycles after the reload are
+    bitwise those of a fresh handle created with the new weights (include/nmg.h,
+    nmg_load_smoother_weights: "loading a level twice replaces it")."""
+    cfg = ni.CONFIGS[0] if dim == 1 else ni.CONFIGS[2].replace(n=64, levels=3, nrhs=3)
+    f = ni.operator_factors(cfg)
+    W1, W2 = ni.weights_seed(cfg, seed=0), ni.weights_seed(cfg, seed=7)
+    y, _ = ni.make_rhs(cfg, f, cfg.alpha)
+    yd = torch.tensor(y, dtype=torch.float64, device=DEV)
+    h = gpu_hierarchy(cfg, f, W1, max_rhs=cfg.nrhs)
+    x1 = torch.zeros_like(yd)
+    for _ in range(3):                         # eager run, graph capture, replay
+        h.vcycle(yd, x1)
+    for l, w in enumerate(W2):
+        h.load_weights(l + 1, ni.cnn_arch(cfg), w)
+    x2 = torch.zeros_like(yd)
+    for _ in range(3):
+        h.vcycle(yd, x2)
+    hf = gpu_hierarchy(cfg, f, W2, max_rhs=cfg.nrhs)
+    x3 = torch.zeros_like(yd)
+    for _ in range(3):
+        hf.vcycle(yd, x3)
+    torch.cuda.synchronize()
+    assert torch.equal(x2, x3)
+    assert not torch.equal(x1, x2)
+
+
+def test_divergence_check_is_opt_in():
+    """SPEC.md:545 rule behind desc.divergence_check: a smoother that overshoots (W_seed scaled by 10:
+    the 3-layer ReLU network's output grows 1000x) drives relres above 10x its initial value for 5
+    consecutive cycles -> nmg_solve returns NMG_ERR_DIVERGED; without the flag the same solve runs
+    its max_cycles and reports the growing history."""
+    import paper_2603_01064_b200 as nmg
+    cfg = ni.CONFIGS[0]
+    f = ni.operator_factors(cfg)
+    W = [10.0 * w for w in ni.weights_seed(cfg)]
+    y, _ = ni.make_rhs(cfg, f, cfg.alpha)
+    yd = torch.tensor(y, dtype=torch.float64, device=DEV)
+    h = gpu_hierarchy(cfg, f, W, max_rhs=cfg.nrhs)
+    rep = h.solve(yd, torch.zeros_like(yd), tol=1e-6, max_cycles=6)
+    hist = np.asarray(rep["history"])
+    assert np.all(hist[:, -1] > 10.0 * hist[:, 0])
+    hd = gpu_hierarchy(cfg, f, W, max_rhs=cfg.nrhs, divergence_check=True)
+    with pytest.raises(nmg.NmgError) as e:
+        hd.solve(yd, torch.zeros_like(yd), tol=1e-6, max_cycles=20)
+    assert e.value.status == 9          # NMG_ERR_DIVERGED
